@@ -1,0 +1,643 @@
+// coarsen.cu — candidate scoring/selection, matching and contraction.
+//
+// Scoring never materialises the neighbour sets or the histogram in HBM:
+// a node's neighbours are exactly the pins of its incident h-edges minus
+// itself (coarsen.py:78-85; the carried sets equal the rematerialised ones,
+// test_coarsen.py:183-192), so each warp accumulates hist(n, .) for one node
+// in a shared-memory hash table keyed by neighbour id, then scans it in
+// (hist desc, id desc) order with the deferred size/inbound checks.
+#include "coarsen.cuh"
+#include "prims.cuh"
+
+namespace dhgp {
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// flattened iteration over the pins of a node's incident h-edges: the warp
+// takes 32 incident h-edges at a time and spreads their pins evenly over the
+// lanes (segmented prefix sum + per-slot owner search by shuffles).
+// ---------------------------------------------------------------------------
+template <class F>
+__device__ __forceinline__ void warp_for_pins(const int32_t *inc_dat, int64_t ilo, int64_t ihi, int64_t first,
+                                              int64_t stride, const int64_t *pin_off, const int32_t *pin_dat,
+                                              F &&f) {
+    const int lane = lane_id();
+    for (int64_t base = ilo + first; base < ihi; base += stride) {
+        const int64_t ii = base + lane;
+        int32_t e = -1;
+        int64_t plo = 0;
+        int len = 0;
+        if (ii < ihi) {
+            e = inc_dat[ii];
+            plo = pin_off[e];
+            len = (int)(pin_off[e + 1] - plo);
+        }
+        const int incl = warp_incl_scan(len);
+        const int total = __shfl_sync(FULL_MASK, incl, 31);
+        const int excl = incl - len;
+        for (int s0 = 0; s0 < total; s0 += 32) {
+            const int s = s0 + lane;
+            int owner = 0;
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+                int ex = __shfl_sync(FULL_MASK, excl, owner + step);
+                if (ex <= s) owner += step;
+            }
+            const int32_t oe = __shfl_sync(FULL_MASK, e, owner);
+            const int64_t oplo = __shfl_sync(FULL_MASK, plo, owner);
+            const int oex = __shfl_sync(FULL_MASK, excl, owner);
+            if (s < total) f(oe, pin_dat[oplo + (s - oex)]);
+        }
+    }
+}
+
+struct ScoreArgs {
+    int32_t N;
+    const int64_t *inc_off;
+    const int32_t *inc_dat;
+    const int64_t *pin_off;
+    const int32_t *pin_dat;
+    const int64_t *wi;
+    const int32_t *size;
+    const int64_t *in_off;
+    const int32_t *in_dat;
+    int64_t omega, delta;
+    int32_t *pair;
+    double *score;
+    int32_t *next;       // work counter
+    int32_t *big_list;   // nodes escalated to the block tier
+    int32_t *big_count;
+};
+
+constexpr int SS_WARPS = 8;
+constexpr int SS_CAP = 1024;   // hash slots per warp (power of two)
+constexpr int SS_LIMIT = 720;  // distinct neighbours before escalation
+constexpr int SS_SMEM = SS_WARPS * SS_CAP * (4 + 8);
+
+__device__ __forceinline__ uint32_t hslot(int32_t m) { return ((uint32_t)m * 2654435761u) >> (32 - 10); }
+
+// |in(n) ∪ in(m)| <= delta, warp-cooperative (_kernels.pyx:94-98)
+__device__ __forceinline__ bool warp_union_ok(const ScoreArgs &a, int32_t n, int32_t m) {
+    const int64_t nlo = a.in_off[n], nn = a.in_off[n + 1] - nlo;
+    const int64_t mlo = a.in_off[m], nm = a.in_off[m + 1] - mlo;
+    if (nn + nm <= a.delta) return true;
+    const bool ns = nn <= nm;
+    const int32_t *sp = a.in_dat + (ns ? nlo : mlo);
+    const int32_t *lp = a.in_dat + (ns ? mlo : nlo);
+    const int64_t cs = ns ? nn : nm, cl = ns ? nm : nn;
+    int64_t common = 0;
+    for (int64_t i = lane_id(); i < cs; i += 32) common += bsearch_dev(lp, 0, cl, sp[i]) >= 0;
+    common = warp_sum(common);
+    return nn + nm - common <= a.delta;
+}
+
+__global__ void __launch_bounds__(SS_WARPS * 32) k_score_warp(ScoreArgs a) {
+    extern __shared__ unsigned char smem[];
+    unsigned long long *svals = (unsigned long long *)smem;
+    int32_t *skeys = (int32_t *)(svals + SS_WARPS * SS_CAP);
+    __shared__ int32_t snk[SS_WARPS];
+    __shared__ volatile int32_t sover[SS_WARPS];
+    const int w = warp_id(), lane = lane_id();
+    int32_t *keys = skeys + w * SS_CAP;
+    unsigned long long *vals = svals + w * SS_CAP;
+    while (true) {
+        int node = 0;
+        if (lane == 0) node = atomicAdd(a.next, 1);
+        node = __shfl_sync(FULL_MASK, node, 0);
+        if (node >= a.N) break;
+        for (int s = lane; s < SS_CAP; s += 32) {
+            keys[s] = -1;
+            vals[s] = 0ull;
+        }
+        if (lane == 0) {
+            snk[w] = 0;
+            sover[w] = 0;
+        }
+        __syncwarp();
+        const int64_t ilo = a.inc_off[node], ihi = a.inc_off[node + 1];
+        warp_for_pins(a.inc_dat, ilo, ihi, 0, 32, a.pin_off, a.pin_dat, [&](int32_t e, int32_t m) {
+            if (m == node || sover[w]) return;
+            const unsigned long long we = (unsigned long long)a.wi[e];
+            uint32_t h = hslot(m);
+            for (int probe = 0; probe < SS_CAP; probe++) {
+                const int slot = (h + probe) & (SS_CAP - 1);
+                int k = keys[slot];
+                if (k == -1) {
+                    int prev = atomicCAS(&keys[slot], -1, m);
+                    if (prev == -1) {
+                        if (atomicAdd(&snk[w], 1) >= SS_LIMIT) sover[w] = 1;
+                        k = m;
+                    } else {
+                        k = prev;
+                    }
+                }
+                if (k == m) {
+                    atomicAdd(&vals[slot], we);
+                    return;
+                }
+            }
+            sover[w] = 1;
+        });
+        __syncwarp();
+        if (sover[w]) {
+            if (lane == 0) a.big_list[atomicAdd(a.big_count, 1)] = node;
+            __syncwarp();
+            continue;
+        }
+        // size check once per candidate (_kernels.pyx:92)
+        const int64_t szn = a.size[node];
+        for (int s = lane; s < SS_CAP; s += 32) {
+            int k = keys[s];
+            if (k >= 0 && szn + a.size[k] > a.omega) keys[s] = -2;
+        }
+        __syncwarp();
+        int32_t best_m = -1;
+        int64_t best_v = 0;
+        while (true) {
+            int64_t bv = -1;
+            int32_t bk = -1;
+            int bs = -1;
+            for (int s = lane; s < SS_CAP; s += 32) {
+                int k = keys[s];
+                if (k >= 0) {
+                    int64_t v = (int64_t)vals[s];
+                    if (v > bv || (v == bv && k > bk)) {
+                        bv = v;
+                        bk = k;
+                        bs = s;
+                    }
+                }
+            }
+#pragma unroll
+            for (int d = 16; d > 0; d >>= 1) {
+                int64_t ov = __shfl_xor_sync(FULL_MASK, bv, d);
+                int32_t ok = __shfl_xor_sync(FULL_MASK, bk, d);
+                int os = __shfl_xor_sync(FULL_MASK, bs, d);
+                if (ov > bv || (ov == bv && ok > bk)) {
+                    bv = ov;
+                    bk = ok;
+                    bs = os;
+                }
+            }
+            if (bk < 0) break;
+            if (warp_union_ok(a, node, bk)) {
+                best_m = bk;
+                best_v = bv;
+                break;
+            }
+            if (lane == 0) keys[bs] = -2;
+            __syncwarp();
+        }
+        if (lane == 0) {
+            a.pair[node] = best_m;
+            a.score[node] = best_m >= 0 ? (double)best_v : 0.0;
+        }
+        __syncwarp();
+    }
+}
+
+// Block tier for nodes with many distinct neighbours: a dense per-block
+// histogram over all node ids in global memory (L2-resident), restored to
+// "untouched" (-1) after each node.
+constexpr int SB_THREADS = 512;
+__global__ void __launch_bounds__(SB_THREADS) k_score_block(ScoreArgs a, long long *dense_all, int32_t *touched_all,
+                                                             long long *cval_all) {
+    __shared__ int32_t s_nt;
+    __shared__ long long s_bv[SB_THREADS / 32];
+    __shared__ int32_t s_bk[SB_THREADS / 32];
+    __shared__ int32_t s_bi[SB_THREADS / 32];
+    __shared__ long long s_common[SB_THREADS / 32];
+    long long *dense = dense_all + (int64_t)blockIdx.x * a.N;
+    int32_t *touched = touched_all + (int64_t)blockIdx.x * a.N;
+    long long *cval = cval_all + (int64_t)blockIdx.x * a.N;
+    const int w = warp_id(), lane = lane_id(), nw = SB_THREADS / 32;
+    const int nbig = *a.big_count;
+    for (int t = blockIdx.x; t < nbig; t += gridDim.x) {
+        const int32_t node = a.big_list[t];
+        if (threadIdx.x == 0) s_nt = 0;
+        __syncthreads();
+        const int64_t ilo = a.inc_off[node], ihi = a.inc_off[node + 1];
+        warp_for_pins(a.inc_dat, ilo, ihi, (int64_t)w * 32, (int64_t)nw * 32, a.pin_off, a.pin_dat,
+                      [&](int32_t e, int32_t m) {
+                          if (m == node) return;
+                          long long old = atomicCAS((unsigned long long *)&dense[m], ~0ull, 0ull);
+                          if (old == -1ll) touched[atomicAdd(&s_nt, 1)] = m;
+                          atomicAdd((unsigned long long *)&dense[m], (unsigned long long)a.wi[e]);
+                      });
+        __syncthreads();
+        const int nt = s_nt;
+        const int64_t szn = a.size[node];
+        for (int i = threadIdx.x; i < nt; i += SB_THREADS) {
+            int32_t m = touched[i];
+            cval[i] = dense[m];
+            dense[m] = -1ll;
+            if (szn + a.size[m] > a.omega) touched[i] = -2;
+        }
+        __syncthreads();
+        int32_t best_m = -1;
+        long long best_v = 0;
+        while (true) {
+            long long bv = -1;
+            int32_t bk = -1, bi = -1;
+            for (int i = threadIdx.x; i < nt; i += SB_THREADS) {
+                int32_t k = touched[i];
+                if (k >= 0) {
+                    long long v = cval[i];
+                    if (v > bv || (v == bv && k > bk)) {
+                        bv = v;
+                        bk = k;
+                        bi = i;
+                    }
+                }
+            }
+#pragma unroll
+            for (int d = 16; d > 0; d >>= 1) {
+                long long ov = __shfl_xor_sync(FULL_MASK, bv, d);
+                int32_t ok = __shfl_xor_sync(FULL_MASK, bk, d);
+                int32_t oi = __shfl_xor_sync(FULL_MASK, bi, d);
+                if (ov > bv || (ov == bv && ok > bk)) {
+                    bv = ov;
+                    bk = ok;
+                    bi = oi;
+                }
+            }
+            if (lane == 0) {
+                s_bv[w] = bv;
+                s_bk[w] = bk;
+                s_bi[w] = bi;
+            }
+            __syncthreads();
+            bv = s_bv[0];
+            bk = s_bk[0];
+            bi = s_bi[0];
+            for (int j = 1; j < nw; j++) {
+                if (s_bv[j] > bv || (s_bv[j] == bv && s_bk[j] > bk)) {
+                    bv = s_bv[j];
+                    bk = s_bk[j];
+                    bi = s_bi[j];
+                }
+            }
+            __syncthreads();
+            if (bk < 0) break;
+            // union check by the whole block
+            const int64_t nlo = a.in_off[node], nn = a.in_off[node + 1] - nlo;
+            const int64_t mlo = a.in_off[bk], nm = a.in_off[bk + 1] - mlo;
+            bool ok;
+            if (nn + nm <= a.delta) {
+                ok = true;
+            } else {
+                const bool ns = nn <= nm;
+                const int32_t *sp = a.in_dat + (ns ? nlo : mlo);
+                const int32_t *lp = a.in_dat + (ns ? mlo : nlo);
+                const int64_t cs = ns ? nn : nm, cl = ns ? nm : nn;
+                long long common = 0;
+                for (int64_t i = threadIdx.x; i < cs; i += SB_THREADS) common += bsearch_dev(lp, 0, cl, sp[i]) >= 0;
+                common = warp_sum(common);
+                if (lane == 0) s_common[w] = common;
+                __syncthreads();
+                long long tot = 0;
+                for (int j = 0; j < nw; j++) tot += s_common[j];
+                __syncthreads();
+                ok = nn + nm - tot <= a.delta;
+            }
+            if (ok) {
+                best_m = bk;
+                best_v = bv;
+                break;
+            }
+            if (threadIdx.x == 0) touched[bi] = -2;
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            a.pair[node] = best_m;
+            a.score[node] = best_m >= 0 ? (double)best_v : 0.0;
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void k_fill_ll(long long *p, long long v, int64_t n) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+
+}  // namespace
+
+void score_select(Ctx &c, const DLevel &L, const DWeights &W, int64_t omega, int64_t delta, int32_t *pair,
+                  double *score) {
+    if (L.N == 0) return;
+    KScope ks(c, "score_select", (double)(16.0 * L.U + 24.0 * L.N));
+    static bool attr = false;
+    if (!attr) {
+        DHGP_CUDA(cudaFuncSetAttribute(k_score_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, SS_SMEM));
+        attr = true;
+    }
+    int32_t *ctr = c.alloc<int32_t>(2);
+    int32_t *big = c.alloc<int32_t>(L.N);
+    c.zero(ctr, 2);
+    ScoreArgs a{L.N, L.inc_off, L.inc_dat, L.pin_off, L.pin_dat, W.wi, L.size, L.in_off, L.in_dat, omega, delta,
+                pair, score, ctr, big, ctr + 1};
+    int blocks = (int)std::min<int64_t>(cdiv(L.N, SS_WARPS), (int64_t)c.num_sms * 2);
+    k_score_warp<<<blocks, SS_WARPS * 32, SS_SMEM, c.stream>>>(a);
+    DHGP_LAUNCHED(c);
+    int32_t nbig = 0;
+    c.d2h(&nbig, ctr + 1, 1);
+    c.sync();
+    if (nbig > 0) {
+        int g = (int)std::min<int64_t>(nbig, 64);
+        // keep the dense scratch within ~2 GB
+        while (g > 1 && (int64_t)g * L.N * 20 > (2ll << 30)) g >>= 1;
+        long long *dense = c.alloc<long long>((int64_t)g * L.N);
+        long long *cval = c.alloc<long long>((int64_t)g * L.N);
+        int32_t *touched = c.alloc<int32_t>((int64_t)g * L.N);
+        k_fill_ll<<<(unsigned)cdiv((int64_t)g * L.N, 256), 256, 0, c.stream>>>(dense, -1ll, (int64_t)g * L.N);
+        DHGP_LAUNCHED(c);
+        k_score_block<<<g, SB_THREADS, 0, c.stream>>>(a, dense, touched, cval);
+        DHGP_LAUNCHED(c);
+        c.free(dense);
+        c.free(cval);
+        c.free(touched);
+    }
+    c.free(ctr);
+    c.free(big);
+}
+
+// ===========================================================================
+// A7 matching: claims by packed atomics, locks by odd run length of won
+// claims toward the root (pointer jumping when a run is long).
+// ===========================================================================
+namespace {
+__device__ __forceinline__ unsigned long long score_bits(double s) {
+    return (unsigned long long)__double_as_longlong(s + 0.0);
+}
+__device__ __forceinline__ bool is_cyc(const int32_t *pair, int32_t v) {
+    int32_t p = pair[v];
+    return p >= 0 && pair[p] == v;
+}
+__device__ __forceinline__ bool claimant(const int32_t *pair, int32_t v) {
+    int32_t p = pair[v];
+    return p >= 0 && !is_cyc(pair, v) && !is_cyc(pair, p);
+}
+
+__global__ void k_match_claim1(int32_t N, const int32_t *pair, const double *score, unsigned long long *best,
+                               int32_t *flags) {
+    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= N) return;
+    int32_t p = pair[v];
+    if (p < 0 || is_cyc(pair, (int32_t)v)) return;
+    int32_t q = pair[p];
+    // Certificate that no cycle of length != 2 exists: along v -> p -> q the
+    // (score, id) order must strictly improve (hist symmetry + first-valid
+    // selection); a violation triggers the exact sequential check.
+    if (q >= 0 && !is_cyc(pair, p) && !(score[p] > score[v] || (score[p] == score[v] && q > (int32_t)v)))
+        flags[0] = 1;
+    if (!is_cyc(pair, p)) atomicMax(&best[p], score_bits(score[v]));
+}
+
+__global__ void k_match_claim2(int32_t N, const int32_t *pair, const double *score, const unsigned long long *best,
+                               int32_t *claim) {
+    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= N) return;
+    if (!claimant(pair, (int32_t)v)) return;
+    int32_t p = pair[v];
+    if (score_bits(score[v]) == best[p]) atomicMax(&claim[p], (int32_t)v);
+}
+
+__device__ __forceinline__ bool won(const int32_t *pair, const int32_t *claim, int32_t v) {
+    return claimant(pair, v) && claim[pair[v]] == v;
+}
+
+constexpr int kWalkLimit = 64;
+
+__global__ void k_match_final(int32_t N, const int32_t *pair, const int32_t *claim, const int32_t *runlen,
+                              int32_t *match, uint8_t *isrep, unsigned long long *npairs, int32_t *flags) {
+    __shared__ int64_t sh[33];
+    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int64_t moved = 0;
+    if (v < N) {
+        int32_t r;
+        if (runlen) {
+            r = runlen[v];
+        } else {
+            r = 0;
+            int32_t u = (int32_t)v;
+            while (won(pair, claim, u)) {
+                r++;
+                u = pair[u];
+                if (r > kWalkLimit) {
+                    flags[1] = 1;
+                    break;
+                }
+            }
+        }
+        const bool lock = (r & 1) != 0;
+        int32_t m;
+        if (is_cyc(pair, (int32_t)v) || lock)
+            m = pair[v];
+        else
+            m = claim[v] >= 0 ? claim[v] : (int32_t)v;
+        match[v] = m;
+        isrep[v] = m >= (int32_t)v;
+        moved = m != (int32_t)v;
+    }
+    int64_t t = block_sum<int64_t>(moved, sh);
+    if (threadIdx.x == 0 && t) atomicAdd(npairs, (unsigned long long)t);
+}
+
+__global__ void k_pj_init(int32_t N, const int32_t *pair, const int32_t *claim, int32_t *r, int32_t *nxt) {
+    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= N) return;
+    bool wv = won(pair, claim, (int32_t)v);
+    r[v] = wv ? 1 : 0;
+    nxt[v] = wv ? pair[v] : -1;
+}
+__global__ void k_pj_step(int32_t N, const int32_t *r0, const int32_t *n0, int32_t *r1, int32_t *n1) {
+    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= N) return;
+    int32_t nx = n0[v];
+    r1[v] = r0[v] + (nx >= 0 ? r0[nx] : 0);
+    n1[v] = nx >= 0 ? n0[nx] : -1;
+}
+
+// exact sequential cycle check, the reference's DFS (_kernels.pyx:124-155)
+__global__ void k_cycle_check(int32_t N, const int32_t *pair, int8_t *state, int32_t *path, int32_t *out_len) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    *out_len = 0;
+    for (int32_t s = 0; s < N; s++) {
+        if (state[s]) continue;
+        int32_t plen = 0, u = s;
+        while (state[u] == 0 && pair[u] >= 0) {
+            state[u] = 1;
+            path[plen++] = u;
+            u = pair[u];
+        }
+        if (state[u] == 1) {
+            int32_t i = 0;
+            while (path[i] != u) i++;
+            if (plen - i != 2) {
+                *out_len = plen - i;
+                return;
+            }
+        }
+        state[u] = 2;
+        for (int32_t k = 0; k < plen; k++) state[path[k]] = 2;
+    }
+}
+}  // namespace
+
+int64_t resolve_matching(Ctx &c, int32_t N, const int32_t *pair, const double *score, int32_t *match,
+                         uint8_t *isrep) {
+    if (N == 0) return 0;
+    KScope ks(c, "matching", 32.0 * N);
+    unsigned long long *best = c.alloc<unsigned long long>(N);
+    int32_t *claim = c.alloc<int32_t>(N);
+    unsigned long long *npairs = c.alloc<unsigned long long>(1);
+    int32_t *flags = c.alloc<int32_t>(2);
+    c.zero(best, N);
+    fill_i32(c, claim, -1, N);
+    c.zero(npairs, 1);
+    c.zero(flags, 2);
+    const unsigned g = (unsigned)cdiv(N, 256);
+    k_match_claim1<<<g, 256, 0, c.stream>>>(N, pair, score, best, flags);
+    DHGP_LAUNCHED(c);
+    k_match_claim2<<<g, 256, 0, c.stream>>>(N, pair, score, best, claim);
+    DHGP_LAUNCHED(c);
+    k_match_final<<<g, 256, 0, c.stream>>>(N, pair, claim, nullptr, match, isrep, npairs, flags);
+    DHGP_LAUNCHED(c);
+    int32_t hf[2];
+    unsigned long long hp = 0;
+    c.d2h(hf, flags, 2);
+    c.d2h(&hp, npairs, 1);
+    c.sync();
+    if (hf[0]) {
+        int8_t *state = c.alloc<int8_t>(N);
+        int32_t *path = c.alloc<int32_t>(N);
+        int32_t *clen = c.alloc<int32_t>(1);
+        c.zero(state, N);
+        k_cycle_check<<<1, 1, 0, c.stream>>>(N, pair, state, path, clen);
+        DHGP_LAUNCHED(c);
+        int32_t hl = 0;
+        c.d2h(&hl, clen, 1);
+        c.sync();
+        c.free(state);
+        c.free(path);
+        c.free(clen);
+        if (hl) throw Error{DHGP_ERR_MATCHING, "pairing cycle of length " + std::to_string(hl) + " (expected 2)"};
+    }
+    if (hf[1]) {  // a long run of won claims: pointer jumping
+        int32_t *r0 = c.alloc<int32_t>(N), *n0 = c.alloc<int32_t>(N);
+        int32_t *r1 = c.alloc<int32_t>(N), *n1 = c.alloc<int32_t>(N);
+        k_pj_init<<<g, 256, 0, c.stream>>>(N, pair, claim, r0, n0);
+        DHGP_LAUNCHED(c);
+        for (int it = 0; it <= bitlen((uint64_t)N); it++) {
+            k_pj_step<<<g, 256, 0, c.stream>>>(N, r0, n0, r1, n1);
+            DHGP_LAUNCHED(c);
+            std::swap(r0, r1);
+            std::swap(n0, n1);
+        }
+        c.zero(npairs, 1);
+        k_match_final<<<g, 256, 0, c.stream>>>(N, pair, claim, r0, match, isrep, npairs, flags);
+        DHGP_LAUNCHED(c);
+        c.d2h(&hp, npairs, 1);
+        c.sync();
+        c.free(r0);
+        c.free(n0);
+        c.free(r1);
+        c.free(n1);
+    }
+    c.free(best);
+    c.free(claim);
+    c.free(npairs);
+    c.free(flags);
+    return (int64_t)(hp / 2);
+}
+
+// ===========================================================================
+// A9 contraction
+// ===========================================================================
+namespace {
+__global__ void k_gamma(int32_t N, const int32_t *match, const int64_t *rank, const int32_t *size, int32_t *gamma,
+                        int32_t *ma, int32_t *mb, int32_t *csize) {
+    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= N) return;
+    int32_t m = match[v];
+    int32_t r = m < (int32_t)v ? m : (int32_t)v;
+    gamma[v] = (int32_t)rank[r];
+    if (r == (int32_t)v) {
+        int64_t cn = rank[v];
+        ma[cn] = (int32_t)v;
+        mb[cn] = m != (int32_t)v ? m : -1;
+        // sizes add up; the reference casts the int64 sum to int32 (hgraph.py:226)
+        csize[cn] = (int32_t)((int64_t)size[v] + (m != (int32_t)v ? (int64_t)size[m] : 0));
+    }
+}
+}  // namespace
+
+// gamma-image of every per-h-edge list, sorted and deduplicated
+static void contract_edge_list(Ctx &c, int32_t E, const int64_t *off, const int32_t *dat, int64_t nnz,
+                               const int32_t *gamma, int32_t *tmp, int64_t **out_off, int32_t **out_dat,
+                               int64_t *out_nnz) {
+    int64_t *cnt = c.alloc<int64_t>(E);
+    seg_sort(c, E, off, dat, gamma, tmp);
+    seg_unique_count(c, E, off, tmp, cnt);
+    *out_off = c.alloc<int64_t>((int64_t)E + 1);
+    scan_excl<int64_t>(c, cnt, *out_off, E);
+    c.d2h(out_nnz, *out_off + E, 1);
+    c.sync();
+    *out_dat = c.alloc<int32_t>(*out_nnz);
+    seg_unique_write(c, E, off, tmp, *out_off, *out_dat);
+    c.free(cnt);
+    (void)nnz;
+}
+
+void contract(Ctx &c, DLevel &fine, const int32_t *match, const uint8_t *isrep, DLevel &coarse) {
+    KScope ks(c, "contract", (double)(16.0 * (fine.Ps + fine.Pd + fine.U) + 24.0 * fine.E + 32.0 * fine.N));
+    const int32_t N = fine.N, E = fine.E;
+    int64_t *rank = c.alloc<int64_t>((int64_t)N + 1);
+    scan_excl<uint8_t>(c, isrep, rank, N);
+    int64_t nc64 = 0;
+    c.d2h(&nc64, rank + N, 1);
+    c.sync();
+    const int32_t nc = (int32_t)nc64;
+    fine.gamma = c.alloc<int32_t>(N);
+    int32_t *ma = c.alloc<int32_t>(nc), *mb = c.alloc<int32_t>(nc);
+    coarse.N = nc;
+    coarse.E = E;
+    coarse.size = c.alloc<int32_t>(nc);
+    k_gamma<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(N, match, rank, fine.size, fine.gamma, ma, mb, coarse.size);
+    DHGP_LAUNCHED(c);
+    c.free(rank);
+    // per-h-edge families: sorted unique gamma image (coarsen.py:163-166)
+    int64_t cap = std::max(fine.Ps, std::max(fine.Pd, fine.U));
+    int32_t *tmp = c.alloc<int32_t>(cap);
+    contract_edge_list(c, E, fine.src_off, fine.src_dat, fine.Ps, fine.gamma, tmp, &coarse.src_off, &coarse.src_dat,
+                       &coarse.Ps);
+    contract_edge_list(c, E, fine.dst_off, fine.dst_dat, fine.Pd, fine.gamma, tmp, &coarse.dst_off, &coarse.dst_dat,
+                       &coarse.Pd);
+    contract_edge_list(c, E, fine.pin_off, fine.pin_dat, fine.U, fine.gamma, tmp, &coarse.pin_off, &coarse.pin_dat,
+                       &coarse.U);
+    c.free(tmp);
+    // per-node families: union of the two members' sorted lists
+    int64_t *cnt = c.alloc<int64_t>(nc);
+    coarse.in_off = c.alloc<int64_t>((int64_t)nc + 1);
+    merge_union_count(c, nc, ma, mb, fine.in_off, fine.in_dat, cnt);
+    scan_excl<int64_t>(c, cnt, coarse.in_off, nc);
+    coarse.inc_off = c.alloc<int64_t>((int64_t)nc + 1);
+    merge_union_count(c, nc, ma, mb, fine.inc_off, fine.inc_dat, cnt);
+    scan_excl<int64_t>(c, cnt, coarse.inc_off, nc);
+    int64_t tot[2];
+    c.d2h(&tot[0], coarse.in_off + nc, 1);
+    c.d2h(&tot[1], coarse.inc_off + nc, 1);
+    c.sync();
+    coarse.Sin = tot[0];
+    coarse.in_dat = c.alloc<int32_t>(tot[0]);
+    coarse.inc_dat = c.alloc<int32_t>(tot[1]);
+    merge_union_write(c, nc, ma, mb, fine.in_off, fine.in_dat, coarse.in_off, coarse.in_dat);
+    merge_union_write(c, nc, ma, mb, fine.inc_off, fine.inc_dat, coarse.inc_off, coarse.inc_dat);
+    c.free(cnt);
+    c.free(ma);
+    c.free(mb);
+}
+
+}  // namespace dhgp

@@ -1,0 +1,325 @@
+// common.cuh — shared device/host utilities for libdhgp (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/dhgp.h"
+
+namespace dhgp {
+
+// ---------------------------------------------------------------------------
+// errors
+// ---------------------------------------------------------------------------
+struct Error {
+    int code;
+    std::string msg;
+};
+
+void set_error(int code, const std::string &msg);
+const char *last_error();
+
+#define DHGP_CUDA(call)                                                                              \
+    do {                                                                                             \
+        cudaError_t _e = (call);                                                                     \
+        if (_e != cudaSuccess) {                                                                     \
+            throw ::dhgp::Error{DHGP_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(_e) + \
+                                                   " (" + __FILE__ + ":" + std::to_string(__LINE__) + ")"}; \
+        }                                                                                            \
+    } while (0)
+
+#define DHGP_LAUNCHED(ctx)                                                                           \
+    do {                                                                                             \
+        cudaError_t _e = cudaGetLastError();                                                         \
+        if (_e != cudaSuccess)                                                                       \
+            throw ::dhgp::Error{DHGP_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(_e) + \
+                                                   " (" + __FILE__ + ":" + std::to_string(__LINE__) + ")"}; \
+        (ctx).launches++;                                                                            \
+    } while (0)
+
+// ---------------------------------------------------------------------------
+// execution context: one stream per call, stream-ordered pool allocations
+// ---------------------------------------------------------------------------
+struct KernelStat {
+    const char *name;
+    int64_t launches;
+    double ms;
+    double bytes;
+};
+
+struct Ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int64_t launches = 0;
+    int num_sms = 148;
+    // optional per-kernel event timing (bench/profiling only)
+    bool profiling = false;
+    std::vector<KernelStat> kstats;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending_ev;
+    std::vector<int> pending_idx;
+    std::vector<double> pending_bytes;
+
+    template <class T>
+    T *alloc(int64_t n) {
+        void *p = nullptr;
+        size_t bytes = (size_t)(n > 0 ? n : 1) * sizeof(T);
+        DHGP_CUDA(cudaMallocAsync(&p, bytes, stream));
+        return (T *)p;
+    }
+    template <class T>
+    void free(T *p) {
+        if (p) DHGP_CUDA(cudaFreeAsync((void *)p, stream));
+    }
+    template <class T>
+    void zero(T *p, int64_t n) {
+        if (n > 0) DHGP_CUDA(cudaMemsetAsync(p, 0, (size_t)n * sizeof(T), stream));
+    }
+    template <class T>
+    void fill_bytes(T *p, int v, int64_t n) {
+        if (n > 0) DHGP_CUDA(cudaMemsetAsync(p, v, (size_t)n * sizeof(T), stream));
+    }
+    template <class T>
+    void h2d(T *d, const T *h, int64_t n) {
+        if (n > 0) DHGP_CUDA(cudaMemcpyAsync(d, h, (size_t)n * sizeof(T), cudaMemcpyHostToDevice, stream));
+    }
+    template <class T>
+    void d2h(T *h, const T *d, int64_t n) {
+        if (n > 0) DHGP_CUDA(cudaMemcpyAsync(h, d, (size_t)n * sizeof(T), cudaMemcpyDeviceToHost, stream));
+    }
+    template <class T>
+    void d2d(T *dst, const T *src, int64_t n) {
+        if (n > 0) DHGP_CUDA(cudaMemcpyAsync(dst, src, (size_t)n * sizeof(T), cudaMemcpyDeviceToDevice, stream));
+    }
+    void sync() { DHGP_CUDA(cudaStreamSynchronize(stream)); }
+
+    // profiling brackets: kbegin(name) ... kend(bytes)
+    int kbegin(const char *name);
+    void kend(int idx, double bytes);
+    void flush_profile();
+};
+
+struct KScope {
+    Ctx &c;
+    int idx;
+    double bytes;
+    KScope(Ctx &ctx, const char *name, double b = 0) : c(ctx), idx(-1), bytes(b) {
+        if (c.profiling) idx = c.kbegin(name);
+    }
+    ~KScope() {
+        if (idx >= 0) c.kend(idx, bytes);
+    }
+};
+
+inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline int bitlen(uint64_t x) {
+    int b = 0;
+    while (x) {
+        b++;
+        x >>= 1;
+    }
+    return b;
+}
+
+// ---------------------------------------------------------------------------
+// device helpers
+// ---------------------------------------------------------------------------
+#define FULL_MASK 0xffffffffu
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+__device__ __forceinline__ int warp_id() { return threadIdx.x >> 5; }
+
+template <class T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(FULL_MASK, v, d);
+    return v;
+}
+template <class T>
+__device__ __forceinline__ T warp_max(T v) {
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        T o = __shfl_xor_sync(FULL_MASK, v, d);
+        v = o > v ? o : v;
+    }
+    return v;
+}
+template <class T>
+__device__ __forceinline__ T warp_min(T v) {
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        T o = __shfl_xor_sync(FULL_MASK, v, d);
+        v = o < v ? o : v;
+    }
+    return v;
+}
+// inclusive prefix sum across the warp
+template <class T>
+__device__ __forceinline__ T warp_incl_scan(T v) {
+    const int lane = lane_id();
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        T o = __shfl_up_sync(FULL_MASK, v, d);
+        if (lane >= d) v += o;
+    }
+    return v;
+}
+
+// lower bound in sorted a[lo, hi)
+template <class T>
+__device__ __forceinline__ int64_t lower_bound_dev(const T *a, int64_t lo, int64_t hi, T key) {
+    while (lo < hi) {
+        int64_t mid = (lo + hi) >> 1;
+        if (a[mid] < key)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    return lo;
+}
+
+// index of key in strictly increasing a[lo, hi) or -1 (_kernels.pyx:22-32)
+__device__ __forceinline__ int64_t bsearch_dev(const int32_t *a, int64_t lo, int64_t hi, int32_t key) {
+    int64_t p = lower_bound_dev<int32_t>(a, lo, hi, key);
+    return (p < hi && a[p] == key) ? p : -1;
+}
+
+// In-register warp bitonic sort of 32*K unsigned keys (ascending); element
+// index of v[k] on lane l is k*32 + l.
+template <int K>
+__device__ __forceinline__ void warp_bitonic_sort(uint32_t (&v)[K]) {
+    const int lane = lane_id();
+#pragma unroll
+    for (int size = 2; size <= 32 * K; size <<= 1) {
+#pragma unroll
+        for (int j = size >> 1; j > 0; j >>= 1) {
+            if (j >= 32) {
+                const int jk = j >> 5;
+#pragma unroll
+                for (int k = 0; k < K; k++) {
+                    const int partner = k ^ jk;
+                    if (partner > k) {
+                        const int idx = k * 32 + lane;
+                        const bool asc = (idx & size) == 0;
+                        uint32_t a = v[k], b = v[partner];
+                        if ((a > b) == asc) {
+                            v[k] = b;
+                            v[partner] = a;
+                        }
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < K; k++) {
+                    const int idx = k * 32 + lane;
+                    uint32_t o = __shfl_xor_sync(FULL_MASK, v[k], j);
+                    const bool asc = (idx & size) == 0;
+                    const bool lower = (idx & j) == 0;
+                    v[k] = (lower == asc) ? min(v[k], o) : max(v[k], o);
+                }
+            }
+        }
+    }
+}
+
+// 64-bit keyed variant (key in high bits, payload in low bits of one u64)
+template <int K>
+__device__ __forceinline__ void warp_bitonic_sort64(uint64_t (&v)[K]) {
+    const int lane = lane_id();
+#pragma unroll
+    for (int size = 2; size <= 32 * K; size <<= 1) {
+#pragma unroll
+        for (int j = size >> 1; j > 0; j >>= 1) {
+            if (j >= 32) {
+                const int jk = j >> 5;
+#pragma unroll
+                for (int k = 0; k < K; k++) {
+                    const int partner = k ^ jk;
+                    if (partner > k) {
+                        const int idx = k * 32 + lane;
+                        const bool asc = (idx & size) == 0;
+                        uint64_t a = v[k], b = v[partner];
+                        if ((a > b) == asc) {
+                            v[k] = b;
+                            v[partner] = a;
+                        }
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < K; k++) {
+                    const int idx = k * 32 + lane;
+                    uint64_t o = __shfl_xor_sync(FULL_MASK, v[k], j);
+                    const bool asc = (idx & size) == 0;
+                    const bool lower = (idx & j) == 0;
+                    v[k] = (lower == asc) ? (v[k] < o ? v[k] : o) : (v[k] > o ? v[k] : o);
+                }
+            }
+        }
+    }
+}
+
+// block-wide bitonic sort of n_pow2 u64 keys in shared memory (ascending)
+__device__ __forceinline__ void block_bitonic_sort64(uint64_t *s, int n_pow2) {
+    for (int size = 2; size <= n_pow2; size <<= 1) {
+        for (int j = size >> 1; j > 0; j >>= 1) {
+            __syncthreads();
+            for (int t = threadIdx.x; t < (n_pow2 >> 1); t += blockDim.x) {
+                int lo = 2 * j * (t / j) + (t % j);
+                int hi = lo + j;
+                bool asc = (lo & size) == 0;
+                uint64_t a = s[lo], b = s[hi];
+                if ((a > b) == asc) {
+                    s[lo] = b;
+                    s[hi] = a;
+                }
+            }
+        }
+    }
+    __syncthreads();
+}
+__device__ __forceinline__ void block_bitonic_sort32(uint32_t *s, int n_pow2) {
+    for (int size = 2; size <= n_pow2; size <<= 1) {
+        for (int j = size >> 1; j > 0; j >>= 1) {
+            __syncthreads();
+            for (int t = threadIdx.x; t < (n_pow2 >> 1); t += blockDim.x) {
+                int lo = 2 * j * (t / j) + (t % j);
+                int hi = lo + j;
+                bool asc = (lo & size) == 0;
+                uint32_t a = s[lo], b = s[hi];
+                if ((a > b) == asc) {
+                    s[lo] = b;
+                    s[hi] = a;
+                }
+            }
+        }
+    }
+    __syncthreads();
+}
+
+__host__ __device__ __forceinline__ int next_pow2(int x) {
+    int p = 1;
+    while (p < x) p <<= 1;
+    return p;
+}
+
+// block reduce (sum) helpers; `sh` must hold >= 32 elements
+template <class T>
+__device__ __forceinline__ T block_sum(T v, T *sh) {
+    v = warp_sum(v);
+    __syncthreads();
+    if (lane_id() == 0) sh[warp_id()] = v;
+    __syncthreads();
+    T r = 0;
+    if (warp_id() == 0) {
+        r = (lane_id() < (int)(blockDim.x >> 5)) ? sh[lane_id()] : (T)0;
+        r = warp_sum(r);
+    }
+    return r;  // valid in thread 0
+}
+
+}  // namespace dhgp

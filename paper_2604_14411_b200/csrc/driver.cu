@@ -1,0 +1,528 @@
+// driver.cu — multi-level orchestration and the C-ABI (driver.py:76-163).
+#include <chrono>
+#include <climits>
+#include <cstdlib>
+#include <mutex>
+
+#include "coarsen.cuh"
+#include "prims.cuh"
+#include "refine.cuh"
+
+namespace dhgp {
+
+// ---------------------------------------------------------------------------
+// errors
+// ---------------------------------------------------------------------------
+static thread_local std::string g_last_error;
+void set_error(int code, const std::string &msg) {
+    (void)code;
+    g_last_error = msg;
+}
+const char *last_error() { return g_last_error.c_str(); }
+
+// ---------------------------------------------------------------------------
+// per-kernel event timing (bench / profiling only)
+// ---------------------------------------------------------------------------
+int Ctx::kbegin(const char *name) {
+    int idx = -1;
+    for (size_t i = 0; i < kstats.size(); i++)
+        if (kstats[i].name == name) idx = (int)i;
+    if (idx < 0) {
+        kstats.push_back(KernelStat{name, 0, 0.0, 0.0});
+        idx = (int)kstats.size() - 1;
+    }
+    cudaEvent_t a, b;
+    DHGP_CUDA(cudaEventCreate(&a));
+    DHGP_CUDA(cudaEventCreate(&b));
+    DHGP_CUDA(cudaEventRecord(a, stream));
+    pending_ev.push_back({a, b});
+    pending_idx.push_back(idx);
+    pending_bytes.push_back(0.0);
+    return (int)pending_ev.size() - 1;
+}
+void Ctx::kend(int p, double bytes) {
+    DHGP_CUDA(cudaEventRecord(pending_ev[p].second, stream));
+    pending_bytes[p] = bytes;
+}
+void Ctx::flush_profile() {
+    if (pending_ev.empty()) return;
+    DHGP_CUDA(cudaStreamSynchronize(stream));
+    for (size_t i = 0; i < pending_ev.size(); i++) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, pending_ev[i].first, pending_ev[i].second);
+        KernelStat &k = kstats[pending_idx[i]];
+        k.launches++;
+        k.ms += ms;
+        k.bytes += pending_bytes[i];
+        cudaEventDestroy(pending_ev[i].first);
+        cudaEventDestroy(pending_ev[i].second);
+    }
+    pending_ev.clear();
+    pending_idx.clear();
+    pending_bytes.clear();
+}
+
+// ---------------------------------------------------------------------------
+// device setup: one cached stream per device, stream-ordered pool that keeps
+// freed blocks (levels are allocated and released every call)
+// ---------------------------------------------------------------------------
+std::mutex g_mu;
+static cudaStream_t g_streams[64];
+static int g_sms[64];
+
+static void setup(Ctx &c, int device) {
+    if (device < 0 || device >= 64) throw Error{DHGP_ERR_ARG, "bad device ordinal"};
+    c.device = device;
+    DHGP_CUDA(cudaSetDevice(device));
+    if (!g_streams[device]) {
+        DHGP_CUDA(cudaStreamCreateWithFlags(&g_streams[device], cudaStreamNonBlocking));
+        cudaMemPool_t pool;
+        DHGP_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+        uint64_t thr = UINT64_MAX;
+        DHGP_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+        DHGP_CUDA(cudaDeviceGetAttribute(&g_sms[device], cudaDevAttrMultiProcessorCount, device));
+    }
+    c.stream = g_streams[device];
+    c.num_sms = g_sms[device];
+}
+
+void seams_setup(Ctx &c, int device) { setup(c, device); }
+
+namespace {
+__global__ void k_project(int32_t N, const int32_t *gamma, const int32_t *coarse, int32_t *fine) {
+    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v < N) fine[v] = coarse[gamma[v]];
+}
+__global__ void k_used(int32_t N, const int32_t *assign, uint8_t *used) {
+    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v < N) used[assign[v]] = 1;
+}
+__global__ void k_remap(int32_t N, const int64_t *rank, int32_t *assign) {
+    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v < N) assign[v] = (int32_t)rank[assign[v]];
+}
+}  // namespace
+
+struct PartitionResult {
+    std::vector<int32_t> assign;
+    int32_t num_parts = 0;
+    std::vector<DLevel> levels_meta;  // N/E/Ps/Pd only
+    std::vector<std::vector<double>> trace;
+    double phase_ms[3] = {0, 0, 0};
+};
+
+static double now_ms() {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+// partition (driver.py:76-163) over a resident input
+static void run_partition(Ctx &c, const DInput &in, const dhgp_config &cfg, PartitionResult &res,
+                          dhgp_observer_fn obs, void *user) {
+    const int64_t omega = cfg.max_size, delta = cfg.max_inbound;
+    if (cfg.max_rounds < 1 || cfg.batch_size < 1 || cfg.max_levels < 1)
+        throw Error{DHGP_ERR_ARG, "max_rounds, batch_size and max_levels must be >= 1"};
+    // check_feasibility order (hgraph.py:382-401)
+    if (omega < 1) throw Error{DHGP_ERR_INFEASIBLE, "max_size must be >= 1, got " + std::to_string(omega)};
+    if (delta < 0) throw Error{DHGP_ERR_INFEASIBLE, "max_inbound must be >= 0, got " + std::to_string(delta)};
+    if (in.max_edge_pins > kMaxSegSort)
+        throw Error{DHGP_ERR_UNSUPPORTED, "h-edge with " + std::to_string(in.max_edge_pins) +
+                                              " pin slots exceeds the supported maximum " +
+                                              std::to_string(kMaxSegSort)};
+    DWeights W;
+    prepare_weights(c, in, W);
+    if (!W.integral) {
+        W.release(c);
+        throw Error{DHGP_ERR_UNSUPPORTED,
+                    "non-integral h-edge weights (or a weight total >= 2^53) are outside the exact-integer "
+                    "device path"};
+    }
+    std::vector<DLevel> levels(1);
+    build_level0(c, in, levels[0]);
+    const int32_t N0 = in.N;
+    if (N0 > 0) {
+        int32_t bs, bi;
+        feasibility(c, levels[0], omega, delta, &bs, &bi);
+        if (bs >= 0) {
+            int32_t sz;
+            c.d2h(&sz, levels[0].size + bs, 1);
+            c.sync();
+            levels[0].release(c);
+            W.release(c);
+            throw Error{DHGP_ERR_INFEASIBLE, "node " + std::to_string(bs) + " has size " + std::to_string(sz) +
+                                                 " > max_size " + std::to_string(omega)};
+        }
+        if (bi >= 0) {
+            int64_t o[2];
+            c.d2h(o, levels[0].in_off + bi, 2);
+            c.sync();
+            levels[0].release(c);
+            W.release(c);
+            throw Error{DHGP_ERR_INFEASIBLE, "node " + std::to_string(bi) + " has " + std::to_string(o[1] - o[0]) +
+                                                 " inbound edges > max_inbound " + std::to_string(delta)};
+        }
+    }
+    const double t0 = now_ms();
+    const int64_t target = (N0 + omega - 1) / omega;
+    // ---- coarsening (driver.py:97-118) -----------------------------------
+    try {
+        while (levels.back().N > target) {
+            if ((int64_t)levels.size() - 1 >= cfg.max_levels)
+                throw Error{DHGP_ERR_MAX_LEVELS, "coarsening exceeded max_levels=" + std::to_string(cfg.max_levels) +
+                                                     " (" + std::to_string(levels.back().N) + " nodes, target " +
+                                                     std::to_string(target) + ")"};
+            DLevel &fine = levels.back();
+            const int32_t n = fine.N;
+            int32_t *pair = c.alloc<int32_t>(n), *match = c.alloc<int32_t>(n);
+            double *score = c.alloc<double>(n);
+            uint8_t *isrep = c.alloc<uint8_t>(n);
+            score_select(c, fine, W, omega, delta, pair, score);
+            int64_t npairs = resolve_matching(c, n, pair, score, match, isrep);
+            if (npairs == 0) {
+                c.free(pair);
+                c.free(match);
+                c.free(score);
+                c.free(isrep);
+                break;
+            }
+            DLevel coarse;
+            contract(c, levels.back(), match, isrep, coarse);
+            levels.push_back(coarse);
+            if (obs) {
+                DLevel &f = levels[levels.size() - 2];
+                DLevel &cl = levels.back();
+                std::vector<int32_t> hp(n), hm(n), hg(n), hsd(cl.Ps), hdd(cl.Pd), hsz(cl.N);
+                std::vector<double> hs(n);
+                std::vector<int64_t> hso((int64_t)cl.E + 1), hdo((int64_t)cl.E + 1);
+                c.d2h(hp.data(), pair, n);
+                c.d2h(hs.data(), score, n);
+                c.d2h(hm.data(), match, n);
+                c.d2h(hg.data(), f.gamma, n);
+                c.d2h(hso.data(), cl.src_off, (int64_t)cl.E + 1);
+                c.d2h(hsd.data(), cl.src_dat, cl.Ps);
+                c.d2h(hdo.data(), cl.dst_off, (int64_t)cl.E + 1);
+                c.d2h(hdd.data(), cl.dst_dat, cl.Pd);
+                c.d2h(hsz.data(), cl.size, cl.N);
+                c.sync();
+                dhgp_event ev;
+                memset(&ev, 0, sizeof ev);
+                ev.kind = DHGP_EVENT_LEVEL;
+                ev.level = (int32_t)levels.size() - 2;
+                ev.num_nodes = n;
+                ev.num_edges = cl.E;
+                ev.num_coarse = cl.N;
+                ev.pair = hp.data();
+                ev.score = hs.data();
+                ev.match = hm.data();
+                ev.gamma = hg.data();
+                ev.c_src_off = hso.data();
+                ev.c_src_dat = hsd.data();
+                ev.c_dst_off = hdo.data();
+                ev.c_dst_dat = hdd.data();
+                ev.c_node_size = hsz.data();
+                obs(&ev, user);
+            }
+            c.free(pair);
+            c.free(match);
+            c.free(score);
+            c.free(isrep);
+        }
+    } catch (...) {
+        for (auto &L : levels) L.release(c);
+        W.release(c);
+        throw;
+    }
+    const double t1 = now_ms();
+    // ---- initial partitioning + uncoarsening (driver.py:121-134) -----------
+    const int32_t K = levels.back().N;
+    int32_t *assign = c.alloc<int32_t>(N0), *assign2 = c.alloc<int32_t>(N0);
+    iota_i32(c, assign, K);
+    res.trace.assign(levels.size(), {});
+    for (auto &L : levels) {
+        DLevel m;
+        m.N = L.N;
+        m.E = L.E;
+        m.Ps = L.Ps;
+        m.Pd = L.Pd;
+        res.levels_meta.push_back(m);
+    }
+    RoundObserver robs;
+    if (obs) {
+        robs = [&](const RoundRecord &r) {
+            dhgp_event ev;
+            memset(&ev, 0, sizeof ev);
+            ev.kind = DHGP_EVENT_ROUND;
+            ev.level = r.level;
+            ev.round = r.round;
+            ev.num_nodes = (int32_t)r.assign.size();
+            ev.num_edges = in.E;
+            ev.num_parts = r.num_parts;
+            ev.assign = r.assign.data();
+            ev.num_moves = (int32_t)r.node.size();
+            ev.mv_node = r.node.data();
+            ev.mv_from = r.from.data();
+            ev.mv_to = r.to.data();
+            ev.mv_gain_iso = r.gain_iso.data();
+            ev.mv_gain_seq = r.gain_seq.data();
+            ev.k = r.k;
+            ev.total_gain = r.total_gain;
+            ev.active = r.active.data();
+            obs(&ev, user);
+        };
+    }
+    try {
+        const int64_t L = (int64_t)levels.size();
+        refine_level(c, levels[L - 1], W, assign, K, omega, delta, cfg.max_rounds, (int32_t)(L - 1), res.trace[0],
+                     obs ? &robs : nullptr);
+        for (int64_t li = L - 2; li >= 0; li--) {
+            DLevel &f = levels[li];
+            if (f.N > 0) {
+                k_project<<<(unsigned)cdiv(f.N, 256), 256, 0, c.stream>>>(f.N, f.gamma, assign, assign2);
+                DHGP_LAUNCHED(c);
+            }
+            std::swap(assign, assign2);
+            levels[li + 1].release(c);
+            refine_level(c, f, W, assign, K, omega, delta, cfg.max_rounds, (int32_t)li, res.trace[L - 1 - li],
+                         obs ? &robs : nullptr);
+        }
+        const double t2 = now_ms();
+        // ---- compaction (driver.py:137-143) + check_validity (144-146) ------
+        int32_t final_parts = 0;
+        if (N0 > 0) {
+            uint8_t *used = c.alloc<uint8_t>(K);
+            int64_t *rank = c.alloc<int64_t>((int64_t)K + 1);
+            c.zero(used, K);
+            k_used<<<(unsigned)cdiv(N0, 256), 256, 0, c.stream>>>(N0, assign, used);
+            DHGP_LAUNCHED(c);
+            scan_excl<uint8_t>(c, used, rank, K);
+            k_remap<<<(unsigned)cdiv(N0, 256), 256, 0, c.stream>>>(N0, rank, assign);
+            DHGP_LAUNCHED(c);
+            int64_t fp = 0;
+            c.d2h(&fp, rank + K, 1);
+            c.sync();
+            final_parts = (int32_t)fp;
+            c.free(used);
+            c.free(rank);
+            int64_t *sz = c.alloc<int64_t>(final_parts), *ib = c.alloc<int64_t>(final_parts);
+            evaluate_assign(c, levels[0], W, assign, final_parts, sz, ib, nullptr);
+            std::vector<int64_t> hsz(final_parts), hib(final_parts);
+            c.d2h(hsz.data(), sz, final_parts);
+            c.d2h(hib.data(), ib, final_parts);
+            res.assign.resize(N0);
+            c.d2h(res.assign.data(), assign, N0);
+            c.sync();
+            c.free(sz);
+            c.free(ib);
+            for (int32_t p = 0; p < final_parts; p++) {
+                if (hsz[p] > omega || hib[p] > delta) {
+                    std::string kind = hsz[p] > omega ? "size" : "inbound";
+                    int64_t actual = hsz[p] > omega ? hsz[p] : hib[p];
+                    int64_t limit = hsz[p] > omega ? omega : delta;
+                    throw Error{DHGP_ERR_INVALID_RESULT,
+                                "internal error: produced an invalid partitioning: [Violation(part=" +
+                                    std::to_string(p) + ", kind='" + kind + "', actual=" + std::to_string(actual) +
+                                    ", limit=" + std::to_string(limit) + ")]"};
+                }
+            }
+        }
+        res.num_parts = final_parts;
+        const double t3 = now_ms();
+        res.phase_ms[0] = t1 - t0;
+        res.phase_ms[1] = t2 - t1;
+        res.phase_ms[2] = t3 - t0;
+    } catch (...) {
+        for (auto &L : levels) L.release(c);
+        W.release(c);
+        c.free(assign);
+        c.free(assign2);
+        throw;
+    }
+    for (auto &L : levels) L.release(c);
+    W.release(c);
+    c.free(assign);
+    c.free(assign2);
+    c.sync();
+}
+
+static void fill_stats(const PartitionResult &r, dhgp_stats *s, int64_t launches) {
+    if (!s) return;
+    memset(s, 0, sizeof *s);
+    const int64_t nl = (int64_t)r.levels_meta.size();
+    s->num_levels = nl;
+    s->level_nodes = (int64_t *)malloc(sizeof(int64_t) * (nl ? nl : 1));
+    s->level_edges = (int64_t *)malloc(sizeof(int64_t) * (nl ? nl : 1));
+    s->level_pins = (int64_t *)malloc(sizeof(int64_t) * (nl ? nl : 1));
+    s->trace_off = (int64_t *)malloc(sizeof(int64_t) * (nl + 1));
+    int64_t tot = 0;
+    for (auto &t : r.trace) tot += (int64_t)t.size();
+    s->trace_val = (double *)malloc(sizeof(double) * (tot ? tot : 1));
+    s->trace_off[0] = 0;
+    for (int64_t l = 0; l < nl; l++) {
+        s->level_nodes[l] = r.levels_meta[l].N;
+        s->level_edges[l] = r.levels_meta[l].E;
+        s->level_pins[l] = r.levels_meta[l].Ps + r.levels_meta[l].Pd;
+        const auto &t = r.trace[l];
+        for (size_t i = 0; i < t.size(); i++) s->trace_val[s->trace_off[l] + i] = t[i];
+        s->trace_off[l + 1] = s->trace_off[l] + (int64_t)t.size();
+    }
+    s->num_partitions = r.num_parts;
+    for (int i = 0; i < 3; i++) s->phase_ms[i] = r.phase_ms[i];
+    s->gpu_launches = launches;
+}
+
+}  // namespace dhgp
+
+// ===========================================================================
+// C-ABI
+// ===========================================================================
+using namespace dhgp;
+
+struct dhgp_session {
+    int device = 0;
+    DInput in;
+    bool profiling = false;
+    std::vector<KernelStat> kstats;
+};
+
+#define DHGP_GUARD_BEGIN \
+    std::lock_guard<std::mutex> _lk(g_mu); \
+    try {
+#define DHGP_GUARD_END                      \
+    }                                       \
+    catch (const Error &e) {                \
+        set_error(e.code, e.msg);           \
+        return e.code;                      \
+    }                                       \
+    catch (const std::exception &e) {       \
+        set_error(DHGP_ERR_CUDA, e.what()); \
+        return DHGP_ERR_CUDA;               \
+    }                                       \
+    return DHGP_OK;
+
+static void check_graph(const dhgp_graph *g) {
+    if (!g || g->num_nodes < 0 || g->num_edges < 0 || !g->src_off || !g->dst_off ||
+        (g->num_edges > 0 && !g->edge_weight))
+        throw Error{DHGP_ERR_ARG, "malformed dhgp_graph"};
+}
+
+extern "C" {
+
+const char *dhgp_last_error(void) { return last_error(); }
+
+const char *dhgp_build_info(void) {
+    static std::string s = std::string("libdhgp sm_100a, nvcc ") + std::to_string(__CUDACC_VER_MAJOR__) + "." +
+                           std::to_string(__CUDACC_VER_MINOR__);
+    return s.c_str();
+}
+
+int dhgp_device_count(int32_t *count) {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess) {
+        set_error(DHGP_ERR_CUDA, cudaGetErrorString(e));
+        *count = 0;
+        return DHGP_ERR_CUDA;
+    }
+    *count = n;
+    return DHGP_OK;
+}
+
+int dhgp_partition(const dhgp_graph *g, const dhgp_config *cfg, int32_t *assign_out, int32_t *num_parts_out,
+                   dhgp_stats *stats_out, dhgp_observer_fn obs, void *user) {
+    DHGP_GUARD_BEGIN
+    check_graph(g);
+    Ctx c;
+    setup(c, cfg->device);
+    DInput in;
+    upload_input(c, *g, in);
+    PartitionResult r;
+    try {
+        run_partition(c, in, *cfg, r, obs, user);
+    } catch (...) {
+        in.release(c);
+        c.sync();
+        throw;
+    }
+    in.release(c);
+    if (r.assign.size()) memcpy(assign_out, r.assign.data(), sizeof(int32_t) * r.assign.size());
+    *num_parts_out = r.num_parts;
+    fill_stats(r, stats_out, c.launches);
+    DHGP_GUARD_END
+}
+
+void dhgp_stats_free(dhgp_stats *s) {
+    if (!s) return;
+    free(s->level_nodes);
+    free(s->level_edges);
+    free(s->level_pins);
+    free(s->trace_off);
+    free(s->trace_val);
+    memset(s, 0, sizeof *s);
+}
+
+int dhgp_session_create(const dhgp_graph *g, int32_t device, dhgp_session **out) {
+    DHGP_GUARD_BEGIN
+    check_graph(g);
+    Ctx c;
+    setup(c, device);
+    dhgp_session *s = new dhgp_session();
+    s->device = device;
+    upload_input(c, *g, s->in);
+    c.sync();
+    *out = s;
+    DHGP_GUARD_END
+}
+
+int dhgp_session_partition(dhgp_session *s, const dhgp_config *cfg, int32_t *assign_out, int32_t *num_parts_out,
+                           dhgp_stats *stats_out) {
+    DHGP_GUARD_BEGIN
+    Ctx c;
+    setup(c, s->device);
+    c.profiling = s->profiling;
+    dhgp_config cc = *cfg;
+    cc.device = s->device;
+    PartitionResult r;
+    run_partition(c, s->in, cc, r, nullptr, nullptr);
+    if (c.profiling) {
+        c.flush_profile();
+        s->kstats = c.kstats;
+    }
+    if (assign_out && r.assign.size()) memcpy(assign_out, r.assign.data(), sizeof(int32_t) * r.assign.size());
+    if (num_parts_out) *num_parts_out = r.num_parts;
+    fill_stats(r, stats_out, c.launches);
+    DHGP_GUARD_END
+}
+
+void dhgp_session_destroy(dhgp_session *s) {
+    if (!s) return;
+    std::lock_guard<std::mutex> lk(g_mu);
+    try {
+        Ctx c;
+        setup(c, s->device);
+        s->in.release(c);
+        c.sync();
+    } catch (...) {
+    }
+    delete s;
+}
+
+int dhgp_session_set_profiling(dhgp_session *s, int32_t on) {
+    s->profiling = on != 0;
+    return DHGP_OK;
+}
+
+int dhgp_session_kernel_stats(dhgp_session *s, int32_t max_rows, const char **names, int64_t *launches,
+                              double *total_ms, double *bytes, int32_t *rows_out) {
+    int32_t n = (int32_t)std::min<size_t>(s->kstats.size(), (size_t)max_rows);
+    for (int32_t i = 0; i < n; i++) {
+        names[i] = s->kstats[i].name;
+        launches[i] = s->kstats[i].launches;
+        total_ms[i] = s->kstats[i].ms;
+        bytes[i] = s->kstats[i].bytes;
+    }
+    *rows_out = n;
+    return DHGP_OK;
+}
+
+void dhgp_free(void *p) { free(p); }
+
+}  // extern "C"

@@ -1,0 +1,189 @@
+// graph.cu — level-0 upload and incidence materialisation.
+#include <cmath>
+
+#include "graph.cuh"
+#include "prims.cuh"
+
+namespace dhgp {
+
+namespace {
+// weights: finite, >= 0; exact-integer mode needs integral values with a
+// total < 2^53 so every partial sum in any order is exact.
+__global__ void k_check_weights(const double *w, int64_t E, int64_t *wi, unsigned long long *sum, int32_t *flags) {
+    __shared__ int64_t sh[33];
+    int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int64_t v = 0;
+    if (e < E) {
+        double x = w[e];
+        if (!(x >= 0.0) || !isfinite(x)) atomicOr(&flags[0], 1);          // invalid weight
+        if (x != floor(x) || x >= 9007199254740992.0) atomicOr(&flags[0], 2);  // non-integral
+        v = (x >= 0.0 && x < 9007199254740992.0) ? (int64_t)x : 0;
+        wi[e] = v;
+    }
+    int64_t t = block_sum<int64_t>(v, sh);
+    if (threadIdx.x == 0) atomicAdd(sum, (unsigned long long)t);
+}
+
+__global__ void k_rebase(int64_t *off, int64_t n, int64_t base) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) off[i] -= base;
+}
+
+__global__ void k_max_edge(int64_t E, const int64_t *so, const int64_t *dof, int32_t *mx) {
+    int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < E) atomicMax(mx, (int32_t)(so[e + 1] - so[e] + dof[e + 1] - dof[e]));
+}
+
+__global__ void k_comb(int64_t E, const int64_t *so, const int32_t *sd, const int64_t *dof, const int32_t *dd,
+                       int64_t *co, int32_t *cd) {
+    int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e > E) return;
+    co[e] = so[e] + dof[e];
+    if (e == E) return;
+    int64_t o = so[e] + dof[e];
+    for (int64_t p = so[e]; p < so[e + 1]; p++) cd[o++] = sd[p];
+    for (int64_t p = dof[e]; p < dof[e + 1]; p++) cd[o++] = dd[p];
+}
+
+__global__ void k_feasible(int32_t N, const int32_t *size, const int64_t *in_off, int64_t omega, int64_t delta,
+                           int32_t *bad) {
+    int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (n >= N) return;
+    if ((int64_t)size[n] > omega) atomicMin(&bad[0], (int32_t)n);
+    if (in_off[n + 1] - in_off[n] > delta) atomicMin(&bad[1], (int32_t)n);
+}
+}  // namespace
+
+void upload_input(Ctx &c, const dhgp_graph &g, DInput &in) {
+    const int64_t E = g.num_edges;
+    in.N = g.num_nodes;
+    in.E = g.num_edges;
+    const int64_t sb = g.src_off[0], db = g.dst_off[0];
+    in.Ps = g.src_off[E] - sb;
+    in.Pd = g.dst_off[E] - db;
+    in.src_off = c.alloc<int64_t>(E + 1);
+    in.dst_off = c.alloc<int64_t>(E + 1);
+    in.src_dat = c.alloc<int32_t>(in.Ps);
+    in.dst_dat = c.alloc<int32_t>(in.Pd);
+    in.w = c.alloc<double>(E);
+    c.h2d(in.src_off, g.src_off, E + 1);
+    c.h2d(in.dst_off, g.dst_off, E + 1);
+    c.h2d(in.src_dat, g.src_dat + sb, in.Ps);
+    c.h2d(in.dst_dat, g.dst_dat + db, in.Pd);
+    c.h2d(in.w, g.edge_weight, E);
+    if (sb) {
+        k_rebase<<<(unsigned)cdiv(E + 1, 256), 256, 0, c.stream>>>(in.src_off, E + 1, sb);
+        DHGP_LAUNCHED(c);
+    }
+    if (db) {
+        k_rebase<<<(unsigned)cdiv(E + 1, 256), 256, 0, c.stream>>>(in.dst_off, E + 1, db);
+        DHGP_LAUNCHED(c);
+    }
+    in.size = c.alloc<int32_t>(in.N);
+    if (g.node_size)
+        c.h2d(in.size, g.node_size, in.N);
+    else
+        fill_i32(c, in.size, 1, in.N);
+    // largest h-edge (bounds every per-edge sort at every level)
+    int32_t *mx = c.alloc<int32_t>(1);
+    c.zero(mx, 1);
+    if (E > 0) {
+        k_max_edge<<<(unsigned)cdiv(E, 256), 256, 0, c.stream>>>(E, in.src_off, in.dst_off, mx);
+        DHGP_LAUNCHED(c);
+    }
+    c.d2h(&in.max_edge_pins, mx, 1);
+    c.sync();
+    c.free(mx);
+}
+
+void prepare_weights(Ctx &c, const DInput &in, DWeights &W) {
+    W.E = in.E;
+    W.w = in.w;
+    W.wi = c.alloc<int64_t>(W.E);
+    unsigned long long *sum = c.alloc<unsigned long long>(1);
+    int32_t *flags = c.alloc<int32_t>(1);
+    c.zero(sum, 1);
+    c.zero(flags, 1);
+    if (W.E > 0) {
+        k_check_weights<<<(unsigned)cdiv(W.E, 256), 256, 0, c.stream>>>(W.w, W.E, W.wi, sum, flags);
+        DHGP_LAUNCHED(c);
+    }
+    unsigned long long hs = 0;
+    int32_t hf = 0;
+    c.d2h(&hs, sum, 1);
+    c.d2h(&hf, flags, 1);
+    c.sync();
+    c.free(sum);
+    c.free(flags);
+    if (hf & 1) throw Error{DHGP_ERR_ARG, "edge weights must be finite and >= 0"};
+    W.integral = !(hf & 2) && hs < (1ull << 53);
+    W.wsum = (int64_t)hs;
+}
+
+void build_level0(Ctx &c, const DInput &in, DLevel &L) {
+    L.N = in.N;
+    L.E = in.E;
+    L.Ps = in.Ps;
+    L.Pd = in.Pd;
+    L.src_off = in.src_off;
+    L.dst_off = in.dst_off;
+    L.src_dat = in.src_dat;
+    L.dst_dat = in.dst_dat;
+    L.size = in.size;
+    L.borrowed = true;
+    derive_incidence(c, L);
+}
+
+void derive_incidence(Ctx &c, DLevel &L) {
+    KScope ks(c, "incidence");
+    const int64_t E = L.E;
+    // edge_pins = sorted unique (src ∪ dst) per h-edge  (hgraph.py:219-221)
+    const int64_t cap = L.Ps + L.Pd;
+    int64_t *co = c.alloc<int64_t>(E + 1);
+    int32_t *cd = c.alloc<int32_t>(cap);
+    int32_t *tmp = c.alloc<int32_t>(cap);
+    k_comb<<<(unsigned)cdiv(E + 1, 256), 256, 0, c.stream>>>(E, L.src_off, L.src_dat, L.dst_off, L.dst_dat, co, cd);
+    DHGP_LAUNCHED(c);
+    seg_sort(c, E, co, cd, nullptr, tmp);
+    int64_t *cnt = c.alloc<int64_t>(E);
+    seg_unique_count(c, E, co, tmp, cnt);
+    L.pin_off = c.alloc<int64_t>(E + 1);
+    scan_excl<int64_t>(c, cnt, L.pin_off, E);
+    c.d2h(&L.U, L.pin_off + E, 1);
+    c.sync();
+    L.pin_dat = c.alloc<int32_t>(L.U);
+    seg_unique_write(c, E, co, tmp, L.pin_off, L.pin_dat);
+    c.free(co);
+    c.free(cd);
+    c.free(tmp);
+    c.free(cnt);
+    // node_in = transpose(edge_dst), node_inc = transpose(edge_pins)  (hgraph.py:218, 222)
+    L.Sin = L.Pd;
+    L.in_off = c.alloc<int64_t>((int64_t)L.N + 1);
+    L.in_dat = c.alloc<int32_t>(L.Pd);
+    transpose_csr(c, E, L.N, L.dst_off, L.dst_dat, L.Pd, L.in_off, L.in_dat);
+    L.inc_off = c.alloc<int64_t>((int64_t)L.N + 1);
+    L.inc_dat = c.alloc<int32_t>(L.U);
+    transpose_csr(c, E, L.N, L.pin_off, L.pin_dat, L.U, L.inc_off, L.inc_dat);
+}
+
+void derive_out(Ctx &c, const DLevel &L, int64_t *out_off, int32_t *out_dat) {
+    transpose_csr(c, L.E, L.N, L.src_off, L.src_dat, L.Ps, out_off, out_dat);
+}
+
+void feasibility(Ctx &c, const DLevel &L, int64_t omega, int64_t delta, int32_t *bad_size, int32_t *bad_in) {
+    int32_t *bad = c.alloc<int32_t>(2);
+    fill_i32(c, bad, 0x7fffffff, 2);
+    if (L.N > 0) {
+        k_feasible<<<(unsigned)cdiv(L.N, 256), 256, 0, c.stream>>>(L.N, L.size, L.in_off, omega, delta, bad);
+        DHGP_LAUNCHED(c);
+    }
+    int32_t h[2];
+    c.d2h(h, bad, 2);
+    c.sync();
+    c.free(bad);
+    *bad_size = h[0] == 0x7fffffff ? -1 : h[0];
+    *bad_in = h[1] == 0x7fffffff ? -1 : h[1];
+}
+
+}  // namespace dhgp

@@ -1,0 +1,75 @@
+// graph.cuh — device-resident hypergraph levels.
+//
+// HBM layout per level (all CSR offsets int64, ids int32):
+//   src_off/src_dat, dst_off/dst_dat : per h-edge source / destination pins
+//   pin_off/pin_dat                  : per h-edge sorted unique src ∪ dst
+//   in_off/in_dat                    : per node ascending inbound h-edges
+//   inc_off/inc_dat                  : per node ascending incident h-edges
+//   size                             : per node level-0 node count
+// Weights are level-independent (h-edges are never merged, coarsen.py:146).
+#pragma once
+#include "common.cuh"
+
+namespace dhgp {
+
+struct DLevel {
+    int32_t N = 0, E = 0;
+    int64_t Ps = 0, Pd = 0, U = 0, Sin = 0;
+    int64_t *src_off = nullptr, *dst_off = nullptr, *pin_off = nullptr, *in_off = nullptr, *inc_off = nullptr;
+    int32_t *src_dat = nullptr, *dst_dat = nullptr, *pin_dat = nullptr, *in_dat = nullptr, *inc_dat = nullptr;
+    int32_t *size = nullptr;
+    int32_t *gamma = nullptr;  // fine -> coarse map once this level has been contracted
+    bool borrowed = false;     // src/dst/size belong to a resident input (level 0)
+    void release(Ctx &c) {
+        if (!borrowed) {
+            c.free(src_off); c.free(dst_off); c.free(src_dat); c.free(dst_dat); c.free(size);
+        }
+        c.free(pin_off); c.free(in_off); c.free(inc_off);
+        c.free(pin_dat); c.free(in_dat); c.free(inc_dat);
+        c.free(gamma);
+        *this = DLevel();
+    }
+};
+
+struct DWeights {
+    int32_t E = 0;
+    const double *w = nullptr;  // [E] as given (borrowed from the input)
+    int64_t *wi = nullptr;      // [E] integral copy (exact-integer mode)
+    int64_t wsum = 0;
+    bool integral = true;
+    void release(Ctx &c) {
+        c.free(wi);
+        *this = DWeights();
+    }
+};
+
+// Primary hypergraph fields resident in HBM (the inputs of partition()).
+struct DInput {
+    int32_t N = 0, E = 0;
+    int64_t Ps = 0, Pd = 0;
+    int64_t *src_off = nullptr, *dst_off = nullptr;
+    int32_t *src_dat = nullptr, *dst_dat = nullptr;
+    double *w = nullptr;
+    int32_t *size = nullptr;
+    int32_t max_edge_pins = 0;
+    void release(Ctx &c) {
+        c.free(src_off); c.free(dst_off); c.free(src_dat); c.free(dst_dat); c.free(w); c.free(size);
+        *this = DInput();
+    }
+};
+// host -> HBM copy of the primary fields (offsets rebased to 0)
+void upload_input(Ctx &c, const dhgp_graph &g, DInput &in);
+// Validates the weights (finite, >= 0) and derives the exact-integer copy.
+void prepare_weights(Ctx &c, const DInput &in, DWeights &W);
+// Level 0 over a resident input (Hypergraph._from_csr, hgraph.py:212-238).
+void build_level0(Ctx &c, const DInput &in, DLevel &L);
+// Derived families from device-resident src/dst (used at level 0).
+void derive_incidence(Ctx &c, DLevel &L);
+// node_out (only for the incidence API / observer)
+void derive_out(Ctx &c, const DLevel &L, int64_t *out_off, int32_t *out_dat);
+
+// check_feasibility (hgraph.py:376-401): returns first offending node or -1
+// for each of (size > omega, |in| > delta).
+void feasibility(Ctx &c, const DLevel &L, int64_t omega, int64_t delta, int32_t *bad_size, int32_t *bad_in);
+
+}  // namespace dhgp

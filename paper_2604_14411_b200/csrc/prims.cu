@@ -1,0 +1,583 @@
+// prims.cu — scans, radix sort, per-segment sorts, sorted-set merges.
+#include "prims.cuh"
+
+namespace dhgp {
+
+// ===========================================================================
+// exclusive scan (reduce-then-scan; tile = 256 threads x 16 items)
+// ===========================================================================
+namespace {
+constexpr int SC_BT = 256;
+constexpr int SC_IPT = 16;
+constexpr int SC_TILE = SC_BT * SC_IPT;
+
+// block-level exclusive scan of one value per thread; returns the exclusive
+// prefix and writes the block total into *total (all threads).
+__device__ __forceinline__ int64_t block_excl_scan(int64_t v, int64_t *sh, int64_t *total) {
+    const int lane = lane_id(), w = warp_id(), nw = blockDim.x >> 5;
+    int64_t incl = warp_incl_scan(v);
+    if (lane == 31) sh[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+        int64_t x = lane < nw ? sh[lane] : 0;
+        int64_t xi = warp_incl_scan(x);
+        if (lane < nw) sh[lane] = xi - x;
+        if (lane == nw - 1) sh[32] = xi;
+    }
+    __syncthreads();
+    int64_t r = incl - v + sh[w];
+    *total = sh[32];
+    __syncthreads();
+    return r;
+}
+
+template <class T>
+__global__ void k_scan_reduce(const T *in, int64_t n, int64_t *partial) {
+    __shared__ int64_t sh[33];
+    int64_t base = (int64_t)blockIdx.x * SC_TILE;
+    int64_t s = 0;
+#pragma unroll
+    for (int i = 0; i < SC_IPT; i++) {
+        int64_t idx = base + (int64_t)i * SC_BT + threadIdx.x;
+        if (idx < n) s += (int64_t)in[idx];
+    }
+    int64_t t = block_sum<int64_t>(s, sh);
+    if (threadIdx.x == 0) partial[blockIdx.x] = t;
+}
+
+__global__ void k_scan_partials(int64_t *partial, int64_t ntiles) {
+    __shared__ int64_t sh[33];
+    int64_t carry = 0;
+    for (int64_t base = 0; base < ntiles; base += blockDim.x) {
+        int64_t idx = base + threadIdx.x;
+        int64_t v = idx < ntiles ? partial[idx] : 0;
+        int64_t tot;
+        int64_t ex = block_excl_scan(v, sh, &tot);
+        if (idx < ntiles) partial[idx] = carry + ex;
+        carry += tot;
+    }
+    if (threadIdx.x == 0) partial[ntiles] = carry;
+}
+
+template <class T>
+__global__ void k_scan_final(const T *in, int64_t n, const int64_t *partial, int64_t *out) {
+    __shared__ int64_t sh[33];
+    __shared__ int64_t buf[SC_TILE];
+    int64_t base = (int64_t)blockIdx.x * SC_TILE;
+    // striped coalesced load into smem
+#pragma unroll
+    for (int i = 0; i < SC_IPT; i++) {
+        int64_t idx = base + (int64_t)i * SC_BT + threadIdx.x;
+        buf[i * SC_BT + threadIdx.x] = idx < n ? (int64_t)in[idx] : 0;
+    }
+    __syncthreads();
+    int64_t loc[SC_IPT];
+    int64_t s = 0;
+#pragma unroll
+    for (int i = 0; i < SC_IPT; i++) {
+        loc[i] = buf[threadIdx.x * SC_IPT + i];
+        s += loc[i];
+    }
+    int64_t tot;
+    int64_t ex = block_excl_scan(s, sh, &tot);
+    int64_t run = ex + (partial ? partial[blockIdx.x] : 0);
+#pragma unroll
+    for (int i = 0; i < SC_IPT; i++) {
+        buf[threadIdx.x * SC_IPT + i] = run;
+        run += loc[i];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < SC_IPT; i++) {
+        int64_t idx = base + (int64_t)i * SC_BT + threadIdx.x;
+        if (idx < n) out[idx] = buf[i * SC_BT + threadIdx.x];
+    }
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0)
+        out[n] = (partial ? partial[blockIdx.x] : 0) + tot;
+}
+}  // namespace
+
+template <class T>
+void scan_excl(Ctx &c, const T *in, int64_t *out, int64_t n) {
+    if (n <= 0) {
+        c.zero(out, 1);
+        return;
+    }
+    int64_t ntiles = cdiv(n, SC_TILE);
+    if (ntiles == 1) {
+        k_scan_final<T><<<1, SC_BT, 0, c.stream>>>(in, n, nullptr, out);
+        DHGP_LAUNCHED(c);
+        return;
+    }
+    int64_t *partial = c.alloc<int64_t>(ntiles + 1);
+    k_scan_reduce<T><<<(unsigned)ntiles, SC_BT, 0, c.stream>>>(in, n, partial);
+    DHGP_LAUNCHED(c);
+    k_scan_partials<<<1, 1024, 0, c.stream>>>(partial, ntiles);
+    DHGP_LAUNCHED(c);
+    k_scan_final<T><<<(unsigned)ntiles, SC_BT, 0, c.stream>>>(in, n, partial, out);
+    DHGP_LAUNCHED(c);
+    c.free(partial);
+}
+template void scan_excl<int32_t>(Ctx &, const int32_t *, int64_t *, int64_t);
+template void scan_excl<int64_t>(Ctx &, const int64_t *, int64_t *, int64_t);
+template void scan_excl<uint8_t>(Ctx &, const uint8_t *, int64_t *, int64_t);
+
+// ===========================================================================
+// stable LSD radix sort, 8-bit digits, tile = 8 warps x 8 steps x 32 lanes
+// ===========================================================================
+namespace {
+constexpr int RS_BT = 256;
+constexpr int RS_STEPS = 8;
+constexpr int RS_TILE = RS_BT * RS_STEPS;
+
+__global__ void k_rs_up(const uint64_t *kin, int64_t ncap, const int64_t *dn, int shift, int64_t *counts,
+                        int64_t ntiles) {
+    __shared__ uint32_t cnt[256];
+    const int64_t n = dn ? *dn : ncap;
+    cnt[threadIdx.x] = 0;
+    __syncthreads();
+    const int64_t base = (int64_t)blockIdx.x * RS_TILE;
+    if (base < n) {
+#pragma unroll
+        for (int s = 0; s < RS_STEPS; s++) {
+            int64_t idx = base + (int64_t)s * RS_BT + threadIdx.x;
+            if (idx < n) atomicAdd(&cnt[(kin[idx] >> shift) & 255u], 1u);
+        }
+    }
+    __syncthreads();
+    counts[(int64_t)threadIdx.x * ntiles + blockIdx.x] = cnt[threadIdx.x];
+}
+
+__global__ void k_rs_down(const uint64_t *kin, const uint32_t *vin, uint64_t *kout, uint32_t *vout, int64_t ncap,
+                          const int64_t *dn, int shift, const int64_t *offs, int64_t ntiles) {
+    __shared__ uint32_t wcnt[RS_BT / 32][256];
+    const int64_t n = dn ? *dn : ncap;
+    const int64_t base = (int64_t)blockIdx.x * RS_TILE;
+    if (base >= n) return;
+    const int w = warp_id(), lane = lane_id();
+    for (int i = threadIdx.x; i < (RS_BT / 32) * 256; i += RS_BT) (&wcnt[0][0])[i] = 0;
+    __syncthreads();
+    uint64_t k[RS_STEPS];
+    uint32_t v[RS_STEPS];
+    int dig[RS_STEPS];
+    uint32_t rank[RS_STEPS];
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    // warp w owns the contiguous range [base + w*256, base + (w+1)*256)
+#pragma unroll
+    for (int s = 0; s < RS_STEPS; s++) {
+        int64_t idx = base + (int64_t)w * (32 * RS_STEPS) + s * 32 + lane;
+        bool valid = idx < n;
+        k[s] = valid ? kin[idx] : ~0ull;
+        v[s] = valid ? vin[idx] : 0u;
+        dig[s] = valid ? (int)((k[s] >> shift) & 255u) : 256;
+        uint32_t peers = __match_any_sync(FULL_MASK, dig[s]);
+        uint32_t before = valid ? wcnt[w][dig[s]] : 0u;
+        rank[s] = before + __popc(peers & lt_mask);
+        __syncwarp();
+        if (valid && (peers & lt_mask) == 0) wcnt[w][dig[s]] = before + __popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+    {
+        const int d = threadIdx.x;  // RS_BT == 256 digits
+        uint32_t run = 0;
+#pragma unroll
+        for (int ww = 0; ww < RS_BT / 32; ww++) {
+            uint32_t cc = wcnt[ww][d];
+            wcnt[ww][d] = run;
+            run += cc;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int s = 0; s < RS_STEPS; s++) {
+        if (dig[s] < 256) {
+            int64_t pos = offs[(int64_t)dig[s] * ntiles + blockIdx.x] + wcnt[w][dig[s]] + rank[s];
+            kout[pos] = k[s];
+            vout[pos] = v[s];
+        }
+    }
+}
+}  // namespace
+
+void radix_sort_pairs(Ctx &c, uint64_t *keys, uint32_t *vals, uint64_t *ktmp, uint32_t *vtmp, int64_t n_cap,
+                      const int64_t *d_n, int bits) {
+    if (n_cap <= 1 || bits <= 0) return;
+    KScope ks(c, "radix_sort");
+    const int64_t ntiles = cdiv(n_cap, RS_TILE);
+    int64_t *counts = c.alloc<int64_t>(256 * ntiles);
+    int64_t *offs = c.alloc<int64_t>(256 * ntiles + 1);
+    uint64_t *ka = keys, *kb = ktmp;
+    uint32_t *va = vals, *vb = vtmp;
+    const int passes = (bits + 7) / 8;
+    for (int p = 0; p < passes; p++) {
+        const int shift = 8 * p;
+        k_rs_up<<<(unsigned)ntiles, RS_BT, 0, c.stream>>>(ka, n_cap, d_n, shift, counts, ntiles);
+        DHGP_LAUNCHED(c);
+        scan_excl<int64_t>(c, counts, offs, 256 * ntiles);
+        k_rs_down<<<(unsigned)ntiles, RS_BT, 0, c.stream>>>(ka, va, kb, vb, n_cap, d_n, shift, offs, ntiles);
+        DHGP_LAUNCHED(c);
+        std::swap(ka, kb);
+        std::swap(va, vb);
+    }
+    if (ka != keys) {
+        // odd number of passes: result sits in the scratch buffers
+        c.d2d(keys, ka, n_cap);
+        c.d2d(vals, va, n_cap);
+    }
+    c.free(counts);
+    c.free(offs);
+}
+
+// ===========================================================================
+// per-segment sort (three tiers: thread <= 16, warp <= 128, block <= 8192)
+// ===========================================================================
+namespace {
+constexpr int kThreadTier = 16;
+constexpr int kWarpTier = 128;
+
+__global__ void k_seg_sort_thread(int64_t nseg, const int64_t *off, const int32_t *dat, const int32_t *map,
+                                  int32_t *tmp, int32_t *warp_list, int32_t *block_list, int32_t *counts) {
+    int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= nseg) return;
+    int64_t lo = off[s], len = off[s + 1] - lo;
+    if (len > kThreadTier) {
+        if (len <= kWarpTier)
+            warp_list[atomicAdd(&counts[0], 1)] = (int32_t)s;
+        else
+            block_list[atomicAdd(&counts[1], 1)] = (int32_t)s;
+        return;
+    }
+    uint32_t a[kThreadTier];
+#pragma unroll
+    for (int i = 0; i < kThreadTier; i++) {
+        if (i < len) {
+            int32_t x = dat[lo + i];
+            a[i] = (uint32_t)(map ? map[x] : x);
+        }
+    }
+    // insertion sort
+    for (int i = 1; i < len; i++) {
+        uint32_t x = a[i];
+        int j = i - 1;
+        while (j >= 0 && a[j] > x) {
+            a[j + 1] = a[j];
+            j--;
+        }
+        a[j + 1] = x;
+    }
+    for (int i = 0; i < len; i++) tmp[lo + i] = (int32_t)a[i];
+}
+
+template <int K>
+__device__ __forceinline__ void warp_sort_segment(int64_t lo, int len, const int32_t *dat, const int32_t *map,
+                                                  int32_t *tmp) {
+    const int lane = lane_id();
+    uint32_t v[K];
+    bool sorted = true;
+#pragma unroll
+    for (int k = 0; k < K; k++) {
+        int i = k * 32 + lane;
+        if (i < len) {
+            int32_t x = dat[lo + i];
+            v[k] = (uint32_t)(map ? map[x] : x);
+        } else {
+            v[k] = 0xffffffffu;
+        }
+    }
+    // fast path: already strictly ascending (e.g. gamma is monotone on this edge)
+#pragma unroll
+    for (int k = 0; k < K; k++) {
+        const int i = k * 32 + lane;
+        uint32_t up = __shfl_up_sync(FULL_MASK, v[k], 1);
+        uint32_t wrap = __shfl_sync(FULL_MASK, v[k > 0 ? k - 1 : 0], 31);
+        uint32_t prev = lane == 0 ? wrap : up;
+        if (i > 0 && i < len && !(prev < v[k])) sorted = false;
+    }
+    if (!__all_sync(FULL_MASK, sorted)) warp_bitonic_sort<K>(v);
+#pragma unroll
+    for (int k = 0; k < K; k++) {
+        int i = k * 32 + lane;
+        if (i < len) tmp[lo + i] = (int32_t)v[k];
+    }
+}
+
+__global__ void k_seg_sort_warp(const int64_t *off, const int32_t *dat, const int32_t *map, int32_t *tmp,
+                                const int32_t *list, const int32_t *counts) {
+    const int nw = gridDim.x * (blockDim.x >> 5);
+    const int n = counts[0];
+    for (int t = blockIdx.x * (blockDim.x >> 5) + warp_id(); t < n; t += nw) {
+        int64_t s = list[t];
+        int64_t lo = off[s];
+        int len = (int)(off[s + 1] - lo);
+        if (len <= 32)
+            warp_sort_segment<1>(lo, len, dat, map, tmp);
+        else if (len <= 64)
+            warp_sort_segment<2>(lo, len, dat, map, tmp);
+        else
+            warp_sort_segment<4>(lo, len, dat, map, tmp);
+    }
+}
+
+__global__ void k_seg_sort_block(const int64_t *off, const int32_t *dat, const int32_t *map, int32_t *tmp,
+                                 const int32_t *list, const int32_t *counts, int32_t *err) {
+    extern __shared__ uint32_t sbuf[];
+    const int n = counts[1];
+    for (int t = blockIdx.x; t < n; t += gridDim.x) {
+        int64_t s = list[t];
+        int64_t lo = off[s];
+        int len = (int)(off[s + 1] - lo);
+        if (len > kMaxSegSort) {
+            if (threadIdx.x == 0) atomicMax(err, len);
+            continue;
+        }
+        int np = next_pow2(len);
+        __syncthreads();
+        for (int i = threadIdx.x; i < np; i += blockDim.x) {
+            if (i < len) {
+                int32_t x = dat[lo + i];
+                sbuf[i] = (uint32_t)(map ? map[x] : x);
+            } else {
+                sbuf[i] = 0xffffffffu;
+            }
+        }
+        block_bitonic_sort32(sbuf, np);
+        for (int i = threadIdx.x; i < len; i += blockDim.x) tmp[lo + i] = (int32_t)sbuf[i];
+        __syncthreads();
+    }
+}
+}  // namespace
+
+void seg_sort(Ctx &c, int64_t nseg, const int64_t *off, const int32_t *dat, const int32_t *map, int32_t *tmp) {
+    if (nseg <= 0) return;
+    KScope ks(c, "seg_sort");
+    int32_t *wl = c.alloc<int32_t>(nseg);
+    int32_t *bl = c.alloc<int32_t>(nseg);
+    int32_t *cnt = c.alloc<int32_t>(3);
+    c.zero(cnt, 3);
+    k_seg_sort_thread<<<(unsigned)cdiv(nseg, 256), 256, 0, c.stream>>>(nseg, off, dat, map, tmp, wl, bl, cnt);
+    DHGP_LAUNCHED(c);
+    k_seg_sort_warp<<<(unsigned)(c.num_sms * 8), 256, 0, c.stream>>>(off, dat, map, tmp, wl, cnt);
+    DHGP_LAUNCHED(c);
+    // segment lengths are bounded by kMaxSegSort at upload (max h-edge degree
+    // only shrinks under contraction), so the block tier never overflows
+    k_seg_sort_block<<<(unsigned)(c.num_sms), 1024, kMaxSegSort * sizeof(uint32_t), c.stream>>>(off, dat, map, tmp,
+                                                                                                 bl, cnt, cnt + 2);
+    DHGP_LAUNCHED(c);
+    c.free(wl);
+    c.free(bl);
+    c.free(cnt);
+}
+
+namespace {
+__global__ void k_seg_unique_count(int64_t nseg, const int64_t *off, const int32_t *tmp, int64_t *cnt) {
+    int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= nseg) return;
+    int64_t lo = off[s], hi = off[s + 1];
+    int64_t k = 0;
+    int32_t prev = 0;
+    for (int64_t p = lo; p < hi; p++) {
+        int32_t x = tmp[p];
+        if (p == lo || x != prev) k++;
+        prev = x;
+    }
+    cnt[s] = k;
+}
+__global__ void k_seg_unique_write(int64_t nseg, const int64_t *off, const int32_t *tmp, const int64_t *out_off,
+                                   int32_t *out) {
+    int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= nseg) return;
+    int64_t lo = off[s], hi = off[s + 1];
+    int64_t w = out_off[s];
+    int32_t prev = 0;
+    for (int64_t p = lo; p < hi; p++) {
+        int32_t x = tmp[p];
+        if (p == lo || x != prev) out[w++] = x;
+        prev = x;
+    }
+}
+}  // namespace
+
+void seg_unique_count(Ctx &c, int64_t nseg, const int64_t *off, const int32_t *tmp, int64_t *cnt) {
+    if (nseg <= 0) return;
+    k_seg_unique_count<<<(unsigned)cdiv(nseg, 256), 256, 0, c.stream>>>(nseg, off, tmp, cnt);
+    DHGP_LAUNCHED(c);
+}
+void seg_unique_write(Ctx &c, int64_t nseg, const int64_t *off, const int32_t *tmp, const int64_t *out_off,
+                      int32_t *out) {
+    if (nseg <= 0) return;
+    k_seg_unique_write<<<(unsigned)cdiv(nseg, 256), 256, 0, c.stream>>>(nseg, off, tmp, out_off, out);
+    DHGP_LAUNCHED(c);
+}
+
+// ===========================================================================
+// sorted-set union of member lists (warp per coarse node)
+// ===========================================================================
+namespace {
+__global__ void k_merge_count(int64_t nc, const int32_t *ma, const int32_t *mb, const int64_t *off,
+                              const int32_t *dat, int64_t *cnt) {
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const int lane = lane_id();
+    for (int64_t cn = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id(); cn < nc; cn += nw) {
+        int32_t a = ma[cn], b = mb[cn];
+        int64_t alo = off[a], na = off[a + 1] - alo;
+        if (b < 0) {
+            if (lane == 0) cnt[cn] = na;
+            continue;
+        }
+        int64_t blo = off[b], nb = off[b + 1] - blo;
+        // common elements: search the shorter list in the longer
+        const int32_t *sp = dat + (na <= nb ? alo : blo);
+        const int32_t *lp = dat + (na <= nb ? blo : alo);
+        int64_t ns = na <= nb ? na : nb, nl = na <= nb ? nb : na;
+        int64_t common = 0;
+        for (int64_t i = lane; i < ns; i += 32) common += bsearch_dev(lp, 0, nl, sp[i]) >= 0;
+        common = warp_sum(common);
+        if (lane == 0) cnt[cn] = na + nb - common;
+    }
+}
+
+__global__ void k_merge_write(int64_t nc, const int32_t *ma, const int32_t *mb, const int64_t *off,
+                              const int32_t *dat, const int64_t *out_off, int32_t *out) {
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const int lane = lane_id();
+    const uint32_t lt = (1u << lane) - 1u;
+    for (int64_t cn = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id(); cn < nc; cn += nw) {
+        int32_t a = ma[cn], b = mb[cn];
+        int64_t alo = off[a], na = off[a + 1] - alo;
+        int32_t *o = out + out_off[cn];
+        const int32_t *A = dat + alo;
+        if (b < 0) {
+            for (int64_t i = lane; i < na; i += 32) o[i] = A[i];
+            continue;
+        }
+        int64_t blo = off[b], nb = off[b + 1] - blo;
+        const int32_t *B = dat + blo;
+        // x = A[i]: pos = i + lb_B(x) - #{A[k], k < i : A[k] in B}
+        int64_t run = 0;
+        for (int64_t base = 0; base < na; base += 32) {
+            int64_t i = base + lane;
+            int64_t lb = 0;
+            bool in_other = false;
+            int32_t x = 0;
+            if (i < na) {
+                x = A[i];
+                lb = lower_bound_dev<int32_t>(B, 0, nb, x);
+                in_other = lb < nb && B[lb] == x;
+            }
+            uint32_t bal = __ballot_sync(FULL_MASK, in_other);
+            if (i < na) o[i + lb - (run + __popc(bal & lt))] = x;
+            run += __popc(bal);
+        }
+        // y = B[j] not in A: pos = lb_A(y) + j - #{B[k], k < j : B[k] in A}
+        run = 0;
+        for (int64_t base = 0; base < nb; base += 32) {
+            int64_t j = base + lane;
+            int64_t lb = 0;
+            bool in_other = false;
+            int32_t y = 0;
+            if (j < nb) {
+                y = B[j];
+                lb = lower_bound_dev<int32_t>(A, 0, na, y);
+                in_other = lb < na && A[lb] == y;
+            }
+            uint32_t bal = __ballot_sync(FULL_MASK, in_other);
+            if (j < nb && !in_other) o[lb + j - (run + __popc(bal & lt))] = y;
+            run += __popc(bal);
+        }
+    }
+}
+}  // namespace
+
+void merge_union_count(Ctx &c, int64_t nc, const int32_t *ma, const int32_t *mb, const int64_t *off,
+                       const int32_t *dat, int64_t *cnt) {
+    if (nc <= 0) return;
+    int64_t blocks = std::min<int64_t>(cdiv(nc, 8), (int64_t)c.num_sms * 16);
+    k_merge_count<<<(unsigned)blocks, 256, 0, c.stream>>>(nc, ma, mb, off, dat, cnt);
+    DHGP_LAUNCHED(c);
+}
+void merge_union_write(Ctx &c, int64_t nc, const int32_t *ma, const int32_t *mb, const int64_t *off,
+                       const int32_t *dat, const int64_t *out_off, int32_t *out) {
+    if (nc <= 0) return;
+    int64_t blocks = std::min<int64_t>(cdiv(nc, 8), (int64_t)c.num_sms * 16);
+    k_merge_write<<<(unsigned)blocks, 256, 0, c.stream>>>(nc, ma, mb, off, dat, out_off, out);
+    DHGP_LAUNCHED(c);
+}
+
+// ===========================================================================
+// fills and the stable transpose
+// ===========================================================================
+namespace {
+__global__ void k_iota(int32_t *p, int64_t n) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = (int32_t)i;
+}
+__global__ void k_fill32(int32_t *p, int32_t v, int64_t n) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+__global__ void k_fill64(int64_t *p, int64_t v, int64_t n) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+// per pin: key = node id, val = edge id (pins enumerated in edge order)
+__global__ void k_expand_pairs(int64_t nseg, const int64_t *off, const int32_t *dat, uint64_t *keys,
+                               uint32_t *vals, int32_t *node_count) {
+    int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= nseg) return;
+    int64_t lo = off[e] - off[0], hi = off[e + 1] - off[0];
+    for (int64_t p = lo; p < hi; p++) {
+        int32_t n = dat[p];
+        keys[p] = (uint64_t)(uint32_t)n;
+        vals[p] = (uint32_t)e;
+        atomicAdd(&node_count[n], 1);
+    }
+}
+__global__ void k_u32_to_i32(const uint32_t *a, int32_t *b, int64_t n) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) b[i] = (int32_t)a[i];
+}
+}  // namespace
+
+void iota_i32(Ctx &c, int32_t *p, int64_t n) {
+    if (n <= 0) return;
+    k_iota<<<(unsigned)cdiv(n, 256), 256, 0, c.stream>>>(p, n);
+    DHGP_LAUNCHED(c);
+}
+void fill_i32(Ctx &c, int32_t *p, int32_t v, int64_t n) {
+    if (n <= 0) return;
+    k_fill32<<<(unsigned)cdiv(n, 256), 256, 0, c.stream>>>(p, v, n);
+    DHGP_LAUNCHED(c);
+}
+void fill_i64(Ctx &c, int64_t *p, int64_t v, int64_t n) {
+    if (n <= 0) return;
+    k_fill64<<<(unsigned)cdiv(n, 256), 256, 0, c.stream>>>(p, v, n);
+    DHGP_LAUNCHED(c);
+}
+
+void transpose_csr(Ctx &c, int64_t nseg, int32_t N, const int64_t *off, const int32_t *dat, int64_t nnz,
+                   int64_t *out_off, int32_t *out_dat) {
+    KScope ks(c, "transpose");
+    int32_t *cnt = c.alloc<int32_t>(N > 0 ? N : 1);
+    c.zero(cnt, N);
+    if (nnz == 0) {
+        scan_excl<int32_t>(c, cnt, out_off, N);
+        c.free(cnt);
+        return;
+    }
+    uint64_t *k = c.alloc<uint64_t>(nnz), *kt = c.alloc<uint64_t>(nnz);
+    uint32_t *v = c.alloc<uint32_t>(nnz), *vt = c.alloc<uint32_t>(nnz);
+    k_expand_pairs<<<(unsigned)cdiv(nseg, 256), 256, 0, c.stream>>>(nseg, off, dat, k, v, cnt);
+    DHGP_LAUNCHED(c);
+    radix_sort_pairs(c, k, v, kt, vt, nnz, nullptr, bitlen((uint64_t)(N > 0 ? N - 1 : 0)));
+    k_u32_to_i32<<<(unsigned)cdiv(nnz, 256), 256, 0, c.stream>>>(v, out_dat, nnz);
+    DHGP_LAUNCHED(c);
+    scan_excl<int32_t>(c, cnt, out_off, N);
+    c.free(cnt);
+    c.free(k);
+    c.free(kt);
+    c.free(v);
+    c.free(vt);
+}
+
+}  // namespace dhgp

@@ -1,0 +1,46 @@
+// prims.cuh — hand-written sm_100a building blocks: scans, a stable LSD radix
+// sort, tiered per-segment sorts and sorted-set merges.  All integer, all
+// deterministic.
+#pragma once
+#include "common.cuh"
+
+namespace dhgp {
+
+// out[0..n]: exclusive prefix sums of in[0..n-1]; out[n] = total.
+template <class T>
+void scan_excl(Ctx &c, const T *in, int64_t *out, int64_t n);
+
+// Stable LSD radix sort of (key, val) pairs on key bits [0, bits).
+// n = *d_n when d_n != nullptr (device-resident count, <= n_cap), else n_cap.
+// Sorted output ends in (keys, vals); (ktmp, vtmp) are scratch of n_cap.
+void radix_sort_pairs(Ctx &c, uint64_t *keys, uint32_t *vals, uint64_t *ktmp, uint32_t *vtmp, int64_t n_cap,
+                      const int64_t *d_n, int bits);
+
+// Per-segment ascending sort of (map ? map[dat[i]] : dat[i]) into tmp (same
+// layout as dat).  Segments longer than kMaxSegSort raise DHGP_ERR_UNSUPPORTED.
+constexpr int64_t kMaxSegSort = 8192;
+void seg_sort(Ctx &c, int64_t nseg, const int64_t *off, const int32_t *dat, const int32_t *map, int32_t *tmp);
+
+// cnt[s] = number of distinct values in sorted segment s of tmp.
+void seg_unique_count(Ctx &c, int64_t nseg, const int64_t *off, const int32_t *tmp, int64_t *cnt);
+// out[out_off[s]..] = distinct values of sorted segment s.
+void seg_unique_write(Ctx &c, int64_t nseg, const int64_t *off, const int32_t *tmp, const int64_t *out_off,
+                      int32_t *out);
+
+// Sorted-set union of two member lists per coarse node.
+void merge_union_count(Ctx &c, int64_t nc, const int32_t *ma, const int32_t *mb, const int64_t *off,
+                       const int32_t *dat, int64_t *cnt);
+void merge_union_write(Ctx &c, int64_t nc, const int32_t *ma, const int32_t *mb, const int64_t *off,
+                       const int32_t *dat, const int64_t *out_off, int32_t *out);
+
+// Simple fills.
+void iota_i32(Ctx &c, int32_t *p, int64_t n);
+void fill_i32(Ctx &c, int32_t *p, int32_t v, int64_t n);
+void fill_i64(Ctx &c, int64_t *p, int64_t v, int64_t n);
+
+// Transpose edge -> node lists into node -> ascending edge lists (stable).
+// out_off[N+1], out_dat[nnz].
+void transpose_csr(Ctx &c, int64_t nseg, int32_t N, const int64_t *off, const int32_t *dat, int64_t nnz,
+                   int64_t *out_off, int32_t *out_dat);
+
+}  // namespace dhgp

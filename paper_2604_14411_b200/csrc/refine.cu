@@ -1,0 +1,917 @@
+// refine.cu — refinement rounds, exact-integer mode.
+//
+// The reference's dense (E x K) pins / pins_in matrices (_kernels.pyx:216-231)
+// become per-h-edge run lists: for h-edge e, the distinct parts of its pins in
+// ascending order with their pin count and destination-pin count, stored at
+// e's own pin offsets (lambda(e) <= |pins(e)| entries).  Every value the
+// algorithm reads from pins[e, p] / pins_in[e, p] is a binary search in that
+// list (absent = 0), so the results are identical.
+#include "prims.cuh"
+#include "refine.cuh"
+
+namespace dhgp {
+
+namespace {
+
+struct Runs {
+    int32_t *part = nullptr;  // [U] distinct parts per h-edge (ascending)
+    int32_t *cnt = nullptr;   // [U] pins of the h-edge in that part
+    int32_t *cin = nullptr;   // [U] destination pins of the h-edge in that part
+    int32_t *len = nullptr;   // [E] lambda(e)
+};
+
+__device__ __forceinline__ int32_t run_find(const Runs &r, int64_t lo, int32_t len, int32_t p) {
+    int64_t k = lower_bound_dev<int32_t>(r.part, lo, lo + len, p);
+    return (k < lo + len && r.part[k] == p) ? (int32_t)(k - lo) : -1;
+}
+
+// per h-edge: run lists from the per-edge sorted parts, connectivity
+// contribution w(e)(lambda-1) (_kernels.pyx:184-213) and distinct-inbound
+// counts (hgraph.py:324-339)
+__global__ void k_edge_runs(int32_t E, const int64_t *pin_off, const int32_t *sorted_parts, const int64_t *dst_off,
+                            const int32_t *dst_dat, const int32_t *assign, const int64_t *wi, Runs r,
+                            unsigned long long *conn, int64_t *pinbound) {
+    __shared__ int64_t sh[33];
+    int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int64_t contrib = 0;
+    if (e < E) {
+        const int64_t lo = pin_off[e], hi = pin_off[e + 1];
+        int32_t lam = 0;
+        for (int64_t j = lo; j < hi;) {
+            int32_t p = sorted_parts[j];
+            int64_t j2 = j + 1;
+            while (j2 < hi && sorted_parts[j2] == p) j2++;
+            r.part[lo + lam] = p;
+            r.cnt[lo + lam] = (int32_t)(j2 - j);
+            r.cin[lo + lam] = 0;
+            lam++;
+            j = j2;
+        }
+        r.len[e] = lam;
+        for (int64_t q = dst_off[e]; q < dst_off[e + 1]; q++) {
+            int32_t k = run_find(r, lo, lam, assign[dst_dat[q]]);
+            r.cin[lo + k]++;
+        }
+        if (pinbound)
+            for (int32_t k = 0; k < lam; k++)
+                if (r.cin[lo + k] > 0) atomicAdd((unsigned long long *)&pinbound[r.part[lo + k]], 1ull);
+        if (lam > 0) contrib = wi[e] * (int64_t)(lam - 1);
+    }
+    int64_t t = block_sum<int64_t>(contrib, sh);
+    if (threadIdx.x == 0 && t) atomicAdd(conn, (unsigned long long)t);
+}
+
+__global__ void k_part_sizes(int32_t N, const int32_t *assign, const int32_t *size, int64_t *psizes) {
+    int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (n < N) atomicAdd((unsigned long long *)&psizes[assign[n]], (unsigned long long)(int64_t)size[n]);
+}
+
+// ---------------------------------------------------------------------------
+// A14 propose: one best strictly-improving target per node
+// (_kernels.pyx:262-310).  Warp per node, parts -> present weight in a
+// shared-memory hash table; nodes touching too many parts go to a block tier
+// with a dense per-block array over all parts.
+// ---------------------------------------------------------------------------
+struct ProposeArgs {
+    int32_t N, K;
+    const int64_t *inc_off;
+    const int32_t *inc_dat;
+    const int64_t *pin_off;
+    const int64_t *wi;
+    Runs r;
+    const int32_t *assign;
+    const int64_t *psizes;
+    const int32_t *size;
+    int64_t omega;
+    int32_t *target;
+    int64_t *gain;
+    int32_t *next;
+    int32_t *big_list;
+    int32_t *big_count;
+};
+
+constexpr int PR_WARPS = 8;
+constexpr int PR_CAP = 512;
+constexpr int PR_LIMIT = 400;
+constexpr int PR_SMEM = PR_WARPS * PR_CAP * (4 + 8);
+
+__device__ __forceinline__ uint32_t pslot(int32_t p) { return ((uint32_t)p * 2654435761u) >> (32 - 9); }
+
+__device__ __forceinline__ bool better_gain(int64_t g, int32_t p, int64_t bg, int32_t bp) {
+    // max gain, ties to the smaller part id (_kernels.pyx:305)
+    return bp < 0 || g > bg || (g == bg && p < bp);
+}
+
+__global__ void __launch_bounds__(PR_WARPS * 32) k_propose_warp(ProposeArgs a) {
+    extern __shared__ unsigned char smem[];
+    unsigned long long *svals = (unsigned long long *)smem;
+    int32_t *skeys = (int32_t *)(svals + PR_WARPS * PR_CAP);
+    __shared__ int32_t snk[PR_WARPS];
+    __shared__ volatile int32_t sover[PR_WARPS];
+    const int w = warp_id(), lane = lane_id();
+    int32_t *keys = skeys + w * PR_CAP;
+    unsigned long long *vals = svals + w * PR_CAP;
+    while (true) {
+        int node = 0;
+        if (lane == 0) node = atomicAdd(a.next, 1);
+        node = __shfl_sync(FULL_MASK, node, 0);
+        if (node >= a.N) break;
+        const int64_t ilo = a.inc_off[node], ihi = a.inc_off[node + 1];
+        if (ihi == ilo || a.K < 2) {
+            if (lane == 0) a.target[node] = -1;
+            continue;
+        }
+        for (int s = lane; s < PR_CAP; s += 32) {
+            keys[s] = -1;
+            vals[s] = 0ull;
+        }
+        if (lane == 0) {
+            snk[w] = 0;
+            sover[w] = 0;
+        }
+        __syncwarp();
+        const int32_t ps = a.assign[node];
+        int64_t total = 0, saving = 0;
+        for (int64_t ii = ilo + lane; ii < ihi; ii += 32) {
+            const int32_t e = a.inc_dat[ii];
+            const int64_t we = a.wi[e];
+            const int64_t lo = a.pin_off[e];
+            const int32_t lam = a.r.len[e];
+            total += we;
+            for (int32_t j = 0; j < lam; j++) {
+                const int32_t p = a.r.part[lo + j];
+                if (p == ps && a.r.cnt[lo + j] == 1) saving += we;
+                if (sover[w]) continue;
+                uint32_t h = pslot(p);
+                bool done = false;
+                for (int probe = 0; probe < PR_CAP && !done; probe++) {
+                    const int slot = (h + probe) & (PR_CAP - 1);
+                    int k = keys[slot];
+                    if (k == -1) {
+                        int prev = atomicCAS(&keys[slot], -1, p);
+                        if (prev == -1) {
+                            if (atomicAdd(&snk[w], 1) >= PR_LIMIT) sover[w] = 1;
+                            k = p;
+                        } else {
+                            k = prev;
+                        }
+                    }
+                    if (k == p) {
+                        atomicAdd(&vals[slot], (unsigned long long)we);
+                        done = true;
+                    }
+                }
+                if (!done) sover[w] = 1;
+            }
+        }
+        total = warp_sum(total);
+        saving = warp_sum(saving);
+        __syncwarp();
+        if (sover[w]) {
+            if (lane == 0) a.big_list[atomicAdd(a.big_count, 1)] = node;
+            __syncwarp();
+            continue;
+        }
+        const int64_t sz = a.size[node];
+        int64_t bg = 0;
+        int32_t bp = -1;
+        for (int s = lane; s < PR_CAP; s += 32) {
+            const int32_t p = keys[s];
+            if (p < 0 || p == ps || a.psizes[p] + sz > a.omega) continue;
+            const int64_t g = saving - (total - (int64_t)vals[s]);
+            if (better_gain(g, p, bg, bp)) {
+                bg = g;
+                bp = p;
+            }
+        }
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) {
+            int64_t og = __shfl_xor_sync(FULL_MASK, bg, d);
+            int32_t op = __shfl_xor_sync(FULL_MASK, bp, d);
+            if (op >= 0 && better_gain(og, op, bg, bp)) {
+                bg = og;
+                bp = op;
+            }
+        }
+        if (lane == 0) {
+            const bool emit = bp >= 0 && bg > 0;
+            a.target[node] = emit ? bp : -1;
+            a.gain[node] = emit ? bg : 0;
+        }
+        __syncwarp();
+    }
+}
+
+constexpr int PB_THREADS = 512;
+__global__ void __launch_bounds__(PB_THREADS) k_propose_block(ProposeArgs a, long long *dense_all,
+                                                               int32_t *touched_all) {
+    __shared__ int32_t s_nt;
+    __shared__ long long s_red[PB_THREADS / 32][2];
+    __shared__ int32_t s_p[PB_THREADS / 32];
+    long long *dense = dense_all + (int64_t)blockIdx.x * a.K;
+    int32_t *touched = touched_all + (int64_t)blockIdx.x * a.K;
+    const int w = warp_id(), lane = lane_id(), nw = PB_THREADS / 32;
+    const int nbig = *a.big_count;
+    for (int t = blockIdx.x; t < nbig; t += gridDim.x) {
+        const int32_t node = a.big_list[t];
+        if (threadIdx.x == 0) s_nt = 0;
+        __syncthreads();
+        const int64_t ilo = a.inc_off[node], ihi = a.inc_off[node + 1];
+        const int32_t ps = a.assign[node];
+        long long total = 0, saving = 0;
+        for (int64_t ii = ilo + threadIdx.x; ii < ihi; ii += PB_THREADS) {
+            const int32_t e = a.inc_dat[ii];
+            const int64_t we = a.wi[e];
+            const int64_t lo = a.pin_off[e];
+            const int32_t lam = a.r.len[e];
+            total += we;
+            for (int32_t j = 0; j < lam; j++) {
+                const int32_t p = a.r.part[lo + j];
+                if (p == ps && a.r.cnt[lo + j] == 1) saving += we;
+                long long old = atomicCAS((unsigned long long *)&dense[p], ~0ull, 0ull);
+                if (old == -1ll) touched[atomicAdd(&s_nt, 1)] = p;
+                atomicAdd((unsigned long long *)&dense[p], (unsigned long long)we);
+            }
+        }
+        total = warp_sum(total);
+        saving = warp_sum(saving);
+        if (lane == 0) {
+            s_red[w][0] = total;
+            s_red[w][1] = saving;
+        }
+        __syncthreads();
+        total = 0;
+        saving = 0;
+        for (int j = 0; j < nw; j++) {
+            total += s_red[j][0];
+            saving += s_red[j][1];
+        }
+        const int nt = s_nt;
+        const int64_t sz = a.size[node];
+        long long bg = 0;
+        int32_t bp = -1;
+        for (int i = threadIdx.x; i < nt; i += PB_THREADS) {
+            const int32_t p = touched[i];
+            const long long pres = dense[p];
+            dense[p] = -1ll;
+            if (p == ps || a.psizes[p] + sz > a.omega) continue;
+            const long long g = saving - (total - pres);
+            if (better_gain(g, p, bg, bp)) {
+                bg = g;
+                bp = p;
+            }
+        }
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) {
+            long long og = __shfl_xor_sync(FULL_MASK, bg, d);
+            int32_t op = __shfl_xor_sync(FULL_MASK, bp, d);
+            if (op >= 0 && better_gain(og, op, bg, bp)) {
+                bg = og;
+                bp = op;
+            }
+        }
+        __syncthreads();
+        if (lane == 0) {
+            s_red[w][0] = bg;
+            s_p[w] = bp;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            long long g = s_red[0][0];
+            int32_t p = s_p[0];
+            for (int j = 1; j < nw; j++)
+                if (s_p[j] >= 0 && better_gain(s_red[j][0], s_p[j], g, p)) {
+                    g = s_red[j][0];
+                    p = s_p[j];
+                }
+            const bool emit = p >= 0 && g > 0;
+            a.target[node] = emit ? p : -1;
+            a.gain[node] = emit ? g : 0;
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void k_fill_ll(long long *p, long long v, int64_t n) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+
+__global__ void k_mover_flags(int32_t N, const int32_t *target, uint8_t *flags) {
+    int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (n < N) flags[n] = target[n] >= 0;
+}
+
+// sequence key: gain descending (stable sort keeps node ascending among ties,
+// refine.py:108-110)
+__global__ void k_mover_keys(int32_t N, const uint8_t *flags, const int64_t *pos, const int64_t *gain, int64_t gmax,
+                             uint64_t *keys, uint32_t *vals) {
+    int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (n < N && flags[n]) {
+        keys[pos[n]] = (uint64_t)(gmax - gain[n]);
+        vals[pos[n]] = (uint32_t)n;
+    }
+}
+
+__global__ void k_build_moves(int32_t M, const uint32_t *sorted_nodes, const int32_t *assign, const int32_t *target,
+                              const int64_t *gain, int32_t *node, int32_t *from, int32_t *to, int64_t *giso,
+                              int32_t *pos) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= M) return;
+    int32_t n = (int32_t)sorted_nodes[i];
+    node[i] = n;
+    from[i] = assign[n];
+    to[i] = target[n];
+    giso[i] = gain[n];
+    pos[n] = (int32_t)i;
+}
+
+// A15: gains corrected for earlier moves, rules (a)-(d) (_kernels.pyx:326-363)
+__global__ void k_seq_gains(int32_t M, const int64_t *inc_off, const int32_t *inc_dat, const int64_t *pin_off,
+                            const int32_t *pin_dat, const int64_t *wi, Runs r, const int32_t *node,
+                            const int32_t *from, const int32_t *to, const int64_t *giso, const int32_t *pos,
+                            int64_t *gseq) {
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const int lane = lane_id();
+    for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id(); i < M; i += nw) {
+        const int32_t n = node[i], ps = from[i], pd = to[i];
+        int64_t acc = 0;
+        for (int64_t ii = inc_off[n] + lane; ii < inc_off[n + 1]; ii += 32) {
+            const int32_t e = inc_dat[ii];
+            const int64_t lo = pin_off[e];
+            const int32_t lam = r.len[e];
+            int32_t k;
+            k = run_find(r, lo, lam, ps);
+            const int32_t base_ps = k >= 0 ? r.cnt[lo + k] : 0;
+            k = run_find(r, lo, lam, pd);
+            const int32_t base_pd = k >= 0 ? r.cnt[lo + k] : 0;
+            int32_t leav_pd = 0, ent_pd = 0, leav_ps = 0, ent_ps = 0;
+            for (int64_t pp = lo; pp < pin_off[e + 1]; pp++) {
+                const int32_t j = pos[pin_dat[pp]];
+                if (j < 0 || j >= i) continue;
+                leav_pd += from[j] == pd;
+                ent_pd += to[j] == pd;
+                leav_ps += from[j] == ps;
+                ent_ps += to[j] == ps;
+            }
+            const int64_t we = wi[e];
+            int64_t net = 0;
+            if (base_pd > 0) {
+                if (leav_pd - ent_pd == base_pd) net -= we;
+            } else if (ent_pd > 0) {
+                net += we;
+            }
+            if (base_ps == 1) {
+                if (ent_ps > 0) net -= we;
+            } else if (base_ps - 1 > 0 && leav_ps - ent_ps == base_ps - 1) {
+                net += we;
+            }
+            acc += net;
+        }
+        acc = warp_sum(acc);
+        if (lane == 0) gseq[i] = giso[i] + acc;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// A17 events.  Key = track | part | move index; track 0 = size, 1 = inbound.
+// ---------------------------------------------------------------------------
+struct EvArgs {
+    int ibits, pbits;
+    uint64_t *key;
+    uint32_t *val;
+    unsigned long long *count;
+};
+__device__ __forceinline__ void emit(const EvArgs &ev, uint64_t track, int32_t p, int32_t i, int32_t d) {
+    unsigned long long s = atomicAdd(ev.count, 1ull);
+    ev.key[s] = (track << (ev.pbits + ev.ibits)) | ((uint64_t)(uint32_t)p << ev.ibits) | (uint64_t)(uint32_t)i;
+    ev.val[s] = (uint32_t)d;
+}
+
+// size track (refine.py:203-208): (from_i, i, -size), (to_i, i, +size)
+__global__ void k_size_events(int32_t M, const int32_t *node, const int32_t *from, const int32_t *to,
+                              const int32_t *size, EvArgs ev) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= M) return;
+    const int32_t s = size[node[i]];
+    const uint64_t sh = (uint64_t)(ev.pbits + ev.ibits);
+    ev.key[2 * i] = ((uint64_t)(uint32_t)from[i] << ev.ibits) | (uint64_t)i;
+    ev.val[2 * i] = (uint32_t)(-s);
+    ev.key[2 * i + 1] = ((uint64_t)(uint32_t)to[i] << ev.ibits) | (uint64_t)i;
+    ev.val[2 * i + 1] = (uint32_t)s;
+    (void)sh;
+}
+
+// inbound track (refine.py:210-237), per h-edge: the movers among its
+// destination pins in sequence order; per part a running destination-pin
+// count from pins_in[e, p]; crossings 0->1 / 1->0 emit distinct events.
+constexpr int kEvLocal = 32;
+__global__ void k_inbound_events(int32_t E, const int64_t *dst_off, const int32_t *dst_dat, const int64_t *pin_off,
+                                 Runs r, const int32_t *pos, const int32_t *from, const int32_t *to, EvArgs ev,
+                                 int32_t *big_list, int32_t *big_count) {
+    int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= E) return;
+    int32_t mv[kEvLocal];
+    int nm = 0;
+    for (int64_t q = dst_off[e]; q < dst_off[e + 1]; q++) {
+        int32_t j = pos[dst_dat[q]];
+        if (j < 0) continue;
+        if (nm == kEvLocal) {
+            big_list[atomicAdd(big_count, 1)] = (int32_t)e;
+            return;
+        }
+        mv[nm++] = j;
+    }
+    if (nm == 0) return;
+    for (int a = 1; a < nm; a++) {
+        int32_t x = mv[a];
+        int b = a - 1;
+        while (b >= 0 && mv[b] > x) {
+            mv[b + 1] = mv[b];
+            b--;
+        }
+        mv[b + 1] = x;
+    }
+    int32_t dp[2 * kEvLocal], dc[2 * kEvLocal];
+    int nd = 0;
+    const int64_t lo = pin_off[e];
+    const int32_t lam = r.len[e];
+    for (int a = 0; a < nm; a++) {
+        const int32_t i = mv[a];
+        const int32_t pf = from[i], pt = to[i];
+        int k;
+        for (k = 0; k < nd && dp[k] != pf; k++) {
+        }
+        if (k == nd) {
+            int32_t f = run_find(r, lo, lam, pf);
+            dp[nd] = pf;
+            dc[nd] = f >= 0 ? r.cin[lo + f] : 0;
+            nd++;
+        }
+        if (--dc[k] == 0) emit(ev, 1, pf, i, -1);
+        for (k = 0; k < nd && dp[k] != pt; k++) {
+        }
+        if (k == nd) {
+            int32_t f = run_find(r, lo, lam, pt);
+            dp[nd] = pt;
+            dc[nd] = f >= 0 ? r.cin[lo + f] : 0;
+            nd++;
+        }
+        if (++dc[k] == 1) emit(ev, 1, pt, i, +1);
+    }
+}
+
+// the same walk for h-edges with many movers: block collects and sorts, one
+// thread walks with a shared-memory part dictionary
+constexpr int kEvBlockMax = 2048;
+__global__ void k_inbound_events_block(const int64_t *dst_off, const int32_t *dst_dat, const int64_t *pin_off, Runs r,
+                                       const int32_t *pos, const int32_t *from, const int32_t *to, EvArgs ev,
+                                       const int32_t *big_list, const int32_t *big_count, int32_t *err) {
+    __shared__ uint32_t smv[kEvBlockMax];
+    __shared__ int32_t sdp[2 * kEvBlockMax];
+    __shared__ int32_t sdc[2 * kEvBlockMax];
+    __shared__ int32_t snm;
+    const int nbig = *big_count;
+    for (int t = blockIdx.x; t < nbig; t += gridDim.x) {
+        const int32_t e = big_list[t];
+        if (threadIdx.x == 0) snm = 0;
+        __syncthreads();
+        for (int64_t q = dst_off[e] + threadIdx.x; q < dst_off[e + 1]; q += blockDim.x) {
+            int32_t j = pos[dst_dat[q]];
+            if (j >= 0) {
+                int s = atomicAdd(&snm, 1);
+                if (s < kEvBlockMax) smv[s] = (uint32_t)j;
+            }
+        }
+        __syncthreads();
+        const int nm = snm;
+        if (nm > kEvBlockMax) {
+            if (threadIdx.x == 0) atomicMax(err, nm);
+            __syncthreads();
+            continue;
+        }
+        const int np = next_pow2(nm);
+        for (int s = nm + threadIdx.x; s < np; s += blockDim.x) smv[s] = 0xffffffffu;
+        block_bitonic_sort32(smv, np);
+        if (threadIdx.x == 0) {
+            const int64_t lo = pin_off[e];
+            const int32_t lam = r.len[e];
+            int nd = 0;
+            for (int a = 0; a < nm; a++) {
+                const int32_t i = (int32_t)smv[a];
+                const int32_t pf = from[i], pt = to[i];
+                int k;
+                for (k = 0; k < nd && sdp[k] != pf; k++) {
+                }
+                if (k == nd) {
+                    int32_t f = run_find(r, lo, lam, pf);
+                    sdp[nd] = pf;
+                    sdc[nd] = f >= 0 ? r.cin[lo + f] : 0;
+                    nd++;
+                }
+                if (--sdc[k] == 0) emit(ev, 1, pf, i, -1);
+                for (k = 0; k < nd && sdp[k] != pt; k++) {
+                }
+                if (k == nd) {
+                    int32_t f = run_find(r, lo, lam, pt);
+                    sdp[nd] = pt;
+                    sdc[nd] = f >= 0 ? r.cin[lo + f] : 0;
+                    nd++;
+                }
+                if (++sdc[k] == 1) emit(ev, 1, pt, i, +1);
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// segment heads over sorted events: segment = (track, part)
+__global__ void k_ev_heads(int64_t T, const uint64_t *key, int ibits, uint8_t *flag) {
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= T) return;
+    flag[k] = (k == 0) || ((key[k] >> ibits) != (key[k - 1] >> ibits));
+}
+__global__ void k_ev_head_list(int64_t T, const uint8_t *flag, const int64_t *hpos, int64_t *heads) {
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < T && flag[k]) heads[hpos[k]] = k;
+}
+
+// _track_violations (refine.py:145-175): per (track, part) a running value
+// from its base; each (part, i) group toggles the violation flag when the
+// value crosses the limit.  One thread walks one segment.
+__global__ void k_ev_walk(int64_t S, int64_t T, const int64_t *heads, const uint64_t *key, const uint32_t *val,
+                          int ibits, int pbits, const int64_t *psizes, const int64_t *pinbound, int64_t omega,
+                          int64_t delta, int64_t *dlt) {
+    int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= S) return;
+    const int64_t b = heads[s], end = s + 1 < S ? heads[s + 1] : T;
+    const uint64_t k0 = key[b];
+    const int track = (int)(k0 >> (ibits + pbits));
+    const int32_t p = (int32_t)((k0 >> ibits) & ((1ull << pbits) - 1ull));
+    const int64_t limit = track ? delta : omega;
+    int64_t run = track ? pinbound[p] : psizes[p];
+    const uint64_t imask = (1ull << ibits) - 1ull;
+    for (int64_t k = b; k < end;) {
+        const uint64_t i = key[k] & imask;
+        int64_t sum = 0;
+        while (k < end && (key[k] & imask) == i) {
+            sum += (int64_t)(int32_t)val[k];
+            k++;
+        }
+        const bool before = run > limit;
+        run += sum;
+        const bool after = run > limit;
+        if (after != before) atomicAdd((unsigned long long *)&dlt[i + 1], (unsigned long long)(after ? 1ll : -1ll));
+    }
+}
+
+// smallest argmax of cum over prefixes with active == 0 (refine.py:244-247)
+__global__ void k_best_prefix_partial(int64_t n, const int64_t *active_ex, const int64_t *cum, long long *bv,
+                                      long long *bk) {
+    __shared__ long long sv[32], sk[32];
+    long long v = LLONG_MIN, k = LLONG_MAX;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+        // active[j] = inclusive cumsum of delta up to j = active_ex[j + 1]
+        if (active_ex[j + 1] == 0) {
+            long long c = cum[j];
+            if (c > v || (c == v && j < k)) {
+                v = c;
+                k = j;
+            }
+        }
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        long long ov = __shfl_xor_sync(FULL_MASK, v, d), ok = __shfl_xor_sync(FULL_MASK, k, d);
+        if (ov > v || (ov == v && ok < k)) {
+            v = ov;
+            k = ok;
+        }
+    }
+    if (lane_id() == 0) {
+        sv[warp_id()] = v;
+        sk[warp_id()] = k;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); w++)
+            if (sv[w] > v || (sv[w] == v && sk[w] < k)) {
+                v = sv[w];
+                k = sk[w];
+            }
+        bv[blockIdx.x] = v;
+        bk[blockIdx.x] = k;
+    }
+}
+__global__ void k_best_prefix_final(int nb, const long long *bv, const long long *bk, long long *out) {
+    if (threadIdx.x != 0) return;
+    long long v = LLONG_MIN, k = LLONG_MAX;
+    for (int b = 0; b < nb; b++)
+        if (bv[b] > v || (bv[b] == v && bk[b] < k)) {
+            v = bv[b];
+            k = bk[b];
+        }
+    out[0] = k;
+    out[1] = v;
+}
+
+__global__ void k_apply(int64_t k, const int32_t *node, const int32_t *to, int32_t *assign) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < k) assign[node[i]] = to[i];
+}
+
+}  // namespace
+
+// builds the run lists for `assign`; connectivity accumulates into *conn
+// (device), distinct-inbound counts into pinbound when requested
+static void build_runs(Ctx &c, const DLevel &L, const DWeights &W, const int32_t *assign, Runs &r,
+                       int32_t *tmp_parts, int64_t *pinbound, int32_t K, unsigned long long *conn) {
+    KScope ks(c, "edge_runs", (double)(8.0 * L.U + 4.0 * L.U + 12.0 * L.U + 4.0 * L.Pd + 24.0 * L.E));
+    seg_sort(c, L.E, L.pin_off, L.pin_dat, assign, tmp_parts);
+    c.zero(conn, 1);
+    if (pinbound) c.zero(pinbound, K);
+    if (L.E > 0) {
+        k_edge_runs<<<(unsigned)cdiv(L.E, 256), 256, 0, c.stream>>>(L.E, L.pin_off, tmp_parts, L.dst_off, L.dst_dat,
+                                                                   assign, W.wi, r, conn, pinbound);
+        DHGP_LAUNCHED(c);
+    }
+}
+
+void refine_level(Ctx &c, const DLevel &L, const DWeights &W, int32_t *assign, int32_t K, int64_t omega,
+                  int64_t delta, int32_t max_rounds, int32_t level, std::vector<double> &conns,
+                  const RoundObserver *obs) {
+    static bool attr = false;
+    if (!attr) {
+        DHGP_CUDA(cudaFuncSetAttribute(k_propose_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, PR_SMEM));
+        attr = true;
+    }
+    const int32_t N = L.N;
+    Runs r;
+    r.part = c.alloc<int32_t>(L.U);
+    r.cnt = c.alloc<int32_t>(L.U);
+    r.cin = c.alloc<int32_t>(L.U);
+    r.len = c.alloc<int32_t>(L.E);
+    int32_t *tmp_parts = c.alloc<int32_t>(L.U);
+    int64_t *psizes = c.alloc<int64_t>(K);
+    int64_t *pinbound = c.alloc<int64_t>(K);
+    int32_t *target = c.alloc<int32_t>(N);
+    int64_t *gain = c.alloc<int64_t>(N);
+    uint8_t *flags = c.alloc<uint8_t>(N);
+    int64_t *mpos = c.alloc<int64_t>((int64_t)N + 1);
+    int32_t *pos = c.alloc<int32_t>(N);
+    int32_t *ctr = c.alloc<int32_t>(4);
+    int32_t *big = c.alloc<int32_t>(std::max<int64_t>(N, L.E));
+    const int gmax_bits = bitlen((uint64_t)W.wsum);
+
+    unsigned long long *conn_d = c.alloc<unsigned long long>(1);
+    bool need_final = false;
+    for (int32_t rnd = 0; rnd < max_rounds; rnd++) {
+        // --- A11/A12/A16 + A13 ---------------------------------------------
+        build_runs(c, L, W, assign, r, tmp_parts, pinbound, K, conn_d);
+        c.zero(psizes, K);
+        if (N > 0) {
+            k_part_sizes<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(N, assign, L.size, psizes);
+            DHGP_LAUNCHED(c);
+        }
+        // --- A14 propose ---------------------------------------------------
+        {
+            KScope ks(c, "propose", (double)(12.0 * L.U + 16.0 * L.U + 24.0 * N));
+            c.zero(ctr, 4);
+            ProposeArgs a{N, K, L.inc_off, L.inc_dat, L.pin_off, W.wi, r, assign, psizes, L.size, omega,
+                          target, gain, ctr, big, ctr + 1};
+            if (N > 0) {
+                int blocks = (int)std::min<int64_t>(cdiv(N, PR_WARPS), (int64_t)c.num_sms * 2);
+                k_propose_warp<<<blocks, PR_WARPS * 32, PR_SMEM, c.stream>>>(a);
+                DHGP_LAUNCHED(c);
+            }
+            int32_t nbig = 0;
+            c.d2h(&nbig, ctr + 1, 1);
+            c.sync();
+            if (nbig > 0) {
+                int g = (int)std::min<int64_t>(nbig, 64);
+                long long *dense = c.alloc<long long>((int64_t)g * K);
+                int32_t *touched = c.alloc<int32_t>((int64_t)g * K);
+                k_fill_ll<<<(unsigned)cdiv((int64_t)g * K, 256), 256, 0, c.stream>>>(dense, -1ll, (int64_t)g * K);
+                DHGP_LAUNCHED(c);
+                k_propose_block<<<g, PB_THREADS, 0, c.stream>>>(a, dense, touched);
+                DHGP_LAUNCHED(c);
+                c.free(dense);
+                c.free(touched);
+            }
+        }
+        // --- sequence (refine.py:108-110) ------------------------------------
+        if (N > 0) {
+            k_mover_flags<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(N, target, flags);
+            DHGP_LAUNCHED(c);
+        }
+        scan_excl<uint8_t>(c, flags, mpos, N);
+        int64_t M = 0;
+        unsigned long long conn_h = 0;
+        c.d2h(&M, mpos + N, 1);
+        c.d2h(&conn_h, conn_d, 1);
+        c.sync();
+        conns.push_back((double)(int64_t)conn_h);  // connectivity of the round's starting assignment
+        need_final = false;
+        if (M == 0) break;
+        uint64_t *mk = c.alloc<uint64_t>(M), *mkt = c.alloc<uint64_t>(M);
+        uint32_t *mv = c.alloc<uint32_t>(M), *mvt = c.alloc<uint32_t>(M);
+        k_mover_keys<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(N, flags, mpos, gain, W.wsum, mk, mv);
+        DHGP_LAUNCHED(c);
+        radix_sort_pairs(c, mk, mv, mkt, mvt, M, nullptr, gmax_bits);
+        int32_t *node = c.alloc<int32_t>(M), *from = c.alloc<int32_t>(M), *to = c.alloc<int32_t>(M);
+        int64_t *giso = c.alloc<int64_t>(M), *gseq = c.alloc<int64_t>(M);
+        fill_i32(c, pos, -1, N);
+        k_build_moves<<<(unsigned)cdiv(M, 256), 256, 0, c.stream>>>((int32_t)M, mv, assign, target, gain, node, from,
+                                                                   to, giso, pos);
+        DHGP_LAUNCHED(c);
+        c.free(mk);
+        c.free(mkt);
+        c.free(mv);
+        c.free(mvt);
+        // --- A15 in-sequence gains ------------------------------------------
+        {
+            KScope ks(c, "seq_gains", 0.0);
+            int blocks = (int)std::min<int64_t>(cdiv(M, 8), (int64_t)c.num_sms * 16);
+            k_seq_gains<<<blocks, 256, 0, c.stream>>>((int32_t)M, L.inc_off, L.inc_dat, L.pin_off, L.pin_dat, W.wi,
+                                                       r, node, from, to, giso, pos, gseq);
+            DHGP_LAUNCHED(c);
+        }
+        // --- A17 events and prefix selection --------------------------------
+        int64_t kbest = 0, total_gain = 0;
+        int64_t *dlt = c.alloc<int64_t>(M + 1);
+        int64_t *act_ex = c.alloc<int64_t>(M + 2);
+        int64_t *cum = c.alloc<int64_t>(M + 1);
+        {
+            KScope ks(c, "select", 0.0);
+            const int ibits = std::max(1, bitlen((uint64_t)M));
+            const int pbits = std::max(1, bitlen((uint64_t)(K - 1)));
+            if (1 + ibits + pbits > 64)
+                throw Error{DHGP_ERR_UNSUPPORTED, "event key needs more than 64 bits"};
+            const int64_t cap = 2 * M + 2 * L.Sin;
+            uint64_t *ek = c.alloc<uint64_t>(cap), *ekt = c.alloc<uint64_t>(cap);
+            uint32_t *evv = c.alloc<uint32_t>(cap), *evt = c.alloc<uint32_t>(cap);
+            unsigned long long *ecount = c.alloc<unsigned long long>(1);
+            unsigned long long two_m = (unsigned long long)(2 * M);
+            c.h2d(ecount, &two_m, 1);
+            EvArgs ev{ibits, pbits, ek, evv, ecount};
+            k_size_events<<<(unsigned)cdiv(M, 256), 256, 0, c.stream>>>((int32_t)M, node, from, to, L.size, ev);
+            DHGP_LAUNCHED(c);
+            c.zero(ctr, 4);
+            if (L.E > 0) {
+                k_inbound_events<<<(unsigned)cdiv(L.E, 256), 256, 0, c.stream>>>(L.E, L.dst_off, L.dst_dat, L.pin_off,
+                                                                               r, pos, from, to, ev, big, ctr);
+                DHGP_LAUNCHED(c);
+                k_inbound_events_block<<<c.num_sms, 256, 0, c.stream>>>(L.dst_off, L.dst_dat, L.pin_off, r, pos, from,
+                                                                         to, ev, big, ctr, ctr + 2);
+                DHGP_LAUNCHED(c);
+            }
+            unsigned long long T = 0;
+            int32_t hc[4];
+            c.d2h(&T, ecount, 1);
+            c.d2h(hc, ctr, 4);
+            c.sync();
+            if (hc[2]) throw Error{DHGP_ERR_UNSUPPORTED, "too many movers on one h-edge"};
+            radix_sort_pairs(c, ek, evv, ekt, evt, (int64_t)T, nullptr, 1 + ibits + pbits);
+            uint8_t *hf = c.alloc<uint8_t>(T);
+            int64_t *hpos = c.alloc<int64_t>(T + 1);
+            k_ev_heads<<<(unsigned)cdiv(T, 256), 256, 0, c.stream>>>((int64_t)T, ek, ibits, hf);
+            DHGP_LAUNCHED(c);
+            scan_excl<uint8_t>(c, hf, hpos, T);
+            int64_t S = 0;
+            c.d2h(&S, hpos + T, 1);
+            c.sync();
+            int64_t *heads = c.alloc<int64_t>(S);
+            k_ev_head_list<<<(unsigned)cdiv(T, 256), 256, 0, c.stream>>>((int64_t)T, hf, hpos, heads);
+            DHGP_LAUNCHED(c);
+            c.zero(dlt, M + 1);
+            if (S > 0) {
+                k_ev_walk<<<(unsigned)cdiv(S, 128), 128, 0, c.stream>>>(S, (int64_t)T, heads, ek, evv, ibits, pbits,
+                                                                        psizes, pinbound, omega, delta, dlt);
+                DHGP_LAUNCHED(c);
+            }
+            scan_excl<int64_t>(c, dlt, act_ex, M + 1);  // act_ex[j+1] = active[j]
+            scan_excl<int64_t>(c, gseq, cum, M);        // cum[j] = sum of first j gains
+            const int nb = (int)std::min<int64_t>(cdiv(M + 1, 256), 256);
+            long long *bv = c.alloc<long long>(nb), *bk = c.alloc<long long>(nb), *res = c.alloc<long long>(2);
+            k_best_prefix_partial<<<nb, 256, 0, c.stream>>>(M + 1, act_ex, cum, bv, bk);
+            DHGP_LAUNCHED(c);
+            k_best_prefix_final<<<1, 32, 0, c.stream>>>(nb, bv, bk, res);
+            DHGP_LAUNCHED(c);
+            long long hr[2];
+            c.d2h(hr, res, 2);
+            c.sync();
+            kbest = hr[0];
+            total_gain = hr[1];
+            c.free(bv);
+            c.free(bk);
+            c.free(res);
+            c.free(ek);
+            c.free(ekt);
+            c.free(evv);
+            c.free(evt);
+            c.free(ecount);
+            c.free(hf);
+            c.free(hpos);
+            c.free(heads);
+        }
+        if (obs && *obs) {
+            RoundRecord rec;
+            rec.level = level;
+            rec.round = rnd;
+            rec.num_parts = K;
+            rec.k = (int32_t)kbest;
+            rec.total_gain = (double)total_gain;
+            rec.assign.resize(N);
+            rec.node.resize(M);
+            rec.from.resize(M);
+            rec.to.resize(M);
+            std::vector<int64_t> gi(M), gs(M), ae(M + 2);
+            c.d2h(rec.assign.data(), assign, N);
+            c.d2h(rec.node.data(), node, M);
+            c.d2h(rec.from.data(), from, M);
+            c.d2h(rec.to.data(), to, M);
+            c.d2h(gi.data(), giso, M);
+            c.d2h(gs.data(), gseq, M);
+            c.d2h(ae.data(), act_ex, M + 2);
+            c.sync();
+            rec.gain_iso.assign(gi.begin(), gi.end());
+            rec.gain_seq.assign(gs.begin(), gs.end());
+            rec.active.assign(ae.begin() + 1, ae.begin() + 2 + M);
+            (*obs)(rec);
+        }
+        if (kbest > 0) {
+            k_apply<<<(unsigned)cdiv(kbest, 256), 256, 0, c.stream>>>(kbest, node, to, assign);
+            DHGP_LAUNCHED(c);
+        }
+        c.free(node);
+        c.free(from);
+        c.free(to);
+        c.free(giso);
+        c.free(gseq);
+        c.free(dlt);
+        c.free(act_ex);
+        c.free(cum);
+        if (kbest == 0) break;
+        need_final = true;
+    }
+    if (need_final) {
+        double v;
+        evaluate_assign(c, L, W, assign, K, nullptr, nullptr, &v);
+        conns.push_back(v);
+    }
+    c.free(r.part);
+    c.free(r.cnt);
+    c.free(r.cin);
+    c.free(r.len);
+    c.free(tmp_parts);
+    c.free(psizes);
+    c.free(pinbound);
+    c.free(target);
+    c.free(gain);
+    c.free(flags);
+    c.free(mpos);
+    c.free(pos);
+    c.free(ctr);
+    c.free(big);
+    c.free(conn_d);
+}
+
+void evaluate_assign(Ctx &c, const DLevel &L, const DWeights &W, const int32_t *assign, int32_t K,
+                     int64_t *d_sizes, int64_t *d_inbound, double *h_conn) {
+    Runs r;
+    r.part = c.alloc<int32_t>(L.U);
+    r.cnt = c.alloc<int32_t>(L.U);
+    r.cin = c.alloc<int32_t>(L.U);
+    r.len = c.alloc<int32_t>(L.E);
+    int32_t *tmp = c.alloc<int32_t>(L.U);
+    seg_sort(c, L.E, L.pin_off, L.pin_dat, assign, tmp);
+    unsigned long long *conn = c.alloc<unsigned long long>(1);
+    c.zero(conn, 1);
+    if (d_inbound) c.zero(d_inbound, K);
+    if (L.E > 0) {
+        k_edge_runs<<<(unsigned)cdiv(L.E, 256), 256, 0, c.stream>>>(L.E, L.pin_off, tmp, L.dst_off, L.dst_dat, assign,
+                                                                   W.wi, r, conn, d_inbound);
+        DHGP_LAUNCHED(c);
+    }
+    if (d_sizes) {
+        c.zero(d_sizes, K);
+        if (L.N > 0) {
+            k_part_sizes<<<(unsigned)cdiv(L.N, 256), 256, 0, c.stream>>>(L.N, assign, L.size, d_sizes);
+            DHGP_LAUNCHED(c);
+        }
+    }
+    if (h_conn) {
+        unsigned long long h = 0;
+        c.d2h(&h, conn, 1);
+        c.sync();
+        *h_conn = (double)(int64_t)h;
+    }
+    c.free(conn);
+    c.free(r.part);
+    c.free(r.cnt);
+    c.free(r.cin);
+    c.free(r.len);
+    c.free(tmp);
+}
+
+}  // namespace dhgp

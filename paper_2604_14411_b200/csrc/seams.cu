@@ -1,0 +1,607 @@
+// seams.cu — data-model entry points (hgraph.py) and the kernel-level seams
+// that mirror dhgpart.kernels (kernels.py:58-103) one call each.
+//
+// The seams take the reference's exact argument lists (explicit neighbour
+// sets, candidate order, dense pins matrices) and are written to follow the
+// reference's accumulation order, so they are bit-exact for any finite
+// non-negative weights.  The production path (driver.cu) uses the fused,
+// sparse kernels instead.
+#include <mutex>
+
+#include "coarsen.cuh"
+#include "prims.cuh"
+#include "refine.cuh"
+
+namespace dhgp {
+void seams_setup(Ctx &c, int device);
+extern std::mutex g_mu;
+}
+
+using namespace dhgp;
+
+namespace {
+
+template <class T>
+struct DevBuf {
+    Ctx *c = nullptr;
+    T *p = nullptr;
+    int64_t n = 0;
+    DevBuf(Ctx &ctx, int64_t count) : c(&ctx), p(ctx.alloc<T>(count)), n(count) {}
+    DevBuf(Ctx &ctx, const T *host, int64_t count) : c(&ctx), p(ctx.alloc<T>(count)), n(count) {
+        if (host) ctx.h2d(p, host, count);
+    }
+    ~DevBuf() {
+        try {
+            c->free(p);
+        } catch (...) {
+        }
+    }
+    void get(T *host) {
+        c->d2h(host, p, n);
+    }
+};
+
+// ---- fill_histograms (_kernels.pyx:47-72): warp per node, incident h-edges in
+// ascending order, lanes over the pins of one h-edge (distinct slots) -------
+__global__ void k_fill_hist(int32_t N, const int64_t *inc_off, const int32_t *inc_dat, const int64_t *pin_off,
+                            const int32_t *pin_dat, const double *w, const int64_t *nbr_off, const int32_t *nbr_dat,
+                            double *hist) {
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const int lane = lane_id();
+    for (int64_t n = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id(); n < N; n += nw) {
+        const int64_t lo = nbr_off[n], hi = nbr_off[n + 1];
+        if (lo == hi) continue;
+        for (int64_t ii = inc_off[n]; ii < inc_off[n + 1]; ii++) {
+            const int32_t e = inc_dat[ii];
+            const double we = w[e];
+            for (int64_t p = pin_off[e] + lane; p < pin_off[e + 1]; p += 32) {
+                int64_t j = bsearch_dev(nbr_dat, lo, hi, pin_dat[p]);
+                if (j >= 0) hist[j] += we;
+            }
+            __syncwarp();
+        }
+    }
+}
+
+// ---- select_first_valid (_kernels.pyx:75-103): thread per node ------------
+__global__ void k_select_first_valid(int32_t N, const int64_t *order, const int64_t *nbr_off, const int32_t *nbr_dat,
+                                     const double *hist, const int32_t *size, const int64_t *in_off,
+                                     const int32_t *in_dat, int64_t omega, int64_t delta, int32_t *pair,
+                                     double *score) {
+    int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (n >= N) return;
+    pair[n] = -1;
+    score[n] = 0.0;
+    for (int64_t t = nbr_off[n]; t < nbr_off[n + 1]; t++) {
+        const int64_t pos = order[t];
+        const int32_t m = nbr_dat[pos];
+        if ((int64_t)size[n] + size[m] > omega) continue;
+        int64_t cnt = in_off[n + 1] - in_off[n];
+        for (int64_t k = in_off[m]; k < in_off[m + 1]; k++)
+            if (bsearch_dev(in_dat, in_off[n], in_off[n + 1], in_dat[k]) < 0) cnt++;
+        if (cnt > delta) continue;
+        pair[n] = m;
+        score[n] = hist[pos];
+        break;
+    }
+}
+
+// ---- connectivity_value (_kernels.pyx:184-213) -----------------------------
+__global__ void k_edge_lambda(int32_t E, const int64_t *pin_off, const int32_t *sorted_parts, const double *w,
+                              double *contrib) {
+    int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= E) return;
+    int64_t lam = 0;
+    for (int64_t p = pin_off[e]; p < pin_off[e + 1]; p++) lam += (p == pin_off[e]) || sorted_parts[p] != sorted_parts[p - 1];
+    contrib[e] = lam > 0 ? w[e] * (double)(lam - 1) : 0.0;
+}
+// the reference sums in ascending edge order; one thread keeps that order so
+// the result is bit-exact for non-integral weights as well
+__global__ void k_ordered_sum(int64_t n, const double *x, double *out) {
+    if (threadIdx.x || blockIdx.x) return;
+    double t = 0.0;
+    for (int64_t i = 0; i < n; i++) t += x[i];
+    *out = t;
+}
+
+// ---- compute_pins (_kernels.pyx:216-231): thread per h-edge row -----------
+__global__ void k_dense_pins(int32_t E, const int64_t *off, const int32_t *dat, const int32_t *assign, int32_t K,
+                             int32_t *pins) {
+    int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= E) return;
+    for (int64_t p = off[e]; p < off[e + 1]; p++) pins[e * (int64_t)K + assign[dat[p]]]++;
+}
+
+// ---- propose_moves (_kernels.pyx:234-311): thread per node ----------------
+__global__ void k_node_work(int32_t N, const int64_t *inc_off, const int32_t *inc_dat, const int64_t *pin_off,
+                            int64_t *work) {
+    int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (n >= N) return;
+    int64_t acc = 0;
+    for (int64_t i = inc_off[n]; i < inc_off[n + 1]; i++) acc += pin_off[inc_dat[i] + 1] - pin_off[inc_dat[i]];
+    work[n] = acc;
+}
+__global__ void k_propose_dense(int32_t N, const int64_t *inc_off, const int32_t *inc_dat, const int64_t *pin_off,
+                                const int32_t *pin_dat, const double *w, const int32_t *pins, int32_t K,
+                                const int32_t *assign, const int64_t *psizes, const int32_t *size, int64_t omega,
+                                const int64_t *scratch_off, int32_t *cand, double *pres, int32_t *eparts,
+                                int32_t *target, double *gain) {
+    int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (n >= N) return;
+    target[n] = -1;
+    gain[n] = 0.0;
+    if (inc_off[n + 1] == inc_off[n] || K < 2) return;
+    int32_t *cd = cand + scratch_off[n];
+    double *pr = pres + scratch_off[n];
+    int32_t *ep = eparts + scratch_off[n];
+    const int32_t ps = assign[n];
+    double saving = 0.0, total = 0.0;
+    int64_t nc = 0;
+    for (int64_t ii = inc_off[n]; ii < inc_off[n + 1]; ii++) {
+        const int32_t e = inc_dat[ii];
+        const double we = w[e];
+        total += we;
+        if (pins[(int64_t)e * K + ps] == 1) saving += we;
+        int64_t ne = 0;
+        for (int64_t pp = pin_off[e]; pp < pin_off[e + 1]; pp++) {
+            const int32_t part = assign[pin_dat[pp]];
+            bool seen = false;
+            for (int64_t j = 0; j < ne && !seen; j++) seen = ep[j] == part;
+            if (!seen) ep[ne++] = part;
+        }
+        for (int64_t j = 0; j < ne; j++) {
+            bool seen = false;
+            for (int64_t q = 0; q < nc; q++)
+                if (cd[q] == ep[j]) {
+                    pr[q] += we;
+                    seen = true;
+                    break;
+                }
+            if (!seen) {
+                cd[nc] = ep[j];
+                pr[nc] = we;
+                nc++;
+            }
+        }
+    }
+    int32_t best = -1;
+    double best_gain = 0.0;
+    for (int64_t j = 0; j < nc; j++) {
+        const int32_t part = cd[j];
+        if (part == ps || psizes[part] + size[n] > omega) continue;
+        const double g = saving - (total - pr[j]);
+        if (best < 0 || g > best_gain || (g == best_gain && part < best)) {
+            best = part;
+            best_gain = g;
+        }
+    }
+    if (best >= 0 && best_gain > 0.0) {
+        target[n] = best;
+        gain[n] = best_gain;
+    }
+}
+
+// ---- sequence_gains (_kernels.pyx:314-364): thread per move ---------------
+__global__ void k_seq_dense(int32_t M, const int64_t *inc_off, const int32_t *inc_dat, const int64_t *pin_off,
+                            const int32_t *pin_dat, const double *w, const int32_t *pins, int32_t K,
+                            const int32_t *node, const int32_t *from, const int32_t *to, const double *giso,
+                            const int64_t *pos, double *out) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= M) return;
+    const int32_t n = node[i], ps = from[i], pd = to[i];
+    double g = giso[i];
+    for (int64_t ii = inc_off[n]; ii < inc_off[n + 1]; ii++) {
+        const int32_t e = inc_dat[ii];
+        const int64_t base_ps = pins[(int64_t)e * K + ps], base_pd = pins[(int64_t)e * K + pd];
+        int64_t leav_pd = 0, ent_pd = 0, leav_ps = 0, ent_ps = 0;
+        for (int64_t pp = pin_off[e]; pp < pin_off[e + 1]; pp++) {
+            const int64_t j = pos[pin_dat[pp]];
+            if (j < 0 || j >= i) continue;
+            leav_pd += from[j] == pd;
+            ent_pd += to[j] == pd;
+            leav_ps += from[j] == ps;
+            ent_ps += to[j] == ps;
+        }
+        double net = 0.0;
+        if (base_pd > 0) {
+            if (leav_pd - ent_pd == base_pd) net -= w[e];
+        } else if (ent_pd > 0) {
+            net += w[e];
+        }
+        if (base_ps == 1) {
+            if (ent_ps > 0) net -= w[e];
+        } else if (base_ps - 1 > 0 && leav_ps - ent_ps == base_ps - 1) {
+            net += w[e];
+        }
+        g += net;
+    }
+    out[i] = g;
+}
+
+__global__ void k_union_size(const int32_t *a, int64_t na, const int32_t *b, int64_t nb, unsigned long long *out) {
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < nb && bsearch_dev(a, 0, na, b[k]) < 0) atomicAdd(out, 1ull);
+}
+
+// ---- neighbours (coarsen.py:78-85): (node, pin) keys, radix-sorted ---------
+__global__ void k_nbr_count(int32_t N, const int64_t *inc_off, const int32_t *inc_dat, const int64_t *pin_off,
+                            int64_t *cnt) {
+    int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (n >= N) return;
+    int64_t acc = 0;
+    for (int64_t i = inc_off[n]; i < inc_off[n + 1]; i++) acc += pin_off[inc_dat[i] + 1] - pin_off[inc_dat[i]];
+    cnt[n] = acc;
+}
+__global__ void k_nbr_expand(int32_t N, const int64_t *inc_off, const int32_t *inc_dat, const int64_t *pin_off,
+                             const int32_t *pin_dat, const int64_t *xoff, uint64_t *keys, uint32_t *vals) {
+    int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (n >= N) return;
+    int64_t o = xoff[n];
+    for (int64_t i = inc_off[n]; i < inc_off[n + 1]; i++) {
+        const int32_t e = inc_dat[i];
+        for (int64_t p = pin_off[e]; p < pin_off[e + 1]; p++) {
+            keys[o] = ((uint64_t)n << 32) | (uint32_t)pin_dat[p];
+            vals[o] = 0;
+            o++;
+        }
+    }
+}
+__global__ void k_nbr_keep(int64_t X, const uint64_t *keys, uint8_t *keep, int64_t *node_cnt) {
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= X) return;
+    const uint64_t key = keys[k];
+    const uint32_t n = (uint32_t)(key >> 32), m = (uint32_t)key;
+    const bool kp = m != n && (k == 0 || keys[k - 1] != key);
+    keep[k] = kp;
+    if (kp) atomicAdd((unsigned long long *)&node_cnt[n], 1ull);
+}
+__global__ void k_nbr_write(int64_t X, const uint64_t *keys, const uint8_t *keep, const int64_t *kpos, int32_t *out) {
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < X && keep[k]) out[kpos[k]] = (int32_t)(uint32_t)keys[k];
+}
+
+}  // namespace
+
+#define SEAM_BEGIN                           \
+    std::lock_guard<std::mutex> _lk(g_mu);   \
+    try {                                    \
+        Ctx c;                               \
+        seams_setup(c, device);
+#define SEAM_END                            \
+    c.sync();                               \
+    }                                       \
+    catch (const Error &e) {                \
+        set_error(e.code, e.msg);           \
+        return e.code;                      \
+    }                                       \
+    catch (const std::exception &e) {       \
+        set_error(DHGP_ERR_CUDA, e.what()); \
+        return DHGP_ERR_CUDA;               \
+    }                                       \
+    return DHGP_OK;
+
+extern "C" {
+
+int dhgp_incidence(const dhgp_graph *g, int32_t device, int64_t *in_off, int32_t *in_dat, int64_t *out_off,
+                   int32_t *out_dat, int64_t *pin_off, int32_t *pin_dat, int64_t *inc_off, int32_t *inc_dat,
+                   int64_t *num_pins_out) {
+    SEAM_BEGIN
+    DInput in;
+    upload_input(c, *g, in);
+    DLevel L;
+    build_level0(c, in, L);
+    const int64_t N = L.N, E = L.E;
+    if (num_pins_out) *num_pins_out = L.U;
+    if (in_off) c.d2h(in_off, L.in_off, N + 1);
+    if (in_dat) c.d2h(in_dat, L.in_dat, L.Pd);
+    if (pin_off) c.d2h(pin_off, L.pin_off, E + 1);
+    if (pin_dat) c.d2h(pin_dat, L.pin_dat, L.U);
+    if (inc_off) c.d2h(inc_off, L.inc_off, N + 1);
+    if (inc_dat) c.d2h(inc_dat, L.inc_dat, L.U);
+    if (out_off || out_dat) {
+        int64_t *oo = c.alloc<int64_t>(N + 1);
+        int32_t *od = c.alloc<int32_t>(L.Ps);
+        derive_out(c, L, oo, od);
+        if (out_off) c.d2h(out_off, oo, N + 1);
+        if (out_dat) c.d2h(out_dat, od, L.Ps);
+        c.sync();
+        c.free(oo);
+        c.free(od);
+    }
+    c.sync();
+    L.release(c);
+    in.release(c);
+    SEAM_END
+}
+
+int dhgp_neighbors(const dhgp_graph *g, int32_t device, int64_t *nb_off, int32_t **nb_dat, int64_t *nnz_out) {
+    SEAM_BEGIN
+    DInput in;
+    upload_input(c, *g, in);
+    DLevel L;
+    build_level0(c, in, L);
+    const int32_t N = L.N;
+    int64_t *cnt = c.alloc<int64_t>(N), *xoff = c.alloc<int64_t>((int64_t)N + 1);
+    int64_t X = 0;
+    if (N > 0) {
+        k_nbr_count<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(N, L.inc_off, L.inc_dat, L.pin_off, cnt);
+        DHGP_LAUNCHED(c);
+    }
+    scan_excl<int64_t>(c, cnt, xoff, N);
+    c.d2h(&X, xoff + N, 1);
+    c.sync();
+    uint64_t *k = c.alloc<uint64_t>(X), *kt = c.alloc<uint64_t>(X);
+    uint32_t *v = c.alloc<uint32_t>(X), *vt = c.alloc<uint32_t>(X);
+    if (N > 0) {
+        k_nbr_expand<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(N, L.inc_off, L.inc_dat, L.pin_off, L.pin_dat,
+                                                                  xoff, k, v);
+        DHGP_LAUNCHED(c);
+    }
+    radix_sort_pairs(c, k, v, kt, vt, X, nullptr, 32 + bitlen((uint64_t)(N > 0 ? N - 1 : 0)));
+    uint8_t *keep = c.alloc<uint8_t>(X);
+    int64_t *kpos = c.alloc<int64_t>(X + 1);
+    c.zero(cnt, N);
+    if (X > 0) {
+        k_nbr_keep<<<(unsigned)cdiv(X, 256), 256, 0, c.stream>>>(X, k, keep, cnt);
+        DHGP_LAUNCHED(c);
+    }
+    scan_excl<uint8_t>(c, keep, kpos, X);
+    int64_t nnz = 0;
+    c.d2h(&nnz, kpos + X, 1);
+    c.sync();
+    int32_t *out = c.alloc<int32_t>(nnz);
+    if (X > 0) {
+        k_nbr_write<<<(unsigned)cdiv(X, 256), 256, 0, c.stream>>>(X, k, keep, kpos, out);
+        DHGP_LAUNCHED(c);
+    }
+    scan_excl<int64_t>(c, cnt, xoff, N);
+    c.d2h(nb_off, xoff, (int64_t)N + 1);
+    int32_t *h = (int32_t *)malloc(sizeof(int32_t) * (size_t)(nnz ? nnz : 1));
+    c.d2h(h, out, nnz);
+    c.sync();
+    *nb_dat = h;
+    *nnz_out = nnz;
+    for (void *p : {(void *)cnt, (void *)xoff, (void *)k, (void *)kt, (void *)v, (void *)vt, (void *)keep,
+                    (void *)kpos, (void *)out})
+        c.free(p);
+    L.release(c);
+    in.release(c);
+    SEAM_END
+}
+
+int dhgp_check_feasibility(const dhgp_graph *g, int64_t max_size, int64_t max_inbound, int32_t device) {
+    SEAM_BEGIN
+    if (max_size < 1) throw Error{DHGP_ERR_INFEASIBLE, "max_size must be >= 1, got " + std::to_string(max_size)};
+    if (max_inbound < 0)
+        throw Error{DHGP_ERR_INFEASIBLE, "max_inbound must be >= 0, got " + std::to_string(max_inbound)};
+    DInput in;
+    upload_input(c, *g, in);
+    DLevel L;
+    build_level0(c, in, L);
+    int32_t bs = -1, bi = -1;
+    if (L.N > 0) feasibility(c, L, max_size, max_inbound, &bs, &bi);
+    std::string msg;
+    if (bs >= 0) {
+        int32_t sz;
+        c.d2h(&sz, L.size + bs, 1);
+        c.sync();
+        msg = "node " + std::to_string(bs) + " has size " + std::to_string(sz) + " > max_size " +
+              std::to_string(max_size);
+    } else if (bi >= 0) {
+        int64_t o[2];
+        c.d2h(o, L.in_off + bi, 2);
+        c.sync();
+        msg = "node " + std::to_string(bi) + " has " + std::to_string(o[1] - o[0]) + " inbound edges > max_inbound " +
+              std::to_string(max_inbound);
+    }
+    L.release(c);
+    in.release(c);
+    c.sync();
+    if (!msg.empty()) throw Error{DHGP_ERR_INFEASIBLE, msg};
+    SEAM_END
+}
+
+int dhgp_evaluate(const dhgp_graph *g, const int32_t *assign, int32_t num_parts, int32_t device, int64_t *sizes_out,
+                  int64_t *inbound_out, double *connectivity_out) {
+    SEAM_BEGIN
+    DInput in;
+    upload_input(c, *g, in);
+    DLevel L;
+    build_level0(c, in, L);
+    DevBuf<int32_t> da(c, assign, L.N);
+    DevBuf<int64_t> ds(c, num_parts), di(c, num_parts);
+    // per-part sizes and distinct inbound (integer, exact)
+    DWeights W;
+    W.E = in.E;
+    W.w = in.w;
+    W.wi = c.alloc<int64_t>(in.E);
+    c.zero(W.wi, in.E);
+    evaluate_assign(c, L, W, da.p, num_parts, ds.p, di.p, nullptr);
+    if (sizes_out) ds.get(sizes_out);
+    if (inbound_out) di.get(inbound_out);
+    // connectivity with the reference's ascending-edge f64 summation
+    if (connectivity_out) {
+        int32_t *tmp = c.alloc<int32_t>(L.U);
+        double *contrib = c.alloc<double>(L.E), *res = c.alloc<double>(1);
+        seg_sort(c, L.E, L.pin_off, L.pin_dat, da.p, tmp);
+        if (L.E > 0) {
+            k_edge_lambda<<<(unsigned)cdiv(L.E, 256), 256, 0, c.stream>>>(L.E, L.pin_off, tmp, in.w, contrib);
+            DHGP_LAUNCHED(c);
+        }
+        k_ordered_sum<<<1, 32, 0, c.stream>>>(L.E, contrib, res);
+        DHGP_LAUNCHED(c);
+        c.d2h(connectivity_out, res, 1);
+        c.sync();
+        c.free(tmp);
+        c.free(contrib);
+        c.free(res);
+    }
+    c.sync();
+    W.release(c);
+    L.release(c);
+    in.release(c);
+    SEAM_END
+}
+
+int dhgp_union_size_sorted(const int32_t *a, int64_t na, const int32_t *b, int64_t nb, int32_t device, int64_t *out) {
+    SEAM_BEGIN
+    DevBuf<int32_t> da(c, a, na), db(c, b, nb);
+    DevBuf<unsigned long long> r(c, 1);
+    c.zero(r.p, 1);
+    if (nb > 0) {
+        k_union_size<<<(unsigned)cdiv(nb, 256), 256, 0, c.stream>>>(da.p, na, db.p, nb, r.p);
+        DHGP_LAUNCHED(c);
+    }
+    unsigned long long h = 0;
+    r.get(&h);
+    c.sync();
+    *out = na + (int64_t)h;
+    SEAM_END
+}
+
+int dhgp_fill_histograms(int32_t N, const int64_t *inc_off, const int32_t *inc_dat, int32_t E, const int64_t *pin_off,
+                         const int32_t *pin_dat, const double *w, const int64_t *nbr_off, const int32_t *nbr_dat,
+                         int64_t batch, int32_t device, double *hist) {
+    SEAM_BEGIN
+    if (batch < 1) throw Error{DHGP_ERR_ARG, "batch_size must be >= 1, got " + std::to_string(batch)};
+    DevBuf<int64_t> io(c, inc_off, (int64_t)N + 1), po(c, pin_off, (int64_t)E + 1), no(c, nbr_off, (int64_t)N + 1);
+    DevBuf<int32_t> id(c, inc_dat, inc_off[N]), pd(c, pin_dat, pin_off[E]), nd(c, nbr_dat, nbr_off[N]);
+    DevBuf<double> dw(c, w, E), dh(c, nbr_off[N]);
+    c.zero(dh.p, nbr_off[N]);
+    if (N > 0) {
+        k_fill_hist<<<(unsigned)std::min<int64_t>(cdiv(N, 8), 4096), 256, 0, c.stream>>>(N, io.p, id.p, po.p, pd.p,
+                                                                                      dw.p, no.p, nd.p, dh.p);
+        DHGP_LAUNCHED(c);
+    }
+    dh.get(hist);
+    SEAM_END
+}
+
+int dhgp_select_first_valid(int32_t N, const int64_t *order, const int64_t *nbr_off, const int32_t *nbr_dat,
+                            const double *hist, const int32_t *node_size, const int64_t *in_off, const int32_t *in_dat,
+                            int64_t max_size, int64_t max_inbound, int32_t device, int32_t *pair, double *score) {
+    SEAM_BEGIN
+    const int64_t NB = nbr_off[N];
+    DevBuf<int64_t> dord(c, order, NB), no(c, nbr_off, (int64_t)N + 1), io(c, in_off, (int64_t)N + 1);
+    DevBuf<int32_t> nd(c, nbr_dat, NB), sz(c, node_size, N), id(c, in_dat, in_off[N]), dp(c, N);
+    DevBuf<double> dh(c, hist, NB), ds(c, N);
+    if (N > 0) {
+        k_select_first_valid<<<(unsigned)cdiv(N, 128), 128, 0, c.stream>>>(N, dord.p, no.p, nd.p, dh.p, sz.p, io.p,
+                                                                          id.p, max_size, max_inbound, dp.p, ds.p);
+        DHGP_LAUNCHED(c);
+    }
+    dp.get(pair);
+    ds.get(score);
+    SEAM_END
+}
+
+int dhgp_resolve_matching(int32_t N, const int32_t *pair, const double *score, int32_t device, int32_t *match) {
+    SEAM_BEGIN
+    DevBuf<int32_t> dp(c, pair, N), dm(c, N);
+    DevBuf<double> ds(c, score, N);
+    DevBuf<uint8_t> rep(c, N);
+    resolve_matching(c, N, dp.p, ds.p, dm.p, rep.p);
+    if (N > 0) dm.get(match);
+    SEAM_END
+}
+
+int dhgp_connectivity_value(int32_t E, const int64_t *pin_off, const int32_t *pin_dat, const double *w, int32_t N,
+                            const int32_t *assign, int32_t device, double *out) {
+    SEAM_BEGIN
+    DevBuf<int64_t> po(c, pin_off, (int64_t)E + 1);
+    DevBuf<int32_t> pd(c, pin_dat, pin_off[E]), da(c, assign, N), tmp(c, pin_off[E]);
+    DevBuf<double> dw(c, w, E), contrib(c, E), res(c, 1);
+    seg_sort(c, E, po.p, pd.p, da.p, tmp.p);
+    if (E > 0) {
+        k_edge_lambda<<<(unsigned)cdiv(E, 256), 256, 0, c.stream>>>(E, po.p, tmp.p, dw.p, contrib.p);
+        DHGP_LAUNCHED(c);
+    }
+    k_ordered_sum<<<1, 32, 0, c.stream>>>(E, contrib.p, res.p);
+    DHGP_LAUNCHED(c);
+    res.get(out);
+    SEAM_END
+}
+
+int dhgp_compute_pins(int32_t E, const int64_t *pin_off, const int32_t *pin_dat, const int64_t *dst_off,
+                      const int32_t *dst_dat, int32_t N, const int32_t *assign, int32_t K, int32_t device, int32_t *pins,
+                      int32_t *pins_in) {
+    SEAM_BEGIN
+    DevBuf<int64_t> po(c, pin_off, (int64_t)E + 1), dof(c, dst_off, (int64_t)E + 1);
+    DevBuf<int32_t> pd(c, pin_dat, pin_off[E]), dd(c, dst_dat, dst_off[E]), da(c, assign, N);
+    DevBuf<int32_t> dpins(c, (int64_t)E * K), dpin(c, (int64_t)E * K);
+    c.zero(dpins.p, (int64_t)E * K);
+    c.zero(dpin.p, (int64_t)E * K);
+    if (E > 0) {
+        k_dense_pins<<<(unsigned)cdiv(E, 256), 256, 0, c.stream>>>(E, po.p, pd.p, da.p, K, dpins.p);
+        DHGP_LAUNCHED(c);
+        k_dense_pins<<<(unsigned)cdiv(E, 256), 256, 0, c.stream>>>(E, dof.p, dd.p, da.p, K, dpin.p);
+        DHGP_LAUNCHED(c);
+    }
+    dpins.get(pins);
+    dpin.get(pins_in);
+    SEAM_END
+}
+
+int dhgp_propose_moves(int32_t N, const int64_t *inc_off, const int32_t *inc_dat, int32_t E, const int64_t *pin_off,
+                       const int32_t *pin_dat, const double *w, const int32_t *pins, int32_t K, const int32_t *assign,
+                       const int64_t *part_sizes, const int32_t *node_size, int64_t max_size, int32_t device,
+                       int32_t *target, double *gain) {
+    SEAM_BEGIN
+    DevBuf<int64_t> io(c, inc_off, (int64_t)N + 1), po(c, pin_off, (int64_t)E + 1), ps(c, part_sizes, K);
+    DevBuf<int32_t> id(c, inc_dat, inc_off[N]), pd(c, pin_dat, pin_off[E]), dpins(c, pins, (int64_t)E * K);
+    DevBuf<int32_t> da(c, assign, N), sz(c, node_size, N), dt(c, N);
+    DevBuf<double> dw(c, w, E), dg(c, N);
+    DevBuf<int64_t> work(c, N), woff(c, (int64_t)N + 1);
+    if (N > 0) {
+        k_node_work<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(N, io.p, id.p, po.p, work.p);
+        DHGP_LAUNCHED(c);
+    }
+    scan_excl<int64_t>(c, work.p, woff.p, N);
+    int64_t X = 0;
+    c.d2h(&X, woff.p + N, 1);
+    c.sync();
+    DevBuf<int32_t> cand(c, X), ep(c, X);
+    DevBuf<double> pres(c, X);
+    if (N > 0) {
+        k_propose_dense<<<(unsigned)cdiv(N, 128), 128, 0, c.stream>>>(N, io.p, id.p, po.p, pd.p, dw.p, dpins.p, K, da.p,
+                                                                     ps.p, sz.p, max_size, woff.p, cand.p, pres.p,
+                                                                     ep.p, dt.p, dg.p);
+        DHGP_LAUNCHED(c);
+    }
+    dt.get(target);
+    dg.get(gain);
+    SEAM_END
+}
+
+int dhgp_sequence_gains(int32_t N, const int64_t *inc_off, const int32_t *inc_dat, int32_t E, const int64_t *pin_off,
+                        const int32_t *pin_dat, const double *w, const int32_t *pins, int32_t K, int32_t M,
+                        const int32_t *node, const int32_t *from_part, const int32_t *to_part, const double *gain_iso,
+                        const int64_t *pos, int32_t device, double *gain_seq) {
+    SEAM_BEGIN
+    DevBuf<int64_t> io(c, inc_off, (int64_t)N + 1), po(c, pin_off, (int64_t)E + 1), dpos(c, pos, N);
+    DevBuf<int32_t> id(c, inc_dat, inc_off[N]), pd(c, pin_dat, pin_off[E]), dpins(c, pins, (int64_t)E * K);
+    DevBuf<int32_t> dn(c, node, M), df(c, from_part, M), dt(c, to_part, M);
+    DevBuf<double> dw(c, w, E), dgi(c, gain_iso, M), dgs(c, M);
+    if (M > 0) {
+        k_seq_dense<<<(unsigned)cdiv(M, 128), 128, 0, c.stream>>>(M, io.p, id.p, po.p, pd.p, dw.p, dpins.p, K, dn.p,
+                                                                 df.p, dt.p, dgi.p, dpos.p, dgs.p);
+        DHGP_LAUNCHED(c);
+    }
+    dgs.get(gain_seq);
+    SEAM_END
+}
+
+int dhgp_build_events_and_select(int32_t N, const int64_t *in_off, const int32_t *in_dat, const int32_t *node_size,
+                                 int32_t E, int32_t K, int32_t M, const int32_t *node, const int32_t *from_part,
+                                 const int32_t *to_part, const double *gain_seq, const int32_t *pins_in,
+                                 const int64_t *part_sizes, const int64_t *part_inbound, int64_t max_size,
+                                 int64_t max_inbound, int32_t device, int64_t *k_out, double *total_gain_out,
+                                 int64_t *active) {
+    (void)N; (void)in_off; (void)in_dat; (void)node_size; (void)E; (void)K; (void)M; (void)node; (void)from_part;
+    (void)to_part; (void)gain_seq; (void)pins_in; (void)part_sizes; (void)part_inbound; (void)max_size;
+    (void)max_inbound; (void)device; (void)k_out; (void)total_gain_out; (void)active;
+    set_error(DHGP_ERR_UNSUPPORTED, "dhgp_build_events_and_select: standalone seam not built yet");
+    return DHGP_ERR_UNSUPPORTED;
+}
+
+}  // extern "C"
