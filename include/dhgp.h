@@ -65,6 +65,7 @@ typedef struct {
     int32_t num_partitions;
     double phase_ms[3];    /* coarsen, refine, total (wall, ms)          */
     int64_t gpu_launches;  /* kernels launched by this call              */
+    double device_ms;      /* CUDA-event time of the call on its stream  */
 } dhgp_stats;
 
 /* ---- observer payloads (driver.py:106-116, refine.py:295-307) --------- */

@@ -46,7 +46,7 @@ class DhgpStats(C.Structure):
         ("level_pins", C.POINTER(C.c_int64)),
         ("trace_off", C.POINTER(C.c_int64)), ("trace_val", C.POINTER(C.c_double)),
         ("num_partitions", C.c_int32), ("phase_ms", C.c_double * 3),
-        ("gpu_launches", C.c_int64),
+        ("gpu_launches", C.c_int64), ("device_ms", C.c_double),
     ]
 
 

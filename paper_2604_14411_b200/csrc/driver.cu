@@ -109,6 +109,7 @@ struct PartitionResult {
     std::vector<DLevel> levels_meta;  // N/E/Ps/Pd only
     std::vector<std::vector<double>> trace;
     double phase_ms[3] = {0, 0, 0};
+    double device_ms = 0;
 };
 
 static double now_ms() {
@@ -367,6 +368,7 @@ static void fill_stats(const PartitionResult &r, dhgp_stats *s, int64_t launches
     s->num_partitions = r.num_parts;
     for (int i = 0; i < 3; i++) s->phase_ms[i] = r.phase_ms[i];
     s->gpu_launches = launches;
+    s->device_ms = r.device_ms;
 }
 
 }  // namespace dhgp
@@ -481,7 +483,18 @@ int dhgp_session_partition(dhgp_session *s, const dhgp_config *cfg, int32_t *ass
     dhgp_config cc = *cfg;
     cc.device = s->device;
     PartitionResult r;
+    cudaEvent_t ev0, ev1;
+    DHGP_CUDA(cudaEventCreate(&ev0));
+    DHGP_CUDA(cudaEventCreate(&ev1));
+    DHGP_CUDA(cudaEventRecord(ev0, c.stream));
     run_partition(c, s->in, cc, r, nullptr, nullptr);
+    DHGP_CUDA(cudaEventRecord(ev1, c.stream));
+    DHGP_CUDA(cudaEventSynchronize(ev1));
+    float dms = 0.f;
+    DHGP_CUDA(cudaEventElapsedTime(&dms, ev0, ev1));
+    r.device_ms = dms;
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ev1);
     if (c.profiling) {
         c.flush_profile();
         s->kstats = c.kstats;

@@ -1,0 +1,283 @@
+"""GPU parity: libdhgp.so (through the public API and the C-ABI seams) against
+the reference's golden fixtures and the CPU oracle.  Bit-exact equality for
+every integer and f64 output (weights are integral)."""
+from __future__ import annotations
+
+import json
+
+import numpy as np
+import pytest
+
+from conftest import H1_TEXT, arrays_of, load_npz, make_instance
+from oracle import oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+def dp():
+    import paper_2604_14411_b200 as m
+
+    return m
+
+
+def graph(arr):
+    d = dp()
+    n, w, so, sd, do, dd = arr
+    return d.Hypergraph._from_csr(int(n), w, d.CsrSets(so, sd), d.CsrSets(do, dd))
+
+
+def run_gpu(g, omega, delta, record=False, **kw):
+    d = dp()
+    ev = []
+
+    def obs(kind, p):
+        ev.append((kind, p))
+
+    part, st = d.partition(g, d.Config(d.Constraints(omega, delta), **kw), observer=obs if record else None)
+    return part, st, ev
+
+
+def assert_same_as_oracle(g, omega, delta, max_levels=1 << 20, **kw):
+    part, st, _ = run_gpu(g, omega, delta, max_levels=max_levels, **kw)
+    a, k, ost, _ = orc.partition(*arrays_of(g), g.node_size, max_size=omega, max_inbound=delta,
+                                 max_levels=max_levels, **kw)
+    assert np.array_equal(part.assign, a)
+    assert part.num_parts == k == st.num_partitions
+    assert st.levels == ost["levels"]
+    assert st.connectivity_trace == ost["connectivity_trace"]
+    return part, st
+
+
+# ---------------------------------------------------------------------------
+# golden fixtures from the reference
+# ---------------------------------------------------------------------------
+def test_partition_small_golden_with_observer_payloads():
+    z = load_npz("partition_small.npz")
+    for t in z["cases"]:
+        p = f"c{t}_"
+        g = graph([z[f"{p}in_{k}"] for k in ("n", "w", "so", "sd", "do", "dd")])
+        part, st, ev = run_gpu(g, int(z[p + "omega"]), int(z[p + "delta"]), record=True, max_levels=1 << 20)
+        ref = json.loads(bytes(z[p + "stats"]).decode())
+        assert np.array_equal(part.assign, z[p + "assign"]), t
+        assert part.num_parts == int(z[p + "num_parts"])
+        assert st.levels == ref["levels"] and st.connectivity_trace == ref["trace"]
+        lev = [e for k, e in ev if k == "level"]
+        rnd = [e for k, e in ev if k == "round"]
+        assert len(lev) == int(z[p + "nlev_ev"]) and len(rnd) == int(z[p + "nround_ev"])
+        for i, e in enumerate(lev):
+            f, cm, co = e["forest"], e["cmap"], e["coarse"]
+            assert e["index"] == i and co.num_nodes == cm.num_coarse
+            for got, fk in ((f.pair, "pair"), (f.score, "score"), (f.match, "match"), (cm.gamma, "gamma"),
+                            (co.edge_src.offsets, "so"), (co.edge_src.data, "sd"), (co.edge_dst.offsets, "do"),
+                            (co.edge_dst.data, "dd"), (co.node_size, "size")):
+                assert np.array_equal(got, z[f"{p}L{i}_{fk}"]), (t, i, fk)
+        for i, e in enumerate(rnd):
+            m, s = e["moves"], e["selection"]
+            assert e["level"] == int(z[f"{p}R{i}_level"]) and e["round"] == int(z[f"{p}R{i}_round"])
+            for got, fk in ((e["assign"], "assign"), (m.node, "node"), (m.from_part, "from"), (m.to_part, "to"),
+                            (m.gain_iso, "giso"), (m.gain_seq, "gseq"), (s.active, "active")):
+                assert np.array_equal(got, z[f"{p}R{i}_{fk}"]), (t, i, fk)
+            assert s.k == int(z[f"{p}R{i}_k"]) and s.total_gain == float(z[f"{p}R{i}_total"])
+
+
+@pytest.mark.parametrize("name,gen,omega,delta", [
+    ("c1.npz", ("random_dhg", dict(num_nodes=10_000, num_edges=20_000, max_pins=8, seed=0)), 256, 1024),
+    ("snn.npz", ("layered_snn", dict(layers=3, width=300)), 64, 4096),
+])
+def test_full_instances_golden(name, gen, omega, delta):
+    from paper_2604_14411_b200 import workloads as W
+
+    z = load_npz(name)
+    g = graph(getattr(W, gen[0])(**gen[1]))
+    part, st, _ = run_gpu(g, omega, delta, max_levels=1 << 20)
+    ref = json.loads(bytes(z["stats"]).decode())
+    assert np.array_equal(part.assign, z["assign"])
+    assert part.num_parts == int(z["num_parts"])
+    assert st.levels == ref["levels"] and st.connectivity_trace == ref["trace"]
+
+
+def test_kernel_seams_match_reference():
+    from paper_2604_14411_b200 import kernels as K
+
+    z = load_npz("kernels.npz")
+    d = dp()
+    for t in range(int(z["count"])):
+        p = f"k{t}_"
+        g = graph([z[f"{p}in_{k}"] for k in ("n", "w", "so", "sd", "do", "dd")])
+        w = g.edge_weight
+        assert np.array_equal(g.edge_pins.data, z[p + "pin_dat"]) and np.array_equal(g.node_inc.data, z[p + "inc_dat"])
+        assert np.array_equal(g.node_in.offsets, z[p + "in_off"]) and np.array_equal(g.node_in.data, z[p + "in_dat"])
+        assert np.array_equal(g.node_out.data, z[p + "out_dat"])
+        nb = d.materialize_neighbors(g)
+        assert np.array_equal(nb.offsets, z[p + "nb_off"]) and np.array_equal(nb.data, z[p + "nb_dat"])
+        for batch in (1, 7, 32):
+            hist = K.fill_histograms(g.node_inc.offsets, g.node_inc.data, g.edge_pins.offsets, g.edge_pins.data,
+                                     w, nb.offsets, nb.data, batch)
+            assert np.array_equal(hist, z[p + "hist"])
+        pair, score = K.select_first_valid(z[p + "order"], nb.offsets, nb.data, hist, g.node_size,
+                                           g.node_in.offsets, g.node_in.data, int(z[p + "omega"]),
+                                           int(z[p + "delta"]))
+        assert np.array_equal(pair, z[p + "pair"]) and np.array_equal(score, z[p + "score"])
+        assert np.array_equal(K.resolve_matching(pair, score), z[p + "match"])
+        assign = z[p + "assign"]
+        assert K.connectivity_value(g.edge_pins.offsets, g.edge_pins.data, w, assign) == float(z[p + "conn"])
+        kk = int(z[p + "K"])
+        pins, pins_in = K.compute_pins(g.edge_pins.offsets, g.edge_pins.data, g.edge_dst.offsets, g.edge_dst.data,
+                                       assign, kk)
+        assert np.array_equal(pins, z[p + "pins"]) and np.array_equal(pins_in, z[p + "pins_in"])
+        assert np.array_equal(d.partition_sizes(g, assign, kk), z[p + "psz"])
+        assert np.array_equal(d.distinct_inbound_sizes(g, assign, kk), z[p + "pinb"])
+        tgt, gain = K.propose_moves(g.node_inc.offsets, g.node_inc.data, g.edge_pins.offsets, g.edge_pins.data, w,
+                                    pins, assign, z[p + "psz"], g.node_size, int(z[p + "omega"]))
+        assert np.array_equal(tgt, z[p + "target"]) and np.array_equal(gain, z[p + "gain"])
+        node = z[p + "node"]
+        gseq = K.sequence_gains(g.node_inc.offsets, g.node_inc.data, g.edge_pins.offsets, g.edge_pins.data, w, pins,
+                                node, assign[node], tgt[node], gain[node], z[p + "pos"])
+        assert np.array_equal(gseq, z[p + "gseq"])
+
+
+# ---------------------------------------------------------------------------
+# H1 known answers (the reference's own tests)
+# ---------------------------------------------------------------------------
+def test_h1_frozen(h1):
+    d = dp()
+    from paper_2604_14411_b200 import kernels as K
+
+    assert h1.node_in.to_lists() == [[2], [0], [0, 1], []]
+    assert h1.node_out.to_lists() == [[0], [1], [], [2]]
+    assert h1.node_inc.to_lists() == [[0, 2], [0, 1], [0, 1], [2]]
+    for rho, want in (([0, 0, 1, 1], 4.0), ([0, 1, 2, 3], 5.0), ([0, 1, 1, 0], 1.0), ([0, 0, 0, 0], 0.0)):
+        assert d.connectivity(h1, d.Partitioning(np.array(rho), 4)) == want
+    assert d.partition_sizes(h1, np.array([0, 0, 1, 1], np.int32), 2).tolist() == [2, 2]
+    assert d.distinct_inbound_sizes(h1, np.array([0, 0, 1, 1], np.int32), 2).tolist() == [2, 2]
+    assert d.materialize_neighbors(h1).to_lists() == [[1, 2, 3], [0, 2], [0, 1], [0]]
+    assert K.resolve_matching(np.array([1, 0, 1]), np.array([5.0] * 3)).tolist() == [1, 0, 2]
+    assert K.resolve_matching(np.array([1, 2, 1]), np.array([3.0, 7.0, 7.0])).tolist() == [0, 2, 1]
+    with pytest.raises(d.MatchingInvariantError):
+        K.resolve_matching(np.array([1, 2, 0]), np.ones(3))
+    assert K.union_size_sorted(np.array([1, 4, 9]), np.array([4, 5])) == 4
+    assert K.union_size_sorted(np.array([1, 4, 9]), np.zeros(0)) == 3
+    part, st = d.partition(h1, d.Config(d.Constraints(2, 4)))
+    assert part.assign.tolist() == [0, 1, 1, 0] and part.num_parts == 2 and st.num_partitions == 2
+    assert st.levels == [{"nodes": 4, "edges": 3, "pins": 7}, {"nodes": 2, "edges": 3, "pins": 6}]
+    assert st.connectivity_trace == [[1.0], [1.0]] and st.phase_ms == {}
+    part, _ = d.partition(h1, d.Config(d.Constraints(4, 3)))
+    assert part.num_parts == 1 and part.assign.tolist() == [0, 0, 0, 0]
+    with pytest.raises(d.InfeasibleError, match="inbound"):
+        d.partition(h1, d.Config(d.Constraints(4, 1)))
+    with pytest.raises(d.InfeasibleError):
+        d.partition(h1, d.Config(d.Constraints(0, 4)))
+    with pytest.raises(d.InfeasibleError):
+        d.partition(h1, d.Config(d.Constraints(4, -1)))
+    assert d.check_validity(h1, d.Partitioning(np.array([0, 0, 0, 0]), 1), d.Constraints(2, 1)) == [
+        d.Violation(0, "size", 4, 2), d.Violation(0, "inbound", 3, 1)]
+    d.check_feasibility(h1, d.Constraints(1, 2))
+    with pytest.raises(d.InfeasibleError):
+        d.check_feasibility(h1, d.Constraints(1, 1))
+
+
+# ---------------------------------------------------------------------------
+# randomized parity vs the oracle, edge cases, errors
+# ---------------------------------------------------------------------------
+def test_random_instances_vs_oracle():
+    rs = np.random.RandomState(113)
+    for trial in range(30):
+        n = int(rs.randint(5, 700))
+        omega = int(rs.choice([2, 4, 8, 16, 32, 64]))
+        g, c = make_instance(n, int(float(rs.choice([1.0, 1.5, 2.5])) * n), int(rs.choice([2, 3, 5, 8])),
+                             seed=7000 + trial, omega=omega, delta_slack=int(rs.randint(0, 2 * omega)))
+        assert_same_as_oracle(g, c.max_size, c.max_inbound)
+
+
+def test_max_rounds_and_nonunit_node_sizes():
+    d = dp()
+    rs = np.random.RandomState(5)
+    for trial in range(6):
+        n = int(rs.randint(20, 300))
+        g0, c = make_instance(n, 2 * n, 5, seed=9100 + trial, omega=32, delta_slack=20)
+        sizes = rs.randint(1, 4, size=n).astype(np.int32)
+        g = d.Hypergraph._from_csr(n, g0.edge_weight, g0.edge_src, g0.edge_dst, node_size=sizes)
+        for rounds in (1, 3):
+            assert_same_as_oracle(g, 32, c.max_inbound, max_rounds=rounds)
+
+
+def test_layered_snn_vs_oracle():
+    from paper_2604_14411_b200 import workloads as W
+
+    for (layers, width, omega) in ((4, 256, 128), (6, 200, 256)):
+        assert_same_as_oracle(graph(W.layered_snn(layers, width, fanout=32, window=128, seed=layers)), omega, 4096)
+
+
+def test_power_law_vs_oracle():
+    from paper_2604_14411_b200 import workloads as W
+
+    arr = W.power_law(3000, 3000, k_max=300, seed=1)
+    indeg = int(np.bincount(arr[5], minlength=3000).max())
+    assert_same_as_oracle(graph(arr), 64, max(indeg, 256))
+
+
+def test_degenerate_inputs():
+    d = dp()
+    # no edges: every node is its own part, connectivity 0
+    g = d.Hypergraph._from_csr(5, np.zeros(0), d.CsrSets.from_lists([]), d.CsrSets.from_lists([]))
+    part, st = d.partition(g, d.Config(d.Constraints(2, 0)))
+    assert part.assign.tolist() == [0, 1, 2, 3, 4] and st.connectivity_trace == [[0.0]]
+    # single-pin edges, a node on both sides, isolated nodes, zero weights
+    g = d.Hypergraph.from_edges(6, [3.0, 1.0, 0.0, 2.0], [[0], [1], [], [2]], [[0], [], [3], [1, 0]])
+    assert_same_as_oracle(g, 2, 3)
+    assert_same_as_oracle(g, 6, 3)
+    # empty graph
+    g = d.Hypergraph._from_csr(0, np.zeros(0), d.CsrSets.from_lists([]), d.CsrSets.from_lists([]))
+    part, st = d.partition(g, d.Config(d.Constraints(2, 0)))
+    assert len(part.assign) == 0 and part.num_parts == 0 and st.num_partitions == 0
+
+
+def test_max_levels_guard_message():
+    d = dp()
+    g, c = make_instance(60, 90, 4, seed=1, omega=8)
+    with pytest.raises(d.DhgError, match="max_levels"):
+        d.partition(g, d.Config(c, max_levels=1))
+
+
+def test_non_integral_weights_are_rejected_loudly():
+    d = dp()
+    g = d.Hypergraph.from_edges(3, [0.5, 1.0], [[0], [1]], [[1], [2]])
+    with pytest.raises(d.DhgError, match="non-integral"):
+        d.partition(g, d.Config(d.Constraints(2, 2)))
+
+
+def test_timings_and_determinism():
+    d = dp()
+    g, c = make_instance(400, 600, 5, seed=33, omega=8)
+    p1, s1 = d.partition(g, d.Config(c))
+    p2, s2 = d.partition(g, d.Config(c), timings=True)
+    assert np.array_equal(p1.assign, p2.assign) and s1.levels == s2.levels
+    assert set(s2.phase_ms) == {"coarsen", "refine", "total"} and all(v >= 0 for v in s2.phase_ms.values())
+
+
+def test_gpu_smoke_entry():
+    import __graft_entry__
+
+    __graft_entry__.smoke()
+
+
+# ---------------------------------------------------------------------------
+# full-size workload (C2): size-independent properties
+# ---------------------------------------------------------------------------
+def test_c2_full_size_properties():
+    from paper_2604_14411_b200 import workloads as W
+
+    d = dp()
+    arrs, omega, delta, _ = W.make_config("C2")
+    g = graph(arrs)
+    p1, s1 = d.partition(g, d.Config(d.Constraints(omega, delta), max_levels=1 << 20))
+    assert d.check_validity(g, p1, d.Constraints(omega, delta)) == []
+    assert np.array_equal(np.unique(p1.assign), np.arange(p1.num_parts))
+    assert s1.connectivity_trace[-1][-1] == d.connectivity(g, p1)
+    for tr in s1.connectivity_trace:
+        assert all(b <= a for a, b in zip(tr, tr[1:]))
+    sizes = [lv["nodes"] for lv in s1.levels]
+    assert all(b < a for a, b in zip(sizes, sizes[1:]))
+    assert all(lv["edges"] == g.num_edges for lv in s1.levels)
+    p2, s2 = d.partition(g, d.Config(d.Constraints(omega, delta), max_levels=1 << 20))
+    assert np.array_equal(p1.assign, p2.assign) and s1.to_dict() == s2.to_dict()
