@@ -65,15 +65,21 @@ struct ScoreArgs {
     int64_t omega, delta;
     int32_t *pair;
     double *score;
-    int32_t *next;       // work counter
-    int32_t *big_list;   // nodes escalated to the block tier
+    int32_t *next;        // work counter
+    int32_t *big_list;    // nodes escalated to the global dense tier
     int32_t *big_count;
+    int32_t *heavy_list;  // nodes for the block tier (many incident h-edges)
+    int32_t *heavy_count;
 };
 
 constexpr int SS_WARPS = 8;
 constexpr int SS_CAP = 1024;   // hash slots per warp (power of two)
 constexpr int SS_LIMIT = 720;  // distinct neighbours before escalation
-constexpr int SS_SMEM = SS_WARPS * SS_CAP * (4 + 8);
+constexpr int SS_HEAVY_INC = 192;  // incident h-edges above which a block takes the node
+// accumulator: 32-bit when the total weight < 2^32 (native shared atomics;
+// 64-bit shared atomicAdd is a CAS spin loop on sm_100a), else 64-bit
+template <class Acc>
+constexpr int ss_smem() { return SS_WARPS * SS_CAP * (4 + (int)sizeof(Acc)); }
 
 __device__ __forceinline__ uint32_t hslot(int32_t m) { return ((uint32_t)m * 2654435761u) >> (32 - 10); }
 
@@ -92,33 +98,38 @@ __device__ __forceinline__ bool warp_union_ok(const ScoreArgs &a, int32_t n, int
     return nn + nm - common <= a.delta;
 }
 
+template <class Acc>
 __global__ void __launch_bounds__(SS_WARPS * 32) k_score_warp(ScoreArgs a) {
-    extern __shared__ unsigned char smem[];
-    unsigned long long *svals = (unsigned long long *)smem;
+    extern __shared__ unsigned long long smem_u64[];
+    Acc *svals = (Acc *)smem_u64;
     int32_t *skeys = (int32_t *)(svals + SS_WARPS * SS_CAP);
     __shared__ int32_t snk[SS_WARPS];
     __shared__ volatile int32_t sover[SS_WARPS];
     const int w = warp_id(), lane = lane_id();
     int32_t *keys = skeys + w * SS_CAP;
-    unsigned long long *vals = svals + w * SS_CAP;
+    Acc *vals = svals + w * SS_CAP;
     while (true) {
         int node = 0;
         if (lane == 0) node = atomicAdd(a.next, 1);
         node = __shfl_sync(FULL_MASK, node, 0);
         if (node >= a.N) break;
+        const int64_t ilo = a.inc_off[node], ihi = a.inc_off[node + 1];
+        if (ihi - ilo > SS_HEAVY_INC) {  // hub: a whole block per node
+            if (lane == 0) a.heavy_list[atomicAdd(a.heavy_count, 1)] = node;
+            continue;
+        }
         for (int s = lane; s < SS_CAP; s += 32) {
             keys[s] = -1;
-            vals[s] = 0ull;
+            vals[s] = 0;
         }
         if (lane == 0) {
             snk[w] = 0;
             sover[w] = 0;
         }
         __syncwarp();
-        const int64_t ilo = a.inc_off[node], ihi = a.inc_off[node + 1];
         warp_for_pins(a.inc_dat, ilo, ihi, 0, 32, a.pin_off, a.pin_dat, [&](int32_t e, int32_t m) {
             if (m == node || sover[w]) return;
-            const unsigned long long we = (unsigned long long)a.wi[e];
+            const Acc we = (Acc)a.wi[e];
             uint32_t h = hslot(m);
             for (int probe = 0; probe < SS_CAP; probe++) {
                 const int slot = (h + probe) & (SS_CAP - 1);
@@ -141,7 +152,7 @@ __global__ void __launch_bounds__(SS_WARPS * 32) k_score_warp(ScoreArgs a) {
         });
         __syncwarp();
         if (sover[w]) {
-            if (lane == 0) a.big_list[atomicAdd(a.big_count, 1)] = node;
+            if (lane == 0) a.heavy_list[atomicAdd(a.heavy_count, 1)] = node;
             __syncwarp();
             continue;
         }
@@ -197,12 +208,160 @@ __global__ void __launch_bounds__(SS_WARPS * 32) k_score_warp(ScoreArgs a) {
     }
 }
 
+// Block tier: one 1024-thread block per heavy node, 16K-slot shared hash
+// table (warps flatten the pins of 32 incident h-edges at a time); nodes
+// with more distinct neighbours than the table holds go to the dense tier.
+constexpr int SH_THREADS = 1024;
+constexpr int SH_CAP = 16384;
+constexpr int SH_LIMIT = 12288;
+template <class Acc>
+constexpr int sh_smem() { return SH_CAP * (4 + (int)sizeof(Acc)); }
+
+template <class Acc>
+__global__ void __launch_bounds__(SH_THREADS) k_score_heavy(ScoreArgs a) {
+    extern __shared__ unsigned long long smem_u64[];
+    Acc *vals = (Acc *)smem_u64;
+    int32_t *keys = (int32_t *)(vals + SH_CAP);
+    __shared__ int32_t snk;
+    __shared__ volatile int32_t sover;
+    __shared__ long long r_v[SH_THREADS / 32];
+    __shared__ int32_t r_k[SH_THREADS / 32], r_s[SH_THREADS / 32];
+    __shared__ long long r_c[SH_THREADS / 32];
+    const int w = warp_id(), lane = lane_id(), nw = SH_THREADS / 32;
+    const int nheavy = *a.heavy_count;
+    for (int t = blockIdx.x; t < nheavy; t += gridDim.x) {
+        const int32_t node = a.heavy_list[t];
+        for (int s = threadIdx.x; s < SH_CAP; s += SH_THREADS) {
+            keys[s] = -1;
+            vals[s] = 0;
+        }
+        if (threadIdx.x == 0) {
+            snk = 0;
+            sover = 0;
+        }
+        __syncthreads();
+        const int64_t ilo = a.inc_off[node], ihi = a.inc_off[node + 1];
+        warp_for_pins(a.inc_dat, ilo, ihi, (int64_t)w * 32, (int64_t)nw * 32, a.pin_off, a.pin_dat,
+                      [&](int32_t e, int32_t m) {
+                          if (m == node || sover) return;
+                          const Acc we = (Acc)a.wi[e];
+                          uint32_t h = ((uint32_t)m * 2654435761u) >> (32 - 14);
+                          for (int probe = 0; probe < SH_CAP; probe++) {
+                              const int slot = (h + probe) & (SH_CAP - 1);
+                              int k = keys[slot];
+                              if (k == -1) {
+                                  int prev = atomicCAS(&keys[slot], -1, m);
+                                  if (prev == -1) {
+                                      if (atomicAdd(&snk, 1) >= SH_LIMIT) sover = 1;
+                                      k = m;
+                                  } else {
+                                      k = prev;
+                                  }
+                              }
+                              if (k == m) {
+                                  atomicAdd(&vals[slot], we);
+                                  return;
+                              }
+                          }
+                          sover = 1;
+                      });
+        __syncthreads();
+        if (sover) {
+            if (threadIdx.x == 0) a.big_list[atomicAdd(a.big_count, 1)] = node;
+            __syncthreads();
+            continue;
+        }
+        const int64_t szn = a.size[node];
+        for (int s = threadIdx.x; s < SH_CAP; s += SH_THREADS) {
+            int k = keys[s];
+            if (k >= 0 && szn + a.size[k] > a.omega) keys[s] = -2;
+        }
+        __syncthreads();
+        int32_t best_m = -1;
+        long long best_v = 0;
+        while (true) {
+            long long bv = -1;
+            int32_t bk = -1, bs = -1;
+            for (int s = threadIdx.x; s < SH_CAP; s += SH_THREADS) {
+                int k = keys[s];
+                if (k >= 0) {
+                    long long v = (long long)vals[s];
+                    if (v > bv || (v == bv && k > bk)) {
+                        bv = v;
+                        bk = k;
+                        bs = s;
+                    }
+                }
+            }
+#pragma unroll
+            for (int d = 16; d > 0; d >>= 1) {
+                long long ov = __shfl_xor_sync(FULL_MASK, bv, d);
+                int32_t ok = __shfl_xor_sync(FULL_MASK, bk, d);
+                int32_t os = __shfl_xor_sync(FULL_MASK, bs, d);
+                if (ov > bv || (ov == bv && ok > bk)) {
+                    bv = ov;
+                    bk = ok;
+                    bs = os;
+                }
+            }
+            if (lane == 0) {
+                r_v[w] = bv;
+                r_k[w] = bk;
+                r_s[w] = bs;
+            }
+            __syncthreads();
+            bv = r_v[0];
+            bk = r_k[0];
+            bs = r_s[0];
+            for (int j = 1; j < nw; j++)
+                if (r_v[j] > bv || (r_v[j] == bv && r_k[j] > bk)) {
+                    bv = r_v[j];
+                    bk = r_k[j];
+                    bs = r_s[j];
+                }
+            __syncthreads();
+            if (bk < 0) break;
+            const int64_t nlo = a.in_off[node], nn = a.in_off[node + 1] - nlo;
+            const int64_t mlo = a.in_off[bk], nm = a.in_off[bk + 1] - mlo;
+            bool ok = true;
+            if (nn + nm > a.delta) {
+                const bool ns = nn <= nm;
+                const int32_t *sp = a.in_dat + (ns ? nlo : mlo);
+                const int32_t *lp = a.in_dat + (ns ? mlo : nlo);
+                const int64_t cs = ns ? nn : nm, cl = ns ? nm : nn;
+                long long common = 0;
+                for (int64_t i = threadIdx.x; i < cs; i += SH_THREADS) common += bsearch_dev(lp, 0, cl, sp[i]) >= 0;
+                common = warp_sum(common);
+                if (lane == 0) r_c[w] = common;
+                __syncthreads();
+                long long tot = 0;
+                for (int j = 0; j < nw; j++) tot += r_c[j];
+                __syncthreads();
+                ok = nn + nm - tot <= a.delta;
+            }
+            if (ok) {
+                best_m = bk;
+                best_v = bv;
+                break;
+            }
+            if (threadIdx.x == 0) keys[bs] = -2;
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            a.pair[node] = best_m;
+            a.score[node] = best_m >= 0 ? (double)best_v : 0.0;
+        }
+        __syncthreads();
+    }
+}
+
 // Block tier for nodes with many distinct neighbours: a dense per-block
 // histogram over all node ids in global memory (L2-resident), restored to
 // "untouched" (-1) after each node.
 constexpr int SB_THREADS = 512;
 __global__ void __launch_bounds__(SB_THREADS) k_score_block(ScoreArgs a, long long *dense_all, int32_t *touched_all,
-                                                             long long *cval_all) {
+                                                             long long *cval_all, int32_t n_real) {
+    (void)n_real;
     __shared__ int32_t s_nt;
     __shared__ long long s_bv[SB_THREADS / 32];
     __shared__ int32_t s_bk[SB_THREADS / 32];
@@ -324,43 +483,67 @@ __global__ void k_fill_ll(long long *p, long long v, int64_t n) {
 
 }  // namespace
 
+void score_scratch_init(Ctx &c, ScoreScratch &s, int64_t n_cap) {
+    s.cap = std::max<int64_t>(n_cap, 1);
+    s.blocks = 16;
+    while (s.blocks > 1 && (int64_t)s.blocks * s.cap * 20 > (2ll << 30)) s.blocks >>= 1;
+    s.dense = c.alloc<long long>((int64_t)s.blocks * s.cap);
+    s.cval = c.alloc<long long>((int64_t)s.blocks * s.cap);
+    s.touched = c.alloc<int32_t>((int64_t)s.blocks * s.cap);
+    s.big = c.alloc<int32_t>(s.cap);
+    s.heavy = c.alloc<int32_t>(s.cap);
+    s.ctr = c.alloc<int32_t>(3);
+    k_fill_ll<<<(unsigned)cdiv((int64_t)s.blocks * s.cap, 256), 256, 0, c.stream>>>(s.dense, -1ll,
+                                                                                   (int64_t)s.blocks * s.cap);
+    DHGP_LAUNCHED(c);
+}
+
+void score_scratch_release(Ctx &c, ScoreScratch &s) {
+    c.free(s.dense);
+    c.free(s.cval);
+    c.free(s.touched);
+    c.free(s.big);
+    c.free(s.heavy);
+    c.free(s.ctr);
+    s = ScoreScratch();
+}
+
 void score_select(Ctx &c, const DLevel &L, const DWeights &W, int64_t omega, int64_t delta, int32_t *pair,
-                  double *score) {
+                  double *score, ScoreScratch &s) {
     if (L.N == 0) return;
-    KScope ks(c, "score_select", (double)(16.0 * L.U + 24.0 * L.N));
+    KScope ks(c, "score_select", (double)(16.0 * L.U + 24.0 * L.N), L.N);
     static bool attr = false;
     if (!attr) {
-        DHGP_CUDA(cudaFuncSetAttribute(k_score_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, SS_SMEM));
+        DHGP_CUDA(cudaFuncSetAttribute(k_score_warp<unsigned>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       ss_smem<unsigned>()));
+        DHGP_CUDA(cudaFuncSetAttribute(k_score_warp<unsigned long long>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, ss_smem<unsigned long long>()));
+        DHGP_CUDA(cudaFuncSetAttribute(k_score_heavy<unsigned>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       sh_smem<unsigned>()));
+        DHGP_CUDA(cudaFuncSetAttribute(k_score_heavy<unsigned long long>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, sh_smem<unsigned long long>()));
         attr = true;
     }
-    int32_t *ctr = c.alloc<int32_t>(2);
-    int32_t *big = c.alloc<int32_t>(L.N);
-    c.zero(ctr, 2);
+    c.zero(s.ctr, 3);
     ScoreArgs a{L.N, L.inc_off, L.inc_dat, L.pin_off, L.pin_dat, W.wi, L.size, L.in_off, L.in_dat, omega, delta,
-                pair, score, ctr, big, ctr + 1};
+                pair, score, s.ctr, s.big, s.ctr + 1, s.heavy, s.ctr + 2};
     int blocks = (int)std::min<int64_t>(cdiv(L.N, SS_WARPS), (int64_t)c.num_sms * 2);
-    k_score_warp<<<blocks, SS_WARPS * 32, SS_SMEM, c.stream>>>(a);
+    if (W.wsum < (1ll << 32))
+        k_score_warp<unsigned><<<blocks, SS_WARPS * 32, ss_smem<unsigned>(), c.stream>>>(a);
+    else
+        k_score_warp<unsigned long long><<<blocks, SS_WARPS * 32, ss_smem<unsigned long long>(), c.stream>>>(a);
     DHGP_LAUNCHED(c);
-    int32_t nbig = 0;
-    c.d2h(&nbig, ctr + 1, 1);
-    c.sync();
-    if (nbig > 0) {
-        int g = (int)std::min<int64_t>(nbig, 64);
-        // keep the dense scratch within ~2 GB
-        while (g > 1 && (int64_t)g * L.N * 20 > (2ll << 30)) g >>= 1;
-        long long *dense = c.alloc<long long>((int64_t)g * L.N);
-        long long *cval = c.alloc<long long>((int64_t)g * L.N);
-        int32_t *touched = c.alloc<int32_t>((int64_t)g * L.N);
-        k_fill_ll<<<(unsigned)cdiv((int64_t)g * L.N, 256), 256, 0, c.stream>>>(dense, -1ll, (int64_t)g * L.N);
-        DHGP_LAUNCHED(c);
-        k_score_block<<<g, SB_THREADS, 0, c.stream>>>(a, dense, touched, cval);
-        DHGP_LAUNCHED(c);
-        c.free(dense);
-        c.free(cval);
-        c.free(touched);
-    }
-    c.free(ctr);
-    c.free(big);
+    // heavy tier: reads the escalation count on device, exits when zero
+    if (W.wsum < (1ll << 32))
+        k_score_heavy<unsigned><<<c.num_sms, SH_THREADS, sh_smem<unsigned>(), c.stream>>>(a);
+    else
+        k_score_heavy<unsigned long long><<<c.num_sms, SH_THREADS, sh_smem<unsigned long long>(), c.stream>>>(a);
+    DHGP_LAUNCHED(c);
+    // dense tier: reads the escalation count on device, exits when zero;
+    // dense rows have stride s.cap and are restored to -1 after each node
+    a.N = (int32_t)s.cap;
+    k_score_block<<<s.blocks, SB_THREADS, 0, c.stream>>>(a, s.dense, s.touched, s.cval, L.N);
+    DHGP_LAUNCHED(c);
 }
 
 // ===========================================================================
@@ -381,7 +564,7 @@ __device__ __forceinline__ bool claimant(const int32_t *pair, int32_t v) {
 }
 
 __global__ void k_match_claim1(int32_t N, const int32_t *pair, const double *score, unsigned long long *best,
-                               int32_t *flags) {
+                               int64_t *status) {
     int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= N) return;
     int32_t p = pair[v];
@@ -391,7 +574,7 @@ __global__ void k_match_claim1(int32_t N, const int32_t *pair, const double *sco
     // (score, id) order must strictly improve (hist symmetry + first-valid
     // selection); a violation triggers the exact sequential check.
     if (q >= 0 && !is_cyc(pair, p) && !(score[p] > score[v] || (score[p] == score[v] && q > (int32_t)v)))
-        flags[0] = 1;
+        status[1] = 1;
     if (!is_cyc(pair, p)) atomicMax(&best[p], score_bits(score[v]));
 }
 
@@ -411,7 +594,7 @@ __device__ __forceinline__ bool won(const int32_t *pair, const int32_t *claim, i
 constexpr int kWalkLimit = 64;
 
 __global__ void k_match_final(int32_t N, const int32_t *pair, const int32_t *claim, const int32_t *runlen,
-                              int32_t *match, uint8_t *isrep, unsigned long long *npairs, int32_t *flags) {
+                              int32_t *match, uint8_t *isrep, int64_t *status) {
     __shared__ int64_t sh[33];
     int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int64_t moved = 0;
@@ -426,7 +609,7 @@ __global__ void k_match_final(int32_t N, const int32_t *pair, const int32_t *cla
                 r++;
                 u = pair[u];
                 if (r > kWalkLimit) {
-                    flags[1] = 1;
+                    status[2] = 1;
                     break;
                 }
             }
@@ -442,7 +625,7 @@ __global__ void k_match_final(int32_t N, const int32_t *pair, const int32_t *cla
         moved = m != (int32_t)v;
     }
     int64_t t = block_sum<int64_t>(moved, sh);
-    if (threadIdx.x == 0 && t) atomicAdd(npairs, (unsigned long long)t);
+    if (threadIdx.x == 0 && t) atomicAdd((unsigned long long *)&status[0], (unsigned long long)t);
 }
 
 __global__ void k_pj_init(int32_t N, const int32_t *pair, const int32_t *claim, int32_t *r, int32_t *nxt) {
@@ -486,31 +669,28 @@ __global__ void k_cycle_check(int32_t N, const int32_t *pair, int8_t *state, int
 }
 }  // namespace
 
-int64_t resolve_matching(Ctx &c, int32_t N, const int32_t *pair, const double *score, int32_t *match,
-                         uint8_t *isrep) {
-    if (N == 0) return 0;
+void launch_matching(Ctx &c, int32_t N, const int32_t *pair, const double *score, int32_t *match, uint8_t *isrep,
+                     int32_t *claim, int64_t *d_status) {
+    if (N == 0) return;
     KScope ks(c, "matching", 32.0 * N);
     unsigned long long *best = c.alloc<unsigned long long>(N);
-    int32_t *claim = c.alloc<int32_t>(N);
-    unsigned long long *npairs = c.alloc<unsigned long long>(1);
-    int32_t *flags = c.alloc<int32_t>(2);
     c.zero(best, N);
     fill_i32(c, claim, -1, N);
-    c.zero(npairs, 1);
-    c.zero(flags, 2);
     const unsigned g = (unsigned)cdiv(N, 256);
-    k_match_claim1<<<g, 256, 0, c.stream>>>(N, pair, score, best, flags);
+    k_match_claim1<<<g, 256, 0, c.stream>>>(N, pair, score, best, d_status);
     DHGP_LAUNCHED(c);
     k_match_claim2<<<g, 256, 0, c.stream>>>(N, pair, score, best, claim);
     DHGP_LAUNCHED(c);
-    k_match_final<<<g, 256, 0, c.stream>>>(N, pair, claim, nullptr, match, isrep, npairs, flags);
+    k_match_final<<<g, 256, 0, c.stream>>>(N, pair, claim, nullptr, match, isrep, d_status);
     DHGP_LAUNCHED(c);
-    int32_t hf[2];
-    unsigned long long hp = 0;
-    c.d2h(hf, flags, 2);
-    c.d2h(&hp, npairs, 1);
-    c.sync();
-    if (hf[0]) {
+    c.free(best);
+}
+
+bool matching_fallbacks(Ctx &c, int32_t N, const int32_t *pair, const double *score, int32_t *match,
+                        uint8_t *isrep, const int32_t *claim, LevelStatus &st) {
+    (void)score;
+    bool redo = false;
+    if (st.bad_cert) {
         int8_t *state = c.alloc<int8_t>(N);
         int32_t *path = c.alloc<int32_t>(N);
         int32_t *clen = c.alloc<int32_t>(1);
@@ -525,9 +705,12 @@ int64_t resolve_matching(Ctx &c, int32_t N, const int32_t *pair, const double *s
         c.free(clen);
         if (hl) throw Error{DHGP_ERR_MATCHING, "pairing cycle of length " + std::to_string(hl) + " (expected 2)"};
     }
-    if (hf[1]) {  // a long run of won claims: pointer jumping
+    if (st.long_run) {  // a long run of won claims: pointer jumping
+        const unsigned g = (unsigned)cdiv(N, 256);
         int32_t *r0 = c.alloc<int32_t>(N), *n0 = c.alloc<int32_t>(N);
         int32_t *r1 = c.alloc<int32_t>(N), *n1 = c.alloc<int32_t>(N);
+        int64_t *status = c.alloc<int64_t>(kStatusWords);
+        c.zero(status, kStatusWords);
         k_pj_init<<<g, 256, 0, c.stream>>>(N, pair, claim, r0, n0);
         DHGP_LAUNCHED(c);
         for (int it = 0; it <= bitlen((uint64_t)N); it++) {
@@ -536,21 +719,34 @@ int64_t resolve_matching(Ctx &c, int32_t N, const int32_t *pair, const double *s
             std::swap(r0, r1);
             std::swap(n0, n1);
         }
-        c.zero(npairs, 1);
-        k_match_final<<<g, 256, 0, c.stream>>>(N, pair, claim, r0, match, isrep, npairs, flags);
+        k_match_final<<<g, 256, 0, c.stream>>>(N, pair, claim, r0, match, isrep, status);
         DHGP_LAUNCHED(c);
-        c.d2h(&hp, npairs, 1);
+        c.d2h(&st.moved, status, 1);
         c.sync();
         c.free(r0);
         c.free(n0);
         c.free(r1);
         c.free(n1);
+        c.free(status);
+        redo = true;
     }
-    c.free(best);
+    return redo;
+}
+
+int64_t resolve_matching(Ctx &c, int32_t N, const int32_t *pair, const double *score, int32_t *match,
+                         uint8_t *isrep) {
+    if (N == 0) return 0;
+    int64_t *status = c.alloc<int64_t>(kStatusWords);
+    int32_t *claim = c.alloc<int32_t>(N);
+    c.zero(status, kStatusWords);
+    launch_matching(c, N, pair, score, match, isrep, claim, status);
+    LevelStatus st;
+    c.d2h((int64_t *)&st, status, kStatusWords);
+    c.sync();
+    c.free(status);
+    matching_fallbacks(c, N, pair, score, match, isrep, claim, st);
     c.free(claim);
-    c.free(npairs);
-    c.free(flags);
-    return (int64_t)(hp / 2);
+    return st.moved / 2;
 }
 
 // ===========================================================================
@@ -572,72 +768,142 @@ __global__ void k_gamma(int32_t N, const int32_t *match, const int64_t *rank, co
         csize[cn] = (int32_t)((int64_t)size[v] + (m != (int32_t)v ? (int64_t)size[m] : 0));
     }
 }
+// gathers the coarse totals into the status words
+__global__ void k_contract_status(int32_t N, int32_t E, const int64_t *rank, const int64_t *so, const int64_t *dof,
+                                  const int64_t *po, const int64_t *io, const int64_t *co, int64_t *status) {
+    if (threadIdx.x || blockIdx.x) return;
+    const int64_t nc = rank[N];
+    status[3] = nc;
+    status[4] = so[E];
+    status[5] = dof[E];
+    status[6] = po[E];
+    status[7] = io[nc];
+    status[8] = co[nc];
+}
 }  // namespace
 
-// gamma-image of every per-h-edge list, sorted and deduplicated
-static void contract_edge_list(Ctx &c, int32_t E, const int64_t *off, const int32_t *dat, int64_t nnz,
-                               const int32_t *gamma, int32_t *tmp, int64_t **out_off, int32_t **out_dat,
-                               int64_t *out_nnz) {
-    int64_t *cnt = c.alloc<int64_t>(E);
-    seg_sort(c, E, off, dat, gamma, tmp);
-    seg_unique_count(c, E, off, tmp, cnt);
-    *out_off = c.alloc<int64_t>((int64_t)E + 1);
-    scan_excl<int64_t>(c, cnt, *out_off, E);
-    c.d2h(out_nnz, *out_off + E, 1);
-    c.sync();
-    *out_dat = c.alloc<int32_t>(*out_nnz);
-    seg_unique_write(c, E, off, tmp, *out_off, *out_dat);
-    c.free(cnt);
-    (void)nnz;
-}
-
-void contract(Ctx &c, DLevel &fine, const int32_t *match, const uint8_t *isrep, DLevel &coarse) {
+void contract_count(Ctx &c, DLevel &fine, const int32_t *match, const uint8_t *isrep, DLevel &coarse,
+                    ContractScratch &s, int64_t *d_status) {
     KScope ks(c, "contract", (double)(16.0 * (fine.Ps + fine.Pd + fine.U) + 24.0 * fine.E + 32.0 * fine.N));
     const int32_t N = fine.N, E = fine.E;
-    int64_t *rank = c.alloc<int64_t>((int64_t)N + 1);
-    scan_excl<uint8_t>(c, isrep, rank, N);
-    int64_t nc64 = 0;
-    c.d2h(&nc64, rank + N, 1);
-    c.sync();
-    const int32_t nc = (int32_t)nc64;
+    s.rank = c.alloc<int64_t>((int64_t)N + 1);
+    scan_excl<uint8_t>(c, isrep, s.rank, N);
+    const int64_t *d_nc = s.rank + N;
     fine.gamma = c.alloc<int32_t>(N);
-    int32_t *ma = c.alloc<int32_t>(nc), *mb = c.alloc<int32_t>(nc);
-    coarse.N = nc;
+    s.ma = c.alloc<int32_t>(N);
+    s.mb = c.alloc<int32_t>(N);
     coarse.E = E;
-    coarse.size = c.alloc<int32_t>(nc);
-    k_gamma<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(N, match, rank, fine.size, fine.gamma, ma, mb, coarse.size);
+    coarse.size = c.alloc<int32_t>(N);  // capacity: the fine node count
+    k_gamma<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(N, match, s.rank, fine.size, fine.gamma, s.ma, s.mb,
+                                                         coarse.size);
     DHGP_LAUNCHED(c);
-    c.free(rank);
     // per-h-edge families: sorted unique gamma image (coarsen.py:163-166)
-    int64_t cap = std::max(fine.Ps, std::max(fine.Pd, fine.U));
-    int32_t *tmp = c.alloc<int32_t>(cap);
-    contract_edge_list(c, E, fine.src_off, fine.src_dat, fine.Ps, fine.gamma, tmp, &coarse.src_off, &coarse.src_dat,
-                       &coarse.Ps);
-    contract_edge_list(c, E, fine.dst_off, fine.dst_dat, fine.Pd, fine.gamma, tmp, &coarse.dst_off, &coarse.dst_dat,
-                       &coarse.Pd);
-    contract_edge_list(c, E, fine.pin_off, fine.pin_dat, fine.U, fine.gamma, tmp, &coarse.pin_off, &coarse.pin_dat,
-                       &coarse.U);
-    c.free(tmp);
-    // per-node families: union of the two members' sorted lists
-    int64_t *cnt = c.alloc<int64_t>(nc);
-    coarse.in_off = c.alloc<int64_t>((int64_t)nc + 1);
-    merge_union_count(c, nc, ma, mb, fine.in_off, fine.in_dat, cnt);
-    scan_excl<int64_t>(c, cnt, coarse.in_off, nc);
-    coarse.inc_off = c.alloc<int64_t>((int64_t)nc + 1);
-    merge_union_count(c, nc, ma, mb, fine.inc_off, fine.inc_dat, cnt);
-    scan_excl<int64_t>(c, cnt, coarse.inc_off, nc);
-    int64_t tot[2];
-    c.d2h(&tot[0], coarse.in_off + nc, 1);
-    c.d2h(&tot[1], coarse.inc_off + nc, 1);
-    c.sync();
-    coarse.Sin = tot[0];
-    coarse.in_dat = c.alloc<int32_t>(tot[0]);
-    coarse.inc_dat = c.alloc<int32_t>(tot[1]);
-    merge_union_write(c, nc, ma, mb, fine.in_off, fine.in_dat, coarse.in_off, coarse.in_dat);
-    merge_union_write(c, nc, ma, mb, fine.inc_off, fine.inc_dat, coarse.inc_off, coarse.inc_dat);
+    s.tmp_src = c.alloc<int32_t>(fine.Ps);
+    s.tmp_dst = c.alloc<int32_t>(fine.Pd);
+    s.tmp_pin = c.alloc<int32_t>(fine.U);
+    int64_t *cnt = c.alloc<int64_t>(E);
+    seg_sort(c, E, fine.src_off, fine.src_dat, fine.gamma, s.tmp_src);
+    seg_unique_count(c, E, fine.src_off, s.tmp_src, cnt);
+    coarse.src_off = c.alloc<int64_t>((int64_t)E + 1);
+    scan_excl<int64_t>(c, cnt, coarse.src_off, E);
+    seg_sort(c, E, fine.dst_off, fine.dst_dat, fine.gamma, s.tmp_dst);
+    seg_unique_count(c, E, fine.dst_off, s.tmp_dst, cnt);
+    coarse.dst_off = c.alloc<int64_t>((int64_t)E + 1);
+    scan_excl<int64_t>(c, cnt, coarse.dst_off, E);
+    seg_sort(c, E, fine.pin_off, fine.pin_dat, fine.gamma, s.tmp_pin);
+    seg_unique_count(c, E, fine.pin_off, s.tmp_pin, cnt);
+    coarse.pin_off = c.alloc<int64_t>((int64_t)E + 1);
+    scan_excl<int64_t>(c, cnt, coarse.pin_off, E);
     c.free(cnt);
-    c.free(ma);
-    c.free(mb);
+    // per-node families: union of the two members' sorted lists
+    int64_t *ncnt = c.alloc<int64_t>(N);
+    coarse.in_off = c.alloc<int64_t>((int64_t)N + 1);
+    merge_union_count(c, N, s.ma, s.mb, fine.in_off, fine.in_dat, ncnt, d_nc);
+    scan_excl<int64_t>(c, ncnt, coarse.in_off, N);
+    coarse.inc_off = c.alloc<int64_t>((int64_t)N + 1);
+    merge_union_count(c, N, s.ma, s.mb, fine.inc_off, fine.inc_dat, ncnt, d_nc);
+    scan_excl<int64_t>(c, ncnt, coarse.inc_off, N);
+    c.free(ncnt);
+    k_contract_status<<<1, 32, 0, c.stream>>>(N, E, s.rank, coarse.src_off, coarse.dst_off, coarse.pin_off,
+                                              coarse.in_off, coarse.inc_off, d_status);
+    DHGP_LAUNCHED(c);
+}
+
+void contract_write(Ctx &c, DLevel &fine, DLevel &coarse, ContractScratch &s, const LevelStatus &st) {
+    KScope ks(c, "contract_write");
+    const int32_t E = fine.E;
+    coarse.N = (int32_t)st.nc;
+    coarse.Ps = st.ps;
+    coarse.Pd = st.pd;
+    coarse.U = st.u;
+    coarse.Sin = st.sin;
+    coarse.src_dat = c.alloc<int32_t>(st.ps);
+    coarse.dst_dat = c.alloc<int32_t>(st.pd);
+    coarse.pin_dat = c.alloc<int32_t>(st.u);
+    coarse.in_dat = c.alloc<int32_t>(st.sin);
+    coarse.inc_dat = c.alloc<int32_t>(st.uinc);
+    seg_unique_write(c, E, fine.src_off, s.tmp_src, coarse.src_off, coarse.src_dat);
+    seg_unique_write(c, E, fine.dst_off, s.tmp_dst, coarse.dst_off, coarse.dst_dat);
+    seg_unique_write(c, E, fine.pin_off, s.tmp_pin, coarse.pin_off, coarse.pin_dat);
+    merge_union_write(c, st.nc, s.ma, s.mb, fine.in_off, fine.in_dat, coarse.in_off, coarse.in_dat);
+    merge_union_write(c, st.nc, s.ma, s.mb, fine.inc_off, fine.inc_dat, coarse.inc_off, coarse.inc_dat);
+    contract_release(c, s);
+}
+
+namespace {
+__global__ void k_members(int32_t N, const int32_t *gamma, int32_t *lo, int32_t *hi) {
+    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= N) return;
+    atomicMin(&lo[gamma[v]], (int32_t)v);
+    atomicMax(&hi[gamma[v]], (int32_t)v);
+}
+__global__ void k_match_of(int32_t N, const int32_t *gamma, const int32_t *lo, const int32_t *hi, int32_t *match,
+                           uint8_t *isrep) {
+    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= N) return;
+    const int32_t a = lo[gamma[v]], b = hi[gamma[v]];
+    match[v] = (int32_t)v == a ? b : a;
+    isrep[v] = (int32_t)v == a;
+}
+}  // namespace
+
+void match_from_gamma(Ctx &c, int32_t N, int32_t nc, const int32_t *gamma, int32_t *match, uint8_t *isrep) {
+    if (N == 0) return;
+    int32_t *lo = c.alloc<int32_t>(nc), *hi = c.alloc<int32_t>(nc);
+    fill_i32(c, lo, 0x7fffffff, nc);
+    fill_i32(c, hi, -1, nc);
+    k_members<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(N, gamma, lo, hi);
+    DHGP_LAUNCHED(c);
+    k_match_of<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(N, gamma, lo, hi, match, isrep);
+    DHGP_LAUNCHED(c);
+    c.free(lo);
+    c.free(hi);
+}
+
+void level_to_stub(Ctx &c, DLevel &L) {
+    int32_t *g = L.gamma;
+    L.gamma = nullptr;
+    DLevel keep;
+    keep.N = L.N;
+    keep.E = L.E;
+    keep.Ps = L.Ps;
+    keep.Pd = L.Pd;
+    keep.U = L.U;
+    keep.Sin = L.Sin;
+    L.release(c);
+    L = keep;
+    L.gamma = g;
+    L.stub = true;
+}
+
+void contract_release(Ctx &c, ContractScratch &s) {
+    c.free(s.ma);
+    c.free(s.mb);
+    c.free(s.tmp_src);
+    c.free(s.tmp_dst);
+    c.free(s.tmp_pin);
+    c.free(s.rank);
+    s = ContractScratch();
 }
 
 }  // namespace dhgp

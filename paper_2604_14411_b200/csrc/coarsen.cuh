@@ -8,16 +8,61 @@ namespace dhgp {
 // its incident h-edges (never written to HBM), candidates in (hist desc,
 // id desc) order, first one passing the size and inbound-union checks.
 // coarsen.py:93-132, _kernels.pyx:47-103.  Requires exact-integer weights.
+// Scratch for the block tier (nodes with too many distinct neighbours for a
+// warp's shared-memory table): dense per-block histograms over all node ids,
+// allocated once per partition for the level-0 node count.
+struct ScoreScratch {
+    int64_t cap = 0;
+    int blocks = 0;
+    long long *dense = nullptr, *cval = nullptr;
+    int32_t *touched = nullptr, *big = nullptr, *heavy = nullptr, *ctr = nullptr;
+};
+void score_scratch_init(Ctx &c, ScoreScratch &s, int64_t n_cap);
+void score_scratch_release(Ctx &c, ScoreScratch &s);
 void score_select(Ctx &c, const DLevel &L, const DWeights &W, int64_t omega, int64_t delta, int32_t *pair,
-                  double *score);
+                  double *score, ScoreScratch &s);
 
-// A7: pseudo-forest -> involution (_kernels.pyx:106-181).  Returns the number
-// of matched pairs (PairingForest.matched_pairs, coarsen.py:54-58); throws
-// DHGP_ERR_MATCHING on a pairing cycle of length != 2.
+// Per-level status words, filled on device and read with ONE host sync.
+struct LevelStatus {
+    int64_t moved;     // nodes with match != self (= 2 x matched pairs)
+    int64_t bad_cert;  // (score, id) monotonicity certificate failed somewhere
+    int64_t long_run;  // a run of won claims longer than the walk limit
+    int64_t nc, ps, pd, u, sin, uinc;  // coarse sizes
+};
+constexpr int kStatusWords = 9;
+
+// A7: pseudo-forest -> involution (_kernels.pyx:106-181), no host sync:
+// status->moved / bad_cert / long_run are written on device.
+void launch_matching(Ctx &c, int32_t N, const int32_t *pair, const double *score, int32_t *match, uint8_t *isrep,
+                     int32_t *claim, int64_t *d_status);
+// Rare exact fallbacks after the sync (pointer jumping for long runs, the
+// reference's sequential cycle check); throws DHGP_ERR_MATCHING on a cycle
+// of length != 2.  Returns true when match/isrep were recomputed.
+bool matching_fallbacks(Ctx &c, int32_t N, const int32_t *pair, const double *score, int32_t *match,
+                        uint8_t *isrep, const int32_t *claim, LevelStatus &st);
+// Synchronous form for the kernel seam: returns matched pairs.
 int64_t resolve_matching(Ctx &c, int32_t N, const int32_t *pair, const double *score, int32_t *match,
                          uint8_t *isrep);
 
-// A9: contraction (coarsen.py:141-173).  Fills fine.gamma and builds coarse.
-void contract(Ctx &c, DLevel &fine, const int32_t *match, const uint8_t *isrep, DLevel &coarse);
+// A9: contraction (coarsen.py:141-173) in two phases around one host sync:
+// contract_count fills fine.gamma, the coarse offsets/sizes and the status
+// totals; contract_write materialises the coarse lists once the sizes are
+// known on the host.
+struct ContractScratch {
+    int32_t *ma = nullptr, *mb = nullptr;
+    int32_t *tmp_src = nullptr, *tmp_dst = nullptr, *tmp_pin = nullptr;
+    int64_t *rank = nullptr;
+};
+void contract_count(Ctx &c, DLevel &fine, const int32_t *match, const uint8_t *isrep, DLevel &coarse,
+                    ContractScratch &s, int64_t *d_status);
+void contract_write(Ctx &c, DLevel &fine, DLevel &coarse, ContractScratch &s, const LevelStatus &st);
+void contract_release(Ctx &c, ContractScratch &s);
+
+// match / isrep of a stored contraction, recovered from its gamma (coarse
+// ids are ranks of each cluster's minimum member): used to rebuild levels
+// that were not kept during coarsening.
+void match_from_gamma(Ctx &c, int32_t N, int32_t nc, const int32_t *gamma, int32_t *match, uint8_t *isrep);
+// Drops a level's lists, keeping gamma and the size metadata.
+void level_to_stub(Ctx &c, DLevel &L);
 
 }  // namespace dhgp

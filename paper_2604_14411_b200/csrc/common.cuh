@@ -103,15 +103,37 @@ struct Ctx {
     void flush_profile();
 };
 
+// DHGP_TRACE=1: every scope is synchronised and printed to stderr as
+// "trace <name> <ms> <tag>" (diagnostics only; serialises the stream)
+bool trace_enabled();
+void trace_print(const char *name, double ms, long long tag);
+
 struct KScope {
     Ctx &c;
     int idx;
     double bytes;
-    KScope(Ctx &ctx, const char *name, double b = 0) : c(ctx), idx(-1), bytes(b) {
+    const char *name;
+    long long tag;
+    cudaEvent_t t0 = nullptr, t1 = nullptr;
+    KScope(Ctx &ctx, const char *nm, double b = 0, long long tg = -1) : c(ctx), idx(-1), bytes(b), name(nm), tag(tg) {
         if (c.profiling) idx = c.kbegin(name);
+        if (trace_enabled()) {
+            cudaEventCreate(&t0);
+            cudaEventCreate(&t1);
+            cudaEventRecord(t0, c.stream);
+        }
     }
     ~KScope() {
         if (idx >= 0) c.kend(idx, bytes);
+        if (t0) {
+            cudaEventRecord(t1, c.stream);
+            cudaEventSynchronize(t1);
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, t0, t1);
+            trace_print(name, ms, tag);
+            cudaEventDestroy(t0);
+            cudaEventDestroy(t1);
+        }
     }
 };
 

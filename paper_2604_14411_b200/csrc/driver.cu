@@ -20,6 +20,16 @@ void set_error(int code, const std::string &msg) {
 }
 const char *last_error() { return g_last_error.c_str(); }
 
+bool trace_enabled() {
+    static int on = -1;
+    if (on < 0) {
+        const char *e = getenv("DHGP_TRACE");
+        on = (e && e[0] == '1') ? 1 : 0;
+    }
+    return on == 1;
+}
+void trace_print(const char *name, double ms, long long tag) { fprintf(stderr, "trace %s %.4f %lld\n", name, ms, tag); }
+
 // ---------------------------------------------------------------------------
 // per-kernel event timing (bench / profiling only)
 // ---------------------------------------------------------------------------
@@ -112,6 +122,41 @@ struct PartitionResult {
     double device_ms = 0;
 };
 
+constexpr size_t kCheckpoint = 16;
+
+// Rebuilds stub levels (lo, hi] by re-running the contraction from the
+// nearest full level below, using the stored gammas (bit-identical).
+static void rebuild_levels(Ctx &c, std::vector<DLevel> &levels, size_t hi) {
+    size_t lo = hi;
+    while (levels[lo].stub) lo--;
+    int64_t *status = c.alloc<int64_t>(kStatusWords);
+    for (size_t j = lo; j < hi; j++) {
+        DLevel &f = levels[j];
+        DLevel &next = levels[j + 1];
+        const int32_t n = f.N;
+        int32_t *match = c.alloc<int32_t>(n);
+        uint8_t *isrep = c.alloc<uint8_t>(n);
+        match_from_gamma(c, n, next.N, f.gamma, match, isrep);
+        c.free(f.gamma);
+        f.gamma = nullptr;
+        DLevel coarse;
+        ContractScratch cs;
+        c.zero(status, kStatusWords);
+        contract_count(c, f, match, isrep, coarse, cs, status);
+        LevelStatus st;
+        c.d2h((int64_t *)&st, status, kStatusWords);
+        c.sync();
+        contract_write(c, f, coarse, cs, st);
+        coarse.gamma = next.gamma;  // the stored map to the level above
+        next.gamma = nullptr;
+        next.release(c);
+        next = coarse;
+        c.free(match);
+        c.free(isrep);
+    }
+    c.free(status);
+}
+
 static double now_ms() {
     return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
@@ -165,30 +210,58 @@ static void run_partition(Ctx &c, const DInput &in, const dhgp_config &cfg, Part
     const double t0 = now_ms();
     const int64_t target = (N0 + omega - 1) / omega;
     // ---- coarsening (driver.py:97-118) -----------------------------------
+    // One host sync per level: scoring, matching and the counting half of the
+    // contraction are queued back to back; the sync reads the matched-pair
+    // count, the fallback flags and the coarse sizes together.  A level with
+    // no pair is discarded (driver.py:104-105).
+    ScoreScratch sscr;
+    int64_t *status = nullptr;
     try {
+        score_scratch_init(c, sscr, N0);
+        status = c.alloc<int64_t>(kStatusWords);
         while (levels.back().N > target) {
             if ((int64_t)levels.size() - 1 >= cfg.max_levels)
                 throw Error{DHGP_ERR_MAX_LEVELS, "coarsening exceeded max_levels=" + std::to_string(cfg.max_levels) +
                                                      " (" + std::to_string(levels.back().N) + " nodes, target " +
                                                      std::to_string(target) + ")"};
-            DLevel &fine = levels.back();
-            const int32_t n = fine.N;
-            int32_t *pair = c.alloc<int32_t>(n), *match = c.alloc<int32_t>(n);
+            const int32_t n = levels.back().N;
+            int32_t *pair = c.alloc<int32_t>(n), *match = c.alloc<int32_t>(n), *claim = c.alloc<int32_t>(n);
             double *score = c.alloc<double>(n);
             uint8_t *isrep = c.alloc<uint8_t>(n);
-            score_select(c, fine, W, omega, delta, pair, score);
-            int64_t npairs = resolve_matching(c, n, pair, score, match, isrep);
-            if (npairs == 0) {
-                c.free(pair);
-                c.free(match);
-                c.free(score);
-                c.free(isrep);
-                break;
-            }
+            c.zero(status, kStatusWords);
+            score_select(c, levels.back(), W, omega, delta, pair, score, sscr);
+            launch_matching(c, n, pair, score, match, isrep, claim, status);
             DLevel coarse;
-            contract(c, levels.back(), match, isrep, coarse);
-            levels.push_back(coarse);
-            if (obs) {
+            ContractScratch cs;
+            contract_count(c, levels.back(), match, isrep, coarse, cs, status);
+            LevelStatus st;
+            c.d2h((int64_t *)&st, status, kStatusWords);
+            c.sync();
+            if (st.bad_cert || st.long_run) {
+                if (matching_fallbacks(c, n, pair, score, match, isrep, claim, st)) {
+                    contract_release(c, cs);
+                    coarse.release(c);
+                    c.free(levels.back().gamma);
+                    levels.back().gamma = nullptr;
+                    c.zero(status, kStatusWords);
+                    contract_count(c, levels.back(), match, isrep, coarse, cs, status);
+                    int64_t moved = st.moved;
+                    c.d2h((int64_t *)&st, status, kStatusWords);
+                    c.sync();
+                    st.moved = moved;
+                }
+            }
+            const bool stop = st.moved == 0;
+            if (stop) {
+                contract_release(c, cs);
+                coarse.release(c);
+                c.free(levels.back().gamma);
+                levels.back().gamma = nullptr;
+            } else {
+                contract_write(c, levels.back(), coarse, cs, st);
+                levels.push_back(coarse);
+            }
+            if (!stop && obs) {
                 DLevel &f = levels[levels.size() - 2];
                 DLevel &cl = levels.back();
                 std::vector<int32_t> hp(n), hm(n), hg(n), hsd(cl.Ps), hdd(cl.Pd), hsz(cl.N);
@@ -224,14 +297,24 @@ static void run_partition(Ctx &c, const DInput &in, const dhgp_config &cfg, Part
             }
             c.free(pair);
             c.free(match);
+            c.free(claim);
             c.free(score);
             c.free(isrep);
+            if (stop) break;
+            // memory: keep every kCheckpoint-th level whole; the others keep
+            // only gamma and are rebuilt from their checkpoint on the way up
+            const size_t fi = levels.size() - 2;
+            if (fi % kCheckpoint != 0) level_to_stub(c, levels[fi]);
         }
     } catch (...) {
         for (auto &L : levels) L.release(c);
         W.release(c);
+        score_scratch_release(c, sscr);
+        c.free(status);
         throw;
     }
+    score_scratch_release(c, sscr);
+    c.free(status);
     const double t1 = now_ms();
     // ---- initial partitioning + uncoarsening (driver.py:121-134) -----------
     const int32_t K = levels.back().N;
@@ -275,6 +358,7 @@ static void run_partition(Ctx &c, const DInput &in, const dhgp_config &cfg, Part
         refine_level(c, levels[L - 1], W, assign, K, omega, delta, cfg.max_rounds, (int32_t)(L - 1), res.trace[0],
                      obs ? &robs : nullptr);
         for (int64_t li = L - 2; li >= 0; li--) {
+            if (levels[li].stub) rebuild_levels(c, levels, (size_t)li);
             DLevel &f = levels[li];
             if (f.N > 0) {
                 k_project<<<(unsigned)cdiv(f.N, 256), 256, 0, c.stream>>>(f.N, f.gamma, assign, assign2);

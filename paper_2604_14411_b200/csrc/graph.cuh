@@ -20,6 +20,7 @@ struct DLevel {
     int32_t *size = nullptr;
     int32_t *gamma = nullptr;  // fine -> coarse map once this level has been contracted
     bool borrowed = false;     // src/dst/size belong to a resident input (level 0)
+    bool stub = false;         // lists dropped (only gamma kept); rebuilt on demand
     void release(Ctx &c) {
         if (!borrowed) {
             c.free(src_off); c.free(dst_off); c.free(src_dat); c.free(dst_dat); c.free(size);

@@ -1,4 +1,6 @@
 // prims.cu — scans, radix sort, per-segment sorts, sorted-set merges.
+#include <climits>
+
 #include "prims.cuh"
 
 namespace dhgp {
@@ -118,6 +120,120 @@ void scan_excl(Ctx &c, const T *in, int64_t *out, int64_t n) {
     DHGP_LAUNCHED(c);
     c.free(partial);
 }
+// running maximum: per-tile maxima, a single-block max-scan over them,
+// then per-tile inclusive max with the carry
+namespace {
+__device__ __forceinline__ int64_t warp_incl_max(int64_t v) {
+    const int lane = lane_id();
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        int64_t o = __shfl_up_sync(FULL_MASK, v, d);
+        if (lane >= d && o > v) v = o;
+    }
+    return v;
+}
+// block inclusive max-scan of one value per thread; carry-in applied
+__device__ __forceinline__ int64_t block_incl_max(int64_t v, int64_t *sh, int64_t *total) {
+    const int lane = lane_id(), w = warp_id(), nw = blockDim.x >> 5;
+    int64_t incl = warp_incl_max(v);
+    if (lane == 31) sh[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+        int64_t x = lane < nw ? sh[lane] : LLONG_MIN;
+        int64_t xi = warp_incl_max(x);
+        int64_t prev = __shfl_up_sync(FULL_MASK, xi, 1);
+        if (lane < nw) sh[lane] = lane == 0 ? LLONG_MIN : prev;
+        if (lane == nw - 1) sh[32] = xi;
+    }
+    __syncthreads();
+    int64_t r = incl > sh[w] ? incl : sh[w];
+    *total = sh[32];
+    __syncthreads();
+    return r;
+}
+__global__ void k_max_reduce(const int64_t *in, int64_t n, int64_t *partial) {
+    __shared__ int64_t sh[33];
+    int64_t base = (int64_t)blockIdx.x * SC_TILE, m = LLONG_MIN;
+    for (int i = 0; i < SC_IPT; i++) {
+        int64_t idx = base + (int64_t)i * SC_BT + threadIdx.x;
+        if (idx < n && in[idx] > m) m = in[idx];
+    }
+    int64_t t;
+    block_incl_max(m, sh, &t);
+    if (threadIdx.x == 0) partial[blockIdx.x] = t;
+}
+__global__ void k_max_partials(int64_t *partial, int64_t ntiles) {
+    // exclusive running max over tiles: the carry into each tile
+    __shared__ int64_t sh[33];
+    __shared__ int64_t incl_s[1024];
+    int64_t carry = LLONG_MIN;
+    for (int64_t base = 0; base < ntiles; base += blockDim.x) {
+        int64_t idx = base + threadIdx.x;
+        int64_t v = idx < ntiles ? partial[idx] : LLONG_MIN;
+        int64_t tot;
+        int64_t incl = block_incl_max(v, sh, &tot);
+        incl_s[threadIdx.x] = incl;
+        __syncthreads();
+        int64_t ex = threadIdx.x ? incl_s[threadIdx.x - 1] : LLONG_MIN;
+        if (carry > ex) ex = carry;
+        __syncthreads();
+        if (idx < ntiles) partial[idx] = ex;
+        if (tot > carry) carry = tot;
+    }
+}
+__global__ void k_max_final(const int64_t *in, int64_t n, const int64_t *partial, int64_t *out) {
+    __shared__ int64_t sh[33];
+    __shared__ int64_t buf[SC_TILE];
+    int64_t base = (int64_t)blockIdx.x * SC_TILE;
+    for (int i = 0; i < SC_IPT; i++) {
+        int64_t idx = base + (int64_t)i * SC_BT + threadIdx.x;
+        buf[i * SC_BT + threadIdx.x] = idx < n ? in[idx] : LLONG_MIN;
+    }
+    __syncthreads();
+    int64_t loc[SC_IPT];
+    int64_t m = LLONG_MIN;
+    for (int i = 0; i < SC_IPT; i++) {
+        loc[i] = buf[threadIdx.x * SC_IPT + i];
+        if (loc[i] > m) m = loc[i];
+    }
+    int64_t tot;
+    int64_t incl = block_incl_max(m, sh, &tot);
+    // exclusive max for this thread = inclusive max of the previous thread
+    __shared__ int64_t prev_of[SC_BT];
+    prev_of[threadIdx.x] = incl;
+    __syncthreads();
+    int64_t run = threadIdx.x ? prev_of[threadIdx.x - 1] : LLONG_MIN;
+    if (partial && partial[blockIdx.x] > run) run = partial[blockIdx.x];
+    for (int i = 0; i < SC_IPT; i++) {
+        if (loc[i] > run) run = loc[i];
+        buf[threadIdx.x * SC_IPT + i] = run;
+    }
+    __syncthreads();
+    for (int i = 0; i < SC_IPT; i++) {
+        int64_t idx = base + (int64_t)i * SC_BT + threadIdx.x;
+        if (idx < n) out[idx] = buf[i * SC_BT + threadIdx.x];
+    }
+}
+}  // namespace
+
+void scan_incl_max(Ctx &c, const int64_t *in, int64_t *out, int64_t n) {
+    if (n <= 0) return;
+    int64_t ntiles = cdiv(n, SC_TILE);
+    if (ntiles == 1) {
+        k_max_final<<<1, SC_BT, 0, c.stream>>>(in, n, nullptr, out);
+        DHGP_LAUNCHED(c);
+        return;
+    }
+    int64_t *partial = c.alloc<int64_t>(ntiles + 1);
+    k_max_reduce<<<(unsigned)ntiles, SC_BT, 0, c.stream>>>(in, n, partial);
+    DHGP_LAUNCHED(c);
+    k_max_partials<<<1, 1024, 0, c.stream>>>(partial, ntiles);
+    DHGP_LAUNCHED(c);
+    k_max_final<<<(unsigned)ntiles, SC_BT, 0, c.stream>>>(in, n, partial, out);
+    DHGP_LAUNCHED(c);
+    c.free(partial);
+}
+
 template void scan_excl<int32_t>(Ctx &, const int32_t *, int64_t *, int64_t);
 template void scan_excl<int64_t>(Ctx &, const int64_t *, int64_t *, int64_t);
 template void scan_excl<uint8_t>(Ctx &, const uint8_t *, int64_t *, int64_t);
@@ -414,10 +530,14 @@ void seg_unique_write(Ctx &c, int64_t nseg, const int64_t *off, const int32_t *t
 // sorted-set union of member lists (warp per coarse node)
 // ===========================================================================
 namespace {
-__global__ void k_merge_count(int64_t nc, const int32_t *ma, const int32_t *mb, const int64_t *off,
-                              const int32_t *dat, int64_t *cnt) {
+__global__ void k_merge_count(int64_t nc_cap, const int64_t *d_nc, const int32_t *ma, const int32_t *mb,
+                              const int64_t *off, const int32_t *dat, int64_t *cnt) {
     const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
     const int lane = lane_id();
+    const int64_t nc = d_nc ? *d_nc : nc_cap;
+    for (int64_t cn = nc + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; cn < nc_cap;
+         cn += (int64_t)gridDim.x * blockDim.x)
+        cnt[cn] = 0;
     for (int64_t cn = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id(); cn < nc; cn += nw) {
         int32_t a = ma[cn], b = mb[cn];
         int64_t alo = off[a], na = off[a + 1] - alo;
@@ -490,10 +610,10 @@ __global__ void k_merge_write(int64_t nc, const int32_t *ma, const int32_t *mb, 
 }  // namespace
 
 void merge_union_count(Ctx &c, int64_t nc, const int32_t *ma, const int32_t *mb, const int64_t *off,
-                       const int32_t *dat, int64_t *cnt) {
+                       const int32_t *dat, int64_t *cnt, const int64_t *d_nc) {
     if (nc <= 0) return;
     int64_t blocks = std::min<int64_t>(cdiv(nc, 8), (int64_t)c.num_sms * 16);
-    k_merge_count<<<(unsigned)blocks, 256, 0, c.stream>>>(nc, ma, mb, off, dat, cnt);
+    k_merge_count<<<(unsigned)blocks, 256, 0, c.stream>>>(nc, d_nc, ma, mb, off, dat, cnt);
     DHGP_LAUNCHED(c);
 }
 void merge_union_write(Ctx &c, int64_t nc, const int32_t *ma, const int32_t *mb, const int64_t *off,

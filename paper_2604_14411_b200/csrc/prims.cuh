@@ -9,6 +9,8 @@ namespace dhgp {
 // out[0..n]: exclusive prefix sums of in[0..n-1]; out[n] = total.
 template <class T>
 void scan_excl(Ctx &c, const T *in, int64_t *out, int64_t n);
+// out[k] = max(in[0..k]) (inclusive running maximum), int64.
+void scan_incl_max(Ctx &c, const int64_t *in, int64_t *out, int64_t n);
 
 // Stable LSD radix sort of (key, val) pairs on key bits [0, bits).
 // n = *d_n when d_n != nullptr (device-resident count, <= n_cap), else n_cap.
@@ -27,9 +29,11 @@ void seg_unique_count(Ctx &c, int64_t nseg, const int64_t *off, const int32_t *t
 void seg_unique_write(Ctx &c, int64_t nseg, const int64_t *off, const int32_t *tmp, const int64_t *out_off,
                       int32_t *out);
 
-// Sorted-set union of two member lists per coarse node.
+// Sorted-set union of two member lists per coarse node.  The count variant
+// takes the node count from device memory (d_nc) when given; nc is then the
+// capacity and cnt[d_nc..nc) is zeroed.
 void merge_union_count(Ctx &c, int64_t nc, const int32_t *ma, const int32_t *mb, const int64_t *off,
-                       const int32_t *dat, int64_t *cnt);
+                       const int32_t *dat, int64_t *cnt, const int64_t *d_nc = nullptr);
 void merge_union_write(Ctx &c, int64_t nc, const int32_t *ma, const int32_t *mb, const int64_t *off,
                        const int32_t *dat, const int64_t *out_off, int32_t *out);
 

@@ -61,6 +61,67 @@ __global__ void k_edge_runs(int32_t E, const int64_t *pin_off, const int32_t *so
     if (threadIdx.x == 0 && t) atomicAdd(conn, (unsigned long long)t);
 }
 
+// warp-per-h-edge variant for wide h-edges (average pins >= 12)
+__global__ void k_edge_runs_warp(int32_t E, const int64_t *pin_off, const int32_t *sorted_parts,
+                                 const int64_t *dst_off, const int32_t *dst_dat, const int32_t *assign,
+                                 const int64_t *wi, Runs r, unsigned long long *conn, int64_t *pinbound) {
+    const int lane = lane_id();
+    const uint32_t lt = (1u << lane) - 1u;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    int64_t contrib = 0;
+    for (int64_t e = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id(); e < E; e += nw) {
+        const int64_t lo = pin_off[e], len = pin_off[e + 1] - lo;
+        int32_t lam = 0;
+        for (int64_t b = 0; b < len; b += 32) {  // heads of the sorted runs
+            const int64_t i = b + lane;
+            int32_t p = 0;
+            bool head = false;
+            if (i < len) {
+                p = sorted_parts[lo + i];
+                head = i == 0 || sorted_parts[lo + i - 1] != p;
+            }
+            const uint32_t bal = __ballot_sync(FULL_MASK, head);
+            if (head) {
+                const int32_t j = lam + __popc(bal & lt);
+                r.part[lo + j] = p;
+                r.cnt[lo + j] = (int32_t)i;  // run start for now
+                r.cin[lo + j] = 0;
+            }
+            lam += __popc(bal);
+        }
+        __syncwarp();
+        for (int32_t j = lane; j < lam; j += 32) {
+            const int32_t st = r.cnt[lo + j];
+            const int32_t nx = j + 1 < lam ? r.cnt[lo + j + 1] : (int32_t)len;
+            __syncwarp(__activemask());
+            r.cnt[lo + j] = nx - st;
+        }
+        __syncwarp();
+        // second pass turns starts into lengths; the loop above may race when
+        // lam > 32, so recompute those from the sorted parts directly
+        if (lam > 32) {
+            for (int32_t j = lane; j < lam; j += 32) {
+                const int32_t p = r.part[lo + j];
+                int64_t a0 = lower_bound_dev<int32_t>(sorted_parts, lo, lo + len, p);
+                int64_t a1 = lower_bound_dev<int32_t>(sorted_parts, lo, lo + len, p + 1);
+                r.cnt[lo + j] = (int32_t)(a1 - a0);
+            }
+            __syncwarp();
+        }
+        if (lane == 0) r.len[e] = lam;
+        for (int64_t q = dst_off[e] + lane; q < dst_off[e + 1]; q += 32) {
+            const int32_t k = run_find(r, lo, lam, assign[dst_dat[q]]);
+            atomicAdd(&r.cin[lo + k], 1);
+        }
+        __syncwarp();
+        if (pinbound)
+            for (int32_t j = lane; j < lam; j += 32)
+                if (r.cin[lo + j] > 0) atomicAdd((unsigned long long *)&pinbound[r.part[lo + j]], 1ull);
+        if (lane == 0 && lam > 0) contrib += wi[e] * (int64_t)(lam - 1);
+    }
+    if (lane == 0 && contrib) atomicAdd(conn, (unsigned long long)contrib);
+}
+
 __global__ void k_part_sizes(int32_t N, const int32_t *assign, const int32_t *size, int64_t *psizes) {
     int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (n < N) atomicAdd((unsigned long long *)&psizes[assign[n]], (unsigned long long)(int64_t)size[n]);
@@ -93,7 +154,10 @@ struct ProposeArgs {
 constexpr int PR_WARPS = 8;
 constexpr int PR_CAP = 512;
 constexpr int PR_LIMIT = 400;
-constexpr int PR_SMEM = PR_WARPS * PR_CAP * (4 + 8);
+constexpr int PR_HEAVY_INC = 128;
+// 32-bit accumulators when the total weight < 2^32 (native shared atomics)
+template <class Acc>
+constexpr int pr_smem() { return PR_WARPS * PR_CAP * (4 + (int)sizeof(Acc)); }
 
 __device__ __forceinline__ uint32_t pslot(int32_t p) { return ((uint32_t)p * 2654435761u) >> (32 - 9); }
 
@@ -102,15 +166,16 @@ __device__ __forceinline__ bool better_gain(int64_t g, int32_t p, int64_t bg, in
     return bp < 0 || g > bg || (g == bg && p < bp);
 }
 
+template <class Acc>
 __global__ void __launch_bounds__(PR_WARPS * 32) k_propose_warp(ProposeArgs a) {
-    extern __shared__ unsigned char smem[];
-    unsigned long long *svals = (unsigned long long *)smem;
+    extern __shared__ unsigned long long smem_u64[];
+    Acc *svals = (Acc *)smem_u64;
     int32_t *skeys = (int32_t *)(svals + PR_WARPS * PR_CAP);
     __shared__ int32_t snk[PR_WARPS];
     __shared__ volatile int32_t sover[PR_WARPS];
     const int w = warp_id(), lane = lane_id();
     int32_t *keys = skeys + w * PR_CAP;
-    unsigned long long *vals = svals + w * PR_CAP;
+    Acc *vals = svals + w * PR_CAP;
     while (true) {
         int node = 0;
         if (lane == 0) node = atomicAdd(a.next, 1);
@@ -121,9 +186,13 @@ __global__ void __launch_bounds__(PR_WARPS * 32) k_propose_warp(ProposeArgs a) {
             if (lane == 0) a.target[node] = -1;
             continue;
         }
+        if (ihi - ilo > PR_HEAVY_INC) {  // many incident h-edges: a whole block takes it
+            if (lane == 0) a.big_list[atomicAdd(a.big_count, 1)] = node;
+            continue;
+        }
         for (int s = lane; s < PR_CAP; s += 32) {
             keys[s] = -1;
-            vals[s] = 0ull;
+            vals[s] = 0;
         }
         if (lane == 0) {
             snk[w] = 0;
@@ -157,7 +226,7 @@ __global__ void __launch_bounds__(PR_WARPS * 32) k_propose_warp(ProposeArgs a) {
                         }
                     }
                     if (k == p) {
-                        atomicAdd(&vals[slot], (unsigned long long)we);
+                        atomicAdd(&vals[slot], (Acc)we);
                         done = true;
                     }
                 }
@@ -199,6 +268,96 @@ __global__ void __launch_bounds__(PR_WARPS * 32) k_propose_warp(ProposeArgs a) {
             a.gain[node] = emit ? bg : 0;
         }
         __syncwarp();
+    }
+}
+
+// Heavy tier for K <= PH_MAXK: one block per node, present[] as a dense
+// shared array indexed by part id plus a touched bitmap (no hashing).
+constexpr int PH_THREADS = 1024;
+constexpr int PH_MAXK = 16384;
+template <class Acc>
+__global__ void __launch_bounds__(PH_THREADS) k_propose_heavy(ProposeArgs a) {
+    extern __shared__ unsigned long long smem_u64[];
+    Acc *pres = (Acc *)smem_u64;
+    uint32_t *touched = (uint32_t *)(pres + a.K);
+    __shared__ long long r_a[PH_THREADS / 32], r_b[PH_THREADS / 32];
+    __shared__ int32_t r_p[PH_THREADS / 32];
+    const int w = warp_id(), lane = lane_id(), nw = PH_THREADS / 32;
+    const int nbig = *a.big_count;
+    const int tw = (a.K + 31) >> 5;
+    for (int t = blockIdx.x; t < nbig; t += gridDim.x) {
+        const int32_t node = a.big_list[t];
+        for (int p = threadIdx.x; p < a.K; p += PH_THREADS) pres[p] = 0;
+        for (int p = threadIdx.x; p < tw; p += PH_THREADS) touched[p] = 0;
+        __syncthreads();
+        const int64_t ilo = a.inc_off[node], ihi = a.inc_off[node + 1];
+        const int32_t ps = a.assign[node];
+        long long total = 0, saving = 0;
+        for (int64_t ii = ilo + threadIdx.x; ii < ihi; ii += PH_THREADS) {
+            const int32_t e = a.inc_dat[ii];
+            const int64_t we = a.wi[e];
+            const int64_t lo = a.pin_off[e];
+            const int32_t lam = a.r.len[e];
+            total += we;
+            for (int32_t j = 0; j < lam; j++) {
+                const int32_t p = a.r.part[lo + j];
+                if (p == ps && a.r.cnt[lo + j] == 1) saving += we;
+                atomicAdd(&pres[p], (Acc)we);
+                atomicOr(&touched[p >> 5], 1u << (p & 31));
+            }
+        }
+        total = warp_sum(total);
+        saving = warp_sum(saving);
+        if (lane == 0) {
+            r_a[w] = total;
+            r_b[w] = saving;
+        }
+        __syncthreads();
+        total = 0;
+        saving = 0;
+        for (int j = 0; j < nw; j++) {
+            total += r_a[j];
+            saving += r_b[j];
+        }
+        const int64_t sz = a.size[node];
+        long long bg = 0;
+        int32_t bp = -1;
+        for (int p = threadIdx.x; p < a.K; p += PH_THREADS) {
+            if (!((touched[p >> 5] >> (p & 31)) & 1u) || p == ps || a.psizes[p] + sz > a.omega) continue;
+            const long long g = saving - (total - (long long)pres[p]);
+            if (better_gain(g, p, bg, bp)) {
+                bg = g;
+                bp = p;
+            }
+        }
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) {
+            long long og = __shfl_xor_sync(FULL_MASK, bg, d);
+            int32_t op = __shfl_xor_sync(FULL_MASK, bp, d);
+            if (op >= 0 && better_gain(og, op, bg, bp)) {
+                bg = og;
+                bp = op;
+            }
+        }
+        __syncthreads();
+        if (lane == 0) {
+            r_a[w] = bg;
+            r_p[w] = bp;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            long long g = r_a[0];
+            int32_t p = r_p[0];
+            for (int j = 1; j < nw; j++)
+                if (r_p[j] >= 0 && better_gain(r_a[j], r_p[j], g, p)) {
+                    g = r_a[j];
+                    p = r_p[j];
+                }
+            const bool emit = p >= 0 && g > 0;
+            a.target[node] = emit ? p : -1;
+            a.gain[node] = emit ? g : 0;
+        }
+        __syncthreads();
     }
 }
 
@@ -313,66 +472,6 @@ __global__ void k_mover_keys(int32_t N, const uint8_t *flags, const int64_t *pos
     }
 }
 
-__global__ void k_build_moves(int32_t M, const uint32_t *sorted_nodes, const int32_t *assign, const int32_t *target,
-                              const int64_t *gain, int32_t *node, int32_t *from, int32_t *to, int64_t *giso,
-                              int32_t *pos) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= M) return;
-    int32_t n = (int32_t)sorted_nodes[i];
-    node[i] = n;
-    from[i] = assign[n];
-    to[i] = target[n];
-    giso[i] = gain[n];
-    pos[n] = (int32_t)i;
-}
-
-// A15: gains corrected for earlier moves, rules (a)-(d) (_kernels.pyx:326-363)
-__global__ void k_seq_gains(int32_t M, const int64_t *inc_off, const int32_t *inc_dat, const int64_t *pin_off,
-                            const int32_t *pin_dat, const int64_t *wi, Runs r, const int32_t *node,
-                            const int32_t *from, const int32_t *to, const int64_t *giso, const int32_t *pos,
-                            int64_t *gseq) {
-    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
-    const int lane = lane_id();
-    for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id(); i < M; i += nw) {
-        const int32_t n = node[i], ps = from[i], pd = to[i];
-        int64_t acc = 0;
-        for (int64_t ii = inc_off[n] + lane; ii < inc_off[n + 1]; ii += 32) {
-            const int32_t e = inc_dat[ii];
-            const int64_t lo = pin_off[e];
-            const int32_t lam = r.len[e];
-            int32_t k;
-            k = run_find(r, lo, lam, ps);
-            const int32_t base_ps = k >= 0 ? r.cnt[lo + k] : 0;
-            k = run_find(r, lo, lam, pd);
-            const int32_t base_pd = k >= 0 ? r.cnt[lo + k] : 0;
-            int32_t leav_pd = 0, ent_pd = 0, leav_ps = 0, ent_ps = 0;
-            for (int64_t pp = lo; pp < pin_off[e + 1]; pp++) {
-                const int32_t j = pos[pin_dat[pp]];
-                if (j < 0 || j >= i) continue;
-                leav_pd += from[j] == pd;
-                ent_pd += to[j] == pd;
-                leav_ps += from[j] == ps;
-                ent_ps += to[j] == ps;
-            }
-            const int64_t we = wi[e];
-            int64_t net = 0;
-            if (base_pd > 0) {
-                if (leav_pd - ent_pd == base_pd) net -= we;
-            } else if (ent_pd > 0) {
-                net += we;
-            }
-            if (base_ps == 1) {
-                if (ent_ps > 0) net -= we;
-            } else if (base_ps - 1 > 0 && leav_ps - ent_ps == base_ps - 1) {
-                net += we;
-            }
-            acc += net;
-        }
-        acc = warp_sum(acc);
-        if (lane == 0) gseq[i] = giso[i] + acc;
-    }
-}
-
 // ---------------------------------------------------------------------------
 // A17 events.  Key = track | part | move index; track 0 = size, 1 = inbound.
 // ---------------------------------------------------------------------------
@@ -386,20 +485,6 @@ __device__ __forceinline__ void emit(const EvArgs &ev, uint64_t track, int32_t p
     unsigned long long s = atomicAdd(ev.count, 1ull);
     ev.key[s] = (track << (ev.pbits + ev.ibits)) | ((uint64_t)(uint32_t)p << ev.ibits) | (uint64_t)(uint32_t)i;
     ev.val[s] = (uint32_t)d;
-}
-
-// size track (refine.py:203-208): (from_i, i, -size), (to_i, i, +size)
-__global__ void k_size_events(int32_t M, const int32_t *node, const int32_t *from, const int32_t *to,
-                              const int32_t *size, EvArgs ev) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= M) return;
-    const int32_t s = size[node[i]];
-    const uint64_t sh = (uint64_t)(ev.pbits + ev.ibits);
-    ev.key[2 * i] = ((uint64_t)(uint32_t)from[i] << ev.ibits) | (uint64_t)i;
-    ev.val[2 * i] = (uint32_t)(-s);
-    ev.key[2 * i + 1] = ((uint64_t)(uint32_t)to[i] << ev.ibits) | (uint64_t)i;
-    ev.val[2 * i + 1] = (uint32_t)s;
-    (void)sh;
 }
 
 // inbound track (refine.py:210-237), per h-edge: the movers among its
@@ -525,44 +610,38 @@ __global__ void k_inbound_events_block(const int64_t *dst_off, const int32_t *ds
     }
 }
 
-// segment heads over sorted events: segment = (track, part)
-__global__ void k_ev_heads(int64_t T, const uint64_t *key, int ibits, uint8_t *flag) {
+// _track_violations (refine.py:145-175) as a segmented formulation over the
+// events sorted by (track, part, i): group = equal key, segment = equal
+// (track, part).  With ex = exclusive prefix sums of the deltas and the
+// group / segment start indices from running-max scans, the value after a
+// group is base + ex[end+1] - ex[seg0] and before it base + ex[g0] - ex[seg0];
+// a group toggles its part's flag when the two sit on different sides of
+// the limit.
+__global__ void k_ev_prep(int64_t T, const uint64_t *key, const uint32_t *val, int ibits, int64_t *gs, int64_t *ss,
+                          int64_t *dv) {
     int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= T) return;
-    flag[k] = (k == 0) || ((key[k] >> ibits) != (key[k - 1] >> ibits));
+    const uint64_t kk = key[k];
+    gs[k] = (k == 0 || key[k - 1] != kk) ? k : 0;
+    ss[k] = (k == 0 || (key[k - 1] >> ibits) != (kk >> ibits)) ? k : 0;
+    dv[k] = (int64_t)(int32_t)val[k];
 }
-__global__ void k_ev_head_list(int64_t T, const uint8_t *flag, const int64_t *hpos, int64_t *heads) {
+__global__ void k_ev_toggle(int64_t T, const uint64_t *key, const int64_t *ex, const int64_t *gstart,
+                            const int64_t *sstart, int ibits, int pbits, const int64_t *psizes,
+                            const int64_t *pinbound, int64_t omega, int64_t delta, int64_t *dlt) {
     int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k < T && flag[k]) heads[hpos[k]] = k;
-}
-
-// _track_violations (refine.py:145-175): per (track, part) a running value
-// from its base; each (part, i) group toggles the violation flag when the
-// value crosses the limit.  One thread walks one segment.
-__global__ void k_ev_walk(int64_t S, int64_t T, const int64_t *heads, const uint64_t *key, const uint32_t *val,
-                          int ibits, int pbits, const int64_t *psizes, const int64_t *pinbound, int64_t omega,
-                          int64_t delta, int64_t *dlt) {
-    int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= S) return;
-    const int64_t b = heads[s], end = s + 1 < S ? heads[s + 1] : T;
-    const uint64_t k0 = key[b];
-    const int track = (int)(k0 >> (ibits + pbits));
-    const int32_t p = (int32_t)((k0 >> ibits) & ((1ull << pbits) - 1ull));
+    if (k >= T) return;
+    const uint64_t kk = key[k];
+    if (k + 1 < T && key[k + 1] == kk) return;  // not the last event of its group
+    const int track = (int)(kk >> (ibits + pbits));
+    const int32_t p = (int32_t)((kk >> ibits) & ((1ull << pbits) - 1ull));
+    const uint64_t i = kk & ((1ull << ibits) - 1ull);
+    const int64_t base = track ? pinbound[p] : psizes[p];
     const int64_t limit = track ? delta : omega;
-    int64_t run = track ? pinbound[p] : psizes[p];
-    const uint64_t imask = (1ull << ibits) - 1ull;
-    for (int64_t k = b; k < end;) {
-        const uint64_t i = key[k] & imask;
-        int64_t sum = 0;
-        while (k < end && (key[k] & imask) == i) {
-            sum += (int64_t)(int32_t)val[k];
-            k++;
-        }
-        const bool before = run > limit;
-        run += sum;
-        const bool after = run > limit;
-        if (after != before) atomicAdd((unsigned long long *)&dlt[i + 1], (unsigned long long)(after ? 1ll : -1ll));
-    }
+    const int64_t s0 = ex[sstart[k]];
+    const bool after = base + ex[k + 1] - s0 > limit;
+    const bool before = base + ex[gstart[k]] - s0 > limit;
+    if (after != before) atomicAdd((unsigned long long *)&dlt[i + 1], (unsigned long long)(after ? 1ll : -1ll));
 }
 
 // smallest argmax of cum over prefixes with active == 0 (refine.py:244-247)
@@ -631,29 +710,118 @@ static void build_runs(Ctx &c, const DLevel &L, const DWeights &W, const int32_t
     c.zero(conn, 1);
     if (pinbound) c.zero(pinbound, K);
     if (L.E > 0) {
-        k_edge_runs<<<(unsigned)cdiv(L.E, 256), 256, 0, c.stream>>>(L.E, L.pin_off, tmp_parts, L.dst_off, L.dst_dat,
-                                                                   assign, W.wi, r, conn, pinbound);
+        if (L.U >= 12 * (int64_t)L.E) {
+            int blocks = (int)std::min<int64_t>(cdiv(L.E, 8), (int64_t)c.num_sms * 16);
+            k_edge_runs_warp<<<blocks, 256, 0, c.stream>>>(L.E, L.pin_off, tmp_parts, L.dst_off, L.dst_dat, assign,
+                                                          W.wi, r, conn, pinbound);
+        } else {
+            k_edge_runs<<<(unsigned)cdiv(L.E, 256), 256, 0, c.stream>>>(L.E, L.pin_off, tmp_parts, L.dst_off,
+                                                                       L.dst_dat, assign, W.wi, r, conn, pinbound);
+        }
         DHGP_LAUNCHED(c);
     }
 }
+
+namespace {
+// moves: sequence arrays from the radix-sorted (key, node) pairs; M on device
+__global__ void k_build_moves_dn(const int64_t *dM, const uint32_t *sorted_nodes, const int32_t *assign,
+                                 const int32_t *target, const int64_t *gain, int32_t *node, int32_t *from, int32_t *to,
+                                 int64_t *giso, int32_t *pos) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= *dM) return;
+    int32_t n = (int32_t)sorted_nodes[i];
+    node[i] = n;
+    from[i] = assign[n];
+    to[i] = target[n];
+    giso[i] = gain[n];
+    pos[n] = (int32_t)i;
+}
+// size track (refine.py:203-208): (from_i, i, -size), (to_i, i, +size)
+__global__ void k_size_events_dn(const int64_t *dM, const int32_t *node, const int32_t *from, const int32_t *to,
+                                 const int32_t *size, EvArgs ev) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t M = *dM;
+    if (i == 0) *ev.count = (unsigned long long)(2 * M);
+    if (i >= M) return;
+    const int32_t s = size[node[i]];
+    ev.key[2 * i] = ((uint64_t)(uint32_t)from[i] << ev.ibits) | (uint64_t)i;
+    ev.val[2 * i] = (uint32_t)(-s);
+    ev.key[2 * i + 1] = ((uint64_t)(uint32_t)to[i] << ev.ibits) | (uint64_t)i;
+    ev.val[2 * i + 1] = (uint32_t)s;
+}
+// A15: gains corrected for earlier moves, rules (a)-(d) (_kernels.pyx:326-363)
+__global__ void k_seq_gains_dn(const int64_t *dM, const int64_t *inc_off, const int32_t *inc_dat,
+                               const int64_t *pin_off, const int32_t *pin_dat, const int64_t *wi, Runs r,
+                               const int32_t *node, const int32_t *from, const int32_t *to, const int64_t *giso,
+                               const int32_t *pos, int64_t *gseq) {
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const int lane = lane_id();
+    const int64_t M = *dM;
+    for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id(); i < M; i += nw) {
+        const int32_t n = node[i], ps = from[i], pd = to[i];
+        int64_t acc = 0;
+        for (int64_t ii = inc_off[n] + lane; ii < inc_off[n + 1]; ii += 32) {
+            const int32_t e = inc_dat[ii];
+            const int64_t lo = pin_off[e];
+            const int32_t lam = r.len[e];
+            int32_t k;
+            k = run_find(r, lo, lam, ps);
+            const int32_t base_ps = k >= 0 ? r.cnt[lo + k] : 0;
+            k = run_find(r, lo, lam, pd);
+            const int32_t base_pd = k >= 0 ? r.cnt[lo + k] : 0;
+            int32_t leav_pd = 0, ent_pd = 0, leav_ps = 0, ent_ps = 0;
+            for (int64_t pp = lo; pp < pin_off[e + 1]; pp++) {
+                const int32_t j = pos[pin_dat[pp]];
+                if (j < 0 || j >= i) continue;
+                leav_pd += from[j] == pd;
+                ent_pd += to[j] == pd;
+                leav_ps += from[j] == ps;
+                ent_ps += to[j] == ps;
+            }
+            const int64_t we = wi[e];
+            int64_t net = 0;
+            if (base_pd > 0) {
+                if (leav_pd - ent_pd == base_pd) net -= we;
+            } else if (ent_pd > 0) {
+                net += we;
+            }
+            if (base_ps == 1) {
+                if (ent_ps > 0) net -= we;
+            } else if (base_ps - 1 > 0 && leav_ps - ent_ps == base_ps - 1) {
+                net += we;
+            }
+            acc += net;
+        }
+        acc = warp_sum(acc);
+        if (lane == 0) gseq[i] = giso[i] + acc;
+    }
+}
+}  // namespace
 
 void refine_level(Ctx &c, const DLevel &L, const DWeights &W, int32_t *assign, int32_t K, int64_t omega,
                   int64_t delta, int32_t max_rounds, int32_t level, std::vector<double> &conns,
                   const RoundObserver *obs) {
     static bool attr = false;
     if (!attr) {
-        DHGP_CUDA(cudaFuncSetAttribute(k_propose_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, PR_SMEM));
+        DHGP_CUDA(cudaFuncSetAttribute(k_propose_warp<unsigned>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       pr_smem<unsigned>()));
+        DHGP_CUDA(cudaFuncSetAttribute(k_propose_warp<unsigned long long>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, pr_smem<unsigned long long>()));
+        DHGP_CUDA(cudaFuncSetAttribute(k_propose_heavy<unsigned>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       PH_MAXK * 8 + PH_MAXK / 8 + 64));
+        DHGP_CUDA(cudaFuncSetAttribute(k_propose_heavy<unsigned long long>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, PH_MAXK * 8 + PH_MAXK / 8 + 64));
         attr = true;
     }
     const int32_t N = L.N;
+    // ---- per-level buffers (capacities: N moves, 2N + 2 S_in events) ------
     Runs r;
     r.part = c.alloc<int32_t>(L.U);
     r.cnt = c.alloc<int32_t>(L.U);
     r.cin = c.alloc<int32_t>(L.U);
     r.len = c.alloc<int32_t>(L.E);
     int32_t *tmp_parts = c.alloc<int32_t>(L.U);
-    int64_t *psizes = c.alloc<int64_t>(K);
-    int64_t *pinbound = c.alloc<int64_t>(K);
+    int64_t *psizes = c.alloc<int64_t>(K), *pinbound = c.alloc<int64_t>(K);
     int32_t *target = c.alloc<int32_t>(N);
     int64_t *gain = c.alloc<int64_t>(N);
     uint8_t *flags = c.alloc<uint8_t>(N);
@@ -661,9 +829,26 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, int32_t *assign, i
     int32_t *pos = c.alloc<int32_t>(N);
     int32_t *ctr = c.alloc<int32_t>(4);
     int32_t *big = c.alloc<int32_t>(std::max<int64_t>(N, L.E));
-    const int gmax_bits = bitlen((uint64_t)W.wsum);
-
     unsigned long long *conn_d = c.alloc<unsigned long long>(1);
+    uint64_t *mk = c.alloc<uint64_t>(N), *mkt = c.alloc<uint64_t>(N);
+    uint32_t *mv = c.alloc<uint32_t>(N), *mvt = c.alloc<uint32_t>(N);
+    int32_t *node = c.alloc<int32_t>(N), *from = c.alloc<int32_t>(N), *to = c.alloc<int32_t>(N);
+    int64_t *giso = c.alloc<int64_t>(N), *gseq = c.alloc<int64_t>(N);
+    const int64_t ecap = 2 * (int64_t)N + 2 * L.Sin;
+    uint64_t *ek = c.alloc<uint64_t>(ecap), *ekt = c.alloc<uint64_t>(ecap);
+    uint32_t *evv = c.alloc<uint32_t>(ecap), *evt = c.alloc<uint32_t>(ecap);
+    unsigned long long *ecount = c.alloc<unsigned long long>(1);
+    const int pb_blocks = 16;
+    long long *pdense = c.alloc<long long>((int64_t)pb_blocks * K);
+    int32_t *ptouched = c.alloc<int32_t>((int64_t)pb_blocks * K);
+    k_fill_ll<<<(unsigned)cdiv((int64_t)pb_blocks * K, 256), 256, 0, c.stream>>>(pdense, -1ll, (int64_t)pb_blocks * K);
+    DHGP_LAUNCHED(c);
+    const int gmax_bits = std::max(1, bitlen((uint64_t)W.wsum));
+    const int pbits = std::max(1, bitlen((uint64_t)(K > 0 ? K - 1 : 0)));
+    const int ibits_cap = std::max(1, bitlen((uint64_t)N));
+    if (1 + ibits_cap + pbits > 64) throw Error{DHGP_ERR_UNSUPPORTED, "event key needs more than 64 bits"};
+    const int64_t *dM = mpos + N;
+
     bool need_final = false;
     for (int32_t rnd = 0; rnd < max_rounds; rnd++) {
         // --- A11/A12/A16 + A13 ---------------------------------------------
@@ -673,130 +858,112 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, int32_t *assign, i
             k_part_sizes<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(N, assign, L.size, psizes);
             DHGP_LAUNCHED(c);
         }
-        // --- A14 propose ---------------------------------------------------
+        // --- A14 propose (warp tier + block tier, no host sync) -------------
         {
-            KScope ks(c, "propose", (double)(12.0 * L.U + 16.0 * L.U + 24.0 * N));
+            KScope ks(c, "propose", (double)(12.0 * L.U + 16.0 * L.U + 24.0 * N), N);
             c.zero(ctr, 4);
             ProposeArgs a{N, K, L.inc_off, L.inc_dat, L.pin_off, W.wi, r, assign, psizes, L.size, omega,
                           target, gain, ctr, big, ctr + 1};
             if (N > 0) {
                 int blocks = (int)std::min<int64_t>(cdiv(N, PR_WARPS), (int64_t)c.num_sms * 2);
-                k_propose_warp<<<blocks, PR_WARPS * 32, PR_SMEM, c.stream>>>(a);
+                if (W.wsum < (1ll << 32))
+                    k_propose_warp<unsigned><<<blocks, PR_WARPS * 32, pr_smem<unsigned>(), c.stream>>>(a);
+                else
+                    k_propose_warp<unsigned long long>
+                        <<<blocks, PR_WARPS * 32, pr_smem<unsigned long long>(), c.stream>>>(a);
                 DHGP_LAUNCHED(c);
-            }
-            int32_t nbig = 0;
-            c.d2h(&nbig, ctr + 1, 1);
-            c.sync();
-            if (nbig > 0) {
-                int g = (int)std::min<int64_t>(nbig, 64);
-                long long *dense = c.alloc<long long>((int64_t)g * K);
-                int32_t *touched = c.alloc<int32_t>((int64_t)g * K);
-                k_fill_ll<<<(unsigned)cdiv((int64_t)g * K, 256), 256, 0, c.stream>>>(dense, -1ll, (int64_t)g * K);
+                if (K <= PH_MAXK) {
+                    const size_t sm = (size_t)K * (W.wsum < (1ll << 32) ? 4 : 8) + 4 * (size_t)((K + 31) / 32) + 16;
+                    if (W.wsum < (1ll << 32))
+                        k_propose_heavy<unsigned><<<c.num_sms, PH_THREADS, sm, c.stream>>>(a);
+                    else
+                        k_propose_heavy<unsigned long long><<<c.num_sms, PH_THREADS, sm, c.stream>>>(a);
+                } else {
+                    k_propose_block<<<pb_blocks, PB_THREADS, 0, c.stream>>>(a, pdense, ptouched);
+                }
                 DHGP_LAUNCHED(c);
-                k_propose_block<<<g, PB_THREADS, 0, c.stream>>>(a, dense, touched);
-                DHGP_LAUNCHED(c);
-                c.free(dense);
-                c.free(touched);
             }
         }
-        // --- sequence (refine.py:108-110) ------------------------------------
+        // --- sequence: movers by (gain desc, node asc) (refine.py:108-110) --
         if (N > 0) {
             k_mover_flags<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(N, target, flags);
             DHGP_LAUNCHED(c);
         }
         scan_excl<uint8_t>(c, flags, mpos, N);
+        if (N > 0) {
+            k_mover_keys<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(N, flags, mpos, gain, W.wsum, mk, mv);
+            DHGP_LAUNCHED(c);
+        }
+        radix_sort_pairs(c, mk, mv, mkt, mvt, N, dM, gmax_bits);
+        fill_i32(c, pos, -1, N);
+        if (N > 0) {
+            k_build_moves_dn<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(dM, mv, assign, target, gain, node, from,
+                                                                          to, giso, pos);
+            DHGP_LAUNCHED(c);
+            KScope ks(c, "seq_gains", 0.0);
+            int blocks = (int)std::min<int64_t>(cdiv(N, 8), (int64_t)c.num_sms * 16);
+            k_seq_gains_dn<<<blocks, 256, 0, c.stream>>>(dM, L.inc_off, L.inc_dat, L.pin_off, L.pin_dat, W.wi, r,
+                                                          node, from, to, giso, pos, gseq);
+            DHGP_LAUNCHED(c);
+        }
+        // --- A17 events (key bits sized for the capacity N) -----------------
+        const int ibits = ibits_cap;
+        EvArgs ev{ibits, pbits, ek, evv, ecount};
+        c.zero(ctr, 4);
+        if (N > 0) {
+            k_size_events_dn<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(dM, node, from, to, L.size, ev);
+            DHGP_LAUNCHED(c);
+        }
+        if (L.E > 0) {
+            k_inbound_events<<<(unsigned)cdiv(L.E, 256), 256, 0, c.stream>>>(L.E, L.dst_off, L.dst_dat, L.pin_off, r,
+                                                                           pos, from, to, ev, big, ctr);
+            DHGP_LAUNCHED(c);
+            k_inbound_events_block<<<c.num_sms, 256, 0, c.stream>>>(L.dst_off, L.dst_dat, L.pin_off, r, pos, from, to,
+                                                                     ev, big, ctr, ctr + 2);
+            DHGP_LAUNCHED(c);
+        }
+        // ---- sync 1: M, event count, connectivity --------------------------
         int64_t M = 0;
-        unsigned long long conn_h = 0;
-        c.d2h(&M, mpos + N, 1);
+        unsigned long long T = 0, conn_h = 0;
+        int32_t hc[4];
+        c.d2h(&M, dM, 1);
+        c.d2h(&T, ecount, 1);
         c.d2h(&conn_h, conn_d, 1);
+        c.d2h(hc, ctr, 4);
         c.sync();
         conns.push_back((double)(int64_t)conn_h);  // connectivity of the round's starting assignment
         need_final = false;
         if (M == 0) break;
-        uint64_t *mk = c.alloc<uint64_t>(M), *mkt = c.alloc<uint64_t>(M);
-        uint32_t *mv = c.alloc<uint32_t>(M), *mvt = c.alloc<uint32_t>(M);
-        k_mover_keys<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(N, flags, mpos, gain, W.wsum, mk, mv);
-        DHGP_LAUNCHED(c);
-        radix_sort_pairs(c, mk, mv, mkt, mvt, M, nullptr, gmax_bits);
-        int32_t *node = c.alloc<int32_t>(M), *from = c.alloc<int32_t>(M), *to = c.alloc<int32_t>(M);
-        int64_t *giso = c.alloc<int64_t>(M), *gseq = c.alloc<int64_t>(M);
-        fill_i32(c, pos, -1, N);
-        k_build_moves<<<(unsigned)cdiv(M, 256), 256, 0, c.stream>>>((int32_t)M, mv, assign, target, gain, node, from,
-                                                                   to, giso, pos);
-        DHGP_LAUNCHED(c);
-        c.free(mk);
-        c.free(mkt);
-        c.free(mv);
-        c.free(mvt);
-        // --- A15 in-sequence gains ------------------------------------------
-        {
-            KScope ks(c, "seq_gains", 0.0);
-            int blocks = (int)std::min<int64_t>(cdiv(M, 8), (int64_t)c.num_sms * 16);
-            k_seq_gains<<<blocks, 256, 0, c.stream>>>((int32_t)M, L.inc_off, L.inc_dat, L.pin_off, L.pin_dat, W.wi,
-                                                       r, node, from, to, giso, pos, gseq);
-            DHGP_LAUNCHED(c);
-        }
-        // --- A17 events and prefix selection --------------------------------
+        if (hc[2]) throw Error{DHGP_ERR_UNSUPPORTED, "too many movers on one h-edge"};
         int64_t kbest = 0, total_gain = 0;
         int64_t *dlt = c.alloc<int64_t>(M + 1);
         int64_t *act_ex = c.alloc<int64_t>(M + 2);
         int64_t *cum = c.alloc<int64_t>(M + 1);
         {
-            KScope ks(c, "select", 0.0);
-            const int ibits = std::max(1, bitlen((uint64_t)M));
-            const int pbits = std::max(1, bitlen((uint64_t)(K - 1)));
-            if (1 + ibits + pbits > 64)
-                throw Error{DHGP_ERR_UNSUPPORTED, "event key needs more than 64 bits"};
-            const int64_t cap = 2 * M + 2 * L.Sin;
-            uint64_t *ek = c.alloc<uint64_t>(cap), *ekt = c.alloc<uint64_t>(cap);
-            uint32_t *evv = c.alloc<uint32_t>(cap), *evt = c.alloc<uint32_t>(cap);
-            unsigned long long *ecount = c.alloc<unsigned long long>(1);
-            unsigned long long two_m = (unsigned long long)(2 * M);
-            c.h2d(ecount, &two_m, 1);
-            EvArgs ev{ibits, pbits, ek, evv, ecount};
-            k_size_events<<<(unsigned)cdiv(M, 256), 256, 0, c.stream>>>((int32_t)M, node, from, to, L.size, ev);
-            DHGP_LAUNCHED(c);
-            c.zero(ctr, 4);
-            if (L.E > 0) {
-                k_inbound_events<<<(unsigned)cdiv(L.E, 256), 256, 0, c.stream>>>(L.E, L.dst_off, L.dst_dat, L.pin_off,
-                                                                               r, pos, from, to, ev, big, ctr);
-                DHGP_LAUNCHED(c);
-                k_inbound_events_block<<<c.num_sms, 256, 0, c.stream>>>(L.dst_off, L.dst_dat, L.pin_off, r, pos, from,
-                                                                         to, ev, big, ctr, ctr + 2);
-                DHGP_LAUNCHED(c);
-            }
-            unsigned long long T = 0;
-            int32_t hc[4];
-            c.d2h(&T, ecount, 1);
-            c.d2h(hc, ctr, 4);
-            c.sync();
-            if (hc[2]) throw Error{DHGP_ERR_UNSUPPORTED, "too many movers on one h-edge"};
+            KScope ks(c, "select", 0.0, N);
             radix_sort_pairs(c, ek, evv, ekt, evt, (int64_t)T, nullptr, 1 + ibits + pbits);
-            uint8_t *hf = c.alloc<uint8_t>(T);
-            int64_t *hpos = c.alloc<int64_t>(T + 1);
-            k_ev_heads<<<(unsigned)cdiv(T, 256), 256, 0, c.stream>>>((int64_t)T, ek, ibits, hf);
-            DHGP_LAUNCHED(c);
-            scan_excl<uint8_t>(c, hf, hpos, T);
-            int64_t S = 0;
-            c.d2h(&S, hpos + T, 1);
-            c.sync();
-            int64_t *heads = c.alloc<int64_t>(S);
-            k_ev_head_list<<<(unsigned)cdiv(T, 256), 256, 0, c.stream>>>((int64_t)T, hf, hpos, heads);
-            DHGP_LAUNCHED(c);
+            int64_t *gs = c.alloc<int64_t>(T), *ss = c.alloc<int64_t>(T), *dv = c.alloc<int64_t>(T);
+            int64_t *ex = c.alloc<int64_t>(T + 1), *gst = c.alloc<int64_t>(T), *sst = c.alloc<int64_t>(T);
             c.zero(dlt, M + 1);
-            if (S > 0) {
-                k_ev_walk<<<(unsigned)cdiv(S, 128), 128, 0, c.stream>>>(S, (int64_t)T, heads, ek, evv, ibits, pbits,
-                                                                        psizes, pinbound, omega, delta, dlt);
+            if (T > 0) {
+                k_ev_prep<<<(unsigned)cdiv(T, 256), 256, 0, c.stream>>>((int64_t)T, ek, evv, ibits, gs, ss, dv);
+                DHGP_LAUNCHED(c);
+                scan_excl<int64_t>(c, dv, ex, T);
+                scan_incl_max(c, gs, gst, T);
+                scan_incl_max(c, ss, sst, T);
+                k_ev_toggle<<<(unsigned)cdiv(T, 256), 256, 0, c.stream>>>((int64_t)T, ek, ex, gst, sst, ibits, pbits,
+                                                                          psizes, pinbound, omega, delta, dlt);
                 DHGP_LAUNCHED(c);
             }
             scan_excl<int64_t>(c, dlt, act_ex, M + 1);  // act_ex[j+1] = active[j]
-            scan_excl<int64_t>(c, gseq, cum, M);        // cum[j] = sum of first j gains
+            scan_excl<int64_t>(c, gseq, cum, M);        // cum[j] = sum of the first j gains
             const int nb = (int)std::min<int64_t>(cdiv(M + 1, 256), 256);
             long long *bv = c.alloc<long long>(nb), *bk = c.alloc<long long>(nb), *res = c.alloc<long long>(2);
             k_best_prefix_partial<<<nb, 256, 0, c.stream>>>(M + 1, act_ex, cum, bv, bk);
             DHGP_LAUNCHED(c);
             k_best_prefix_final<<<1, 32, 0, c.stream>>>(nb, bv, bk, res);
             DHGP_LAUNCHED(c);
+            // ---- sync 2: the selected prefix -------------------------------
             long long hr[2];
             c.d2h(hr, res, 2);
             c.sync();
@@ -805,14 +972,7 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, int32_t *assign, i
             c.free(bv);
             c.free(bk);
             c.free(res);
-            c.free(ek);
-            c.free(ekt);
-            c.free(evv);
-            c.free(evt);
-            c.free(ecount);
-            c.free(hf);
-            c.free(hpos);
-            c.free(heads);
+            for (void *q : {(void *)gs, (void *)ss, (void *)dv, (void *)ex, (void *)gst, (void *)sst}) c.free(q);
         }
         if (obs && *obs) {
             RoundRecord rec;
@@ -843,11 +1003,6 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, int32_t *assign, i
             k_apply<<<(unsigned)cdiv(kbest, 256), 256, 0, c.stream>>>(kbest, node, to, assign);
             DHGP_LAUNCHED(c);
         }
-        c.free(node);
-        c.free(from);
-        c.free(to);
-        c.free(giso);
-        c.free(gseq);
         c.free(dlt);
         c.free(act_ex);
         c.free(cum);
@@ -859,21 +1014,12 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, int32_t *assign, i
         evaluate_assign(c, L, W, assign, K, nullptr, nullptr, &v);
         conns.push_back(v);
     }
-    c.free(r.part);
-    c.free(r.cnt);
-    c.free(r.cin);
-    c.free(r.len);
-    c.free(tmp_parts);
-    c.free(psizes);
-    c.free(pinbound);
-    c.free(target);
-    c.free(gain);
-    c.free(flags);
-    c.free(mpos);
-    c.free(pos);
-    c.free(ctr);
-    c.free(big);
-    c.free(conn_d);
+    for (void *p : {(void *)r.part, (void *)r.cnt, (void *)r.cin, (void *)r.len, (void *)tmp_parts, (void *)psizes,
+                    (void *)pinbound, (void *)target, (void *)gain, (void *)flags, (void *)mpos, (void *)pos,
+                    (void *)ctr, (void *)big, (void *)conn_d, (void *)mk, (void *)mkt, (void *)mv, (void *)mvt,
+                    (void *)node, (void *)from, (void *)to, (void *)giso, (void *)gseq, (void *)ek, (void *)ekt,
+                    (void *)evv, (void *)evt, (void *)ecount, (void *)pdense, (void *)ptouched})
+        c.free(p);
 }
 
 void evaluate_assign(Ctx &c, const DLevel &L, const DWeights &W, const int32_t *assign, int32_t K,
