@@ -191,7 +191,8 @@ def run_ours(args, ws, rank, local):
         _lib.raise_for(L.dhgp_session_partition(sess, C.byref(cc), _lib.ptr(assign), C.byref(nparts), C.byref(st)))
         out = (st.device_ms, st.gpu_launches, st.num_levels,
                [st.trace_val[i] for i in range(st.trace_off[st.num_levels])],
-               [st.level_pins[i] for i in range(st.num_levels)])
+               [st.level_pins[i] for i in range(st.num_levels)],
+               {"coarsen_ms": round(st.phase_ms[0], 1), "refine_ms": round(st.phase_ms[1], 1)})
         L.dhgp_stats_free(C.byref(st))
         return out
 
@@ -212,7 +213,7 @@ def run_ours(args, ws, rank, local):
         for _ in range(args.steps):
             flush.zero_()
             barrier()
-            dms, nl, levels, trace, lpins = one()
+            dms, nl, levels, trace, lpins, phases = one()
             barrier()
             times.append(dms / 1e3)
             launches += nl
@@ -311,6 +312,7 @@ def run_ours(args, ws, rank, local):
         "clocks": clk.summary(),
         "roofline": roofline,
         "cpu_baseline": cpu,
+        "phase_ms": phases,
         "kernels": sorted(kstats, key=lambda k: -k["ms"])[:12],
     }
     print(json.dumps(line), flush=True)

@@ -527,11 +527,15 @@ void score_select(Ctx &c, const DLevel &L, const DWeights &W, int64_t omega, int
     c.zero(s.ctr, 3);
     ScoreArgs a{L.N, L.inc_off, L.inc_dat, L.pin_off, L.pin_dat, W.wi, L.size, L.in_off, L.in_dat, omega, delta,
                 pair, score, s.ctr, s.big, s.ctr + 1, s.heavy, s.ctr + 2};
-    int blocks = (int)std::min<int64_t>(cdiv(L.N, SS_WARPS), (int64_t)c.num_sms * 2);
-    if (W.wsum < (1ll << 32))
+    if (W.wsum < (1ll << 32)) {
+        static int g32 = resident_grid(c, k_score_warp<unsigned>, SS_WARPS * 32, ss_smem<unsigned>());
+        int blocks = (int)std::min<int64_t>(cdiv(L.N, SS_WARPS), g32);
         k_score_warp<unsigned><<<blocks, SS_WARPS * 32, ss_smem<unsigned>(), c.stream>>>(a);
-    else
+    } else {
+        static int g64 = resident_grid(c, k_score_warp<unsigned long long>, SS_WARPS * 32, ss_smem<unsigned long long>());
+        int blocks = (int)std::min<int64_t>(cdiv(L.N, SS_WARPS), g64);
         k_score_warp<unsigned long long><<<blocks, SS_WARPS * 32, ss_smem<unsigned long long>(), c.stream>>>(a);
+    }
     DHGP_LAUNCHED(c);
     // heavy tier: reads the escalation count on device, exits when zero
     if (W.wsum < (1ll << 32))
@@ -817,11 +821,15 @@ void contract_count(Ctx &c, DLevel &fine, const int32_t *match, const uint8_t *i
     c.free(cnt);
     // per-node families: union of the two members' sorted lists
     int64_t *ncnt = c.alloc<int64_t>(N);
+    s.big_in = c.alloc<int32_t>(N);
+    s.big_inc = c.alloc<int32_t>(N);
+    s.big_cnt = c.alloc<int32_t>(2);
+    c.zero(s.big_cnt, 2);
     coarse.in_off = c.alloc<int64_t>((int64_t)N + 1);
-    merge_union_count(c, N, s.ma, s.mb, fine.in_off, fine.in_dat, ncnt, d_nc);
+    merge_union_count(c, N, s.ma, s.mb, fine.in_off, fine.in_dat, ncnt, d_nc, s.big_in, s.big_cnt);
     scan_excl<int64_t>(c, ncnt, coarse.in_off, N);
     coarse.inc_off = c.alloc<int64_t>((int64_t)N + 1);
-    merge_union_count(c, N, s.ma, s.mb, fine.inc_off, fine.inc_dat, ncnt, d_nc);
+    merge_union_count(c, N, s.ma, s.mb, fine.inc_off, fine.inc_dat, ncnt, d_nc, s.big_inc, s.big_cnt + 1);
     scan_excl<int64_t>(c, ncnt, coarse.inc_off, N);
     c.free(ncnt);
     k_contract_status<<<1, 32, 0, c.stream>>>(N, E, s.rank, coarse.src_off, coarse.dst_off, coarse.pin_off,
@@ -845,8 +853,10 @@ void contract_write(Ctx &c, DLevel &fine, DLevel &coarse, ContractScratch &s, co
     seg_unique_write(c, E, fine.src_off, s.tmp_src, coarse.src_off, coarse.src_dat);
     seg_unique_write(c, E, fine.dst_off, s.tmp_dst, coarse.dst_off, coarse.dst_dat);
     seg_unique_write(c, E, fine.pin_off, s.tmp_pin, coarse.pin_off, coarse.pin_dat);
-    merge_union_write(c, st.nc, s.ma, s.mb, fine.in_off, fine.in_dat, coarse.in_off, coarse.in_dat);
-    merge_union_write(c, st.nc, s.ma, s.mb, fine.inc_off, fine.inc_dat, coarse.inc_off, coarse.inc_dat);
+    merge_union_write(c, st.nc, s.ma, s.mb, fine.in_off, fine.in_dat, coarse.in_off, coarse.in_dat, s.big_in,
+                      s.big_cnt);
+    merge_union_write(c, st.nc, s.ma, s.mb, fine.inc_off, fine.inc_dat, coarse.inc_off, coarse.inc_dat, s.big_inc,
+                      s.big_cnt + 1);
     contract_release(c, s);
 }
 
@@ -903,6 +913,9 @@ void contract_release(Ctx &c, ContractScratch &s) {
     c.free(s.tmp_dst);
     c.free(s.tmp_pin);
     c.free(s.rank);
+    c.free(s.big_in);
+    c.free(s.big_inc);
+    c.free(s.big_cnt);
     s = ContractScratch();
 }
 

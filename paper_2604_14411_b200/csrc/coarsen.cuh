@@ -52,6 +52,7 @@ struct ContractScratch {
     int32_t *ma = nullptr, *mb = nullptr;
     int32_t *tmp_src = nullptr, *tmp_dst = nullptr, *tmp_pin = nullptr;
     int64_t *rank = nullptr;
+    int32_t *big_in = nullptr, *big_inc = nullptr, *big_cnt = nullptr;  // large unions (block tier)
 };
 void contract_count(Ctx &c, DLevel &fine, const int32_t *match, const uint8_t *isrep, DLevel &coarse,
                     ContractScratch &s, int64_t *d_status);

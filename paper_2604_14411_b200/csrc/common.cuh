@@ -138,6 +138,15 @@ struct KScope {
 };
 
 inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// grid for a persistent / grid-stride kernel: resident blocks per SM x SMs
+template <class K>
+inline int resident_grid(const Ctx &c, K kernel, int threads, size_t smem) {
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem) != cudaSuccess || per_sm < 1)
+        per_sm = 1;
+    return per_sm * c.num_sms;
+}
 inline int bitlen(uint64_t x) {
     int b = 0;
     while (x) {

@@ -356,7 +356,7 @@ static void run_partition(Ctx &c, const DInput &in, const dhgp_config &cfg, Part
     try {
         const int64_t L = (int64_t)levels.size();
         refine_level(c, levels[L - 1], W, assign, K, omega, delta, cfg.max_rounds, (int32_t)(L - 1), res.trace[0],
-                     obs ? &robs : nullptr);
+                     obs ? &robs : nullptr, in.max_edge_pins);
         for (int64_t li = L - 2; li >= 0; li--) {
             if (levels[li].stub) rebuild_levels(c, levels, (size_t)li);
             DLevel &f = levels[li];
@@ -367,7 +367,7 @@ static void run_partition(Ctx &c, const DInput &in, const dhgp_config &cfg, Part
             std::swap(assign, assign2);
             levels[li + 1].release(c);
             refine_level(c, f, W, assign, K, omega, delta, cfg.max_rounds, (int32_t)li, res.trace[L - 1 - li],
-                         obs ? &robs : nullptr);
+                         obs ? &robs : nullptr, in.max_edge_pins);
         }
         const double t2 = now_ms();
         // ---- compaction (driver.py:137-143) + check_validity (144-146) ------

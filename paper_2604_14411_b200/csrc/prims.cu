@@ -316,6 +316,49 @@ __global__ void k_rs_down(const uint64_t *kin, const uint32_t *vin, uint64_t *ko
 }
 }  // namespace
 
+namespace {
+__global__ void __launch_bounds__(1024) k_small_sort(uint64_t *keys, uint32_t *vals, int n) {
+    __shared__ uint64_t sk[kSmallSort];
+    __shared__ uint32_t sv[kSmallSort];
+    int np = 1;
+    while (np < n) np <<= 1;
+    for (int i = threadIdx.x; i < np; i += blockDim.x) {
+        sk[i] = i < n ? keys[i] : ~0ull;
+        sv[i] = i < n ? vals[i] : 0xffffffffu;
+    }
+    for (int size = 2; size <= np; size <<= 1) {
+        for (int j = size >> 1; j > 0; j >>= 1) {
+            __syncthreads();
+            for (int t = threadIdx.x; t < (np >> 1); t += blockDim.x) {
+                const int lo = 2 * j * (t / j) + (t % j), hi = lo + j;
+                const bool asc = (lo & size) == 0;
+                const uint64_t a = sk[lo], b = sk[hi];
+                const uint32_t va = sv[lo], vb = sv[hi];
+                const bool gt = a > b || (a == b && va > vb);
+                if (gt == asc) {
+                    sk[lo] = b;
+                    sk[hi] = a;
+                    sv[lo] = vb;
+                    sv[hi] = va;
+                }
+            }
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        keys[i] = sk[i];
+        vals[i] = sv[i];
+    }
+}
+}  // namespace
+
+void small_sort_pairs(Ctx &c, uint64_t *keys, uint32_t *vals, int64_t n) {
+    if (n <= 1) return;
+    KScope ks(c, "radix_sort");
+    k_small_sort<<<1, 1024, 0, c.stream>>>(keys, vals, (int)n);
+    DHGP_LAUNCHED(c);
+}
+
 void radix_sort_pairs(Ctx &c, uint64_t *keys, uint32_t *vals, uint64_t *ktmp, uint32_t *vtmp, int64_t n_cap,
                       const int64_t *d_n, int bits) {
     if (n_cap <= 1 || bits <= 0) return;
@@ -530,8 +573,10 @@ void seg_unique_write(Ctx &c, int64_t nseg, const int64_t *off, const int32_t *t
 // sorted-set union of member lists (warp per coarse node)
 // ===========================================================================
 namespace {
+constexpr int64_t kMergeBig = 2048;
 __global__ void k_merge_count(int64_t nc_cap, const int64_t *d_nc, const int32_t *ma, const int32_t *mb,
-                              const int64_t *off, const int32_t *dat, int64_t *cnt) {
+                              const int64_t *off, const int32_t *dat, int64_t *cnt, int32_t *big_list,
+                              int32_t *big_count) {
     const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
     const int lane = lane_id();
     const int64_t nc = d_nc ? *d_nc : nc_cap;
@@ -546,6 +591,10 @@ __global__ void k_merge_count(int64_t nc_cap, const int64_t *d_nc, const int32_t
             continue;
         }
         int64_t blo = off[b], nb = off[b + 1] - blo;
+        if (big_list && na + nb > kMergeBig) {  // a block takes it
+            if (lane == 0) big_list[atomicAdd(big_count, 1)] = (int32_t)cn;
+            continue;
+        }
         // common elements: search the shorter list in the longer
         const int32_t *sp = dat + (na <= nb ? alo : blo);
         const int32_t *lp = dat + (na <= nb ? blo : alo);
@@ -558,7 +607,7 @@ __global__ void k_merge_count(int64_t nc_cap, const int64_t *d_nc, const int32_t
 }
 
 __global__ void k_merge_write(int64_t nc, const int32_t *ma, const int32_t *mb, const int64_t *off,
-                              const int32_t *dat, const int64_t *out_off, int32_t *out) {
+                              const int32_t *dat, const int64_t *out_off, int32_t *out, bool skip_big) {
     const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
     const int lane = lane_id();
     const uint32_t lt = (1u << lane) - 1u;
@@ -572,6 +621,7 @@ __global__ void k_merge_write(int64_t nc, const int32_t *ma, const int32_t *mb, 
             continue;
         }
         int64_t blo = off[b], nb = off[b + 1] - blo;
+        if (skip_big && na + nb > kMergeBig) continue;
         const int32_t *B = dat + blo;
         // x = A[i]: pos = i + lb_B(x) - #{A[k], k < i : A[k] in B}
         int64_t run = 0;
@@ -607,21 +657,107 @@ __global__ void k_merge_write(int64_t nc, const int32_t *ma, const int32_t *mb, 
         }
     }
 }
+
+// block-per-node union for large member lists (hubs), same formulas as the
+// warp version with a block-wide prefix over the "in the other list" flags
+__device__ __forceinline__ int64_t block_excl_flags(bool f, int64_t *sh_w, int64_t *total) {
+    const int lane = lane_id(), w = warp_id(), nw = blockDim.x >> 5;
+    const uint32_t bal = __ballot_sync(FULL_MASK, f);
+    if (lane == 0) sh_w[w] = __popc(bal);
+    __syncthreads();
+    int64_t before = 0, tot = 0;
+    for (int j = 0; j < nw; j++) {
+        if (j < w) before += sh_w[j];
+        tot += sh_w[j];
+    }
+    __syncthreads();
+    *total = tot;
+    return before + __popc(bal & ((1u << lane) - 1u));
+}
+__global__ void k_merge_count_big(const int32_t *list, const int32_t *count, const int32_t *ma, const int32_t *mb,
+                                  const int64_t *off, const int32_t *dat, int64_t *cnt) {
+    __shared__ int64_t sh[32];
+    const int n = *count;
+    for (int t = blockIdx.x; t < n; t += gridDim.x) {
+        const int32_t cn = list[t], a = ma[cn], b = mb[cn];
+        const int64_t alo = off[a], na = off[a + 1] - alo, blo = off[b], nb = off[b + 1] - blo;
+        const int32_t *sp = dat + (na <= nb ? alo : blo), *lp = dat + (na <= nb ? blo : alo);
+        const int64_t ns = na <= nb ? na : nb, nl = na <= nb ? nb : na;
+        int64_t common = 0;
+        for (int64_t i = threadIdx.x; i < ns; i += blockDim.x) common += bsearch_dev(lp, 0, nl, sp[i]) >= 0;
+        int64_t tot = block_sum<int64_t>(common, sh);
+        if (threadIdx.x == 0) cnt[cn] = na + nb - tot;
+        __syncthreads();
+    }
+}
+__global__ void k_merge_write_big(const int32_t *list, const int32_t *count, const int32_t *ma, const int32_t *mb,
+                                  const int64_t *off, const int32_t *dat, const int64_t *out_off, int32_t *out) {
+    __shared__ int64_t sh[32];
+    const int n = *count;
+    for (int t = blockIdx.x; t < n; t += gridDim.x) {
+        const int32_t cn = list[t], a = ma[cn], b = mb[cn];
+        const int64_t alo = off[a], na = off[a + 1] - alo, blo = off[b], nb = off[b + 1] - blo;
+        const int32_t *A = dat + alo, *B = dat + blo;
+        int32_t *o = out + out_off[cn];
+        int64_t run = 0;
+        for (int64_t base = 0; base < na; base += blockDim.x) {
+            const int64_t i = base + threadIdx.x;
+            int64_t lb = 0;
+            bool in_other = false;
+            int32_t x = 0;
+            if (i < na) {
+                x = A[i];
+                lb = lower_bound_dev<int32_t>(B, 0, nb, x);
+                in_other = lb < nb && B[lb] == x;
+            }
+            int64_t tot;
+            const int64_t ex = block_excl_flags(in_other, sh, &tot);
+            if (i < na) o[i + lb - (run + ex)] = x;
+            run += tot;
+        }
+        run = 0;
+        for (int64_t base = 0; base < nb; base += blockDim.x) {
+            const int64_t j = base + threadIdx.x;
+            int64_t lb = 0;
+            bool in_other = false;
+            int32_t y = 0;
+            if (j < nb) {
+                y = B[j];
+                lb = lower_bound_dev<int32_t>(A, 0, na, y);
+                in_other = lb < na && A[lb] == y;
+            }
+            int64_t tot;
+            const int64_t ex = block_excl_flags(in_other, sh, &tot);
+            if (j < nb && !in_other) o[lb + j - (run + ex)] = y;
+            run += tot;
+        }
+        __syncthreads();
+    }
+}
 }  // namespace
 
 void merge_union_count(Ctx &c, int64_t nc, const int32_t *ma, const int32_t *mb, const int64_t *off,
-                       const int32_t *dat, int64_t *cnt, const int64_t *d_nc) {
+                       const int32_t *dat, int64_t *cnt, const int64_t *d_nc, int32_t *big_list, int32_t *big_count) {
     if (nc <= 0) return;
     int64_t blocks = std::min<int64_t>(cdiv(nc, 8), (int64_t)c.num_sms * 16);
-    k_merge_count<<<(unsigned)blocks, 256, 0, c.stream>>>(nc, d_nc, ma, mb, off, dat, cnt);
+    k_merge_count<<<(unsigned)blocks, 256, 0, c.stream>>>(nc, d_nc, ma, mb, off, dat, cnt, big_list, big_count);
     DHGP_LAUNCHED(c);
+    if (big_list) {
+        k_merge_count_big<<<c.num_sms, 1024, 0, c.stream>>>(big_list, big_count, ma, mb, off, dat, cnt);
+        DHGP_LAUNCHED(c);
+    }
 }
 void merge_union_write(Ctx &c, int64_t nc, const int32_t *ma, const int32_t *mb, const int64_t *off,
-                       const int32_t *dat, const int64_t *out_off, int32_t *out) {
+                       const int32_t *dat, const int64_t *out_off, int32_t *out, const int32_t *big_list,
+                       const int32_t *big_count) {
     if (nc <= 0) return;
     int64_t blocks = std::min<int64_t>(cdiv(nc, 8), (int64_t)c.num_sms * 16);
-    k_merge_write<<<(unsigned)blocks, 256, 0, c.stream>>>(nc, ma, mb, off, dat, out_off, out);
+    k_merge_write<<<(unsigned)blocks, 256, 0, c.stream>>>(nc, ma, mb, off, dat, out_off, out, big_list != nullptr);
     DHGP_LAUNCHED(c);
+    if (big_list) {
+        k_merge_write_big<<<c.num_sms, 1024, 0, c.stream>>>(big_list, big_count, ma, mb, off, dat, out_off, out);
+        DHGP_LAUNCHED(c);
+    }
 }
 
 // ===========================================================================

@@ -18,6 +18,12 @@ void scan_incl_max(Ctx &c, const int64_t *in, int64_t *out, int64_t n);
 void radix_sort_pairs(Ctx &c, uint64_t *keys, uint32_t *vals, uint64_t *ktmp, uint32_t *vtmp, int64_t n_cap,
                       const int64_t *d_n, int bits);
 
+// Single-CTA sort of (key, val) pairs by (key, val) for n <= kSmallSort
+// (one launch; not stable in general, stable when vals ascend in input order
+// and are distinct).
+constexpr int64_t kSmallSort = 4096;
+void small_sort_pairs(Ctx &c, uint64_t *keys, uint32_t *vals, int64_t n);
+
 // Per-segment ascending sort of (map ? map[dat[i]] : dat[i]) into tmp (same
 // layout as dat).  Segments longer than kMaxSegSort raise DHGP_ERR_UNSUPPORTED.
 constexpr int64_t kMaxSegSort = 8192;
@@ -32,10 +38,14 @@ void seg_unique_write(Ctx &c, int64_t nseg, const int64_t *off, const int32_t *t
 // Sorted-set union of two member lists per coarse node.  The count variant
 // takes the node count from device memory (d_nc) when given; nc is then the
 // capacity and cnt[d_nc..nc) is zeroed.
+// Unions of more than 2048 elements go to a block-per-node kernel through
+// big_list (filled by the count call, reused by the write call).
 void merge_union_count(Ctx &c, int64_t nc, const int32_t *ma, const int32_t *mb, const int64_t *off,
-                       const int32_t *dat, int64_t *cnt, const int64_t *d_nc = nullptr);
+                       const int32_t *dat, int64_t *cnt, const int64_t *d_nc = nullptr, int32_t *big_list = nullptr,
+                       int32_t *big_count = nullptr);
 void merge_union_write(Ctx &c, int64_t nc, const int32_t *ma, const int32_t *mb, const int64_t *off,
-                       const int32_t *dat, const int64_t *out_off, int32_t *out);
+                       const int32_t *dat, const int64_t *out_off, int32_t *out, const int32_t *big_list = nullptr,
+                       const int32_t *big_count = nullptr);
 
 // Simple fills.
 void iota_i32(Ctx &c, int32_t *p, int64_t n);

@@ -122,6 +122,90 @@ __global__ void k_edge_runs_warp(int32_t E, const int64_t *pin_off, const int32_
     if (lane == 0 && contrib) atomicAdd(conn, (unsigned long long)contrib);
 }
 
+// Fused run lists for h-edges of <= 128 pins: a warp maps the pins to parts,
+// sorts them in registers (bitonic) and derives the runs from ballots; no
+// temporary array and one launch per round.
+template <int K>
+__device__ __forceinline__ int32_t warp_edge_runs(int64_t e, int64_t lo, int len, const int32_t *pin_dat,
+                                                  const int64_t *dst_off, const int32_t *dst_dat,
+                                                  const int32_t *assign, Runs r, int64_t *pinbound) {
+    const int lane = lane_id();
+    const uint32_t lt = (1u << lane) - 1u;
+    uint32_t v[K];
+#pragma unroll
+    for (int k = 0; k < K; k++) {
+        const int i = k * 32 + lane;
+        v[k] = i < len ? (uint32_t)assign[pin_dat[lo + i]] : 0xffffffffu;
+    }
+    warp_bitonic_sort<K>(v);
+    uint32_t bal[K];
+    bool head[K];
+#pragma unroll
+    for (int k = 0; k < K; k++) {
+        const int i = k * 32 + lane;
+        const uint32_t up = __shfl_up_sync(FULL_MASK, v[k], 1);
+        const uint32_t wrap = __shfl_sync(FULL_MASK, v[k > 0 ? k - 1 : 0], 31);
+        const uint32_t prev = lane == 0 ? wrap : up;
+        head[k] = i < len && (i == 0 || v[k] != prev);
+        bal[k] = __ballot_sync(FULL_MASK, head[k]);
+    }
+    int32_t before = 0;
+#pragma unroll
+    for (int k = 0; k < K; k++) {
+        if (head[k]) {
+            const int i = k * 32 + lane;
+            const uint32_t rest = bal[k] & ~((2u << lane) - 1u);
+            int next = len;
+            if (rest) {
+                next = k * 32 + __ffs(rest) - 1;
+            } else {
+#pragma unroll
+                for (int k2 = K - 1; k2 > k; k2--)
+                    if (bal[k2]) next = k2 * 32 + __ffs(bal[k2]) - 1;
+            }
+            const int32_t j = before + __popc(bal[k] & lt);
+            r.part[lo + j] = (int32_t)v[k];
+            r.cnt[lo + j] = next - i;
+            r.cin[lo + j] = 0;
+        }
+        before += __popc(bal[k]);
+    }
+    const int32_t lam = before;
+    __syncwarp();
+    for (int64_t q = dst_off[e] + lane; q < dst_off[e + 1]; q += 32) {
+        const int32_t k = run_find(r, lo, lam, assign[dst_dat[q]]);
+        atomicAdd(&r.cin[lo + k], 1);
+    }
+    __syncwarp();
+    if (pinbound)
+        for (int32_t j = lane; j < lam; j += 32)
+            if (r.cin[lo + j] > 0) atomicAdd((unsigned long long *)&pinbound[r.part[lo + j]], 1ull);
+    return lam;
+}
+
+__global__ void k_edge_runs_fused(int32_t E, const int64_t *pin_off, const int32_t *pin_dat, const int64_t *dst_off,
+                                  const int32_t *dst_dat, const int32_t *assign, const int64_t *wi, Runs r,
+                                  unsigned long long *conn, int64_t *pinbound) {
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    int64_t contrib = 0;
+    for (int64_t e = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id(); e < E; e += nw) {
+        const int64_t lo = pin_off[e];
+        const int len = (int)(pin_off[e + 1] - lo);
+        int32_t lam;
+        if (len <= 32)
+            lam = warp_edge_runs<1>(e, lo, len, pin_dat, dst_off, dst_dat, assign, r, pinbound);
+        else if (len <= 64)
+            lam = warp_edge_runs<2>(e, lo, len, pin_dat, dst_off, dst_dat, assign, r, pinbound);
+        else
+            lam = warp_edge_runs<4>(e, lo, len, pin_dat, dst_off, dst_dat, assign, r, pinbound);
+        if (lane_id() == 0) {
+            r.len[e] = lam;
+            if (lam > 0) contrib += wi[e] * (int64_t)(lam - 1);
+        }
+    }
+    if (lane_id() == 0 && contrib) atomicAdd(conn, (unsigned long long)contrib);
+}
+
 __global__ void k_part_sizes(int32_t N, const int32_t *assign, const int32_t *size, int64_t *psizes) {
     int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (n < N) atomicAdd((unsigned long long *)&psizes[assign[n]], (unsigned long long)(int64_t)size[n]);
@@ -704,11 +788,22 @@ __global__ void k_apply(int64_t k, const int32_t *node, const int32_t *to, int32
 // builds the run lists for `assign`; connectivity accumulates into *conn
 // (device), distinct-inbound counts into pinbound when requested
 static void build_runs(Ctx &c, const DLevel &L, const DWeights &W, const int32_t *assign, Runs &r,
-                       int32_t *tmp_parts, int64_t *pinbound, int32_t K, unsigned long long *conn) {
+                       int32_t *tmp_parts, int64_t *pinbound, int32_t K, unsigned long long *conn,
+                       int32_t max_edge_pins) {
     KScope ks(c, "edge_runs", (double)(8.0 * L.U + 4.0 * L.U + 12.0 * L.U + 4.0 * L.Pd + 24.0 * L.E));
-    seg_sort(c, L.E, L.pin_off, L.pin_dat, assign, tmp_parts);
     c.zero(conn, 1);
     if (pinbound) c.zero(pinbound, K);
+    if (max_edge_pins <= 128) {
+        if (L.E > 0) {
+            static int g = resident_grid(c, k_edge_runs_fused, 256, 0);
+            int blocks = (int)std::min<int64_t>(cdiv(L.E, 8), g);
+            k_edge_runs_fused<<<blocks, 256, 0, c.stream>>>(L.E, L.pin_off, L.pin_dat, L.dst_off, L.dst_dat, assign,
+                                                           W.wi, r, conn, pinbound);
+            DHGP_LAUNCHED(c);
+        }
+        return;
+    }
+    seg_sort(c, L.E, L.pin_off, L.pin_dat, assign, tmp_parts);
     if (L.E > 0) {
         if (L.U >= 12 * (int64_t)L.E) {
             int blocks = (int)std::min<int64_t>(cdiv(L.E, 8), (int64_t)c.num_sms * 16);
@@ -800,7 +895,7 @@ __global__ void k_seq_gains_dn(const int64_t *dM, const int64_t *inc_off, const 
 
 void refine_level(Ctx &c, const DLevel &L, const DWeights &W, int32_t *assign, int32_t K, int64_t omega,
                   int64_t delta, int32_t max_rounds, int32_t level, std::vector<double> &conns,
-                  const RoundObserver *obs) {
+                  const RoundObserver *obs, int32_t max_edge_pins) {
     static bool attr = false;
     if (!attr) {
         DHGP_CUDA(cudaFuncSetAttribute(k_propose_warp<unsigned>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -852,7 +947,7 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, int32_t *assign, i
     bool need_final = false;
     for (int32_t rnd = 0; rnd < max_rounds; rnd++) {
         // --- A11/A12/A16 + A13 ---------------------------------------------
-        build_runs(c, L, W, assign, r, tmp_parts, pinbound, K, conn_d);
+        build_runs(c, L, W, assign, r, tmp_parts, pinbound, K, conn_d, max_edge_pins);
         c.zero(psizes, K);
         if (N > 0) {
             k_part_sizes<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(N, assign, L.size, psizes);
@@ -865,12 +960,17 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, int32_t *assign, i
             ProposeArgs a{N, K, L.inc_off, L.inc_dat, L.pin_off, W.wi, r, assign, psizes, L.size, omega,
                           target, gain, ctr, big, ctr + 1};
             if (N > 0) {
-                int blocks = (int)std::min<int64_t>(cdiv(N, PR_WARPS), (int64_t)c.num_sms * 2);
-                if (W.wsum < (1ll << 32))
+                if (W.wsum < (1ll << 32)) {
+                    static int g32 = resident_grid(c, k_propose_warp<unsigned>, PR_WARPS * 32, pr_smem<unsigned>());
+                    int blocks = (int)std::min<int64_t>(cdiv(N, PR_WARPS), g32);
                     k_propose_warp<unsigned><<<blocks, PR_WARPS * 32, pr_smem<unsigned>(), c.stream>>>(a);
-                else
+                } else {
+                    static int g64 = resident_grid(c, k_propose_warp<unsigned long long>, PR_WARPS * 32,
+                                                   pr_smem<unsigned long long>());
+                    int blocks = (int)std::min<int64_t>(cdiv(N, PR_WARPS), g64);
                     k_propose_warp<unsigned long long>
                         <<<blocks, PR_WARPS * 32, pr_smem<unsigned long long>(), c.stream>>>(a);
+                }
                 DHGP_LAUNCHED(c);
                 if (K <= PH_MAXK) {
                     const size_t sm = (size_t)K * (W.wsum < (1ll << 32) ? 4 : 8) + 4 * (size_t)((K + 31) / 32) + 16;
@@ -890,30 +990,40 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, int32_t *assign, i
             DHGP_LAUNCHED(c);
         }
         scan_excl<uint8_t>(c, flags, mpos, N);
+        // ---- sync 1: M and the connectivity of the round's assignment -----
+        int64_t M = 0;
+        unsigned long long conn_h = 0;
+        c.d2h(&M, dM, 1);
+        c.d2h(&conn_h, conn_d, 1);
+        c.sync();
+        conns.push_back((double)(int64_t)conn_h);
+        need_final = false;
+        if (M == 0) break;
         if (N > 0) {
             k_mover_keys<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(N, flags, mpos, gain, W.wsum, mk, mv);
             DHGP_LAUNCHED(c);
         }
-        radix_sort_pairs(c, mk, mv, mkt, mvt, N, dM, gmax_bits);
+        if (M <= kSmallSort)
+            small_sort_pairs(c, mk, mv, M);  // vals (nodes) are distinct and ascend: stable
+        else
+            radix_sort_pairs(c, mk, mv, mkt, mvt, M, nullptr, gmax_bits);
         fill_i32(c, pos, -1, N);
-        if (N > 0) {
-            k_build_moves_dn<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(dM, mv, assign, target, gain, node, from,
-                                                                          to, giso, pos);
-            DHGP_LAUNCHED(c);
+        k_build_moves_dn<<<(unsigned)cdiv(M, 256), 256, 0, c.stream>>>(dM, mv, assign, target, gain, node, from, to,
+                                                                       giso, pos);
+        DHGP_LAUNCHED(c);
+        {
             KScope ks(c, "seq_gains", 0.0);
-            int blocks = (int)std::min<int64_t>(cdiv(N, 8), (int64_t)c.num_sms * 16);
+            int blocks = (int)std::min<int64_t>(cdiv(M, 8), (int64_t)c.num_sms * 16);
             k_seq_gains_dn<<<blocks, 256, 0, c.stream>>>(dM, L.inc_off, L.inc_dat, L.pin_off, L.pin_dat, W.wi, r,
                                                           node, from, to, giso, pos, gseq);
             DHGP_LAUNCHED(c);
         }
-        // --- A17 events (key bits sized for the capacity N) -----------------
-        const int ibits = ibits_cap;
+        // --- A17 events: key = track | part | move index --------------------
+        const int ibits = std::max(1, bitlen((uint64_t)M));
         EvArgs ev{ibits, pbits, ek, evv, ecount};
         c.zero(ctr, 4);
-        if (N > 0) {
-            k_size_events_dn<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(dM, node, from, to, L.size, ev);
-            DHGP_LAUNCHED(c);
-        }
+        k_size_events_dn<<<(unsigned)cdiv(M, 256), 256, 0, c.stream>>>(dM, node, from, to, L.size, ev);
+        DHGP_LAUNCHED(c);
         if (L.E > 0) {
             k_inbound_events<<<(unsigned)cdiv(L.E, 256), 256, 0, c.stream>>>(L.E, L.dst_off, L.dst_dat, L.pin_off, r,
                                                                            pos, from, to, ev, big, ctr);
@@ -922,18 +1032,12 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, int32_t *assign, i
                                                                      ev, big, ctr, ctr + 2);
             DHGP_LAUNCHED(c);
         }
-        // ---- sync 1: M, event count, connectivity --------------------------
-        int64_t M = 0;
-        unsigned long long T = 0, conn_h = 0;
+        // ---- sync 2: event count --------------------------------------------
+        unsigned long long T = 0;
         int32_t hc[4];
-        c.d2h(&M, dM, 1);
         c.d2h(&T, ecount, 1);
-        c.d2h(&conn_h, conn_d, 1);
         c.d2h(hc, ctr, 4);
         c.sync();
-        conns.push_back((double)(int64_t)conn_h);  // connectivity of the round's starting assignment
-        need_final = false;
-        if (M == 0) break;
         if (hc[2]) throw Error{DHGP_ERR_UNSUPPORTED, "too many movers on one h-edge"};
         int64_t kbest = 0, total_gain = 0;
         int64_t *dlt = c.alloc<int64_t>(M + 1);
@@ -941,7 +1045,10 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, int32_t *assign, i
         int64_t *cum = c.alloc<int64_t>(M + 1);
         {
             KScope ks(c, "select", 0.0, N);
-            radix_sort_pairs(c, ek, evv, ekt, evt, (int64_t)T, nullptr, 1 + ibits + pbits);
+            if ((int64_t)T <= kSmallSort)
+                small_sort_pairs(c, ek, evv, (int64_t)T);  // equal keys only need grouping
+            else
+                radix_sort_pairs(c, ek, evv, ekt, evt, (int64_t)T, nullptr, 1 + ibits + pbits);
             int64_t *gs = c.alloc<int64_t>(T), *ss = c.alloc<int64_t>(T), *dv = c.alloc<int64_t>(T);
             int64_t *ex = c.alloc<int64_t>(T + 1), *gst = c.alloc<int64_t>(T), *sst = c.alloc<int64_t>(T);
             c.zero(dlt, M + 1);

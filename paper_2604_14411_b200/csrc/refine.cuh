@@ -21,7 +21,7 @@ using RoundObserver = std::function<void(const RoundRecord &)>;
 // refined in place; connectivity values are appended to `conns`.
 void refine_level(Ctx &c, const DLevel &L, const DWeights &W, int32_t *assign, int32_t K, int64_t omega,
                   int64_t delta, int32_t max_rounds, int32_t level, std::vector<double> &conns,
-                  const RoundObserver *obs);
+                  const RoundObserver *obs, int32_t max_edge_pins);
 
 // connectivity (A12) and per-part sizes / distinct inbound (A13/A16) of an
 // assignment; any of the outputs may be null.
