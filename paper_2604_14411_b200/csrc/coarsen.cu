@@ -511,7 +511,7 @@ void score_scratch_release(Ctx &c, ScoreScratch &s) {
 void score_select(Ctx &c, const DLevel &L, const DWeights &W, int64_t omega, int64_t delta, int32_t *pair,
                   double *score, ScoreScratch &s) {
     if (L.N == 0) return;
-    KScope ks(c, "score_select", (double)(16.0 * L.U + 24.0 * L.N), L.N);
+    KScope ks(c, "score_select", (double)(32.0 * L.N + 8.0 * L.U + 16.0 * L.E + 4.0 * L.Sin), L.N);
     static bool attr = false;
     if (!attr) {
         DHGP_CUDA(cudaFuncSetAttribute(k_score_warp<unsigned>, cudaFuncAttributeMaxDynamicSharedMemorySize,

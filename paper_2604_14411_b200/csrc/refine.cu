@@ -790,7 +790,7 @@ __global__ void k_apply(int64_t k, const int32_t *node, const int32_t *to, int32
 static void build_runs(Ctx &c, const DLevel &L, const DWeights &W, const int32_t *assign, Runs &r,
                        int32_t *tmp_parts, int64_t *pinbound, int32_t K, unsigned long long *conn,
                        int32_t max_edge_pins) {
-    KScope ks(c, "edge_runs", (double)(8.0 * L.U + 4.0 * L.U + 12.0 * L.U + 4.0 * L.Pd + 24.0 * L.E));
+    KScope ks(c, "edge_runs", (double)(20.0 * L.E + 20.0 * L.U + 8.0 * L.Pd));
     c.zero(conn, 1);
     if (pinbound) c.zero(pinbound, K);
     if (max_edge_pins <= 128) {
@@ -955,7 +955,7 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, int32_t *assign, i
         }
         // --- A14 propose (warp tier + block tier, no host sync) -------------
         {
-            KScope ks(c, "propose", (double)(12.0 * L.U + 16.0 * L.U + 24.0 * N), N);
+            KScope ks(c, "propose", (double)(28.0 * N + 12.0 * L.U + 20.0 * L.E + 8.0 * K), N);
             c.zero(ctr, 4);
             ProposeArgs a{N, K, L.inc_off, L.inc_dat, L.pin_off, W.wi, r, assign, psizes, L.size, omega,
                           target, gain, ctr, big, ctr + 1};
