@@ -70,12 +70,11 @@ struct ScoreArgs {
     int32_t *big_count;
     int32_t *heavy_list;  // nodes for the block tier (many incident h-edges)
     int32_t *heavy_count;
+    Tiers t;
 };
 
 constexpr int SS_WARPS = 8;
 constexpr int SS_CAP = 1024;   // hash slots per warp (power of two)
-constexpr int SS_LIMIT = 720;  // distinct neighbours before escalation
-constexpr int SS_HEAVY_INC = 192;  // incident h-edges above which a block takes the node
 // accumulator: 32-bit when the total weight < 2^32 (native shared atomics;
 // 64-bit shared atomicAdd is a CAS spin loop on sm_100a), else 64-bit
 template <class Acc>
@@ -114,7 +113,7 @@ __global__ void __launch_bounds__(SS_WARPS * 32) k_score_warp(ScoreArgs a) {
         node = __shfl_sync(FULL_MASK, node, 0);
         if (node >= a.N) break;
         const int64_t ilo = a.inc_off[node], ihi = a.inc_off[node + 1];
-        if (ihi - ilo > SS_HEAVY_INC) {  // hub: a whole block per node
+        if (ihi - ilo > a.t.ss_heavy_inc) {  // hub: a whole block per node
             if (lane == 0) a.heavy_list[atomicAdd(a.heavy_count, 1)] = node;
             continue;
         }
@@ -137,7 +136,7 @@ __global__ void __launch_bounds__(SS_WARPS * 32) k_score_warp(ScoreArgs a) {
                 if (k == -1) {
                     int prev = atomicCAS(&keys[slot], -1, m);
                     if (prev == -1) {
-                        if (atomicAdd(&snk[w], 1) >= SS_LIMIT) sover[w] = 1;
+                        if (atomicAdd(&snk[w], 1) >= a.t.ss_limit) sover[w] = 1;
                         k = m;
                     } else {
                         k = prev;
@@ -213,7 +212,6 @@ __global__ void __launch_bounds__(SS_WARPS * 32) k_score_warp(ScoreArgs a) {
 // with more distinct neighbours than the table holds go to the dense tier.
 constexpr int SH_THREADS = 1024;
 constexpr int SH_CAP = 16384;
-constexpr int SH_LIMIT = 12288;
 template <class Acc>
 constexpr int sh_smem() { return SH_CAP * (4 + (int)sizeof(Acc)); }
 
@@ -252,7 +250,7 @@ __global__ void __launch_bounds__(SH_THREADS) k_score_heavy(ScoreArgs a) {
                               if (k == -1) {
                                   int prev = atomicCAS(&keys[slot], -1, m);
                                   if (prev == -1) {
-                                      if (atomicAdd(&snk, 1) >= SH_LIMIT) sover = 1;
+                                      if (atomicAdd(&snk, 1) >= a.t.sh_limit) sover = 1;
                                       k = m;
                                   } else {
                                       k = prev;
@@ -485,8 +483,8 @@ __global__ void k_fill_ll(long long *p, long long v, int64_t n) {
 
 void score_scratch_init(Ctx &c, ScoreScratch &s, int64_t n_cap) {
     s.cap = std::max<int64_t>(n_cap, 1);
-    s.blocks = 16;
-    while (s.blocks > 1 && (int64_t)s.blocks * s.cap * 20 > (2ll << 30)) s.blocks >>= 1;
+    // as many dense rows (20 B per node id each) as 4 GiB allows, <= 2 per SM
+    s.blocks = (int)std::max<int64_t>(1, std::min<int64_t>(2ll * c.num_sms, (4ll << 30) / (20 * s.cap)));
     s.dense = c.alloc<long long>((int64_t)s.blocks * s.cap);
     s.cval = c.alloc<long long>((int64_t)s.blocks * s.cap);
     s.touched = c.alloc<int32_t>((int64_t)s.blocks * s.cap);
@@ -526,7 +524,7 @@ void score_select(Ctx &c, const DLevel &L, const DWeights &W, int64_t omega, int
     }
     c.zero(s.ctr, 3);
     ScoreArgs a{L.N, L.inc_off, L.inc_dat, L.pin_off, L.pin_dat, W.wi, L.size, L.in_off, L.in_dat, omega, delta,
-                pair, score, s.ctr, s.big, s.ctr + 1, s.heavy, s.ctr + 2};
+                pair, score, s.ctr, s.big, s.ctr + 1, s.heavy, s.ctr + 2, tiers()};
     if (W.wsum < (1ll << 32)) {
         static int g32 = resident_grid(c, k_score_warp<unsigned>, SS_WARPS * 32, ss_smem<unsigned>());
         int blocks = (int)std::min<int64_t>(cdiv(L.N, SS_WARPS), g32);
@@ -802,6 +800,7 @@ void contract_count(Ctx &c, DLevel &fine, const int32_t *match, const uint8_t *i
                                                          coarse.size);
     DHGP_LAUNCHED(c);
     // per-h-edge families: sorted unique gamma image (coarsen.py:163-166)
+    KScope kcs(c, "cc_edges");
     s.tmp_src = c.alloc<int32_t>(fine.Ps);
     s.tmp_dst = c.alloc<int32_t>(fine.Pd);
     s.tmp_pin = c.alloc<int32_t>(fine.U);
@@ -819,6 +818,8 @@ void contract_count(Ctx &c, DLevel &fine, const int32_t *match, const uint8_t *i
     coarse.pin_off = c.alloc<int64_t>((int64_t)E + 1);
     scan_excl<int64_t>(c, cnt, coarse.pin_off, E);
     c.free(cnt);
+    kcs.close();
+    KScope kcn(c, "cc_nodes");
     // per-node families: union of the two members' sorted lists
     int64_t *ncnt = c.alloc<int64_t>(N);
     s.big_in = c.alloc<int32_t>(N);
@@ -845,18 +846,30 @@ void contract_write(Ctx &c, DLevel &fine, DLevel &coarse, ContractScratch &s, co
     coarse.Pd = st.pd;
     coarse.U = st.u;
     coarse.Sin = st.sin;
-    coarse.src_dat = c.alloc<int32_t>(st.ps);
-    coarse.dst_dat = c.alloc<int32_t>(st.pd);
-    coarse.pin_dat = c.alloc<int32_t>(st.u);
-    coarse.in_dat = c.alloc<int32_t>(st.sin);
-    coarse.inc_dat = c.alloc<int32_t>(st.uinc);
-    seg_unique_write(c, E, fine.src_off, s.tmp_src, coarse.src_off, coarse.src_dat);
-    seg_unique_write(c, E, fine.dst_off, s.tmp_dst, coarse.dst_off, coarse.dst_dat);
-    seg_unique_write(c, E, fine.pin_off, s.tmp_pin, coarse.pin_off, coarse.pin_dat);
-    merge_union_write(c, st.nc, s.ma, s.mb, fine.in_off, fine.in_dat, coarse.in_off, coarse.in_dat, s.big_in,
-                      s.big_cnt);
-    merge_union_write(c, st.nc, s.ma, s.mb, fine.inc_off, fine.inc_dat, coarse.inc_off, coarse.inc_dat, s.big_inc,
-                      s.big_cnt + 1);
+    {
+        KScope k1(c, "cw_alloc");
+        coarse.src_dat = c.alloc<int32_t>(st.ps);
+        coarse.dst_dat = c.alloc<int32_t>(st.pd);
+        coarse.pin_dat = c.alloc<int32_t>(st.u);
+        coarse.in_dat = c.alloc<int32_t>(st.sin);
+        coarse.inc_dat = c.alloc<int32_t>(st.uinc);
+    }
+    {
+        KScope k2(c, "cw_unique");
+        seg_unique_write(c, E, fine.src_off, s.tmp_src, coarse.src_off, coarse.src_dat);
+        seg_unique_write(c, E, fine.dst_off, s.tmp_dst, coarse.dst_off, coarse.dst_dat);
+        seg_unique_write(c, E, fine.pin_off, s.tmp_pin, coarse.pin_off, coarse.pin_dat);
+    }
+    {
+        KScope k2(c, "cw_merge_in");
+        merge_union_write(c, st.nc, s.ma, s.mb, fine.in_off, fine.in_dat, coarse.in_off, coarse.in_dat, s.big_in,
+                          s.big_cnt);
+    }
+    {
+        KScope k2(c, "cw_merge_inc");
+        merge_union_write(c, st.nc, s.ma, s.mb, fine.inc_off, fine.inc_dat, coarse.inc_off, coarse.inc_dat,
+                          s.big_inc, s.big_cnt + 1);
+    }
     contract_release(c, s);
 }
 

@@ -123,8 +123,11 @@ struct KScope {
             cudaEventRecord(t0, c.stream);
         }
     }
-    ~KScope() {
+    ~KScope() { close(); }
+    // ends the scope early (the destructor then does nothing)
+    void close() {
         if (idx >= 0) c.kend(idx, bytes);
+        idx = -1;
         if (t0) {
             cudaEventRecord(t1, c.stream);
             cudaEventSynchronize(t1);
@@ -133,9 +136,23 @@ struct KScope {
             trace_print(name, ms, tag);
             cudaEventDestroy(t0);
             cudaEventDestroy(t1);
+            t0 = t1 = nullptr;
         }
     }
 };
+
+// Escalation thresholds of the tiered per-node kernels (warp -> block ->
+// dense).  DHGP_FORCE_TIERS=1 shrinks them so that small parity tests drive
+// every tier; results never depend on them.
+struct Tiers {
+    int ss_limit = 720;       // score: distinct neighbours per warp table
+    int ss_heavy_inc = 192;   // score: incident h-edges above which a block takes the node
+    int sh_limit = 12288;     // score: distinct neighbours per block table
+    int pr_limit = 400;       // propose: distinct parts per warp table
+    int pr_heavy_inc = 128;   // propose: incident h-edges above which a block takes the node
+    int pm_limit = 3072;      // propose: distinct parts per medium-tier table
+};
+const Tiers &tiers();
 
 inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 

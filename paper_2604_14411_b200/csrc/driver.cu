@@ -28,6 +28,22 @@ bool trace_enabled() {
     }
     return on == 1;
 }
+const Tiers &tiers() {
+    static Tiers t = [] {
+        Tiers x;
+        const char *e = getenv("DHGP_FORCE_TIERS");
+        if (e && e[0] == '1') {
+            x.ss_limit = 3;
+            x.ss_heavy_inc = 2;
+            x.sh_limit = 6;
+            x.pr_limit = 2;
+            x.pr_heavy_inc = 1;
+            x.pm_limit = 3;
+        }
+        return x;
+    }();
+    return t;
+}
 void trace_print(const char *name, double ms, long long tag) { fprintf(stderr, "trace %s %.4f %lld\n", name, ms, tag); }
 
 // ---------------------------------------------------------------------------
@@ -157,6 +173,28 @@ static void rebuild_levels(Ctx &c, std::vector<DLevel> &levels, size_t hi) {
     c.free(status);
 }
 
+// Grows the device's stream-ordered pool once to `want` bytes (capped at 60%
+// of the free memory), so that level allocations during coarsening never
+// wait on the driver to map fresh physical memory.  The pool keeps what it
+// reserved (release threshold = max), so later calls pay nothing.
+static size_t g_pool_reserved[64];
+static void reserve_pool(Ctx &c, size_t want) {
+    if (want <= g_pool_reserved[c.device]) return;
+    size_t freeb = 0, total = 0;
+    DHGP_CUDA(cudaMemGetInfo(&freeb, &total));
+    const size_t cap = g_pool_reserved[c.device] + (size_t)(0.6 * (double)freeb);
+    want = std::min(want, cap);
+    if (want <= g_pool_reserved[c.device] || want < ((size_t)64 << 20)) return;
+    void *p = nullptr;
+    if (cudaMallocAsync(&p, want, c.stream) != cudaSuccess) {
+        cudaGetLastError();
+        return;
+    }
+    DHGP_CUDA(cudaFreeAsync(p, c.stream));
+    c.sync();
+    g_pool_reserved[c.device] = want;
+}
+
 static double now_ms() {
     return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
@@ -184,6 +222,12 @@ static void run_partition(Ctx &c, const DInput &in, const dhgp_config &cfg, Part
     }
     std::vector<DLevel> levels(1);
     build_level0(c, in, levels[0]);
+    {
+        const DLevel &l0 = levels[0];
+        const size_t b0 = 8 * (3 * (size_t)l0.E + 2 * (size_t)l0.N + 8) +
+                          4 * ((size_t)l0.Ps + l0.Pd + 2 * l0.U + l0.Sin + 2 * (size_t)l0.N);
+        reserve_pool(c, 32 * b0);
+    }
     const int32_t N0 = in.N;
     if (N0 > 0) {
         int32_t bs, bi;

@@ -231,14 +231,59 @@ struct ProposeArgs {
     int32_t *target;
     int64_t *gain;
     int32_t *next;
-    int32_t *big_list;
+    int32_t *big_list;  // warp tier -> medium tier
     int32_t *big_count;
+    int32_t *dense_list;  // medium tier -> dense tier
+    int32_t *dense_count;
+    Tiers t;
 };
+
+// Flattened iteration over the (h-edge, run) pairs of a node's incident
+// h-edges: the warp takes 32 incident h-edges at a time (ilo + first, then
+// + stride) and spreads their runs evenly over the lanes, so one wide h-edge
+// does not serialise on one lane.  f(e, w(e), k) with k the run's index in
+// the run arrays.  Returns this lane's share of sum w(e).
+template <class F>
+__device__ __forceinline__ int64_t warp_for_runs(const int32_t *inc_dat, int64_t ilo, int64_t ihi, int64_t first,
+                                                 int64_t stride, const int64_t *pin_off, const int32_t *len,
+                                                 const int64_t *wi, F &&f) {
+    const int lane = lane_id();
+    int64_t total = 0;
+    for (int64_t base = ilo + first; base < ihi; base += stride) {
+        const int64_t ii = base + lane;
+        int32_t e = -1;
+        int64_t plo = 0, we = 0;
+        int l = 0;
+        if (ii < ihi) {
+            e = inc_dat[ii];
+            plo = pin_off[e];
+            l = len[e];
+            we = wi[e];
+            total += we;
+        }
+        const int incl = warp_incl_scan(l);
+        const int tot = __shfl_sync(FULL_MASK, incl, 31);
+        const int excl = incl - l;
+        for (int s0 = 0; s0 < tot; s0 += 32) {
+            const int sl = s0 + lane;
+            int owner = 0;
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+                const int ex = __shfl_sync(FULL_MASK, excl, owner + step);
+                if (ex <= sl) owner += step;
+            }
+            const int32_t oe = __shfl_sync(FULL_MASK, e, owner);
+            const int64_t oplo = __shfl_sync(FULL_MASK, plo, owner);
+            const int64_t owe = __shfl_sync(FULL_MASK, we, owner);
+            const int oex = __shfl_sync(FULL_MASK, excl, owner);
+            if (sl < tot) f(oe, owe, oplo + (sl - oex));
+        }
+    }
+    return total;
+}
 
 constexpr int PR_WARPS = 8;
 constexpr int PR_CAP = 512;
-constexpr int PR_LIMIT = 400;
-constexpr int PR_HEAVY_INC = 128;
 // 32-bit accumulators when the total weight < 2^32 (native shared atomics)
 template <class Acc>
 constexpr int pr_smem() { return PR_WARPS * PR_CAP * (4 + (int)sizeof(Acc)); }
@@ -270,7 +315,7 @@ __global__ void __launch_bounds__(PR_WARPS * 32) k_propose_warp(ProposeArgs a) {
             if (lane == 0) a.target[node] = -1;
             continue;
         }
-        if (ihi - ilo > PR_HEAVY_INC) {  // many incident h-edges: a whole block takes it
+        if (ihi - ilo > a.t.pr_heavy_inc) {  // many incident h-edges: a whole block takes it
             if (lane == 0) a.big_list[atomicAdd(a.big_count, 1)] = node;
             continue;
         }
@@ -285,38 +330,30 @@ __global__ void __launch_bounds__(PR_WARPS * 32) k_propose_warp(ProposeArgs a) {
         __syncwarp();
         const int32_t ps = a.assign[node];
         int64_t total = 0, saving = 0;
-        for (int64_t ii = ilo + lane; ii < ihi; ii += 32) {
-            const int32_t e = a.inc_dat[ii];
-            const int64_t we = a.wi[e];
-            const int64_t lo = a.pin_off[e];
-            const int32_t lam = a.r.len[e];
-            total += we;
-            for (int32_t j = 0; j < lam; j++) {
-                const int32_t p = a.r.part[lo + j];
-                if (p == ps && a.r.cnt[lo + j] == 1) saving += we;
-                if (sover[w]) continue;
-                uint32_t h = pslot(p);
-                bool done = false;
-                for (int probe = 0; probe < PR_CAP && !done; probe++) {
-                    const int slot = (h + probe) & (PR_CAP - 1);
-                    int k = keys[slot];
-                    if (k == -1) {
-                        int prev = atomicCAS(&keys[slot], -1, p);
-                        if (prev == -1) {
-                            if (atomicAdd(&snk[w], 1) >= PR_LIMIT) sover[w] = 1;
-                            k = p;
-                        } else {
-                            k = prev;
-                        }
-                    }
-                    if (k == p) {
-                        atomicAdd(&vals[slot], (Acc)we);
-                        done = true;
+        total = warp_for_runs(a.inc_dat, ilo, ihi, 0, 32, a.pin_off, a.r.len, a.wi, [&](int32_t, int64_t we, int64_t k) {
+            const int32_t p = a.r.part[k];
+            if (p == ps && a.r.cnt[k] == 1) saving += we;
+            if (sover[w]) return;
+            const uint32_t h = pslot(p);
+            for (int probe = 0; probe < PR_CAP; probe++) {
+                const int slot = (h + probe) & (PR_CAP - 1);
+                int kk = keys[slot];
+                if (kk == -1) {
+                    const int prev = atomicCAS(&keys[slot], -1, p);
+                    if (prev == -1) {
+                        if (atomicAdd(&snk[w], 1) >= a.t.pr_limit) sover[w] = 1;
+                        kk = p;
+                    } else {
+                        kk = prev;
                     }
                 }
-                if (!done) sover[w] = 1;
+                if (kk == p) {
+                    atomicAdd(&vals[slot], (Acc)we);
+                    return;
+                }
             }
-        }
+            sover[w] = 1;
+        });
         total = warp_sum(total);
         saving = warp_sum(saving);
         __syncwarp();
@@ -355,41 +392,176 @@ __global__ void __launch_bounds__(PR_WARPS * 32) k_propose_warp(ProposeArgs a) {
     }
 }
 
-// Heavy tier for K <= PH_MAXK: one block per node, present[] as a dense
-// shared array indexed by part id plus a touched bitmap (no hashing).
-constexpr int PH_THREADS = 1024;
-constexpr int PH_MAXK = 16384;
+// Medium tier: one 256-thread CTA per node with a 4096-slot shared hash
+// table (nodes with many incident h-edges, or more distinct parts than a
+// warp's table holds).  Nodes touching more than PM_LIMIT parts go on to the
+// dense tier.
+constexpr int PM_THREADS = 256;
+constexpr int PM_CAP = 8192;
 template <class Acc>
-__global__ void __launch_bounds__(PH_THREADS) k_propose_heavy(ProposeArgs a) {
+constexpr int pm_smem() { return PM_CAP * (4 + (int)sizeof(Acc)); }
+__device__ __forceinline__ uint32_t pmslot(int32_t p) { return ((uint32_t)p * 2654435761u) >> (32 - 13); }
+
+__device__ __forceinline__ void block_best_gain(long long bg, int32_t bp, long long *r_g, int32_t *r_p, int nw,
+                                                long long *out_g, int32_t *out_p) {
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        long long og = __shfl_xor_sync(FULL_MASK, bg, d);
+        int32_t op = __shfl_xor_sync(FULL_MASK, bp, d);
+        if (op >= 0 && better_gain(og, op, bg, bp)) {
+            bg = og;
+            bp = op;
+        }
+    }
+    if (lane_id() == 0) {
+        r_g[warp_id()] = bg;
+        r_p[warp_id()] = bp;
+    }
+    __syncthreads();
+    long long g = r_g[0];
+    int32_t p = r_p[0];
+    for (int j = 1; j < nw; j++)
+        if (r_p[j] >= 0 && better_gain(r_g[j], r_p[j], g, p)) {
+            g = r_g[j];
+            p = r_p[j];
+        }
+    *out_g = g;
+    *out_p = p;
+}
+
+template <class Acc>
+__global__ void __launch_bounds__(PM_THREADS) k_propose_mid(ProposeArgs a) {
     extern __shared__ unsigned long long smem_u64[];
-    Acc *pres = (Acc *)smem_u64;
-    uint32_t *touched = (uint32_t *)(pres + a.K);
-    __shared__ long long r_a[PH_THREADS / 32], r_b[PH_THREADS / 32];
-    __shared__ int32_t r_p[PH_THREADS / 32];
-    const int w = warp_id(), lane = lane_id(), nw = PH_THREADS / 32;
-    const int nbig = *a.big_count;
-    const int tw = (a.K + 31) >> 5;
-    for (int t = blockIdx.x; t < nbig; t += gridDim.x) {
+    Acc *vals = (Acc *)smem_u64;
+    int32_t *keys = (int32_t *)(vals + PM_CAP);
+    __shared__ int32_t snk;
+    __shared__ volatile int32_t sover;
+    __shared__ long long r_a[PM_THREADS / 32], r_b[PM_THREADS / 32];
+    __shared__ int32_t r_p[PM_THREADS / 32];
+    const int w = warp_id(), lane = lane_id(), nw = PM_THREADS / 32;
+    const int nmid = *a.big_count;
+    for (int t = blockIdx.x; t < nmid; t += gridDim.x) {
         const int32_t node = a.big_list[t];
-        for (int p = threadIdx.x; p < a.K; p += PH_THREADS) pres[p] = 0;
-        for (int p = threadIdx.x; p < tw; p += PH_THREADS) touched[p] = 0;
+        for (int s = threadIdx.x; s < PM_CAP; s += PM_THREADS) {
+            keys[s] = -1;
+            vals[s] = 0;
+        }
+        if (threadIdx.x == 0) {
+            snk = 0;
+            sover = 0;
+        }
         __syncthreads();
         const int64_t ilo = a.inc_off[node], ihi = a.inc_off[node + 1];
         const int32_t ps = a.assign[node];
         long long total = 0, saving = 0;
-        for (int64_t ii = ilo + threadIdx.x; ii < ihi; ii += PH_THREADS) {
-            const int32_t e = a.inc_dat[ii];
-            const int64_t we = a.wi[e];
-            const int64_t lo = a.pin_off[e];
-            const int32_t lam = a.r.len[e];
-            total += we;
-            for (int32_t j = 0; j < lam; j++) {
-                const int32_t p = a.r.part[lo + j];
-                if (p == ps && a.r.cnt[lo + j] == 1) saving += we;
-                atomicAdd(&pres[p], (Acc)we);
-                atomicOr(&touched[p >> 5], 1u << (p & 31));
+        total = warp_for_runs(a.inc_dat, ilo, ihi, (int64_t)w * 32, (int64_t)nw * 32, a.pin_off, a.r.len, a.wi,
+                              [&](int32_t, int64_t we, int64_t k) {
+                                  const int32_t p = a.r.part[k];
+                                  if (p == ps && a.r.cnt[k] == 1) saving += we;
+                                  if (sover) return;
+                                  const uint32_t h = pmslot(p);
+                                  for (int probe = 0; probe < PM_CAP; probe++) {
+                                      const int slot = (h + probe) & (PM_CAP - 1);
+                                      int kk = keys[slot];
+                                      if (kk == -1) {
+                                          const int prev = atomicCAS(&keys[slot], -1, p);
+                                          if (prev == -1) {
+                                              if (atomicAdd(&snk, 1) >= a.t.pm_limit) sover = 1;
+                                              kk = p;
+                                          } else {
+                                              kk = prev;
+                                          }
+                                      }
+                                      if (kk == p) {
+                                          atomicAdd(&vals[slot], (Acc)we);
+                                          return;
+                                      }
+                                  }
+                                  sover = 1;
+                              });
+        total = warp_sum(total);
+        saving = warp_sum(saving);
+        if (lane == 0) {
+            r_a[w] = total;
+            r_b[w] = saving;
+        }
+        __syncthreads();
+        if (sover) {
+            if (threadIdx.x == 0) a.dense_list[atomicAdd(a.dense_count, 1)] = node;
+            __syncthreads();
+            continue;
+        }
+        total = 0;
+        saving = 0;
+        for (int j = 0; j < nw; j++) {
+            total += r_a[j];
+            saving += r_b[j];
+        }
+        __syncthreads();
+        const int64_t sz = a.size[node];
+        long long bg = 0;
+        int32_t bp = -1;
+        for (int s = threadIdx.x; s < PM_CAP; s += PM_THREADS) {
+            const int32_t p = keys[s];
+            if (p < 0 || p == ps || a.psizes[p] + sz > a.omega) continue;
+            const long long g = saving - (total - (long long)vals[s]);
+            if (better_gain(g, p, bg, bp)) {
+                bg = g;
+                bp = p;
             }
         }
+        long long g;
+        int32_t p;
+        block_best_gain(bg, bp, r_a, r_p, nw, &g, &p);
+        if (threadIdx.x == 0) {
+            const bool emit = p >= 0 && g > 0;
+            a.target[node] = emit ? p : -1;
+            a.gain[node] = emit ? g : 0;
+        }
+        __syncthreads();
+    }
+}
+
+// Dense tier for K <= PH_MAXK: one block per node, present[] as a dense
+// shared array indexed by part id plus the list of touched parts (each
+// node costs O(its distinct parts), not O(K)).
+constexpr int PH_THREADS = 1024;
+// largest K whose dense arrays (present + touched list + bitmap) fit the
+// 227 KB of shared memory of one CTA
+template <class Acc>
+constexpr int ph_maxk() { return (int)((220 * 1024 - 64) * 8 / (8 * (sizeof(Acc) + 4) + 1)); }
+template <class Acc>
+constexpr size_t ph_smem(int K) { return (size_t)K * (sizeof(Acc) + 4) + 4 * (size_t)((K + 31) / 32) + 16; }
+template <class Acc>
+__global__ void __launch_bounds__(PH_THREADS) k_propose_heavy(ProposeArgs a) {
+    extern __shared__ unsigned long long smem_u64[];
+    Acc *pres = (Acc *)smem_u64;
+    int32_t *tlist = (int32_t *)(pres + a.K);
+    uint32_t *touched = (uint32_t *)(tlist + a.K);
+    __shared__ int32_t s_nt;
+    __shared__ long long r_a[PH_THREADS / 32], r_b[PH_THREADS / 32];
+    __shared__ int32_t r_p[PH_THREADS / 32];
+    const int w = warp_id(), lane = lane_id(), nw = PH_THREADS / 32;
+    const int nbig = *a.dense_count;
+    if ((int)blockIdx.x >= nbig) return;
+    const int tw = (a.K + 31) >> 5;
+    for (int p = threadIdx.x; p < a.K; p += PH_THREADS) pres[p] = 0;
+    for (int p = threadIdx.x; p < tw; p += PH_THREADS) touched[p] = 0;
+    for (int t = blockIdx.x; t < nbig; t += gridDim.x) {
+        const int32_t node = a.dense_list[t];
+        if (threadIdx.x == 0) s_nt = 0;
+        __syncthreads();
+        const int64_t ilo = a.inc_off[node], ihi = a.inc_off[node + 1];
+        const int32_t ps = a.assign[node];
+        long long total = 0, saving = 0;
+        total = warp_for_runs(a.inc_dat, ilo, ihi, (int64_t)w * 32, (int64_t)nw * 32, a.pin_off, a.r.len, a.wi,
+                              [&](int32_t, int64_t we, int64_t k) {
+                                  const int32_t p = a.r.part[k];
+                                  if (p == ps && a.r.cnt[k] == 1) saving += we;
+                                  atomicAdd(&pres[p], (Acc)we);
+                                  const uint32_t bit = 1u << (p & 31);
+                                  if (!(atomicOr(&touched[p >> 5], bit) & bit)) tlist[atomicAdd(&s_nt, 1)] = p;
+                              });
         total = warp_sum(total);
         saving = warp_sum(saving);
         if (lane == 0) {
@@ -403,40 +575,27 @@ __global__ void __launch_bounds__(PH_THREADS) k_propose_heavy(ProposeArgs a) {
             total += r_a[j];
             saving += r_b[j];
         }
+        const int nt = s_nt;
+        __syncthreads();
         const int64_t sz = a.size[node];
         long long bg = 0;
         int32_t bp = -1;
-        for (int p = threadIdx.x; p < a.K; p += PH_THREADS) {
-            if (!((touched[p >> 5] >> (p & 31)) & 1u) || p == ps || a.psizes[p] + sz > a.omega) continue;
-            const long long g = saving - (total - (long long)pres[p]);
+        for (int i = threadIdx.x; i < nt; i += PH_THREADS) {
+            const int32_t p = tlist[i];
+            const long long pv = (long long)pres[p];
+            pres[p] = 0;
+            touched[p >> 5] = 0;
+            if (p == ps || a.psizes[p] + sz > a.omega) continue;
+            const long long g = saving - (total - pv);
             if (better_gain(g, p, bg, bp)) {
                 bg = g;
                 bp = p;
             }
         }
-#pragma unroll
-        for (int d = 16; d > 0; d >>= 1) {
-            long long og = __shfl_xor_sync(FULL_MASK, bg, d);
-            int32_t op = __shfl_xor_sync(FULL_MASK, bp, d);
-            if (op >= 0 && better_gain(og, op, bg, bp)) {
-                bg = og;
-                bp = op;
-            }
-        }
-        __syncthreads();
-        if (lane == 0) {
-            r_a[w] = bg;
-            r_p[w] = bp;
-        }
-        __syncthreads();
+        long long g;
+        int32_t p;
+        block_best_gain(bg, bp, r_a, r_p, nw, &g, &p);
         if (threadIdx.x == 0) {
-            long long g = r_a[0];
-            int32_t p = r_p[0];
-            for (int j = 1; j < nw; j++)
-                if (r_p[j] >= 0 && better_gain(r_a[j], r_p[j], g, p)) {
-                    g = r_a[j];
-                    p = r_p[j];
-                }
             const bool emit = p >= 0 && g > 0;
             a.target[node] = emit ? p : -1;
             a.gain[node] = emit ? g : 0;
@@ -454,28 +613,22 @@ __global__ void __launch_bounds__(PB_THREADS) k_propose_block(ProposeArgs a, lon
     long long *dense = dense_all + (int64_t)blockIdx.x * a.K;
     int32_t *touched = touched_all + (int64_t)blockIdx.x * a.K;
     const int w = warp_id(), lane = lane_id(), nw = PB_THREADS / 32;
-    const int nbig = *a.big_count;
+    const int nbig = *a.dense_count;
     for (int t = blockIdx.x; t < nbig; t += gridDim.x) {
-        const int32_t node = a.big_list[t];
+        const int32_t node = a.dense_list[t];
         if (threadIdx.x == 0) s_nt = 0;
         __syncthreads();
         const int64_t ilo = a.inc_off[node], ihi = a.inc_off[node + 1];
         const int32_t ps = a.assign[node];
         long long total = 0, saving = 0;
-        for (int64_t ii = ilo + threadIdx.x; ii < ihi; ii += PB_THREADS) {
-            const int32_t e = a.inc_dat[ii];
-            const int64_t we = a.wi[e];
-            const int64_t lo = a.pin_off[e];
-            const int32_t lam = a.r.len[e];
-            total += we;
-            for (int32_t j = 0; j < lam; j++) {
-                const int32_t p = a.r.part[lo + j];
-                if (p == ps && a.r.cnt[lo + j] == 1) saving += we;
-                long long old = atomicCAS((unsigned long long *)&dense[p], ~0ull, 0ull);
-                if (old == -1ll) touched[atomicAdd(&s_nt, 1)] = p;
-                atomicAdd((unsigned long long *)&dense[p], (unsigned long long)we);
-            }
-        }
+        total = warp_for_runs(a.inc_dat, ilo, ihi, (int64_t)w * 32, (int64_t)nw * 32, a.pin_off, a.r.len, a.wi,
+                              [&](int32_t, int64_t we, int64_t k) {
+                                  const int32_t p = a.r.part[k];
+                                  if (p == ps && a.r.cnt[k] == 1) saving += we;
+                                  const long long old = atomicCAS((unsigned long long *)&dense[p], ~0ull, 0ull);
+                                  if (old == -1ll) touched[atomicAdd(&s_nt, 1)] = p;
+                                  atomicAdd((unsigned long long *)&dense[p], (unsigned long long)we);
+                              });
         total = warp_sum(total);
         saving = warp_sum(saving);
         if (lane == 0) {
@@ -903,9 +1056,14 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, int32_t *assign, i
         DHGP_CUDA(cudaFuncSetAttribute(k_propose_warp<unsigned long long>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, pr_smem<unsigned long long>()));
         DHGP_CUDA(cudaFuncSetAttribute(k_propose_heavy<unsigned>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       PH_MAXK * 8 + PH_MAXK / 8 + 64));
+                                       (int)ph_smem<unsigned>(ph_maxk<unsigned>())));
         DHGP_CUDA(cudaFuncSetAttribute(k_propose_heavy<unsigned long long>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, PH_MAXK * 8 + PH_MAXK / 8 + 64));
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)ph_smem<unsigned long long>(ph_maxk<unsigned long long>())));
+        DHGP_CUDA(cudaFuncSetAttribute(k_propose_mid<unsigned>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       pm_smem<unsigned>()));
+        DHGP_CUDA(cudaFuncSetAttribute(k_propose_mid<unsigned long long>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       pm_smem<unsigned long long>()));
         attr = true;
     }
     const int32_t N = L.N;
@@ -924,6 +1082,7 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, int32_t *assign, i
     int32_t *pos = c.alloc<int32_t>(N);
     int32_t *ctr = c.alloc<int32_t>(4);
     int32_t *big = c.alloc<int32_t>(std::max<int64_t>(N, L.E));
+    int32_t *big2 = c.alloc<int32_t>(N);
     unsigned long long *conn_d = c.alloc<unsigned long long>(1);
     uint64_t *mk = c.alloc<uint64_t>(N), *mkt = c.alloc<uint64_t>(N);
     uint32_t *mv = c.alloc<uint32_t>(N), *mvt = c.alloc<uint32_t>(N);
@@ -933,11 +1092,17 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, int32_t *assign, i
     uint64_t *ek = c.alloc<uint64_t>(ecap), *ekt = c.alloc<uint64_t>(ecap);
     uint32_t *evv = c.alloc<uint32_t>(ecap), *evt = c.alloc<uint32_t>(ecap);
     unsigned long long *ecount = c.alloc<unsigned long long>(1);
-    const int pb_blocks = 16;
+    // dense global tier (K too large for shared memory): per-block rows of K
+    // counters + touched lists, as many blocks as ~1 GiB allows (4 per SM max)
+    const int pb_blocks = (int)std::max<int64_t>(
+        1, std::min<int64_t>((int64_t)c.num_sms * 4, (int64_t)(1ll << 30) / std::max<int64_t>(1, 12ll * K)));
     long long *pdense = c.alloc<long long>((int64_t)pb_blocks * K);
     int32_t *ptouched = c.alloc<int32_t>((int64_t)pb_blocks * K);
-    k_fill_ll<<<(unsigned)cdiv((int64_t)pb_blocks * K, 256), 256, 0, c.stream>>>(pdense, -1ll, (int64_t)pb_blocks * K);
-    DHGP_LAUNCHED(c);
+    if (K > 0) {
+        k_fill_ll<<<(unsigned)cdiv((int64_t)pb_blocks * K, 256), 256, 0, c.stream>>>(pdense, -1ll,
+                                                                                   (int64_t)pb_blocks * K);
+        DHGP_LAUNCHED(c);
+    }
     const int gmax_bits = std::max(1, bitlen((uint64_t)W.wsum));
     const int pbits = std::max(1, bitlen((uint64_t)(K > 0 ? K - 1 : 0)));
     const int ibits_cap = std::max(1, bitlen((uint64_t)N));
@@ -958,9 +1123,10 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, int32_t *assign, i
             KScope ks(c, "propose", (double)(28.0 * N + 12.0 * L.U + 20.0 * L.E + 8.0 * K), N);
             c.zero(ctr, 4);
             ProposeArgs a{N, K, L.inc_off, L.inc_dat, L.pin_off, W.wi, r, assign, psizes, L.size, omega,
-                          target, gain, ctr, big, ctr + 1};
+                          target, gain, ctr, big, ctr + 1, big2, ctr + 2, tiers()};
             if (N > 0) {
-                if (W.wsum < (1ll << 32)) {
+                const bool narrow = W.wsum < (1ll << 32);
+                if (narrow) {
                     static int g32 = resident_grid(c, k_propose_warp<unsigned>, PR_WARPS * 32, pr_smem<unsigned>());
                     int blocks = (int)std::min<int64_t>(cdiv(N, PR_WARPS), g32);
                     k_propose_warp<unsigned><<<blocks, PR_WARPS * 32, pr_smem<unsigned>(), c.stream>>>(a);
@@ -972,12 +1138,23 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, int32_t *assign, i
                         <<<blocks, PR_WARPS * 32, pr_smem<unsigned long long>(), c.stream>>>(a);
                 }
                 DHGP_LAUNCHED(c);
-                if (K <= PH_MAXK) {
-                    const size_t sm = (size_t)K * (W.wsum < (1ll << 32) ? 4 : 8) + 4 * (size_t)((K + 31) / 32) + 16;
-                    if (W.wsum < (1ll << 32))
-                        k_propose_heavy<unsigned><<<c.num_sms, PH_THREADS, sm, c.stream>>>(a);
-                    else
-                        k_propose_heavy<unsigned long long><<<c.num_sms, PH_THREADS, sm, c.stream>>>(a);
+                KScope kh(c, "propose_heavy");
+                // medium tier: reads the escalation count on device, exits when zero
+                if (narrow) {
+                    static int m32 = resident_grid(c, k_propose_mid<unsigned>, PM_THREADS, pm_smem<unsigned>());
+                    k_propose_mid<unsigned><<<m32, PM_THREADS, pm_smem<unsigned>(), c.stream>>>(a);
+                } else {
+                    static int m64 = resident_grid(c, k_propose_mid<unsigned long long>, PM_THREADS,
+                                                   pm_smem<unsigned long long>());
+                    k_propose_mid<unsigned long long>
+                        <<<m64, PM_THREADS, pm_smem<unsigned long long>(), c.stream>>>(a);
+                }
+                DHGP_LAUNCHED(c);
+                if (narrow && K <= ph_maxk<unsigned>()) {
+                    k_propose_heavy<unsigned><<<c.num_sms, PH_THREADS, ph_smem<unsigned>(K), c.stream>>>(a);
+                } else if (!narrow && K <= ph_maxk<unsigned long long>()) {
+                    k_propose_heavy<unsigned long long>
+                        <<<c.num_sms, PH_THREADS, ph_smem<unsigned long long>(K), c.stream>>>(a);
                 } else {
                     k_propose_block<<<pb_blocks, PB_THREADS, 0, c.stream>>>(a, pdense, ptouched);
                 }
@@ -1123,7 +1300,7 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, int32_t *assign, i
     }
     for (void *p : {(void *)r.part, (void *)r.cnt, (void *)r.cin, (void *)r.len, (void *)tmp_parts, (void *)psizes,
                     (void *)pinbound, (void *)target, (void *)gain, (void *)flags, (void *)mpos, (void *)pos,
-                    (void *)ctr, (void *)big, (void *)conn_d, (void *)mk, (void *)mkt, (void *)mv, (void *)mvt,
+                    (void *)ctr, (void *)big, (void *)big2, (void *)conn_d, (void *)mk, (void *)mkt, (void *)mv, (void *)mvt,
                     (void *)node, (void *)from, (void *)to, (void *)giso, (void *)gseq, (void *)ek, (void *)ekt,
                     (void *)evv, (void *)evt, (void *)ecount, (void *)pdense, (void *)ptouched})
         c.free(p);

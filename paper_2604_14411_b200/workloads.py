@@ -145,8 +145,11 @@ def power_law(num_nodes: int, num_edges: int, alpha: float = 2.1, k_max: int = 5
         if kk <= 64:
             win = min(4 * kk + 8, num_nodes)
             pins = (base[e] + rs.choice(win, size=kk, replace=False)) % num_nodes
-        else:
-            pins = rs.choice(num_nodes, size=kk, replace=False)
+        else:  # kk distinct ids, uniformly (rejection of repeats, then a random order)
+            pins = np.unique(rs.randint(0, num_nodes, size=kk + kk // 4 + 8))
+            while len(pins) < kk:
+                pins = np.unique(np.concatenate([pins, rs.randint(0, num_nodes, size=kk)]))
+            pins = rs.permutation(pins)[:kk]
         srcs.append(pins[: ks[e]])
         dsts.append(pins[ks[e]:])
     w = rs.randint(1, 10, size=num_edges).astype(np.float64)

@@ -281,3 +281,45 @@ def test_c2_full_size_properties():
     assert all(lv["edges"] == g.num_edges for lv in s1.levels)
     p2, s2 = d.partition(g, d.Config(d.Constraints(omega, delta), max_levels=1 << 20))
     assert np.array_equal(p1.assign, p2.assign) and s1.to_dict() == s2.to_dict()
+
+
+_FORCED_TIERS_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1]); sys.path.insert(0, sys.argv[1] + "/tests")
+from conftest import arrays_of, make_instance
+from oracle import oracle as orc
+import paper_2604_14411_b200 as dp
+from paper_2604_14411_b200 import workloads as W
+cases = []
+rs = np.random.RandomState(77)
+for t in range(8):
+    n = int(rs.randint(50, 600))
+    g, c = make_instance(n, 2 * n, int(rs.choice([3, 5, 8])), seed=8800 + t, omega=int(rs.choice([8, 32, 64])),
+                         delta_slack=int(rs.randint(0, 40)))
+    cases.append((g, c.max_size, c.max_inbound))
+arr = W.power_law(1500, 1500, k_max=200, seed=3)
+indeg = int(np.bincount(arr[5], minlength=1500).max())
+n, w, so, sd, do, dd = arr
+cases.append((dp.Hypergraph._from_csr(n, w, dp.CsrSets(so, sd), dp.CsrSets(do, dd)), 128, max(indeg, 256)))
+for g, om, de in cases:
+    part, st = dp.partition(g, dp.Config(dp.Constraints(om, de), max_levels=1 << 20))
+    a, k, ost, _ = orc.partition(*arrays_of(g), g.node_size, max_size=om, max_inbound=de, max_levels=1 << 20)
+    assert np.array_equal(part.assign, a), "assign differs"
+    assert st.levels == ost["levels"] and st.connectivity_trace == ost["connectivity_trace"]
+print("forced tiers ok", len(cases))
+"""
+
+
+def test_every_kernel_tier_under_forced_escalation():
+    """DHGP_FORCE_TIERS=1 shrinks the warp/block escalation thresholds so that
+    the medium, block and dense tiers of scoring and proposing all run."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = str(Path(__file__).resolve().parents[1])
+    r = subprocess.run([sys.executable, "-c", _FORCED_TIERS_SCRIPT, root], capture_output=True, text=True,
+                       env=dict(os.environ, DHGP_FORCE_TIERS="1"), timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    assert "forced tiers ok" in r.stdout
