@@ -131,6 +131,35 @@ int dhgp_session_kernel_stats(dhgp_session *s, int32_t max_rows, const char **na
                               double *total_ms, double *bytes, int32_t *rows_out);
 int dhgp_session_set_profiling(dhgp_session *s, int32_t on);
 
+/* ---- multi-GPU: node-range sharding ----------------
+ * No reference interface: the reference is single-threaded.  These extend
+ * dhgp_partition (driver.py:76-163) to one process per GPU; the result is
+ * bit-identical to the single-GPU call at every world size.  Scoring
+ * (coarsen.py:93-132), proposals (refine.py:82-116) and in-sequence gains
+ * (refine.py:119-142) are computed per node / move range and completed by an
+ * in-place allgather; everything else runs replicated. */
+#define DHGP_COMM_NCCL 1 /* ncclAllGather on the library stream (libnccl.so.2, loaded at run time) */
+#define DHGP_COMM_HOST 2 /* the caller's allgather over host memory (gloo, MPI, tests) */
+typedef struct dhgp_comm dhgp_comm;
+/* in place: buf holds world * bytes_per_rank bytes; rank r's part is at
+ * r * bytes_per_rank.  Return 0 on success. */
+typedef int (*dhgp_allgather_fn)(void *user, void *buf, int64_t bytes_per_rank);
+int dhgp_comm_nccl_unique_id(uint8_t *id_out /* [128] */);
+int dhgp_comm_init_nccl(int32_t world, int32_t rank, const uint8_t *id /* [128] */, int32_t device,
+                        dhgp_comm **out);
+int dhgp_comm_init_host(int32_t world, int32_t rank, dhgp_allgather_fn fn, void *user, dhgp_comm **out);
+/* phases over fewer than min_units nodes (or moves) run replicated (default 65536) */
+int dhgp_comm_set_min_units(dhgp_comm *cm, int64_t min_units);
+int dhgp_comm_stats(const dhgp_comm *cm, int64_t *allgathers, double *bytes);
+void dhgp_comm_destroy(dhgp_comm *cm);
+int dhgp_partition_sharded(const dhgp_graph *g, const dhgp_config *cfg, dhgp_comm *cm, int32_t *assign_out,
+                           int32_t *num_parts_out, dhgp_stats *stats_out);
+int dhgp_session_set_comm(dhgp_session *s, dhgp_comm *cm); /* NULL = single GPU */
+/* the range rule of every sharded phase: returns 1 (and [lo, hi), chunk) when
+ * n units are split over `world` ranks, 0 when the phase runs replicated */
+int dhgp_shard_range(int32_t world, int32_t rank, int64_t min_units, int64_t n, int64_t *lo, int64_t *hi,
+                     int64_t *chunk);
+
 /* ---- data model (hgraph.py) ------------------------------------------ */
 /* Hypergraph._from_csr derived families — hgraph.py:212-238.  Output
  * sizes: in = dst_off[E], out = src_off[E], pins/inc = *num_pins_out

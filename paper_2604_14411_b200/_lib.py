@@ -87,6 +87,8 @@ EXPORTS = [
     "dhgp_evaluate", "dhgp_union_size_sorted", "dhgp_fill_histograms", "dhgp_select_first_valid",
     "dhgp_resolve_matching", "dhgp_connectivity_value", "dhgp_compute_pins", "dhgp_propose_moves",
     "dhgp_sequence_gains", "dhgp_build_events_and_select",
+    "dhgp_comm_nccl_unique_id", "dhgp_comm_init_nccl", "dhgp_comm_init_host", "dhgp_comm_set_min_units",
+    "dhgp_comm_stats", "dhgp_comm_destroy", "dhgp_partition_sharded", "dhgp_session_set_comm", "dhgp_shard_range",
 ]
 
 _lib = None
@@ -104,6 +106,8 @@ def load(require_device: bool = True):
         L = C.CDLL(str(LIB_PATH))
         L.dhgp_last_error.restype = C.c_char_p
         L.dhgp_build_info.restype = C.c_char_p
+        L.dhgp_comm_destroy.argtypes = [C.c_void_p]
+        L.dhgp_comm_destroy.restype = None
         _lib = L
     if require_device and not _device_checked:
         n = C.c_int32(0)

@@ -7,6 +7,7 @@
 // in a shared-memory hash table keyed by neighbour id, then scans it in
 // (hist desc, id desc) order with the deferred size/inbound checks.
 #include "coarsen.cuh"
+#include "comm.cuh"
 #include "prims.cuh"
 
 namespace dhgp {
@@ -71,6 +72,7 @@ struct ScoreArgs {
     int32_t *heavy_list;  // nodes for the block tier (many incident h-edges)
     int32_t *heavy_count;
     Tiers t;
+    int32_t lo, hi;  // this rank's node range (comm.cuh); [0, N) on one GPU
 };
 
 constexpr int SS_WARPS = 8;
@@ -109,9 +111,9 @@ __global__ void __launch_bounds__(SS_WARPS * 32) k_score_warp(ScoreArgs a) {
     Acc *vals = svals + w * SS_CAP;
     while (true) {
         int node = 0;
-        if (lane == 0) node = atomicAdd(a.next, 1);
+        if (lane == 0) node = a.lo + atomicAdd(a.next, 1);
         node = __shfl_sync(FULL_MASK, node, 0);
-        if (node >= a.N) break;
+        if (node >= a.hi) break;
         const int64_t ilo = a.inc_off[node], ihi = a.inc_off[node + 1];
         if (ihi - ilo > a.t.ss_heavy_inc) {  // hub: a whole block per node
             if (lane == 0) a.heavy_list[atomicAdd(a.heavy_count, 1)] = node;
@@ -524,14 +526,18 @@ void score_select(Ctx &c, const DLevel &L, const DWeights &W, int64_t omega, int
     }
     c.zero(s.ctr, 3);
     ScoreArgs a{L.N, L.inc_off, L.inc_dat, L.pin_off, L.pin_dat, W.wi, L.size, L.in_off, L.in_dat, omega, delta,
-                pair, score, s.ctr, s.big, s.ctr + 1, s.heavy, s.ctr + 2, tiers()};
+                pair, score, s.ctr, s.big, s.ctr + 1, s.heavy, s.ctr + 2, tiers(), 0, L.N};
+    const Shard sh = shard_of(c.comm, L.N);
+    a.lo = (int32_t)sh.lo;
+    a.hi = (int32_t)sh.hi;
+    const int64_t nmine = std::max<int64_t>(1, sh.hi - sh.lo);
     if (W.wsum < (1ll << 32)) {
         static int g32 = resident_grid(c, k_score_warp<unsigned>, SS_WARPS * 32, ss_smem<unsigned>());
-        int blocks = (int)std::min<int64_t>(cdiv(L.N, SS_WARPS), g32);
+        int blocks = (int)std::min<int64_t>(cdiv(nmine, SS_WARPS), g32);
         k_score_warp<unsigned><<<blocks, SS_WARPS * 32, ss_smem<unsigned>(), c.stream>>>(a);
     } else {
         static int g64 = resident_grid(c, k_score_warp<unsigned long long>, SS_WARPS * 32, ss_smem<unsigned long long>());
-        int blocks = (int)std::min<int64_t>(cdiv(L.N, SS_WARPS), g64);
+        int blocks = (int)std::min<int64_t>(cdiv(nmine, SS_WARPS), g64);
         k_score_warp<unsigned long long><<<blocks, SS_WARPS * 32, ss_smem<unsigned long long>(), c.stream>>>(a);
     }
     DHGP_LAUNCHED(c);
@@ -546,6 +552,10 @@ void score_select(Ctx &c, const DLevel &L, const DWeights &W, int64_t omega, int
     a.N = (int32_t)s.cap;
     k_score_block<<<s.blocks, SB_THREADS, 0, c.stream>>>(a, s.dense, s.touched, s.cval, L.N);
     DHGP_LAUNCHED(c);
+    if (sh.on) {  // complete (pair, score) from the other ranks' node ranges
+        allgather(c, c.comm, pair, sizeof(int32_t), sh.chunk);
+        allgather(c, c.comm, score, sizeof(double), sh.chunk);
+    }
 }
 
 // ===========================================================================

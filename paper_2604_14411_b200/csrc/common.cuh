@@ -52,7 +52,10 @@ struct KernelStat {
     double bytes;
 };
 
+struct Comm;
+
 struct Ctx {
+    Comm *comm = nullptr;  // node-range sharding across ranks (comm.cuh); null = single GPU
     int device = 0;
     cudaStream_t stream = nullptr;
     int64_t launches = 0;
@@ -143,7 +146,8 @@ struct KScope {
 
 // Escalation thresholds of the tiered per-node kernels (warp -> block ->
 // dense).  DHGP_FORCE_TIERS=1 shrinks them so that small parity tests drive
-// every tier; results never depend on them.
+// every tier (=2 keeps the small-K dense path, =1 disables it); results
+// never depend on them.
 struct Tiers {
     int ss_limit = 720;       // score: distinct neighbours per warp table
     int ss_heavy_inc = 192;   // score: incident h-edges above which a block takes the node
@@ -151,6 +155,7 @@ struct Tiers {
     int pr_limit = 400;       // propose: distinct parts per warp table
     int pr_heavy_inc = 128;   // propose: incident h-edges above which a block takes the node
     int pm_limit = 3072;      // propose: distinct parts per medium-tier table
+    int small_k = 4096;       // propose: K up to which escalated nodes use dense shared arrays
 };
 const Tiers &tiers();
 

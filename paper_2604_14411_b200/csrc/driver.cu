@@ -5,6 +5,7 @@
 #include <mutex>
 
 #include "coarsen.cuh"
+#include "comm.cuh"
 #include "prims.cuh"
 #include "refine.cuh"
 
@@ -32,7 +33,8 @@ const Tiers &tiers() {
     static Tiers t = [] {
         Tiers x;
         const char *e = getenv("DHGP_FORCE_TIERS");
-        if (e && e[0] == '1') {
+        if (e && (e[0] == '1' || e[0] == '2')) {
+            if (e[0] == '1') x.small_k = 0;
             x.ss_limit = 3;
             x.ss_heavy_inc = 2;
             x.sh_limit = 6;
@@ -269,8 +271,9 @@ static void run_partition(Ctx &c, const DInput &in, const dhgp_config &cfg, Part
                                                      " (" + std::to_string(levels.back().N) + " nodes, target " +
                                                      std::to_string(target) + ")"};
             const int32_t n = levels.back().N;
-            int32_t *pair = c.alloc<int32_t>(n), *match = c.alloc<int32_t>(n), *claim = c.alloc<int32_t>(n);
-            double *score = c.alloc<double>(n);
+            const int64_t ncap = shard_capacity(c.comm, n);  // room for the allgather of (pair, score)
+            int32_t *pair = c.alloc<int32_t>(ncap), *match = c.alloc<int32_t>(n), *claim = c.alloc<int32_t>(n);
+            double *score = c.alloc<double>(ncap);
             uint8_t *isrep = c.alloc<uint8_t>(n);
             c.zero(status, kStatusWords);
             score_select(c, levels.back(), W, omega, delta, pair, score, sscr);
@@ -506,7 +509,10 @@ static void fill_stats(const PartitionResult &r, dhgp_stats *s, int64_t launches
 // ===========================================================================
 using namespace dhgp;
 
+Comm *comm_of(dhgp_comm *cm);
+
 struct dhgp_session {
+    dhgp_comm *comm = nullptr;
     int device = 0;
     DInput in;
     bool profiling = false;
@@ -556,12 +562,13 @@ int dhgp_device_count(int32_t *count) {
     return DHGP_OK;
 }
 
-int dhgp_partition(const dhgp_graph *g, const dhgp_config *cfg, int32_t *assign_out, int32_t *num_parts_out,
-                   dhgp_stats *stats_out, dhgp_observer_fn obs, void *user) {
+static int partition_impl(const dhgp_graph *g, const dhgp_config *cfg, dhgp_comm *cm, int32_t *assign_out,
+                          int32_t *num_parts_out, dhgp_stats *stats_out, dhgp_observer_fn obs, void *user) {
     DHGP_GUARD_BEGIN
     check_graph(g);
     Ctx c;
     setup(c, cfg->device);
+    c.comm = comm_of(cm);
     DInput in;
     upload_input(c, *g, in);
     PartitionResult r;
@@ -577,6 +584,22 @@ int dhgp_partition(const dhgp_graph *g, const dhgp_config *cfg, int32_t *assign_
     *num_parts_out = r.num_parts;
     fill_stats(r, stats_out, c.launches);
     DHGP_GUARD_END
+}
+
+int dhgp_partition(const dhgp_graph *g, const dhgp_config *cfg, int32_t *assign_out, int32_t *num_parts_out,
+                   dhgp_stats *stats_out, dhgp_observer_fn obs, void *user) {
+    return partition_impl(g, cfg, nullptr, assign_out, num_parts_out, stats_out, obs, user);
+}
+
+int dhgp_partition_sharded(const dhgp_graph *g, const dhgp_config *cfg, dhgp_comm *cm, int32_t *assign_out,
+                           int32_t *num_parts_out, dhgp_stats *stats_out) {
+    return partition_impl(g, cfg, cm, assign_out, num_parts_out, stats_out, nullptr, nullptr);
+}
+
+int dhgp_session_set_comm(dhgp_session *s, dhgp_comm *cm) {
+    if (!s) return DHGP_ERR_ARG;
+    s->comm = cm;
+    return DHGP_OK;
 }
 
 void dhgp_stats_free(dhgp_stats *s) {
@@ -607,6 +630,7 @@ int dhgp_session_partition(dhgp_session *s, const dhgp_config *cfg, int32_t *ass
     DHGP_GUARD_BEGIN
     Ctx c;
     setup(c, s->device);
+    c.comm = comm_of(s->comm);
     c.profiling = s->profiling;
     dhgp_config cc = *cfg;
     cc.device = s->device;

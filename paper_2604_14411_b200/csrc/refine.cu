@@ -6,6 +6,7 @@
 // e's own pin offsets (lambda(e) <= |pins(e)| entries).  Every value the
 // algorithm reads from pins[e, p] / pins_in[e, p] is a binary search in that
 // list (absent = 0), so the results are identical.
+#include "comm.cuh"
 #include "prims.cuh"
 #include "refine.cuh"
 
@@ -236,6 +237,7 @@ struct ProposeArgs {
     int32_t *dense_list;  // medium tier -> dense tier
     int32_t *dense_count;
     Tiers t;
+    int32_t lo, hi;  // this rank's node range (comm.cuh); [0, N) on one GPU
 };
 
 // Flattened iteration over the (h-edge, run) pairs of a node's incident
@@ -307,9 +309,9 @@ __global__ void __launch_bounds__(PR_WARPS * 32) k_propose_warp(ProposeArgs a) {
     Acc *vals = svals + w * PR_CAP;
     while (true) {
         int node = 0;
-        if (lane == 0) node = atomicAdd(a.next, 1);
+        if (lane == 0) node = a.lo + atomicAdd(a.next, 1);
         node = __shfl_sync(FULL_MASK, node, 0);
-        if (node >= a.N) break;
+        if (node >= a.hi) break;
         const int64_t ilo = a.inc_off[node], ihi = a.inc_off[node + 1];
         if (ihi == ilo || a.K < 2) {
             if (lane == 0) a.target[node] = -1;
@@ -532,21 +534,21 @@ template <class Acc>
 constexpr int ph_maxk() { return (int)((220 * 1024 - 64) * 8 / (8 * (sizeof(Acc) + 4) + 1)); }
 template <class Acc>
 constexpr size_t ph_smem(int K) { return (size_t)K * (sizeof(Acc) + 4) + 4 * (size_t)((K + 31) / 32) + 16; }
-template <class Acc>
-__global__ void __launch_bounds__(PH_THREADS) k_propose_heavy(ProposeArgs a) {
+template <class Acc, int THREADS = PH_THREADS>
+__global__ void __launch_bounds__(THREADS) k_propose_heavy(ProposeArgs a) {
     extern __shared__ unsigned long long smem_u64[];
     Acc *pres = (Acc *)smem_u64;
     int32_t *tlist = (int32_t *)(pres + a.K);
     uint32_t *touched = (uint32_t *)(tlist + a.K);
     __shared__ int32_t s_nt;
-    __shared__ long long r_a[PH_THREADS / 32], r_b[PH_THREADS / 32];
-    __shared__ int32_t r_p[PH_THREADS / 32];
-    const int w = warp_id(), lane = lane_id(), nw = PH_THREADS / 32;
+    __shared__ long long r_a[THREADS / 32], r_b[THREADS / 32];
+    __shared__ int32_t r_p[THREADS / 32];
+    const int w = warp_id(), lane = lane_id(), nw = THREADS / 32;
     const int nbig = *a.dense_count;
     if ((int)blockIdx.x >= nbig) return;
     const int tw = (a.K + 31) >> 5;
-    for (int p = threadIdx.x; p < a.K; p += PH_THREADS) pres[p] = 0;
-    for (int p = threadIdx.x; p < tw; p += PH_THREADS) touched[p] = 0;
+    for (int p = threadIdx.x; p < a.K; p += THREADS) pres[p] = 0;
+    for (int p = threadIdx.x; p < tw; p += THREADS) touched[p] = 0;
     for (int t = blockIdx.x; t < nbig; t += gridDim.x) {
         const int32_t node = a.dense_list[t];
         if (threadIdx.x == 0) s_nt = 0;
@@ -580,7 +582,7 @@ __global__ void __launch_bounds__(PH_THREADS) k_propose_heavy(ProposeArgs a) {
         const int64_t sz = a.size[node];
         long long bg = 0;
         int32_t bp = -1;
-        for (int i = threadIdx.x; i < nt; i += PH_THREADS) {
+        for (int i = threadIdx.x; i < nt; i += THREADS) {
             const int32_t p = tlist[i];
             const long long pv = (long long)pres[p];
             pres[p] = 0;
@@ -998,14 +1000,13 @@ __global__ void k_size_events_dn(const int64_t *dM, const int32_t *node, const i
     ev.val[2 * i + 1] = (uint32_t)s;
 }
 // A15: gains corrected for earlier moves, rules (a)-(d) (_kernels.pyx:326-363)
-__global__ void k_seq_gains_dn(const int64_t *dM, const int64_t *inc_off, const int32_t *inc_dat,
+__global__ void k_seq_gains_dn(int64_t mlo, int64_t mhi, const int64_t *inc_off, const int32_t *inc_dat,
                                const int64_t *pin_off, const int32_t *pin_dat, const int64_t *wi, Runs r,
                                const int32_t *node, const int32_t *from, const int32_t *to, const int64_t *giso,
                                const int32_t *pos, int64_t *gseq) {
     const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
     const int lane = lane_id();
-    const int64_t M = *dM;
-    for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id(); i < M; i += nw) {
+    for (int64_t i = mlo + (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id(); i < mhi; i += nw) {
         const int32_t n = node[i], ps = from[i], pd = to[i];
         int64_t acc = 0;
         for (int64_t ii = inc_off[n] + lane; ii < inc_off[n + 1]; ii += 32) {
@@ -1075,8 +1076,8 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, int32_t *assign, i
     r.len = c.alloc<int32_t>(L.E);
     int32_t *tmp_parts = c.alloc<int32_t>(L.U);
     int64_t *psizes = c.alloc<int64_t>(K), *pinbound = c.alloc<int64_t>(K);
-    int32_t *target = c.alloc<int32_t>(N);
-    int64_t *gain = c.alloc<int64_t>(N);
+    int32_t *target = c.alloc<int32_t>(shard_capacity(c.comm, N));
+    int64_t *gain = c.alloc<int64_t>(shard_capacity(c.comm, N));
     uint8_t *flags = c.alloc<uint8_t>(N);
     int64_t *mpos = c.alloc<int64_t>((int64_t)N + 1);
     int32_t *pos = c.alloc<int32_t>(N);
@@ -1087,7 +1088,7 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, int32_t *assign, i
     uint64_t *mk = c.alloc<uint64_t>(N), *mkt = c.alloc<uint64_t>(N);
     uint32_t *mv = c.alloc<uint32_t>(N), *mvt = c.alloc<uint32_t>(N);
     int32_t *node = c.alloc<int32_t>(N), *from = c.alloc<int32_t>(N), *to = c.alloc<int32_t>(N);
-    int64_t *giso = c.alloc<int64_t>(N), *gseq = c.alloc<int64_t>(N);
+    int64_t *giso = c.alloc<int64_t>(N), *gseq = c.alloc<int64_t>(shard_capacity(c.comm, N) + 64);
     const int64_t ecap = 2 * (int64_t)N + 2 * L.Sin;
     uint64_t *ek = c.alloc<uint64_t>(ecap), *ekt = c.alloc<uint64_t>(ecap);
     uint32_t *evv = c.alloc<uint32_t>(ecap), *evt = c.alloc<uint32_t>(ecap);
@@ -1123,22 +1124,45 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, int32_t *assign, i
             KScope ks(c, "propose", (double)(28.0 * N + 12.0 * L.U + 20.0 * L.E + 8.0 * K), N);
             c.zero(ctr, 4);
             ProposeArgs a{N, K, L.inc_off, L.inc_dat, L.pin_off, W.wi, r, assign, psizes, L.size, omega,
-                          target, gain, ctr, big, ctr + 1, big2, ctr + 2, tiers()};
+                          target, gain, ctr, big, ctr + 1, big2, ctr + 2, tiers(), 0, N};
+            const Shard sh = shard_of(c.comm, N);
+            a.lo = (int32_t)sh.lo;
+            a.hi = (int32_t)sh.hi;
+            const int64_t nmine = std::max<int64_t>(1, sh.hi - sh.lo);
             if (N > 0) {
                 const bool narrow = W.wsum < (1ll << 32);
                 if (narrow) {
                     static int g32 = resident_grid(c, k_propose_warp<unsigned>, PR_WARPS * 32, pr_smem<unsigned>());
-                    int blocks = (int)std::min<int64_t>(cdiv(N, PR_WARPS), g32);
+                    int blocks = (int)std::min<int64_t>(cdiv(nmine, PR_WARPS), g32);
                     k_propose_warp<unsigned><<<blocks, PR_WARPS * 32, pr_smem<unsigned>(), c.stream>>>(a);
                 } else {
                     static int g64 = resident_grid(c, k_propose_warp<unsigned long long>, PR_WARPS * 32,
                                                    pr_smem<unsigned long long>());
-                    int blocks = (int)std::min<int64_t>(cdiv(N, PR_WARPS), g64);
+                    int blocks = (int)std::min<int64_t>(cdiv(nmine, PR_WARPS), g64);
                     k_propose_warp<unsigned long long>
                         <<<blocks, PR_WARPS * 32, pr_smem<unsigned long long>(), c.stream>>>(a);
                 }
                 DHGP_LAUNCHED(c);
                 KScope kh(c, "propose_heavy");
+                constexpr int kSmallK = 4096;
+                if (K <= std::min(kSmallK, tiers().small_k)) {
+                    // few parts: the escalated nodes go straight to dense shared
+                    // arrays over the parts (no hashing), 256 threads per node
+                    ProposeArgs b = a;
+                    b.dense_list = big;
+                    b.dense_count = ctr + 1;
+                    if (narrow) {
+                        static int s32 = resident_grid(c, k_propose_heavy<unsigned, 256>, 256,
+                                                       ph_smem<unsigned>(kSmallK));
+                        k_propose_heavy<unsigned, 256><<<s32, 256, ph_smem<unsigned>(K), c.stream>>>(b);
+                    } else {
+                        static int s64 = resident_grid(c, k_propose_heavy<unsigned long long, 256>, 256,
+                                                       ph_smem<unsigned long long>(kSmallK));
+                        k_propose_heavy<unsigned long long, 256>
+                            <<<s64, 256, ph_smem<unsigned long long>(K), c.stream>>>(b);
+                    }
+                    DHGP_LAUNCHED(c);
+                } else {
                 // medium tier: reads the escalation count on device, exits when zero
                 if (narrow) {
                     static int m32 = resident_grid(c, k_propose_mid<unsigned>, PM_THREADS, pm_smem<unsigned>());
@@ -1159,6 +1183,11 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, int32_t *assign, i
                     k_propose_block<<<pb_blocks, PB_THREADS, 0, c.stream>>>(a, pdense, ptouched);
                 }
                 DHGP_LAUNCHED(c);
+                }
+            }
+            if (sh.on) {  // complete (target, gain) from the other ranks' node ranges
+                allgather(c, c.comm, target, sizeof(int32_t), sh.chunk);
+                allgather(c, c.comm, gain, sizeof(int64_t), sh.chunk);
             }
         }
         // --- sequence: movers by (gain desc, node asc) (refine.py:108-110) --
@@ -1190,10 +1219,12 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, int32_t *assign, i
         DHGP_LAUNCHED(c);
         {
             KScope ks(c, "seq_gains", 0.0);
-            int blocks = (int)std::min<int64_t>(cdiv(M, 8), (int64_t)c.num_sms * 16);
-            k_seq_gains_dn<<<blocks, 256, 0, c.stream>>>(dM, L.inc_off, L.inc_dat, L.pin_off, L.pin_dat, W.wi, r,
-                                                          node, from, to, giso, pos, gseq);
+            const Shard ms = shard_of(c.comm, M);  // this rank's move range
+            int blocks = (int)std::min<int64_t>(cdiv(std::max<int64_t>(1, ms.hi - ms.lo), 8), (int64_t)c.num_sms * 16);
+            k_seq_gains_dn<<<blocks, 256, 0, c.stream>>>(ms.lo, ms.hi, L.inc_off, L.inc_dat, L.pin_off, L.pin_dat,
+                                                          W.wi, r, node, from, to, giso, pos, gseq);
             DHGP_LAUNCHED(c);
+            if (ms.on) allgather(c, c.comm, gseq, sizeof(int64_t), ms.chunk);
         }
         // --- A17 events: key = track | part | move index --------------------
         const int ibits = std::max(1, bitlen((uint64_t)M));

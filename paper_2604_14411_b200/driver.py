@@ -135,6 +135,12 @@ def partition(g: Hypergraph, cfg: Config, observer=None, timings: bool = False) 
             L.dhgp_stats_free(C.byref(st))
         raise bridge.error
     _lib.raise_for(rc)
+    stats = _stats_from(L, st, timings)
+    return Partitioning(assign[: g.num_nodes].copy(), int(nparts.value)), stats
+
+
+def _stats_from(L, st, timings: bool) -> RunStats:
+    """RunStats from a filled dhgp_stats (frees the library's buffers)."""
     try:
         nl = st.num_levels
         tro = _lib.take(st.trace_off, nl + 1, np.int64)
@@ -151,4 +157,4 @@ def partition(g: Hypergraph, cfg: Config, observer=None, timings: bool = False) 
         stats._gpu_launches = int(st.gpu_launches)  # not part of to_dict()
     finally:
         L.dhgp_stats_free(C.byref(st))
-    return Partitioning(assign[: g.num_nodes].copy(), int(nparts.value)), stats
+    return stats

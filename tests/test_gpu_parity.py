@@ -319,7 +319,8 @@ def test_every_kernel_tier_under_forced_escalation():
     from pathlib import Path
 
     root = str(Path(__file__).resolve().parents[1])
-    r = subprocess.run([sys.executable, "-c", _FORCED_TIERS_SCRIPT, root], capture_output=True, text=True,
-                       env=dict(os.environ, DHGP_FORCE_TIERS="1"), timeout=600)
-    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
-    assert "forced tiers ok" in r.stdout
+    for mode in ("1", "2"):  # 1: medium + block tiers; 2: the small-K dense path
+        r = subprocess.run([sys.executable, "-c", _FORCED_TIERS_SCRIPT, root], capture_output=True, text=True,
+                           env=dict(os.environ, DHGP_FORCE_TIERS=mode), timeout=600)
+        assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+        assert "forced tiers ok" in r.stdout
