@@ -298,3 +298,64 @@ def build_events_and_select(num_nodes, num_edges, in_off, in_dat, node_size, nod
 def union_size_sorted(a, b):
     a, b = _c(a, np.int32), _c(b, np.int32)
     return int(lib().orc_union_size_sorted(_p(a), C.c_int64(len(a)), _p(b), C.c_int64(len(b))))
+
+
+# ---- stepwise replay: one level of a run too large for the CPU ----
+
+def coarsen_level(num_nodes, weights, src_off, src_dat, dst_off, dst_dat, node_size, *, max_size, max_inbound):
+    """One coarsening level (coarsen.py:93-173) of the given level graph: the
+    payload of its "level" event (pair, score, match, gamma, coarse graph),
+    or None when the level finds no pair.  Level l+1 depends only on level l
+    (the carried neighbour sets equal the rematerialised ones)."""
+    L = lib()
+    w = _c(weights, np.float64)
+    so, sd = _c(src_off, np.int64), _c(src_dat, np.int32)
+    do, dd = _c(dst_off, np.int64), _c(dst_dat, np.int32)
+    ns = _c(node_size, np.int32)
+    assign = np.zeros(max(num_nodes, 1), dtype=np.int32)
+    nparts = C.c_int32(0)
+    st = DhgpStats()
+    events: list[dict] = []
+
+    def _obs(evp, _user):
+        if evp.contents.kind == 1:
+            events.append(event_to_dict(evp.contents))
+
+    cb = OBSERVER(_obs)
+    L.orc_partition(
+        C.c_int32(num_nodes), C.c_int32(len(w)), w.ctypes.data_as(C.c_void_p),
+        so.ctypes.data_as(C.c_void_p), sd.ctypes.data_as(C.c_void_p),
+        do.ctypes.data_as(C.c_void_p), dd.ctypes.data_as(C.c_void_p), ns.ctypes.data_as(C.c_void_p),
+        C.c_int64(max_size), C.c_int64(max_inbound), C.c_int32(1), C.c_int32(1),
+        assign.ctypes.data_as(C.c_void_p), C.byref(nparts), C.byref(st), cb, None,
+    )
+    L.orc_stats_free(C.byref(st))
+    return events[0] if events else None
+
+
+def refine_level(num_nodes, weights, src_off, src_dat, dst_off, dst_dat, node_size, assign, num_parts, *,
+                 max_size, max_inbound, max_rounds=8, level=0):
+    """refine_level (refine.py:262-318) of one level graph from an entry
+    assignment: (final assign, connectivity trace, round events)."""
+    L = lib()
+    w = _c(weights, np.float64)
+    so, sd = _c(src_off, np.int64), _c(src_dat, np.int32)
+    do, dd = _c(dst_off, np.int64), _c(dst_dat, np.int32)
+    ns = _c(node_size, np.int32)
+    a = np.array(assign, dtype=np.int32, copy=True)
+    conns = np.zeros(max_rounds + 1, dtype=np.float64)
+    nc = C.c_int64(0)
+    events: list[dict] = []
+
+    def _obs(evp, _user):
+        events.append(event_to_dict(evp.contents))
+
+    cb = OBSERVER(_obs)
+    L.orc_refine_level(
+        C.c_int32(num_nodes), C.c_int32(len(w)), w.ctypes.data_as(C.c_void_p),
+        so.ctypes.data_as(C.c_void_p), sd.ctypes.data_as(C.c_void_p),
+        do.ctypes.data_as(C.c_void_p), dd.ctypes.data_as(C.c_void_p), ns.ctypes.data_as(C.c_void_p),
+        a.ctypes.data_as(C.c_void_p), C.c_int32(num_parts), C.c_int64(max_size), C.c_int64(max_inbound),
+        C.c_int32(max_rounds), C.c_int32(level), cb, None, conns.ctypes.data_as(C.c_void_p), C.byref(nc),
+    )
+    return a[:num_nodes], conns[: nc.value].tolist(), events

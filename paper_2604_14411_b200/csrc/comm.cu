@@ -65,7 +65,7 @@ Shard shard_of(const Comm *cm, int64_t n) {
     s.lo = 0;
     s.hi = n;
     s.chunk = n;
-    if (!cm || cm->world <= 1 || n < cm->min_units || n <= 0) return s;
+    if (!cm || (cm->world <= 1 && !cm->exercise) || n < cm->min_units || n <= 0) return s;
     s.on = true;
     s.chunk = cdiv(n, cm->world);
     s.lo = std::min<int64_t>(n, (int64_t)cm->rank * s.chunk);
@@ -74,12 +74,12 @@ Shard shard_of(const Comm *cm, int64_t n) {
 }
 
 int64_t shard_capacity(const Comm *cm, int64_t n) {
-    if (!cm || cm->world <= 1) return n;
+    if (!cm) return n;
     return std::max<int64_t>(n, cdiv(n, cm->world) * cm->world);
 }
 
 void allgather(Ctx &c, Comm *cm, void *buf, size_t elem, int64_t chunk) {
-    if (!cm || cm->world <= 1 || chunk <= 0) return;
+    if (!cm || (cm->world <= 1 && !cm->exercise) || chunk <= 0) return;
     const size_t part = (size_t)chunk * elem;
     cm->calls++;
     cm->bytes += (double)part * (cm->world - 1);
@@ -142,6 +142,8 @@ int dhgp_comm_init_nccl(int32_t world, int32_t rank, const uint8_t *id, int32_t 
         cm->c.rank = rank;
         cm->c.device = device;
         cm->c.kind = DHGP_COMM_NCCL;
+        const char *ex = getenv("DHGP_COMM_EXERCISE");
+        cm->c.exercise = ex && ex[0] == '1';
         int r = nccl().CommInitRank(&cm->c.nccl, world, uid, rank);
         if (r != 0) {
             delete cm;
@@ -164,6 +166,8 @@ int dhgp_comm_init_host(int32_t world, int32_t rank, dhgp_allgather_fn fn, void 
     cm->c.world = world;
     cm->c.rank = rank;
     cm->c.kind = DHGP_COMM_HOST;
+    const char *ex = getenv("DHGP_COMM_EXERCISE");
+    cm->c.exercise = ex && ex[0] == '1';
     cm->c.fn = fn;
     cm->c.user = user;
     *out = cm;

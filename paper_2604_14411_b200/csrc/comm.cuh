@@ -22,6 +22,7 @@ struct Comm {
     void *pinned = nullptr;       // host staging for DHGP_COMM_HOST
     size_t pinned_cap = 0;
     int64_t min_units = 1 << 16;  // phases over fewer units run replicated (no exchange)
+    bool exercise = false;        // world 1: still issue the exchanges (DHGP_COMM_EXERCISE=1, tests)
     int64_t calls = 0;            // allgathers issued
     double bytes = 0;             // bytes received per rank
 };

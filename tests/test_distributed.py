@@ -198,14 +198,18 @@ def test_nccl_communicator_world1():
     port = _free_port()
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
+    os.environ["DHGP_COMM_EXERCISE"] = "1"  # issue the in-place ncclAllGather even at world size 1
     dist.init_process_group("gloo", rank=0, world_size=1)
     try:
         cm = dd.Communicator.nccl()
-        g, om, de = _instances()[0]
-        cfg = dp.Config(dp.Constraints(om, de), max_levels=1 << 20)
-        a, sa = dd.partition(g, cfg, cm)
-        b, sb = dp.partition(g, cfg)
-        assert np.array_equal(a.assign, b.assign) and sa.connectivity_trace == sb.connectivity_trace
+        cm.set_min_units(0)
+        for g, om, de in _instances():
+            cfg = dp.Config(dp.Constraints(om, de), max_levels=1 << 20)
+            a, sa = dd.partition(g, cfg, cm)
+            b, sb = dp.partition(g, cfg)
+            assert np.array_equal(a.assign, b.assign) and sa.connectivity_trace == sb.connectivity_trace
+        assert cm.stats()["allgathers"] > 0
         cm.close()
     finally:
+        os.environ.pop("DHGP_COMM_EXERCISE", None)
         dist.destroy_process_group()

@@ -324,3 +324,13 @@ def test_every_kernel_tier_under_forced_escalation():
                            env=dict(os.environ, DHGP_FORCE_TIERS=mode), timeout=600)
         assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
         assert "forced tiers ok" in r.stdout
+
+
+def test_c2_stepwise_levels_match_oracle():
+    """Full-size C2 (the bench workload): sampled coarsening and refinement
+    levels of one GPU run replayed by the oracle (tests/stepwise_parity.py)."""
+    import stepwise_parity as sp
+
+    out = sp.check_config("C2", [990], [0, 900])
+    assert len(out["coarsen"]) == 1 and len(out["refine"]) >= 1
+    assert all(r["bit_exact"] for r in out["coarsen"] + out["refine"]), out
