@@ -142,6 +142,11 @@ struct PartitionResult {
 
 constexpr size_t kCheckpoint = 16;
 
+// device bytes of one level's lists (what level_to_stub would release)
+static size_t level_bytes(const DLevel &L) {
+    return 8 * (3 * (size_t)L.E + 2 * (size_t)L.N + 5) + 4 * ((size_t)L.Ps + L.Pd + L.U + L.Sin + L.U + L.N);
+}
+
 // Rebuilds stub levels (lo, hi] by re-running the contraction from the
 // nearest full level below, using the stored gammas (bit-identical).
 static void rebuild_levels(Ctx &c, std::vector<DLevel> &levels, size_t hi) {
@@ -262,6 +267,16 @@ static void run_partition(Ctx &c, const DInput &in, const dhgp_config &cfg, Part
     // no pair is discarded (driver.py:104-105).
     ScoreScratch sscr;
     int64_t *status = nullptr;
+    // bytes of non-checkpoint levels kept whole (no rebuild during
+    // uncoarsening): up to 40% of the memory free at this point
+    size_t kept = 0, keep_budget = 0;
+    {
+        size_t freeb = 0, total = 0;
+        DHGP_CUDA(cudaMemGetInfo(&freeb, &total));
+        keep_budget = (size_t)(0.4 * (double)(freeb + (g_pool_reserved[c.device] > 0 ? g_pool_reserved[c.device] : 0)));
+        const char *e = getenv("DHGP_KEEP_LEVELS_BYTES");  // tests: force the checkpoint/rebuild path
+        if (e) keep_budget = (size_t)strtoull(e, nullptr, 10);
+    }
     try {
         score_scratch_init(c, sscr, N0);
         status = c.alloc<int64_t>(kStatusWords);
@@ -348,10 +363,17 @@ static void run_partition(Ctx &c, const DInput &in, const dhgp_config &cfg, Part
             c.free(score);
             c.free(isrep);
             if (stop) break;
-            // memory: keep every kCheckpoint-th level whole; the others keep
-            // only gamma and are rebuilt from their checkpoint on the way up
+            // memory: every kCheckpoint-th level stays whole; the others stay
+            // whole while they fit the level budget, else keep only gamma and
+            // are rebuilt from their checkpoint on the way up
             const size_t fi = levels.size() - 2;
-            if (fi % kCheckpoint != 0) level_to_stub(c, levels[fi]);
+            if (fi % kCheckpoint != 0) {
+                const size_t lb = level_bytes(levels[fi]);
+                if (kept + lb <= keep_budget)
+                    kept += lb;
+                else
+                    level_to_stub(c, levels[fi]);
+            }
         }
     } catch (...) {
         for (auto &L : levels) L.release(c);

@@ -6,7 +6,7 @@
 namespace dhgp {
 
 // ===========================================================================
-// exclusive scan (reduce-then-scan; tile = 256 threads x 16 items)
+// exclusive scan (single pass, decoupled look-back; tile = 256 threads x 16 items)
 // ===========================================================================
 namespace {
 constexpr int SC_BT = 256;
@@ -31,34 +31,6 @@ __device__ __forceinline__ int64_t block_excl_scan(int64_t v, int64_t *sh, int64
     *total = sh[32];
     __syncthreads();
     return r;
-}
-
-template <class T>
-__global__ void k_scan_reduce(const T *in, int64_t n, int64_t *partial) {
-    __shared__ int64_t sh[33];
-    int64_t base = (int64_t)blockIdx.x * SC_TILE;
-    int64_t s = 0;
-#pragma unroll
-    for (int i = 0; i < SC_IPT; i++) {
-        int64_t idx = base + (int64_t)i * SC_BT + threadIdx.x;
-        if (idx < n) s += (int64_t)in[idx];
-    }
-    int64_t t = block_sum<int64_t>(s, sh);
-    if (threadIdx.x == 0) partial[blockIdx.x] = t;
-}
-
-__global__ void k_scan_partials(int64_t *partial, int64_t ntiles) {
-    __shared__ int64_t sh[33];
-    int64_t carry = 0;
-    for (int64_t base = 0; base < ntiles; base += blockDim.x) {
-        int64_t idx = base + threadIdx.x;
-        int64_t v = idx < ntiles ? partial[idx] : 0;
-        int64_t tot;
-        int64_t ex = block_excl_scan(v, sh, &tot);
-        if (idx < ntiles) partial[idx] = carry + ex;
-        carry += tot;
-    }
-    if (threadIdx.x == 0) partial[ntiles] = carry;
 }
 
 template <class T>
@@ -97,6 +69,103 @@ __global__ void k_scan_final(const T *in, int64_t n, const int64_t *partial, int
     if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0)
         out[n] = (partial ? partial[blockIdx.x] : 0) + tot;
 }
+// Single-pass exclusive scan with decoupled look-back: each tile publishes
+// its aggregate, then its inclusive prefix once known; a tile's prefix is
+// found by walking back over its predecessors' published values (32 at a
+// time, one warp).  Tile status words carry an epoch so the scratch is never
+// cleared between calls (calls on a device are serialised).
+constexpr uint32_t kAggBit = 1u, kIncBit = 2u;
+template <class T>
+__global__ void __launch_bounds__(SC_BT) k_scan_onepass(const T *in, int64_t n, int64_t *out, uint32_t *flag,
+                                                        int64_t *agg, int64_t *inc, uint32_t epoch) {
+    __shared__ int64_t sh[33];
+    __shared__ int64_t buf[SC_TILE];
+    __shared__ int64_t s_prefix;
+    const int64_t tile = blockIdx.x;
+    const int64_t base = tile * SC_TILE;
+#pragma unroll
+    for (int i = 0; i < SC_IPT; i++) {
+        const int64_t idx = base + (int64_t)i * SC_BT + threadIdx.x;
+        buf[i * SC_BT + threadIdx.x] = idx < n ? (int64_t)in[idx] : 0;
+    }
+    __syncthreads();
+    int64_t loc[SC_IPT];
+    int64_t s = 0;
+#pragma unroll
+    for (int i = 0; i < SC_IPT; i++) {
+        loc[i] = buf[threadIdx.x * SC_IPT + i];
+        s += loc[i];
+    }
+    int64_t tot;
+    const int64_t ex = block_excl_scan(s, sh, &tot);
+    if (threadIdx.x < 32) {
+        const int lane = lane_id();
+        int64_t prefix = 0;
+        if (tile == 0) {
+            if (lane == 0) {
+                inc[0] = tot;
+                __threadfence();
+                atomicExch(&flag[0], (epoch << 2) | kIncBit);
+            }
+        } else {
+            if (lane == 0) {
+                agg[tile] = tot;
+                __threadfence();
+                atomicExch(&flag[tile], (epoch << 2) | kAggBit);
+            }
+            // look back: predecessors tile-1-lane, 32 per step
+            int64_t j = tile - 1;
+            while (true) {
+                const int64_t t = j - lane;
+                uint32_t f = 0;
+                if (t >= 0) {
+                    do {
+                        f = *(volatile uint32_t *)&flag[t];
+                    } while ((f >> 2) != epoch);  // not yet published in this call
+                }
+                __threadfence();
+                const bool has_inc = t >= 0 && (f & kIncBit);
+                const uint32_t incmask = __ballot_sync(FULL_MASK, has_inc);
+                // lanes up to (and including) the first with an inclusive value
+                const int stop = incmask ? __ffs(incmask) - 1 : 31;
+                int64_t v = 0;
+                if (t >= 0 && lane <= stop) v = has_inc ? *(volatile int64_t *)&inc[t] : *(volatile int64_t *)&agg[t];
+                prefix += warp_sum(v);
+                if (incmask || j - 31 < 0) break;
+                j -= 32;
+            }
+            if (lane == 0) {
+                inc[tile] = prefix + tot;
+                __threadfence();
+                atomicExch(&flag[tile], (epoch << 2) | kIncBit);
+            }
+        }
+        if (lane == 0) s_prefix = prefix;
+    }
+    __syncthreads();
+    int64_t run = ex + s_prefix;
+#pragma unroll
+    for (int i = 0; i < SC_IPT; i++) {
+        buf[threadIdx.x * SC_IPT + i] = run;
+        run += loc[i];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < SC_IPT; i++) {
+        const int64_t idx = base + (int64_t)i * SC_BT + threadIdx.x;
+        if (idx < n) out[idx] = buf[i * SC_BT + threadIdx.x];
+    }
+    if (tile == gridDim.x - 1 && threadIdx.x == 0) out[n] = s_prefix + tot;
+}
+
+// persistent per-device look-back scratch (grown on demand)
+struct ScanScratch {
+    uint32_t *flag = nullptr;
+    int64_t *agg = nullptr, *inc = nullptr;
+    int64_t cap = 0;
+    uint32_t epoch = 0;
+};
+ScanScratch g_scan[64];
 }  // namespace
 
 template <class T>
@@ -105,20 +174,34 @@ void scan_excl(Ctx &c, const T *in, int64_t *out, int64_t n) {
         c.zero(out, 1);
         return;
     }
-    int64_t ntiles = cdiv(n, SC_TILE);
+    const int64_t ntiles = cdiv(n, SC_TILE);
     if (ntiles == 1) {
         k_scan_final<T><<<1, SC_BT, 0, c.stream>>>(in, n, nullptr, out);
         DHGP_LAUNCHED(c);
         return;
     }
-    int64_t *partial = c.alloc<int64_t>(ntiles + 1);
-    k_scan_reduce<T><<<(unsigned)ntiles, SC_BT, 0, c.stream>>>(in, n, partial);
+    ScanScratch &ss = g_scan[c.device];
+    if (ss.cap < ntiles) {
+        // stream-ordered: earlier kernels on this stream are done with the old buffers
+        if (ss.flag) {
+            DHGP_CUDA(cudaFreeAsync(ss.flag, c.stream));
+            DHGP_CUDA(cudaFreeAsync(ss.agg, c.stream));
+            DHGP_CUDA(cudaFreeAsync(ss.inc, c.stream));
+        }
+        ss.cap = std::max<int64_t>(ntiles, 4096);
+        DHGP_CUDA(cudaMallocAsync((void **)&ss.flag, sizeof(uint32_t) * ss.cap, c.stream));
+        DHGP_CUDA(cudaMallocAsync((void **)&ss.agg, sizeof(int64_t) * ss.cap, c.stream));
+        DHGP_CUDA(cudaMallocAsync((void **)&ss.inc, sizeof(int64_t) * ss.cap, c.stream));
+        DHGP_CUDA(cudaMemsetAsync(ss.flag, 0, sizeof(uint32_t) * ss.cap, c.stream));
+        ss.epoch = 0;
+    }
+    ss.epoch = (ss.epoch + 1) & 0x3fffffffu;
+    if (ss.epoch == 0) {  // wrapped: clear so no stale word matches
+        DHGP_CUDA(cudaMemsetAsync(ss.flag, 0, sizeof(uint32_t) * ss.cap, c.stream));
+        ss.epoch = 1;
+    }
+    k_scan_onepass<T><<<(unsigned)ntiles, SC_BT, 0, c.stream>>>(in, n, out, ss.flag, ss.agg, ss.inc, ss.epoch);
     DHGP_LAUNCHED(c);
-    k_scan_partials<<<1, 1024, 0, c.stream>>>(partial, ntiles);
-    DHGP_LAUNCHED(c);
-    k_scan_final<T><<<(unsigned)ntiles, SC_BT, 0, c.stream>>>(in, n, partial, out);
-    DHGP_LAUNCHED(c);
-    c.free(partial);
 }
 // running maximum: per-tile maxima, a single-block max-scan over them,
 // then per-tile inclusive max with the carry

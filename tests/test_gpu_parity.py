@@ -312,7 +312,9 @@ print("forced tiers ok", len(cases))
 
 def test_every_kernel_tier_under_forced_escalation():
     """DHGP_FORCE_TIERS=1 shrinks the warp/block escalation thresholds so that
-    the medium, block and dense tiers of scoring and proposing all run."""
+    the medium, block and dense tiers of scoring and proposing all run;
+    DHGP_KEEP_LEVELS_BYTES=0 forces the checkpoint + rebuild path for every
+    level that is not a checkpoint."""
     import os
     import subprocess
     import sys
@@ -321,7 +323,7 @@ def test_every_kernel_tier_under_forced_escalation():
     root = str(Path(__file__).resolve().parents[1])
     for mode in ("1", "2"):  # 1: medium + block tiers; 2: the small-K dense path
         r = subprocess.run([sys.executable, "-c", _FORCED_TIERS_SCRIPT, root], capture_output=True, text=True,
-                           env=dict(os.environ, DHGP_FORCE_TIERS=mode), timeout=600)
+                           env=dict(os.environ, DHGP_FORCE_TIERS=mode, DHGP_KEEP_LEVELS_BYTES="0"), timeout=600)
         assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
         assert "forced tiers ok" in r.stdout
 
