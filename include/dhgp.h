@@ -160,6 +160,27 @@ int dhgp_session_set_comm(dhgp_session *s, dhgp_comm *cm); /* NULL = single GPU 
 int dhgp_shard_range(int32_t world, int32_t rank, int64_t min_units, int64_t n, int64_t *lo, int64_t *hi,
                      int64_t *chunk);
 
+/* ---- input path on the GPU: hgraph.parse_dhg (hgraph.py:409-467) ------
+ * text = the edge lines (everything after the header line, trailing blank
+ * lines removed).  begin: finds the lines and parses every line whose tokens
+ * are unsigned decimal integers; returns the line count (the caller raises
+ * the reference's count error when it differs from num_edges; nothing else is
+ * done then) and the number of "slow" lines the host must parse itself.
+ * finish: takes the host's results for those lines (pin counts, weight,
+ * error flag, ids), builds the CSR and flags every bad line; *first_bad_line
+ * is the first one (-1 if none) — the caller re-derives its message. */
+typedef struct dhgp_parse dhgp_parse;
+int dhgp_parse_dhg_begin(const char *text, int64_t len, int64_t num_edges, int64_t num_nodes, int32_t device,
+                         dhgp_parse **out, int64_t *lines_found, int64_t *num_slow);
+int dhgp_parse_dhg_slow_lines(dhgp_parse *ps, int64_t *line_idx, int64_t *byte_lo, int64_t *byte_hi);
+int dhgp_parse_dhg_finish(dhgp_parse *ps, const int64_t *slow_ks, const int64_t *slow_kd, const double *slow_w,
+                          const uint8_t *slow_err, const int64_t *slow_ids_off, const int32_t *slow_ids,
+                          int64_t *first_bad_line, int64_t *nsrc, int64_t *ndst);
+int dhgp_parse_dhg_fetch(dhgp_parse *ps, double *w, int64_t *src_off, int32_t *src_dat, int64_t *dst_off,
+                         int32_t *dst_dat);
+int dhgp_parse_dhg_line_range(dhgp_parse *ps, int64_t line, int64_t *byte_lo, int64_t *byte_hi);
+void dhgp_parse_free(dhgp_parse *ps);
+
 /* ---- data model (hgraph.py) ------------------------------------------ */
 /* Hypergraph._from_csr derived families — hgraph.py:212-238.  Output
  * sizes: in = dst_off[E], out = src_off[E], pins/inc = *num_pins_out

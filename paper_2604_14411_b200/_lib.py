@@ -89,6 +89,8 @@ EXPORTS = [
     "dhgp_sequence_gains", "dhgp_build_events_and_select",
     "dhgp_comm_nccl_unique_id", "dhgp_comm_init_nccl", "dhgp_comm_init_host", "dhgp_comm_set_min_units",
     "dhgp_comm_stats", "dhgp_comm_destroy", "dhgp_partition_sharded", "dhgp_session_set_comm", "dhgp_shard_range",
+    "dhgp_parse_dhg_begin", "dhgp_parse_dhg_slow_lines", "dhgp_parse_dhg_finish", "dhgp_parse_dhg_fetch",
+    "dhgp_parse_dhg_line_range", "dhgp_parse_free",
 ]
 
 _lib = None
@@ -108,6 +110,8 @@ def load(require_device: bool = True):
         L.dhgp_build_info.restype = C.c_char_p
         L.dhgp_comm_destroy.argtypes = [C.c_void_p]
         L.dhgp_comm_destroy.restype = None
+        L.dhgp_parse_free.argtypes = [C.c_void_p]
+        L.dhgp_parse_free.restype = None
         _lib = L
     if require_device and not _device_checked:
         n = C.c_int32(0)

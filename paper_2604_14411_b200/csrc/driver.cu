@@ -274,6 +274,7 @@ static void run_partition(Ctx &c, const DInput &in, const dhgp_config &cfg, Part
         size_t freeb = 0, total = 0;
         DHGP_CUDA(cudaMemGetInfo(&freeb, &total));
         keep_budget = (size_t)(0.4 * (double)(freeb + (g_pool_reserved[c.device] > 0 ? g_pool_reserved[c.device] : 0)));
+        keep_budget = std::min(keep_budget, 64 * level_bytes(levels[0]));  // bounded first-call pool growth
         const char *e = getenv("DHGP_KEEP_LEVELS_BYTES");  // tests: force the checkpoint/rebuild path
         if (e) keep_budget = (size_t)strtoull(e, nullptr, 10);
     }

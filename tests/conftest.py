@@ -25,7 +25,7 @@ def pytest_configure(config):
 def h1():
     import paper_2604_14411_b200 as dp
 
-    return dp.parse_dhg(H1_TEXT)
+    return dp.parse_dhg_host(H1_TEXT)
 
 
 def arrays_of(g):

@@ -44,9 +44,11 @@ def test_product_fails_loudly_without_device(monkeypatch):
         _lib.load()
     import paper_2604_14411_b200 as dp
 
-    g = dp.parse_dhg(H1_TEXT)
+    g = dp.parse_dhg_host(H1_TEXT)
     with pytest.raises(_lib.CudaUnavailableError):
         dp.partition(g, dp.Config(dp.Constraints(2, 4)))
+    with pytest.raises(_lib.CudaUnavailableError):
+        dp.parse_dhg(H1_TEXT)  # the GPU parser has no host fallback either
 
 
 def test_product_package_never_imports_the_oracle():
@@ -91,7 +93,7 @@ def test_csrsets_and_parse_dhg(h1):
         dp.CsrSets.from_lists([[3, 1]]).validate(strictly_increasing=True)
     for bad in ("", "3\n", "1 2\n1 1 1 0 5\n", "1 2\n-1 1 1 0 1\n", "1 2\n1 2 0 1 1\n", "2 2\n1 1 1 0 1\n"):
         with pytest.raises(dp.DhgParseError):
-            dp.parse_dhg(bad)
+            dp.parse_dhg_host(bad)
 
 
 def test_partition_files_roundtrip():
@@ -137,3 +139,23 @@ def test_snn_generator_shape():
 def test_hypergraph_is_immutable(h1):
     with pytest.raises(AttributeError):
         h1.num_nodes = 5
+
+
+def test_host_parse_restatement_matches_reference_golden():
+    """parse_dhg_host (the line rules the GPU parser defers to) against the
+    reference's own parse_dhg outputs and messages (tests/golden/parse_cases.json)."""
+    import json
+
+    import paper_2604_14411_b200 as dp
+
+    for case in json.loads((ROOT / "tests" / "golden" / "parse_cases.json").read_text()):
+        if case["ok"]:
+            g = dp.parse_dhg_host(case["text"])
+            assert g.num_nodes == case["num_nodes"]
+            assert g.edge_weight.tolist() == case["weights"]
+            assert g.edge_src.offsets.tolist() == case["src_off"] and g.edge_src.data.tolist() == case["src_dat"]
+            assert g.edge_dst.offsets.tolist() == case["dst_off"] and g.edge_dst.data.tolist() == case["dst_dat"]
+        else:
+            with pytest.raises(dp.DhgParseError) as ei:
+                dp.parse_dhg_host(case["text"])
+            assert (str(ei.value), ei.value.line) == (case["msg"], case["line"]), case["text"]
