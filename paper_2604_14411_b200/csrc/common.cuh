@@ -54,6 +54,16 @@ struct KernelStat {
 
 struct Comm;
 
+// Device memory: one arena per device over large cudaMalloc chunks, with a
+// best-fit free list (address-ordered, coalescing).  All library work on a
+// device runs on one stream in issue order, so a block freed on the host can
+// be handed out again at once — the stream orders the old and the new use
+// (the semantics of cudaMallocAsync on one stream).  Growing by cudaMalloc
+// chunks is ~100x cheaper than growing a stream-ordered pool (measured:
+// tests/micro/pool_growth.cu), and the chunks are kept for the process.
+void *arena_alloc(int device, size_t bytes);
+void arena_free(int device, void *p);
+
 struct Ctx {
     Comm *comm = nullptr;  // node-range sharding across ranks (comm.cuh); null = single GPU
     int device = 0;
@@ -69,14 +79,12 @@ struct Ctx {
 
     template <class T>
     T *alloc(int64_t n) {
-        void *p = nullptr;
-        size_t bytes = (size_t)(n > 0 ? n : 1) * sizeof(T);
-        DHGP_CUDA(cudaMallocAsync(&p, bytes, stream));
-        return (T *)p;
+        const size_t bytes = (size_t)(n > 0 ? n : 1) * sizeof(T);
+        return (T *)arena_alloc(device, bytes);
     }
     template <class T>
     void free(T *p) {
-        if (p) DHGP_CUDA(cudaFreeAsync((void *)p, stream));
+        if (p) arena_free(device, (void *)p);
     }
     template <class T>
     void zero(T *p, int64_t n) {

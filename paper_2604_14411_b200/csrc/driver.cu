@@ -2,7 +2,9 @@
 #include <chrono>
 #include <climits>
 #include <cstdlib>
+#include <map>
 #include <mutex>
+#include <unordered_map>
 
 #include "coarsen.cuh"
 #include "comm.cuh"
@@ -91,10 +93,108 @@ void Ctx::flush_profile() {
 }
 
 // ---------------------------------------------------------------------------
-// device setup: one cached stream per device, stream-ordered pool that keeps
-// freed blocks (levels are allocated and released every call)
+// device setup: one cached stream per device (memory: the arena above)
 // ---------------------------------------------------------------------------
 std::mutex g_mu;
+
+// ---------------------------------------------------------------------------
+// device arena (common.cuh)
+// ---------------------------------------------------------------------------
+namespace {
+struct Arena {
+    std::mutex mu;
+    std::map<char *, size_t> chunks;            // base -> bytes
+    std::map<char *, size_t> free_by_addr;      // free block -> bytes
+    std::multimap<size_t, char *> free_by_size;  // bytes -> free block
+    std::unordered_map<char *, size_t> used;     // allocated block -> bytes
+    size_t reserved = 0;
+
+    void insert_free(char *p, size_t n) {
+        free_by_addr[p] = n;
+        free_by_size.emplace(n, p);
+    }
+    void erase_free(std::map<char *, size_t>::iterator it) {
+        auto r = free_by_size.equal_range(it->second);
+        for (auto j = r.first; j != r.second; ++j)
+            if (j->second == it->first) {
+                free_by_size.erase(j);
+                break;
+            }
+        free_by_addr.erase(it);
+    }
+    char *chunk_end(char *p) {
+        auto it = chunks.upper_bound(p);
+        --it;
+        return it->first + it->second;
+    }
+    void *alloc(int device, size_t bytes) {
+        bytes = (bytes + 255) & ~(size_t)255;
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = free_by_size.lower_bound(bytes);
+        if (it == free_by_size.end()) {
+            // grow: at least 1 GiB, at least the reserve so far (doubling), capped at 32 GiB per chunk
+            size_t want = std::max<size_t>(bytes, std::min<size_t>(std::max<size_t>(1ull << 30, reserved),
+                                                                   32ull << 30));
+            char *base = nullptr;
+            cudaError_t e = cudaMalloc((void **)&base, want);
+            if (e != cudaSuccess && want > bytes) {
+                cudaGetLastError();
+                want = bytes;
+                e = cudaMalloc((void **)&base, want);
+            }
+            if (e != cudaSuccess) {
+                cudaGetLastError();
+                throw Error{DHGP_ERR_CUDA, "device memory exhausted: cannot allocate " + std::to_string(bytes) +
+                                               " bytes (" + std::to_string(reserved) + " held by libdhgp on device " +
+                                               std::to_string(device) + ")"};
+            }
+            chunks[base] = want;
+            reserved += want;
+            insert_free(base, want);
+            it = free_by_size.lower_bound(bytes);
+        }
+        char *p = it->second;
+        const size_t have = it->first;
+        erase_free(free_by_addr.find(p));
+        if (have > bytes) insert_free(p + bytes, have - bytes);
+        used[p] = bytes;
+        return p;
+    }
+    void release(void *vp) {
+        char *p = (char *)vp;
+        std::lock_guard<std::mutex> lk(mu);
+        auto u = used.find(p);
+        if (u == used.end()) throw Error{DHGP_ERR_CUDA, "arena: free of an unknown pointer"};
+        size_t n = u->second;
+        used.erase(u);
+        char *end = chunk_end(p);
+        // coalesce with the following and the preceding free blocks of the same chunk
+        auto nx = free_by_addr.find(p + n);
+        if (nx != free_by_addr.end() && p + n < end) {
+            n += nx->second;
+            erase_free(nx);
+        }
+        auto pv = free_by_addr.lower_bound(p);
+        if (pv != free_by_addr.begin()) {
+            --pv;
+            if (pv->first + pv->second == p && chunk_end(pv->first) == end) {
+                p = pv->first;
+                n += pv->second;
+                erase_free(pv);
+            }
+        }
+        insert_free(p, n);
+    }
+};
+Arena g_arena[64];
+}  // namespace
+
+void *arena_alloc(int device, size_t bytes) { return g_arena[device].alloc(device, bytes); }
+static size_t arena_reserved(int device) {
+    std::lock_guard<std::mutex> lk(g_arena[device].mu);
+    return g_arena[device].reserved;
+}
+void arena_free(int device, void *p) { g_arena[device].release(p); }
 static cudaStream_t g_streams[64];
 static int g_sms[64];
 
@@ -104,10 +204,6 @@ static void setup(Ctx &c, int device) {
     DHGP_CUDA(cudaSetDevice(device));
     if (!g_streams[device]) {
         DHGP_CUDA(cudaStreamCreateWithFlags(&g_streams[device], cudaStreamNonBlocking));
-        cudaMemPool_t pool;
-        DHGP_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
-        uint64_t thr = UINT64_MAX;
-        DHGP_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
         DHGP_CUDA(cudaDeviceGetAttribute(&g_sms[device], cudaDevAttrMultiProcessorCount, device));
     }
     c.stream = g_streams[device];
@@ -180,28 +276,6 @@ static void rebuild_levels(Ctx &c, std::vector<DLevel> &levels, size_t hi) {
     c.free(status);
 }
 
-// Grows the device's stream-ordered pool once to `want` bytes (capped at 60%
-// of the free memory), so that level allocations during coarsening never
-// wait on the driver to map fresh physical memory.  The pool keeps what it
-// reserved (release threshold = max), so later calls pay nothing.
-static size_t g_pool_reserved[64];
-static void reserve_pool(Ctx &c, size_t want) {
-    if (want <= g_pool_reserved[c.device]) return;
-    size_t freeb = 0, total = 0;
-    DHGP_CUDA(cudaMemGetInfo(&freeb, &total));
-    const size_t cap = g_pool_reserved[c.device] + (size_t)(0.6 * (double)freeb);
-    want = std::min(want, cap);
-    if (want <= g_pool_reserved[c.device] || want < ((size_t)64 << 20)) return;
-    void *p = nullptr;
-    if (cudaMallocAsync(&p, want, c.stream) != cudaSuccess) {
-        cudaGetLastError();
-        return;
-    }
-    DHGP_CUDA(cudaFreeAsync(p, c.stream));
-    c.sync();
-    g_pool_reserved[c.device] = want;
-}
-
 static double now_ms() {
     return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
@@ -229,12 +303,7 @@ static void run_partition(Ctx &c, const DInput &in, const dhgp_config &cfg, Part
     }
     std::vector<DLevel> levels(1);
     build_level0(c, in, levels[0]);
-    {
-        const DLevel &l0 = levels[0];
-        const size_t b0 = 8 * (3 * (size_t)l0.E + 2 * (size_t)l0.N + 8) +
-                          4 * ((size_t)l0.Ps + l0.Pd + 2 * l0.U + l0.Sin + 2 * (size_t)l0.N);
-        reserve_pool(c, 32 * b0);
-    }
+
     const int32_t N0 = in.N;
     if (N0 > 0) {
         int32_t bs, bi;
@@ -273,8 +342,7 @@ static void run_partition(Ctx &c, const DInput &in, const dhgp_config &cfg, Part
     {
         size_t freeb = 0, total = 0;
         DHGP_CUDA(cudaMemGetInfo(&freeb, &total));
-        keep_budget = (size_t)(0.4 * (double)(freeb + (g_pool_reserved[c.device] > 0 ? g_pool_reserved[c.device] : 0)));
-        keep_budget = std::min(keep_budget, 64 * level_bytes(levels[0]));  // bounded first-call pool growth
+        keep_budget = (size_t)(0.4 * (double)(freeb + arena_reserved(c.device)));
         const char *e = getenv("DHGP_KEEP_LEVELS_BYTES");  // tests: force the checkpoint/rebuild path
         if (e) keep_budget = (size_t)strtoull(e, nullptr, 10);
     }

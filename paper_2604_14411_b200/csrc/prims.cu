@@ -184,14 +184,14 @@ void scan_excl(Ctx &c, const T *in, int64_t *out, int64_t n) {
     if (ss.cap < ntiles) {
         // stream-ordered: earlier kernels on this stream are done with the old buffers
         if (ss.flag) {
-            DHGP_CUDA(cudaFreeAsync(ss.flag, c.stream));
-            DHGP_CUDA(cudaFreeAsync(ss.agg, c.stream));
-            DHGP_CUDA(cudaFreeAsync(ss.inc, c.stream));
+            c.free(ss.flag);
+            c.free(ss.agg);
+            c.free(ss.inc);
         }
         ss.cap = std::max<int64_t>(ntiles, 4096);
-        DHGP_CUDA(cudaMallocAsync((void **)&ss.flag, sizeof(uint32_t) * ss.cap, c.stream));
-        DHGP_CUDA(cudaMallocAsync((void **)&ss.agg, sizeof(int64_t) * ss.cap, c.stream));
-        DHGP_CUDA(cudaMallocAsync((void **)&ss.inc, sizeof(int64_t) * ss.cap, c.stream));
+        ss.flag = c.alloc<uint32_t>(ss.cap);
+        ss.agg = c.alloc<int64_t>(ss.cap);
+        ss.inc = c.alloc<int64_t>(ss.cap);
         DHGP_CUDA(cudaMemsetAsync(ss.flag, 0, sizeof(uint32_t) * ss.cap, c.stream));
         ss.epoch = 0;
     }

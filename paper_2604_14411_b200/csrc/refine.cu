@@ -933,6 +933,205 @@ __global__ void k_best_prefix_final(int nb, const long long *bv, const long long
     out[1] = v;
 }
 
+// ---------------------------------------------------------------------------
+// A17 in one CTA for small rounds (T <= SEL_T events, M <= SEL_M moves): the
+// event sort, the segmented toggle formulation, active[] and the best prefix
+// in shared memory — the same arithmetic as the multi-kernel path below, in
+// one launch and without reading T on the host.  res[2] = 1 when the round
+// is too large (the host then runs the multi-kernel path).
+// ---------------------------------------------------------------------------
+constexpr int SEL_T = 4096, SEL_M = 4096, SEL_THREADS = 1024;
+constexpr size_t sel_smem() {
+    return (size_t)SEL_T * 8 + (size_t)SEL_T * 4 + (size_t)(SEL_T + 1) * 8 + 2 * (size_t)SEL_T * 4 +
+           (size_t)(SEL_M + 2) * 4 + (size_t)(SEL_M + 1) * 8 + 64;
+}
+
+// block-wide exclusive scan of a per-thread value (SEL_THREADS threads)
+__device__ __forceinline__ int64_t sel_excl(int64_t v, int64_t *sh, int64_t *total) {
+    const int lane = lane_id(), w = warp_id(), nw = SEL_THREADS / 32;
+    const int64_t incl = warp_incl_scan(v);
+    if (lane == 31) sh[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+        const int64_t x = lane < nw ? sh[lane] : 0;
+        const int64_t xi = warp_incl_scan(x);
+        if (lane < nw) sh[lane] = xi - x;
+        if (lane == nw - 1) sh[32] = xi;
+    }
+    __syncthreads();
+    const int64_t r = incl - v + sh[w];
+    *total = sh[32];
+    __syncthreads();
+    return r;
+}
+// out[0..n] = exclusive prefix sums of f(0..n-1) (each thread a contiguous chunk)
+template <class F>
+__device__ __forceinline__ void sel_scan_sum(int n, F f, int64_t *out, int64_t *sh) {
+    const int per = (n + SEL_THREADS - 1) / SEL_THREADS;
+    const int a = min(n, (int)threadIdx.x * per), b = min(n, a + per);
+    int64_t loc = 0;
+    for (int i = a; i < b; i++) loc += f(i);
+    int64_t tot;
+    int64_t run = sel_excl(loc, sh, &tot);
+    for (int i = a; i < b; i++) {
+        const int64_t v = f(i);
+        out[i] = run;
+        run += v;
+    }
+    if (threadIdx.x == 0) out[n] = tot;
+    __syncthreads();
+}
+// in-place inclusive running maximum of a[0..n) (non-negative values)
+__device__ __forceinline__ void sel_runmax(int n, int32_t *a, int64_t *sh) {
+    const int per = (n + SEL_THREADS - 1) / SEL_THREADS;
+    const int lo = min(n, (int)threadIdx.x * per), hi = min(n, lo + per);
+    int32_t m = 0;
+    for (int i = lo; i < hi; i++) m = max(m, a[i]);
+    // exclusive running max over threads
+    const int lane = lane_id(), w = warp_id();
+    int32_t incl = m;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int32_t o = __shfl_up_sync(FULL_MASK, incl, d);
+        if (lane >= d) incl = max(incl, o);
+    }
+    if (lane == 31) sh[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+        const int64_t x = lane < SEL_THREADS / 32 ? sh[lane] : 0;
+        int64_t xi = x;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int64_t o = __shfl_up_sync(FULL_MASK, xi, d);
+            if (lane >= d) xi = max(xi, o);
+        }
+        const int64_t prev = __shfl_up_sync(FULL_MASK, xi, 1);
+        if (lane < SEL_THREADS / 32) sh[lane] = lane == 0 ? 0 : prev;
+    }
+    __syncthreads();
+    int32_t excl = __shfl_up_sync(FULL_MASK, incl, 1);
+    if (lane == 0) excl = 0;
+    int32_t run = max(excl, (int32_t)sh[w]);
+    for (int i = lo; i < hi; i++) {
+        run = max(run, a[i]);
+        a[i] = run;
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(SEL_THREADS) k_select_small(const unsigned long long *ecount, int64_t M,
+                                                              const uint64_t *ekey, const uint32_t *evals,
+                                                              const int64_t *gseq, const int64_t *psizes,
+                                                              const int64_t *pinbound, int64_t omega, int64_t delta,
+                                                              int ibits, int pbits, int64_t *act_ex_out,
+                                                              long long *res) {
+    extern __shared__ unsigned long long smem_u64[];
+    __shared__ int64_t sh[33];
+    __shared__ long long s_bv[32], s_bk[32];
+    const int64_t T = (int64_t)*ecount;
+    if (T > SEL_T || M > SEL_M - 2) {
+        if (threadIdx.x == 0) res[2] = 1;
+        return;
+    }
+    uint64_t *sk = (uint64_t *)smem_u64;
+    uint32_t *sv = (uint32_t *)(sk + SEL_T);
+    int64_t *ex = (int64_t *)(sv + SEL_T);
+    int32_t *gst = (int32_t *)(ex + SEL_T + 1);
+    int32_t *sst = gst + SEL_T;
+    int32_t *dlt = sst + SEL_T;
+    int64_t *cum = (int64_t *)(((uintptr_t)(dlt + SEL_M + 2) + 7) & ~(uintptr_t)7);
+    const int n = (int)T;
+    // 1. sort the events by key (equal keys only need grouping)
+    int np = 1;
+    while (np < n) np <<= 1;
+    for (int i = threadIdx.x; i < np; i += SEL_THREADS) {
+        sk[i] = i < n ? ekey[i] : ~0ull;
+        sv[i] = i < n ? evals[i] : 0u;
+    }
+    for (int size = 2; size <= np; size <<= 1) {
+        for (int j = size >> 1; j > 0; j >>= 1) {
+            __syncthreads();
+            for (int t = threadIdx.x; t < (np >> 1); t += SEL_THREADS) {
+                const int lo = 2 * j * (t / j) + (t % j), hi = lo + j;
+                const bool asc = (lo & size) == 0;
+                const uint64_t a = sk[lo], b = sk[hi];
+                if ((a > b) == asc) {
+                    sk[lo] = b;
+                    sk[hi] = a;
+                    const uint32_t va = sv[lo];
+                    sv[lo] = sv[hi];
+                    sv[hi] = va;
+                }
+            }
+        }
+    }
+    __syncthreads();
+    // 2. group / segment starts, deltas' exclusive sums
+    for (int k = threadIdx.x; k < n; k += SEL_THREADS) {
+        const uint64_t kk = sk[k];
+        gst[k] = (k == 0 || sk[k - 1] != kk) ? k : 0;
+        sst[k] = (k == 0 || (sk[k - 1] >> ibits) != (kk >> ibits)) ? k : 0;
+    }
+    for (int i = threadIdx.x; i < (int)M + 2; i += SEL_THREADS) dlt[i] = 0;
+    __syncthreads();
+    sel_scan_sum(n, [&](int k) { return (int64_t)(int32_t)sv[k]; }, ex, sh);
+    sel_runmax(n, gst, sh);
+    sel_runmax(n, sst, sh);
+    // 3. toggles (refine.py:145-175)
+    for (int k = threadIdx.x; k < n; k += SEL_THREADS) {
+        const uint64_t kk = sk[k];
+        if (k + 1 < n && sk[k + 1] == kk) continue;
+        const int track = (int)(kk >> (ibits + pbits));
+        const int32_t p = (int32_t)((kk >> ibits) & ((1ull << pbits) - 1ull));
+        const int64_t i = (int64_t)(kk & ((1ull << ibits) - 1ull));
+        const int64_t base = track ? pinbound[p] : psizes[p];
+        const int64_t limit = track ? delta : omega;
+        const int64_t s0 = ex[sst[k]];
+        const bool after = base + ex[k + 1] - s0 > limit;
+        const bool before = base + ex[gst[k]] - s0 > limit;
+        if (after != before) atomicAdd(&dlt[i + 1], after ? 1 : -1);
+    }
+    __syncthreads();
+    // 4. active[j] = act_ex[j + 1]; cum = exclusive sums of gain_seq
+    int64_t *act = ex;  // reuse: the events are done
+    sel_scan_sum((int)M + 1, [&](int j) { return (int64_t)dlt[j]; }, act, sh);
+    for (int j = threadIdx.x; j < (int)M + 2; j += SEL_THREADS) act_ex_out[j] = act[j];
+    sel_scan_sum((int)M, [&](int j) { return gseq[j]; }, cum, sh);
+    // 5. smallest argmax of cum over prefixes with active == 0 (refine.py:244-247)
+    long long v = LLONG_MIN, bk = LLONG_MAX;
+    for (int j = threadIdx.x; j <= (int)M; j += SEL_THREADS)
+        if (act[j + 1] == 0) {
+            const long long c = cum[j];
+            if (c > v || (c == v && j < bk)) {
+                v = c;
+                bk = j;
+            }
+        }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        const long long ov = __shfl_xor_sync(FULL_MASK, v, d), ok = __shfl_xor_sync(FULL_MASK, bk, d);
+        if (ov > v || (ov == v && ok < bk)) {
+            v = ov;
+            bk = ok;
+        }
+    }
+    if (lane_id() == 0) {
+        s_bv[warp_id()] = v;
+        s_bk[warp_id()] = bk;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < SEL_THREADS / 32; w++)
+            if (s_bv[w] > v || (s_bv[w] == v && s_bk[w] < bk)) {
+                v = s_bv[w];
+                bk = s_bk[w];
+            }
+        res[0] = bk;
+        res[1] = v;
+        res[2] = 0;
+    }
+}
+
 __global__ void k_apply(int64_t k, const int32_t *node, const int32_t *to, int32_t *assign) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < k) assign[node[i]] = to[i];
@@ -1061,6 +1260,7 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, int32_t *assign, i
         DHGP_CUDA(cudaFuncSetAttribute(k_propose_heavy<unsigned long long>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)ph_smem<unsigned long long>(ph_maxk<unsigned long long>())));
+        DHGP_CUDA(cudaFuncSetAttribute(k_select_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sel_smem()));
         DHGP_CUDA(cudaFuncSetAttribute(k_propose_mid<unsigned>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        pm_smem<unsigned>()));
         DHGP_CUDA(cudaFuncSetAttribute(k_propose_mid<unsigned long long>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1093,6 +1293,7 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, int32_t *assign, i
     uint64_t *ek = c.alloc<uint64_t>(ecap), *ekt = c.alloc<uint64_t>(ecap);
     uint32_t *evv = c.alloc<uint32_t>(ecap), *evt = c.alloc<uint32_t>(ecap);
     unsigned long long *ecount = c.alloc<unsigned long long>(1);
+    long long *sres = c.alloc<long long>(4);
     // dense global tier (K too large for shared memory): per-block rows of K
     // counters + touched lists, as many blocks as ~1 GiB allows (4 per SM max)
     const int pb_blocks = (int)std::max<int64_t>(
@@ -1240,54 +1441,65 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, int32_t *assign, i
                                                                      ev, big, ctr, ctr + 2);
             DHGP_LAUNCHED(c);
         }
-        // ---- sync 2: event count --------------------------------------------
-        unsigned long long T = 0;
-        int32_t hc[4];
-        c.d2h(&T, ecount, 1);
-        c.d2h(hc, ctr, 4);
-        c.sync();
-        if (hc[2]) throw Error{DHGP_ERR_UNSUPPORTED, "too many movers on one h-edge"};
+        // --- A17 select: one CTA for small rounds, T read on device ----------
         int64_t kbest = 0, total_gain = 0;
         int64_t *dlt = c.alloc<int64_t>(M + 1);
         int64_t *act_ex = c.alloc<int64_t>(M + 2);
         int64_t *cum = c.alloc<int64_t>(M + 1);
         {
             KScope ks(c, "select", 0.0, N);
-            if ((int64_t)T <= kSmallSort)
-                small_sort_pairs(c, ek, evv, (int64_t)T);  // equal keys only need grouping
-            else
-                radix_sort_pairs(c, ek, evv, ekt, evt, (int64_t)T, nullptr, 1 + ibits + pbits);
-            int64_t *gs = c.alloc<int64_t>(T), *ss = c.alloc<int64_t>(T), *dv = c.alloc<int64_t>(T);
-            int64_t *ex = c.alloc<int64_t>(T + 1), *gst = c.alloc<int64_t>(T), *sst = c.alloc<int64_t>(T);
-            c.zero(dlt, M + 1);
-            if (T > 0) {
-                k_ev_prep<<<(unsigned)cdiv(T, 256), 256, 0, c.stream>>>((int64_t)T, ek, evv, ibits, gs, ss, dv);
-                DHGP_LAUNCHED(c);
-                scan_excl<int64_t>(c, dv, ex, T);
-                scan_incl_max(c, gs, gst, T);
-                scan_incl_max(c, ss, sst, T);
-                k_ev_toggle<<<(unsigned)cdiv(T, 256), 256, 0, c.stream>>>((int64_t)T, ek, ex, gst, sst, ibits, pbits,
-                                                                          psizes, pinbound, omega, delta, dlt);
-                DHGP_LAUNCHED(c);
-            }
-            scan_excl<int64_t>(c, dlt, act_ex, M + 1);  // act_ex[j+1] = active[j]
-            scan_excl<int64_t>(c, gseq, cum, M);        // cum[j] = sum of the first j gains
-            const int nb = (int)std::min<int64_t>(cdiv(M + 1, 256), 256);
-            long long *bv = c.alloc<long long>(nb), *bk = c.alloc<long long>(nb), *res = c.alloc<long long>(2);
-            k_best_prefix_partial<<<nb, 256, 0, c.stream>>>(M + 1, act_ex, cum, bv, bk);
+            k_select_small<<<1, SEL_THREADS, sel_smem(), c.stream>>>(ecount, M, ek, evv, gseq, psizes, pinbound,
+                                                                    omega, delta, ibits, pbits, act_ex, sres);
             DHGP_LAUNCHED(c);
-            k_best_prefix_final<<<1, 32, 0, c.stream>>>(nb, bv, bk, res);
-            DHGP_LAUNCHED(c);
-            // ---- sync 2: the selected prefix -------------------------------
-            long long hr[2];
-            c.d2h(hr, res, 2);
+            // ---- sync 2: the selected prefix (or "too large"), error flags ---
+            long long hr[3];
+            int32_t hc[4];
+            c.d2h(hr, sres, 3);
+            c.d2h(hc, ctr, 4);
             c.sync();
+            if (hc[2]) throw Error{DHGP_ERR_UNSUPPORTED, "too many movers on one h-edge"};
             kbest = hr[0];
             total_gain = hr[1];
-            c.free(bv);
-            c.free(bk);
-            c.free(res);
-            for (void *q : {(void *)gs, (void *)ss, (void *)dv, (void *)ex, (void *)gst, (void *)sst}) c.free(q);
+            if (hr[2]) {  // a large round: the multi-kernel path
+                unsigned long long T = 0;
+                c.d2h(&T, ecount, 1);
+                c.sync();
+                if ((int64_t)T <= kSmallSort)
+                    small_sort_pairs(c, ek, evv, (int64_t)T);  // equal keys only need grouping
+                else
+                    radix_sort_pairs(c, ek, evv, ekt, evt, (int64_t)T, nullptr, 1 + ibits + pbits);
+                int64_t *gs = c.alloc<int64_t>(T), *ss = c.alloc<int64_t>(T), *dv = c.alloc<int64_t>(T);
+                int64_t *ex = c.alloc<int64_t>(T + 1), *gst = c.alloc<int64_t>(T), *sst = c.alloc<int64_t>(T);
+                c.zero(dlt, M + 1);
+                if (T > 0) {
+                    k_ev_prep<<<(unsigned)cdiv(T, 256), 256, 0, c.stream>>>((int64_t)T, ek, evv, ibits, gs, ss, dv);
+                    DHGP_LAUNCHED(c);
+                    scan_excl<int64_t>(c, dv, ex, T);
+                    scan_incl_max(c, gs, gst, T);
+                    scan_incl_max(c, ss, sst, T);
+                    k_ev_toggle<<<(unsigned)cdiv(T, 256), 256, 0, c.stream>>>((int64_t)T, ek, ex, gst, sst, ibits,
+                                                                              pbits, psizes, pinbound, omega, delta,
+                                                                              dlt);
+                    DHGP_LAUNCHED(c);
+                }
+                scan_excl<int64_t>(c, dlt, act_ex, M + 1);  // act_ex[j+1] = active[j]
+                scan_excl<int64_t>(c, gseq, cum, M);        // cum[j] = sum of the first j gains
+                const int nb = (int)std::min<int64_t>(cdiv(M + 1, 256), 256);
+                long long *bv = c.alloc<long long>(nb), *bk = c.alloc<long long>(nb), *res = c.alloc<long long>(2);
+                k_best_prefix_partial<<<nb, 256, 0, c.stream>>>(M + 1, act_ex, cum, bv, bk);
+                DHGP_LAUNCHED(c);
+                k_best_prefix_final<<<1, 32, 0, c.stream>>>(nb, bv, bk, res);
+                DHGP_LAUNCHED(c);
+                long long h2[2];
+                c.d2h(h2, res, 2);
+                c.sync();
+                kbest = h2[0];
+                total_gain = h2[1];
+                c.free(bv);
+                c.free(bk);
+                c.free(res);
+                for (void *q : {(void *)gs, (void *)ss, (void *)dv, (void *)ex, (void *)gst, (void *)sst}) c.free(q);
+            }
         }
         if (obs && *obs) {
             RoundRecord rec;
@@ -1333,7 +1545,7 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, int32_t *assign, i
                     (void *)pinbound, (void *)target, (void *)gain, (void *)flags, (void *)mpos, (void *)pos,
                     (void *)ctr, (void *)big, (void *)big2, (void *)conn_d, (void *)mk, (void *)mkt, (void *)mv, (void *)mvt,
                     (void *)node, (void *)from, (void *)to, (void *)giso, (void *)gseq, (void *)ek, (void *)ekt,
-                    (void *)evv, (void *)evt, (void *)ecount, (void *)pdense, (void *)ptouched})
+                    (void *)evv, (void *)evt, (void *)ecount, (void *)sres, (void *)pdense, (void *)ptouched})
         c.free(p);
 }
 
