@@ -320,8 +320,8 @@ def run_ours(args, ws, rank, local):
                    "levels": int(ref_out[2]), "parts": int(nparts.value),
                    "final_connectivity": ref_out[3][-1] if ref_out[3] else None,
                    "l2": "flushed (512 MiB write) before every timed step",
-                   "parallelism": (f"node-range sharded over {ws} GPUs (ncclAllGather of pair/score, "
-                                   f"target/gain, gain_seq; everything else replicated)") if ws > 1 else "single GPU"},
+                   "parallelism": (f"node-range sharded over {ws} GPUs (ncclAllGather of pair/score and "
+                                   f"target/gain; everything else replicated)") if ws > 1 else "single GPU"},
         "e2e": {"value": round(e2e, 6), "unit": "s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),

@@ -135,9 +135,9 @@ int dhgp_session_set_profiling(dhgp_session *s, int32_t on);
  * No reference interface: the reference is single-threaded.  These extend
  * dhgp_partition (driver.py:76-163) to one process per GPU; the result is
  * bit-identical to the single-GPU call at every world size.  Scoring
- * (coarsen.py:93-132), proposals (refine.py:82-116) and in-sequence gains
- * (refine.py:119-142) are computed per node / move range and completed by an
- * in-place allgather; everything else runs replicated. */
+ * (coarsen.py:93-132) and proposals (refine.py:82-116) are computed per node
+ * range and completed by an in-place allgather; everything else runs
+ * replicated. */
 #define DHGP_COMM_NCCL 1 /* ncclAllGather on the library stream (libnccl.so.2, loaded at run time) */
 #define DHGP_COMM_HOST 2 /* the caller's allgather over host memory (gloo, MPI, tests) */
 typedef struct dhgp_comm dhgp_comm;

@@ -1,10 +1,10 @@
 // comm.cuh — node-range sharding across ranks.
 //
 // One process per GPU.  Every rank holds a replica of every level (the
-// contraction and the event pipeline run replicated and are deterministic);
-// the per-node phases — candidate scoring (A4-A6), move proposals (A14) and
-// in-sequence gains (A15) — are computed for this rank's contiguous node (or
-// move) range only and completed by an in-place allgather of their outputs.
+// contraction, the sequence gains and the event pipeline run replicated and
+// are deterministic); the per-node phases — candidate scoring (A4-A6) and
+// move proposals (A14) — are computed for this rank's contiguous node range
+// only and completed by an in-place allgather of their outputs.
 // The exchanged values are exact integers / f64 and every later tie-break is
 // the reference's global total order, so the result is bit-identical to the
 // single-GPU run at any world size.

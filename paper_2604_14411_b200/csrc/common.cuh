@@ -164,6 +164,7 @@ struct Tiers {
     int pr_heavy_inc = 128;   // propose: incident h-edges above which a block takes the node
     int pm_limit = 3072;      // propose: distinct parts per medium-tier table
     int small_k = 4096;       // propose: K up to which escalated nodes use dense shared arrays
+    int edge_movers = 32;     // events / sequence gains: movers per h-edge for the thread tier (<= 32)
 };
 const Tiers &tiers();
 

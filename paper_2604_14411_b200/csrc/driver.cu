@@ -43,6 +43,7 @@ const Tiers &tiers() {
             x.pr_limit = 2;
             x.pr_heavy_inc = 1;
             x.pm_limit = 3;
+            x.edge_movers = 2;
         }
         return x;
     }();

@@ -732,7 +732,7 @@ __device__ __forceinline__ void emit(const EvArgs &ev, uint64_t track, int32_t p
 constexpr int kEvLocal = 32;
 __global__ void k_inbound_events(int32_t E, const int64_t *dst_off, const int32_t *dst_dat, const int64_t *pin_off,
                                  Runs r, const int32_t *pos, const int32_t *from, const int32_t *to, EvArgs ev,
-                                 int32_t *big_list, int32_t *big_count) {
+                                 int32_t *big_list, int32_t *big_count, int cap) {
     int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= E) return;
     int32_t mv[kEvLocal];
@@ -740,7 +740,7 @@ __global__ void k_inbound_events(int32_t E, const int64_t *dst_off, const int32_
     for (int64_t q = dst_off[e]; q < dst_off[e + 1]; q++) {
         int32_t j = pos[dst_dat[q]];
         if (j < 0) continue;
-        if (nm == kEvLocal) {
+        if (nm == cap) {
             big_list[atomicAdd(big_count, 1)] = (int32_t)e;
             return;
         }
@@ -1198,51 +1198,140 @@ __global__ void k_size_events_dn(const int64_t *dM, const int32_t *node, const i
     ev.key[2 * i + 1] = ((uint64_t)(uint32_t)to[i] << ev.ibits) | (uint64_t)i;
     ev.val[2 * i + 1] = (uint32_t)s;
 }
-// A15: gains corrected for earlier moves, rules (a)-(d) (_kernels.pyx:326-363)
-__global__ void k_seq_gains_dn(int64_t mlo, int64_t mhi, const int64_t *inc_off, const int32_t *inc_dat,
-                               const int64_t *pin_off, const int32_t *pin_dat, const int64_t *wi, Runs r,
-                               const int32_t *node, const int32_t *from, const int32_t *to, const int64_t *giso,
-                               const int32_t *pos, int64_t *gseq) {
-    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
-    const int lane = lane_id();
-    for (int64_t i = mlo + (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id(); i < mhi; i += nw) {
-        const int32_t n = node[i], ps = from[i], pd = to[i];
-        int64_t acc = 0;
-        for (int64_t ii = inc_off[n] + lane; ii < inc_off[n + 1]; ii += 32) {
-            const int32_t e = inc_dat[ii];
-            const int64_t lo = pin_off[e];
-            const int32_t lam = r.len[e];
-            int32_t k;
-            k = run_find(r, lo, lam, ps);
+// A15: gains corrected for earlier moves, rules (a)-(d) (_kernels.pyx:326-363),
+// computed per h-edge: the movers among an h-edge's pins, in sequence order,
+// give every (move, h-edge) term from counts over the earlier movers on that
+// h-edge — O(sum |e|) for the round instead of O(sum over moves of the pins
+// of their h-edges).  Terms are integers, summed with atomics (exact).
+__device__ __forceinline__ int64_t seq_net(int64_t we, int32_t base_ps, int32_t base_pd, int32_t leav_pd,
+                                           int32_t ent_pd, int32_t leav_ps, int32_t ent_ps) {
+    int64_t net = 0;
+    if (base_pd > 0) {
+        if (leav_pd - ent_pd == base_pd) net -= we;
+    } else if (ent_pd > 0) {
+        net += we;
+    }
+    if (base_ps == 1) {
+        if (ent_ps > 0) net -= we;
+    } else if (base_ps - 1 > 0 && leav_ps - ent_ps == base_ps - 1) {
+        net += we;
+    }
+    return net;
+}
+constexpr int kSgLocal = 32;
+__global__ void k_seq_gains_edge(int32_t E, const int64_t *pin_off, const int32_t *pin_dat, const int64_t *wi,
+                                 Runs r, const int32_t *pos, const int32_t *from, const int32_t *to,
+                                 unsigned long long *gacc, int32_t *big_list, int32_t *big_count, int cap) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= E) return;
+    int32_t mv[kSgLocal];
+    int nm = 0;
+    const int64_t lo = pin_off[e], hi = pin_off[e + 1];
+    for (int64_t pp = lo; pp < hi; pp++) {
+        const int32_t j = pos[pin_dat[pp]];
+        if (j < 0) continue;
+        if (nm == cap) {
+            big_list[atomicAdd(big_count, 1)] = (int32_t)e;
+            return;
+        }
+        mv[nm++] = j;
+    }
+    if (nm == 0) return;
+    for (int a = 1; a < nm; a++) {
+        const int32_t x = mv[a];
+        int b = a - 1;
+        while (b >= 0 && mv[b] > x) {
+            mv[b + 1] = mv[b];
+            b--;
+        }
+        mv[b + 1] = x;
+    }
+    int32_t mf[kSgLocal], mt[kSgLocal];
+    for (int a = 0; a < nm; a++) {
+        mf[a] = from[mv[a]];
+        mt[a] = to[mv[a]];
+    }
+    const int64_t we = wi[e];
+    const int32_t lam = r.len[e];
+    for (int a = 0; a < nm; a++) {
+        const int32_t ps = mf[a], pd = mt[a];
+        int32_t leav_pd = 0, ent_pd = 0, leav_ps = 0, ent_ps = 0;
+        for (int b = 0; b < a; b++) {
+            leav_pd += mf[b] == pd;
+            ent_pd += mt[b] == pd;
+            leav_ps += mf[b] == ps;
+            ent_ps += mt[b] == ps;
+        }
+        int32_t k = run_find(r, lo, lam, ps);
+        const int32_t base_ps = k >= 0 ? r.cnt[lo + k] : 0;
+        k = run_find(r, lo, lam, pd);
+        const int32_t base_pd = k >= 0 ? r.cnt[lo + k] : 0;
+        const int64_t net = seq_net(we, base_ps, base_pd, leav_pd, ent_pd, leav_ps, ent_ps);
+        if (net) atomicAdd(&gacc[mv[a]], (unsigned long long)net);
+    }
+}
+// the same for h-edges with many movers: a block gathers and sorts them, each
+// thread takes some movers and counts over the earlier ones
+constexpr int kSgBlockMax = 2048;
+__global__ void k_seq_gains_edge_block(const int64_t *pin_off, const int32_t *pin_dat, const int64_t *wi, Runs r,
+                                       const int32_t *pos, const int32_t *from, const int32_t *to,
+                                       unsigned long long *gacc, const int32_t *big_list, const int32_t *big_count,
+                                       int32_t *err) {
+    __shared__ uint32_t smv[kSgBlockMax];
+    __shared__ int32_t sf[kSgBlockMax], st[kSgBlockMax];
+    __shared__ int32_t snm;
+    const int nbig = *big_count;
+    for (int t = blockIdx.x; t < nbig; t += gridDim.x) {
+        const int32_t e = big_list[t];
+        if (threadIdx.x == 0) snm = 0;
+        __syncthreads();
+        const int64_t lo = pin_off[e], hi = pin_off[e + 1];
+        for (int64_t pp = lo + threadIdx.x; pp < hi; pp += blockDim.x) {
+            const int32_t j = pos[pin_dat[pp]];
+            if (j >= 0) {
+                const int q = atomicAdd(&snm, 1);
+                if (q < kSgBlockMax) smv[q] = (uint32_t)j;
+            }
+        }
+        __syncthreads();
+        const int nm = snm;
+        if (nm > kSgBlockMax) {
+            if (threadIdx.x == 0) atomicMax(err, nm);
+            __syncthreads();
+            continue;
+        }
+        const int np = next_pow2(nm);
+        for (int q = nm + threadIdx.x; q < np; q += blockDim.x) smv[q] = 0xffffffffu;
+        block_bitonic_sort32(smv, np);
+        for (int a = threadIdx.x; a < nm; a += blockDim.x) {
+            sf[a] = from[smv[a]];
+            st[a] = to[smv[a]];
+        }
+        __syncthreads();
+        const int64_t we = wi[e];
+        const int32_t lam = r.len[e];
+        for (int a = threadIdx.x; a < nm; a += blockDim.x) {
+            const int32_t ps = sf[a], pd = st[a];
+            int32_t leav_pd = 0, ent_pd = 0, leav_ps = 0, ent_ps = 0;
+            for (int b = 0; b < a; b++) {
+                leav_pd += sf[b] == pd;
+                ent_pd += st[b] == pd;
+                leav_ps += sf[b] == ps;
+                ent_ps += st[b] == ps;
+            }
+            int32_t k = run_find(r, lo, lam, ps);
             const int32_t base_ps = k >= 0 ? r.cnt[lo + k] : 0;
             k = run_find(r, lo, lam, pd);
             const int32_t base_pd = k >= 0 ? r.cnt[lo + k] : 0;
-            int32_t leav_pd = 0, ent_pd = 0, leav_ps = 0, ent_ps = 0;
-            for (int64_t pp = lo; pp < pin_off[e + 1]; pp++) {
-                const int32_t j = pos[pin_dat[pp]];
-                if (j < 0 || j >= i) continue;
-                leav_pd += from[j] == pd;
-                ent_pd += to[j] == pd;
-                leav_ps += from[j] == ps;
-                ent_ps += to[j] == ps;
-            }
-            const int64_t we = wi[e];
-            int64_t net = 0;
-            if (base_pd > 0) {
-                if (leav_pd - ent_pd == base_pd) net -= we;
-            } else if (ent_pd > 0) {
-                net += we;
-            }
-            if (base_ps == 1) {
-                if (ent_ps > 0) net -= we;
-            } else if (base_ps - 1 > 0 && leav_ps - ent_ps == base_ps - 1) {
-                net += we;
-            }
-            acc += net;
+            const int64_t net = seq_net(we, base_ps, base_pd, leav_pd, ent_pd, leav_ps, ent_ps);
+            if (net) atomicAdd(&gacc[smv[a]], (unsigned long long)net);
         }
-        acc = warp_sum(acc);
-        if (lane == 0) gseq[i] = giso[i] + acc;
+        __syncthreads();
     }
+}
+__global__ void k_seq_gains_finish(int64_t M, const int64_t *giso, const unsigned long long *gacc, int64_t *gseq) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < M) gseq[i] = giso[i] + (int64_t)gacc[i];
 }
 }  // namespace
 
@@ -1288,7 +1377,8 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, int32_t *assign, i
     uint64_t *mk = c.alloc<uint64_t>(N), *mkt = c.alloc<uint64_t>(N);
     uint32_t *mv = c.alloc<uint32_t>(N), *mvt = c.alloc<uint32_t>(N);
     int32_t *node = c.alloc<int32_t>(N), *from = c.alloc<int32_t>(N), *to = c.alloc<int32_t>(N);
-    int64_t *giso = c.alloc<int64_t>(N), *gseq = c.alloc<int64_t>(shard_capacity(c.comm, N) + 64);
+    int64_t *giso = c.alloc<int64_t>(N), *gseq = c.alloc<int64_t>(N), *gseq_acc = c.alloc<int64_t>(N);
+    int32_t *sg_big = c.alloc<int32_t>(L.E), *sg_ctr = c.alloc<int32_t>(2);
     const int64_t ecap = 2 * (int64_t)N + 2 * L.Sin;
     uint64_t *ek = c.alloc<uint64_t>(ecap), *ekt = c.alloc<uint64_t>(ecap);
     uint32_t *evv = c.alloc<uint32_t>(ecap), *evt = c.alloc<uint32_t>(ecap);
@@ -1419,13 +1509,22 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, int32_t *assign, i
                                                                        giso, pos);
         DHGP_LAUNCHED(c);
         {
+            // replicated on every rank: O(sum |e|), no exchange
             KScope ks(c, "seq_gains", 0.0);
-            const Shard ms = shard_of(c.comm, M);  // this rank's move range
-            int blocks = (int)std::min<int64_t>(cdiv(std::max<int64_t>(1, ms.hi - ms.lo), 8), (int64_t)c.num_sms * 16);
-            k_seq_gains_dn<<<blocks, 256, 0, c.stream>>>(ms.lo, ms.hi, L.inc_off, L.inc_dat, L.pin_off, L.pin_dat,
-                                                          W.wi, r, node, from, to, giso, pos, gseq);
+            unsigned long long *gacc = (unsigned long long *)gseq_acc;
+            c.zero(gacc, M);
+            c.zero(sg_ctr, 2);
+            if (L.E > 0) {
+                k_seq_gains_edge<<<(unsigned)cdiv(L.E, 256), 256, 0, c.stream>>>(L.E, L.pin_off, L.pin_dat, W.wi, r,
+                                                                                 pos, from, to, gacc, sg_big, sg_ctr,
+                                                                                 tiers().edge_movers);
+                DHGP_LAUNCHED(c);
+                k_seq_gains_edge_block<<<c.num_sms, 256, 0, c.stream>>>(L.pin_off, L.pin_dat, W.wi, r, pos, from, to,
+                                                                         gacc, sg_big, sg_ctr, sg_ctr + 1);
+                DHGP_LAUNCHED(c);
+            }
+            k_seq_gains_finish<<<(unsigned)cdiv(M, 256), 256, 0, c.stream>>>(M, giso, gacc, gseq);
             DHGP_LAUNCHED(c);
-            if (ms.on) allgather(c, c.comm, gseq, sizeof(int64_t), ms.chunk);
         }
         // --- A17 events: key = track | part | move index --------------------
         const int ibits = std::max(1, bitlen((uint64_t)M));
@@ -1435,7 +1534,8 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, int32_t *assign, i
         DHGP_LAUNCHED(c);
         if (L.E > 0) {
             k_inbound_events<<<(unsigned)cdiv(L.E, 256), 256, 0, c.stream>>>(L.E, L.dst_off, L.dst_dat, L.pin_off, r,
-                                                                           pos, from, to, ev, big, ctr);
+                                                                           pos, from, to, ev, big, ctr,
+                                                                           tiers().edge_movers);
             DHGP_LAUNCHED(c);
             k_inbound_events_block<<<c.num_sms, 256, 0, c.stream>>>(L.dst_off, L.dst_dat, L.pin_off, r, pos, from, to,
                                                                      ev, big, ctr, ctr + 2);
@@ -1454,10 +1554,12 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, int32_t *assign, i
             // ---- sync 2: the selected prefix (or "too large"), error flags ---
             long long hr[3];
             int32_t hc[4];
+            int32_t hs[2];
             c.d2h(hr, sres, 3);
             c.d2h(hc, ctr, 4);
+            c.d2h(hs, sg_ctr, 2);
             c.sync();
-            if (hc[2]) throw Error{DHGP_ERR_UNSUPPORTED, "too many movers on one h-edge"};
+            if (hc[2] || hs[1]) throw Error{DHGP_ERR_UNSUPPORTED, "too many movers on one h-edge"};
             kbest = hr[0];
             total_gain = hr[1];
             if (hr[2]) {  // a large round: the multi-kernel path
@@ -1544,7 +1646,8 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, int32_t *assign, i
     for (void *p : {(void *)r.part, (void *)r.cnt, (void *)r.cin, (void *)r.len, (void *)tmp_parts, (void *)psizes,
                     (void *)pinbound, (void *)target, (void *)gain, (void *)flags, (void *)mpos, (void *)pos,
                     (void *)ctr, (void *)big, (void *)big2, (void *)conn_d, (void *)mk, (void *)mkt, (void *)mv, (void *)mvt,
-                    (void *)node, (void *)from, (void *)to, (void *)giso, (void *)gseq, (void *)ek, (void *)ekt,
+                    (void *)node, (void *)from, (void *)to, (void *)giso, (void *)gseq, (void *)gseq_acc, (void *)sg_big,
+                    (void *)sg_ctr, (void *)ek, (void *)ekt,
                     (void *)evv, (void *)evt, (void *)ecount, (void *)sres, (void *)pdense, (void *)ptouched})
         c.free(p);
 }

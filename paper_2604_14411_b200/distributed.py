@@ -1,10 +1,12 @@
 """Multi-GPU partitioning by node-range sharding.
 
 One process per GPU.  Each rank holds a replica of the hypergraph and of every
-coarsening level; scoring (coarsen.py:93-132), move proposals
-(refine.py:82-116) and in-sequence gains (refine.py:119-142) are computed for
-the rank's node / move range and completed by an in-place allgather inside
-``libdhgp.so``; the rest of the pipeline runs replicated.  The exchanged
+coarsening level; candidate scoring (coarsen.py:93-132) and move proposals
+(refine.py:82-116) — the per-node phases whose work is the sum of the
+neighbourhood sizes — are computed for the rank's node range and completed
+by an in-place allgather inside ``libdhgp.so``; the rest of the pipeline
+(contraction, matching, the O(sum |e|) sequence gains, the event pipeline)
+runs replicated.  The exchanged
 values are exact (int32 ids, int64 gains, f64 scores) and every tie-break is
 the reference's global total order, so every rank returns the same result as
 the single-GPU :func:`partition` — bit for bit, at any world size.
