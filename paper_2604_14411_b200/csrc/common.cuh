@@ -164,11 +164,13 @@ struct Tiers {
     int pr_heavy_inc = 128;   // propose: incident h-edges above which a block takes the node
     int pm_limit = 3072;      // propose: distinct parts per medium-tier table
     int small_k = 4096;       // propose: K up to which escalated nodes use dense shared arrays
+    int pr_hub_inc = 2048;    // propose: incident h-edges above which a node is split over many CTAs
     int edge_movers = 32;     // events / sequence gains: movers per h-edge for the thread tier (<= 32)
 };
 const Tiers &tiers();
 
 inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+__device__ __forceinline__ int64_t cdiv_dev(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 // grid for a persistent / grid-stride kernel: resident blocks per SM x SMs
 template <class K>

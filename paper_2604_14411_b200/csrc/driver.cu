@@ -42,6 +42,7 @@ const Tiers &tiers() {
             x.sh_limit = 6;
             x.pr_limit = 2;
             x.pr_heavy_inc = 1;
+            x.pr_hub_inc = 6;
             x.pm_limit = 3;
             x.edge_movers = 2;
         }
@@ -214,10 +215,6 @@ static void setup(Ctx &c, int device) {
 void seams_setup(Ctx &c, int device) { setup(c, device); }
 
 namespace {
-__global__ void k_project(int32_t N, const int32_t *gamma, const int32_t *coarse, int32_t *fine) {
-    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (v < N) fine[v] = coarse[gamma[v]];
-}
 __global__ void k_used(int32_t N, const int32_t *assign, uint8_t *used) {
     int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (v < N) used[assign[v]] = 1;
@@ -492,22 +489,27 @@ static void run_partition(Ctx &c, const DInput &in, const dhgp_config &cfg, Part
             obs(&ev, user);
         };
     }
+    // incremental refinement (refine.cuh) unless an h-edge is too wide for
+    // the warp run-list kernel, or DHGP_FULL_REFINE=1 (tests: both modes)
+    RefineState rst;
+    {
+        const char *fe = getenv("DHGP_FULL_REFINE");
+        const bool inc = in.max_edge_pins <= 128 && !(fe && fe[0] == '1');
+        refine_state_init(c, rst, levels[0], K, inc);
+    }
     try {
         const int64_t L = (int64_t)levels.size();
-        refine_level(c, levels[L - 1], W, assign, K, omega, delta, cfg.max_rounds, (int32_t)(L - 1), res.trace[0],
-                     obs ? &robs : nullptr, in.max_edge_pins);
+        refine_level(c, levels[L - 1], W, rst, assign, K, omega, delta, cfg.max_rounds, (int32_t)(L - 1),
+                     res.trace[0], obs ? &robs : nullptr, in.max_edge_pins);
         for (int64_t li = L - 2; li >= 0; li--) {
             if (levels[li].stub) rebuild_levels(c, levels, (size_t)li);
             DLevel &f = levels[li];
-            if (f.N > 0) {
-                k_project<<<(unsigned)cdiv(f.N, 256), 256, 0, c.stream>>>(f.N, f.gamma, assign, assign2);
-                DHGP_LAUNCHED(c);
-            }
-            std::swap(assign, assign2);
+            refine_project(c, rst, f, levels[li + 1].N, assign, assign2);
             levels[li + 1].release(c);
-            refine_level(c, f, W, assign, K, omega, delta, cfg.max_rounds, (int32_t)li, res.trace[L - 1 - li],
+            refine_level(c, f, W, rst, assign, K, omega, delta, cfg.max_rounds, (int32_t)li, res.trace[L - 1 - li],
                          obs ? &robs : nullptr, in.max_edge_pins);
         }
+        refine_state_release(c, rst);
         const double t2 = now_ms();
         // ---- compaction (driver.py:137-143) + check_validity (144-146) ------
         int32_t final_parts = 0;
@@ -554,6 +556,7 @@ static void run_partition(Ctx &c, const DInput &in, const dhgp_config &cfg, Part
         res.phase_ms[1] = t2 - t1;
         res.phase_ms[2] = t3 - t0;
     } catch (...) {
+        refine_state_release(c, rst);
         for (auto &L : levels) L.release(c);
         W.release(c);
         c.free(assign);

@@ -15,6 +15,7 @@ namespace dhgp {
 namespace {
 
 struct Runs {
+    const int64_t *off = nullptr;  // [E+1] run base per h-edge (>= |pins(e)| slots each)
     int32_t *part = nullptr;  // [U] distinct parts per h-edge (ascending)
     int32_t *cnt = nullptr;   // [U] pins of the h-edge in that part
     int32_t *cin = nullptr;   // [U] destination pins of the h-edge in that part
@@ -36,9 +37,9 @@ __global__ void k_edge_runs(int32_t E, const int64_t *pin_off, const int32_t *so
     int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int64_t contrib = 0;
     if (e < E) {
-        const int64_t lo = pin_off[e], hi = pin_off[e + 1];
+        const int64_t plo = pin_off[e], hi = pin_off[e + 1], lo = r.off[e];
         int32_t lam = 0;
-        for (int64_t j = lo; j < hi;) {
+        for (int64_t j = plo; j < hi;) {
             int32_t p = sorted_parts[j];
             int64_t j2 = j + 1;
             while (j2 < hi && sorted_parts[j2] == p) j2++;
@@ -71,15 +72,15 @@ __global__ void k_edge_runs_warp(int32_t E, const int64_t *pin_off, const int32_
     const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
     int64_t contrib = 0;
     for (int64_t e = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id(); e < E; e += nw) {
-        const int64_t lo = pin_off[e], len = pin_off[e + 1] - lo;
+        const int64_t plo = pin_off[e], len = pin_off[e + 1] - plo, lo = r.off[e];
         int32_t lam = 0;
         for (int64_t b = 0; b < len; b += 32) {  // heads of the sorted runs
             const int64_t i = b + lane;
             int32_t p = 0;
             bool head = false;
             if (i < len) {
-                p = sorted_parts[lo + i];
-                head = i == 0 || sorted_parts[lo + i - 1] != p;
+                p = sorted_parts[plo + i];
+                head = i == 0 || sorted_parts[plo + i - 1] != p;
             }
             const uint32_t bal = __ballot_sync(FULL_MASK, head);
             if (head) {
@@ -103,8 +104,8 @@ __global__ void k_edge_runs_warp(int32_t E, const int64_t *pin_off, const int32_
         if (lam > 32) {
             for (int32_t j = lane; j < lam; j += 32) {
                 const int32_t p = r.part[lo + j];
-                int64_t a0 = lower_bound_dev<int32_t>(sorted_parts, lo, lo + len, p);
-                int64_t a1 = lower_bound_dev<int32_t>(sorted_parts, lo, lo + len, p + 1);
+                int64_t a0 = lower_bound_dev<int32_t>(sorted_parts, plo, plo + len, p);
+                int64_t a1 = lower_bound_dev<int32_t>(sorted_parts, plo, plo + len, p + 1);
                 r.cnt[lo + j] = (int32_t)(a1 - a0);
             }
             __syncwarp();
@@ -127,7 +128,7 @@ __global__ void k_edge_runs_warp(int32_t E, const int64_t *pin_off, const int32_
 // sorts them in registers (bitonic) and derives the runs from ballots; no
 // temporary array and one launch per round.
 template <int K>
-__device__ __forceinline__ int32_t warp_edge_runs(int64_t e, int64_t lo, int len, const int32_t *pin_dat,
+__device__ __forceinline__ int32_t warp_edge_runs(int64_t e, int64_t plo, int64_t lo, int len, const int32_t *pin_dat,
                                                   const int64_t *dst_off, const int32_t *dst_dat,
                                                   const int32_t *assign, Runs r, int64_t *pinbound) {
     const int lane = lane_id();
@@ -136,7 +137,7 @@ __device__ __forceinline__ int32_t warp_edge_runs(int64_t e, int64_t lo, int len
 #pragma unroll
     for (int k = 0; k < K; k++) {
         const int i = k * 32 + lane;
-        v[k] = i < len ? (uint32_t)assign[pin_dat[lo + i]] : 0xffffffffu;
+        v[k] = i < len ? (uint32_t)assign[pin_dat[plo + i]] : 0xffffffffu;
     }
     warp_bitonic_sort<K>(v);
     uint32_t bal[K];
@@ -190,15 +191,15 @@ __global__ void k_edge_runs_fused(int32_t E, const int64_t *pin_off, const int32
     const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
     int64_t contrib = 0;
     for (int64_t e = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id(); e < E; e += nw) {
-        const int64_t lo = pin_off[e];
-        const int len = (int)(pin_off[e + 1] - lo);
+        const int64_t plo = pin_off[e], lo = r.off[e];
+        const int len = (int)(pin_off[e + 1] - plo);
         int32_t lam;
         if (len <= 32)
-            lam = warp_edge_runs<1>(e, lo, len, pin_dat, dst_off, dst_dat, assign, r, pinbound);
+            lam = warp_edge_runs<1>(e, plo, lo, len, pin_dat, dst_off, dst_dat, assign, r, pinbound);
         else if (len <= 64)
-            lam = warp_edge_runs<2>(e, lo, len, pin_dat, dst_off, dst_dat, assign, r, pinbound);
+            lam = warp_edge_runs<2>(e, plo, lo, len, pin_dat, dst_off, dst_dat, assign, r, pinbound);
         else
-            lam = warp_edge_runs<4>(e, lo, len, pin_dat, dst_off, dst_dat, assign, r, pinbound);
+            lam = warp_edge_runs<4>(e, plo, lo, len, pin_dat, dst_off, dst_dat, assign, r, pinbound);
         if (lane_id() == 0) {
             r.len[e] = lam;
             if (lam > 0) contrib += wi[e] * (int64_t)(lam - 1);
@@ -218,11 +219,15 @@ __global__ void k_part_sizes(int32_t N, const int32_t *assign, const int32_t *si
 // shared-memory hash table; nodes touching too many parts go to a block tier
 // with a dense per-block array over all parts.
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ bool better_gain(int64_t g, int32_t p, int64_t bg, int32_t bp) {
+    // max gain, ties to the smaller part id (_kernels.pyx:305)
+    return bp < 0 || g > bg || (g == bg && p < bp);
+}
+
 struct ProposeArgs {
     int32_t N, K;
     const int64_t *inc_off;
     const int32_t *inc_dat;
-    const int64_t *pin_off;
     const int64_t *wi;
     Runs r;
     const int32_t *assign;
@@ -238,7 +243,70 @@ struct ProposeArgs {
     int32_t *dense_count;
     Tiers t;
     int32_t lo, hi;  // this rank's node range (comm.cuh); [0, N) on one GPU
+    // incremental mode: only the listed (dirty) nodes, their flags cleared
+    const int32_t *list = nullptr;
+    const int32_t *list_count = nullptr;
+    int32_t *ndirty = nullptr;
+    // per node: the positive-gain parts the size bound filtered out (the
+    // proposal may change when one of them shrinks): fsens = their count
+    // (3 = more than two), fpart[2n .. 2n+1] = the first two
+    uint8_t *fsens = nullptr;
+    int32_t *fpart = nullptr;
+    // hub tier: nodes with very many incident h-edges, split over CTAs
+    int32_t *hub_list = nullptr;
+    int32_t *hub_count = nullptr;
 };
+constexpr int HUB_MAX = 256;     // hubs per propose pass (more go to the block tiers)
+constexpr int HUB_CHUNK = 256;   // incident h-edges per CTA work item
+
+// the next node of a persistent warp/CTA loop: all of [lo, hi), or the
+// listed nodes inside [lo, hi); -1 = done, -2 = skip (another rank's node)
+__device__ __forceinline__ int32_t propose_node(const ProposeArgs &a, int idx) {
+    if (a.list) {
+        if (idx >= *a.list_count) return -1;
+        const int32_t n = a.list[idx];
+        return (n < a.lo || n >= a.hi) ? -2 : n;
+    }
+    const int64_t n = (int64_t)a.lo + idx;
+    return n >= a.hi ? -1 : (int32_t)n;
+}
+
+__device__ __forceinline__ void warp_best_gain(long long &bg, int32_t &bp) {
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        const long long og = __shfl_xor_sync(FULL_MASK, bg, d);
+        const int32_t op = __shfl_xor_sync(FULL_MASK, bp, d);
+        if (op >= 0 && better_gain(og, op, bg, bp)) {
+            bg = og;
+            bp = op;
+        }
+    }
+}
+// one candidate part p with gain g: eligible ones compete for the target,
+// size-filtered positive ones are recorded (shared counter nf, first two in f)
+__device__ __forceinline__ void consider_part(int32_t p, long long g, bool fits, long long &bg, int32_t &bp, int *nf,
+                                              int32_t *f) {
+    if (fits) {
+        if (better_gain(g, p, bg, bp)) {
+            bg = g;
+            bp = p;
+        }
+    } else if (g > 0) {
+        const int i = atomicAdd(nf, 1);
+        if (i < 2) f[i] = p;
+    }
+}
+__device__ __forceinline__ void write_proposal(const ProposeArgs &a, int32_t node, long long g, int32_t p, int nf,
+                                               const int32_t *f) {
+    const bool emit = p >= 0 && g > 0;
+    a.target[node] = emit ? p : -1;
+    a.gain[node] = emit ? g : 0;
+    if (a.fsens) {
+        a.fsens[node] = (uint8_t)min(nf, 3);
+        a.fpart[2 * (int64_t)node] = nf > 0 ? f[0] : -1;
+        a.fpart[2 * (int64_t)node + 1] = nf > 1 ? f[1] : -1;
+    }
+}
 
 // Flattened iteration over the (h-edge, run) pairs of a node's incident
 // h-edges: the warp takes 32 incident h-edges at a time (ilo + first, then
@@ -292,10 +360,6 @@ constexpr int pr_smem() { return PR_WARPS * PR_CAP * (4 + (int)sizeof(Acc)); }
 
 __device__ __forceinline__ uint32_t pslot(int32_t p) { return ((uint32_t)p * 2654435761u) >> (32 - 9); }
 
-__device__ __forceinline__ bool better_gain(int64_t g, int32_t p, int64_t bg, int32_t bp) {
-    // max gain, ties to the smaller part id (_kernels.pyx:305)
-    return bp < 0 || g > bg || (g == bg && p < bp);
-}
 
 template <class Acc>
 __global__ void __launch_bounds__(PR_WARPS * 32) k_propose_warp(ProposeArgs a) {
@@ -304,17 +368,32 @@ __global__ void __launch_bounds__(PR_WARPS * 32) k_propose_warp(ProposeArgs a) {
     int32_t *skeys = (int32_t *)(svals + PR_WARPS * PR_CAP);
     __shared__ int32_t snk[PR_WARPS];
     __shared__ volatile int32_t sover[PR_WARPS];
+    __shared__ int s_nf[PR_WARPS];
+    __shared__ int32_t s_f[PR_WARPS][2];
     const int w = warp_id(), lane = lane_id();
     int32_t *keys = skeys + w * PR_CAP;
     Acc *vals = svals + w * PR_CAP;
     while (true) {
-        int node = 0;
-        if (lane == 0) node = a.lo + atomicAdd(a.next, 1);
-        node = __shfl_sync(FULL_MASK, node, 0);
-        if (node >= a.hi) break;
+        int idx = 0;
+        if (lane == 0) idx = atomicAdd(a.next, 1);
+        idx = __shfl_sync(FULL_MASK, idx, 0);
+        const int32_t node = propose_node(a, idx);
+        if (node == -1) break;
+        if (a.ndirty && lane == 0 && a.list) a.ndirty[a.list[idx]] = 0;
+        if (node < 0) continue;
         const int64_t ilo = a.inc_off[node], ihi = a.inc_off[node + 1];
         if (ihi == ilo || a.K < 2) {
-            if (lane == 0) a.target[node] = -1;
+            if (lane == 0) write_proposal(a, node, 0, -1, 0, nullptr);
+            continue;
+        }
+        if (a.hub_list && ihi - ilo > a.t.pr_hub_inc) {  // hub: many CTAs take it
+            if (lane == 0) {
+                const int slot = atomicAdd(a.hub_count, 1);
+                if (slot < HUB_MAX)
+                    a.hub_list[slot] = node;
+                else
+                    a.big_list[atomicAdd(a.big_count, 1)] = node;
+            }
             continue;
         }
         if (ihi - ilo > a.t.pr_heavy_inc) {  // many incident h-edges: a whole block takes it
@@ -332,7 +411,7 @@ __global__ void __launch_bounds__(PR_WARPS * 32) k_propose_warp(ProposeArgs a) {
         __syncwarp();
         const int32_t ps = a.assign[node];
         int64_t total = 0, saving = 0;
-        total = warp_for_runs(a.inc_dat, ilo, ihi, 0, 32, a.pin_off, a.r.len, a.wi, [&](int32_t, int64_t we, int64_t k) {
+        total = warp_for_runs(a.inc_dat, ilo, ihi, 0, 32, a.r.off, a.r.len, a.wi, [&](int32_t, int64_t we, int64_t k) {
             const int32_t p = a.r.part[k];
             if (p == ps && a.r.cnt[k] == 1) saving += we;
             if (sover[w]) return;
@@ -365,31 +444,19 @@ __global__ void __launch_bounds__(PR_WARPS * 32) k_propose_warp(ProposeArgs a) {
             continue;
         }
         const int64_t sz = a.size[node];
-        int64_t bg = 0;
+        long long bg = 0;
         int32_t bp = -1;
+        if (lane == 0) s_nf[w] = 0;
+        __syncwarp();
         for (int s = lane; s < PR_CAP; s += 32) {
             const int32_t p = keys[s];
-            if (p < 0 || p == ps || a.psizes[p] + sz > a.omega) continue;
-            const int64_t g = saving - (total - (int64_t)vals[s]);
-            if (better_gain(g, p, bg, bp)) {
-                bg = g;
-                bp = p;
-            }
+            if (p < 0 || p == ps) continue;
+            consider_part(p, saving - (total - (long long)vals[s]), a.psizes[p] + sz <= a.omega, bg, bp, &s_nf[w],
+                          s_f[w]);
         }
-#pragma unroll
-        for (int d = 16; d > 0; d >>= 1) {
-            int64_t og = __shfl_xor_sync(FULL_MASK, bg, d);
-            int32_t op = __shfl_xor_sync(FULL_MASK, bp, d);
-            if (op >= 0 && better_gain(og, op, bg, bp)) {
-                bg = og;
-                bp = op;
-            }
-        }
-        if (lane == 0) {
-            const bool emit = bp >= 0 && bg > 0;
-            a.target[node] = emit ? bp : -1;
-            a.gain[node] = emit ? bg : 0;
-        }
+        warp_best_gain(bg, bp);
+        __syncwarp();
+        if (lane == 0) write_proposal(a, node, bg, bp, s_nf[w], s_f[w]);
         __syncwarp();
     }
 }
@@ -440,6 +507,8 @@ __global__ void __launch_bounds__(PM_THREADS) k_propose_mid(ProposeArgs a) {
     __shared__ volatile int32_t sover;
     __shared__ long long r_a[PM_THREADS / 32], r_b[PM_THREADS / 32];
     __shared__ int32_t r_p[PM_THREADS / 32];
+    __shared__ int s_nf;
+    __shared__ int32_t s_f[2];
     const int w = warp_id(), lane = lane_id(), nw = PM_THREADS / 32;
     const int nmid = *a.big_count;
     for (int t = blockIdx.x; t < nmid; t += gridDim.x) {
@@ -456,7 +525,7 @@ __global__ void __launch_bounds__(PM_THREADS) k_propose_mid(ProposeArgs a) {
         const int64_t ilo = a.inc_off[node], ihi = a.inc_off[node + 1];
         const int32_t ps = a.assign[node];
         long long total = 0, saving = 0;
-        total = warp_for_runs(a.inc_dat, ilo, ihi, (int64_t)w * 32, (int64_t)nw * 32, a.pin_off, a.r.len, a.wi,
+        total = warp_for_runs(a.inc_dat, ilo, ihi, (int64_t)w * 32, (int64_t)nw * 32, a.r.off, a.r.len, a.wi,
                               [&](int32_t, int64_t we, int64_t k) {
                                   const int32_t p = a.r.part[k];
                                   if (p == ps && a.r.cnt[k] == 1) saving += we;
@@ -503,23 +572,17 @@ __global__ void __launch_bounds__(PM_THREADS) k_propose_mid(ProposeArgs a) {
         const int64_t sz = a.size[node];
         long long bg = 0;
         int32_t bp = -1;
+        if (threadIdx.x == 0) s_nf = 0;
+        __syncthreads();
         for (int s = threadIdx.x; s < PM_CAP; s += PM_THREADS) {
             const int32_t p = keys[s];
-            if (p < 0 || p == ps || a.psizes[p] + sz > a.omega) continue;
-            const long long g = saving - (total - (long long)vals[s]);
-            if (better_gain(g, p, bg, bp)) {
-                bg = g;
-                bp = p;
-            }
+            if (p < 0 || p == ps) continue;
+            consider_part(p, saving - (total - (long long)vals[s]), a.psizes[p] + sz <= a.omega, bg, bp, &s_nf, s_f);
         }
         long long g;
         int32_t p;
         block_best_gain(bg, bp, r_a, r_p, nw, &g, &p);
-        if (threadIdx.x == 0) {
-            const bool emit = p >= 0 && g > 0;
-            a.target[node] = emit ? p : -1;
-            a.gain[node] = emit ? g : 0;
-        }
+        if (threadIdx.x == 0) write_proposal(a, node, g, p, s_nf, s_f);
         __syncthreads();
     }
 }
@@ -543,6 +606,8 @@ __global__ void __launch_bounds__(THREADS) k_propose_heavy(ProposeArgs a) {
     __shared__ int32_t s_nt;
     __shared__ long long r_a[THREADS / 32], r_b[THREADS / 32];
     __shared__ int32_t r_p[THREADS / 32];
+    __shared__ int s_nf;
+    __shared__ int32_t s_f[2];
     const int w = warp_id(), lane = lane_id(), nw = THREADS / 32;
     const int nbig = *a.dense_count;
     if ((int)blockIdx.x >= nbig) return;
@@ -556,7 +621,7 @@ __global__ void __launch_bounds__(THREADS) k_propose_heavy(ProposeArgs a) {
         const int64_t ilo = a.inc_off[node], ihi = a.inc_off[node + 1];
         const int32_t ps = a.assign[node];
         long long total = 0, saving = 0;
-        total = warp_for_runs(a.inc_dat, ilo, ihi, (int64_t)w * 32, (int64_t)nw * 32, a.pin_off, a.r.len, a.wi,
+        total = warp_for_runs(a.inc_dat, ilo, ihi, (int64_t)w * 32, (int64_t)nw * 32, a.r.off, a.r.len, a.wi,
                               [&](int32_t, int64_t we, int64_t k) {
                                   const int32_t p = a.r.part[k];
                                   if (p == ps && a.r.cnt[k] == 1) saving += we;
@@ -582,25 +647,115 @@ __global__ void __launch_bounds__(THREADS) k_propose_heavy(ProposeArgs a) {
         const int64_t sz = a.size[node];
         long long bg = 0;
         int32_t bp = -1;
+        if (threadIdx.x == 0) s_nf = 0;
+        __syncthreads();
         for (int i = threadIdx.x; i < nt; i += THREADS) {
             const int32_t p = tlist[i];
             const long long pv = (long long)pres[p];
             pres[p] = 0;
             touched[p >> 5] = 0;
-            if (p == ps || a.psizes[p] + sz > a.omega) continue;
-            const long long g = saving - (total - pv);
-            if (better_gain(g, p, bg, bp)) {
-                bg = g;
-                bp = p;
-            }
+            if (p == ps) continue;
+            consider_part(p, saving - (total - pv), a.psizes[p] + sz <= a.omega, bg, bp, &s_nf, s_f);
         }
         long long g;
         int32_t p;
         block_best_gain(bg, bp, r_a, r_p, nw, &g, &p);
+        if (threadIdx.x == 0) write_proposal(a, node, g, p, s_nf, s_f);
+        __syncthreads();
+    }
+}
+
+
+// Hub tier (K <= small_k): a node with thousands of incident h-edges is cut
+// into HUB_CHUNK-edge work items spread over the grid; each CTA accumulates
+// present[] for its chunk in shared memory and adds it to the hub's global
+// row; the CTA finishing a hub's last chunk selects the target.
+template <class Acc>
+__global__ void __launch_bounds__(256) k_propose_hub(ProposeArgs a, long long *hacc, long long *htot,
+                                                     int32_t *hdone) {
+    extern __shared__ unsigned long long smem_u64[];
+    Acc *pres = (Acc *)smem_u64;
+    __shared__ long long r_a[8], r_b[8];
+    __shared__ int32_t r_p[8];
+    __shared__ int s_last, s_nf;
+    __shared__ int32_t s_f[2];
+    const int nh = min(*a.hub_count, HUB_MAX);
+    const int w = warp_id(), lane = lane_id(), nw = 8;
+    const int K = a.K;
+    for (int64_t t = blockIdx.x;; t += gridDim.x) {
+        int h = -1;
+        int64_t chunk = 0, base = 0, nch = 0;
+        for (int j = 0; j < nh; j++) {
+            const int32_t n = a.hub_list[j];
+            nch = cdiv_dev(a.inc_off[n + 1] - a.inc_off[n], (int64_t)HUB_CHUNK);
+            if (t < base + nch) {
+                h = j;
+                chunk = t - base;
+                break;
+            }
+            base += nch;
+        }
+        if (h < 0) break;
+        const int32_t node = a.hub_list[h];
+        const int64_t ilo = a.inc_off[node] + chunk * HUB_CHUNK;
+        const int64_t ihi = min(a.inc_off[node + 1], ilo + (int64_t)HUB_CHUNK);
+        for (int p = threadIdx.x; p < K; p += blockDim.x) pres[p] = 0;
+        __syncthreads();
+        const int32_t ps = a.assign[node];
+        long long total = 0, saving = 0;
+        total = warp_for_runs(a.inc_dat, ilo, ihi, (int64_t)w * 32, (int64_t)nw * 32, a.r.off, a.r.len, a.wi,
+                              [&](int32_t, int64_t we, int64_t k) {
+                                  const int32_t p = a.r.part[k];
+                                  if (p == ps && a.r.cnt[k] == 1) saving += we;
+                                  atomicAdd(&pres[p], (Acc)we);
+                              });
+        total = warp_sum(total);
+        saving = warp_sum(saving);
+        if (lane == 0) {
+            r_a[w] = total;
+            r_b[w] = saving;
+        }
+        __syncthreads();
+        long long *row = hacc + (int64_t)h * K;
+        for (int p = threadIdx.x; p < K; p += blockDim.x)
+            if (pres[p]) atomicAdd((unsigned long long *)&row[p], (unsigned long long)pres[p]);
         if (threadIdx.x == 0) {
-            const bool emit = p >= 0 && g > 0;
-            a.target[node] = emit ? p : -1;
-            a.gain[node] = emit ? g : 0;
+            long long t0 = 0, s0 = 0;
+            for (int j = 0; j < nw; j++) {
+                t0 += r_a[j];
+                s0 += r_b[j];
+            }
+            atomicAdd((unsigned long long *)&htot[2 * h], (unsigned long long)t0);
+            atomicAdd((unsigned long long *)&htot[2 * h + 1], (unsigned long long)s0);
+        }
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) s_last = atomicAdd(&hdone[h], 1) == (int)(nch - 1);
+        __syncthreads();
+        if (s_last) {
+            __threadfence();
+            const long long tot = __ldcg(&htot[2 * h]), sav = __ldcg(&htot[2 * h + 1]);
+            const int64_t sz = a.size[node];
+            long long bg = 0;
+            int32_t bp = -1;
+            if (threadIdx.x == 0) s_nf = 0;
+            __syncthreads();
+            for (int p = threadIdx.x; p < K; p += blockDim.x) {
+                const long long v = __ldcg(&row[p]);
+                if (v == 0) continue;  // absent, or only zero-weight h-edges (gain <= 0)
+                row[p] = 0;
+                if (p == ps) continue;
+                consider_part(p, sav - (tot - v), a.psizes[p] + sz <= a.omega, bg, bp, &s_nf, s_f);
+            }
+            long long g;
+            int32_t pp;
+            block_best_gain(bg, bp, r_a, r_p, nw, &g, &pp);
+            if (threadIdx.x == 0) {
+                write_proposal(a, node, g, pp, s_nf, s_f);
+                htot[2 * h] = 0;
+                htot[2 * h + 1] = 0;
+                hdone[h] = 0;
+            }
         }
         __syncthreads();
     }
@@ -612,6 +767,8 @@ __global__ void __launch_bounds__(PB_THREADS) k_propose_block(ProposeArgs a, lon
     __shared__ int32_t s_nt;
     __shared__ long long s_red[PB_THREADS / 32][2];
     __shared__ int32_t s_p[PB_THREADS / 32];
+    __shared__ int s_nf;
+    __shared__ int32_t s_f[2];
     long long *dense = dense_all + (int64_t)blockIdx.x * a.K;
     int32_t *touched = touched_all + (int64_t)blockIdx.x * a.K;
     const int w = warp_id(), lane = lane_id(), nw = PB_THREADS / 32;
@@ -623,7 +780,7 @@ __global__ void __launch_bounds__(PB_THREADS) k_propose_block(ProposeArgs a, lon
         const int64_t ilo = a.inc_off[node], ihi = a.inc_off[node + 1];
         const int32_t ps = a.assign[node];
         long long total = 0, saving = 0;
-        total = warp_for_runs(a.inc_dat, ilo, ihi, (int64_t)w * 32, (int64_t)nw * 32, a.pin_off, a.r.len, a.wi,
+        total = warp_for_runs(a.inc_dat, ilo, ihi, (int64_t)w * 32, (int64_t)nw * 32, a.r.off, a.r.len, a.wi,
                               [&](int32_t, int64_t we, int64_t k) {
                                   const int32_t p = a.r.part[k];
                                   if (p == ps && a.r.cnt[k] == 1) saving += we;
@@ -648,26 +805,16 @@ __global__ void __launch_bounds__(PB_THREADS) k_propose_block(ProposeArgs a, lon
         const int64_t sz = a.size[node];
         long long bg = 0;
         int32_t bp = -1;
+        if (threadIdx.x == 0) s_nf = 0;
+        __syncthreads();
         for (int i = threadIdx.x; i < nt; i += PB_THREADS) {
             const int32_t p = touched[i];
             const long long pres = dense[p];
             dense[p] = -1ll;
-            if (p == ps || a.psizes[p] + sz > a.omega) continue;
-            const long long g = saving - (total - pres);
-            if (better_gain(g, p, bg, bp)) {
-                bg = g;
-                bp = p;
-            }
+            if (p == ps) continue;
+            consider_part(p, saving - (total - pres), a.psizes[p] + sz <= a.omega, bg, bp, &s_nf, s_f);
         }
-#pragma unroll
-        for (int d = 16; d > 0; d >>= 1) {
-            long long og = __shfl_xor_sync(FULL_MASK, bg, d);
-            int32_t op = __shfl_xor_sync(FULL_MASK, bp, d);
-            if (op >= 0 && better_gain(og, op, bg, bp)) {
-                bg = og;
-                bp = op;
-            }
-        }
+        warp_best_gain(bg, bp);
         __syncthreads();
         if (lane == 0) {
             s_red[w][0] = bg;
@@ -682,9 +829,7 @@ __global__ void __launch_bounds__(PB_THREADS) k_propose_block(ProposeArgs a, lon
                     g = s_red[j][0];
                     p = s_p[j];
                 }
-            const bool emit = p >= 0 && g > 0;
-            a.target[node] = emit ? p : -1;
-            a.gain[node] = emit ? g : 0;
+            write_proposal(a, node, g, p, s_nf, s_f);
         }
         __syncthreads();
     }
@@ -730,11 +875,22 @@ __device__ __forceinline__ void emit(const EvArgs &ev, uint64_t track, int32_t p
 // destination pins in sequence order; per part a running destination-pin
 // count from pins_in[e, p]; crossings 0->1 / 1->0 emit distinct events.
 constexpr int kEvLocal = 32;
-__global__ void k_inbound_events(int32_t E, const int64_t *dst_off, const int32_t *dst_dat, const int64_t *pin_off,
-                                 Runs r, const int32_t *pos, const int32_t *from, const int32_t *to, EvArgs ev,
-                                 int32_t *big_list, int32_t *big_count, int cap) {
-    int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= E) return;
+__device__ __noinline__ void inbound_events_edge(int32_t e, const int64_t *dst_off, const int32_t *dst_dat, Runs r,
+                                                 const int32_t *pos, const int32_t *from, const int32_t *to,
+                                                 EvArgs ev, int32_t *big_list, int32_t *big_count, int cap);
+// edges: all E, or the list elist[0 .. *ecount) when elist is set
+__global__ void k_inbound_events(int32_t E, const int32_t *elist, const int32_t *ecount, const int64_t *dst_off,
+                                 const int32_t *dst_dat, Runs r, const int32_t *pos, const int32_t *from,
+                                 const int32_t *to, EvArgs ev, int32_t *big_list, int32_t *big_count, int cap) {
+    const int64_t ne = elist ? (int64_t)*ecount : (int64_t)E;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < ne;
+         idx += (int64_t)gridDim.x * blockDim.x)
+        inbound_events_edge(elist ? elist[idx] : (int32_t)idx, dst_off, dst_dat, r, pos, from, to, ev, big_list,
+                            big_count, cap);
+}
+__device__ __noinline__ void inbound_events_edge(int32_t e, const int64_t *dst_off, const int32_t *dst_dat, Runs r,
+                                                 const int32_t *pos, const int32_t *from, const int32_t *to,
+                                                 EvArgs ev, int32_t *big_list, int32_t *big_count, int cap) {
     int32_t mv[kEvLocal];
     int nm = 0;
     for (int64_t q = dst_off[e]; q < dst_off[e + 1]; q++) {
@@ -758,7 +914,7 @@ __global__ void k_inbound_events(int32_t E, const int64_t *dst_off, const int32_
     }
     int32_t dp[2 * kEvLocal], dc[2 * kEvLocal];
     int nd = 0;
-    const int64_t lo = pin_off[e];
+    const int64_t lo = r.off[e];
     const int32_t lam = r.len[e];
     for (int a = 0; a < nm; a++) {
         const int32_t i = mv[a];
@@ -788,7 +944,7 @@ __global__ void k_inbound_events(int32_t E, const int64_t *dst_off, const int32_
 // the same walk for h-edges with many movers: block collects and sorts, one
 // thread walks with a shared-memory part dictionary
 constexpr int kEvBlockMax = 2048;
-__global__ void k_inbound_events_block(const int64_t *dst_off, const int32_t *dst_dat, const int64_t *pin_off, Runs r,
+__global__ void k_inbound_events_block(const int64_t *dst_off, const int32_t *dst_dat, Runs r,
                                        const int32_t *pos, const int32_t *from, const int32_t *to, EvArgs ev,
                                        const int32_t *big_list, const int32_t *big_count, int32_t *err) {
     __shared__ uint32_t smv[kEvBlockMax];
@@ -818,7 +974,7 @@ __global__ void k_inbound_events_block(const int64_t *dst_off, const int32_t *ds
         for (int s = nm + threadIdx.x; s < np; s += blockDim.x) smv[s] = 0xffffffffu;
         block_bitonic_sort32(smv, np);
         if (threadIdx.x == 0) {
-            const int64_t lo = pin_off[e];
+            const int64_t lo = r.off[e];
             const int32_t lam = r.len[e];
             int nd = 0;
             for (int a = 0; a < nm; a++) {
@@ -1219,11 +1375,25 @@ __device__ __forceinline__ int64_t seq_net(int64_t we, int32_t base_ps, int32_t 
     return net;
 }
 constexpr int kSgLocal = 32;
-__global__ void k_seq_gains_edge(int32_t E, const int64_t *pin_off, const int32_t *pin_dat, const int64_t *wi,
-                                 Runs r, const int32_t *pos, const int32_t *from, const int32_t *to,
-                                 unsigned long long *gacc, int32_t *big_list, int32_t *big_count, int cap) {
-    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= E) return;
+__device__ __noinline__ void seq_gains_edge(int32_t e, const int64_t *pin_off, const int32_t *pin_dat,
+                                            const int64_t *wi, Runs r, const int32_t *pos, const int32_t *from,
+                                            const int32_t *to, unsigned long long *gacc, int32_t *big_list,
+                                            int32_t *big_count, int cap);
+// edges: all E, or the list elist[0 .. *ecount) when elist is set
+__global__ void k_seq_gains_edge(int32_t E, const int32_t *elist, const int32_t *ecount, const int64_t *pin_off,
+                                 const int32_t *pin_dat, const int64_t *wi, Runs r, const int32_t *pos,
+                                 const int32_t *from, const int32_t *to, unsigned long long *gacc,
+                                 int32_t *big_list, int32_t *big_count, int cap) {
+    const int64_t ne = elist ? (int64_t)*ecount : (int64_t)E;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < ne;
+         idx += (int64_t)gridDim.x * blockDim.x)
+        seq_gains_edge(elist ? elist[idx] : (int32_t)idx, pin_off, pin_dat, wi, r, pos, from, to, gacc, big_list,
+                       big_count, cap);
+}
+__device__ __noinline__ void seq_gains_edge(int32_t e, const int64_t *pin_off, const int32_t *pin_dat,
+                                            const int64_t *wi, Runs r, const int32_t *pos, const int32_t *from,
+                                            const int32_t *to, unsigned long long *gacc, int32_t *big_list,
+                                            int32_t *big_count, int cap) {
     int32_t mv[kSgLocal];
     int nm = 0;
     const int64_t lo = pin_off[e], hi = pin_off[e + 1];
@@ -1253,6 +1423,7 @@ __global__ void k_seq_gains_edge(int32_t E, const int64_t *pin_off, const int32_
     }
     const int64_t we = wi[e];
     const int32_t lam = r.len[e];
+    const int64_t ro = r.off[e];
     for (int a = 0; a < nm; a++) {
         const int32_t ps = mf[a], pd = mt[a];
         int32_t leav_pd = 0, ent_pd = 0, leav_ps = 0, ent_ps = 0;
@@ -1262,10 +1433,10 @@ __global__ void k_seq_gains_edge(int32_t E, const int64_t *pin_off, const int32_
             leav_ps += mf[b] == ps;
             ent_ps += mt[b] == ps;
         }
-        int32_t k = run_find(r, lo, lam, ps);
-        const int32_t base_ps = k >= 0 ? r.cnt[lo + k] : 0;
-        k = run_find(r, lo, lam, pd);
-        const int32_t base_pd = k >= 0 ? r.cnt[lo + k] : 0;
+        int32_t k = run_find(r, ro, lam, ps);
+        const int32_t base_ps = k >= 0 ? r.cnt[ro + k] : 0;
+        k = run_find(r, ro, lam, pd);
+        const int32_t base_pd = k >= 0 ? r.cnt[ro + k] : 0;
         const int64_t net = seq_net(we, base_ps, base_pd, leav_pd, ent_pd, leav_ps, ent_ps);
         if (net) atomicAdd(&gacc[mv[a]], (unsigned long long)net);
     }
@@ -1310,6 +1481,7 @@ __global__ void k_seq_gains_edge_block(const int64_t *pin_off, const int32_t *pi
         __syncthreads();
         const int64_t we = wi[e];
         const int32_t lam = r.len[e];
+        const int64_t ro = r.off[e];
         for (int a = threadIdx.x; a < nm; a += blockDim.x) {
             const int32_t ps = sf[a], pd = st[a];
             int32_t leav_pd = 0, ent_pd = 0, leav_ps = 0, ent_ps = 0;
@@ -1319,10 +1491,10 @@ __global__ void k_seq_gains_edge_block(const int64_t *pin_off, const int32_t *pi
                 leav_ps += sf[b] == ps;
                 ent_ps += st[b] == ps;
             }
-            int32_t k = run_find(r, lo, lam, ps);
-            const int32_t base_ps = k >= 0 ? r.cnt[lo + k] : 0;
-            k = run_find(r, lo, lam, pd);
-            const int32_t base_pd = k >= 0 ? r.cnt[lo + k] : 0;
+            int32_t k = run_find(r, ro, lam, ps);
+            const int32_t base_ps = k >= 0 ? r.cnt[ro + k] : 0;
+            k = run_find(r, ro, lam, pd);
+            const int32_t base_pd = k >= 0 ? r.cnt[ro + k] : 0;
             const int64_t net = seq_net(we, base_ps, base_pd, leav_pd, ent_pd, leav_ps, ent_ps);
             if (net) atomicAdd(&gacc[smv[a]], (unsigned long long)net);
         }
@@ -1333,10 +1505,332 @@ __global__ void k_seq_gains_finish(int64_t M, const int64_t *giso, const unsigne
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < M) gseq[i] = giso[i] + (int64_t)gacc[i];
 }
+
+// ---------------------------------------------------------------------------
+// Incremental refinement (RefineState, refine.cuh).
+//
+// Why a split during projection changes no other node's proposal: splitting
+// cluster c (part P) into a, b raises pins[e, P] (and maybe pins_in[e, P]) by
+// one on the h-edges holding both halves and changes nothing else.  A node
+// n != a, b on such an h-edge with part P already counted both itself and c
+// there (pins >= 2 before and after), so its saving term (pins == 1) is
+// unchanged; for n outside P the set of parts on e and n's own count are
+// unchanged, so present[] and saving are too.  Part sizes are sums over
+// members and do not change.  Hence only a and b need new proposals, and the
+// h-edges only need their counts refreshed.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void push_once(int32_t *flag, int32_t bits, int32_t x, int32_t *list, int32_t *count) {
+    if (atomicOr(flag, bits) == 0) list[atomicAdd(count, 1)] = x;
+}
+
+// dirty h-edges: run lists recomputed for the current assignment.
+// Split-only h-edges (bit 0) keep their parts and destination-part set, so
+// only the counts change (no pinbound / connectivity terms).  H-edges dirtied
+// by moves (bit 1) correct pinbound and connectivity by the difference and
+// mark the pins whose proposal terms changed: a pin's proposal reads, per
+// incident h-edge, the set of parts present (present[]) and whether its own
+// part has exactly one pin there (saving).  So if the part set changed, every
+// pin is dirty; otherwise only pins of a part whose "exactly one pin" state
+// flipped (the movers themselves are marked by k_apply_inc).  pinbound
+// deltas are aggregated per CTA in shared memory when K is small (the parts
+// of a hub are hot addresses).
+constexpr int RU_SMEM_K = 8192;
+__global__ void k_runs_update(const int32_t *elist, const int32_t *ecount, int32_t *edirty, const int64_t *pin_off,
+                              const int32_t *pin_dat, const int64_t *dst_off, const int32_t *dst_dat,
+                              const int32_t *assign, const int64_t *wi, Runs r, unsigned long long *conn,
+                              int64_t *pinbound, int32_t K, int32_t *ndirty, int32_t *nlist, int32_t *ncount) {
+    __shared__ int32_t sdelta[RU_SMEM_K];
+    __shared__ int32_t s_oldp[8][128], s_oldc[8][128];
+    const bool local = K <= RU_SMEM_K;
+    if (local)
+        for (int p = threadIdx.x; p < K; p += blockDim.x) sdelta[p] = 0;
+    __syncthreads();
+    const int lane = lane_id();
+    const int64_t ne = *ecount;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    long long contrib = 0;
+    for (int64_t idx = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id(); idx < ne; idx += nw) {
+        const int32_t e = elist[idx];
+        const int32_t flag = edirty[e];
+        const bool moved = flag & 2;
+        const int64_t plo = pin_off[e], lo = r.off[e];
+        const int len = (int)(pin_off[e + 1] - plo);
+        const int32_t old = r.len[e];
+        int32_t *op = s_oldp[warp_id()], *oc = s_oldc[warp_id()];
+        if (moved)
+            for (int32_t j = lane; j < old; j += 32) {
+                op[j] = r.part[lo + j];
+                oc[j] = r.cnt[lo + j];
+                if (r.cin[lo + j] > 0) {
+                    if (local)
+                        atomicSub(&sdelta[r.part[lo + j]], 1);
+                    else
+                        atomicAdd((unsigned long long *)&pinbound[r.part[lo + j]], ~0ull);
+                }
+            }
+        __syncwarp();
+        int32_t lam;
+        if (len <= 32)
+            lam = warp_edge_runs<1>(e, plo, lo, len, pin_dat, dst_off, dst_dat, assign, r, nullptr);
+        else if (len <= 64)
+            lam = warp_edge_runs<2>(e, plo, lo, len, pin_dat, dst_off, dst_dat, assign, r, nullptr);
+        else
+            lam = warp_edge_runs<4>(e, plo, lo, len, pin_dat, dst_off, dst_dat, assign, r, nullptr);
+        __syncwarp();
+        if (moved) {
+            for (int32_t j = lane; j < lam; j += 32)
+                if (r.cin[lo + j] > 0) {
+                    if (local)
+                        atomicAdd(&sdelta[r.part[lo + j]], 1);
+                    else
+                        atomicAdd((unsigned long long *)&pinbound[r.part[lo + j]], 1ull);
+                }
+            bool same = lam == old;
+            uint32_t flips[4] = {0u, 0u, 0u, 0u};
+            if (same) {
+#pragma unroll
+                for (int q = 0; q < 4; q++) {
+                    const int32_t j = q * 32 + lane;
+                    bool f = false;
+                    if (j < lam) {
+                        same &= r.part[lo + j] == op[j];
+                        f = (r.cnt[lo + j] == 1) != (oc[j] == 1);
+                    }
+                    flips[q] = __ballot_sync(FULL_MASK, f);
+                }
+                same = __all_sync(FULL_MASK, same);
+            }
+            const bool any = flips[0] | flips[1] | flips[2] | flips[3];
+            if (!same || any)
+                for (int64_t j = plo + lane; j < plo + len; j += 32) {
+                    const int32_t n = pin_dat[j];
+                    bool mark = !same;
+                    if (!mark) {
+                        const int32_t k = run_find(r, lo, lam, assign[n]);
+                        mark = (flips[k >> 5] >> (k & 31)) & 1u;
+                    }
+                    if (mark) push_once(&ndirty[n], 1, n, nlist, ncount);
+                }
+        }
+        if (lane == 0) {
+            r.len[e] = lam;
+            edirty[e] = 0;
+            if (moved) contrib += wi[e] * (long long)((lam > 0 ? lam - 1 : 0) - (old > 0 ? old - 1 : 0));
+        }
+    }
+    if (lane == 0 && contrib) atomicAdd(conn, (unsigned long long)contrib);
+    if (local) {
+        __syncthreads();
+        for (int p = threadIdx.x; p < K; p += blockDim.x)
+            if (sdelta[p]) atomicAdd((unsigned long long *)&pinbound[p], (unsigned long long)(long long)sdelta[p]);
+    }
+}
+
+// (item, incidence) pairs of a list of nodes, spread over the whole grid:
+// item i takes `slices` CTAs, each striding over i's incident h-edges, so a
+// hub's thousands of h-edges do not serialise on one warp
+template <class NodeOf, class F>
+__device__ __forceinline__ void grid_incidences(int64_t nitems, NodeOf node_of, const int64_t *inc_off,
+                                                const int32_t *inc_dat, F f) {
+    if (nitems <= 0) return;
+    const int64_t G = gridDim.x;
+    const int64_t slices = G > nitems ? G / nitems : 1;  // CTAs per item
+    for (int64_t t = blockIdx.x; t < nitems * slices; t += G) {
+        const int64_t i = t / slices, sl = t - i * slices;
+        const int32_t n = node_of(i);
+        const int64_t hi = inc_off[n + 1];
+        for (int64_t j = inc_off[n] + sl * blockDim.x + threadIdx.x; j < hi; j += slices * blockDim.x)
+            f(i, inc_dat[j]);
+    }
+}
+// after moves: nodes whose proposal depends on a changed part size — the
+// target no longer fits (a target that still fits stays the best eligible
+// part), or a size-filtered positive-gain part shrank and may now fit
+// (pflags bit 1 = shrank; fsens 3 = more filtered parts than recorded)
+__global__ void k_mark_psize(int32_t N, const int32_t *target, const uint8_t *fsens, const int32_t *fpart,
+                             const uint8_t *pflags, const int64_t *psizes, const int32_t *size, int64_t omega,
+                             int32_t *ndirty, int32_t *nlist, int32_t *ncount) {
+    const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (n >= N) return;
+    const int32_t t = target[n];
+    bool d = t >= 0 && psizes[t] + size[n] > omega;
+    const int f = fsens[n];
+    if (f == 3)
+        d = true;
+    else if (f > 0)
+        d |= (pflags[fpart[2 * n]] & 2) || (f == 2 && (pflags[fpart[2 * n + 1]] & 2));
+    if (d) push_once(&ndirty[n], 1, (int32_t)n, nlist, ncount);
+}
+
+// the round's movers' h-edges (for the sequence gains and inbound events)
+__global__ void k_mover_edges(const int64_t *dM, const int32_t *node, const int64_t *inc_off, const int32_t *inc_dat,
+                              int32_t *emflag, int32_t *mlist, int32_t *mcount) {
+    grid_incidences(*dM, [&](int64_t i) { return node[i]; }, inc_off, inc_dat,
+                    [&](int64_t, int32_t e) { push_once(&emflag[e], 1, e, mlist, mcount); });
+}
+
+// apply the first k moves (refine.py:250-254) and record what they dirty:
+// part sizes, grown parts, the movers' h-edges; also clears the round's
+// mover-edge flags
+__global__ void k_apply_inc(int64_t k, const int32_t *node, const int32_t *from, const int32_t *to,
+                            const int32_t *size, const int64_t *inc_off, const int32_t *inc_dat, int32_t *assign,
+                            int64_t *psizes, uint8_t *pflags, int32_t *edirty, int32_t *elist, int32_t *ecount,
+                            int32_t *emflag, const int32_t *mlist, const int32_t *mcount, int32_t *ndirty,
+                            int32_t *nlist, int32_t *ncount) {
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = tid; i < k; i += nt) {
+        const int32_t n = node[i];
+        push_once(&ndirty[n], 1, n, nlist, ncount);
+        const long long s = size[n];
+        assign[n] = to[i];
+        atomicAdd((unsigned long long *)&psizes[from[i]], (unsigned long long)(-s));
+        atomicAdd((unsigned long long *)&psizes[to[i]], (unsigned long long)s);
+        pflags[from[i]] = 2;
+    }
+    grid_incidences(k, [&](int64_t i) { return node[i]; }, inc_off, inc_dat,
+                    [&](int64_t, int32_t e) { push_once(&edirty[e], 2, e, elist, ecount); });
+    const int64_t nm = *mcount;
+    for (int64_t i = tid; i < nm; i += nt) emflag[mlist[i]] = 0;
+}
+
+__global__ void k_project(int32_t N, const int32_t *gamma, const int32_t *coarse, int32_t *fine) {
+    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v < N) fine[v] = coarse[gamma[v]];
+}
+
+__global__ void k_gamma_count(int32_t N, const int32_t *gamma, int32_t *ccount) {
+    const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (n < N) atomicAdd(&ccount[gamma[n]], 1);
+}
+
+// projection of the carried state to the finer level; halves of split
+// clusters are dirty (new nodes)
+__global__ void k_project_state(int32_t N, const int32_t *gamma, const int32_t *ccount, const int32_t *assign_c,
+                                const int32_t *target_c, const int64_t *gain_c, const uint8_t *fsens_c,
+                                const int32_t *fpart_c, const int32_t *ndirty_c, int32_t *assign_f,
+                                int32_t *target_f, int64_t *gain_f, uint8_t *fsens_f, int32_t *fpart_f,
+                                int32_t *ndirty_f, int32_t *nlist, int32_t *ncount,
+                                int32_t *splist, int32_t *spcount) {
+    const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (n >= N) return;
+    const int32_t g = gamma[n];
+    const bool split = ccount[g] == 2;
+    assign_f[n] = assign_c[g];
+    target_f[n] = target_c[g];
+    gain_f[n] = gain_c[g];
+    fsens_f[n] = fsens_c[g];
+    fpart_f[2 * n] = fpart_c[2 * (int64_t)g];
+    fpart_f[2 * n + 1] = fpart_c[2 * (int64_t)g + 1];
+    const bool d = split || ndirty_c[g];
+    ndirty_f[n] = d;
+    if (d) nlist[atomicAdd(ncount, 1)] = (int32_t)n;
+    if (split) splist[atomicAdd(spcount, 1)] = (int32_t)n;
+}
+
+__global__ void k_mark_split_edges(const int32_t *splist, const int32_t *spcount, const int64_t *inc_off,
+                                   const int32_t *inc_dat, int32_t *edirty, int32_t *elist, int32_t *ecount) {
+    grid_incidences(*spcount, [&](int64_t i) { return splist[i]; }, inc_off, inc_dat,
+                    [&](int64_t, int32_t e) { push_once(&edirty[e], 1, e, elist, ecount); });
+}
+
+enum { CT_NLIST = 0, CT_ELIST = 1, CT_MLIST = 2, CT_SPLIST = 3 };
 }  // namespace
 
-void refine_level(Ctx &c, const DLevel &L, const DWeights &W, int32_t *assign, int32_t K, int64_t omega,
-                  int64_t delta, int32_t max_rounds, int32_t level, std::vector<double> &conns,
+void refine_state_init(Ctx &c, RefineState &st, const DLevel &level0, int32_t K, bool incremental) {
+    st = RefineState();
+    st.inc = incremental;
+    st.K = K;
+    st.E = level0.E;
+    st.ncap = std::max<int64_t>(1, shard_capacity(c.comm, level0.N));
+    st.roff = level0.pin_off;
+    st.rpart = c.alloc<int32_t>(level0.U);
+    st.rcnt = c.alloc<int32_t>(level0.U);
+    st.rcin = c.alloc<int32_t>(level0.U);
+    st.rlen = c.alloc<int32_t>(level0.E);
+    st.psizes = c.alloc<int64_t>(K);
+    st.pinbound = c.alloc<int64_t>(K);
+    st.pflags = c.alloc<uint8_t>(K);
+    st.conn = c.alloc<unsigned long long>(1);
+    st.target = c.alloc<int32_t>(st.ncap);
+    st.target2 = c.alloc<int32_t>(st.ncap);
+    st.gain = c.alloc<int64_t>(st.ncap);
+    st.gain2 = c.alloc<int64_t>(st.ncap);
+    st.fsens = c.alloc<uint8_t>(st.ncap);
+    st.fsens2 = c.alloc<uint8_t>(st.ncap);
+    st.fpart = c.alloc<int32_t>(2 * st.ncap);
+    st.fpart2 = c.alloc<int32_t>(2 * st.ncap);
+    const int64_t n0 = std::max<int32_t>(1, level0.N), e0 = std::max<int32_t>(1, level0.E);
+    st.ndirty = c.alloc<int32_t>(n0);
+    st.ndirty2 = c.alloc<int32_t>(n0);
+    st.nlist = c.alloc<int32_t>(n0);
+    st.splist = c.alloc<int32_t>(n0);
+    st.ccount = c.alloc<int32_t>(n0);
+    st.edirty = c.alloc<int32_t>(e0);
+    st.elist = c.alloc<int32_t>(e0);
+    st.emflag = c.alloc<int32_t>(e0);
+    st.mlist = c.alloc<int32_t>(e0);
+    st.ctr = c.alloc<int32_t>(8);
+    st.hacc = c.alloc<long long>((int64_t)HUB_MAX * std::max(1, K));
+    st.htot = c.alloc<long long>(2 * HUB_MAX);
+    st.hdone = c.alloc<int32_t>(HUB_MAX);
+    st.hlist = c.alloc<int32_t>(HUB_MAX);
+    c.zero(st.hacc, (int64_t)HUB_MAX * std::max(1, K));
+    c.zero(st.htot, 2 * HUB_MAX);
+    c.zero(st.hdone, HUB_MAX);
+    c.zero(st.pflags, K);
+    c.zero(st.fsens, st.ncap);
+    c.zero(st.ndirty, n0);
+    c.zero(st.edirty, e0);
+    c.zero(st.emflag, e0);
+    c.zero(st.ctr, 8);
+    c.zero(st.rlen, level0.E);
+}
+
+void refine_state_release(Ctx &c, RefineState &st) {
+    for (void *p : {(void *)st.rpart, (void *)st.rcnt, (void *)st.rcin, (void *)st.rlen, (void *)st.psizes,
+                    (void *)st.pinbound, (void *)st.pflags, (void *)st.conn, (void *)st.target, (void *)st.target2,
+                    (void *)st.gain, (void *)st.gain2, (void *)st.fsens, (void *)st.fsens2, (void *)st.fpart, (void *)st.fpart2, (void *)st.ndirty,
+                    (void *)st.ndirty2, (void *)st.nlist, (void *)st.splist, (void *)st.ccount, (void *)st.edirty,
+                    (void *)st.elist, (void *)st.emflag, (void *)st.mlist, (void *)st.ctr, (void *)st.hacc,
+                    (void *)st.htot, (void *)st.hdone, (void *)st.hlist})
+        c.free(p);
+    st = RefineState();
+}
+
+void refine_project(Ctx &c, RefineState &st, const DLevel &fine, int32_t coarse_n, int32_t *&assign,
+                    int32_t *&assign2) {
+    const int32_t N = fine.N;
+    if (N > 0) {
+        if (st.inc) {
+            c.zero(st.ccount, std::max<int32_t>(1, coarse_n));
+            k_gamma_count<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(N, fine.gamma, st.ccount);
+            DHGP_LAUNCHED(c);
+            c.zero(st.ctr + CT_NLIST, 1);
+            c.zero(st.ctr + CT_SPLIST, 1);
+            k_project_state<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(
+                N, fine.gamma, st.ccount, assign, st.target, st.gain, st.fsens, st.fpart, st.ndirty, assign2,
+                st.target2, st.gain2, st.fsens2, st.fpart2, st.ndirty2, st.nlist, st.ctr + CT_NLIST, st.splist,
+                st.ctr + CT_SPLIST);
+            DHGP_LAUNCHED(c);
+            static int g = resident_grid(c, k_mark_split_edges, 256, 0);
+            k_mark_split_edges<<<g, 256, 0, c.stream>>>(st.splist, st.ctr + CT_SPLIST, fine.inc_off, fine.inc_dat,
+                                                        st.edirty, st.elist, st.ctr + CT_ELIST);
+            DHGP_LAUNCHED(c);
+            std::swap(st.target, st.target2);
+            std::swap(st.gain, st.gain2);
+            std::swap(st.fsens, st.fsens2);
+            std::swap(st.fpart, st.fpart2);
+            std::swap(st.ndirty, st.ndirty2);
+        } else {
+            k_project<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(N, fine.gamma, assign, assign2);
+            DHGP_LAUNCHED(c);
+        }
+    }
+    std::swap(assign, assign2);
+}
+
+void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, int32_t *assign, int32_t K,
+                  int64_t omega, int64_t delta, int32_t max_rounds, int32_t level, std::vector<double> &conns,
                   const RoundObserver *obs, int32_t max_edge_pins) {
     static bool attr = false;
     if (!attr) {
@@ -1357,23 +1851,25 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, int32_t *assign, i
         attr = true;
     }
     const int32_t N = L.N;
-    // ---- per-level buffers (capacities: N moves, 2N + 2 S_in events) ------
+    // ---- state (run lists at the level-0 pin offsets, part counters) -------
     Runs r;
-    r.part = c.alloc<int32_t>(L.U);
-    r.cnt = c.alloc<int32_t>(L.U);
-    r.cin = c.alloc<int32_t>(L.U);
-    r.len = c.alloc<int32_t>(L.E);
-    int32_t *tmp_parts = c.alloc<int32_t>(L.U);
-    int64_t *psizes = c.alloc<int64_t>(K), *pinbound = c.alloc<int64_t>(K);
-    int32_t *target = c.alloc<int32_t>(shard_capacity(c.comm, N));
-    int64_t *gain = c.alloc<int64_t>(shard_capacity(c.comm, N));
+    r.off = st.roff;
+    r.part = st.rpart;
+    r.cnt = st.rcnt;
+    r.cin = st.rcin;
+    r.len = st.rlen;
+    int64_t *psizes = st.psizes, *pinbound = st.pinbound;
+    int32_t *target = st.target;
+    int64_t *gain = st.gain;
+    unsigned long long *conn_d = st.conn;
+    // ---- per-level buffers (capacities: N moves, 2N + 2 S_in events) ------
+    int32_t *tmp_parts = max_edge_pins > 128 ? c.alloc<int32_t>(L.U) : nullptr;
     uint8_t *flags = c.alloc<uint8_t>(N);
     int64_t *mpos = c.alloc<int64_t>((int64_t)N + 1);
     int32_t *pos = c.alloc<int32_t>(N);
     int32_t *ctr = c.alloc<int32_t>(4);
     int32_t *big = c.alloc<int32_t>(std::max<int64_t>(N, L.E));
     int32_t *big2 = c.alloc<int32_t>(N);
-    unsigned long long *conn_d = c.alloc<unsigned long long>(1);
     uint64_t *mk = c.alloc<uint64_t>(N), *mkt = c.alloc<uint64_t>(N);
     uint32_t *mv = c.alloc<uint32_t>(N), *mvt = c.alloc<uint32_t>(N);
     int32_t *node = c.alloc<int32_t>(N), *from = c.alloc<int32_t>(N), *to = c.alloc<int32_t>(N);
@@ -1386,8 +1882,11 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, int32_t *assign, i
     long long *sres = c.alloc<long long>(4);
     // dense global tier (K too large for shared memory): per-block rows of K
     // counters + touched lists, as many blocks as ~1 GiB allows (4 per SM max)
-    const int pb_blocks = (int)std::max<int64_t>(
-        1, std::min<int64_t>((int64_t)c.num_sms * 4, (int64_t)(1ll << 30) / std::max<int64_t>(1, 12ll * K)));
+    const bool need_dense = K > ph_maxk<unsigned>() && K > std::min(4096, tiers().small_k);
+    const int pb_blocks = need_dense ? (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)c.num_sms * 4,
+                                                                              (int64_t)(1ll << 30) /
+                                                                                  std::max<int64_t>(1, 12ll * K)))
+                                     : 1;
     long long *pdense = c.alloc<long long>((int64_t)pb_blocks * K);
     int32_t *ptouched = c.alloc<int32_t>((int64_t)pb_blocks * K);
     if (K > 0) {
@@ -1400,26 +1899,71 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, int32_t *assign, i
     const int ibits_cap = std::max(1, bitlen((uint64_t)N));
     if (1 + ibits_cap + pbits > 64) throw Error{DHGP_ERR_UNSUPPORTED, "event key needs more than 64 bits"};
     const int64_t *dM = mpos + N;
+    static int g_ru = resident_grid(c, k_runs_update, 256, 0);
+    static int g_me = resident_grid(c, k_mover_edges, 256, 0);
+    static int g_ap = resident_grid(c, k_apply_inc, 256, 0);
+    const unsigned g_edges = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(L.E, 256), (int64_t)c.num_sms * 8));
+    auto runs_update = [&]() {
+        k_runs_update<<<g_ru, 256, 0, c.stream>>>(st.elist, st.ctr + CT_ELIST, st.edirty, L.pin_off, L.pin_dat,
+                                                 L.dst_off, L.dst_dat, assign, W.wi, r, conn_d, pinbound, K, st.ndirty,
+                                                 st.nlist, st.ctr + CT_NLIST);
+        DHGP_LAUNCHED(c);
+        c.zero(st.ctr + CT_ELIST, 1);
+    };
 
     bool need_final = false;
     for (int32_t rnd = 0; rnd < max_rounds; rnd++) {
-        // --- A11/A12/A16 + A13 ---------------------------------------------
-        build_runs(c, L, W, assign, r, tmp_parts, pinbound, K, conn_d, max_edge_pins);
-        c.zero(psizes, K);
-        if (N > 0) {
-            k_part_sizes<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(N, assign, L.size, psizes);
-            DHGP_LAUNCHED(c);
+        const bool full = !st.inc || st.fresh;
+        if (full) {
+            // --- A11/A12/A16 + A13 over everything ----------------------------
+            build_runs(c, L, W, assign, r, tmp_parts, pinbound, K, conn_d, max_edge_pins);
+            c.zero(psizes, K);
+            if (N > 0) {
+                k_part_sizes<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(N, assign, L.size, psizes);
+                DHGP_LAUNCHED(c);
+            }
+        } else {
+            // --- only what the last moves / the projection touched -----------
+            KScope ks(c, "runs_update");
+            runs_update();
+            if (st.moved && N > 0) {
+                k_mark_psize<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(N, target, st.fsens, st.fpart, st.pflags,
+                                                                           psizes, L.size, omega, st.ndirty,
+                                                                           st.nlist, st.ctr + CT_NLIST);
+                DHGP_LAUNCHED(c);
+                c.zero(st.pflags, K);
+            }
         }
+        st.moved = false;
         // --- A14 propose (warp tier + block tier, no host sync) -------------
         {
             KScope ks(c, "propose", (double)(28.0 * N + 12.0 * L.U + 20.0 * L.E + 8.0 * K), N);
             c.zero(ctr, 4);
-            ProposeArgs a{N, K, L.inc_off, L.inc_dat, L.pin_off, W.wi, r, assign, psizes, L.size, omega,
+            ProposeArgs a{N, K, L.inc_off, L.inc_dat, W.wi, r, assign, psizes, L.size, omega,
                           target, gain, ctr, big, ctr + 1, big2, ctr + 2, tiers(), 0, N};
+            a.fsens = st.fsens;
+            a.fpart = st.fpart;
+            constexpr int kSmallK = 4096;
+            const bool small_k = K <= std::min(kSmallK, tiers().small_k);
+            if (small_k) {
+                a.hub_list = st.hlist;
+                a.hub_count = ctr + 3;
+            }
+            if (!full) {
+                a.list = st.nlist;
+                a.list_count = st.ctr + CT_NLIST;
+                a.ndirty = st.ndirty;
+            }
             const Shard sh = shard_of(c.comm, N);
             a.lo = (int32_t)sh.lo;
             a.hi = (int32_t)sh.hi;
-            const int64_t nmine = std::max<int64_t>(1, sh.hi - sh.lo);
+            const int64_t nmine = full ? std::max<int64_t>(1, sh.hi - sh.lo) : (int64_t)1 << 40;
+            if (trace_enabled() && !full) {  // diagnostics: dirty-set sizes
+                int32_t hc[8];
+                c.d2h(hc, st.ctr, 8);
+                c.sync();
+                fprintf(stderr, "dirty level %d round %d N %d nodes %d\n", level, rnd, N, hc[CT_NLIST]);
+            }
             if (N > 0) {
                 const bool narrow = W.wsum < (1ll << 32);
                 if (narrow) {
@@ -1434,9 +1978,18 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, int32_t *assign, i
                         <<<blocks, PR_WARPS * 32, pr_smem<unsigned long long>(), c.stream>>>(a);
                 }
                 DHGP_LAUNCHED(c);
+                if (!full) c.zero(st.ctr + CT_NLIST, 1);
                 KScope kh(c, "propose_heavy");
-                constexpr int kSmallK = 4096;
-                if (K <= std::min(kSmallK, tiers().small_k)) {
+                if (small_k) {
+                    if (narrow) {
+                        static int h32 = resident_grid(c, k_propose_hub<unsigned>, 256, 4 * kSmallK);
+                        k_propose_hub<unsigned><<<h32, 256, 4 * K, c.stream>>>(a, st.hacc, st.htot, st.hdone);
+                    } else {
+                        static int h64 = resident_grid(c, k_propose_hub<unsigned long long>, 256, 8 * kSmallK);
+                        k_propose_hub<unsigned long long>
+                            <<<h64, 256, 8 * K, c.stream>>>(a, st.hacc, st.htot, st.hdone);
+                    }
+                    DHGP_LAUNCHED(c);
                     // few parts: the escalated nodes go straight to dense shared
                     // arrays over the parts (no hashing), 256 threads per node
                     ProposeArgs b = a;
@@ -1454,33 +2007,42 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, int32_t *assign, i
                     }
                     DHGP_LAUNCHED(c);
                 } else {
-                // medium tier: reads the escalation count on device, exits when zero
-                if (narrow) {
-                    static int m32 = resident_grid(c, k_propose_mid<unsigned>, PM_THREADS, pm_smem<unsigned>());
-                    k_propose_mid<unsigned><<<m32, PM_THREADS, pm_smem<unsigned>(), c.stream>>>(a);
-                } else {
-                    static int m64 = resident_grid(c, k_propose_mid<unsigned long long>, PM_THREADS,
-                                                   pm_smem<unsigned long long>());
-                    k_propose_mid<unsigned long long>
-                        <<<m64, PM_THREADS, pm_smem<unsigned long long>(), c.stream>>>(a);
-                }
-                DHGP_LAUNCHED(c);
-                if (narrow && K <= ph_maxk<unsigned>()) {
-                    k_propose_heavy<unsigned><<<c.num_sms, PH_THREADS, ph_smem<unsigned>(K), c.stream>>>(a);
-                } else if (!narrow && K <= ph_maxk<unsigned long long>()) {
-                    k_propose_heavy<unsigned long long>
-                        <<<c.num_sms, PH_THREADS, ph_smem<unsigned long long>(K), c.stream>>>(a);
-                } else {
-                    k_propose_block<<<pb_blocks, PB_THREADS, 0, c.stream>>>(a, pdense, ptouched);
-                }
-                DHGP_LAUNCHED(c);
+                    // medium tier: reads the escalation count on device, exits when zero
+                    if (narrow) {
+                        static int m32 = resident_grid(c, k_propose_mid<unsigned>, PM_THREADS, pm_smem<unsigned>());
+                        k_propose_mid<unsigned><<<m32, PM_THREADS, pm_smem<unsigned>(), c.stream>>>(a);
+                    } else {
+                        static int m64 = resident_grid(c, k_propose_mid<unsigned long long>, PM_THREADS,
+                                                       pm_smem<unsigned long long>());
+                        k_propose_mid<unsigned long long>
+                            <<<m64, PM_THREADS, pm_smem<unsigned long long>(), c.stream>>>(a);
+                    }
+                    DHGP_LAUNCHED(c);
+                    if (narrow && K <= ph_maxk<unsigned>()) {
+                        k_propose_heavy<unsigned><<<c.num_sms, PH_THREADS, ph_smem<unsigned>(K), c.stream>>>(a);
+                    } else if (!narrow && K <= ph_maxk<unsigned long long>()) {
+                        k_propose_heavy<unsigned long long>
+                            <<<c.num_sms, PH_THREADS, ph_smem<unsigned long long>(K), c.stream>>>(a);
+                    } else {
+                        k_propose_block<<<pb_blocks, PB_THREADS, 0, c.stream>>>(a, pdense, ptouched);
+                    }
+                    DHGP_LAUNCHED(c);
                 }
             }
-            if (sh.on) {  // complete (target, gain) from the other ranks' node ranges
+            if (trace_enabled()) {
+                int32_t hc[4];
+                c.d2h(hc, ctr, 4);
+                c.sync();
+                fprintf(stderr, "tiers level %d round %d big %d dense %d hubs %d\n", level, rnd, hc[1], hc[2], hc[3]);
+            }
+            if (sh.on) {  // complete (target, gain, fsens) from the other ranks' node ranges
                 allgather(c, c.comm, target, sizeof(int32_t), sh.chunk);
                 allgather(c, c.comm, gain, sizeof(int64_t), sh.chunk);
+                allgather(c, c.comm, st.fsens, sizeof(uint8_t), sh.chunk);
+                allgather(c, c.comm, st.fpart, 2 * sizeof(int32_t), sh.chunk);
             }
         }
+        st.fresh = false;
         // --- sequence: movers by (gain desc, node asc) (refine.py:108-110) --
         if (N > 0) {
             k_mover_flags<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(N, target, flags);
@@ -1508,6 +2070,17 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, int32_t *assign, i
         k_build_moves_dn<<<(unsigned)cdiv(M, 256), 256, 0, c.stream>>>(dM, mv, assign, target, gain, node, from, to,
                                                                        giso, pos);
         DHGP_LAUNCHED(c);
+        // h-edges holding a mover: the only ones with sequence-gain terms or
+        // inbound events (incremental mode; the full mode scans every h-edge)
+        const int32_t *elist = nullptr, *elist_n = nullptr;
+        if (st.inc) {
+            k_mover_edges<<<g_me, 256, 0, c.stream>>>(dM, node, L.inc_off, L.inc_dat, st.emflag, st.mlist,
+                                                      st.ctr + CT_MLIST);
+            DHGP_LAUNCHED(c);
+            elist = st.mlist;
+            elist_n = st.ctr + CT_MLIST;
+        }
+        const unsigned g_list = st.inc ? g_edges : (unsigned)std::max<int64_t>(1, cdiv(L.E, 256));
         {
             // replicated on every rank: O(sum |e|), no exchange
             KScope ks(c, "seq_gains", 0.0);
@@ -1515,9 +2088,8 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, int32_t *assign, i
             c.zero(gacc, M);
             c.zero(sg_ctr, 2);
             if (L.E > 0) {
-                k_seq_gains_edge<<<(unsigned)cdiv(L.E, 256), 256, 0, c.stream>>>(L.E, L.pin_off, L.pin_dat, W.wi, r,
-                                                                                 pos, from, to, gacc, sg_big, sg_ctr,
-                                                                                 tiers().edge_movers);
+                k_seq_gains_edge<<<g_list, 256, 0, c.stream>>>(L.E, elist, elist_n, L.pin_off, L.pin_dat, W.wi, r, pos,
+                                                               from, to, gacc, sg_big, sg_ctr, tiers().edge_movers);
                 DHGP_LAUNCHED(c);
                 k_seq_gains_edge_block<<<c.num_sms, 256, 0, c.stream>>>(L.pin_off, L.pin_dat, W.wi, r, pos, from, to,
                                                                          gacc, sg_big, sg_ctr, sg_ctr + 1);
@@ -1533,12 +2105,11 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, int32_t *assign, i
         k_size_events_dn<<<(unsigned)cdiv(M, 256), 256, 0, c.stream>>>(dM, node, from, to, L.size, ev);
         DHGP_LAUNCHED(c);
         if (L.E > 0) {
-            k_inbound_events<<<(unsigned)cdiv(L.E, 256), 256, 0, c.stream>>>(L.E, L.dst_off, L.dst_dat, L.pin_off, r,
-                                                                           pos, from, to, ev, big, ctr,
-                                                                           tiers().edge_movers);
+            k_inbound_events<<<g_list, 256, 0, c.stream>>>(L.E, elist, elist_n, L.dst_off, L.dst_dat, r, pos, from, to,
+                                                           ev, big, ctr, tiers().edge_movers);
             DHGP_LAUNCHED(c);
-            k_inbound_events_block<<<c.num_sms, 256, 0, c.stream>>>(L.dst_off, L.dst_dat, L.pin_off, r, pos, from, to,
-                                                                     ev, big, ctr, ctr + 2);
+            k_inbound_events_block<<<c.num_sms, 256, 0, c.stream>>>(L.dst_off, L.dst_dat, r, pos, from, to, ev, big,
+                                                                     ctr, ctr + 2);
             DHGP_LAUNCHED(c);
         }
         // --- A17 select: one CTA for small rounds, T read on device ----------
@@ -1628,7 +2199,16 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, int32_t *assign, i
             rec.active.assign(ae.begin() + 1, ae.begin() + 2 + M);
             (*obs)(rec);
         }
-        if (kbest > 0) {
+        if (st.inc) {
+            // apply + record the dirt; clears the mover-edge flags either way
+            k_apply_inc<<<g_ap, 256, 0, c.stream>>>(kbest, node, from, to, L.size, L.inc_off, L.inc_dat, assign,
+                                                    psizes, st.pflags, st.edirty, st.elist, st.ctr + CT_ELIST,
+                                                    st.emflag, st.mlist, st.ctr + CT_MLIST, st.ndirty, st.nlist,
+                                                    st.ctr + CT_NLIST);
+            DHGP_LAUNCHED(c);
+            c.zero(st.ctr + CT_MLIST, 1);
+            if (kbest > 0) st.moved = true;
+        } else if (kbest > 0) {
             k_apply<<<(unsigned)cdiv(kbest, 256), 256, 0, c.stream>>>(kbest, node, to, assign);
             DHGP_LAUNCHED(c);
         }
@@ -1639,22 +2219,31 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, int32_t *assign, i
         need_final = true;
     }
     if (need_final) {
-        double v;
-        evaluate_assign(c, L, W, assign, K, nullptr, nullptr, &v);
-        conns.push_back(v);
+        // connectivity after the last applied round
+        if (st.inc) {
+            runs_update();
+            unsigned long long h = 0;
+            c.d2h(&h, conn_d, 1);
+            c.sync();
+            conns.push_back((double)(int64_t)h);
+        } else {
+            double v;
+            evaluate_assign(c, L, W, assign, K, nullptr, nullptr, &v);
+            conns.push_back(v);
+        }
     }
-    for (void *p : {(void *)r.part, (void *)r.cnt, (void *)r.cin, (void *)r.len, (void *)tmp_parts, (void *)psizes,
-                    (void *)pinbound, (void *)target, (void *)gain, (void *)flags, (void *)mpos, (void *)pos,
-                    (void *)ctr, (void *)big, (void *)big2, (void *)conn_d, (void *)mk, (void *)mkt, (void *)mv, (void *)mvt,
-                    (void *)node, (void *)from, (void *)to, (void *)giso, (void *)gseq, (void *)gseq_acc, (void *)sg_big,
-                    (void *)sg_ctr, (void *)ek, (void *)ekt,
-                    (void *)evv, (void *)evt, (void *)ecount, (void *)sres, (void *)pdense, (void *)ptouched})
+    for (void *p : {(void *)tmp_parts, (void *)flags, (void *)mpos, (void *)pos, (void *)ctr, (void *)big,
+                    (void *)big2, (void *)mk, (void *)mkt, (void *)mv, (void *)mvt, (void *)node, (void *)from,
+                    (void *)to, (void *)giso, (void *)gseq, (void *)gseq_acc, (void *)sg_big, (void *)sg_ctr,
+                    (void *)ek, (void *)ekt, (void *)evv, (void *)evt, (void *)ecount, (void *)sres, (void *)pdense,
+                    (void *)ptouched})
         c.free(p);
 }
 
 void evaluate_assign(Ctx &c, const DLevel &L, const DWeights &W, const int32_t *assign, int32_t K,
                      int64_t *d_sizes, int64_t *d_inbound, double *h_conn) {
     Runs r;
+    r.off = L.pin_off;
     r.part = c.alloc<int32_t>(L.U);
     r.cnt = c.alloc<int32_t>(L.U);
     r.cin = c.alloc<int32_t>(L.U);

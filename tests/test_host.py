@@ -52,9 +52,13 @@ def test_product_fails_loudly_without_device(monkeypatch):
 
 
 def test_product_package_never_imports_the_oracle():
-    for p in (ROOT / "paper_2604_14411_b200").rglob("*.py"):
-        src = p.read_text()
-        assert "oracle" not in re.sub(r"#.*|\"\"\"[\s\S]*?\"\"\"", "", src).replace("_oracle", ""), p
+    # No import of the oracle package and no path to its libraries.  The bare
+    # word may appear (the CLI names the reference's out-of-scope "oracle"
+    # subcommand), so the check is on imports and file names.
+    bad = re.compile(r"^\s*(from|import)\s+oracle\b|liboracle|oracle[/\\.]_ref|oracle\.py|dhgp_oracle", re.M)
+    for p in list((ROOT / "paper_2604_14411_b200").rglob("*.py")) + list((ROOT / "paper_2604_14411_b200").rglob("*.cu*")):
+        src = re.sub(r"#.*|\"\"\"[\s\S]*?\"\"\"", "", p.read_text())
+        assert not bad.search(src), p
 
 
 def test_config_validation():

@@ -4,6 +4,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if os.environ.get("DHGP_TRACE") != "1":
     env = dict(os.environ, DHGP_TRACE="1")
     r = subprocess.run([sys.executable, __file__] + sys.argv[1:], env=env, capture_output=True, text=True)
+    if os.environ.get("DHGP_TRACE_RAW"):
+        with open(os.environ["DHGP_TRACE_RAW"], "w") as f:
+            f.write(r.stdout + r.stderr)
     agg = collections.defaultdict(lambda: [0, 0.0, []])
     for ln in r.stderr.splitlines():
         if ln.startswith("trace "):
@@ -30,3 +33,6 @@ import time
 t = time.perf_counter()
 p, s = dp.partition(g, dp.Config(dp.Constraints(om, de), max_levels=1 << 20))
 print("total", time.perf_counter() - t, len(s.levels), p.num_parts)
+import json
+print("LEVELS", json.dumps(s.levels))
+print("TRACE", json.dumps([len(t) for t in s.connectivity_trace]))
