@@ -874,74 +874,8 @@ __device__ __forceinline__ void emit(const EvArgs &ev, uint64_t track, int32_t p
 // inbound track (refine.py:210-237), per h-edge: the movers among its
 // destination pins in sequence order; per part a running destination-pin
 // count from pins_in[e, p]; crossings 0->1 / 1->0 emit distinct events.
-constexpr int kEvLocal = 32;
-__device__ __noinline__ void inbound_events_edge(int32_t e, const int64_t *dst_off, const int32_t *dst_dat, Runs r,
-                                                 const int32_t *pos, const int32_t *from, const int32_t *to,
-                                                 EvArgs ev, int32_t *big_list, int32_t *big_count, int cap);
-// edges: all E, or the list elist[0 .. *ecount) when elist is set
-__global__ void k_inbound_events(int32_t E, const int32_t *elist, const int32_t *ecount, const int64_t *dst_off,
-                                 const int32_t *dst_dat, Runs r, const int32_t *pos, const int32_t *from,
-                                 const int32_t *to, EvArgs ev, int32_t *big_list, int32_t *big_count, int cap) {
-    const int64_t ne = elist ? (int64_t)*ecount : (int64_t)E;
-    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < ne;
-         idx += (int64_t)gridDim.x * blockDim.x)
-        inbound_events_edge(elist ? elist[idx] : (int32_t)idx, dst_off, dst_dat, r, pos, from, to, ev, big_list,
-                            big_count, cap);
-}
-__device__ __noinline__ void inbound_events_edge(int32_t e, const int64_t *dst_off, const int32_t *dst_dat, Runs r,
-                                                 const int32_t *pos, const int32_t *from, const int32_t *to,
-                                                 EvArgs ev, int32_t *big_list, int32_t *big_count, int cap) {
-    int32_t mv[kEvLocal];
-    int nm = 0;
-    for (int64_t q = dst_off[e]; q < dst_off[e + 1]; q++) {
-        int32_t j = pos[dst_dat[q]];
-        if (j < 0) continue;
-        if (nm == cap) {
-            big_list[atomicAdd(big_count, 1)] = (int32_t)e;
-            return;
-        }
-        mv[nm++] = j;
-    }
-    if (nm == 0) return;
-    for (int a = 1; a < nm; a++) {
-        int32_t x = mv[a];
-        int b = a - 1;
-        while (b >= 0 && mv[b] > x) {
-            mv[b + 1] = mv[b];
-            b--;
-        }
-        mv[b + 1] = x;
-    }
-    int32_t dp[2 * kEvLocal], dc[2 * kEvLocal];
-    int nd = 0;
-    const int64_t lo = r.off[e];
-    const int32_t lam = r.len[e];
-    for (int a = 0; a < nm; a++) {
-        const int32_t i = mv[a];
-        const int32_t pf = from[i], pt = to[i];
-        int k;
-        for (k = 0; k < nd && dp[k] != pf; k++) {
-        }
-        if (k == nd) {
-            int32_t f = run_find(r, lo, lam, pf);
-            dp[nd] = pf;
-            dc[nd] = f >= 0 ? r.cin[lo + f] : 0;
-            nd++;
-        }
-        if (--dc[k] == 0) emit(ev, 1, pf, i, -1);
-        for (k = 0; k < nd && dp[k] != pt; k++) {
-        }
-        if (k == nd) {
-            int32_t f = run_find(r, lo, lam, pt);
-            dp[nd] = pt;
-            dc[nd] = f >= 0 ? r.cin[lo + f] : 0;
-            nd++;
-        }
-        if (++dc[k] == 1) emit(ev, 1, pt, i, +1);
-    }
-}
-
-// the same walk for h-edges with many movers: block collects and sorts, one
+// This is the walk for h-edges with many movers (the warp kernel
+// k_round_edges takes the others): the block collects and sorts them, one
 // thread walks with a shared-memory part dictionary
 constexpr int kEvBlockMax = 2048;
 __global__ void k_inbound_events_block(const int64_t *dst_off, const int32_t *dst_dat, Runs r,
@@ -1374,73 +1308,6 @@ __device__ __forceinline__ int64_t seq_net(int64_t we, int32_t base_ps, int32_t 
     }
     return net;
 }
-constexpr int kSgLocal = 32;
-__device__ __noinline__ void seq_gains_edge(int32_t e, const int64_t *pin_off, const int32_t *pin_dat,
-                                            const int64_t *wi, Runs r, const int32_t *pos, const int32_t *from,
-                                            const int32_t *to, unsigned long long *gacc, int32_t *big_list,
-                                            int32_t *big_count, int cap);
-// edges: all E, or the list elist[0 .. *ecount) when elist is set
-__global__ void k_seq_gains_edge(int32_t E, const int32_t *elist, const int32_t *ecount, const int64_t *pin_off,
-                                 const int32_t *pin_dat, const int64_t *wi, Runs r, const int32_t *pos,
-                                 const int32_t *from, const int32_t *to, unsigned long long *gacc,
-                                 int32_t *big_list, int32_t *big_count, int cap) {
-    const int64_t ne = elist ? (int64_t)*ecount : (int64_t)E;
-    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < ne;
-         idx += (int64_t)gridDim.x * blockDim.x)
-        seq_gains_edge(elist ? elist[idx] : (int32_t)idx, pin_off, pin_dat, wi, r, pos, from, to, gacc, big_list,
-                       big_count, cap);
-}
-__device__ __noinline__ void seq_gains_edge(int32_t e, const int64_t *pin_off, const int32_t *pin_dat,
-                                            const int64_t *wi, Runs r, const int32_t *pos, const int32_t *from,
-                                            const int32_t *to, unsigned long long *gacc, int32_t *big_list,
-                                            int32_t *big_count, int cap) {
-    int32_t mv[kSgLocal];
-    int nm = 0;
-    const int64_t lo = pin_off[e], hi = pin_off[e + 1];
-    for (int64_t pp = lo; pp < hi; pp++) {
-        const int32_t j = pos[pin_dat[pp]];
-        if (j < 0) continue;
-        if (nm == cap) {
-            big_list[atomicAdd(big_count, 1)] = (int32_t)e;
-            return;
-        }
-        mv[nm++] = j;
-    }
-    if (nm == 0) return;
-    for (int a = 1; a < nm; a++) {
-        const int32_t x = mv[a];
-        int b = a - 1;
-        while (b >= 0 && mv[b] > x) {
-            mv[b + 1] = mv[b];
-            b--;
-        }
-        mv[b + 1] = x;
-    }
-    int32_t mf[kSgLocal], mt[kSgLocal];
-    for (int a = 0; a < nm; a++) {
-        mf[a] = from[mv[a]];
-        mt[a] = to[mv[a]];
-    }
-    const int64_t we = wi[e];
-    const int32_t lam = r.len[e];
-    const int64_t ro = r.off[e];
-    for (int a = 0; a < nm; a++) {
-        const int32_t ps = mf[a], pd = mt[a];
-        int32_t leav_pd = 0, ent_pd = 0, leav_ps = 0, ent_ps = 0;
-        for (int b = 0; b < a; b++) {
-            leav_pd += mf[b] == pd;
-            ent_pd += mt[b] == pd;
-            leav_ps += mf[b] == ps;
-            ent_ps += mt[b] == ps;
-        }
-        int32_t k = run_find(r, ro, lam, ps);
-        const int32_t base_ps = k >= 0 ? r.cnt[ro + k] : 0;
-        k = run_find(r, ro, lam, pd);
-        const int32_t base_pd = k >= 0 ? r.cnt[ro + k] : 0;
-        const int64_t net = seq_net(we, base_ps, base_pd, leav_pd, ent_pd, leav_ps, ent_ps);
-        if (net) atomicAdd(&gacc[mv[a]], (unsigned long long)net);
-    }
-}
 // the same for h-edges with many movers: a block gathers and sorts them, each
 // thread takes some movers and counts over the earlier ones
 constexpr int kSgBlockMax = 2048;
@@ -1501,6 +1368,107 @@ __global__ void k_seq_gains_edge_block(const int64_t *pin_off, const int32_t *pi
         __syncthreads();
     }
 }
+
+// Warp per h-edge (all E, or the movers' h-edge list): the round's terms of
+// one h-edge from its movers in sequence order — the sequence-gain terms of
+// rules (a)-(d) over its pins (A15) and the inbound-track crossings over its
+// destination pins (A17).  Lane a holds the a-th mover; the counts over the
+// earlier movers are shuffles, so each term is independent:
+//   dc[p] before mover a leaves = pins_in[e, p] - #{b < a: from_b = p} + #{b < a: to_b = p}
+// and "--dc == 0" / "++dc == 1" of the sequential walk become tests on it.
+// H-edges with more than `cap` movers go to the block kernels.
+__device__ __forceinline__ int warp_collect_movers(const int32_t *dat, int64_t lo, int64_t hi, const int32_t *pos,
+                                                   int32_t *smv) {
+    const int lane = lane_id();
+    const uint32_t lt = (1u << lane) - 1u;
+    int nm = 0;
+    for (int64_t b = lo; b < hi; b += 32) {
+        const int64_t q = b + lane;
+        const int32_t j = q < hi ? pos[dat[q]] : -1;
+        const uint32_t bal = __ballot_sync(FULL_MASK, j >= 0);
+        if (j >= 0) {
+            const int slot = nm + __popc(bal & lt);
+            if (slot < 32) smv[slot] = j;
+        }
+        nm += __popc(bal);
+    }
+    __syncwarp();
+    return nm;
+}
+__global__ void __launch_bounds__(256) k_round_edges(int32_t E, const int32_t *elist, const int32_t *ecount,
+                                                     const int64_t *pin_off, const int32_t *pin_dat,
+                                                     const int64_t *dst_off, const int32_t *dst_dat,
+                                                     const int64_t *wi, Runs r, const int32_t *pos,
+                                                     const int32_t *from, const int32_t *to,
+                                                     unsigned long long *gacc, EvArgs ev, int32_t *sg_big,
+                                                     int32_t *sg_count, int32_t *ev_big, int32_t *ev_count,
+                                                     int cap) {
+    __shared__ int32_t s_mv[8][32];
+    const int lane = lane_id();
+    int32_t *smv = s_mv[warp_id()];
+    const int64_t ne = elist ? (int64_t)*ecount : (int64_t)E;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t idx = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id(); idx < ne; idx += nw) {
+        const int32_t e = elist ? elist[idx] : (int32_t)idx;
+        const int64_t ro = r.off[e];
+        const int32_t lam = r.len[e];
+        // ---- sequence gains over all pins --------------------------------
+        int nm = warp_collect_movers(pin_dat, pin_off[e], pin_off[e + 1], pos, smv);
+        if (nm > cap) {
+            if (lane == 0) sg_big[atomicAdd(sg_count, 1)] = e;
+        } else if (nm > 0) {
+            uint32_t v[1] = {lane < nm ? (uint32_t)smv[lane] : 0xffffffffu};
+            warp_bitonic_sort<1>(v);
+            const int32_t i = (int32_t)v[0];
+            const int32_t ps = lane < nm ? from[i] : -1, pd = lane < nm ? to[i] : -1;
+            int32_t leav_pd = 0, ent_pd = 0, leav_ps = 0, ent_ps = 0;
+            for (int b = 0; b < nm; b++) {
+                const int32_t fb = __shfl_sync(FULL_MASK, ps, b), tb = __shfl_sync(FULL_MASK, pd, b);
+                if (b < lane) {
+                    leav_pd += fb == pd;
+                    ent_pd += tb == pd;
+                    leav_ps += fb == ps;
+                    ent_ps += tb == ps;
+                }
+            }
+            if (lane < nm) {
+                int32_t k = run_find(r, ro, lam, ps);
+                const int32_t base_ps = k >= 0 ? r.cnt[ro + k] : 0;
+                k = run_find(r, ro, lam, pd);
+                const int32_t base_pd = k >= 0 ? r.cnt[ro + k] : 0;
+                const int64_t net = seq_net(wi[e], base_ps, base_pd, leav_pd, ent_pd, leav_ps, ent_ps);
+                if (net) atomicAdd(&gacc[i], (unsigned long long)net);
+            }
+        }
+        __syncwarp();
+        // ---- inbound-track crossings over the destination pins -----------
+        nm = warp_collect_movers(dst_dat, dst_off[e], dst_off[e + 1], pos, smv);
+        if (nm > cap) {
+            if (lane == 0) ev_big[atomicAdd(ev_count, 1)] = e;
+        } else if (nm > 0) {
+            uint32_t v[1] = {lane < nm ? (uint32_t)smv[lane] : 0xffffffffu};
+            warp_bitonic_sort<1>(v);
+            const int32_t i = (int32_t)v[0];
+            const int32_t pf = lane < nm ? from[i] : -1, pt = lane < nm ? to[i] : -1;
+            int32_t df = 0, dt = 0;  // net arrivals minus departures of pf / pt before mover a
+            for (int b = 0; b < nm; b++) {
+                const int32_t fb = __shfl_sync(FULL_MASK, pf, b), tb = __shfl_sync(FULL_MASK, pt, b);
+                if (b < lane) {
+                    df += (tb == pf) - (fb == pf);
+                    dt += (tb == pt) - (fb == pt);
+                }
+            }
+            if (lane < nm) {
+                int32_t k = run_find(r, ro, lam, pf);
+                if ((k >= 0 ? r.cin[ro + k] : 0) + df - 1 == 0) emit(ev, 1, pf, i, -1);
+                k = run_find(r, ro, lam, pt);
+                if ((k >= 0 ? r.cin[ro + k] : 0) + dt == 0) emit(ev, 1, pt, i, +1);
+            }
+        }
+        __syncwarp();
+    }
+}
+
 __global__ void k_seq_gains_finish(int64_t M, const int64_t *giso, const unsigned long long *gacc, int64_t *gseq) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < M) gseq[i] = giso[i] + (int64_t)gacc[i];
@@ -1902,7 +1870,6 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
     static int g_ru = resident_grid(c, k_runs_update, 256, 0);
     static int g_me = resident_grid(c, k_mover_edges, 256, 0);
     static int g_ap = resident_grid(c, k_apply_inc, 256, 0);
-    const unsigned g_edges = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(L.E, 256), (int64_t)c.num_sms * 8));
     auto runs_update = [&]() {
         k_runs_update<<<g_ru, 256, 0, c.stream>>>(st.elist, st.ctr + CT_ELIST, st.edirty, L.pin_off, L.pin_dat,
                                                  L.dst_off, L.dst_dat, assign, W.wi, r, conn_d, pinbound, K, st.ndirty,
@@ -2080,36 +2047,33 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
             elist = st.mlist;
             elist_n = st.ctr + CT_MLIST;
         }
-        const unsigned g_list = st.inc ? g_edges : (unsigned)std::max<int64_t>(1, cdiv(L.E, 256));
+        // --- A15 sequence gains + A17 events (replicated: O(sum |e|), no exchange)
+        const int ibits = std::max(1, bitlen((uint64_t)M));
+        EvArgs ev{ibits, pbits, ek, evv, ecount};
         {
-            // replicated on every rank: O(sum |e|), no exchange
             KScope ks(c, "seq_gains", 0.0);
             unsigned long long *gacc = (unsigned long long *)gseq_acc;
             c.zero(gacc, M);
             c.zero(sg_ctr, 2);
+            c.zero(ctr, 4);
+            // size track (and the event count) first: the edge kernel appends
+            k_size_events_dn<<<(unsigned)cdiv(M, 256), 256, 0, c.stream>>>(dM, node, from, to, L.size, ev);
+            DHGP_LAUNCHED(c);
             if (L.E > 0) {
-                k_seq_gains_edge<<<g_list, 256, 0, c.stream>>>(L.E, elist, elist_n, L.pin_off, L.pin_dat, W.wi, r, pos,
-                                                               from, to, gacc, sg_big, sg_ctr, tiers().edge_movers);
+                static int g_re = resident_grid(c, k_round_edges, 256, 0);
+                const unsigned gre = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(L.E, 8), g_re));
+                k_round_edges<<<gre, 256, 0, c.stream>>>(L.E, elist, elist_n, L.pin_off, L.pin_dat, L.dst_off,
+                                                         L.dst_dat, W.wi, r, pos, from, to, gacc, ev, sg_big, sg_ctr,
+                                                         big, ctr, tiers().edge_movers);
                 DHGP_LAUNCHED(c);
                 k_seq_gains_edge_block<<<c.num_sms, 256, 0, c.stream>>>(L.pin_off, L.pin_dat, W.wi, r, pos, from, to,
                                                                          gacc, sg_big, sg_ctr, sg_ctr + 1);
                 DHGP_LAUNCHED(c);
+                k_inbound_events_block<<<c.num_sms, 256, 0, c.stream>>>(L.dst_off, L.dst_dat, r, pos, from, to, ev,
+                                                                         big, ctr, ctr + 2);
+                DHGP_LAUNCHED(c);
             }
             k_seq_gains_finish<<<(unsigned)cdiv(M, 256), 256, 0, c.stream>>>(M, giso, gacc, gseq);
-            DHGP_LAUNCHED(c);
-        }
-        // --- A17 events: key = track | part | move index --------------------
-        const int ibits = std::max(1, bitlen((uint64_t)M));
-        EvArgs ev{ibits, pbits, ek, evv, ecount};
-        c.zero(ctr, 4);
-        k_size_events_dn<<<(unsigned)cdiv(M, 256), 256, 0, c.stream>>>(dM, node, from, to, L.size, ev);
-        DHGP_LAUNCHED(c);
-        if (L.E > 0) {
-            k_inbound_events<<<g_list, 256, 0, c.stream>>>(L.E, elist, elist_n, L.dst_off, L.dst_dat, r, pos, from, to,
-                                                           ev, big, ctr, tiers().edge_movers);
-            DHGP_LAUNCHED(c);
-            k_inbound_events_block<<<c.num_sms, 256, 0, c.stream>>>(L.dst_off, L.dst_dat, r, pos, from, to, ev, big,
-                                                                     ctr, ctr + 2);
             DHGP_LAUNCHED(c);
         }
         // --- A17 select: one CTA for small rounds, T read on device ----------
