@@ -37,18 +37,27 @@ __device__ __forceinline__ void warp_for_pins(const int32_t *inc_dat, int64_t il
         const int incl = warp_incl_scan(len);
         const int total = __shfl_sync(FULL_MASK, incl, 31);
         const int excl = incl - len;
-        for (int s0 = 0; s0 < total; s0 += 32) {
-            const int s = s0 + lane;
-            int owner = 0;
+        // four pins per lane in flight before any is used (the loads are the
+        // latency; the hash inserts are cheap)
+        for (int s0 = 0; s0 < total; s0 += 128) {
+            int32_t oe[4], m[4];
 #pragma unroll
-            for (int step = 16; step > 0; step >>= 1) {
-                int ex = __shfl_sync(FULL_MASK, excl, owner + step);
-                if (ex <= s) owner += step;
+            for (int u = 0; u < 4; u++) {
+                const int s = s0 + u * 32 + lane;
+                int owner = 0;
+#pragma unroll
+                for (int step = 16; step > 0; step >>= 1) {
+                    int ex = __shfl_sync(FULL_MASK, excl, owner + step);
+                    if (ex <= s) owner += step;
+                }
+                oe[u] = __shfl_sync(FULL_MASK, e, owner);
+                const int64_t oplo = __shfl_sync(FULL_MASK, plo, owner);
+                const int oex = __shfl_sync(FULL_MASK, excl, owner);
+                m[u] = s < total ? pin_dat[oplo + (s - oex)] : -1;
             }
-            const int32_t oe = __shfl_sync(FULL_MASK, e, owner);
-            const int64_t oplo = __shfl_sync(FULL_MASK, plo, owner);
-            const int oex = __shfl_sync(FULL_MASK, excl, owner);
-            if (s < total) f(oe, pin_dat[oplo + (s - oex)]);
+#pragma unroll
+            for (int u = 0; u < 4; u++)
+                if (s0 + u * 32 + lane < total) f(oe[u], m[u]);
         }
     }
 }
@@ -792,6 +801,75 @@ __global__ void k_contract_status(int32_t N, int32_t E, const int64_t *rank, con
     status[7] = io[nc];
     status[8] = co[nc];
 }
+
+// Fused per-h-edge contraction (h-edges of <= 128 pin slots): a warp maps
+// each of the src / dst / pin lists through gamma, sorts it in registers
+// (skipped when already strictly ascending: gamma is monotone on lists
+// without a displaced cluster member) and de-duplicates it by ballots
+// (coarsen.py:163-166; hgraph.py:221).  The count pass writes the coarse
+// lengths, the write pass the lists at the scanned offsets.
+template <int K>
+__device__ __forceinline__ int warp_gamma_list(const int32_t *dat, int64_t lo, int len, const int32_t *gamma,
+                                               int32_t *out) {
+    const int lane = lane_id();
+    const uint32_t lt = (1u << lane) - 1u;
+    uint32_t v[K];
+    bool sorted = true;
+#pragma unroll
+    for (int k = 0; k < K; k++) {
+        const int i = k * 32 + lane;
+        v[k] = i < len ? (uint32_t)gamma[dat[lo + i]] : 0xffffffffu;
+    }
+#pragma unroll
+    for (int k = 0; k < K; k++) {
+        const int i = k * 32 + lane;
+        const uint32_t up = __shfl_up_sync(FULL_MASK, v[k], 1);
+        const uint32_t wrap = __shfl_sync(FULL_MASK, v[k > 0 ? k - 1 : 0], 31);
+        const uint32_t prev = lane == 0 ? wrap : up;
+        if (i > 0 && i < len && !(prev < v[k])) sorted = false;
+    }
+    if (!__all_sync(FULL_MASK, sorted)) warp_bitonic_sort<K>(v);
+    int total = 0;
+#pragma unroll
+    for (int k = 0; k < K; k++) {
+        const int i = k * 32 + lane;
+        const uint32_t up = __shfl_up_sync(FULL_MASK, v[k], 1);
+        const uint32_t wrap = __shfl_sync(FULL_MASK, v[k > 0 ? k - 1 : 0], 31);
+        const uint32_t prev = lane == 0 ? wrap : up;
+        const bool head = i < len && (i == 0 || v[k] != prev);
+        const uint32_t bal = __ballot_sync(FULL_MASK, head);
+        if (out && head) out[total + __popc(bal & lt)] = (int32_t)v[k];
+        total += __popc(bal);
+    }
+    return total;
+}
+__device__ __forceinline__ int warp_gamma_any(const int32_t *dat, int64_t lo, int len, const int32_t *gamma,
+                                              int32_t *out) {
+    if (len <= 32) return warp_gamma_list<1>(dat, lo, len, gamma, out);
+    if (len <= 64) return warp_gamma_list<2>(dat, lo, len, gamma, out);
+    return warp_gamma_list<4>(dat, lo, len, gamma, out);
+}
+struct EdgeFam {
+    const int64_t *off;
+    const int32_t *dat;
+    int32_t *cnt;            // count pass
+    const int64_t *out_off;  // write pass
+    int32_t *out;
+};
+__global__ void __launch_bounds__(256) k_contract_edges(int32_t E, const int32_t *gamma, EdgeFam f0, EdgeFam f1,
+                                                        EdgeFam f2, bool write) {
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t e = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id(); e < E; e += nw) {
+#pragma unroll
+        for (int q = 0; q < 3; q++) {
+            const EdgeFam &f = q == 0 ? f0 : (q == 1 ? f1 : f2);
+            const int64_t lo = f.off[e];
+            const int len = (int)(f.off[e + 1] - lo);
+            const int n = warp_gamma_any(f.dat, lo, len, gamma, write ? f.out + f.out_off[e] : nullptr);
+            if (!write && lane_id() == 0) f.cnt[e] = n;
+        }
+    }
+}
 }  // namespace
 
 void contract_count(Ctx &c, DLevel &fine, const int32_t *match, const uint8_t *isrep, DLevel &coarse,
@@ -811,6 +889,27 @@ void contract_count(Ctx &c, DLevel &fine, const int32_t *match, const uint8_t *i
     DHGP_LAUNCHED(c);
     // per-h-edge families: sorted unique gamma image (coarsen.py:163-166)
     KScope kcs(c, "cc_edges");
+    coarse.maxp = fine.maxp;
+    s.fused = fine.maxp <= 128;
+    if (s.fused) {
+        int32_t *cnt = c.alloc<int32_t>(3 * (int64_t)E);
+        if (E > 0) {
+            static int g = resident_grid(c, k_contract_edges, 256, 0);
+            const unsigned gr = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(E, 8), g));
+            k_contract_edges<<<gr, 256, 0, c.stream>>>(E, fine.gamma, EdgeFam{fine.src_off, fine.src_dat, cnt},
+                                                       EdgeFam{fine.dst_off, fine.dst_dat, cnt + E},
+                                                       EdgeFam{fine.pin_off, fine.pin_dat, cnt + 2 * (int64_t)E},
+                                                       false);
+            DHGP_LAUNCHED(c);
+        }
+        coarse.src_off = c.alloc<int64_t>((int64_t)E + 1);
+        coarse.dst_off = c.alloc<int64_t>((int64_t)E + 1);
+        coarse.pin_off = c.alloc<int64_t>((int64_t)E + 1);
+        scan_excl<int32_t>(c, cnt, coarse.src_off, E);
+        scan_excl<int32_t>(c, cnt + E, coarse.dst_off, E);
+        scan_excl<int32_t>(c, cnt + 2 * (int64_t)E, coarse.pin_off, E);
+        c.free(cnt);
+    } else {
     s.tmp_src = c.alloc<int32_t>(fine.Ps);
     s.tmp_dst = c.alloc<int32_t>(fine.Pd);
     s.tmp_pin = c.alloc<int32_t>(fine.U);
@@ -828,6 +927,7 @@ void contract_count(Ctx &c, DLevel &fine, const int32_t *match, const uint8_t *i
     coarse.pin_off = c.alloc<int64_t>((int64_t)E + 1);
     scan_excl<int64_t>(c, cnt, coarse.pin_off, E);
     c.free(cnt);
+    }
     kcs.close();
     KScope kcn(c, "cc_nodes");
     // per-node families: union of the two members' sorted lists
@@ -866,9 +966,21 @@ void contract_write(Ctx &c, DLevel &fine, DLevel &coarse, ContractScratch &s, co
     }
     {
         KScope k2(c, "cw_unique");
-        seg_unique_write(c, E, fine.src_off, s.tmp_src, coarse.src_off, coarse.src_dat);
-        seg_unique_write(c, E, fine.dst_off, s.tmp_dst, coarse.dst_off, coarse.dst_dat);
-        seg_unique_write(c, E, fine.pin_off, s.tmp_pin, coarse.pin_off, coarse.pin_dat);
+        if (s.fused) {
+            if (E > 0) {
+                static int g = resident_grid(c, k_contract_edges, 256, 0);
+                const unsigned gr = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(E, 8), g));
+                k_contract_edges<<<gr, 256, 0, c.stream>>>(
+                    E, fine.gamma, EdgeFam{fine.src_off, fine.src_dat, nullptr, coarse.src_off, coarse.src_dat},
+                    EdgeFam{fine.dst_off, fine.dst_dat, nullptr, coarse.dst_off, coarse.dst_dat},
+                    EdgeFam{fine.pin_off, fine.pin_dat, nullptr, coarse.pin_off, coarse.pin_dat}, true);
+                DHGP_LAUNCHED(c);
+            }
+        } else {
+            seg_unique_write(c, E, fine.src_off, s.tmp_src, coarse.src_off, coarse.src_dat);
+            seg_unique_write(c, E, fine.dst_off, s.tmp_dst, coarse.dst_off, coarse.dst_dat);
+            seg_unique_write(c, E, fine.pin_off, s.tmp_pin, coarse.pin_off, coarse.pin_dat);
+        }
     }
     {
         KScope k2(c, "cw_merge_in");
@@ -923,6 +1035,7 @@ void level_to_stub(Ctx &c, DLevel &L) {
     keep.Pd = L.Pd;
     keep.U = L.U;
     keep.Sin = L.Sin;
+    keep.maxp = L.maxp;
     L.release(c);
     L = keep;
     L.gamma = g;

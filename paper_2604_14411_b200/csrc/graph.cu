@@ -131,6 +131,7 @@ void build_level0(Ctx &c, const DInput &in, DLevel &L) {
     L.dst_dat = in.dst_dat;
     L.size = in.size;
     L.borrowed = true;
+    L.maxp = in.max_edge_pins;
     derive_incidence(c, L);
 }
 

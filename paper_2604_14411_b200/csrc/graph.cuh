@@ -19,6 +19,7 @@ struct DLevel {
     int32_t *src_dat = nullptr, *dst_dat = nullptr, *pin_dat = nullptr, *in_dat = nullptr, *inc_dat = nullptr;
     int32_t *size = nullptr;
     int32_t *gamma = nullptr;  // fine -> coarse map once this level has been contracted
+    int32_t maxp = 0;          // bound on any h-edge's pin slots (src + dst) at this level
     bool borrowed = false;     // src/dst/size belong to a resident input (level 0)
     bool stub = false;         // lists dropped (only gamma kept); rebuilt on demand
     void release(Ctx &c) {

@@ -670,7 +670,11 @@ __global__ void k_merge_count(int64_t nc_cap, const int64_t *d_nc, const int32_t
         int32_t a = ma[cn], b = mb[cn];
         int64_t alo = off[a], na = off[a + 1] - alo;
         if (b < 0) {
-            if (lane == 0) cnt[cn] = na;
+            if (lane == 0) {
+                cnt[cn] = na;
+                // a long list is copied by a block (a warp would serialise on it)
+                if (big_list && na > kMergeBig) big_list[atomicAdd(big_count, 1)] = (int32_t)cn;
+            }
             continue;
         }
         int64_t blo = off[b], nb = off[b + 1] - blo;
@@ -700,6 +704,7 @@ __global__ void k_merge_write(int64_t nc, const int32_t *ma, const int32_t *mb, 
         int32_t *o = out + out_off[cn];
         const int32_t *A = dat + alo;
         if (b < 0) {
+            if (skip_big && na > kMergeBig) continue;
             for (int64_t i = lane; i < na; i += 32) o[i] = A[i];
             continue;
         }
@@ -763,6 +768,7 @@ __global__ void k_merge_count_big(const int32_t *list, const int32_t *count, con
     const int n = *count;
     for (int t = blockIdx.x; t < n; t += gridDim.x) {
         const int32_t cn = list[t], a = ma[cn], b = mb[cn];
+        if (b < 0) continue;  // a long unmerged list: counted by the warp kernel
         const int64_t alo = off[a], na = off[a + 1] - alo, blo = off[b], nb = off[b + 1] - blo;
         const int32_t *sp = dat + (na <= nb ? alo : blo), *lp = dat + (na <= nb ? blo : alo);
         const int64_t ns = na <= nb ? na : nb, nl = na <= nb ? nb : na;
@@ -779,6 +785,12 @@ __global__ void k_merge_write_big(const int32_t *list, const int32_t *count, con
     const int n = *count;
     for (int t = blockIdx.x; t < n; t += gridDim.x) {
         const int32_t cn = list[t], a = ma[cn], b = mb[cn];
+        if (b < 0) {  // a long unmerged list: block copy
+            const int64_t alo = off[a], na = off[a + 1] - alo;
+            int32_t *o = out + out_off[cn];
+            for (int64_t i = threadIdx.x; i < na; i += blockDim.x) o[i] = dat[alo + i];
+            continue;
+        }
         const int64_t alo = off[a], na = off[a + 1] - alo, blo = off[b], nb = off[b + 1] - blo;
         const int32_t *A = dat + alo, *B = dat + blo;
         int32_t *o = out + out_off[cn];
