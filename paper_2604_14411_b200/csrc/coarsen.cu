@@ -82,7 +82,51 @@ struct ScoreArgs {
     int32_t *heavy_count;
     Tiers t;
     int32_t lo, hi;  // this rank's node range (comm.cuh); [0, N) on one GPU
+    // incremental scoring (score_select_inc): only the listed nodes ...
+    const int32_t *list = nullptr;
+    const int32_t *list_count = nullptr;
+    // ... and, for merged clusters, their (neighbour, cluster, hist) pairs
+    // that beat the neighbour's carried choice are emitted as tuples
+    const int32_t *mb = nullptr;     // [N] partner of the cluster's min member (-1 = not merged)
+    const int32_t *rep = nullptr;    // [N] min member (previous-level id)
+    const int64_t *thr_s = nullptr;  // [N] carried score ...
+    const int32_t *thr_p = nullptr;  // [N] ... and pair (previous-level id; -1 = none)
+    int32_t *tup_v = nullptr, *tup_b = nullptr;
+    int64_t *tup_h = nullptr;
+    int32_t *tup_count = nullptr;
+    int64_t tup_cap = 0;
 };
+
+// next node of a persistent scoring loop: [lo, hi) or the listed nodes in it
+// (-1 = done, -2 = skip)
+__device__ __forceinline__ int32_t score_node(const ScoreArgs &a, int idx) {
+    if (a.list) {
+        if (idx >= *a.list_count) return -1;
+        const int32_t n = a.list[idx];
+        return (n < a.lo || n >= a.hi) ? -2 : n;
+    }
+    const int64_t n = (int64_t)a.lo + idx;
+    return n >= a.hi ? -1 : (int32_t)n;
+}
+
+// merged cluster `node`, neighbour m with hist h (size bound already met):
+// a candidate for m when m did not merge and (h, node) outranks m's carried
+// choice (score, pair) — hist desc, then id desc, where ids compare through
+// the clusters' min members (coarse ids are order-isomorphic to them)
+__device__ __forceinline__ void emit_tuple(const ScoreArgs &a, int32_t node, int32_t m, long long h) {
+    if (!a.mb || a.mb[m] >= 0) return;
+    const int32_t tp = a.thr_p[m];
+    if (tp >= 0) {
+        const long long ts = a.thr_s[m];
+        if (!(h > ts || (h == ts && a.rep[node] >= tp))) return;
+    }
+    const int i = atomicAdd(a.tup_count, 1);
+    if (i < a.tup_cap) {
+        a.tup_v[i] = m;
+        a.tup_b[i] = node;
+        a.tup_h[i] = h;
+    }
+}
 
 constexpr int SS_WARPS = 8;
 constexpr int SS_CAP = 1024;   // hash slots per warp (power of two)
@@ -119,10 +163,12 @@ __global__ void __launch_bounds__(SS_WARPS * 32) k_score_warp(ScoreArgs a) {
     int32_t *keys = skeys + w * SS_CAP;
     Acc *vals = svals + w * SS_CAP;
     while (true) {
-        int node = 0;
-        if (lane == 0) node = a.lo + atomicAdd(a.next, 1);
-        node = __shfl_sync(FULL_MASK, node, 0);
-        if (node >= a.hi) break;
+        int idx = 0;
+        if (lane == 0) idx = atomicAdd(a.next, 1);
+        idx = __shfl_sync(FULL_MASK, idx, 0);
+        const int32_t node = score_node(a, idx);
+        if (node == -1) break;
+        if (node < 0) continue;
         const int64_t ilo = a.inc_off[node], ihi = a.inc_off[node + 1];
         if (ihi - ilo > a.t.ss_heavy_inc) {  // hub: a whole block per node
             if (lane == 0) a.heavy_list[atomicAdd(a.heavy_count, 1)] = node;
@@ -171,6 +217,7 @@ __global__ void __launch_bounds__(SS_WARPS * 32) k_score_warp(ScoreArgs a) {
         for (int s = lane; s < SS_CAP; s += 32) {
             int k = keys[s];
             if (k >= 0 && szn + a.size[k] > a.omega) keys[s] = -2;
+            else if (k >= 0) emit_tuple(a, node, k, (long long)vals[s]);
         }
         __syncwarp();
         int32_t best_m = -1;
@@ -284,6 +331,7 @@ __global__ void __launch_bounds__(SH_THREADS) k_score_heavy(ScoreArgs a) {
         for (int s = threadIdx.x; s < SH_CAP; s += SH_THREADS) {
             int k = keys[s];
             if (k >= 0 && szn + a.size[k] > a.omega) keys[s] = -2;
+            else if (k >= 0) emit_tuple(a, node, k, (long long)vals[s]);
         }
         __syncthreads();
         int32_t best_m = -1;
@@ -401,6 +449,7 @@ __global__ void __launch_bounds__(SB_THREADS) k_score_block(ScoreArgs a, long lo
             cval[i] = dense[m];
             dense[m] = -1ll;
             if (szn + a.size[m] > a.omega) touched[i] = -2;
+            else emit_tuple(a, node, m, cval[i]);
         }
         __syncthreads();
         int32_t best_m = -1;
@@ -485,6 +534,68 @@ __global__ void __launch_bounds__(SB_THREADS) k_score_block(ScoreArgs a, long lo
     }
 }
 
+
+// ---- incremental scoring (score_select_inc) ------------------------------
+// kind: 0 merged cluster (rescored), 1 carried pair still a singleton,
+// 2 no carried pair, 3 carried pair merged (rescored unless a tuple wins)
+__global__ void k_inc_base(int32_t N, const int32_t *ma, const int32_t *mb, const int32_t *gamma_prev,
+                           const int32_t *prev_pair, const double *prev_score, uint8_t *kind, int64_t *thr_s,
+                           int32_t *thr_p, unsigned long long *best, int32_t *list, int32_t *list_count) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= N) return;
+    best[c] = 0ull;
+    if (mb[c] >= 0) {
+        kind[c] = 0;
+        thr_p[c] = -1;
+        list[atomicAdd(list_count, 1)] = (int32_t)c;
+        return;
+    }
+    const int32_t f = ma[c], p = prev_pair[f];
+    if (p < 0) {
+        kind[c] = 2;
+        thr_p[c] = -1;
+        return;
+    }
+    thr_s[c] = (int64_t)prev_score[f];
+    thr_p[c] = p;
+    kind[c] = mb[gamma_prev[p]] >= 0 ? 3 : 1;
+}
+// tuples that pass the inbound-union bound compete by (hist, cluster id)
+__global__ void k_inc_tuples(ScoreArgs a, unsigned long long *best) {
+    const int64_t nt = min((int64_t)*a.tup_count, a.tup_cap);
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id(); i < nt; i += nw) {
+        const int32_t v = a.tup_v[i], b = a.tup_b[i];
+        if (warp_union_ok(a, v, b) && lane_id() == 0)
+            atomicMax(&best[v], ((unsigned long long)(a.tup_h[i] + 1) << 32) | (unsigned long long)(uint32_t)b);
+    }
+}
+__global__ void k_inc_finalize(int32_t N, const uint8_t *kind, const int64_t *thr_s, const int32_t *thr_p,
+                               const unsigned long long *best, const int32_t *gamma_prev, const int32_t *tup_count,
+                               int64_t tup_cap, int32_t *pair, double *score, int32_t *list, int32_t *list_count) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= N) return;
+    const int k = kind[c];
+    if (k == 0) return;
+    if ((int64_t)*tup_count > tup_cap) {  // tuples were dropped: rescore
+        list[atomicAdd(list_count, 1)] = (int32_t)c;
+        return;
+    }
+    const unsigned long long b = best[c];
+    if (b) {
+        pair[c] = (int32_t)(uint32_t)(b & 0xffffffffull);
+        score[c] = (double)((long long)(b >> 32) - 1);
+    } else if (k == 1) {
+        pair[c] = gamma_prev[thr_p[c]];
+        score[c] = (double)thr_s[c];
+    } else if (k == 2) {
+        pair[c] = -1;
+        score[c] = 0.0;
+    } else {
+        list[atomicAdd(list_count, 1)] = (int32_t)c;
+    }
+}
+
 __global__ void k_fill_ll(long long *p, long long v, int64_t n) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) p[i] = v;
@@ -517,29 +628,24 @@ void score_scratch_release(Ctx &c, ScoreScratch &s) {
     s = ScoreScratch();
 }
 
-void score_select(Ctx &c, const DLevel &L, const DWeights &W, int64_t omega, int64_t delta, int32_t *pair,
-                  double *score, ScoreScratch &s) {
-    if (L.N == 0) return;
-    KScope ks(c, "score_select", (double)(32.0 * L.N + 8.0 * L.U + 16.0 * L.E + 4.0 * L.Sin), L.N);
+static void score_attrs(Ctx &c) {
     static bool attr = false;
-    if (!attr) {
-        DHGP_CUDA(cudaFuncSetAttribute(k_score_warp<unsigned>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       ss_smem<unsigned>()));
-        DHGP_CUDA(cudaFuncSetAttribute(k_score_warp<unsigned long long>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, ss_smem<unsigned long long>()));
-        DHGP_CUDA(cudaFuncSetAttribute(k_score_heavy<unsigned>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       sh_smem<unsigned>()));
-        DHGP_CUDA(cudaFuncSetAttribute(k_score_heavy<unsigned long long>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, sh_smem<unsigned long long>()));
-        attr = true;
-    }
+    if (attr) return;
+    DHGP_CUDA(cudaFuncSetAttribute(k_score_warp<unsigned>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   ss_smem<unsigned>()));
+    DHGP_CUDA(cudaFuncSetAttribute(k_score_warp<unsigned long long>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   ss_smem<unsigned long long>()));
+    DHGP_CUDA(cudaFuncSetAttribute(k_score_heavy<unsigned>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   sh_smem<unsigned>()));
+    DHGP_CUDA(cudaFuncSetAttribute(k_score_heavy<unsigned long long>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   sh_smem<unsigned long long>()));
+    attr = true;
+}
+
+// the three scoring tiers over all of [a.lo, a.hi) or over a.list
+static void score_tiers(Ctx &c, ScoreArgs a, const DWeights &W, ScoreScratch &s, int32_t n_real) {
     c.zero(s.ctr, 3);
-    ScoreArgs a{L.N, L.inc_off, L.inc_dat, L.pin_off, L.pin_dat, W.wi, L.size, L.in_off, L.in_dat, omega, delta,
-                pair, score, s.ctr, s.big, s.ctr + 1, s.heavy, s.ctr + 2, tiers(), 0, L.N};
-    const Shard sh = shard_of(c.comm, L.N);
-    a.lo = (int32_t)sh.lo;
-    a.hi = (int32_t)sh.hi;
-    const int64_t nmine = std::max<int64_t>(1, sh.hi - sh.lo);
+    const int64_t nmine = a.list ? ((int64_t)1 << 40) : std::max<int64_t>(1, (int64_t)a.hi - a.lo);
     if (W.wsum < (1ll << 32)) {
         static int g32 = resident_grid(c, k_score_warp<unsigned>, SS_WARPS * 32, ss_smem<unsigned>());
         int blocks = (int)std::min<int64_t>(cdiv(nmine, SS_WARPS), g32);
@@ -559,12 +665,85 @@ void score_select(Ctx &c, const DLevel &L, const DWeights &W, int64_t omega, int
     // dense tier: reads the escalation count on device, exits when zero;
     // dense rows have stride s.cap and are restored to -1 after each node
     a.N = (int32_t)s.cap;
-    k_score_block<<<s.blocks, SB_THREADS, 0, c.stream>>>(a, s.dense, s.touched, s.cval, L.N);
+    k_score_block<<<s.blocks, SB_THREADS, 0, c.stream>>>(a, s.dense, s.touched, s.cval, n_real);
     DHGP_LAUNCHED(c);
+}
+
+void score_select(Ctx &c, const DLevel &L, const DWeights &W, int64_t omega, int64_t delta, int32_t *pair,
+                  double *score, ScoreScratch &s) {
+    if (L.N == 0) return;
+    KScope ks(c, "score_select", (double)(32.0 * L.N + 8.0 * L.U + 16.0 * L.E + 4.0 * L.Sin), L.N);
+    score_attrs(c);
+    ScoreArgs a{L.N, L.inc_off, L.inc_dat, L.pin_off, L.pin_dat, W.wi, L.size, L.in_off, L.in_dat, omega, delta,
+                pair, score, s.ctr, s.big, s.ctr + 1, s.heavy, s.ctr + 2, tiers(), 0, L.N};
+    const Shard sh = shard_of(c.comm, L.N);
+    a.lo = (int32_t)sh.lo;
+    a.hi = (int32_t)sh.hi;
+    score_tiers(c, a, W, s, L.N);
     if (sh.on) {  // complete (pair, score) from the other ranks' node ranges
         allgather(c, c.comm, pair, sizeof(int32_t), sh.chunk);
         allgather(c, c.comm, score, sizeof(double), sh.chunk);
     }
+}
+
+bool score_inc_supported(const Ctx &c, const DWeights &W) {
+    return !shard_of(c.comm, 1).on && W.wsum < (1ll << 31) - 2;
+}
+
+void score_select_inc(Ctx &c, const DLevel &L, const DWeights &W, int64_t omega, int64_t delta, int32_t *pair,
+                      double *score, ScoreScratch &s, const ScoreCarry &cy) {
+    const int32_t N = L.N;
+    if (N == 0) return;
+    KScope ks(c, "score_select", (double)(32.0 * L.N + 8.0 * L.U + 16.0 * L.E + 4.0 * L.Sin), L.N);
+    score_attrs(c);
+    uint8_t *kind = c.alloc<uint8_t>(N);
+    int64_t *thr_s = c.alloc<int64_t>(N);
+    int32_t *thr_p = c.alloc<int32_t>(N);
+    unsigned long long *best = c.alloc<unsigned long long>(N);
+    int32_t *list = c.alloc<int32_t>(N), *list2 = c.alloc<int32_t>(N), *lc = c.alloc<int32_t>(3);
+    const int64_t cap = 8 * (int64_t)N + (1 << 20);
+    int32_t *tv = c.alloc<int32_t>(cap), *tb = c.alloc<int32_t>(cap);
+    int64_t *th = c.alloc<int64_t>(cap);
+    c.zero(lc, 3);
+    k_inc_base<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(N, cy.ma, cy.mb, cy.gamma_prev, cy.prev_pair,
+                                                            cy.prev_score, kind, thr_s, thr_p, best, list, lc);
+    DHGP_LAUNCHED(c);
+    // pass 1: the merged clusters, emitting their beating neighbour tuples
+    ScoreArgs a{N, L.inc_off, L.inc_dat, L.pin_off, L.pin_dat, W.wi, L.size, L.in_off, L.in_dat, omega, delta,
+                pair, score, s.ctr, s.big, s.ctr + 1, s.heavy, s.ctr + 2, tiers(), 0, N};
+    a.list = list;
+    a.list_count = lc;
+    a.mb = cy.mb;
+    a.rep = cy.ma;
+    a.thr_s = thr_s;
+    a.thr_p = thr_p;
+    a.tup_v = tv;
+    a.tup_b = tb;
+    a.tup_h = th;
+    a.tup_count = lc + 2;
+    a.tup_cap = cap;
+    score_tiers(c, a, W, s, N);
+    static int gt = resident_grid(c, k_inc_tuples, 256, 0);
+    k_inc_tuples<<<gt, 256, 0, c.stream>>>(a, best);
+    DHGP_LAUNCHED(c);
+    k_inc_finalize<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(N, kind, thr_s, thr_p, best, cy.gamma_prev, lc + 2,
+                                                                cap, pair, score, list2, lc + 1);
+    DHGP_LAUNCHED(c);
+    // pass 2: singletons whose carried pair merged and no cluster outranks it
+    ScoreArgs b{N, L.inc_off, L.inc_dat, L.pin_off, L.pin_dat, W.wi, L.size, L.in_off, L.in_dat, omega, delta,
+                pair, score, s.ctr, s.big, s.ctr + 1, s.heavy, s.ctr + 2, tiers(), 0, N};
+    b.list = list2;
+    b.list_count = lc + 1;
+    score_tiers(c, b, W, s, N);
+    if (trace_enabled()) {
+        int32_t h[3];
+        c.d2h(h, lc, 3);
+        c.sync();
+        fprintf(stderr, "scoreinc N %d merged %d rescored %d tuples %d\n", N, h[0], h[1], h[2]);
+    }
+    for (void *q : {(void *)kind, (void *)thr_s, (void *)thr_p, (void *)best, (void *)list, (void *)list2, (void *)lc,
+                    (void *)tv, (void *)tb, (void *)th})
+        c.free(q);
 }
 
 // ===========================================================================
@@ -992,7 +1171,11 @@ void contract_write(Ctx &c, DLevel &fine, DLevel &coarse, ContractScratch &s, co
         merge_union_write(c, st.nc, s.ma, s.mb, fine.inc_off, fine.inc_dat, coarse.inc_off, coarse.inc_dat,
                           s.big_inc, s.big_cnt + 1);
     }
+    int32_t *ma = s.ma, *mb = s.mb;
+    s.ma = s.mb = nullptr;
     contract_release(c, s);
+    s.ma = ma;
+    s.mb = mb;
 }
 
 namespace {
@@ -1040,6 +1223,12 @@ void level_to_stub(Ctx &c, DLevel &L) {
     L = keep;
     L.gamma = g;
     L.stub = true;
+}
+
+void contract_release_members(Ctx &c, ContractScratch &s) {
+    c.free(s.ma);
+    c.free(s.mb);
+    s.ma = s.mb = nullptr;
 }
 
 void contract_release(Ctx &c, ContractScratch &s) {

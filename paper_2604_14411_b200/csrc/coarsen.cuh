@@ -22,6 +22,26 @@ void score_scratch_release(Ctx &c, ScoreScratch &s);
 void score_select(Ctx &c, const DLevel &L, const DWeights &W, int64_t omega, int64_t delta, int32_t *pair,
                   double *score, ScoreScratch &s);
 
+// Incremental scoring of the next level.  A node that did not merge keeps
+// its histogram entries for every neighbour that did not merge (same h-edges,
+// same members) and the size / inbound verdicts for them, so its first valid
+// candidate can only change through the new clusters: each merged cluster is
+// rescored and its histogram emits (neighbour, cluster, hist) when that
+// outranks the neighbour's carried (score, pair); the best such tuple passing
+// the inbound-union bound wins, else the carried pair stands.  When the
+// carried pair itself merged and no cluster outranks it, the node is
+// rescored (its next candidate is unknown).  Bit-identical to score_select.
+struct ScoreCarry {
+    const int32_t *prev_pair = nullptr;   // previous level's pair / score (previous-level ids)
+    const double *prev_score = nullptr;
+    const int32_t *gamma_prev = nullptr;  // previous level -> this level
+    const int32_t *ma = nullptr;          // this level's node -> its min member (previous-level id)
+    const int32_t *mb = nullptr;          // ... -> the other member, -1 if not merged
+};
+bool score_inc_supported(const Ctx &c, const DWeights &W);
+void score_select_inc(Ctx &c, const DLevel &L, const DWeights &W, int64_t omega, int64_t delta, int32_t *pair,
+                      double *score, ScoreScratch &s, const ScoreCarry &carry);
+
 // Per-level status words, filled on device and read with ONE host sync.
 struct LevelStatus {
     int64_t moved;     // nodes with match != self (= 2 x matched pairs)
@@ -59,6 +79,9 @@ void contract_count(Ctx &c, DLevel &fine, const int32_t *match, const uint8_t *i
                     ContractScratch &s, int64_t *d_status);
 void contract_write(Ctx &c, DLevel &fine, DLevel &coarse, ContractScratch &s, const LevelStatus &st);
 void contract_release(Ctx &c, ContractScratch &s);
+// contract_write leaves s.ma / s.mb (cluster members, for ScoreCarry); the
+// caller frees them with this
+void contract_release_members(Ctx &c, ContractScratch &s);
 
 // match / isrep of a stored contraction, recovered from its gamma (coarse
 // ids are ranks of each cluster's minimum member): used to rebuild levels

@@ -264,6 +264,7 @@ static void rebuild_levels(Ctx &c, std::vector<DLevel> &levels, size_t hi) {
         c.d2h((int64_t *)&st, status, kStatusWords);
         c.sync();
         contract_write(c, f, coarse, cs, st);
+        contract_release_members(c, cs);
         coarse.gamma = next.gamma;  // the stored map to the level above
         next.gamma = nullptr;
         next.release(c);
@@ -334,6 +335,19 @@ static void run_partition(Ctx &c, const DInput &in, const dhgp_config &cfg, Part
     // no pair is discarded (driver.py:104-105).
     ScoreScratch sscr;
     int64_t *status = nullptr;
+    // incremental scoring carries the previous level's choices and clusters
+    const char *fs = getenv("DHGP_FULL_SCORE");  // tests: the full rescoring every level
+    const bool inc_score = score_inc_supported(c, W) && !(fs && fs[0] == '1');
+    int32_t *prev_pair = nullptr, *cma = nullptr, *cmb = nullptr;
+    double *prev_score = nullptr;
+    auto free_carry = [&]() {
+        c.free(prev_pair);
+        c.free(prev_score);
+        c.free(cma);
+        c.free(cmb);
+        prev_pair = cma = cmb = nullptr;
+        prev_score = nullptr;
+    };
     // bytes of non-checkpoint levels kept whole (no rebuild during
     // uncoarsening): up to 40% of the memory free at this point
     size_t kept = 0, keep_budget = 0;
@@ -358,7 +372,17 @@ static void run_partition(Ctx &c, const DInput &in, const dhgp_config &cfg, Part
             double *score = c.alloc<double>(ncap);
             uint8_t *isrep = c.alloc<uint8_t>(n);
             c.zero(status, kStatusWords);
-            score_select(c, levels.back(), W, omega, delta, pair, score, sscr);
+            if (inc_score && prev_pair) {
+                ScoreCarry cy;
+                cy.prev_pair = prev_pair;
+                cy.prev_score = prev_score;
+                cy.gamma_prev = levels[levels.size() - 2].gamma;
+                cy.ma = cma;
+                cy.mb = cmb;
+                score_select_inc(c, levels.back(), W, omega, delta, pair, score, sscr, cy);
+            } else {
+                score_select(c, levels.back(), W, omega, delta, pair, score, sscr);
+            }
             launch_matching(c, n, pair, score, match, isrep, claim, status);
             DLevel coarse;
             ContractScratch cs;
@@ -424,10 +448,20 @@ static void run_partition(Ctx &c, const DInput &in, const dhgp_config &cfg, Part
                 ev.c_node_size = hsz.data();
                 obs(&ev, user);
             }
-            c.free(pair);
+            free_carry();
+            if (!stop && inc_score) {  // this level's choices and clusters feed the next scoring
+                prev_pair = pair;
+                prev_score = score;
+                cma = cs.ma;
+                cmb = cs.mb;
+                cs.ma = cs.mb = nullptr;
+            } else {
+                c.free(pair);
+                c.free(score);
+                contract_release_members(c, cs);
+            }
             c.free(match);
             c.free(claim);
-            c.free(score);
             c.free(isrep);
             if (stop) break;
             // memory: every kCheckpoint-th level stays whole; the others stay
@@ -443,12 +477,14 @@ static void run_partition(Ctx &c, const DInput &in, const dhgp_config &cfg, Part
             }
         }
     } catch (...) {
+        free_carry();
         for (auto &L : levels) L.release(c);
         W.release(c);
         score_scratch_release(c, sscr);
         c.free(status);
         throw;
     }
+    free_carry();
     score_scratch_release(c, sscr);
     c.free(status);
     const double t1 = now_ms();

@@ -338,11 +338,12 @@ def test_c2_stepwise_levels_match_oracle():
     assert all(r["bit_exact"] for r in out["coarsen"] + out["refine"]), out
 
 
-def test_full_and_incremental_refinement_agree(monkeypatch):
-    """DHGP_FULL_REFINE=1 recomputes every run list and proposal each round
-    (the direct restatement); the default incremental mode recomputes only
-    what moves and projections dirtied.  Both must equal the oracle, and on
-    the full-size C2 workload each other."""
+def test_full_and_incremental_paths_agree(monkeypatch):
+    """DHGP_FULL_REFINE=1 / DHGP_FULL_SCORE=1 recompute every run list,
+    proposal and candidate score on every round / level (the direct
+    restatement); the default incremental paths recompute only what moves,
+    projections and merges dirtied.  Both must equal the oracle, and on the
+    full-size C2 workload each other."""
     from paper_2604_14411_b200 import workloads as W
 
     rs = np.random.RandomState(4242)
@@ -353,8 +354,10 @@ def test_full_and_incremental_refinement_agree(monkeypatch):
                              omega=int(rs.choice([4, 16, 64])), delta_slack=int(rs.randint(0, 30)))
         cases.append((g, c.max_size, c.max_inbound, int(rs.choice([1, 2, 8]))))
     cases.append((graph(W.layered_snn(5, 300, fanout=32, window=96, seed=9)), 256, 4096, 8))
+    cases.append((graph(W.layered_snn(8, 400, fanout=48, window=128, seed=3)), 512, 1024, 8))
     for mode in ("1", "0"):
         monkeypatch.setenv("DHGP_FULL_REFINE", mode)
+        monkeypatch.setenv("DHGP_FULL_SCORE", mode)
         for g, om, de, mr in cases:
             assert_same_as_oracle(g, om, de, max_rounds=mr)
     arrs, om, de, _ = W.make_config("C2")
@@ -362,6 +365,7 @@ def test_full_and_incremental_refinement_agree(monkeypatch):
     res = []
     for mode in ("1", "0"):
         monkeypatch.setenv("DHGP_FULL_REFINE", mode)
+        monkeypatch.setenv("DHGP_FULL_SCORE", mode)
         res.append(run_gpu(g, om, de, max_levels=1 << 20)[:2])
     (p1, s1), (p2, s2) = res
     assert np.array_equal(p1.assign, p2.assign) and s1.to_dict() == s2.to_dict()
