@@ -13,61 +13,61 @@ constexpr int SC_BT = 256;
 constexpr int SC_IPT = 16;
 constexpr int SC_TILE = SC_BT * SC_IPT;
 
-// block-level exclusive scan of one value per thread; returns the exclusive
-// prefix and writes the block total into *total (all threads).
-__device__ __forceinline__ int64_t block_excl_scan(int64_t v, int64_t *sh, int64_t *total) {
-    const int lane = lane_id(), w = warp_id(), nw = blockDim.x >> 5;
-    int64_t incl = warp_incl_scan(v);
-    if (lane == 31) sh[w] = incl;
-    __syncthreads();
-    if (w == 0) {
-        int64_t x = lane < nw ? sh[lane] : 0;
-        int64_t xi = warp_incl_scan(x);
-        if (lane < nw) sh[lane] = xi - x;
-        if (lane == nw - 1) sh[32] = xi;
+// One tile, warp-striped: warp w owns elements [w*512, (w+1)*512) of the
+// tile, lane l holds element r*32 + l of it in v[r] (coalesced loads); the
+// scan runs over registers with shuffles (no shared-memory transpose).
+// v[] becomes the exclusive prefix within the tile; returns the tile total.
+template <class T>
+__device__ __forceinline__ int64_t tile_excl_scan(const T *in, int64_t n, int64_t base, int64_t (&v)[SC_IPT],
+                                                  int64_t *sh) {
+    const int lane = lane_id(), w = warp_id();
+    const int64_t wb = base + (int64_t)w * (SC_IPT * 32);
+#pragma unroll
+    for (int r = 0; r < SC_IPT; r++) {
+        const int64_t idx = wb + r * 32 + lane;
+        v[r] = idx < n ? (int64_t)in[idx] : 0;
     }
+    int64_t carry = 0;
+#pragma unroll
+    for (int r = 0; r < SC_IPT; r++) {
+        const int64_t x = warp_incl_scan(v[r]);
+        const int64_t e = x - v[r] + carry;
+        carry += __shfl_sync(FULL_MASK, x, 31);
+        v[r] = e;
+    }
+    if (lane == 0) sh[w] = carry;
     __syncthreads();
-    int64_t r = incl - v + sh[w];
-    *total = sh[32];
-    __syncthreads();
-    return r;
+    int64_t before = 0, tot = 0;
+#pragma unroll
+    for (int j = 0; j < SC_BT / 32; j++) {
+        const int64_t t = sh[j];
+        if (j < w) before += t;
+        tot += t;
+    }
+#pragma unroll
+    for (int r = 0; r < SC_IPT; r++) v[r] += before;
+    return tot;
+}
+__device__ __forceinline__ void tile_store(int64_t *out, int64_t n, int64_t base, const int64_t (&v)[SC_IPT],
+                                           int64_t add) {
+    const int lane = lane_id(), w = warp_id();
+    const int64_t wb = base + (int64_t)w * (SC_IPT * 32);
+#pragma unroll
+    for (int r = 0; r < SC_IPT; r++) {
+        const int64_t idx = wb + r * 32 + lane;
+        if (idx < n) out[idx] = v[r] + add;
+    }
 }
 
 template <class T>
-__global__ void k_scan_final(const T *in, int64_t n, const int64_t *partial, int64_t *out) {
-    __shared__ int64_t sh[33];
-    __shared__ int64_t buf[SC_TILE];
-    int64_t base = (int64_t)blockIdx.x * SC_TILE;
-    // striped coalesced load into smem
-#pragma unroll
-    for (int i = 0; i < SC_IPT; i++) {
-        int64_t idx = base + (int64_t)i * SC_BT + threadIdx.x;
-        buf[i * SC_BT + threadIdx.x] = idx < n ? (int64_t)in[idx] : 0;
-    }
-    __syncthreads();
-    int64_t loc[SC_IPT];
-    int64_t s = 0;
-#pragma unroll
-    for (int i = 0; i < SC_IPT; i++) {
-        loc[i] = buf[threadIdx.x * SC_IPT + i];
-        s += loc[i];
-    }
-    int64_t tot;
-    int64_t ex = block_excl_scan(s, sh, &tot);
-    int64_t run = ex + (partial ? partial[blockIdx.x] : 0);
-#pragma unroll
-    for (int i = 0; i < SC_IPT; i++) {
-        buf[threadIdx.x * SC_IPT + i] = run;
-        run += loc[i];
-    }
-    __syncthreads();
-#pragma unroll
-    for (int i = 0; i < SC_IPT; i++) {
-        int64_t idx = base + (int64_t)i * SC_BT + threadIdx.x;
-        if (idx < n) out[idx] = buf[i * SC_BT + threadIdx.x];
-    }
-    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0)
-        out[n] = (partial ? partial[blockIdx.x] : 0) + tot;
+__global__ void __launch_bounds__(SC_BT) k_scan_final(const T *in, int64_t n, const int64_t *partial, int64_t *out) {
+    __shared__ int64_t sh[SC_BT / 32];
+    const int64_t base = (int64_t)blockIdx.x * SC_TILE;
+    int64_t v[SC_IPT];
+    const int64_t tot = tile_excl_scan(in, n, base, v, sh);
+    const int64_t add = partial ? partial[blockIdx.x] : 0;
+    tile_store(out, n, base, v, add);
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) out[n] = add + tot;
 }
 // Single-pass exclusive scan with decoupled look-back: each tile publishes
 // its aggregate, then its inclusive prefix once known; a tile's prefix is
@@ -78,26 +78,12 @@ constexpr uint32_t kAggBit = 1u, kIncBit = 2u;
 template <class T>
 __global__ void __launch_bounds__(SC_BT) k_scan_onepass(const T *in, int64_t n, int64_t *out, uint32_t *flag,
                                                         int64_t *agg, int64_t *inc, uint32_t epoch) {
-    __shared__ int64_t sh[33];
-    __shared__ int64_t buf[SC_TILE];
+    __shared__ int64_t sh[SC_BT / 32];
     __shared__ int64_t s_prefix;
     const int64_t tile = blockIdx.x;
     const int64_t base = tile * SC_TILE;
-#pragma unroll
-    for (int i = 0; i < SC_IPT; i++) {
-        const int64_t idx = base + (int64_t)i * SC_BT + threadIdx.x;
-        buf[i * SC_BT + threadIdx.x] = idx < n ? (int64_t)in[idx] : 0;
-    }
-    __syncthreads();
-    int64_t loc[SC_IPT];
-    int64_t s = 0;
-#pragma unroll
-    for (int i = 0; i < SC_IPT; i++) {
-        loc[i] = buf[threadIdx.x * SC_IPT + i];
-        s += loc[i];
-    }
-    int64_t tot;
-    const int64_t ex = block_excl_scan(s, sh, &tot);
+    int64_t v[SC_IPT];
+    const int64_t tot = tile_excl_scan(in, n, base, v, sh);
     if (threadIdx.x < 32) {
         const int lane = lane_id();
         int64_t prefix = 0;
@@ -143,18 +129,7 @@ __global__ void __launch_bounds__(SC_BT) k_scan_onepass(const T *in, int64_t n, 
         if (lane == 0) s_prefix = prefix;
     }
     __syncthreads();
-    int64_t run = ex + s_prefix;
-#pragma unroll
-    for (int i = 0; i < SC_IPT; i++) {
-        buf[threadIdx.x * SC_IPT + i] = run;
-        run += loc[i];
-    }
-    __syncthreads();
-#pragma unroll
-    for (int i = 0; i < SC_IPT; i++) {
-        const int64_t idx = base + (int64_t)i * SC_BT + threadIdx.x;
-        if (idx < n) out[idx] = buf[i * SC_BT + threadIdx.x];
-    }
+    tile_store(out, n, base, v, s_prefix);
     if (tile == gridDim.x - 1 && threadIdx.x == 0) out[n] = s_prefix + tot;
 }
 
