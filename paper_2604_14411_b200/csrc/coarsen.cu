@@ -560,14 +560,29 @@ __global__ void k_inc_base(int32_t N, const int32_t *ma, const int32_t *mb, cons
     thr_p[c] = p;
     kind[c] = mb[gamma_prev[p]] >= 0 ? 3 : 1;
 }
-// tuples that pass the inbound-union bound compete by (hist, cluster id)
-__global__ void k_inc_tuples(ScoreArgs a, unsigned long long *best) {
+// tuples that pass the inbound-union bound compete by (hist, cluster id):
+// thread per tuple when |in(v)| + |in(b)| <= delta (no search needed), the
+// others are listed for a warp each
+__device__ __forceinline__ unsigned long long tuple_key(long long h, int32_t b) {
+    return ((unsigned long long)(h + 1) << 32) | (unsigned long long)(uint32_t)b;
+}
+__global__ void k_inc_tuples_quick(ScoreArgs a, unsigned long long *best, int32_t *hard, int32_t *hard_count) {
     const int64_t nt = min((int64_t)*a.tup_count, a.tup_cap);
-    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
-    for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id(); i < nt; i += nw) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nt; i += (int64_t)gridDim.x * blockDim.x) {
         const int32_t v = a.tup_v[i], b = a.tup_b[i];
-        if (warp_union_ok(a, v, b) && lane_id() == 0)
-            atomicMax(&best[v], ((unsigned long long)(a.tup_h[i] + 1) << 32) | (unsigned long long)(uint32_t)b);
+        if ((a.in_off[v + 1] - a.in_off[v]) + (a.in_off[b + 1] - a.in_off[b]) <= a.delta)
+            atomicMax(&best[v], tuple_key(a.tup_h[i], b));
+        else
+            hard[atomicAdd(hard_count, 1)] = (int32_t)i;
+    }
+}
+__global__ void k_inc_tuples(ScoreArgs a, unsigned long long *best, const int32_t *hard, const int32_t *hard_count) {
+    const int64_t nt = *hard_count;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id(); t < nt; t += nw) {
+        const int32_t i = hard[t];
+        const int32_t v = a.tup_v[i], b = a.tup_b[i];
+        if (warp_union_ok(a, v, b) && lane_id() == 0) atomicMax(&best[v], tuple_key(a.tup_h[i], b));
     }
 }
 __global__ void k_inc_finalize(int32_t N, const uint8_t *kind, const int64_t *thr_s, const int32_t *thr_p,
@@ -700,11 +715,11 @@ void score_select_inc(Ctx &c, const DLevel &L, const DWeights &W, int64_t omega,
     int64_t *thr_s = c.alloc<int64_t>(N);
     int32_t *thr_p = c.alloc<int32_t>(N);
     unsigned long long *best = c.alloc<unsigned long long>(N);
-    int32_t *list = c.alloc<int32_t>(N), *list2 = c.alloc<int32_t>(N), *lc = c.alloc<int32_t>(3);
+    int32_t *list = c.alloc<int32_t>(N), *list2 = c.alloc<int32_t>(N), *lc = c.alloc<int32_t>(4);
     const int64_t cap = 8 * (int64_t)N + (1 << 20);
-    int32_t *tv = c.alloc<int32_t>(cap), *tb = c.alloc<int32_t>(cap);
+    int32_t *tv = c.alloc<int32_t>(cap), *tb = c.alloc<int32_t>(cap), *hard = c.alloc<int32_t>(cap);
     int64_t *th = c.alloc<int64_t>(cap);
-    c.zero(lc, 3);
+    c.zero(lc, 4);
     k_inc_base<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(N, cy.ma, cy.mb, cy.gamma_prev, cy.prev_pair,
                                                             cy.prev_score, kind, thr_s, thr_p, best, list, lc);
     DHGP_LAUNCHED(c);
@@ -723,8 +738,11 @@ void score_select_inc(Ctx &c, const DLevel &L, const DWeights &W, int64_t omega,
     a.tup_count = lc + 2;
     a.tup_cap = cap;
     score_tiers(c, a, W, s, N);
+    static int gq = resident_grid(c, k_inc_tuples_quick, 256, 0);
+    k_inc_tuples_quick<<<gq, 256, 0, c.stream>>>(a, best, hard, lc + 3);
+    DHGP_LAUNCHED(c);
     static int gt = resident_grid(c, k_inc_tuples, 256, 0);
-    k_inc_tuples<<<gt, 256, 0, c.stream>>>(a, best);
+    k_inc_tuples<<<gt, 256, 0, c.stream>>>(a, best, hard, lc + 3);
     DHGP_LAUNCHED(c);
     k_inc_finalize<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(N, kind, thr_s, thr_p, best, cy.gamma_prev, lc + 2,
                                                                 cap, pair, score, list2, lc + 1);
@@ -742,7 +760,7 @@ void score_select_inc(Ctx &c, const DLevel &L, const DWeights &W, int64_t omega,
         fprintf(stderr, "scoreinc N %d merged %d rescored %d tuples %d\n", N, h[0], h[1], h[2]);
     }
     for (void *q : {(void *)kind, (void *)thr_s, (void *)thr_p, (void *)best, (void *)list, (void *)list2, (void *)lc,
-                    (void *)tv, (void *)tb, (void *)th})
+                    (void *)tv, (void *)tb, (void *)th, (void *)hard})
         c.free(q);
 }
 

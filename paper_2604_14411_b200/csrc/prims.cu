@@ -680,7 +680,16 @@ __global__ void k_merge_write(int64_t nc, const int32_t *ma, const int32_t *mb, 
         const int32_t *A = dat + alo;
         if (b < 0) {
             if (skip_big && na > kMergeBig) continue;
-            for (int64_t i = lane; i < na; i += 32) o[i] = A[i];
+            // four loads in flight per lane before the stores
+            int64_t i = lane;
+            for (; i + 96 < na; i += 128) {
+                const int32_t x0 = A[i], x1 = A[i + 32], x2 = A[i + 64], x3 = A[i + 96];
+                o[i] = x0;
+                o[i + 32] = x1;
+                o[i + 64] = x2;
+                o[i + 96] = x3;
+            }
+            for (; i < na; i += 32) o[i] = A[i];
             continue;
         }
         int64_t blo = off[b], nb = off[b + 1] - blo;

@@ -679,23 +679,40 @@ __global__ void __launch_bounds__(256) k_propose_hub(ProposeArgs a, long long *h
     __shared__ int32_t r_p[8];
     __shared__ int s_last, s_nf;
     __shared__ int32_t s_f[2];
+    __shared__ int32_t s_pref[HUB_MAX + 1], s_wt[8];
     const int nh = min(*a.hub_count, HUB_MAX);
+    if (nh == 0) return;
     const int w = warp_id(), lane = lane_id(), nw = 8;
     const int K = a.K;
-    for (int64_t t = blockIdx.x;; t += gridDim.x) {
-        int h = -1;
-        int64_t chunk = 0, base = 0, nch = 0;
-        for (int j = 0; j < nh; j++) {
-            const int32_t n = a.hub_list[j];
-            nch = cdiv_dev(a.inc_off[n + 1] - a.inc_off[n], (int64_t)HUB_CHUNK);
-            if (t < base + nch) {
-                h = j;
-                chunk = t - base;
-                break;
-            }
-            base += nch;
+    // work items = (hub, chunk): chunk counts of the hubs, block-scanned
+    {
+        int32_t cnt = 0;
+        if ((int)threadIdx.x < nh) {
+            const int32_t n = a.hub_list[threadIdx.x];
+            cnt = (int32_t)cdiv_dev(a.inc_off[n + 1] - a.inc_off[n], (int64_t)HUB_CHUNK);
         }
-        if (h < 0) break;
+        const int32_t incl = warp_incl_scan(cnt);
+        if (lane == 31) s_wt[w] = incl;
+        __syncthreads();
+        int32_t before = 0;
+        for (int j = 0; j < w; j++) before += s_wt[j];
+        s_pref[threadIdx.x + 1] = before + incl;
+        if (threadIdx.x == 0) s_pref[0] = 0;
+        __syncthreads();
+    }
+    const int64_t items = s_pref[nh];
+    for (int64_t t = blockIdx.x; t < items; t += gridDim.x) {
+        int lo = 0, hi = nh;  // the hub h with s_pref[h] <= t < s_pref[h + 1]
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (s_pref[mid] <= t)
+                lo = mid;
+            else
+                hi = mid;
+        }
+        const int h = lo;
+        const int64_t chunk = t - s_pref[h];
+        const int64_t nch = s_pref[h + 1] - s_pref[h];
         const int32_t node = a.hub_list[h];
         const int64_t ilo = a.inc_off[node] + chunk * HUB_CHUNK;
         const int64_t ihi = min(a.inc_off[node + 1], ilo + (int64_t)HUB_CHUNK);
