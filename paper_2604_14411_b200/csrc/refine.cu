@@ -881,7 +881,13 @@ struct EvArgs {
     uint64_t *key;
     uint32_t *val;
     unsigned long long *count;
+    // inbound track, pre-aggregated per move: _track_violations only reads
+    // the delta sum of each (part, move) group, and move i's inbound
+    // crossings all sit at its source (1 -> 0) or target (0 -> 1) part
+    int32_t *in_from = nullptr, *in_to = nullptr;
 };
+__device__ __forceinline__ void inbound_leave(const EvArgs &ev, int32_t i) { atomicSub(&ev.in_from[i], 1); }
+__device__ __forceinline__ void inbound_enter(const EvArgs &ev, int32_t i) { atomicAdd(&ev.in_to[i], 1); }
 __device__ __forceinline__ void emit(const EvArgs &ev, uint64_t track, int32_t p, int32_t i, int32_t d) {
     unsigned long long s = atomicAdd(ev.count, 1ull);
     ev.key[s] = (track << (ev.pbits + ev.ibits)) | ((uint64_t)(uint32_t)p << ev.ibits) | (uint64_t)(uint32_t)i;
@@ -940,7 +946,7 @@ __global__ void k_inbound_events_block(const int64_t *dst_off, const int32_t *ds
                     sdc[nd] = f >= 0 ? r.cin[lo + f] : 0;
                     nd++;
                 }
-                if (--sdc[k] == 0) emit(ev, 1, pf, i, -1);
+                if (--sdc[k] == 0) inbound_leave(ev, i);
                 for (k = 0; k < nd && sdp[k] != pt; k++) {
                 }
                 if (k == nd) {
@@ -949,7 +955,7 @@ __global__ void k_inbound_events_block(const int64_t *dst_off, const int32_t *ds
                     sdc[nd] = f >= 0 ? r.cin[lo + f] : 0;
                     nd++;
                 }
-                if (++sdc[k] == 1) emit(ev, 1, pt, i, +1);
+                if (++sdc[k] == 1) inbound_enter(ev, i);
             }
         }
         __syncthreads();
@@ -1477,15 +1483,23 @@ __global__ void __launch_bounds__(256) k_round_edges(int32_t E, const int32_t *e
             }
             if (lane < nm) {
                 int32_t k = run_find(r, ro, lam, pf);
-                if ((k >= 0 ? r.cin[ro + k] : 0) + df - 1 == 0) emit(ev, 1, pf, i, -1);
+                if ((k >= 0 ? r.cin[ro + k] : 0) + df - 1 == 0) inbound_leave(ev, i);
                 k = run_find(r, ro, lam, pt);
-                if ((k >= 0 ? r.cin[ro + k] : 0) + dt == 0) emit(ev, 1, pt, i, +1);
+                if ((k >= 0 ? r.cin[ro + k] : 0) + dt == 0) inbound_enter(ev, i);
             }
         }
         __syncwarp();
     }
 }
 
+// the inbound track's aggregated (part, move) groups as events
+__global__ void k_inbound_emit(int64_t M, const int32_t *from, const int32_t *to, EvArgs ev) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= M) return;
+    const int32_t a = ev.in_from[i], b = ev.in_to[i];
+    if (a) emit(ev, 1, from[i], (int32_t)i, a);
+    if (b) emit(ev, 1, to[i], (int32_t)i, b);
+}
 __global__ void k_seq_gains_finish(int64_t M, const int64_t *giso, const unsigned long long *gacc, int64_t *gseq) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < M) gseq[i] = giso[i] + (int64_t)gacc[i];
@@ -1847,7 +1861,7 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
     int32_t *target = st.target;
     int64_t *gain = st.gain;
     unsigned long long *conn_d = st.conn;
-    // ---- per-level buffers (capacities: N moves, 2N + 2 S_in events) ------
+    // ---- per-level buffers (capacities: N moves, 4N events) -----------------
     int32_t *tmp_parts = max_edge_pins > 128 ? c.alloc<int32_t>(L.U) : nullptr;
     uint8_t *flags = c.alloc<uint8_t>(N);
     int64_t *mpos = c.alloc<int64_t>((int64_t)N + 1);
@@ -1859,8 +1873,9 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
     uint32_t *mv = c.alloc<uint32_t>(N), *mvt = c.alloc<uint32_t>(N);
     int32_t *node = c.alloc<int32_t>(N), *from = c.alloc<int32_t>(N), *to = c.alloc<int32_t>(N);
     int64_t *giso = c.alloc<int64_t>(N), *gseq = c.alloc<int64_t>(N), *gseq_acc = c.alloc<int64_t>(N);
+    int32_t *ev_from = c.alloc<int32_t>(N), *ev_to = c.alloc<int32_t>(N);
     int32_t *sg_big = c.alloc<int32_t>(L.E), *sg_ctr = c.alloc<int32_t>(2);
-    const int64_t ecap = 2 * (int64_t)N + 2 * L.Sin;
+    const int64_t ecap = 4 * (int64_t)N + 4;  // 2 size + 2 aggregated inbound events per move
     uint64_t *ek = c.alloc<uint64_t>(ecap), *ekt = c.alloc<uint64_t>(ecap);
     uint32_t *evv = c.alloc<uint32_t>(ecap), *evt = c.alloc<uint32_t>(ecap);
     unsigned long long *ecount = c.alloc<unsigned long long>(1);
@@ -2067,12 +2082,16 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
         // --- A15 sequence gains + A17 events (replicated: O(sum |e|), no exchange)
         const int ibits = std::max(1, bitlen((uint64_t)M));
         EvArgs ev{ibits, pbits, ek, evv, ecount};
+        ev.in_from = ev_from;
+        ev.in_to = ev_to;
         {
             KScope ks(c, "seq_gains", 0.0);
             unsigned long long *gacc = (unsigned long long *)gseq_acc;
             c.zero(gacc, M);
             c.zero(sg_ctr, 2);
             c.zero(ctr, 4);
+            c.zero(ev_from, M);
+            c.zero(ev_to, M);
             // size track (and the event count) first: the edge kernel appends
             k_size_events_dn<<<(unsigned)cdiv(M, 256), 256, 0, c.stream>>>(dM, node, from, to, L.size, ev);
             DHGP_LAUNCHED(c);
@@ -2088,6 +2107,8 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
                 DHGP_LAUNCHED(c);
                 k_inbound_events_block<<<c.num_sms, 256, 0, c.stream>>>(L.dst_off, L.dst_dat, r, pos, from, to, ev,
                                                                          big, ctr, ctr + 2);
+                DHGP_LAUNCHED(c);
+                k_inbound_emit<<<(unsigned)cdiv(M, 256), 256, 0, c.stream>>>(M, from, to, ev);
                 DHGP_LAUNCHED(c);
             }
             k_seq_gains_finish<<<(unsigned)cdiv(M, 256), 256, 0, c.stream>>>(M, giso, gacc, gseq);
@@ -2118,6 +2139,7 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
                 unsigned long long T = 0;
                 c.d2h(&T, ecount, 1);
                 c.sync();
+                if (trace_enabled()) fprintf(stderr, "largeselect level %d M %lld T %llu\n", level, (long long)M, T);
                 if ((int64_t)T <= kSmallSort)
                     small_sort_pairs(c, ek, evv, (int64_t)T);  // equal keys only need grouping
                 else
@@ -2215,7 +2237,8 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
     }
     for (void *p : {(void *)tmp_parts, (void *)flags, (void *)mpos, (void *)pos, (void *)ctr, (void *)big,
                     (void *)big2, (void *)mk, (void *)mkt, (void *)mv, (void *)mvt, (void *)node, (void *)from,
-                    (void *)to, (void *)giso, (void *)gseq, (void *)gseq_acc, (void *)sg_big, (void *)sg_ctr,
+                    (void *)to, (void *)giso, (void *)gseq, (void *)gseq_acc, (void *)ev_from, (void *)ev_to,
+                    (void *)sg_big, (void *)sg_ctr,
                     (void *)ek, (void *)ekt, (void *)evv, (void *)evt, (void *)ecount, (void *)sres, (void *)pdense,
                     (void *)ptouched})
         c.free(p);
