@@ -1053,10 +1053,43 @@ struct EdgeFam {
     const int64_t *out_off;  // write pass
     int32_t *out;
 };
+// the common short case (all three lists <= 32): the six loads of the three
+// lists are issued together, then each list is finished from registers
+__device__ __forceinline__ int warp_gamma_short(uint32_t g, int len, int32_t *out) {
+    const int lane = lane_id();
+    const uint32_t lt = (1u << lane) - 1u;
+    uint32_t v[1] = {lane < len ? g : 0xffffffffu};
+    const uint32_t up = __shfl_up_sync(FULL_MASK, v[0], 1);
+    const bool ok = lane == 0 || lane >= len || up < v[0];
+    if (!__all_sync(FULL_MASK, ok)) warp_bitonic_sort<1>(v);
+    const uint32_t prev = __shfl_up_sync(FULL_MASK, v[0], 1);
+    const bool head = lane < len && (lane == 0 || v[0] != prev);
+    const uint32_t bal = __ballot_sync(FULL_MASK, head);
+    if (out && head) out[__popc(bal & lt)] = (int32_t)v[0];
+    return __popc(bal);
+}
 __global__ void __launch_bounds__(256) k_contract_edges(int32_t E, const int32_t *gamma, EdgeFam f0, EdgeFam f1,
                                                         EdgeFam f2, bool write) {
     const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const int lane = lane_id();
     for (int64_t e = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id(); e < E; e += nw) {
+        const int64_t l0 = f0.off[e], l1 = f1.off[e], l2 = f2.off[e];
+        const int n0 = (int)(f0.off[e + 1] - l0), n1 = (int)(f1.off[e + 1] - l1), n2 = (int)(f2.off[e + 1] - l2);
+        if (n0 <= 32 && n1 <= 32 && n2 <= 32) {
+            const int32_t x0 = lane < n0 ? f0.dat[l0 + lane] : 0, x1 = lane < n1 ? f1.dat[l1 + lane] : 0,
+                          x2 = lane < n2 ? f2.dat[l2 + lane] : 0;
+            const uint32_t g0 = lane < n0 ? (uint32_t)gamma[x0] : 0u, g1 = lane < n1 ? (uint32_t)gamma[x1] : 0u,
+                           g2 = lane < n2 ? (uint32_t)gamma[x2] : 0u;
+            const int c0 = warp_gamma_short(g0, n0, write ? f0.out + f0.out_off[e] : nullptr);
+            const int c1 = warp_gamma_short(g1, n1, write ? f1.out + f1.out_off[e] : nullptr);
+            const int c2 = warp_gamma_short(g2, n2, write ? f2.out + f2.out_off[e] : nullptr);
+            if (!write && lane == 0) {
+                f0.cnt[e] = c0;
+                f1.cnt[e] = c1;
+                f2.cnt[e] = c2;
+            }
+            continue;
+        }
 #pragma unroll
         for (int q = 0; q < 3; q++) {
             const EdgeFam &f = q == 0 ? f0 : (q == 1 ? f1 : f2);
