@@ -19,11 +19,14 @@ namespace {
 // takes 32 incident h-edges at a time and spreads their pins evenly over the
 // lanes (segmented prefix sum + per-slot owner search by shuffles).
 // ---------------------------------------------------------------------------
+// `work` (profiling only) accumulates the algorithmic bytes read: 28 B per
+// incident h-edge (list entry, two offsets, weight) + 4 B per pin
 template <class F>
 __device__ __forceinline__ void warp_for_pins(const int32_t *inc_dat, int64_t ilo, int64_t ihi, int64_t first,
                                               int64_t stride, const int64_t *pin_off, const int32_t *pin_dat,
-                                              F &&f) {
+                                              F &&f, unsigned long long *work = nullptr) {
     const int lane = lane_id();
+    unsigned long long wb = 0;
     for (int64_t base = ilo + first; base < ihi; base += stride) {
         const int64_t ii = base + lane;
         int32_t e = -1;
@@ -37,6 +40,7 @@ __device__ __forceinline__ void warp_for_pins(const int32_t *inc_dat, int64_t il
         const int incl = warp_incl_scan(len);
         const int total = __shfl_sync(FULL_MASK, incl, 31);
         const int excl = incl - len;
+        wb += 28ull * (unsigned long long)min((int64_t)32, ihi - base) + 4ull * (unsigned long long)total;
         // four pins per lane in flight before any is used (the loads are the
         // latency; the hash inserts are cheap)
         for (int s0 = 0; s0 < total; s0 += 128) {
@@ -60,6 +64,7 @@ __device__ __forceinline__ void warp_for_pins(const int32_t *inc_dat, int64_t il
                 if (s0 + u * 32 + lane < total) f(oe[u], m[u]);
         }
     }
+    if (work && lane == 0 && wb) atomicAdd(work, wb);
 }
 
 struct ScoreArgs {
@@ -95,6 +100,7 @@ struct ScoreArgs {
     int64_t *tup_h = nullptr;
     int32_t *tup_count = nullptr;
     int64_t tup_cap = 0;
+    unsigned long long *work = nullptr;  // profiling: algorithmic bytes
 };
 
 // next node of a persistent scoring loop: [lo, hi) or the listed nodes in it
@@ -205,7 +211,7 @@ __global__ void __launch_bounds__(SS_WARPS * 32) k_score_warp(ScoreArgs a) {
                 }
             }
             sover[w] = 1;
-        });
+        }, a.work);
         __syncwarp();
         if (sover[w]) {
             if (lane == 0) a.heavy_list[atomicAdd(a.heavy_count, 1)] = node;
@@ -320,7 +326,8 @@ __global__ void __launch_bounds__(SH_THREADS) k_score_heavy(ScoreArgs a) {
                               }
                           }
                           sover = 1;
-                      });
+                      },
+                      a.work);
         __syncthreads();
         if (sover) {
             if (threadIdx.x == 0) a.big_list[atomicAdd(a.big_count, 1)] = node;
@@ -440,7 +447,8 @@ __global__ void __launch_bounds__(SB_THREADS) k_score_block(ScoreArgs a, long lo
                           long long old = atomicCAS((unsigned long long *)&dense[m], ~0ull, 0ull);
                           if (old == -1ll) touched[atomicAdd(&s_nt, 1)] = m;
                           atomicAdd((unsigned long long *)&dense[m], (unsigned long long)a.wi[e]);
-                      });
+                      },
+                      a.work);
         __syncthreads();
         const int nt = s_nt;
         const int64_t szn = a.size[node];
@@ -687,14 +695,27 @@ static void score_tiers(Ctx &c, ScoreArgs a, const DWeights &W, ScoreScratch &s,
 void score_select(Ctx &c, const DLevel &L, const DWeights &W, int64_t omega, int64_t delta, int32_t *pair,
                   double *score, ScoreScratch &s) {
     if (L.N == 0) return;
-    KScope ks(c, "score_select", (double)(32.0 * L.N + 8.0 * L.U + 16.0 * L.E + 4.0 * L.Sin), L.N);
+    KScope ks(c, "score_select", 0.0, L.N);
     score_attrs(c);
     ScoreArgs a{L.N, L.inc_off, L.inc_dat, L.pin_off, L.pin_dat, W.wi, L.size, L.in_off, L.in_dat, omega, delta,
                 pair, score, s.ctr, s.big, s.ctr + 1, s.heavy, s.ctr + 2, tiers(), 0, L.N};
     const Shard sh = shard_of(c.comm, L.N);
     a.lo = (int32_t)sh.lo;
     a.hi = (int32_t)sh.hi;
+    unsigned long long *work = nullptr;
+    if (c.profiling) {
+        work = c.alloc<unsigned long long>(1);
+        c.zero(work, 1);
+        a.work = work;
+    }
     score_tiers(c, a, W, s, L.N);
+    if (work) {  // measured algorithmic bytes (lists actually read) + outputs
+        unsigned long long h = 0;
+        c.d2h(&h, work, 1);
+        c.sync();
+        ks.bytes = (double)h + 12.0 * (double)(sh.hi - sh.lo);
+        c.free(work);
+    }
     if (sh.on) {  // complete (pair, score) from the other ranks' node ranges
         allgather(c, c.comm, pair, sizeof(int32_t), sh.chunk);
         allgather(c, c.comm, score, sizeof(double), sh.chunk);
@@ -709,7 +730,7 @@ void score_select_inc(Ctx &c, const DLevel &L, const DWeights &W, int64_t omega,
                       double *score, ScoreScratch &s, const ScoreCarry &cy) {
     const int32_t N = L.N;
     if (N == 0) return;
-    KScope ks(c, "score_select", (double)(32.0 * L.N + 8.0 * L.U + 16.0 * L.E + 4.0 * L.Sin), L.N);
+    KScope ks(c, "score_select", 0.0, L.N);
     score_attrs(c);
     uint8_t *kind = c.alloc<uint8_t>(N);
     int64_t *thr_s = c.alloc<int64_t>(N);
@@ -737,6 +758,12 @@ void score_select_inc(Ctx &c, const DLevel &L, const DWeights &W, int64_t omega,
     a.tup_h = th;
     a.tup_count = lc + 2;
     a.tup_cap = cap;
+    unsigned long long *work = nullptr;
+    if (c.profiling) {
+        work = c.alloc<unsigned long long>(1);
+        c.zero(work, 1);
+        a.work = work;
+    }
     score_tiers(c, a, W, s, N);
     static int gq = resident_grid(c, k_inc_tuples_quick, 256, 0);
     k_inc_tuples_quick<<<gq, 256, 0, c.stream>>>(a, best, hard, lc + 3);
@@ -752,7 +779,18 @@ void score_select_inc(Ctx &c, const DLevel &L, const DWeights &W, int64_t omega,
                 pair, score, s.ctr, s.big, s.ctr + 1, s.heavy, s.ctr + 2, tiers(), 0, N};
     b.list = list2;
     b.list_count = lc + 1;
+    b.work = work;
     score_tiers(c, b, W, s, N);
+    if (work) {  // measured algorithmic bytes: lists read by both passes, the per-node
+                 // carry (pair, score, gamma, members: 24 B) and the tuples (16 B each)
+        unsigned long long h = 0;
+        int32_t nt = 0;
+        c.d2h(&h, work, 1);
+        c.d2h(&nt, lc + 2, 1);
+        c.sync();
+        ks.bytes = (double)h + 36.0 * N + 16.0 * std::min<int64_t>(nt, cap);
+        c.free(work);
+    }
     if (trace_enabled()) {
         int32_t h[3];
         c.d2h(h, lc, 3);
@@ -1104,7 +1142,10 @@ __global__ void __launch_bounds__(256) k_contract_edges(int32_t E, const int32_t
 
 void contract_count(Ctx &c, DLevel &fine, const int32_t *match, const uint8_t *isrep, DLevel &coarse,
                     ContractScratch &s, int64_t *d_status) {
-    KScope ks(c, "contract", (double)(16.0 * (fine.Ps + fine.Pd + fine.U) + 24.0 * fine.E + 32.0 * fine.N));
+    // algorithmic bytes: each fine h-edge list entry and its gamma image read
+    // once (8 B), per-h-edge offsets read and counts / coarse offsets written
+    // (60 B), per-node rank / gamma / members (24 B)
+    KScope ks(c, "contract", (double)(8.0 * (fine.Ps + fine.Pd + fine.U) + 60.0 * fine.E + 24.0 * fine.N));
     const int32_t N = fine.N, E = fine.E;
     s.rank = c.alloc<int64_t>((int64_t)N + 1);
     scan_excl<uint8_t>(c, isrep, s.rank, N);
@@ -1179,7 +1220,12 @@ void contract_count(Ctx &c, DLevel &fine, const int32_t *match, const uint8_t *i
 }
 
 void contract_write(Ctx &c, DLevel &fine, DLevel &coarse, ContractScratch &s, const LevelStatus &st) {
-    KScope ks(c, "contract_write");
+    // algorithmic bytes: fine h-edge lists + gamma read (8 B per entry), coarse
+    // lists written (4 B), fine node lists read and coarse ones written (4 B
+    // each), offsets (16 B per h-edge, 16 B per coarse node)
+    KScope ks(c, "contract_write",
+              (double)(8.0 * (fine.Ps + fine.Pd + fine.U) + 4.0 * (st.ps + st.pd + st.u) +
+                       4.0 * (fine.Sin + fine.U) + 4.0 * (st.sin + st.uinc) + 16.0 * fine.E + 16.0 * st.nc));
     const int32_t E = fine.E;
     coarse.N = (int32_t)st.nc;
     coarse.Ps = st.ps;

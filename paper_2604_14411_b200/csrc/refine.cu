@@ -255,6 +255,7 @@ struct ProposeArgs {
     // hub tier: nodes with very many incident h-edges, split over CTAs
     int32_t *hub_list = nullptr;
     int32_t *hub_count = nullptr;
+    unsigned long long *work = nullptr;  // profiling: algorithmic bytes
 };
 constexpr int HUB_MAX = 256;     // hubs per propose pass (more go to the block tiers)
 constexpr int HUB_CHUNK = 256;   // incident h-edges per CTA work item
@@ -316,9 +317,12 @@ __device__ __forceinline__ void write_proposal(const ProposeArgs &a, int32_t nod
 template <class F>
 __device__ __forceinline__ int64_t warp_for_runs(const int32_t *inc_dat, int64_t ilo, int64_t ihi, int64_t first,
                                                  int64_t stride, const int64_t *pin_off, const int32_t *len,
-                                                 const int64_t *wi, F &&f) {
+                                                 const int64_t *wi, unsigned long long *work, F &&f) {
+    // `work` (profiling only): algorithmic bytes read — 24 B per incident
+    // h-edge (list entry, run base, run count, weight) + 8 B per run
     const int lane = lane_id();
     int64_t total = 0;
+    unsigned long long wb = 0;
     for (int64_t base = ilo + first; base < ihi; base += stride) {
         const int64_t ii = base + lane;
         int32_t e = -1;
@@ -334,6 +338,7 @@ __device__ __forceinline__ int64_t warp_for_runs(const int32_t *inc_dat, int64_t
         const int incl = warp_incl_scan(l);
         const int tot = __shfl_sync(FULL_MASK, incl, 31);
         const int excl = incl - l;
+        wb += 24ull * (unsigned long long)min((int64_t)32, ihi - base) + 8ull * (unsigned long long)tot;
         for (int s0 = 0; s0 < tot; s0 += 32) {
             const int sl = s0 + lane;
             int owner = 0;
@@ -349,6 +354,7 @@ __device__ __forceinline__ int64_t warp_for_runs(const int32_t *inc_dat, int64_t
             if (sl < tot) f(oe, owe, oplo + (sl - oex));
         }
     }
+    if (work && lane == 0 && wb) atomicAdd(work, wb);
     return total;
 }
 
@@ -411,7 +417,7 @@ __global__ void __launch_bounds__(PR_WARPS * 32) k_propose_warp(ProposeArgs a) {
         __syncwarp();
         const int32_t ps = a.assign[node];
         int64_t total = 0, saving = 0;
-        total = warp_for_runs(a.inc_dat, ilo, ihi, 0, 32, a.r.off, a.r.len, a.wi, [&](int32_t, int64_t we, int64_t k) {
+        total = warp_for_runs(a.inc_dat, ilo, ihi, 0, 32, a.r.off, a.r.len, a.wi, a.work, [&](int32_t, int64_t we, int64_t k) {
             const int32_t p = a.r.part[k];
             if (p == ps && a.r.cnt[k] == 1) saving += we;
             if (sover[w]) return;
@@ -525,7 +531,7 @@ __global__ void __launch_bounds__(PM_THREADS) k_propose_mid(ProposeArgs a) {
         const int64_t ilo = a.inc_off[node], ihi = a.inc_off[node + 1];
         const int32_t ps = a.assign[node];
         long long total = 0, saving = 0;
-        total = warp_for_runs(a.inc_dat, ilo, ihi, (int64_t)w * 32, (int64_t)nw * 32, a.r.off, a.r.len, a.wi,
+        total = warp_for_runs(a.inc_dat, ilo, ihi, (int64_t)w * 32, (int64_t)nw * 32, a.r.off, a.r.len, a.wi, a.work,
                               [&](int32_t, int64_t we, int64_t k) {
                                   const int32_t p = a.r.part[k];
                                   if (p == ps && a.r.cnt[k] == 1) saving += we;
@@ -621,7 +627,7 @@ __global__ void __launch_bounds__(THREADS) k_propose_heavy(ProposeArgs a) {
         const int64_t ilo = a.inc_off[node], ihi = a.inc_off[node + 1];
         const int32_t ps = a.assign[node];
         long long total = 0, saving = 0;
-        total = warp_for_runs(a.inc_dat, ilo, ihi, (int64_t)w * 32, (int64_t)nw * 32, a.r.off, a.r.len, a.wi,
+        total = warp_for_runs(a.inc_dat, ilo, ihi, (int64_t)w * 32, (int64_t)nw * 32, a.r.off, a.r.len, a.wi, a.work,
                               [&](int32_t, int64_t we, int64_t k) {
                                   const int32_t p = a.r.part[k];
                                   if (p == ps && a.r.cnt[k] == 1) saving += we;
@@ -720,7 +726,7 @@ __global__ void __launch_bounds__(256) k_propose_hub(ProposeArgs a, long long *h
         __syncthreads();
         const int32_t ps = a.assign[node];
         long long total = 0, saving = 0;
-        total = warp_for_runs(a.inc_dat, ilo, ihi, (int64_t)w * 32, (int64_t)nw * 32, a.r.off, a.r.len, a.wi,
+        total = warp_for_runs(a.inc_dat, ilo, ihi, (int64_t)w * 32, (int64_t)nw * 32, a.r.off, a.r.len, a.wi, a.work,
                               [&](int32_t, int64_t we, int64_t k) {
                                   const int32_t p = a.r.part[k];
                                   if (p == ps && a.r.cnt[k] == 1) saving += we;
@@ -797,7 +803,7 @@ __global__ void __launch_bounds__(PB_THREADS) k_propose_block(ProposeArgs a, lon
         const int64_t ilo = a.inc_off[node], ihi = a.inc_off[node + 1];
         const int32_t ps = a.assign[node];
         long long total = 0, saving = 0;
-        total = warp_for_runs(a.inc_dat, ilo, ihi, (int64_t)w * 32, (int64_t)nw * 32, a.r.off, a.r.len, a.wi,
+        total = warp_for_runs(a.inc_dat, ilo, ihi, (int64_t)w * 32, (int64_t)nw * 32, a.r.off, a.r.len, a.wi, a.work,
                               [&](int32_t, int64_t we, int64_t k) {
                                   const int32_t p = a.r.part[k];
                                   if (p == ps && a.r.cnt[k] == 1) saving += we;
@@ -1936,12 +1942,18 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
         st.moved = false;
         // --- A14 propose (warp tier + block tier, no host sync) -------------
         {
-            KScope ks(c, "propose", (double)(28.0 * N + 12.0 * L.U + 20.0 * L.E + 8.0 * K), N);
+            KScope ks(c, "propose", 0.0, N);
+            unsigned long long *work = nullptr;
+            if (c.profiling) {
+                work = c.alloc<unsigned long long>(1);
+                c.zero(work, 1);
+            }
             c.zero(ctr, 4);
             ProposeArgs a{N, K, L.inc_off, L.inc_dat, W.wi, r, assign, psizes, L.size, omega,
                           target, gain, ctr, big, ctr + 1, big2, ctr + 2, tiers(), 0, N};
             a.fsens = st.fsens;
             a.fpart = st.fpart;
+            a.work = work;
             constexpr int kSmallK = 4096;
             const bool small_k = K <= std::min(kSmallK, tiers().small_k);
             if (small_k) {
@@ -2027,6 +2039,13 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
                     }
                     DHGP_LAUNCHED(c);
                 }
+            }
+            if (work) {  // measured algorithmic bytes: lists read (+ per node assign/size/outputs, full mode)
+                unsigned long long h = 0;
+                c.d2h(&h, work, 1);
+                c.sync();
+                ks.bytes = (double)h + 24.0 * (full ? (double)N : 0.0);
+                c.free(work);
             }
             if (trace_enabled()) {
                 int32_t hc[4];
