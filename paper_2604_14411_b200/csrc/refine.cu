@@ -894,11 +894,6 @@ struct EvArgs {
 };
 __device__ __forceinline__ void inbound_leave(const EvArgs &ev, int32_t i) { atomicSub(&ev.in_from[i], 1); }
 __device__ __forceinline__ void inbound_enter(const EvArgs &ev, int32_t i) { atomicAdd(&ev.in_to[i], 1); }
-__device__ __forceinline__ void emit(const EvArgs &ev, uint64_t track, int32_t p, int32_t i, int32_t d) {
-    unsigned long long s = atomicAdd(ev.count, 1ull);
-    ev.key[s] = (track << (ev.pbits + ev.ibits)) | ((uint64_t)(uint32_t)p << ev.ibits) | (uint64_t)(uint32_t)i;
-    ev.val[s] = (uint32_t)d;
-}
 
 // inbound track (refine.py:210-237), per h-edge: the movers among its
 // destination pins in sequence order; per part a running destination-pin
@@ -1304,19 +1299,6 @@ __global__ void k_build_moves_dn(const int64_t *dM, const uint32_t *sorted_nodes
     giso[i] = gain[n];
     pos[n] = (int32_t)i;
 }
-// size track (refine.py:203-208): (from_i, i, -size), (to_i, i, +size)
-__global__ void k_size_events_dn(const int64_t *dM, const int32_t *node, const int32_t *from, const int32_t *to,
-                                 const int32_t *size, EvArgs ev) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t M = *dM;
-    if (i == 0) *ev.count = (unsigned long long)(2 * M);
-    if (i >= M) return;
-    const int32_t s = size[node[i]];
-    ev.key[2 * i] = ((uint64_t)(uint32_t)from[i] << ev.ibits) | (uint64_t)i;
-    ev.val[2 * i] = (uint32_t)(-s);
-    ev.key[2 * i + 1] = ((uint64_t)(uint32_t)to[i] << ev.ibits) | (uint64_t)i;
-    ev.val[2 * i + 1] = (uint32_t)s;
-}
 // A15: gains corrected for earlier moves, rules (a)-(d) (_kernels.pyx:326-363),
 // computed per h-edge: the movers among an h-edge's pins, in sequence order,
 // give every (move, h-edge) term from counts over the earlier movers on that
@@ -1498,18 +1480,48 @@ __global__ void __launch_bounds__(256) k_round_edges(int32_t E, const int32_t *e
     }
 }
 
-// the inbound track's aggregated (part, move) groups as events
-__global__ void k_inbound_emit(int64_t M, const int32_t *from, const int32_t *to, EvArgs ev) {
+// movers compacted in any order (they are sorted right after): key = the
+// sequence key (gain desc) with the node id in the low 32 bits, so equal
+// gains order by node (refine.py:108-110) in any sort; pos[] reset on the way
+__global__ void k_mover_compact(int32_t N, const int32_t *target, const int64_t *gain, int64_t gmax, uint64_t *keys,
+                                uint32_t *vals, int32_t *pos, unsigned long long *count) {
+    const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool mv = n < N && target[n] >= 0;
+    if (n < N) pos[n] = -1;
+    const uint32_t bal = __ballot_sync(FULL_MASK, mv);
+    if (!bal) return;
+    const int lane = lane_id();
+    unsigned long long base = 0;
+    if (lane == __ffs(bal) - 1) base = atomicAdd(count, (unsigned long long)__popc(bal));
+    base = __shfl_sync(FULL_MASK, base, __ffs(bal) - 1);
+    if (mv) {
+        const unsigned long long s = base + __popc(bal & ((1u << lane) - 1u));
+        keys[s] = ((uint64_t)(gmax - gain[n]) << 32) | (uint64_t)(uint32_t)n;
+        vals[s] = (uint32_t)n;
+    }
+}
+// per move, after the h-edge kernels: the size track (refine.py:203-208),
+// the aggregated inbound groups, and gain_seq = gain_iso + the h-edge terms
+__global__ void k_round_moves(const int64_t *dM, const int32_t *node, const int32_t *from, const int32_t *to,
+                              const int32_t *size, EvArgs ev, const int64_t *giso, const unsigned long long *gacc,
+                              int64_t *gseq) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= M) return;
+    if (i >= *dM) return;
+    gseq[i] = giso[i] + (int64_t)gacc[i];
+    const int32_t s = size[node[i]], f = from[i], t = to[i];
     const int32_t a = ev.in_from[i], b = ev.in_to[i];
-    if (a) emit(ev, 1, from[i], (int32_t)i, a);
-    if (b) emit(ev, 1, to[i], (int32_t)i, b);
+    unsigned long long k = atomicAdd(ev.count, (unsigned long long)(2 + (a != 0) + (b != 0)));
+    auto put = [&](uint64_t track, int32_t p, int32_t d) {
+        ev.key[k] = (track << (ev.pbits + ev.ibits)) | ((uint64_t)(uint32_t)p << ev.ibits) | (uint64_t)i;
+        ev.val[k] = (uint32_t)d;
+        k++;
+    };
+    put(0, f, -s);
+    put(0, t, s);
+    if (a) put(1, f, a);
+    if (b) put(1, t, b);
 }
-__global__ void k_seq_gains_finish(int64_t M, const int64_t *giso, const unsigned long long *gacc, int64_t *gseq) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < M) gseq[i] = giso[i] + (int64_t)gacc[i];
-}
+
 
 // ---------------------------------------------------------------------------
 // Incremental refinement (RefineState, refine.cuh).
@@ -1904,7 +1916,7 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
     const int pbits = std::max(1, bitlen((uint64_t)(K > 0 ? K - 1 : 0)));
     const int ibits_cap = std::max(1, bitlen((uint64_t)N));
     if (1 + ibits_cap + pbits > 64) throw Error{DHGP_ERR_UNSUPPORTED, "event key needs more than 64 bits"};
-    const int64_t *dM = mpos + N;
+    int64_t *dM = mpos + N;
     static int g_ru = resident_grid(c, k_runs_update, 256, 0);
     static int g_me = resident_grid(c, k_mover_edges, 256, 0);
     static int g_ap = resident_grid(c, k_apply_inc, 256, 0);
@@ -2062,11 +2074,23 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
         }
         st.fresh = false;
         // --- sequence: movers by (gain desc, node asc) (refine.py:108-110) --
-        if (N > 0) {
-            k_mover_flags<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(N, target, flags);
-            DHGP_LAUNCHED(c);
+        // packed (key, node) when the key fits 32 bits: an unordered atomic
+        // compaction then sorts correctly; else the ordered flags + scan
+        const bool packed = gmax_bits <= 32;
+        if (packed) {
+            c.zero(dM, 1);
+            if (N > 0) {
+                k_mover_compact<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(N, target, gain, W.wsum, mk, mv, pos,
+                                                                             (unsigned long long *)dM);
+                DHGP_LAUNCHED(c);
+            }
+        } else {
+            if (N > 0) {
+                k_mover_flags<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(N, target, flags);
+                DHGP_LAUNCHED(c);
+            }
+            scan_excl<uint8_t>(c, flags, mpos, N);
         }
-        scan_excl<uint8_t>(c, flags, mpos, N);
         // ---- sync 1: M and the connectivity of the round's assignment -----
         int64_t M = 0;
         unsigned long long conn_h = 0;
@@ -2076,15 +2100,22 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
         conns.push_back((double)(int64_t)conn_h);
         need_final = false;
         if (M == 0) break;
-        if (N > 0) {
-            k_mover_keys<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(N, flags, mpos, gain, W.wsum, mk, mv);
-            DHGP_LAUNCHED(c);
+        if (packed) {
+            if (M <= kSmallSort)
+                small_sort_pairs(c, mk, mv, M);
+            else
+                radix_sort_pairs(c, mk, mv, mkt, mvt, M, nullptr, gmax_bits + 32);
+        } else {
+            if (N > 0) {
+                k_mover_keys<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(N, flags, mpos, gain, W.wsum, mk, mv);
+                DHGP_LAUNCHED(c);
+            }
+            if (M <= kSmallSort)
+                small_sort_pairs(c, mk, mv, M);  // vals (nodes) are distinct and ascend: stable
+            else
+                radix_sort_pairs(c, mk, mv, mkt, mvt, M, nullptr, gmax_bits);
+            fill_i32(c, pos, -1, N);
         }
-        if (M <= kSmallSort)
-            small_sort_pairs(c, mk, mv, M);  // vals (nodes) are distinct and ascend: stable
-        else
-            radix_sort_pairs(c, mk, mv, mkt, mvt, M, nullptr, gmax_bits);
-        fill_i32(c, pos, -1, N);
         k_build_moves_dn<<<(unsigned)cdiv(M, 256), 256, 0, c.stream>>>(dM, mv, assign, target, gain, node, from, to,
                                                                        giso, pos);
         DHGP_LAUNCHED(c);
@@ -2111,9 +2142,7 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
             c.zero(ctr, 4);
             c.zero(ev_from, M);
             c.zero(ev_to, M);
-            // size track (and the event count) first: the edge kernel appends
-            k_size_events_dn<<<(unsigned)cdiv(M, 256), 256, 0, c.stream>>>(dM, node, from, to, L.size, ev);
-            DHGP_LAUNCHED(c);
+            c.zero(ecount, 1);
             if (L.E > 0) {
                 static int g_re = resident_grid(c, k_round_edges, 256, 0);
                 const unsigned gre = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(L.E, 8), g_re));
@@ -2127,10 +2156,9 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
                 k_inbound_events_block<<<c.num_sms, 256, 0, c.stream>>>(L.dst_off, L.dst_dat, r, pos, from, to, ev,
                                                                          big, ctr, ctr + 2);
                 DHGP_LAUNCHED(c);
-                k_inbound_emit<<<(unsigned)cdiv(M, 256), 256, 0, c.stream>>>(M, from, to, ev);
-                DHGP_LAUNCHED(c);
             }
-            k_seq_gains_finish<<<(unsigned)cdiv(M, 256), 256, 0, c.stream>>>(M, giso, gacc, gseq);
+            k_round_moves<<<(unsigned)cdiv(M, 256), 256, 0, c.stream>>>(dM, node, from, to, L.size, ev, giso, gacc,
+                                                                       gseq);
             DHGP_LAUNCHED(c);
         }
         // --- A17 select: one CTA for small rounds, T read on device ----------
