@@ -327,6 +327,63 @@ __device__ __forceinline__ void warp_bitonic_sort64(uint64_t (&v)[K]) {
     }
 }
 
+// Sorts n <= 4096 u64 keys ascending with one 1024-thread CTA: each warp
+// sorts a 128-key run in registers, then runs of 128..2048 are merged
+// pairwise by co-ranks — a key's output slot is its offset in its run plus
+// its rank in the partner run (lower bound for the first run's keys, upper
+// bound for the second's, so ties keep run order).  `a` holds the input and
+// receives the output; `b` is scratch; both have room for 4096 keys.
+__device__ __forceinline__ int rank_in_run(const uint64_t *r, int len, uint64_t x, bool upper) {
+    int lo = 0, hi = len;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (upper ? (r[mid] <= x) : (r[mid] < x))
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    return lo;
+}
+__device__ __forceinline__ void block_sort_u64_4096(uint64_t *a, uint64_t *b, int n) {
+    const int t = threadIdx.x, lane = lane_id(), w = warp_id();
+    int np = 128;
+    while (np < n) np <<= 1;
+    if (w * 128 < np) {
+        uint64_t v[4];
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const int idx = w * 128 + k * 32 + lane;
+            v[k] = idx < n ? a[idx] : ~0ull;
+        }
+        warp_bitonic_sort64<4>(v);
+#pragma unroll
+        for (int k = 0; k < 4; k++) b[w * 128 + k * 32 + lane] = v[k];
+    }
+    __syncthreads();
+    uint64_t *src = b, *dst = a;
+    for (int run = 128; run < np; run <<= 1) {
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            const int i = q * 1024 + t;
+            if (i < np) {
+                const int ps = i & ~(2 * run - 1);
+                const bool first = (i & run) == 0;
+                const uint64_t x = src[i];
+                const int r = first ? rank_in_run(src + ps + run, run, x, false) : rank_in_run(src + ps, run, x, true);
+                dst[ps + (i - ps - (first ? 0 : run)) + r] = x;
+            }
+        }
+        __syncthreads();
+        uint64_t *tmp = src;
+        src = dst;
+        dst = tmp;
+    }
+    if (src != a) {
+        for (int i = t; i < np; i += blockDim.x) a[i] = src[i];
+        __syncthreads();
+    }
+}
+
 // block-wide bitonic sort of n_pow2 u64 keys in shared memory (ascending)
 __device__ __forceinline__ void block_bitonic_sort64(uint64_t *s, int n_pow2) {
     for (int size = 2; size <= n_pow2; size <<= 1) {

@@ -408,12 +408,36 @@ __global__ void __launch_bounds__(1024) k_small_sort(uint64_t *keys, uint32_t *v
         vals[i] = sv[i];
     }
 }
+// unique u64 keys whose low 32 bits are the value (the packed mover keys)
+__global__ void __launch_bounds__(1024) k_small_sort_packed(uint64_t *keys, uint32_t *vals, int n) {
+    extern __shared__ unsigned long long sm[];
+    uint64_t *a = (uint64_t *)sm, *b = a + kSmallSort;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) a[i] = keys[i];
+    __syncthreads();
+    block_sort_u64_4096(a, b, n);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        keys[i] = a[i];
+        vals[i] = (uint32_t)a[i];
+    }
+}
 }  // namespace
 
 void small_sort_pairs(Ctx &c, uint64_t *keys, uint32_t *vals, int64_t n) {
     if (n <= 1) return;
     KScope ks(c, "radix_sort");
     k_small_sort<<<1, 1024, 0, c.stream>>>(keys, vals, (int)n);
+    DHGP_LAUNCHED(c);
+}
+void small_sort_packed(Ctx &c, uint64_t *keys, uint32_t *vals, int64_t n) {
+    if (n <= 1) return;
+    KScope ks(c, "radix_sort");
+    static bool attr = false;
+    if (!attr) {
+        DHGP_CUDA(cudaFuncSetAttribute(k_small_sort_packed, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)(2 * kSmallSort * sizeof(uint64_t))));
+        attr = true;
+    }
+    k_small_sort_packed<<<1, 1024, 2 * kSmallSort * sizeof(uint64_t), c.stream>>>(keys, vals, (int)n);
     DHGP_LAUNCHED(c);
 }
 

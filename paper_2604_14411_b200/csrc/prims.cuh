@@ -22,6 +22,8 @@ void radix_sort_pairs(Ctx &c, uint64_t *keys, uint32_t *vals, uint64_t *ktmp, ui
 // (one launch; not stable in general, stable when vals ascend in input order
 // and are distinct).
 constexpr int64_t kSmallSort = 4096;
+// the same for unique keys carrying their value in the low 32 bits
+void small_sort_packed(Ctx &c, uint64_t *keys, uint32_t *vals, int64_t n);
 void small_sort_pairs(Ctx &c, uint64_t *keys, uint32_t *vals, int64_t n);
 
 // Per-segment ascending sort of (map ? map[dat[i]] : dat[i]) into tmp (same

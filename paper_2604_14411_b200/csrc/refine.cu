@@ -1138,7 +1138,7 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select_small(const unsigned lon
                                                               const int64_t *gseq, const int64_t *psizes,
                                                               const int64_t *pinbound, int64_t omega, int64_t delta,
                                                               int ibits, int pbits, int64_t *act_ex_out,
-                                                              long long *res) {
+                                                              long long *res, bool packed) {
     extern __shared__ unsigned long long smem_u64[];
     __shared__ int64_t sh[33];
     __shared__ long long s_bv[32], s_bk[32];
@@ -1158,11 +1158,22 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select_small(const unsigned lon
     // 1. sort the events by key (equal keys only need grouping)
     int np = 1;
     while (np < n) np <<= 1;
-    for (int i = threadIdx.x; i < np; i += SEL_THREADS) {
+    if (packed) {  // key < 2^32: (key, delta) in one u64, register runs + co-rank merges
+        for (int i = threadIdx.x; i < n; i += SEL_THREADS) sk[i] = (ekey[i] << 32) | (uint64_t)evals[i];
+        __syncthreads();
+        block_sort_u64_4096(sk, (uint64_t *)ex, n);  // ex is free until step 2
+        for (int i = threadIdx.x; i < n; i += SEL_THREADS) {
+            const uint64_t x = sk[i];
+            sv[i] = (uint32_t)x;
+            sk[i] = x >> 32;
+        }
+        np = 1;  // skip the bitonic network
+    }
+    for (int i = threadIdx.x; i < np && !packed; i += SEL_THREADS) {
         sk[i] = i < n ? ekey[i] : ~0ull;
         sv[i] = i < n ? evals[i] : 0u;
     }
-    for (int size = 2; size <= np; size <<= 1) {
+    for (int size = 2; size <= np && !packed; size <<= 1) {
         for (int j = size >> 1; j > 0; j >>= 1) {
             __syncthreads();
             for (int t = threadIdx.x; t < (np >> 1); t += SEL_THREADS) {
@@ -2102,7 +2113,7 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
         if (M == 0) break;
         if (packed) {
             if (M <= kSmallSort)
-                small_sort_pairs(c, mk, mv, M);
+                small_sort_packed(c, mk, mv, M);
             else
                 radix_sort_pairs(c, mk, mv, mkt, mvt, M, nullptr, gmax_bits + 32);
         } else {
@@ -2168,8 +2179,10 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
         int64_t *cum = c.alloc<int64_t>(M + 1);
         {
             KScope ks(c, "select", 0.0, N);
+            const bool packed_ev = 1 + ibits + pbits <= 32;
             k_select_small<<<1, SEL_THREADS, sel_smem(), c.stream>>>(ecount, M, ek, evv, gseq, psizes, pinbound,
-                                                                    omega, delta, ibits, pbits, act_ex, sres);
+                                                                    omega, delta, ibits, pbits, act_ex, sres,
+                                                                    packed_ev);
             DHGP_LAUNCHED(c);
             // ---- sync 2: the selected prefix (or "too large"), error flags ---
             long long hr[3];
