@@ -1176,9 +1176,8 @@ void contract_count(Ctx &c, DLevel &fine, const int32_t *match, const uint8_t *i
         coarse.src_off = c.alloc<int64_t>((int64_t)E + 1);
         coarse.dst_off = c.alloc<int64_t>((int64_t)E + 1);
         coarse.pin_off = c.alloc<int64_t>((int64_t)E + 1);
-        scan_excl<int32_t>(c, cnt, coarse.src_off, E);
-        scan_excl<int32_t>(c, cnt + E, coarse.dst_off, E);
-        scan_excl<int32_t>(c, cnt + 2 * (int64_t)E, coarse.pin_off, E);
+        scan_excl3<int32_t>(c, cnt, coarse.src_off, cnt + E, coarse.dst_off, cnt + 2 * (int64_t)E, coarse.pin_off,
+                            E);
         c.free(cnt);
     } else {
     s.tmp_src = c.alloc<int32_t>(fine.Ps);
@@ -1202,17 +1201,16 @@ void contract_count(Ctx &c, DLevel &fine, const int32_t *match, const uint8_t *i
     kcs.close();
     KScope kcn(c, "cc_nodes");
     // per-node families: union of the two members' sorted lists
-    int64_t *ncnt = c.alloc<int64_t>(N);
+    int64_t *ncnt = c.alloc<int64_t>(2 * (int64_t)N);
     s.big_in = c.alloc<int32_t>(N);
     s.big_inc = c.alloc<int32_t>(N);
     s.big_cnt = c.alloc<int32_t>(2);
     c.zero(s.big_cnt, 2);
     coarse.in_off = c.alloc<int64_t>((int64_t)N + 1);
-    merge_union_count(c, N, s.ma, s.mb, fine.in_off, fine.in_dat, ncnt, d_nc, s.big_in, s.big_cnt);
-    scan_excl<int64_t>(c, ncnt, coarse.in_off, N);
     coarse.inc_off = c.alloc<int64_t>((int64_t)N + 1);
-    merge_union_count(c, N, s.ma, s.mb, fine.inc_off, fine.inc_dat, ncnt, d_nc, s.big_inc, s.big_cnt + 1);
-    scan_excl<int64_t>(c, ncnt, coarse.inc_off, N);
+    merge_union_count2(c, N, s.ma, s.mb, fine.in_off, fine.in_dat, ncnt, s.big_in, s.big_cnt, fine.inc_off,
+                       fine.inc_dat, ncnt + N, s.big_inc, s.big_cnt + 1, d_nc);
+    scan_excl3<int64_t>(c, ncnt, coarse.in_off, ncnt + N, coarse.inc_off, nullptr, nullptr, N);
     c.free(ncnt);
     k_contract_status<<<1, 32, 0, c.stream>>>(N, E, s.rank, coarse.src_off, coarse.dst_off, coarse.pin_off,
                                               coarse.in_off, coarse.inc_off, d_status);
@@ -1259,14 +1257,10 @@ void contract_write(Ctx &c, DLevel &fine, DLevel &coarse, ContractScratch &s, co
         }
     }
     {
-        KScope k2(c, "cw_merge_in");
-        merge_union_write(c, st.nc, s.ma, s.mb, fine.in_off, fine.in_dat, coarse.in_off, coarse.in_dat, s.big_in,
-                          s.big_cnt);
-    }
-    {
-        KScope k2(c, "cw_merge_inc");
-        merge_union_write(c, st.nc, s.ma, s.mb, fine.inc_off, fine.inc_dat, coarse.inc_off, coarse.inc_dat,
-                          s.big_inc, s.big_cnt + 1);
+        KScope k2(c, "cw_merge");
+        merge_union_write2(c, st.nc, s.ma, s.mb, fine.in_off, fine.in_dat, coarse.in_off, coarse.in_dat, s.big_in,
+                           s.big_cnt, fine.inc_off, fine.inc_dat, coarse.inc_off, coarse.inc_dat, s.big_inc,
+                           s.big_cnt + 1);
     }
     int32_t *ma = s.ma, *mb = s.mb;
     s.ma = s.mb = nullptr;

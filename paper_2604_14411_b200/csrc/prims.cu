@@ -59,8 +59,17 @@ __device__ __forceinline__ void tile_store(int64_t *out, int64_t n, int64_t base
     }
 }
 
+// up to three independent scans of the same length in one launch (blockIdx.y)
 template <class T>
-__global__ void __launch_bounds__(SC_BT) k_scan_final(const T *in, int64_t n, const int64_t *partial, int64_t *out) {
+struct ScanSet {
+    const T *in[3];
+    int64_t *out[3];
+};
+
+template <class T>
+__global__ void __launch_bounds__(SC_BT) k_scan_final(ScanSet<T> set, int64_t n, const int64_t *partial) {
+    const T *in = set.in[blockIdx.y];
+    int64_t *out = set.out[blockIdx.y];
     __shared__ int64_t sh[SC_BT / 32];
     const int64_t base = (int64_t)blockIdx.x * SC_TILE;
     int64_t v[SC_IPT];
@@ -76,8 +85,12 @@ __global__ void __launch_bounds__(SC_BT) k_scan_final(const T *in, int64_t n, co
 // cleared between calls (calls on a device are serialised).
 constexpr uint32_t kAggBit = 1u, kIncBit = 2u;
 template <class T>
-__global__ void __launch_bounds__(SC_BT) k_scan_onepass(const T *in, int64_t n, int64_t *out, uint32_t *flag,
-                                                        int64_t *agg, int64_t *inc, uint32_t epoch) {
+__global__ void __launch_bounds__(SC_BT) k_scan_onepass(ScanSet<T> set, int64_t n, uint32_t *flag0, int64_t *agg0,
+                                                        int64_t *inc0, int64_t stride, uint32_t epoch) {
+    const T *in = set.in[blockIdx.y];
+    int64_t *out = set.out[blockIdx.y];
+    uint32_t *flag = flag0 + blockIdx.y * stride;
+    int64_t *agg = agg0 + blockIdx.y * stride, *inc = inc0 + blockIdx.y * stride;
     __shared__ int64_t sh[SC_BT / 32];
     __shared__ int64_t s_prefix;
     const int64_t tile = blockIdx.x;
@@ -144,26 +157,28 @@ ScanScratch g_scan[64];
 }  // namespace
 
 template <class T>
-void scan_excl(Ctx &c, const T *in, int64_t *out, int64_t n) {
+static void scan_set(Ctx &c, const ScanSet<T> &set, int k, int64_t n) {
     if (n <= 0) {
-        c.zero(out, 1);
+        for (int q = 0; q < k; q++) c.zero(set.out[q], 1);
         return;
     }
     const int64_t ntiles = cdiv(n, SC_TILE);
     if (ntiles == 1) {
-        k_scan_final<T><<<1, SC_BT, 0, c.stream>>>(in, n, nullptr, out);
+        k_scan_final<T><<<dim3(1, k), SC_BT, 0, c.stream>>>(set, n, nullptr);
         DHGP_LAUNCHED(c);
         return;
     }
+    ScanSet<T> s2 = set;
     ScanScratch &ss = g_scan[c.device];
-    if (ss.cap < ntiles) {
+    const int64_t need = 3 * ntiles;
+    if (ss.cap < need) {
         // stream-ordered: earlier kernels on this stream are done with the old buffers
         if (ss.flag) {
             c.free(ss.flag);
             c.free(ss.agg);
             c.free(ss.inc);
         }
-        ss.cap = std::max<int64_t>(ntiles, 4096);
+        ss.cap = std::max<int64_t>(need, 3 * 4096);
         ss.flag = c.alloc<uint32_t>(ss.cap);
         ss.agg = c.alloc<int64_t>(ss.cap);
         ss.inc = c.alloc<int64_t>(ss.cap);
@@ -175,9 +190,26 @@ void scan_excl(Ctx &c, const T *in, int64_t *out, int64_t n) {
         DHGP_CUDA(cudaMemsetAsync(ss.flag, 0, sizeof(uint32_t) * ss.cap, c.stream));
         ss.epoch = 1;
     }
-    k_scan_onepass<T><<<(unsigned)ntiles, SC_BT, 0, c.stream>>>(in, n, out, ss.flag, ss.agg, ss.inc, ss.epoch);
+    k_scan_onepass<T><<<dim3((unsigned)ntiles, k), SC_BT, 0, c.stream>>>(s2, n, ss.flag, ss.agg, ss.inc, ntiles,
+                                                                         ss.epoch);
     DHGP_LAUNCHED(c);
 }
+
+template <class T>
+void scan_excl(Ctx &c, const T *in, int64_t *out, int64_t n) {
+    ScanSet<T> set{{in, nullptr, nullptr}, {out, nullptr, nullptr}};
+    scan_set(c, set, 1, n);
+}
+template <class T>
+void scan_excl3(Ctx &c, const T *in0, int64_t *out0, const T *in1, int64_t *out1, const T *in2, int64_t *out2,
+                int64_t n) {
+    ScanSet<T> set{{in0, in1, in2}, {out0, out1, out2}};
+    scan_set(c, set, in2 ? 3 : 2, n);
+}
+template void scan_excl3<int32_t>(Ctx &, const int32_t *, int64_t *, const int32_t *, int64_t *, const int32_t *,
+                                  int64_t *, int64_t);
+template void scan_excl3<int64_t>(Ctx &, const int64_t *, int64_t *, const int64_t *, int64_t *, const int64_t *,
+                                  int64_t *, int64_t);
 // running maximum: per-tile maxima, a single-block max-scan over them,
 // then per-tile inclusive max with the carry
 namespace {
@@ -656,9 +688,30 @@ void seg_unique_write(Ctx &c, int64_t nseg, const int64_t *off, const int32_t *t
 // ===========================================================================
 namespace {
 constexpr int64_t kMergeBig = 2048;
-__global__ void k_merge_count(int64_t nc_cap, const int64_t *d_nc, const int32_t *ma, const int32_t *mb,
-                              const int64_t *off, const int32_t *dat, int64_t *cnt, int32_t *big_list,
-                              int32_t *big_count) {
+// two node families (in, inc) per launch: blockIdx.y picks one
+struct MergeFam {
+    const int64_t *off;
+    const int32_t *dat;
+    int64_t *cnt;            // count pass
+    const int64_t *out_off;  // write pass
+    int32_t *out;
+    int32_t *big_list;
+    int32_t *big_count;
+};
+struct MergeFams {
+    MergeFam f[2];
+};
+__device__ __forceinline__ void merge_count_body(int64_t nc_cap, const int64_t *d_nc, const int32_t *ma,
+                                                 const int32_t *mb, const int64_t *off, const int32_t *dat,
+                                                 int64_t *cnt, int32_t *big_list, int32_t *big_count);
+__global__ void k_merge_count2(int64_t nc_cap, const int64_t *d_nc, const int32_t *ma, const int32_t *mb,
+                               MergeFams fs) {
+    const MergeFam &f = fs.f[blockIdx.y];
+    merge_count_body(nc_cap, d_nc, ma, mb, f.off, f.dat, f.cnt, f.big_list, f.big_count);
+}
+__device__ __forceinline__ void merge_count_body(int64_t nc_cap, const int64_t *d_nc, const int32_t *ma,
+                                                 const int32_t *mb, const int64_t *off, const int32_t *dat,
+                                                 int64_t *cnt, int32_t *big_list, int32_t *big_count) {
     const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
     const int lane = lane_id();
     const int64_t nc = d_nc ? *d_nc : nc_cap;
@@ -692,8 +745,16 @@ __global__ void k_merge_count(int64_t nc_cap, const int64_t *d_nc, const int32_t
     }
 }
 
-__global__ void k_merge_write(int64_t nc, const int32_t *ma, const int32_t *mb, const int64_t *off,
-                              const int32_t *dat, const int64_t *out_off, int32_t *out, bool skip_big) {
+__device__ __forceinline__ void merge_write_body(int64_t nc, const int32_t *ma, const int32_t *mb, const int64_t *off,
+                                                 const int32_t *dat, const int64_t *out_off, int32_t *out,
+                                                 bool skip_big);
+__global__ void k_merge_write2(int64_t nc, const int32_t *ma, const int32_t *mb, MergeFams fs, bool skip_big) {
+    const MergeFam &f = fs.f[blockIdx.y];
+    merge_write_body(nc, ma, mb, f.off, f.dat, f.out_off, f.out, skip_big);
+}
+__device__ __forceinline__ void merge_write_body(int64_t nc, const int32_t *ma, const int32_t *mb, const int64_t *off,
+                                                 const int32_t *dat, const int64_t *out_off, int32_t *out,
+                                                 bool skip_big) {
     const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
     const int lane = lane_id();
     const uint32_t lt = (1u << lane) - 1u;
@@ -770,8 +831,16 @@ __device__ __forceinline__ int64_t block_excl_flags(bool f, int64_t *sh_w, int64
     *total = tot;
     return before + __popc(bal & ((1u << lane) - 1u));
 }
-__global__ void k_merge_count_big(const int32_t *list, const int32_t *count, const int32_t *ma, const int32_t *mb,
-                                  const int64_t *off, const int32_t *dat, int64_t *cnt) {
+__device__ __forceinline__ void merge_count_big_body(const int32_t *list, const int32_t *count, const int32_t *ma,
+                                                     const int32_t *mb, const int64_t *off, const int32_t *dat,
+                                                     int64_t *cnt);
+__global__ void k_merge_count_big2(const int32_t *ma, const int32_t *mb, MergeFams fs) {
+    const MergeFam &f = fs.f[blockIdx.y];
+    merge_count_big_body(f.big_list, f.big_count, ma, mb, f.off, f.dat, f.cnt);
+}
+__device__ __forceinline__ void merge_count_big_body(const int32_t *list, const int32_t *count, const int32_t *ma,
+                                                     const int32_t *mb, const int64_t *off, const int32_t *dat,
+                                                     int64_t *cnt) {
     __shared__ int64_t sh[32];
     const int n = *count;
     for (int t = blockIdx.x; t < n; t += gridDim.x) {
@@ -787,8 +856,16 @@ __global__ void k_merge_count_big(const int32_t *list, const int32_t *count, con
         __syncthreads();
     }
 }
-__global__ void k_merge_write_big(const int32_t *list, const int32_t *count, const int32_t *ma, const int32_t *mb,
-                                  const int64_t *off, const int32_t *dat, const int64_t *out_off, int32_t *out) {
+__device__ __forceinline__ void merge_write_big_body(const int32_t *list, const int32_t *count, const int32_t *ma,
+                                                     const int32_t *mb, const int64_t *off, const int32_t *dat,
+                                                     const int64_t *out_off, int32_t *out);
+__global__ void k_merge_write_big2(const int32_t *ma, const int32_t *mb, MergeFams fs) {
+    const MergeFam &f = fs.f[blockIdx.y];
+    merge_write_big_body(f.big_list, f.big_count, ma, mb, f.off, f.dat, f.out_off, f.out);
+}
+__device__ __forceinline__ void merge_write_big_body(const int32_t *list, const int32_t *count, const int32_t *ma,
+                                                     const int32_t *mb, const int64_t *off, const int32_t *dat,
+                                                     const int64_t *out_off, int32_t *out) {
     __shared__ int64_t sh[32];
     const int n = *count;
     for (int t = blockIdx.x; t < n; t += gridDim.x) {
@@ -839,28 +916,30 @@ __global__ void k_merge_write_big(const int32_t *list, const int32_t *count, con
 }
 }  // namespace
 
-void merge_union_count(Ctx &c, int64_t nc, const int32_t *ma, const int32_t *mb, const int64_t *off,
-                       const int32_t *dat, int64_t *cnt, const int64_t *d_nc, int32_t *big_list, int32_t *big_count) {
+void merge_union_count2(Ctx &c, int64_t nc, const int32_t *ma, const int32_t *mb, const int64_t *off0,
+                        const int32_t *dat0, int64_t *cnt0, int32_t *big0, int32_t *bigc0, const int64_t *off1,
+                        const int32_t *dat1, int64_t *cnt1, int32_t *big1, int32_t *bigc1, const int64_t *d_nc) {
     if (nc <= 0) return;
-    int64_t blocks = std::min<int64_t>(cdiv(nc, 8), (int64_t)c.num_sms * 16);
-    k_merge_count<<<(unsigned)blocks, 256, 0, c.stream>>>(nc, d_nc, ma, mb, off, dat, cnt, big_list, big_count);
+    MergeFams fs{{MergeFam{off0, dat0, cnt0, nullptr, nullptr, big0, bigc0},
+                  MergeFam{off1, dat1, cnt1, nullptr, nullptr, big1, bigc1}}};
+    const int64_t blocks = std::min<int64_t>(cdiv(nc, 8), (int64_t)c.num_sms * 16);
+    k_merge_count2<<<dim3((unsigned)blocks, 2), 256, 0, c.stream>>>(nc, d_nc, ma, mb, fs);
     DHGP_LAUNCHED(c);
-    if (big_list) {
-        k_merge_count_big<<<c.num_sms, 1024, 0, c.stream>>>(big_list, big_count, ma, mb, off, dat, cnt);
-        DHGP_LAUNCHED(c);
-    }
+    k_merge_count_big2<<<dim3(c.num_sms, 2), 1024, 0, c.stream>>>(ma, mb, fs);
+    DHGP_LAUNCHED(c);
 }
-void merge_union_write(Ctx &c, int64_t nc, const int32_t *ma, const int32_t *mb, const int64_t *off,
-                       const int32_t *dat, const int64_t *out_off, int32_t *out, const int32_t *big_list,
-                       const int32_t *big_count) {
+void merge_union_write2(Ctx &c, int64_t nc, const int32_t *ma, const int32_t *mb, const int64_t *off0,
+                        const int32_t *dat0, const int64_t *out_off0, int32_t *out0, int32_t *big0, int32_t *bigc0,
+                        const int64_t *off1, const int32_t *dat1, const int64_t *out_off1, int32_t *out1,
+                        int32_t *big1, int32_t *bigc1) {
     if (nc <= 0) return;
-    int64_t blocks = std::min<int64_t>(cdiv(nc, 8), (int64_t)c.num_sms * 16);
-    k_merge_write<<<(unsigned)blocks, 256, 0, c.stream>>>(nc, ma, mb, off, dat, out_off, out, big_list != nullptr);
+    MergeFams fs{{MergeFam{off0, dat0, nullptr, out_off0, out0, big0, bigc0},
+                  MergeFam{off1, dat1, nullptr, out_off1, out1, big1, bigc1}}};
+    const int64_t blocks = std::min<int64_t>(cdiv(nc, 8), (int64_t)c.num_sms * 16);
+    k_merge_write2<<<dim3((unsigned)blocks, 2), 256, 0, c.stream>>>(nc, ma, mb, fs, true);
     DHGP_LAUNCHED(c);
-    if (big_list) {
-        k_merge_write_big<<<c.num_sms, 1024, 0, c.stream>>>(big_list, big_count, ma, mb, off, dat, out_off, out);
-        DHGP_LAUNCHED(c);
-    }
+    k_merge_write_big2<<<dim3(c.num_sms, 2), 1024, 0, c.stream>>>(ma, mb, fs);
+    DHGP_LAUNCHED(c);
 }
 
 // ===========================================================================

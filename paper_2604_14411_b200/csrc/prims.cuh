@@ -9,6 +9,11 @@ namespace dhgp {
 // out[0..n]: exclusive prefix sums of in[0..n-1]; out[n] = total.
 template <class T>
 void scan_excl(Ctx &c, const T *in, int64_t *out, int64_t n);
+// two or three independent exclusive scans of length n in one launch
+// (in2 == nullptr: two)
+template <class T>
+void scan_excl3(Ctx &c, const T *in0, int64_t *out0, const T *in1, int64_t *out1, const T *in2, int64_t *out2,
+                int64_t n);
 // out[k] = max(in[0..k]) (inclusive running maximum), int64.
 void scan_incl_max(Ctx &c, const int64_t *in, int64_t *out, int64_t n);
 
@@ -42,12 +47,13 @@ void seg_unique_write(Ctx &c, int64_t nseg, const int64_t *off, const int32_t *t
 // capacity and cnt[d_nc..nc) is zeroed.
 // Unions of more than 2048 elements go to a block-per-node kernel through
 // big_list (filled by the count call, reused by the write call).
-void merge_union_count(Ctx &c, int64_t nc, const int32_t *ma, const int32_t *mb, const int64_t *off,
-                       const int32_t *dat, int64_t *cnt, const int64_t *d_nc = nullptr, int32_t *big_list = nullptr,
-                       int32_t *big_count = nullptr);
-void merge_union_write(Ctx &c, int64_t nc, const int32_t *ma, const int32_t *mb, const int64_t *off,
-                       const int32_t *dat, const int64_t *out_off, int32_t *out, const int32_t *big_list = nullptr,
-                       const int32_t *big_count = nullptr);
+void merge_union_count2(Ctx &c, int64_t nc, const int32_t *ma, const int32_t *mb, const int64_t *off0,
+                        const int32_t *dat0, int64_t *cnt0, int32_t *big0, int32_t *bigc0, const int64_t *off1,
+                        const int32_t *dat1, int64_t *cnt1, int32_t *big1, int32_t *bigc1, const int64_t *d_nc);
+void merge_union_write2(Ctx &c, int64_t nc, const int32_t *ma, const int32_t *mb, const int64_t *off0,
+                        const int32_t *dat0, const int64_t *out_off0, int32_t *out0, int32_t *big0, int32_t *bigc0,
+                        const int64_t *off1, const int32_t *dat1, const int64_t *out_off1, int32_t *out1,
+                        int32_t *big1, int32_t *bigc1);
 
 // Simple fills.
 void iota_i32(Ctx &c, int32_t *p, int64_t n);
