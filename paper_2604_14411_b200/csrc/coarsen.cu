@@ -1138,6 +1138,97 @@ __global__ void __launch_bounds__(256) k_contract_edges(int32_t E, const int32_t
         }
     }
 }
+
+// Flattened contraction of one list family over a batch of 32 h-edges: the
+// warp spreads the batch's list slots over its lanes (as warp_for_pins), so
+// short lists do not leave lanes idle and 32 slots' gamma gathers are in
+// flight together.  A slot is a head when it differs from its predecessor in
+// the same list; a list whose gamma image is not strictly ascending (a
+// displaced cluster member) is "slow" and redone per list by
+// warp_gamma_any.  Count pass: per-list head counts and slow flags; write
+// pass: heads at out_off + (heads before it), with ranks inside a chunk from
+// __match_any_sync over the owning list.
+__device__ __forceinline__ void flat_family(const EdgeFam &f, int64_t e0, int nb, const int32_t *gamma, bool write,
+                                            uint8_t *slow, int32_t *run, uint8_t *bad) {
+    const int lane = lane_id();
+    const uint32_t lt = (1u << lane) - 1u;
+    int64_t lo = 0;
+    int len = 0;
+    uint8_t sl = 0;
+    if (lane < nb) {
+        lo = f.off[e0 + lane];
+        len = (int)(f.off[e0 + lane + 1] - lo);
+        if (write) sl = slow[e0 + lane];
+    }
+    const int incl = warp_incl_scan(len);
+    const int total = __shfl_sync(FULL_MASK, incl, 31);
+    const int excl = incl - len;
+    run[lane] = 0;
+    bad[lane] = 0;
+    __syncwarp();
+    uint32_t pv = 0;
+    for (int s0 = 0; s0 < total; s0 += 32) {
+        const int s = s0 + lane;
+        int own = 0;
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+            const int ex = __shfl_sync(FULL_MASK, excl, own + step);
+            if (ex <= s) own += step;
+        }
+        const bool valid = s < total;
+        const int64_t olo = __shfl_sync(FULL_MASK, lo, own);
+        const int oex = __shfl_sync(FULL_MASK, excl, own);
+        const uint8_t osl = (uint8_t)__shfl_sync(FULL_MASK, (int)sl, own);
+        const uint32_t g = valid ? (uint32_t)gamma[f.dat[olo + (s - oex)]] : 0xffffffffu;
+        const uint32_t up = __shfl_up_sync(FULL_MASK, g, 1);
+        const uint32_t prev = lane == 0 ? pv : up;
+        const bool first = s == oex;
+        if (valid && !first && !(prev < g)) bad[own] = 1;
+        const bool head = valid && (first || g != prev);
+        const uint32_t hm = __ballot_sync(FULL_MASK, head);
+        const uint32_t peers = __match_any_sync(FULL_MASK, valid ? own : 64 + lane);
+        const int rank = __popc(peers & hm & lt);
+        if (write && head && !osl) f.out[f.out_off[e0 + own] + run[own] + rank] = (int32_t)g;
+        __syncwarp();
+        if (valid && lane == 31 - __clz(peers)) run[own] += __popc(peers & hm);
+        pv = __shfl_sync(FULL_MASK, g, 31);
+        __syncwarp();
+    }
+    bool sw = false;  // this lane's list needs the per-list path
+    if (lane < nb) {
+        if (write) {
+            sw = sl;
+        } else {
+            sw = bad[lane];
+            slow[e0 + lane] = (uint8_t)sw;
+            if (!sw) f.cnt[e0 + lane] = run[lane];
+        }
+    }
+    uint32_t m = __ballot_sync(FULL_MASK, sw);
+    while (m) {
+        const int j = __ffs(m) - 1;
+        m &= m - 1;
+        const int64_t e = e0 + j;
+        const int64_t lj = __shfl_sync(FULL_MASK, lo, j);
+        const int nj = __shfl_sync(FULL_MASK, len, j);
+        const int n = warp_gamma_any(f.dat, lj, nj, gamma, write ? f.out + f.out_off[e] : nullptr);
+        if (!write && lane == 0) f.cnt[e] = n;
+    }
+    __syncwarp();
+}
+__global__ void __launch_bounds__(256) k_contract_flat(int32_t E, const int32_t *gamma, EdgeFam f0, EdgeFam f1,
+                                                       EdgeFam f2, bool write, uint8_t *slow) {
+    __shared__ int32_t s_run[8][32];
+    __shared__ uint8_t s_bad[8][32];
+    const int w = warp_id();
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t e0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + w) * 32; e0 < E; e0 += nw * 32) {
+        const int nb = (int)min((int64_t)32, (int64_t)E - e0);
+        flat_family(f0, e0, nb, gamma, write, slow, s_run[w], s_bad[w]);
+        flat_family(f1, e0, nb, gamma, write, slow + E, s_run[w], s_bad[w]);
+        flat_family(f2, e0, nb, gamma, write, slow + 2 * (int64_t)E, s_run[w], s_bad[w]);
+    }
+}
 }  // namespace
 
 void contract_count(Ctx &c, DLevel &fine, const int32_t *match, const uint8_t *isrep, DLevel &coarse,
@@ -1162,15 +1253,25 @@ void contract_count(Ctx &c, DLevel &fine, const int32_t *match, const uint8_t *i
     KScope kcs(c, "cc_edges");
     coarse.maxp = fine.maxp;
     s.fused = fine.maxp <= 128;
+    // short lists on average (the tail of C3): slots flattened over the warp;
+    // longer ones: a warp per h-edge
+    // (when there are enough h-edges to give every resident warp a batch)
+    s.flat = fine.Ps + fine.Pd + fine.U <= 3 * 12 * (int64_t)E && (int64_t)E >= 32 * 48 * (int64_t)c.num_sms;
     if (s.fused) {
         int32_t *cnt = c.alloc<int32_t>(3 * (int64_t)E);
+        s.slow = c.alloc<uint8_t>(3 * (int64_t)E);
         if (E > 0) {
-            static int g = resident_grid(c, k_contract_edges, 256, 0);
-            const unsigned gr = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(E, 8), g));
-            k_contract_edges<<<gr, 256, 0, c.stream>>>(E, fine.gamma, EdgeFam{fine.src_off, fine.src_dat, cnt},
-                                                       EdgeFam{fine.dst_off, fine.dst_dat, cnt + E},
-                                                       EdgeFam{fine.pin_off, fine.pin_dat, cnt + 2 * (int64_t)E},
-                                                       false);
+            const EdgeFam f0{fine.src_off, fine.src_dat, cnt}, f1{fine.dst_off, fine.dst_dat, cnt + E},
+                f2{fine.pin_off, fine.pin_dat, cnt + 2 * (int64_t)E};
+            if (s.flat) {
+                static int g = resident_grid(c, k_contract_flat, 256, 0);
+                const unsigned gr = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(E, 256), g));
+                k_contract_flat<<<gr, 256, 0, c.stream>>>(E, fine.gamma, f0, f1, f2, false, s.slow);
+            } else {
+                static int g = resident_grid(c, k_contract_edges, 256, 0);
+                const unsigned gr = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(E, 8), g));
+                k_contract_edges<<<gr, 256, 0, c.stream>>>(E, fine.gamma, f0, f1, f2, false);
+            }
             DHGP_LAUNCHED(c);
         }
         coarse.src_off = c.alloc<int64_t>((int64_t)E + 1);
@@ -1242,12 +1343,18 @@ void contract_write(Ctx &c, DLevel &fine, DLevel &coarse, ContractScratch &s, co
         KScope k2(c, "cw_unique");
         if (s.fused) {
             if (E > 0) {
-                static int g = resident_grid(c, k_contract_edges, 256, 0);
-                const unsigned gr = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(E, 8), g));
-                k_contract_edges<<<gr, 256, 0, c.stream>>>(
-                    E, fine.gamma, EdgeFam{fine.src_off, fine.src_dat, nullptr, coarse.src_off, coarse.src_dat},
-                    EdgeFam{fine.dst_off, fine.dst_dat, nullptr, coarse.dst_off, coarse.dst_dat},
-                    EdgeFam{fine.pin_off, fine.pin_dat, nullptr, coarse.pin_off, coarse.pin_dat}, true);
+                const EdgeFam f0{fine.src_off, fine.src_dat, nullptr, coarse.src_off, coarse.src_dat},
+                    f1{fine.dst_off, fine.dst_dat, nullptr, coarse.dst_off, coarse.dst_dat},
+                    f2{fine.pin_off, fine.pin_dat, nullptr, coarse.pin_off, coarse.pin_dat};
+                if (s.flat) {
+                    static int g = resident_grid(c, k_contract_flat, 256, 0);
+                    const unsigned gr = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(E, 256), g));
+                    k_contract_flat<<<gr, 256, 0, c.stream>>>(E, fine.gamma, f0, f1, f2, true, s.slow);
+                } else {
+                    static int g = resident_grid(c, k_contract_edges, 256, 0);
+                    const unsigned gr = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(E, 8), g));
+                    k_contract_edges<<<gr, 256, 0, c.stream>>>(E, fine.gamma, f0, f1, f2, true);
+                }
                 DHGP_LAUNCHED(c);
             }
         } else {
@@ -1332,6 +1439,7 @@ void contract_release(Ctx &c, ContractScratch &s) {
     c.free(s.big_in);
     c.free(s.big_inc);
     c.free(s.big_cnt);
+    c.free(s.slow);
     s = ContractScratch();
 }
 

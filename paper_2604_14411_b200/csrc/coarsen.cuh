@@ -73,7 +73,9 @@ struct ContractScratch {
     int32_t *tmp_src = nullptr, *tmp_dst = nullptr, *tmp_pin = nullptr;
     int64_t *rank = nullptr;
     int32_t *big_in = nullptr, *big_inc = nullptr, *big_cnt = nullptr;  // large unions (block tier)
-    bool fused = false;  // h-edge lists rebuilt by the fused warp kernel (no sorted temporaries)
+    bool fused = false;  // h-edge lists rebuilt by the flattened warp kernel (no sorted temporaries)
+    uint8_t *slow = nullptr;  // [3E] lists that need the per-list sort (count pass -> write pass)
+    bool flat = false;        // flattened kernel (short lists) vs warp per h-edge
 };
 void contract_count(Ctx &c, DLevel &fine, const int32_t *match, const uint8_t *isrep, DLevel &coarse,
                     ContractScratch &s, int64_t *d_status);

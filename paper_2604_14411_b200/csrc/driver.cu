@@ -349,12 +349,12 @@ static void run_partition(Ctx &c, const DInput &in, const dhgp_config &cfg, Part
         prev_score = nullptr;
     };
     // bytes of non-checkpoint levels kept whole (no rebuild during
-    // uncoarsening): up to 40% of the memory free at this point
+    // uncoarsening): up to 65% of the memory free at this point
     size_t kept = 0, keep_budget = 0;
     {
         size_t freeb = 0, total = 0;
         DHGP_CUDA(cudaMemGetInfo(&freeb, &total));
-        keep_budget = (size_t)(0.4 * (double)(freeb + arena_reserved(c.device)));
+        keep_budget = (size_t)(0.65 * (double)(freeb + arena_reserved(c.device)));
         const char *e = getenv("DHGP_KEEP_LEVELS_BYTES");  // tests: force the checkpoint/rebuild path
         if (e) keep_budget = (size_t)strtoull(e, nullptr, 10);
     }

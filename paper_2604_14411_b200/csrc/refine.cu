@@ -475,7 +475,6 @@ constexpr int PM_THREADS = 256;
 constexpr int PM_CAP = 8192;
 template <class Acc>
 constexpr int pm_smem() { return PM_CAP * (4 + (int)sizeof(Acc)); }
-__device__ __forceinline__ uint32_t pmslot(int32_t p) { return ((uint32_t)p * 2654435761u) >> (32 - 13); }
 
 __device__ __forceinline__ void block_best_gain(long long bg, int32_t bp, long long *r_g, int32_t *r_p, int nw,
                                                 long long *out_g, int32_t *out_p) {
@@ -515,11 +514,27 @@ __global__ void __launch_bounds__(PM_THREADS) k_propose_mid(ProposeArgs a) {
     __shared__ int32_t r_p[PM_THREADS / 32];
     __shared__ int s_nf;
     __shared__ int32_t s_f[2];
+    __shared__ long long s_runs;
     const int w = warp_id(), lane = lane_id(), nw = PM_THREADS / 32;
     const int nmid = *a.big_count;
     for (int t = blockIdx.x; t < nmid; t += gridDim.x) {
         const int32_t node = a.big_list[t];
-        for (int s = threadIdx.x; s < PM_CAP; s += PM_THREADS) {
+        const int64_t ilo = a.inc_off[node], ihi = a.inc_off[node + 1];
+        // table sized to the node: its distinct parts are at most min(K, sum of
+        // its h-edges' run counts); zeroing and scanning 8192 slots per node
+        // dominated when K is large and nodes touch few parts
+        if (threadIdx.x == 0) s_runs = 0;
+        __syncthreads();
+        long long nr = 0;
+        for (int64_t i = ilo + threadIdx.x; i < ihi; i += PM_THREADS) nr += a.r.len[a.inc_dat[i]];
+        nr = warp_sum(nr);
+        if (lane == 0) atomicAdd((unsigned long long *)&s_runs, (unsigned long long)nr);
+        __syncthreads();
+        int lg = 6;
+        while ((1ll << lg) < 2 * min((long long)a.K, s_runs) && lg < 13) lg++;
+        const int cap = 1 << lg;
+        const int limit = min(a.t.pm_limit, cap - cap / 4);
+        for (int s = threadIdx.x; s < cap; s += PM_THREADS) {
             keys[s] = -1;
             vals[s] = 0;
         }
@@ -528,7 +543,6 @@ __global__ void __launch_bounds__(PM_THREADS) k_propose_mid(ProposeArgs a) {
             sover = 0;
         }
         __syncthreads();
-        const int64_t ilo = a.inc_off[node], ihi = a.inc_off[node + 1];
         const int32_t ps = a.assign[node];
         long long total = 0, saving = 0;
         total = warp_for_runs(a.inc_dat, ilo, ihi, (int64_t)w * 32, (int64_t)nw * 32, a.r.off, a.r.len, a.wi, a.work,
@@ -536,14 +550,14 @@ __global__ void __launch_bounds__(PM_THREADS) k_propose_mid(ProposeArgs a) {
                                   const int32_t p = a.r.part[k];
                                   if (p == ps && a.r.cnt[k] == 1) saving += we;
                                   if (sover) return;
-                                  const uint32_t h = pmslot(p);
-                                  for (int probe = 0; probe < PM_CAP; probe++) {
-                                      const int slot = (h + probe) & (PM_CAP - 1);
+                                  const uint32_t h = ((uint32_t)p * 2654435761u) >> (32 - lg);
+                                  for (int probe = 0; probe < cap; probe++) {
+                                      const int slot = (h + probe) & (cap - 1);
                                       int kk = keys[slot];
                                       if (kk == -1) {
                                           const int prev = atomicCAS(&keys[slot], -1, p);
                                           if (prev == -1) {
-                                              if (atomicAdd(&snk, 1) >= a.t.pm_limit) sover = 1;
+                                              if (atomicAdd(&snk, 1) >= limit) sover = 1;
                                               kk = p;
                                           } else {
                                               kk = prev;
@@ -580,7 +594,7 @@ __global__ void __launch_bounds__(PM_THREADS) k_propose_mid(ProposeArgs a) {
         int32_t bp = -1;
         if (threadIdx.x == 0) s_nf = 0;
         __syncthreads();
-        for (int s = threadIdx.x; s < PM_CAP; s += PM_THREADS) {
+        for (int s = threadIdx.x; s < cap; s += PM_THREADS) {
             const int32_t p = keys[s];
             if (p < 0 || p == ps) continue;
             consider_part(p, saving - (total - (long long)vals[s]), a.psizes[p] + sz <= a.omega, bg, bp, &s_nf, s_f);
