@@ -76,6 +76,18 @@ struct Ctx {
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending_ev;
     std::vector<int> pending_idx;
     std::vector<double> pending_bytes;
+    // Small device -> host reads (status words, counts) go through a pinned
+    // bounce buffer: a cudaMemcpyAsync into pageable memory is staged by the
+    // driver and costs several microseconds each, and the refinement round
+    // does five of them.  The values land at their destinations in sync().
+    static constexpr size_t kPinnedBytes = 1 << 16;
+    char *pinned = nullptr;
+    size_t pin_used = 0;
+    struct PinnedRead {
+        void *dst;
+        size_t off, bytes;
+    };
+    std::vector<PinnedRead> pin_reads;
 
     template <class T>
     T *alloc(int64_t n) {
@@ -100,13 +112,27 @@ struct Ctx {
     }
     template <class T>
     void d2h(T *h, const T *d, int64_t n) {
-        if (n > 0) DHGP_CUDA(cudaMemcpyAsync(h, d, (size_t)n * sizeof(T), cudaMemcpyDeviceToHost, stream));
+        if (n <= 0) return;
+        const size_t bytes = (size_t)n * sizeof(T);
+        if (pinned && bytes <= 4096) {
+            if (pin_used + bytes > kPinnedBytes) sync();
+            DHGP_CUDA(cudaMemcpyAsync(pinned + pin_used, d, bytes, cudaMemcpyDeviceToHost, stream));
+            pin_reads.push_back(PinnedRead{(void *)h, pin_used, bytes});
+            pin_used += (bytes + 15) & ~(size_t)15;
+            return;
+        }
+        DHGP_CUDA(cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, stream));
     }
     template <class T>
     void d2d(T *dst, const T *src, int64_t n) {
         if (n > 0) DHGP_CUDA(cudaMemcpyAsync(dst, src, (size_t)n * sizeof(T), cudaMemcpyDeviceToDevice, stream));
     }
-    void sync() { DHGP_CUDA(cudaStreamSynchronize(stream)); }
+    void sync() {
+        DHGP_CUDA(cudaStreamSynchronize(stream));
+        for (const PinnedRead &r : pin_reads) memcpy(r.dst, pinned + r.off, r.bytes);
+        pin_reads.clear();
+        pin_used = 0;
+    }
 
     // profiling brackets: kbegin(name) ... kend(bytes)
     int kbegin(const char *name);

@@ -199,6 +199,7 @@ static size_t arena_reserved(int device) {
 void arena_free(int device, void *p) { g_arena[device].release(p); }
 static cudaStream_t g_streams[64];
 static int g_sms[64];
+static char *g_pinned[64];
 
 static void setup(Ctx &c, int device) {
     if (device < 0 || device >= 64) throw Error{DHGP_ERR_ARG, "bad device ordinal"};
@@ -207,9 +208,11 @@ static void setup(Ctx &c, int device) {
     if (!g_streams[device]) {
         DHGP_CUDA(cudaStreamCreateWithFlags(&g_streams[device], cudaStreamNonBlocking));
         DHGP_CUDA(cudaDeviceGetAttribute(&g_sms[device], cudaDevAttrMultiProcessorCount, device));
+        DHGP_CUDA(cudaHostAlloc((void **)&g_pinned[device], Ctx::kPinnedBytes, cudaHostAllocDefault));
     }
     c.stream = g_streams[device];
     c.num_sms = g_sms[device];
+    c.pinned = g_pinned[device];
 }
 
 void seams_setup(Ctx &c, int device) { setup(c, device); }
