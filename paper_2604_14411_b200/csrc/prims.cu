@@ -943,6 +943,41 @@ void merge_union_write2(Ctx &c, int64_t nc, const int32_t *ma, const int32_t *mb
 }
 
 // ===========================================================================
+// several small zero-fills in one launch (blockIdx.y = buffer)
+// ===========================================================================
+namespace {
+struct ZeroSet {
+    void *p[8];
+    int64_t bytes[8];
+};
+__global__ void k_zero_many(ZeroSet z) {
+    char *p = (char *)z.p[blockIdx.y];
+    const int64_t nb = z.bytes[blockIdx.y];
+    const int64_t nw = nb >> 2;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nw; i += (int64_t)gridDim.x * blockDim.x)
+        ((uint32_t *)p)[i] = 0u;
+    if (blockIdx.x == 0 && threadIdx.x < (nb & 3)) p[nw * 4 + threadIdx.x] = 0;
+}
+}  // namespace
+
+void zero_many(Ctx &c, std::initializer_list<std::pair<void *, int64_t>> bufs) {
+    ZeroSet z;
+    int n = 0;
+    int64_t mx = 0;
+    for (const auto &b : bufs) {
+        if (b.second <= 0 || !b.first) continue;
+        z.p[n] = b.first;
+        z.bytes[n] = b.second;
+        mx = std::max(mx, b.second);
+        n++;
+    }
+    if (n == 0) return;
+    const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(mx / 4, 256), 64));
+    k_zero_many<<<dim3(gx, n), 256, 0, c.stream>>>(z);
+    DHGP_LAUNCHED(c);
+}
+
+// ===========================================================================
 // fills and the stable transpose
 // ===========================================================================
 namespace {

@@ -2,6 +2,8 @@
 // sort, tiered per-segment sorts and sorted-set merges.  All integer, all
 // deterministic.
 #pragma once
+#include <initializer_list>
+#include <utility>
 #include "common.cuh"
 
 namespace dhgp {
@@ -27,6 +29,8 @@ void radix_sort_pairs(Ctx &c, uint64_t *keys, uint32_t *vals, uint64_t *ktmp, ui
 // (one launch; not stable in general, stable when vals ascend in input order
 // and are distinct).
 constexpr int64_t kSmallSort = 4096;
+// up to eight zero-fills (pointer, bytes; 4-byte aligned) in one launch
+void zero_many(Ctx &c, std::initializer_list<std::pair<void *, int64_t>> bufs);
 // the same for unique keys carrying their value in the low 32 bits
 void small_sort_packed(Ctx &c, uint64_t *keys, uint32_t *vals, int64_t n);
 void small_sort_pairs(Ctx &c, uint64_t *keys, uint32_t *vals, int64_t n);

@@ -1945,12 +1945,12 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
     static int g_ru = resident_grid(c, k_runs_update, 256, 0);
     static int g_me = resident_grid(c, k_mover_edges, 256, 0);
     static int g_ap = resident_grid(c, k_apply_inc, 256, 0);
-    auto runs_update = [&]() {
+    auto runs_update = [&](bool reset) {
         k_runs_update<<<g_ru, 256, 0, c.stream>>>(st.elist, st.ctr + CT_ELIST, st.edirty, L.pin_off, L.pin_dat,
                                                  L.dst_off, L.dst_dat, assign, W.wi, r, conn_d, pinbound, K, st.ndirty,
                                                  st.nlist, st.ctr + CT_NLIST);
         DHGP_LAUNCHED(c);
-        c.zero(st.ctr + CT_ELIST, 1);
+        if (reset) c.zero(st.ctr + CT_ELIST, 1);
     };
 
     bool need_final = false;
@@ -1967,14 +1967,17 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
         } else {
             // --- only what the last moves / the projection touched -----------
             KScope ks(c, "runs_update");
-            runs_update();
-            if (st.moved && N > 0) {
+            runs_update(false);
+            const bool mp = st.moved && N > 0;
+            if (mp) {
                 k_mark_psize<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(N, target, st.fsens, st.fpart, st.pflags,
                                                                            psizes, L.size, omega, st.ndirty,
                                                                            st.nlist, st.ctr + CT_NLIST);
                 DHGP_LAUNCHED(c);
-                c.zero(st.pflags, K);
             }
+            // the dirty-edge list is consumed, the shrink flags too; the
+            // propose counters start at zero
+            zero_many(c, {{st.ctr + CT_ELIST, 4}, {st.pflags, mp ? (int64_t)K : 0}, {ctr, 16}});
         }
         st.moved = false;
         // --- A14 propose (warp tier + block tier, no host sync) -------------
@@ -1985,7 +1988,7 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
                 work = c.alloc<unsigned long long>(1);
                 c.zero(work, 1);
             }
-            c.zero(ctr, 4);
+            if (full) c.zero(ctr, 4);
             ProposeArgs a{N, K, L.inc_off, L.inc_dat, W.wi, r, assign, psizes, L.size, omega,
                           target, gain, ctr, big, ctr + 1, big2, ctr + 2, tiers(), 0, N};
             a.fsens = st.fsens;
@@ -2026,7 +2029,8 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
                         <<<blocks, PR_WARPS * 32, pr_smem<unsigned long long>(), c.stream>>>(a);
                 }
                 DHGP_LAUNCHED(c);
-                if (!full) c.zero(st.ctr + CT_NLIST, 1);
+                // the dirty-node list is consumed; the mover count starts at zero
+                zero_many(c, {{full ? nullptr : (void *)(st.ctr + CT_NLIST), 4}, {dM, 8}});
                 KScope kh(c, "propose_heavy");
                 if (small_k) {
                     if (narrow) {
@@ -2103,7 +2107,7 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
         // compaction then sorts correctly; else the ordered flags + scan
         const bool packed = gmax_bits <= 32;
         if (packed) {
-            c.zero(dM, 1);
+            if (N == 0) c.zero(dM, 1);
             if (N > 0) {
                 k_mover_compact<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(N, target, gain, W.wsum, mk, mv, pos,
                                                                              (unsigned long long *)dM);
@@ -2162,12 +2166,7 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
         {
             KScope ks(c, "seq_gains", 0.0);
             unsigned long long *gacc = (unsigned long long *)gseq_acc;
-            c.zero(gacc, M);
-            c.zero(sg_ctr, 2);
-            c.zero(ctr, 4);
-            c.zero(ev_from, M);
-            c.zero(ev_to, M);
-            c.zero(ecount, 1);
+            zero_many(c, {{gacc, 8 * M}, {sg_ctr, 8}, {ctr, 16}, {ev_from, 4 * M}, {ev_to, 4 * M}, {ecount, 8}});
             if (L.E > 0) {
                 static int g_re = resident_grid(c, k_round_edges, 256, 0);
                 const unsigned gre = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(L.E, 8), g_re));
@@ -2298,7 +2297,7 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
     if (need_final) {
         // connectivity after the last applied round
         if (st.inc) {
-            runs_update();
+            runs_update(true);
             unsigned long long h = 0;
             c.d2h(&h, conn_d, 1);
             c.sync();
