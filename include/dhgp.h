@@ -195,6 +195,12 @@ int dhgp_neighbors(const dhgp_graph *g, int32_t device, int64_t *nb_off, int32_t
 void dhgp_free(void *p);
 /* hgraph.check_feasibility — hgraph.py:376-401 (message in last_error) */
 int dhgp_check_feasibility(const dhgp_graph *g, int64_t max_size, int64_t max_inbound, int32_t device);
+/* baselines.one_pass (method 0, baselines.py:16-40) and
+ * baselines.overlap_greedy (method 1, baselines.py:43-91): the reference's
+ * comparison partitioners, bit-identical; check_feasibility first.
+ * assign_out: [num_nodes], caller-owned. */
+int dhgp_baseline(const dhgp_graph *g, int64_t max_size, int64_t max_inbound, int32_t method, int32_t device,
+                  int32_t *assign_out, int32_t *num_parts_out);
 /* hgraph.partition_sizes / distinct_inbound_sizes / connectivity —
  * hgraph.py:317-356 */
 int dhgp_evaluate(const dhgp_graph *g, const int32_t *assign, int32_t num_parts, int32_t device, int64_t *sizes_out,

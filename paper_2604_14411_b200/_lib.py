@@ -84,7 +84,7 @@ EXPORTS = [
     "dhgp_last_error", "dhgp_build_info", "dhgp_device_count", "dhgp_partition", "dhgp_stats_free",
     "dhgp_session_create", "dhgp_session_partition", "dhgp_session_destroy", "dhgp_session_kernel_stats",
     "dhgp_session_set_profiling", "dhgp_incidence", "dhgp_neighbors", "dhgp_free", "dhgp_check_feasibility",
-    "dhgp_evaluate", "dhgp_union_size_sorted", "dhgp_fill_histograms", "dhgp_select_first_valid",
+    "dhgp_evaluate", "dhgp_baseline", "dhgp_union_size_sorted", "dhgp_fill_histograms", "dhgp_select_first_valid",
     "dhgp_resolve_matching", "dhgp_connectivity_value", "dhgp_compute_pins", "dhgp_propose_moves",
     "dhgp_sequence_gains", "dhgp_build_events_and_select",
     "dhgp_comm_nccl_unique_id", "dhgp_comm_init_nccl", "dhgp_comm_init_host", "dhgp_comm_set_min_units",
