@@ -280,6 +280,66 @@ __global__ void k_nbr_write(int64_t X, const uint64_t *keys, const uint8_t *keep
     }                                       \
     return DHGP_OK;
 
+namespace {
+// build_events_and_select (refine.py:178-247) for the seam, as one
+// sequential walk in move order: the running per-(part, h-edge) destination
+// counts (a working copy of the dense pins_in), the per-part size and
+// distinct-inbound values and their violation flags are exactly the groups
+// _track_violations forms — every (part, move) group of both tracks sits at
+// the move's source or target part, and each part's groups are visited in
+// move order.  Then active = cumsum(delta) and the smallest argmax of the
+// sequential f64 prefix gain among active == 0 prefixes.
+__global__ void k_seam_select(int32_t M, int32_t K, const int64_t *in_off, const int32_t *in_dat,
+                              const int32_t *node_size, const int32_t *node, const int32_t *from, const int32_t *to,
+                              const double *gain_seq, int32_t *pins_in, int64_t *psize, int64_t *pinb, int64_t omega,
+                              int64_t delta, int64_t *active, int64_t *k_out, double *total) {
+    if (threadIdx.x || blockIdx.x) return;
+    int64_t act = 0;
+    active[0] = 0;
+    for (int32_t i = 0; i < M; i++) {
+        const int32_t n = node[i], f = from[i], t = to[i];
+        int64_t tog = 0;
+        // size track: (f, i, -size), (t, i, +size)
+        const int64_t s = node_size[n];
+        {
+            const bool b0 = psize[f] > omega, b1 = psize[t] > omega;
+            psize[f] -= s;
+            psize[t] += s;
+            const bool a0 = psize[f] > omega, a1 = psize[t] > omega;
+            tog += (a0 != b0 ? (a0 ? 1 : -1) : 0) + (a1 != b1 ? (a1 ? 1 : -1) : 0);
+        }
+        // inbound track: per inbound h-edge, 1 -> 0 at f and 0 -> 1 at t
+        int64_t df = 0, dt = 0;
+        for (int64_t j = in_off[n]; j < in_off[n + 1]; j++) {
+            const int64_t e = in_dat[j];
+            if (--pins_in[e * K + f] == 0) df--;
+            if (++pins_in[e * K + t] == 1) dt++;
+        }
+        {
+            const bool b0 = pinb[f] > delta, b1 = pinb[t] > delta;
+            pinb[f] += df;
+            pinb[t] += dt;
+            const bool a0 = pinb[f] > delta, a1 = pinb[t] > delta;
+            tog += (a0 != b0 ? (a0 ? 1 : -1) : 0) + (a1 != b1 ? (a1 ? 1 : -1) : 0);
+        }
+        act += tog;
+        active[i + 1] = act;
+    }
+    double cum = 0.0, best = 0.0;
+    int64_t k = 0;  // the empty prefix (active[0] == 0) always competes
+    for (int32_t j = 1; j <= M; j++) {
+        cum += gain_seq[j - 1];
+        if (active[j] == 0 && cum > best) {
+            best = cum;
+            k = j;
+        }
+    }
+    *k_out = k;
+    *total = best;
+}
+
+}  // namespace
+
 extern "C" {
 
 int dhgp_incidence(const dhgp_graph *g, int32_t device, int64_t *in_off, int32_t *in_dat, int64_t *out_off,
@@ -597,11 +657,20 @@ int dhgp_build_events_and_select(int32_t N, const int64_t *in_off, const int32_t
                                  const int64_t *part_sizes, const int64_t *part_inbound, int64_t max_size,
                                  int64_t max_inbound, int32_t device, int64_t *k_out, double *total_gain_out,
                                  int64_t *active) {
-    (void)N; (void)in_off; (void)in_dat; (void)node_size; (void)E; (void)K; (void)M; (void)node; (void)from_part;
-    (void)to_part; (void)gain_seq; (void)pins_in; (void)part_sizes; (void)part_inbound; (void)max_size;
-    (void)max_inbound; (void)device; (void)k_out; (void)total_gain_out; (void)active;
-    set_error(DHGP_ERR_UNSUPPORTED, "dhgp_build_events_and_select: standalone seam not built yet");
-    return DHGP_ERR_UNSUPPORTED;
+    SEAM_BEGIN
+    DevBuf<int64_t> io(c, in_off, (int64_t)N + 1), ps(c, part_sizes, K), pi(c, part_inbound, K);
+    DevBuf<int32_t> id(c, in_dat, in_off[N]), ns(c, node_size, N), cnt(c, pins_in, (int64_t)E * K);
+    DevBuf<int32_t> dn(c, node, M), df(c, from_part, M), dt(c, to_part, M);
+    DevBuf<double> dg(c, gain_seq, M);
+    DevBuf<int64_t> act(c, (int64_t)M + 1), res(c, 1);
+    DevBuf<double> tot(c, 1);
+    k_seam_select<<<1, 1, 0, c.stream>>>(M, K, io.p, id.p, ns.p, dn.p, df.p, dt.p, dg.p, cnt.p, ps.p, pi.p, max_size,
+                                         max_inbound, act.p, res.p, tot.p);
+    DHGP_LAUNCHED(c);
+    act.get(active);
+    res.get(k_out);
+    tot.get(total_gain_out);
+    SEAM_END
 }
 
 }  // extern "C"

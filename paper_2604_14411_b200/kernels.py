@@ -153,8 +153,29 @@ def sequence_gains(inc_off, inc_dat, pin_off, pin_dat, w, pins, node, from_part,
     return out[:m]
 
 
+def build_events_and_select(num_nodes, in_off, in_dat, node_size, node, from_part, to_part, gain_seq, pins_in,
+                            part_sizes, part_inbound, max_size, max_inbound):
+    """refine.build_events_and_select (refine.py:178-247) over explicit
+    arrays: the dense pins_in matrix (E x K) as in the reference.  Returns
+    (k, total_gain, active)."""
+    in_off, in_dat, node_size = _i64(in_off), _i32(in_dat), _i32(node_size)
+    node, from_part, to_part, gain_seq = _i32(node), _i32(from_part), _i32(to_part), _f64(gain_seq)
+    pins_in, part_sizes, part_inbound = _i32(pins_in), _i64(part_sizes), _i64(part_inbound)
+    m = len(node)
+    active = np.zeros(m + 1, dtype=np.int64)
+    k = C.c_int64(0)
+    tg = C.c_double(0.0)
+    rc = _lib.load().dhgp_build_events_and_select(
+        C.c_int32(num_nodes), _lib.ptr(in_off), _lib.ptr(in_dat), _lib.ptr(node_size), C.c_int32(pins_in.shape[0]),
+        C.c_int32(pins_in.shape[1]), C.c_int32(m), _lib.ptr(node), _lib.ptr(from_part), _lib.ptr(to_part),
+        _lib.ptr(gain_seq), _lib.ptr(pins_in), _lib.ptr(part_sizes), _lib.ptr(part_inbound), C.c_int64(max_size),
+        C.c_int64(max_inbound), _dev(), C.byref(k), C.byref(tg), _lib.ptr(active))
+    _lib.raise_for(rc)
+    return int(k.value), float(tg.value), active
+
+
 __all__ = [
     "available_backends", "active_backend", "set_backend", "get_module", "union_size_sorted",
     "fill_histograms", "select_first_valid", "resolve_matching", "connectivity_value", "compute_pins",
-    "propose_moves", "sequence_gains", "DhgError",
+    "propose_moves", "sequence_gains", "build_events_and_select", "DhgError",
 ]

@@ -134,6 +134,11 @@ def test_kernel_seams_match_reference():
         gseq = K.sequence_gains(g.node_inc.offsets, g.node_inc.data, g.edge_pins.offsets, g.edge_pins.data, w, pins,
                                 node, assign[node], tgt[node], gain[node], z[p + "pos"])
         assert np.array_equal(gseq, z[p + "gseq"])
+        k, tg, active = K.build_events_and_select(g.num_nodes, g.node_in.offsets, g.node_in.data, g.node_size, node,
+                                                  assign[node], tgt[node], gseq, pins_in, z[p + "psz"],
+                                                  z[p + "pinb"], int(z[p + "omega"]), int(z[p + "delta"]))
+        assert k == int(z[p + "sel_k"]) and tg == float(z[p + "sel_total"])
+        assert np.array_equal(active, z[p + "sel_active"])
 
 
 # ---------------------------------------------------------------------------
