@@ -528,12 +528,12 @@ static void run_partition(Ctx &c, const DInput &in, const dhgp_config &cfg, Part
             obs(&ev, user);
         };
     }
-    // incremental refinement (refine.cuh) unless an h-edge is too wide for
-    // the warp run-list kernel, or DHGP_FULL_REFINE=1 (tests: both modes)
+    // incremental refinement (refine.cuh) unless DHGP_FULL_REFINE=1 (tests:
+    // both modes)
     RefineState rst;
     {
         const char *fe = getenv("DHGP_FULL_REFINE");
-        const bool inc = in.max_edge_pins <= 128 && !(fe && fe[0] == '1');
+        const bool inc = !(fe && fe[0] == '1');
         refine_state_init(c, rst, levels[0], K, inc);
     }
     try {

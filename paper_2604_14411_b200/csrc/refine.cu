@@ -1580,7 +1580,8 @@ constexpr int RU_SMEM_K = 8192;
 __global__ void k_runs_update(const int32_t *elist, const int32_t *ecount, int32_t *edirty, const int64_t *pin_off,
                               const int32_t *pin_dat, const int64_t *dst_off, const int32_t *dst_dat,
                               const int32_t *assign, const int64_t *wi, Runs r, unsigned long long *conn,
-                              int64_t *pinbound, int32_t K, int32_t *ndirty, int32_t *nlist, int32_t *ncount) {
+                              int64_t *pinbound, int32_t K, int32_t *ndirty, int32_t *nlist, int32_t *ncount,
+                              int32_t *wide, int32_t *wide_count) {
     __shared__ int32_t sdelta[RU_SMEM_K];
     __shared__ int32_t s_oldp[8][128], s_oldc[8][128];
     const bool local = K <= RU_SMEM_K;
@@ -1597,6 +1598,10 @@ __global__ void k_runs_update(const int32_t *elist, const int32_t *ecount, int32
         const bool moved = flag & 2;
         const int64_t plo = pin_off[e], lo = r.off[e];
         const int len = (int)(pin_off[e + 1] - plo);
+        if (len > 128) {  // k_runs_update_wide takes it (a block per h-edge)
+            if (lane_id() == 0) wide[atomicAdd(wide_count, 1)] = e;
+            continue;
+        }
         const int32_t old = r.len[e];
         int32_t *op = s_oldp[warp_id()], *oc = s_oldc[warp_id()];
         if (moved)
@@ -1685,6 +1690,115 @@ __device__ __forceinline__ void grid_incidences(int64_t nitems, NodeOf node_of, 
             f(i, inc_dat[j]);
     }
 }
+
+// The same update for h-edges of more than 128 pin slots (power-law inputs):
+// a CTA per h-edge sorts the pins' parts in shared memory (<= kMaxSegSort),
+// derives the runs by a block scan of the heads, and applies the identical
+// pinbound / connectivity differences and pin marking.
+__global__ void __launch_bounds__(1024) k_runs_update_wide(const int32_t *wide, const int32_t *wide_count,
+                                                           int32_t *edirty, const int64_t *pin_off,
+                                                           const int32_t *pin_dat, const int64_t *dst_off,
+                                                           const int32_t *dst_dat, const int32_t *assign,
+                                                           const int64_t *wi, Runs r, unsigned long long *conn,
+                                                           int64_t *pinbound, int32_t *ndirty, int32_t *nlist,
+                                                           int32_t *ncount) {
+    extern __shared__ unsigned long long smem_u64[];
+    uint32_t *sv = (uint32_t *)smem_u64;              // [kMaxSegSort] sorted parts
+    int32_t *op = (int32_t *)(sv + kMaxSegSort);      // [kMaxSegSort] old parts
+    int32_t *oc = op + kMaxSegSort;                   // [kMaxSegSort] old counts
+    uint8_t *flip = (uint8_t *)(oc + kMaxSegSort);    // [kMaxSegSort] per new run
+    __shared__ int32_t s_wsum[32];
+    __shared__ int s_same;
+    const int t = threadIdx.x, lane = lane_id(), w = warp_id(), nwarp = blockDim.x >> 5;
+    const int nwide = *wide_count;
+    for (int q = blockIdx.x; q < nwide; q += gridDim.x) {
+        const int32_t e = wide[q];
+        const bool moved = edirty[e] & 2;
+        const int64_t plo = pin_off[e], lo = r.off[e];
+        const int len = (int)(pin_off[e + 1] - plo);
+        const int32_t old = r.len[e];
+        for (int j = t; j < old; j += blockDim.x) {
+            op[j] = r.part[lo + j];
+            oc[j] = r.cnt[lo + j];
+            if (moved && r.cin[lo + j] > 0) atomicAdd((unsigned long long *)&pinbound[op[j]], ~0ull);
+        }
+        const int np = next_pow2(len);
+        for (int j = t; j < np; j += blockDim.x) sv[j] = j < len ? (uint32_t)assign[pin_dat[plo + j]] : 0xffffffffu;
+        block_bitonic_sort32(sv, np);
+        // heads -> run slots by a block exclusive scan (one pass per 1024 slots)
+        int base = 0;
+        for (int c0 = 0; c0 < len; c0 += blockDim.x) {
+            const int i = c0 + t;
+            const bool head = i < len && (i == 0 || sv[i] != sv[i - 1]);
+            const uint32_t bal = __ballot_sync(FULL_MASK, head);
+            if (lane == 0) s_wsum[w] = __popc(bal);
+            __syncthreads();
+            int before = base, tot = 0;
+            for (int j = 0; j < nwarp; j++) {
+                if (j < w) before += s_wsum[j];
+                tot += s_wsum[j];
+            }
+            if (head) {
+                const int k = before + __popc(bal & ((1u << lane) - 1u));
+                r.part[lo + k] = (int32_t)sv[i];
+                r.cin[lo + k] = 0;
+            }
+            base += tot;
+            __syncthreads();
+        }
+        const int lam = base;
+        // run lengths from the sorted parts (binary searches; no in-place hazard)
+        for (int k = t; k < lam; k += blockDim.x) {
+            const uint32_t p = (uint32_t)r.part[lo + k];
+            int a0 = 0, a1 = len;  // first index with sv >= p
+            while (a0 < a1) {
+                const int m = (a0 + a1) >> 1;
+                if (sv[m] < p) a0 = m + 1; else a1 = m;
+            }
+            int b0 = a0, b1 = len;  // first index with sv > p
+            while (b0 < b1) {
+                const int m = (b0 + b1) >> 1;
+                if (sv[m] <= p) b0 = m + 1; else b1 = m;
+            }
+            r.cnt[lo + k] = b0 - a0;
+        }
+        __syncthreads();
+        for (int64_t qd = dst_off[e] + t; qd < dst_off[e + 1]; qd += blockDim.x) {
+            const int32_t k = run_find(r, lo, lam, assign[dst_dat[qd]]);
+            atomicAdd(&r.cin[lo + k], 1);
+        }
+        __syncthreads();
+        if (moved) {
+            for (int k = t; k < lam; k += blockDim.x)
+                if (r.cin[lo + k] > 0) atomicAdd((unsigned long long *)&pinbound[r.part[lo + k]], 1ull);
+            if (t == 0) s_same = lam == old;
+            __syncthreads();
+            if (s_same)
+                for (int k = t; k < lam; k += blockDim.x) {
+                    if (r.part[lo + k] != op[k]) s_same = 0;
+                    flip[k] = (r.cnt[lo + k] == 1) != (oc[k] == 1);
+                }
+            __syncthreads();
+            const bool same = s_same;
+            for (int64_t j = plo + t; j < plo + len; j += blockDim.x) {
+                const int32_t n = pin_dat[j];
+                bool mark = !same;
+                if (!mark) mark = flip[run_find(r, lo, lam, assign[n])];
+                if (mark) push_once(&ndirty[n], 1, n, nlist, ncount);
+            }
+        }
+        if (t == 0) {
+            r.len[e] = lam;
+            edirty[e] = 0;
+            if (moved) {
+                const long long d = wi[e] * (long long)((lam > 0 ? lam - 1 : 0) - (old > 0 ? old - 1 : 0));
+                if (d) atomicAdd(conn, (unsigned long long)d);
+            }
+        }
+        __syncthreads();
+    }
+}
+
 // after moves: nodes whose proposal depends on a changed part size — the
 // target no longer fits (a target that still fits stays the best eligible
 // part), or a size-filtered positive-gain part shrank and may now fit
@@ -1775,7 +1889,7 @@ __global__ void k_mark_split_edges(const int32_t *splist, const int32_t *spcount
                     [&](int64_t, int32_t e) { push_once(&edirty[e], 1, e, elist, ecount); });
 }
 
-enum { CT_NLIST = 0, CT_ELIST = 1, CT_MLIST = 2, CT_SPLIST = 3 };
+enum { CT_NLIST = 0, CT_ELIST = 1, CT_MLIST = 2, CT_SPLIST = 3, CT_WIDE = 4 };
 }  // namespace
 
 void refine_state_init(Ctx &c, RefineState &st, const DLevel &level0, int32_t K, bool incremental) {
@@ -1811,6 +1925,7 @@ void refine_state_init(Ctx &c, RefineState &st, const DLevel &level0, int32_t K,
     st.elist = c.alloc<int32_t>(e0);
     st.emflag = c.alloc<int32_t>(e0);
     st.mlist = c.alloc<int32_t>(e0);
+    st.wide = c.alloc<int32_t>(e0);
     st.ctr = c.alloc<int32_t>(8);
     st.hacc = c.alloc<long long>((int64_t)HUB_MAX * std::max(1, K));
     st.htot = c.alloc<long long>(2 * HUB_MAX);
@@ -1833,7 +1948,7 @@ void refine_state_release(Ctx &c, RefineState &st) {
                     (void *)st.pinbound, (void *)st.pflags, (void *)st.conn, (void *)st.target, (void *)st.target2,
                     (void *)st.gain, (void *)st.gain2, (void *)st.fsens, (void *)st.fsens2, (void *)st.fpart, (void *)st.fpart2, (void *)st.ndirty,
                     (void *)st.ndirty2, (void *)st.nlist, (void *)st.splist, (void *)st.ccount, (void *)st.edirty,
-                    (void *)st.elist, (void *)st.emflag, (void *)st.mlist, (void *)st.ctr, (void *)st.hacc,
+                    (void *)st.elist, (void *)st.emflag, (void *)st.mlist, (void *)st.wide, (void *)st.ctr, (void *)st.hacc,
                     (void *)st.htot, (void *)st.hdone, (void *)st.hlist})
         c.free(p);
     st = RefineState();
@@ -1945,12 +2060,25 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
     static int g_ru = resident_grid(c, k_runs_update, 256, 0);
     static int g_me = resident_grid(c, k_mover_edges, 256, 0);
     static int g_ap = resident_grid(c, k_apply_inc, 256, 0);
+    const bool wide_edges = max_edge_pins > 128;
     auto runs_update = [&](bool reset) {
         k_runs_update<<<g_ru, 256, 0, c.stream>>>(st.elist, st.ctr + CT_ELIST, st.edirty, L.pin_off, L.pin_dat,
                                                  L.dst_off, L.dst_dat, assign, W.wi, r, conn_d, pinbound, K, st.ndirty,
-                                                 st.nlist, st.ctr + CT_NLIST);
+                                                 st.nlist, st.ctr + CT_NLIST, st.wide, st.ctr + CT_WIDE);
         DHGP_LAUNCHED(c);
-        if (reset) c.zero(st.ctr + CT_ELIST, 1);
+        if (wide_edges) {
+            static bool wattr = false;
+            if (!wattr) {
+                DHGP_CUDA(cudaFuncSetAttribute(k_runs_update_wide, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)(13 * kMaxSegSort)));
+                wattr = true;
+            }
+            k_runs_update_wide<<<c.num_sms, 1024, 13 * kMaxSegSort, c.stream>>>(
+                st.wide, st.ctr + CT_WIDE, st.edirty, L.pin_off, L.pin_dat, L.dst_off, L.dst_dat, assign, W.wi, r,
+                conn_d, pinbound, st.ndirty, st.nlist, st.ctr + CT_NLIST);
+            DHGP_LAUNCHED(c);
+        }
+        if (reset) zero_many(c, {{st.ctr + CT_ELIST, 4}, {st.ctr + CT_WIDE, 4}});
     };
 
     bool need_final = false;
@@ -1977,7 +2105,7 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
             }
             // the dirty-edge list is consumed, the shrink flags too; the
             // propose counters start at zero
-            zero_many(c, {{st.ctr + CT_ELIST, 4}, {st.pflags, mp ? (int64_t)K : 0}, {ctr, 16}});
+            zero_many(c, {{st.ctr + CT_ELIST, 4}, {st.pflags, mp ? (int64_t)K : 0}, {ctr, 16}, {st.ctr + CT_WIDE, 4}});
         }
         st.moved = false;
         // --- A14 propose (warp tier + block tier, no host sync) -------------

@@ -49,6 +49,7 @@ struct RefineState {
     int32_t *nlist = nullptr, *splist = nullptr, *ccount = nullptr;  // [N0]
     int32_t *edirty = nullptr, *elist = nullptr;           // [E] dirty h-edges (bit 0 split, bit 1 moved)
     int32_t *emflag = nullptr, *mlist = nullptr;           // [E] h-edges of the round's movers
+    int32_t *wide = nullptr;                               // [E] dirty h-edges over 128 pins (block update)
     int32_t *ctr = nullptr;                                // [8] list counters
     long long *hacc = nullptr, *htot = nullptr;            // propose hub tier: [HUB_MAX x K], [2 HUB_MAX]
     int32_t *hdone = nullptr, *hlist = nullptr;            // [HUB_MAX]

@@ -360,6 +360,8 @@ def test_full_and_incremental_paths_agree(monkeypatch):
         cases.append((g, c.max_size, c.max_inbound, int(rs.choice([1, 2, 8]))))
     cases.append((graph(W.layered_snn(5, 300, fanout=32, window=96, seed=9)), 256, 4096, 8))
     cases.append((graph(W.layered_snn(8, 400, fanout=48, window=128, seed=3)), 512, 1024, 8))
+    arr = W.power_law(2500, 2500, k_max=400, seed=11)  # h-edges over 128 pins: the block run-list update
+    cases.append((graph(arr), 64, max(int(np.bincount(arr[5], minlength=2500).max()), 256), 8))
     for mode in ("1", "0"):
         monkeypatch.setenv("DHGP_FULL_REFINE", mode)
         monkeypatch.setenv("DHGP_FULL_SCORE", mode)
