@@ -190,7 +190,7 @@ struct Tiers {
     int pr_heavy_inc = 64;    // propose: incident h-edges above which a block takes the node
     int pm_limit = 3072;      // propose: distinct parts per medium-tier table
     int small_k = 4096;       // propose: K up to which escalated nodes use dense shared arrays
-    int pr_hub_inc = 512;     // propose: incident h-edges above which a node is split over many CTAs
+    int pr_hub_inc = 128;     // propose: incident h-edges above which a node is split over many CTAs
     int edge_movers = 32;     // events / sequence gains: movers per h-edge for the thread tier (<= 32)
 };
 const Tiers &tiers();

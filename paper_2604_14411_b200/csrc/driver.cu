@@ -46,6 +46,8 @@ const Tiers &tiers() {
             x.pm_limit = 3;
             x.edge_movers = 2;
         }
+        const char *h = getenv("DHGP_HUB_INC");  // tuning: propose hub-tier threshold
+        if (h) x.pr_hub_inc = atoi(h);
         return x;
     }();
     return t;

@@ -255,10 +255,16 @@ struct ProposeArgs {
     // hub tier: nodes with very many incident h-edges, split over CTAs
     int32_t *hub_list = nullptr;
     int32_t *hub_count = nullptr;
+    int32_t hub_max = 0;
+    const int32_t *hub_pref = nullptr;  // [hub_max + 1] chunk prefix (k_hub_prefix)
     unsigned long long *work = nullptr;  // profiling: algorithmic bytes
 };
-constexpr int HUB_MAX = 256;     // hubs per propose pass (more go to the block tiers)
-constexpr int HUB_CHUNK = 256;   // incident h-edges per CTA work item
+// hubs per propose pass: as many as 256 MB of accumulator rows allow (more go
+// to the block tiers); the chunk prefix over them is one small kernel
+inline int hub_max_for(int32_t K) {
+    return (int)std::max<int64_t>(256, std::min<int64_t>(1 << 15, (256ll << 20) / (8ll * std::max(1, K))));
+}
+constexpr int HUB_CHUNK = 256;  // incident h-edges per CTA work item
 
 // the next node of a persistent warp/CTA loop: all of [lo, hi), or the
 // listed nodes inside [lo, hi); -1 = done, -2 = skip (another rank's node)
@@ -395,7 +401,7 @@ __global__ void __launch_bounds__(PR_WARPS * 32) k_propose_warp(ProposeArgs a) {
         if (a.hub_list && ihi - ilo > a.t.pr_hub_inc) {  // hub: many CTAs take it
             if (lane == 0) {
                 const int slot = atomicAdd(a.hub_count, 1);
-                if (slot < HUB_MAX)
+                if (slot < a.hub_max)
                     a.hub_list[slot] = node;
                 else
                     a.big_list[atomicAdd(a.big_count, 1)] = node;
@@ -686,6 +692,36 @@ __global__ void __launch_bounds__(THREADS) k_propose_heavy(ProposeArgs a) {
 }
 
 
+// chunk counts of the listed hubs, scanned by one CTA (the hub kernel's
+// work items are (hub, chunk) pairs)
+__global__ void __launch_bounds__(1024) k_hub_prefix(const int32_t *hub_list, const int32_t *hub_count, int hub_max,
+                                                     const int64_t *inc_off, int32_t *pref) {
+    __shared__ int32_t s_wt[32];
+    const int nh = min(*hub_count, hub_max);
+    const int lane = lane_id(), w = warp_id();
+    int32_t carry = 0;
+    if (threadIdx.x == 0) pref[0] = 0;
+    for (int b = 0; b < nh; b += 1024) {
+        const int i = b + threadIdx.x;
+        int32_t cnt = 0;
+        if (i < nh) {
+            const int32_t n = hub_list[i];
+            cnt = (int32_t)cdiv_dev(inc_off[n + 1] - inc_off[n], (int64_t)HUB_CHUNK);
+        }
+        const int32_t incl = warp_incl_scan(cnt);
+        if (lane == 31) s_wt[w] = incl;
+        __syncthreads();
+        int32_t before = 0, tot = 0;
+        for (int j = 0; j < 32; j++) {
+            if (j < w) before += s_wt[j];
+            tot += s_wt[j];
+        }
+        if (i < nh) pref[i + 1] = carry + before + incl;
+        carry += tot;
+        __syncthreads();
+    }
+}
+
 // Hub tier (K <= small_k): a node with thousands of incident h-edges is cut
 // into HUB_CHUNK-edge work items spread over the grid; each CTA accumulates
 // present[] for its chunk in shared memory and adds it to the hub's global
@@ -699,27 +735,12 @@ __global__ void __launch_bounds__(256) k_propose_hub(ProposeArgs a, long long *h
     __shared__ int32_t r_p[8];
     __shared__ int s_last, s_nf;
     __shared__ int32_t s_f[2];
-    __shared__ int32_t s_pref[HUB_MAX + 1], s_wt[8];
-    const int nh = min(*a.hub_count, HUB_MAX);
+    const int nh = min(*a.hub_count, a.hub_max);
     if (nh == 0) return;
     const int w = warp_id(), lane = lane_id(), nw = 8;
     const int K = a.K;
-    // work items = (hub, chunk): chunk counts of the hubs, block-scanned
-    {
-        int32_t cnt = 0;
-        if ((int)threadIdx.x < nh) {
-            const int32_t n = a.hub_list[threadIdx.x];
-            cnt = (int32_t)cdiv_dev(a.inc_off[n + 1] - a.inc_off[n], (int64_t)HUB_CHUNK);
-        }
-        const int32_t incl = warp_incl_scan(cnt);
-        if (lane == 31) s_wt[w] = incl;
-        __syncthreads();
-        int32_t before = 0;
-        for (int j = 0; j < w; j++) before += s_wt[j];
-        s_pref[threadIdx.x + 1] = before + incl;
-        if (threadIdx.x == 0) s_pref[0] = 0;
-        __syncthreads();
-    }
+    // work items = (hub, chunk), located in the chunk prefix of k_hub_prefix
+    const int32_t *s_pref = a.hub_pref;
     const int64_t items = s_pref[nh];
     for (int64_t t = blockIdx.x; t < items; t += gridDim.x) {
         int lo = 0, hi = nh;  // the hub h with s_pref[h] <= t < s_pref[h + 1]
@@ -1927,13 +1948,16 @@ void refine_state_init(Ctx &c, RefineState &st, const DLevel &level0, int32_t K,
     st.mlist = c.alloc<int32_t>(e0);
     st.wide = c.alloc<int32_t>(e0);
     st.ctr = c.alloc<int32_t>(8);
-    st.hacc = c.alloc<long long>((int64_t)HUB_MAX * std::max(1, K));
-    st.htot = c.alloc<long long>(2 * HUB_MAX);
-    st.hdone = c.alloc<int32_t>(HUB_MAX);
-    st.hlist = c.alloc<int32_t>(HUB_MAX);
-    c.zero(st.hacc, (int64_t)HUB_MAX * std::max(1, K));
-    c.zero(st.htot, 2 * HUB_MAX);
-    c.zero(st.hdone, HUB_MAX);
+    st.hub_max = hub_max_for(K);
+    const int64_t hm = st.hub_max;
+    st.hacc = c.alloc<long long>(hm * std::max(1, K));
+    st.htot = c.alloc<long long>(2 * hm);
+    st.hdone = c.alloc<int32_t>(hm);
+    st.hlist = c.alloc<int32_t>(hm);
+    st.hpref = c.alloc<int32_t>(hm + 1);
+    c.zero(st.hacc, hm * std::max(1, K));
+    c.zero(st.htot, 2 * hm);
+    c.zero(st.hdone, hm);
     c.zero(st.pflags, K);
     c.zero(st.fsens, st.ncap);
     c.zero(st.ndirty, n0);
@@ -1949,7 +1973,7 @@ void refine_state_release(Ctx &c, RefineState &st) {
                     (void *)st.gain, (void *)st.gain2, (void *)st.fsens, (void *)st.fsens2, (void *)st.fpart, (void *)st.fpart2, (void *)st.ndirty,
                     (void *)st.ndirty2, (void *)st.nlist, (void *)st.splist, (void *)st.ccount, (void *)st.edirty,
                     (void *)st.elist, (void *)st.emflag, (void *)st.mlist, (void *)st.wide, (void *)st.ctr, (void *)st.hacc,
-                    (void *)st.htot, (void *)st.hdone, (void *)st.hlist})
+                    (void *)st.htot, (void *)st.hdone, (void *)st.hlist, (void *)st.hpref})
         c.free(p);
     st = RefineState();
 }
@@ -2127,6 +2151,8 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
             if (small_k) {
                 a.hub_list = st.hlist;
                 a.hub_count = ctr + 3;
+                a.hub_max = st.hub_max;
+                a.hub_pref = st.hpref;
             }
             if (!full) {
                 a.list = st.nlist;
@@ -2161,6 +2187,8 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
                 zero_many(c, {{full ? nullptr : (void *)(st.ctr + CT_NLIST), 4}, {dM, 8}});
                 KScope kh(c, "propose_heavy");
                 if (small_k) {
+                    k_hub_prefix<<<1, 1024, 0, c.stream>>>(st.hlist, ctr + 3, st.hub_max, L.inc_off, st.hpref);
+                    DHGP_LAUNCHED(c);
                     if (narrow) {
                         static int h32 = resident_grid(c, k_propose_hub<unsigned>, 256, 4 * kSmallK);
                         k_propose_hub<unsigned><<<h32, 256, 4 * K, c.stream>>>(a, st.hacc, st.htot, st.hdone);

@@ -51,8 +51,10 @@ struct RefineState {
     int32_t *emflag = nullptr, *mlist = nullptr;           // [E] h-edges of the round's movers
     int32_t *wide = nullptr;                               // [E] dirty h-edges over 128 pins (block update)
     int32_t *ctr = nullptr;                                // [8] list counters
-    long long *hacc = nullptr, *htot = nullptr;            // propose hub tier: [HUB_MAX x K], [2 HUB_MAX]
-    int32_t *hdone = nullptr, *hlist = nullptr;            // [HUB_MAX]
+    int32_t hub_max = 0;                                   // propose hub tier capacity
+    long long *hacc = nullptr, *htot = nullptr;            // [hub_max x K], [2 hub_max]
+    int32_t *hdone = nullptr, *hlist = nullptr;            // [hub_max]
+    int32_t *hpref = nullptr;                              // [hub_max + 1] work-item prefix
 };
 void refine_state_init(Ctx &c, RefineState &st, const DLevel &level0, int32_t K, bool incremental);
 void refine_state_release(Ctx &c, RefineState &st);
