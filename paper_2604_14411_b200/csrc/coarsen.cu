@@ -134,6 +134,54 @@ __device__ __forceinline__ void emit_tuple(const ScoreArgs &a, int32_t node, int
     }
 }
 
+// Size filter (_kernels.pyx:92) and tuple emission over a hash table's
+// slots [first, cap) with the given stride: the per-slot gathers (size, and
+// for merged clusters the neighbour's partner and carried choice) are issued
+// for U slots at once, so a thread waits for one round trip per U slots
+// rather than one per slot.
+template <int U, class Acc>
+__device__ __forceinline__ void filter_emit(const ScoreArgs &a, int32_t node, int32_t *keys, const Acc *vals,
+                                            int first, int stride, int cap) {
+    const int64_t szn = a.size[node];
+    const int32_t rn = a.mb ? a.rep[node] : 0;
+    for (int s0 = first; s0 < cap; s0 += U * stride) {
+        int32_t k[U], sz[U], mbv[U], tp[U];
+        long long ts[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int s = s0 + u * stride;
+            k[u] = s < cap ? keys[s] : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const bool v = k[u] >= 0;
+            sz[u] = v ? a.size[k[u]] : 0;
+            mbv[u] = (v && a.mb) ? a.mb[k[u]] : 0;
+            tp[u] = (v && a.mb) ? a.thr_p[k[u]] : -1;
+            ts[u] = (v && a.mb) ? (long long)a.thr_s[k[u]] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            if (k[u] < 0) continue;
+            const int s = s0 + u * stride;
+            if (szn + sz[u] > a.omega) {
+                keys[s] = -2;
+                continue;
+            }
+            // emit_tuple with the gathers above
+            if (!a.mb || mbv[u] >= 0) continue;
+            const long long h = (long long)vals[s];
+            if (tp[u] >= 0 && !(h > ts[u] || (h == ts[u] && rn >= tp[u]))) continue;
+            const int i = atomicAdd(a.tup_count, 1);
+            if (i < a.tup_cap) {
+                a.tup_v[i] = k[u];
+                a.tup_b[i] = node;
+                a.tup_h[i] = h;
+            }
+        }
+    }
+}
+
 constexpr int SS_WARPS = 8;
 constexpr int SS_CAP = 1024;   // hash slots per warp (power of two)
 // accumulator: 32-bit when the total weight < 2^32 (native shared atomics;
@@ -219,12 +267,7 @@ __global__ void __launch_bounds__(SS_WARPS * 32) k_score_warp(ScoreArgs a) {
             continue;
         }
         // size check once per candidate (_kernels.pyx:92)
-        const int64_t szn = a.size[node];
-        for (int s = lane; s < SS_CAP; s += 32) {
-            int k = keys[s];
-            if (k >= 0 && szn + a.size[k] > a.omega) keys[s] = -2;
-            else if (k >= 0) emit_tuple(a, node, k, (long long)vals[s]);
-        }
+        filter_emit<8>(a, node, keys, vals, lane, 32, SS_CAP);
         __syncwarp();
         int32_t best_m = -1;
         int64_t best_v = 0;
@@ -334,12 +377,7 @@ __global__ void __launch_bounds__(SH_THREADS) k_score_heavy(ScoreArgs a) {
             __syncthreads();
             continue;
         }
-        const int64_t szn = a.size[node];
-        for (int s = threadIdx.x; s < SH_CAP; s += SH_THREADS) {
-            int k = keys[s];
-            if (k >= 0 && szn + a.size[k] > a.omega) keys[s] = -2;
-            else if (k >= 0) emit_tuple(a, node, k, (long long)vals[s]);
-        }
+        filter_emit<8>(a, node, keys, vals, threadIdx.x, SH_THREADS, SH_CAP);
         __syncthreads();
         int32_t best_m = -1;
         long long best_v = 0;
@@ -1010,7 +1048,7 @@ int64_t resolve_matching(Ctx &c, int32_t N, const int32_t *pair, const double *s
 // ===========================================================================
 namespace {
 __global__ void k_gamma(int32_t N, const int32_t *match, const int64_t *rank, const int32_t *size, int32_t *gamma,
-                        int32_t *ma, int32_t *mb, int32_t *csize) {
+                        int32_t *ma, int32_t *mb, int32_t *csize, int32_t *mlist, int32_t *mcount) {
     int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= N) return;
     int32_t m = match[v];
@@ -1020,6 +1058,7 @@ __global__ void k_gamma(int32_t N, const int32_t *match, const int64_t *rank, co
         int64_t cn = rank[v];
         ma[cn] = (int32_t)v;
         mb[cn] = m != (int32_t)v ? m : -1;
+        if (m != (int32_t)v) mlist[atomicAdd(mcount, 1)] = (int32_t)cn;  // merged clusters (any order)
         // sizes add up; the reference casts the int64 sum to int32 (hgraph.py:226)
         csize[cn] = (int32_t)((int64_t)size[v] + (m != (int32_t)v ? (int64_t)size[m] : 0));
     }
@@ -1035,6 +1074,283 @@ __global__ void k_contract_status(int32_t N, int32_t E, const int64_t *rank, con
     status[6] = po[E];
     status[7] = io[nc];
     status[8] = co[nc];
+}
+
+// Per-node families (in, inc) of the coarse level: the sorted union of the
+// two members' lists (coarse node_in / node_inc via hgraph.py:221-236 after
+// coarsen.py:163-171).  H-edge ids are level-independent and an unmerged
+// node keeps its list, so the coarse arrays are the fine arrays with the
+// merged clusters' lists replaced by unions: runs of consecutive singleton
+// clusters are one contiguous copy, and only the merged clusters (a few
+// dozen per level on the SNN shapes) do set arithmetic, a CTA each.
+struct NodeFam {
+    const int64_t *off;
+    const int32_t *dat;
+    int64_t *cnt;            // count pass
+    const int64_t *out_off;  // write pass
+    int32_t *out;
+};
+struct NodeFams {
+    NodeFam f[2];
+};
+constexpr int kNodeChunk = 64;     // coarse nodes per copy work item (<= block size)
+constexpr int kUnionStage = 4096;  // shorter member list staged in shared memory up to this length
+
+__device__ __forceinline__ int64_t blk_excl_flags(bool f, int64_t *sh_w, int64_t *total) {
+    const int lane = lane_id(), w = warp_id(), nw = blockDim.x >> 5;
+    const uint32_t bal = __ballot_sync(FULL_MASK, f);
+    if (lane == 0) sh_w[w] = __popc(bal);
+    __syncthreads();
+    int64_t before = 0, tot = 0;
+    for (int j = 0; j < nw; j++) {
+        if (j < w) before += sh_w[j];
+        tot += sh_w[j];
+    }
+    __syncthreads();
+    *total = tot;
+    return before + __popc(bal & ((1u << lane) - 1u));
+}
+
+// thread per coarse node: a singleton's count is its member's length; zero
+// past nc (the offsets scan runs over the fine count)
+__global__ void k_node_count(int64_t nc_cap, const int64_t *d_nc, const int32_t *ma, const int32_t *mb, NodeFams fs) {
+    const NodeFam &f = fs.f[blockIdx.y];
+    const int64_t nc = *d_nc;
+    for (int64_t cn = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; cn < nc_cap;
+         cn += (int64_t)gridDim.x * blockDim.x) {
+        if (cn >= nc) {
+            f.cnt[cn] = 0;
+        } else if (mb[cn] < 0) {
+            const int32_t a = ma[cn];
+            f.cnt[cn] = f.off[a + 1] - f.off[a];
+        }
+    }
+}
+
+// Merged clusters, a CTA each (any order): the union of the members' sorted
+// h-edge lists, |A u B| in the count pass, the list in the write pass.
+//  - bitmap: the two lists are set in a shared-memory bitmap over the h-edge
+//    ids (when E/8 bytes fit and the lists are long enough to pay for the
+//    scan); the union is the set bits in order (block scan of popcounts);
+//  - staged: the shorter list S sits in shared memory with, per element, the
+//    running count of S-only elements: x = L[i] lands at i + (S-only
+//    elements below x), y = S[j] not in L at lb_L(y) + (S-only before j);
+//  - otherwise both directions by binary search in global memory.
+// The count pass also flags, in emark, the h-edges of the absorbed member:
+// only their src / dst / pin lists can map to an unsorted or duplicated
+// gamma image (gamma is strictly increasing on the minimum members).
+constexpr int UN_THREADS = 1024;
+template <bool WRITE>
+__global__ void __launch_bounds__(UN_THREADS) k_node_union(const int32_t *ma, const int32_t *mb, const int32_t *mlist,
+                                                           const int32_t *mcount, NodeFams fs, uint8_t *emark,
+                                                           int words) {
+    extern __shared__ uint32_t s_bm[];
+    __shared__ int32_t s_val[kUnionStage], s_pre[kUnionStage + 1];
+    __shared__ int64_t sh[32];
+    const NodeFam &f = fs.f[blockIdx.y];
+    const int n = *mcount;
+    for (int t = blockIdx.x; t < n; t += gridDim.x) {
+        const int32_t cn = mlist[t], a = ma[cn], b = mb[cn];
+        const int64_t alo = f.off[a], na = f.off[a + 1] - alo, blo = f.off[b], nb = f.off[b + 1] - blo;
+        if (!WRITE && emark && blockIdx.y == 1)
+            for (int64_t i = threadIdx.x; i < nb; i += blockDim.x) emark[f.dat[blo + i]] = 1;
+        const bool a_short = na <= nb;
+        const int32_t *S = f.dat + (a_short ? alo : blo), *L = f.dat + (a_short ? blo : alo);
+        const int64_t ns = a_short ? na : nb, nl = a_short ? nb : na;
+        if (words > 0 && 8 * (na + nb) >= words) {
+            for (int w = threadIdx.x; w < words; w += blockDim.x) s_bm[w] = 0u;
+            __syncthreads();
+            for (int64_t i = threadIdx.x; i < na; i += blockDim.x) {
+                const int32_t x = f.dat[alo + i];
+                atomicOr(&s_bm[x >> 5], 1u << (x & 31));
+            }
+            for (int64_t i = threadIdx.x; i < nb; i += blockDim.x) {
+                const int32_t x = f.dat[blo + i];
+                atomicOr(&s_bm[x >> 5], 1u << (x & 31));
+            }
+            __syncthreads();
+            const int per = (words + blockDim.x - 1) / blockDim.x;
+            const int w0 = min(words, (int)threadIdx.x * per), w1 = min(words, w0 + per);
+            int64_t cnt = 0;
+            for (int w = w0; w < w1; w++) cnt += __popc(s_bm[w]);
+            int64_t tot;
+            // exclusive block prefix of the per-thread counts
+            const int lane = lane_id(), wp = warp_id(), nwp = blockDim.x >> 5;
+            const int64_t incl = warp_incl_scan(cnt);
+            if (lane == 31) sh[wp] = incl;
+            __syncthreads();
+            int64_t before = 0;
+            tot = 0;
+            for (int j = 0; j < nwp; j++) {
+                if (j < wp) before += sh[j];
+                tot += sh[j];
+            }
+            before += incl - cnt;
+            if (WRITE) {
+                int32_t *o = f.out + f.out_off[cn] + before;
+                for (int w = w0; w < w1; w++) {
+                    uint32_t bits = s_bm[w];
+                    while (bits) {
+                        const int bpos = __ffs(bits) - 1;
+                        bits &= bits - 1;
+                        *o++ = w * 32 + bpos;
+                    }
+                }
+            } else if (threadIdx.x == 0) {
+                f.cnt[cn] = tot;
+            }
+            __syncthreads();
+            continue;
+        }
+        if (!WRITE) {
+            int64_t common = 0;
+            for (int64_t i = threadIdx.x; i < ns; i += blockDim.x) common += bsearch_dev(L, 0, nl, S[i]) >= 0;
+            const int64_t tot = block_sum<int64_t>(common, sh);
+            if (threadIdx.x == 0) f.cnt[cn] = na + nb - tot;
+            __syncthreads();
+            continue;
+        }
+        int32_t *o = f.out + f.out_off[cn];
+        if (ns <= kUnionStage) {
+            int64_t run = 0;
+            for (int64_t base = 0; base < ns; base += blockDim.x) {
+                const int64_t j = base + threadIdx.x;
+                bool only = false;
+                int32_t y = 0;
+                int64_t lb = 0;
+                if (j < ns) {
+                    y = S[j];
+                    lb = lower_bound_dev<int32_t>(L, 0, nl, y);
+                    only = !(lb < nl && L[lb] == y);
+                    s_val[j] = y;
+                }
+                int64_t tot;
+                const int64_t ex = blk_excl_flags(only, sh, &tot);
+                if (j < ns) {
+                    s_pre[j] = (int32_t)(run + ex);
+                    if (only) o[lb + run + ex] = y;
+                }
+                run += tot;
+            }
+            if (threadIdx.x == 0) s_pre[ns] = (int32_t)run;
+            __syncthreads();
+            const int B = blockDim.x;
+            int64_t i = threadIdx.x;
+            for (; i + B < nl; i += 2 * B) {
+                const int32_t x0 = L[i], x1 = L[i + B];
+                const int64_t p0 = lower_bound_dev<int32_t>(s_val, 0, ns, x0);
+                const int64_t p1 = lower_bound_dev<int32_t>(s_val, 0, ns, x1);
+                o[i + s_pre[p0]] = x0;
+                o[i + B + s_pre[p1]] = x1;
+            }
+            for (; i < nl; i += B) {
+                const int32_t x = L[i];
+                o[i + s_pre[lower_bound_dev<int32_t>(s_val, 0, ns, x)]] = x;
+            }
+            __syncthreads();
+            continue;
+        }
+        const int32_t *A = f.dat + alo, *Bl = f.dat + blo;
+        int64_t run = 0;
+        for (int64_t base = 0; base < na; base += blockDim.x) {
+            const int64_t i = base + threadIdx.x;
+            int64_t lb = 0;
+            bool in_other = false;
+            int32_t x = 0;
+            if (i < na) {
+                x = A[i];
+                lb = lower_bound_dev<int32_t>(Bl, 0, nb, x);
+                in_other = lb < nb && Bl[lb] == x;
+            }
+            int64_t tot;
+            const int64_t ex = blk_excl_flags(in_other, sh, &tot);
+            if (i < na) o[i + lb - (run + ex)] = x;
+            run += tot;
+        }
+        run = 0;
+        for (int64_t base = 0; base < nb; base += blockDim.x) {
+            const int64_t j = base + threadIdx.x;
+            int64_t lb = 0;
+            bool in_other = false;
+            int32_t y = 0;
+            if (j < nb) {
+                y = Bl[j];
+                lb = lower_bound_dev<int32_t>(A, 0, na, y);
+                in_other = lb < na && A[lb] == y;
+            }
+            int64_t tot;
+            const int64_t ex = blk_excl_flags(in_other, sh, &tot);
+            if (j < nb && !in_other) o[lb + j - (run + ex)] = y;
+            run += tot;
+        }
+    }
+}
+
+// Singleton lists.  Work item = (chunk of kNodeChunk coarse nodes, slice):
+// a chunk of consecutive singletons (no merged cluster and no absorbed member
+// between them) is one contiguous range, split over `split` CTAs; otherwise
+// its singleton lists are flattened over the CTAs of the chunk (a slot's list
+// is found by a search over the chunk's prefix).  Merged clusters are skipped.
+__global__ void __launch_bounds__(256) k_node_write(int64_t nc, int split, const int32_t *ma, const int32_t *mb,
+                                                    NodeFams fs) {
+    const NodeFam &f = fs.f[blockIdx.y];
+    __shared__ int64_t s_src[kNodeChunk], s_dst[kNodeChunk], s_end[kNodeChunk];
+    const int64_t nch = (nc + kNodeChunk - 1) / kNodeChunk;
+    const int64_t items = nch * split;
+    const int64_t stride = (int64_t)split * blockDim.x;
+    for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+        const int64_t ch = it / split, sl = it - ch * split;
+        const int64_t c0 = ch * kNodeChunk, c1 = min(nc, c0 + kNodeChunk);
+        const int64_t cn = c0 + threadIdx.x;
+        const int32_t a0 = ma[c0];
+        bool clean = true;
+        if (cn < c1) clean = mb[cn] < 0 && ma[cn] == a0 + (int32_t)(cn - c0);
+        if (__syncthreads_and(clean)) {
+            const int32_t a1 = ma[c1 - 1];
+            const int64_t lo = f.off[a0], len = f.off[a1 + 1] - lo;
+            const int32_t *src = f.dat + lo;
+            int32_t *dst = f.out + f.out_off[c0];
+            int64_t i = sl * blockDim.x + threadIdx.x;
+            for (; i + 3 * stride < len; i += 4 * stride) {
+                const int32_t x0 = src[i], x1 = src[i + stride], x2 = src[i + 2 * stride], x3 = src[i + 3 * stride];
+                dst[i] = x0;
+                dst[i + stride] = x1;
+                dst[i + 2 * stride] = x2;
+                dst[i + 3 * stride] = x3;
+            }
+            for (; i < len; i += stride) dst[i] = src[i];
+            continue;
+        }
+        if (threadIdx.x < 32) {
+            int64_t len[2] = {0, 0};
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                const int64_t q = c0 + threadIdx.x + 32 * h;
+                if (q < c1 && mb[q] < 0) {
+                    const int32_t a = ma[q];
+                    s_src[threadIdx.x + 32 * h] = f.off[a];
+                    s_dst[threadIdx.x + 32 * h] = f.out_off[q];
+                    len[h] = f.off[a + 1] - f.off[a];
+                }
+            }
+            const int64_t i0 = warp_incl_scan(len[0]);
+            const int64_t t0 = __shfl_sync(FULL_MASK, i0, 31);
+            const int64_t i1 = warp_incl_scan(len[1]) + t0;
+            s_end[threadIdx.x] = i0;
+            s_end[threadIdx.x + 32] = i1;
+        }
+        __syncthreads();
+        const int64_t total = s_end[kNodeChunk - 1];
+        for (int64_t i = sl * blockDim.x + threadIdx.x; i < total; i += stride) {
+            int q = 0;  // first list whose end is past i
+#pragma unroll
+            for (int step = kNodeChunk / 2; step > 0; step >>= 1)
+                if (s_end[q + step - 1] <= i) q += step;
+            const int64_t k = i - (q > 0 ? s_end[q - 1] : 0);
+            f.out[s_dst[q] + k] = f.dat[s_src[q] + k];
+        }
+        __syncthreads();
+    }
 }
 
 // Fused per-h-edge contraction (h-edges of <= 128 pin slots): a warp maps
@@ -1107,12 +1423,20 @@ __device__ __forceinline__ int warp_gamma_short(uint32_t g, int len, int32_t *ou
     return __popc(bal);
 }
 __global__ void __launch_bounds__(256) k_contract_edges(int32_t E, const int32_t *gamma, EdgeFam f0, EdgeFam f1,
-                                                        EdgeFam f2, bool write) {
+                                                        EdgeFam f2, bool write, const uint8_t *emark) {
     const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
     const int lane = lane_id();
     for (int64_t e = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id(); e < E; e += nw) {
         const int64_t l0 = f0.off[e], l1 = f1.off[e], l2 = f2.off[e];
         const int n0 = (int)(f0.off[e + 1] - l0), n1 = (int)(f1.off[e + 1] - l1), n2 = (int)(f2.off[e + 1] - l2);
+        if (!write && emark && !emark[e]) {  // no absorbed member: the image keeps every slot
+            if (lane == 0) {
+                f0.cnt[e] = n0;
+                f1.cnt[e] = n1;
+                f2.cnt[e] = n2;
+            }
+            continue;
+        }
         if (n0 <= 32 && n1 <= 32 && n2 <= 32) {
             const int32_t x0 = lane < n0 ? f0.dat[l0 + lane] : 0, x1 = lane < n1 ? f1.dat[l1 + lane] : 0,
                           x2 = lane < n2 ? f2.dat[l2 + lane] : 0;
@@ -1149,16 +1473,23 @@ __global__ void __launch_bounds__(256) k_contract_edges(int32_t E, const int32_t
 // pass: heads at out_off + (heads before it), with ranks inside a chunk from
 // __match_any_sync over the owning list.
 __device__ __forceinline__ void flat_family(const EdgeFam &f, int64_t e0, int nb, const int32_t *gamma, bool write,
-                                            uint8_t *slow, int32_t *run, uint8_t *bad) {
+                                            uint8_t *slow, int32_t *run, uint8_t *bad, const uint8_t *emark) {
     const int lane = lane_id();
     const uint32_t lt = (1u << lane) - 1u;
     int64_t lo = 0;
     int len = 0;
     uint8_t sl = 0;
+    bool keep = false;  // count pass, no absorbed member: the image keeps every slot
     if (lane < nb) {
         lo = f.off[e0 + lane];
         len = (int)(f.off[e0 + lane + 1] - lo);
         if (write) sl = slow[e0 + lane];
+        if (!write && emark && !emark[e0 + lane]) {
+            keep = true;
+            slow[e0 + lane] = 0;
+            f.cnt[e0 + lane] = len;
+            len = 0;
+        }
     }
     const int incl = warp_incl_scan(len);
     const int total = __shfl_sync(FULL_MASK, incl, 31);
@@ -1198,7 +1529,7 @@ __device__ __forceinline__ void flat_family(const EdgeFam &f, int64_t e0, int nb
     if (lane < nb) {
         if (write) {
             sw = sl;
-        } else {
+        } else if (!keep) {
             sw = bad[lane];
             slow[e0 + lane] = (uint8_t)sw;
             if (!sw) f.cnt[e0 + lane] = run[lane];
@@ -1217,19 +1548,34 @@ __device__ __forceinline__ void flat_family(const EdgeFam &f, int64_t e0, int nb
     __syncwarp();
 }
 __global__ void __launch_bounds__(256) k_contract_flat(int32_t E, const int32_t *gamma, EdgeFam f0, EdgeFam f1,
-                                                       EdgeFam f2, bool write, uint8_t *slow) {
+                                                       EdgeFam f2, bool write, uint8_t *slow,
+                                                       const uint8_t *emark) {
     __shared__ int32_t s_run[8][32];
     __shared__ uint8_t s_bad[8][32];
     const int w = warp_id();
     const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
     for (int64_t e0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + w) * 32; e0 < E; e0 += nw * 32) {
         const int nb = (int)min((int64_t)32, (int64_t)E - e0);
-        flat_family(f0, e0, nb, gamma, write, slow, s_run[w], s_bad[w]);
-        flat_family(f1, e0, nb, gamma, write, slow + E, s_run[w], s_bad[w]);
-        flat_family(f2, e0, nb, gamma, write, slow + 2 * (int64_t)E, s_run[w], s_bad[w]);
+        flat_family(f0, e0, nb, gamma, write, slow, s_run[w], s_bad[w], emark);
+        flat_family(f1, e0, nb, gamma, write, slow + E, s_run[w], s_bad[w], emark);
+        flat_family(f2, e0, nb, gamma, write, slow + 2 * (int64_t)E, s_run[w], s_bad[w], emark);
     }
 }
 }  // namespace
+
+// words of the union kernel's shared bitmap over the h-edge ids (0 = no
+// bitmap: more than ~1.3M h-edges)
+static int union_words(Ctx &c, int32_t E) {
+    static bool attr = false;
+    constexpr int kMaxWords = 40960;  // 160 KB
+    if (!attr) {
+        DHGP_CUDA(cudaFuncSetAttribute(k_node_union<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * kMaxWords));
+        DHGP_CUDA(cudaFuncSetAttribute(k_node_union<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * kMaxWords));
+        attr = true;
+    }
+    const int64_t w = cdiv((int64_t)E, 32);
+    return w <= kMaxWords ? (int)w : 0;
+}
 
 void contract_count(Ctx &c, DLevel &fine, const int32_t *match, const uint8_t *isrep, DLevel &coarse,
                     ContractScratch &s, int64_t *d_status) {
@@ -1246,9 +1592,33 @@ void contract_count(Ctx &c, DLevel &fine, const int32_t *match, const uint8_t *i
     s.mb = c.alloc<int32_t>(N);
     coarse.E = E;
     coarse.size = c.alloc<int32_t>(N);  // capacity: the fine node count
+    s.mlist = c.alloc<int32_t>(N / 2 + 1);
+    s.mcount = c.alloc<int32_t>(1);
+    s.emark = c.alloc<uint8_t>(E);
+    zero_many(c, {{s.mcount, 4}, {s.emark, E}});
     k_gamma<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(N, match, s.rank, fine.size, fine.gamma, s.ma, s.mb,
-                                                         coarse.size);
+                                                         coarse.size, s.mlist, s.mcount);
     DHGP_LAUNCHED(c);
+    // per-node families first: the merged clusters flag the h-edges whose
+    // lists need the sort / de-duplication
+    KScope kcn(c, "cc_nodes");
+    int64_t *ncnt = c.alloc<int64_t>(2 * (int64_t)N);
+    coarse.in_off = c.alloc<int64_t>((int64_t)N + 1);
+    coarse.inc_off = c.alloc<int64_t>((int64_t)N + 1);
+    {
+        const NodeFams fs{{NodeFam{fine.in_off, fine.in_dat, ncnt, nullptr, nullptr},
+                           NodeFam{fine.inc_off, fine.inc_dat, ncnt + N, nullptr, nullptr}}};
+        const unsigned ga = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(N, 256), (int64_t)c.num_sms * 8));
+        k_node_count<<<dim3(ga, 2), 256, 0, c.stream>>>(N, d_nc, s.ma, s.mb, fs);
+        DHGP_LAUNCHED(c);
+        const int words = union_words(c, E);
+        k_node_union<false><<<dim3(c.num_sms, 2), UN_THREADS, 4 * words, c.stream>>>(s.ma, s.mb, s.mlist, s.mcount, fs,
+                                                                                     s.emark, words);
+        DHGP_LAUNCHED(c);
+    }
+    scan_excl3<int64_t>(c, ncnt, coarse.in_off, ncnt + N, coarse.inc_off, nullptr, nullptr, N);
+    c.free(ncnt);
+    kcn.close();
     // per-h-edge families: sorted unique gamma image (coarsen.py:163-166)
     KScope kcs(c, "cc_edges");
     coarse.maxp = fine.maxp;
@@ -1266,11 +1636,11 @@ void contract_count(Ctx &c, DLevel &fine, const int32_t *match, const uint8_t *i
             if (s.flat) {
                 static int g = resident_grid(c, k_contract_flat, 256, 0);
                 const unsigned gr = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(E, 256), g));
-                k_contract_flat<<<gr, 256, 0, c.stream>>>(E, fine.gamma, f0, f1, f2, false, s.slow);
+                k_contract_flat<<<gr, 256, 0, c.stream>>>(E, fine.gamma, f0, f1, f2, false, s.slow, s.emark);
             } else {
                 static int g = resident_grid(c, k_contract_edges, 256, 0);
                 const unsigned gr = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(E, 8), g));
-                k_contract_edges<<<gr, 256, 0, c.stream>>>(E, fine.gamma, f0, f1, f2, false);
+                k_contract_edges<<<gr, 256, 0, c.stream>>>(E, fine.gamma, f0, f1, f2, false, s.emark);
             }
             DHGP_LAUNCHED(c);
         }
@@ -1300,19 +1670,6 @@ void contract_count(Ctx &c, DLevel &fine, const int32_t *match, const uint8_t *i
     c.free(cnt);
     }
     kcs.close();
-    KScope kcn(c, "cc_nodes");
-    // per-node families: union of the two members' sorted lists
-    int64_t *ncnt = c.alloc<int64_t>(2 * (int64_t)N);
-    s.big_in = c.alloc<int32_t>(N);
-    s.big_inc = c.alloc<int32_t>(N);
-    s.big_cnt = c.alloc<int32_t>(2);
-    c.zero(s.big_cnt, 2);
-    coarse.in_off = c.alloc<int64_t>((int64_t)N + 1);
-    coarse.inc_off = c.alloc<int64_t>((int64_t)N + 1);
-    merge_union_count2(c, N, s.ma, s.mb, fine.in_off, fine.in_dat, ncnt, s.big_in, s.big_cnt, fine.inc_off,
-                       fine.inc_dat, ncnt + N, s.big_inc, s.big_cnt + 1, d_nc);
-    scan_excl3<int64_t>(c, ncnt, coarse.in_off, ncnt + N, coarse.inc_off, nullptr, nullptr, N);
-    c.free(ncnt);
     k_contract_status<<<1, 32, 0, c.stream>>>(N, E, s.rank, coarse.src_off, coarse.dst_off, coarse.pin_off,
                                               coarse.in_off, coarse.inc_off, d_status);
     DHGP_LAUNCHED(c);
@@ -1349,11 +1706,11 @@ void contract_write(Ctx &c, DLevel &fine, DLevel &coarse, ContractScratch &s, co
                 if (s.flat) {
                     static int g = resident_grid(c, k_contract_flat, 256, 0);
                     const unsigned gr = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(E, 256), g));
-                    k_contract_flat<<<gr, 256, 0, c.stream>>>(E, fine.gamma, f0, f1, f2, true, s.slow);
+                    k_contract_flat<<<gr, 256, 0, c.stream>>>(E, fine.gamma, f0, f1, f2, true, s.slow, nullptr);
                 } else {
                     static int g = resident_grid(c, k_contract_edges, 256, 0);
                     const unsigned gr = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(E, 8), g));
-                    k_contract_edges<<<gr, 256, 0, c.stream>>>(E, fine.gamma, f0, f1, f2, true);
+                    k_contract_edges<<<gr, 256, 0, c.stream>>>(E, fine.gamma, f0, f1, f2, true, nullptr);
                 }
                 DHGP_LAUNCHED(c);
             }
@@ -1365,9 +1722,21 @@ void contract_write(Ctx &c, DLevel &fine, DLevel &coarse, ContractScratch &s, co
     }
     {
         KScope k2(c, "cw_merge");
-        merge_union_write2(c, st.nc, s.ma, s.mb, fine.in_off, fine.in_dat, coarse.in_off, coarse.in_dat, s.big_in,
-                           s.big_cnt, fine.inc_off, fine.inc_dat, coarse.inc_off, coarse.inc_dat, s.big_inc,
-                           s.big_cnt + 1);
+        if (st.nc > 0) {
+            const NodeFams fs{{NodeFam{fine.in_off, fine.in_dat, nullptr, coarse.in_off, coarse.in_dat},
+                               NodeFam{fine.inc_off, fine.inc_dat, nullptr, coarse.inc_off, coarse.inc_dat}}};
+            // slices per chunk: about 4K list entries per CTA
+            const int64_t per_chunk = cdiv(std::max(fine.Sin, fine.U) * kNodeChunk, std::max<int64_t>(1, fine.N));
+            const int split = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(per_chunk, 4096), 64));
+            const int64_t items = cdiv(st.nc, kNodeChunk) * split;
+            const unsigned g = (unsigned)std::min<int64_t>(items, (int64_t)c.num_sms * 16);
+            k_node_write<<<dim3(g, 2), 256, 0, c.stream>>>(st.nc, split, s.ma, s.mb, fs);
+            DHGP_LAUNCHED(c);
+            const int words = union_words(c, E);
+            k_node_union<true><<<dim3(c.num_sms, 2), UN_THREADS, 4 * words, c.stream>>>(s.ma, s.mb, s.mlist, s.mcount,
+                                                                                        fs, nullptr, words);
+            DHGP_LAUNCHED(c);
+        }
     }
     int32_t *ma = s.ma, *mb = s.mb;
     s.ma = s.mb = nullptr;
@@ -1436,9 +1805,9 @@ void contract_release(Ctx &c, ContractScratch &s) {
     c.free(s.tmp_dst);
     c.free(s.tmp_pin);
     c.free(s.rank);
-    c.free(s.big_in);
-    c.free(s.big_inc);
-    c.free(s.big_cnt);
+    c.free(s.mlist);
+    c.free(s.mcount);
+    c.free(s.emark);
     c.free(s.slow);
     s = ContractScratch();
 }

@@ -72,7 +72,8 @@ struct ContractScratch {
     int32_t *ma = nullptr, *mb = nullptr;
     int32_t *tmp_src = nullptr, *tmp_dst = nullptr, *tmp_pin = nullptr;
     int64_t *rank = nullptr;
-    int32_t *big_in = nullptr, *big_inc = nullptr, *big_cnt = nullptr;  // large unions (block tier)
+    int32_t *mlist = nullptr, *mcount = nullptr;  // merged coarse nodes (any order) and their count
+    uint8_t *emark = nullptr;  // [E] h-edges holding an absorbed (non-minimum) member
     bool fused = false;  // h-edge lists rebuilt by the flattened warp kernel (no sorted temporaries)
     uint8_t *slow = nullptr;  // [3E] lists that need the per-list sort (count pass -> write pass)
     bool flat = false;        // flattened kernel (short lists) vs warp per h-edge

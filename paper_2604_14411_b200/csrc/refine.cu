@@ -934,20 +934,30 @@ __device__ __forceinline__ void inbound_enter(const EvArgs &ev, int32_t i) { ato
 // destination pins in sequence order; per part a running destination-pin
 // count from pins_in[e, p]; crossings 0->1 / 1->0 emit distinct events.
 // This is the walk for h-edges with many movers (the warp kernel
-// k_round_edges takes the others): the block collects and sorts them, one
-// thread walks with a shared-memory part dictionary
+// k_round_edges takes the others).  The walk only couples movers through a
+// shared part, so it runs per part: the block collects and sorts the movers,
+// gathers the distinct parts they touch (shared hash), and a warp per part
+// sweeps the movers 32 at a time — delta -1 when the mover leaves the part,
+// +1 when it enters — with a warp scan for the running count: a leave that
+// brings it to 0 and an enter that brings it to 1 are the crossings.
 constexpr int kEvBlockMax = 2048;
-__global__ void k_inbound_events_block(const int64_t *dst_off, const int32_t *dst_dat, Runs r,
+constexpr int kEvParts = 2 * kEvBlockMax;  // hash slots (>= distinct parts: 2 per mover)
+__global__ void __launch_bounds__(256) k_inbound_events_block(const int64_t *dst_off, const int32_t *dst_dat, Runs r,
                                        const int32_t *pos, const int32_t *from, const int32_t *to, EvArgs ev,
                                        const int32_t *big_list, const int32_t *big_count, int32_t *err) {
     __shared__ uint32_t smv[kEvBlockMax];
-    __shared__ int32_t sdp[2 * kEvBlockMax];
-    __shared__ int32_t sdc[2 * kEvBlockMax];
-    __shared__ int32_t snm;
+    __shared__ int32_t skey[kEvParts];
+    __shared__ int32_t sparts[kEvParts];
+    __shared__ int32_t snm, snp;
+    const int lane = lane_id(), w = warp_id(), nw = blockDim.x >> 5;
     const int nbig = *big_count;
     for (int t = blockIdx.x; t < nbig; t += gridDim.x) {
         const int32_t e = big_list[t];
-        if (threadIdx.x == 0) snm = 0;
+        if (threadIdx.x == 0) {
+            snm = 0;
+            snp = 0;
+        }
+        for (int s = threadIdx.x; s < kEvParts; s += blockDim.x) skey[s] = -1;
         __syncthreads();
         for (int64_t q = dst_off[e] + threadIdx.x; q < dst_off[e + 1]; q += blockDim.x) {
             int32_t j = pos[dst_dat[q]];
@@ -966,32 +976,48 @@ __global__ void k_inbound_events_block(const int64_t *dst_off, const int32_t *ds
         const int np = next_pow2(nm);
         for (int s = nm + threadIdx.x; s < np; s += blockDim.x) smv[s] = 0xffffffffu;
         block_bitonic_sort32(smv, np);
-        if (threadIdx.x == 0) {
-            const int64_t lo = r.off[e];
-            const int32_t lam = r.len[e];
-            int nd = 0;
-            for (int a = 0; a < nm; a++) {
-                const int32_t i = (int32_t)smv[a];
-                const int32_t pf = from[i], pt = to[i];
-                int k;
-                for (k = 0; k < nd && sdp[k] != pf; k++) {
+        // distinct parts among the movers' sources and targets
+        for (int a = threadIdx.x; a < 2 * nm; a += blockDim.x) {
+            const int32_t i = (int32_t)smv[a >> 1];
+            const int32_t p = (a & 1) ? to[i] : from[i];
+            uint32_t h = ((uint32_t)p * 2654435761u) & (kEvParts - 1);
+            while (true) {
+                const int32_t k = skey[h];
+                if (k == p) break;
+                if (k == -1) {
+                    const int32_t prev = atomicCAS(&skey[h], -1, p);
+                    if (prev == -1) {
+                        sparts[atomicAdd(&snp, 1)] = p;
+                        break;
+                    }
+                    if (prev == p) break;
                 }
-                if (k == nd) {
-                    int32_t f = run_find(r, lo, lam, pf);
-                    sdp[nd] = pf;
-                    sdc[nd] = f >= 0 ? r.cin[lo + f] : 0;
-                    nd++;
+                h = (h + 1) & (kEvParts - 1);
+            }
+        }
+        __syncthreads();
+        const int npart = snp;
+        const int64_t lo = r.off[e];
+        const int32_t lam = r.len[e];
+        for (int q = w; q < npart; q += nw) {
+            const int32_t p = sparts[q];
+            int32_t run = 0;
+            if (lane == 0) {
+                const int32_t f = run_find(r, lo, lam, p);
+                run = f >= 0 ? r.cin[lo + f] : 0;
+            }
+            run = __shfl_sync(FULL_MASK, run, 0);
+            for (int a0 = 0; a0 < nm; a0 += 32) {
+                const int a = a0 + lane;
+                int32_t i = 0, d = 0;
+                if (a < nm) {
+                    i = (int32_t)smv[a];
+                    d = (to[i] == p) - (from[i] == p);
                 }
-                if (--sdc[k] == 0) inbound_leave(ev, i);
-                for (k = 0; k < nd && sdp[k] != pt; k++) {
-                }
-                if (k == nd) {
-                    int32_t f = run_find(r, lo, lam, pt);
-                    sdp[nd] = pt;
-                    sdc[nd] = f >= 0 ? r.cin[lo + f] : 0;
-                    nd++;
-                }
-                if (++sdc[k] == 1) inbound_enter(ev, i);
+                const int32_t incl = warp_incl_scan(d) + run;
+                if (d < 0 && incl == 0) inbound_leave(ev, i);
+                if (d > 0 && incl == 1) inbound_enter(ev, i);
+                run = __shfl_sync(FULL_MASK, incl, 31);
             }
         }
         __syncthreads();
