@@ -24,7 +24,7 @@ namespace {
 template <class F>
 __device__ __forceinline__ void warp_for_pins(const int32_t *inc_dat, int64_t ilo, int64_t ihi, int64_t first,
                                               int64_t stride, const int64_t *pin_off, const int32_t *pin_dat,
-                                              F &&f, unsigned long long *work = nullptr) {
+                                              F &&f, unsigned long long *work = nullptr, int bsz = 32) {
     const int lane = lane_id();
     unsigned long long wb = 0;
     for (int64_t base = ilo + first; base < ihi; base += stride) {
@@ -32,7 +32,7 @@ __device__ __forceinline__ void warp_for_pins(const int32_t *inc_dat, int64_t il
         int32_t e = -1;
         int64_t plo = 0;
         int len = 0;
-        if (ii < ihi) {
+        if (lane < bsz && ii < ihi) {
             e = inc_dat[ii];
             plo = pin_off[e];
             len = (int)(pin_off[e + 1] - plo);
@@ -40,7 +40,7 @@ __device__ __forceinline__ void warp_for_pins(const int32_t *inc_dat, int64_t il
         const int incl = warp_incl_scan(len);
         const int total = __shfl_sync(FULL_MASK, incl, 31);
         const int excl = incl - len;
-        wb += 28ull * (unsigned long long)min((int64_t)32, ihi - base) + 4ull * (unsigned long long)total;
+        wb += 28ull * (unsigned long long)min((int64_t)bsz, ihi - base) + 4ull * (unsigned long long)total;
         // four pins per lane in flight before any is used (the loads are the
         // latency; the hash inserts are cheap)
         for (int s0 = 0; s0 < total; s0 += 128) {
@@ -101,6 +101,8 @@ struct ScoreArgs {
     int32_t *tup_count = nullptr;
     int64_t tup_cap = 0;
     unsigned long long *work = nullptr;  // profiling: algorithmic bytes
+    // diagnostics (DHGP_TRACE): candidate iterations and nodes, warp / block tier
+    unsigned long long *probe = nullptr;
 };
 
 // next node of a persistent scoring loop: [lo, hi) or the listed nodes in it
@@ -271,7 +273,9 @@ __global__ void __launch_bounds__(SS_WARPS * 32) k_score_warp(ScoreArgs a) {
         __syncwarp();
         int32_t best_m = -1;
         int64_t best_v = 0;
+        int iters = 0;
         while (true) {
+            iters++;
             int64_t bv = -1;
             int32_t bk = -1;
             int bs = -1;
@@ -309,6 +313,10 @@ __global__ void __launch_bounds__(SS_WARPS * 32) k_score_warp(ScoreArgs a) {
         if (lane == 0) {
             a.pair[node] = best_m;
             a.score[node] = best_m >= 0 ? (double)best_v : 0.0;
+            if (a.probe) {
+                atomicAdd(&a.probe[0], (unsigned long long)iters);
+                atomicAdd(&a.probe[2], 1ull);
+            }
         }
         __syncwarp();
     }
@@ -346,7 +354,9 @@ __global__ void __launch_bounds__(SH_THREADS) k_score_heavy(ScoreArgs a) {
         }
         __syncthreads();
         const int64_t ilo = a.inc_off[node], ihi = a.inc_off[node + 1];
-        warp_for_pins(a.inc_dat, ilo, ihi, (int64_t)w * 32, (int64_t)nw * 32, a.pin_off, a.pin_dat,
+        // h-edges per warp batch: a node's h-edges spread over all warps
+        const int bsz = (int)max((int64_t)1, min((int64_t)32, (ihi - ilo + nw - 1) / nw));
+        warp_for_pins(a.inc_dat, ilo, ihi, (int64_t)w * bsz, (int64_t)nw * bsz, a.pin_off, a.pin_dat,
                       [&](int32_t e, int32_t m) {
                           if (m == node || sover) return;
                           const Acc we = (Acc)a.wi[e];
@@ -370,7 +380,7 @@ __global__ void __launch_bounds__(SH_THREADS) k_score_heavy(ScoreArgs a) {
                           }
                           sover = 1;
                       },
-                      a.work);
+                      a.work, bsz);
         __syncthreads();
         if (sover) {
             if (threadIdx.x == 0) a.big_list[atomicAdd(a.big_count, 1)] = node;
@@ -381,7 +391,9 @@ __global__ void __launch_bounds__(SH_THREADS) k_score_heavy(ScoreArgs a) {
         __syncthreads();
         int32_t best_m = -1;
         long long best_v = 0;
+        int iters = 0;
         while (true) {
+            iters++;
             long long bv = -1;
             int32_t bk = -1, bs = -1;
             for (int s = threadIdx.x; s < SH_CAP; s += SH_THREADS) {
@@ -452,6 +464,10 @@ __global__ void __launch_bounds__(SH_THREADS) k_score_heavy(ScoreArgs a) {
         if (threadIdx.x == 0) {
             a.pair[node] = best_m;
             a.score[node] = best_m >= 0 ? (double)best_v : 0.0;
+            if (a.probe) {
+                atomicAdd(&a.probe[1], (unsigned long long)iters);
+                atomicAdd(&a.probe[3], 1ull);
+            }
         }
         __syncthreads();
     }
@@ -479,14 +495,16 @@ __global__ void __launch_bounds__(SB_THREADS) k_score_block(ScoreArgs a, long lo
         if (threadIdx.x == 0) s_nt = 0;
         __syncthreads();
         const int64_t ilo = a.inc_off[node], ihi = a.inc_off[node + 1];
-        warp_for_pins(a.inc_dat, ilo, ihi, (int64_t)w * 32, (int64_t)nw * 32, a.pin_off, a.pin_dat,
+        // h-edges per warp batch: a node's h-edges spread over all warps
+        const int bsz = (int)max((int64_t)1, min((int64_t)32, (ihi - ilo + nw - 1) / nw));
+        warp_for_pins(a.inc_dat, ilo, ihi, (int64_t)w * bsz, (int64_t)nw * bsz, a.pin_off, a.pin_dat,
                       [&](int32_t e, int32_t m) {
                           if (m == node) return;
                           long long old = atomicCAS((unsigned long long *)&dense[m], ~0ull, 0ull);
                           if (old == -1ll) touched[atomicAdd(&s_nt, 1)] = m;
                           atomicAdd((unsigned long long *)&dense[m], (unsigned long long)a.wi[e]);
                       },
-                      a.work);
+                      a.work, bsz);
         __syncthreads();
         const int nt = s_nt;
         const int64_t szn = a.size[node];
@@ -796,6 +814,12 @@ void score_select_inc(Ctx &c, const DLevel &L, const DWeights &W, int64_t omega,
     a.tup_h = th;
     a.tup_count = lc + 2;
     a.tup_cap = cap;
+    unsigned long long *probe = nullptr;
+    if (trace_enabled()) {
+        probe = c.alloc<unsigned long long>(4);
+        c.zero(probe, 4);
+        a.probe = probe;
+    }
     unsigned long long *work = nullptr;
     if (c.profiling) {
         work = c.alloc<unsigned long long>(1);
@@ -818,6 +842,7 @@ void score_select_inc(Ctx &c, const DLevel &L, const DWeights &W, int64_t omega,
     b.list = list2;
     b.list_count = lc + 1;
     b.work = work;
+    b.probe = probe;
     score_tiers(c, b, W, s, N);
     if (work) {  // measured algorithmic bytes: lists read by both passes, the per-node
                  // carry (pair, score, gamma, members: 24 B) and the tuples (16 B each)
@@ -831,9 +856,13 @@ void score_select_inc(Ctx &c, const DLevel &L, const DWeights &W, int64_t omega,
     }
     if (trace_enabled()) {
         int32_t h[3];
+        unsigned long long pr[4];
         c.d2h(h, lc, 3);
+        c.d2h(pr, probe, 4);
         c.sync();
-        fprintf(stderr, "scoreinc N %d merged %d rescored %d tuples %d\n", N, h[0], h[1], h[2]);
+        fprintf(stderr, "scoreinc N %d merged %d rescored %d tuples %d warp_nodes %llu warp_iters %llu heavy_nodes %llu heavy_iters %llu\n",
+                N, h[0], h[1], h[2], pr[2], pr[0], pr[3], pr[1]);
+        c.free(probe);
     }
     for (void *q : {(void *)kind, (void *)thr_s, (void *)thr_p, (void *)best, (void *)list, (void *)list2, (void *)lc,
                     (void *)tv, (void *)tb, (void *)th, (void *)hard})

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <chrono>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -127,8 +128,14 @@ struct Ctx {
     void d2d(T *dst, const T *src, int64_t n) {
         if (n > 0) DHGP_CUDA(cudaMemcpyAsync(dst, src, (size_t)n * sizeof(T), cudaMemcpyDeviceToDevice, stream));
     }
+    // diagnostics: host time blocked in sync() and the number of syncs
+    double sync_wait_ms = 0.0;
+    int64_t syncs = 0;
     void sync() {
+        const auto t0 = std::chrono::steady_clock::now();
         DHGP_CUDA(cudaStreamSynchronize(stream));
+        sync_wait_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        syncs++;
         for (const PinnedRead &r : pin_reads) memcpy(r.dst, pinned + r.off, r.bytes);
         pin_reads.clear();
         pin_used = 0;

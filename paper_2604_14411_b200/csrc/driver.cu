@@ -332,6 +332,9 @@ static void run_partition(Ctx &c, const DInput &in, const dhgp_config &cfg, Part
         }
     }
     const double t0 = now_ms();
+    c.sync_wait_ms = 0.0;
+    c.syncs = 0;
+    const int64_t launches0 = c.launches;
     const int64_t target = (N0 + omega - 1) / omega;
     // ---- coarsening (driver.py:97-118) -----------------------------------
     // One host sync per level: scoring, matching and the counting half of the
@@ -596,6 +599,9 @@ static void run_partition(Ctx &c, const DInput &in, const dhgp_config &cfg, Part
         res.phase_ms[0] = t1 - t0;
         res.phase_ms[1] = t2 - t1;
         res.phase_ms[2] = t3 - t0;
+        if (getenv("DHGP_SYNCSTAT"))
+            fprintf(stderr, "syncstat wall_ms %.1f sync_wait_ms %.1f syncs %lld launches %lld\n", t3 - t0,
+                    c.sync_wait_ms, (long long)c.syncs, (long long)(c.launches - launches0));
     } catch (...) {
         refine_state_release(c, rst);
         for (auto &L : levels) L.release(c);

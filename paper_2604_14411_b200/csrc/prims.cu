@@ -441,7 +441,13 @@ __global__ void __launch_bounds__(1024) k_small_sort(uint64_t *keys, uint32_t *v
     }
 }
 // unique u64 keys whose low 32 bits are the value (the packed mover keys)
-__global__ void __launch_bounds__(1024) k_small_sort_packed(uint64_t *keys, uint32_t *vals, int n) {
+__global__ void __launch_bounds__(1024) k_small_sort_packed(uint64_t *keys, uint32_t *vals, int n,
+                                                            const int64_t *dn) {
+    if (dn) {  // count on device: a no-op when it does not fit
+        const int64_t m = *dn;
+        if (m <= 1 || m > kSmallSort) return;
+        n = (int)m;
+    }
     extern __shared__ unsigned long long sm[];
     uint64_t *a = (uint64_t *)sm, *b = a + kSmallSort;
     for (int i = threadIdx.x; i < n; i += blockDim.x) a[i] = keys[i];
@@ -460,8 +466,8 @@ void small_sort_pairs(Ctx &c, uint64_t *keys, uint32_t *vals, int64_t n) {
     k_small_sort<<<1, 1024, 0, c.stream>>>(keys, vals, (int)n);
     DHGP_LAUNCHED(c);
 }
-void small_sort_packed(Ctx &c, uint64_t *keys, uint32_t *vals, int64_t n) {
-    if (n <= 1) return;
+void small_sort_packed(Ctx &c, uint64_t *keys, uint32_t *vals, int64_t n, const int64_t *dn) {
+    if (!dn && n <= 1) return;
     KScope ks(c, "radix_sort");
     static bool attr = false;
     if (!attr) {
@@ -469,7 +475,7 @@ void small_sort_packed(Ctx &c, uint64_t *keys, uint32_t *vals, int64_t n) {
                                        (int)(2 * kSmallSort * sizeof(uint64_t))));
         attr = true;
     }
-    k_small_sort_packed<<<1, 1024, 2 * kSmallSort * sizeof(uint64_t), c.stream>>>(keys, vals, (int)n);
+    k_small_sort_packed<<<1, 1024, 2 * kSmallSort * sizeof(uint64_t), c.stream>>>(keys, vals, (int)n, dn);
     DHGP_LAUNCHED(c);
 }
 

@@ -32,7 +32,8 @@ constexpr int64_t kSmallSort = 4096;
 // up to eight zero-fills (pointer, bytes; 4-byte aligned) in one launch
 void zero_many(Ctx &c, std::initializer_list<std::pair<void *, int64_t>> bufs);
 // the same for unique keys carrying their value in the low 32 bits
-void small_sort_packed(Ctx &c, uint64_t *keys, uint32_t *vals, int64_t n);
+// dn != null: the count is read on device (n ignored); no-op above kSmallSort
+void small_sort_packed(Ctx &c, uint64_t *keys, uint32_t *vals, int64_t n, const int64_t *dn = nullptr);
 void small_sort_pairs(Ctx &c, uint64_t *keys, uint32_t *vals, int64_t n);
 
 // Per-segment ascending sort of (map ? map[dat[i]] : dat[i]) into tmp (same

@@ -22,6 +22,11 @@ struct Runs {
     int32_t *len = nullptr;   // [E] lambda(e)
 };
 
+// Rounds are launched speculatively for up to kSpecCap movers before the
+// host knows M (one host sync per round instead of two); kernels of such a
+// launch are no-ops when M turns out larger, and the host redoes the tail.
+constexpr int64_t kSpecCap = kSmallSort;
+
 __device__ __forceinline__ int32_t run_find(const Runs &r, int64_t lo, int32_t len, int32_t p) {
     int64_t k = lower_bound_dev<int32_t>(r.part, lo, lo + len, p);
     return (k < lo + len && r.part[k] == p) ? (int32_t)(k - lo) : -1;
@@ -322,7 +327,7 @@ __device__ __forceinline__ void write_proposal(const ProposeArgs &a, int32_t nod
 // the run arrays.  Returns this lane's share of sum w(e).
 template <class F>
 __device__ __forceinline__ int64_t warp_for_runs(const int32_t *inc_dat, int64_t ilo, int64_t ihi, int64_t first,
-                                                 int64_t stride, const int64_t *pin_off, const int32_t *len,
+                                                 int64_t stride, int bsz, const int64_t *pin_off, const int32_t *len,
                                                  const int64_t *wi, unsigned long long *work, F &&f) {
     // `work` (profiling only): algorithmic bytes read — 24 B per incident
     // h-edge (list entry, run base, run count, weight) + 8 B per run
@@ -334,7 +339,7 @@ __device__ __forceinline__ int64_t warp_for_runs(const int32_t *inc_dat, int64_t
         int32_t e = -1;
         int64_t plo = 0, we = 0;
         int l = 0;
-        if (ii < ihi) {
+        if (lane < bsz && ii < ihi) {
             e = inc_dat[ii];
             plo = pin_off[e];
             l = len[e];
@@ -344,7 +349,7 @@ __device__ __forceinline__ int64_t warp_for_runs(const int32_t *inc_dat, int64_t
         const int incl = warp_incl_scan(l);
         const int tot = __shfl_sync(FULL_MASK, incl, 31);
         const int excl = incl - l;
-        wb += 24ull * (unsigned long long)min((int64_t)32, ihi - base) + 8ull * (unsigned long long)tot;
+        wb += 24ull * (unsigned long long)min((int64_t)bsz, ihi - base) + 8ull * (unsigned long long)tot;
         for (int s0 = 0; s0 < tot; s0 += 32) {
             const int sl = s0 + lane;
             int owner = 0;
@@ -423,7 +428,7 @@ __global__ void __launch_bounds__(PR_WARPS * 32) k_propose_warp(ProposeArgs a) {
         __syncwarp();
         const int32_t ps = a.assign[node];
         int64_t total = 0, saving = 0;
-        total = warp_for_runs(a.inc_dat, ilo, ihi, 0, 32, a.r.off, a.r.len, a.wi, a.work, [&](int32_t, int64_t we, int64_t k) {
+        total = warp_for_runs(a.inc_dat, ilo, ihi, 0, 32, 32, a.r.off, a.r.len, a.wi, a.work, [&](int32_t, int64_t we, int64_t k) {
             const int32_t p = a.r.part[k];
             if (p == ps && a.r.cnt[k] == 1) saving += we;
             if (sover[w]) return;
@@ -551,7 +556,9 @@ __global__ void __launch_bounds__(PM_THREADS) k_propose_mid(ProposeArgs a) {
         __syncthreads();
         const int32_t ps = a.assign[node];
         long long total = 0, saving = 0;
-        total = warp_for_runs(a.inc_dat, ilo, ihi, (int64_t)w * 32, (int64_t)nw * 32, a.r.off, a.r.len, a.wi, a.work,
+        // h-edges per warp batch: a node's h-edges spread over all warps
+        const int rb = (int)max((int64_t)1, min((int64_t)32, (ihi - ilo + nw - 1) / nw));
+        total = warp_for_runs(a.inc_dat, ilo, ihi, (int64_t)w * rb, (int64_t)nw * rb, rb, a.r.off, a.r.len, a.wi, a.work,
                               [&](int32_t, int64_t we, int64_t k) {
                                   const int32_t p = a.r.part[k];
                                   if (p == ps && a.r.cnt[k] == 1) saving += we;
@@ -647,7 +654,9 @@ __global__ void __launch_bounds__(THREADS) k_propose_heavy(ProposeArgs a) {
         const int64_t ilo = a.inc_off[node], ihi = a.inc_off[node + 1];
         const int32_t ps = a.assign[node];
         long long total = 0, saving = 0;
-        total = warp_for_runs(a.inc_dat, ilo, ihi, (int64_t)w * 32, (int64_t)nw * 32, a.r.off, a.r.len, a.wi, a.work,
+        // h-edges per warp batch: a node's h-edges spread over all warps
+        const int rb = (int)max((int64_t)1, min((int64_t)32, (ihi - ilo + nw - 1) / nw));
+        total = warp_for_runs(a.inc_dat, ilo, ihi, (int64_t)w * rb, (int64_t)nw * rb, rb, a.r.off, a.r.len, a.wi, a.work,
                               [&](int32_t, int64_t we, int64_t k) {
                                   const int32_t p = a.r.part[k];
                                   if (p == ps && a.r.cnt[k] == 1) saving += we;
@@ -761,7 +770,9 @@ __global__ void __launch_bounds__(256) k_propose_hub(ProposeArgs a, long long *h
         __syncthreads();
         const int32_t ps = a.assign[node];
         long long total = 0, saving = 0;
-        total = warp_for_runs(a.inc_dat, ilo, ihi, (int64_t)w * 32, (int64_t)nw * 32, a.r.off, a.r.len, a.wi, a.work,
+        // h-edges per warp batch: a node's h-edges spread over all warps
+        const int rb = (int)max((int64_t)1, min((int64_t)32, (ihi - ilo + nw - 1) / nw));
+        total = warp_for_runs(a.inc_dat, ilo, ihi, (int64_t)w * rb, (int64_t)nw * rb, rb, a.r.off, a.r.len, a.wi, a.work,
                               [&](int32_t, int64_t we, int64_t k) {
                                   const int32_t p = a.r.part[k];
                                   if (p == ps && a.r.cnt[k] == 1) saving += we;
@@ -838,7 +849,9 @@ __global__ void __launch_bounds__(PB_THREADS) k_propose_block(ProposeArgs a, lon
         const int64_t ilo = a.inc_off[node], ihi = a.inc_off[node + 1];
         const int32_t ps = a.assign[node];
         long long total = 0, saving = 0;
-        total = warp_for_runs(a.inc_dat, ilo, ihi, (int64_t)w * 32, (int64_t)nw * 32, a.r.off, a.r.len, a.wi, a.work,
+        // h-edges per warp batch: a node's h-edges spread over all warps
+        const int rb = (int)max((int64_t)1, min((int64_t)32, (ihi - ilo + nw - 1) / nw));
+        total = warp_for_runs(a.inc_dat, ilo, ihi, (int64_t)w * rb, (int64_t)nw * rb, rb, a.r.off, a.r.len, a.wi, a.work,
                               [&](int32_t, int64_t we, int64_t k) {
                                   const int32_t p = a.r.part[k];
                                   if (p == ps && a.r.cnt[k] == 1) saving += we;
@@ -1194,7 +1207,7 @@ __device__ __forceinline__ void sel_runmax(int n, int32_t *a, int64_t *sh) {
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(SEL_THREADS) k_select_small(const unsigned long long *ecount, int64_t M,
+__global__ void __launch_bounds__(SEL_THREADS) k_select_small(const unsigned long long *ecount, const int64_t *dM,
                                                               const uint64_t *ekey, const uint32_t *evals,
                                                               const int64_t *gseq, const int64_t *psizes,
                                                               const int64_t *pinbound, int64_t omega, int64_t delta,
@@ -1204,6 +1217,7 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select_small(const unsigned lon
     __shared__ int64_t sh[33];
     __shared__ long long s_bv[32], s_bk[32];
     const int64_t T = (int64_t)*ecount;
+    const int64_t M = *dM;
     if (T > SEL_T || M > SEL_M - 2) {
         if (threadIdx.x == 0) res[2] = 1;
         return;
@@ -1361,15 +1375,17 @@ namespace {
 // moves: sequence arrays from the radix-sorted (key, node) pairs; M on device
 __global__ void k_build_moves_dn(const int64_t *dM, const uint32_t *sorted_nodes, const int32_t *assign,
                                  const int32_t *target, const int64_t *gain, int32_t *node, int32_t *from, int32_t *to,
-                                 int64_t *giso, int32_t *pos) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= *dM) return;
-    int32_t n = (int32_t)sorted_nodes[i];
-    node[i] = n;
-    from[i] = assign[n];
-    to[i] = target[n];
-    giso[i] = gain[n];
-    pos[n] = (int32_t)i;
+                                 int64_t *giso, int32_t *pos, bool spec) {
+    const int64_t M = *dM;
+    if (spec && M > kSpecCap) return;  // speculative launch, M too large
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < M; i += (int64_t)gridDim.x * blockDim.x) {
+        int32_t n = (int32_t)sorted_nodes[i];
+        node[i] = n;
+        from[i] = assign[n];
+        to[i] = target[n];
+        giso[i] = gain[n];
+        pos[n] = (int32_t)i;
+    }
 }
 // A15: gains corrected for earlier moves, rules (a)-(d) (_kernels.pyx:326-363),
 // computed per h-edge: the movers among an h-edge's pins, in sequence order,
@@ -1485,7 +1501,8 @@ __global__ void __launch_bounds__(256) k_round_edges(int32_t E, const int32_t *e
                                                      const int32_t *from, const int32_t *to,
                                                      unsigned long long *gacc, EvArgs ev, int32_t *sg_big,
                                                      int32_t *sg_count, int32_t *ev_big, int32_t *ev_count,
-                                                     int cap) {
+                                                     int cap, const int64_t *spec_m) {
+    if (spec_m && *spec_m > kSpecCap) return;  // speculative launch, M too large
     __shared__ int32_t s_mv[8][32];
     const int lane = lane_id();
     int32_t *smv = s_mv[warp_id()];
@@ -1574,11 +1591,9 @@ __global__ void k_mover_compact(int32_t N, const int32_t *target, const int64_t 
 }
 // per move, after the h-edge kernels: the size track (refine.py:203-208),
 // the aggregated inbound groups, and gain_seq = gain_iso + the h-edge terms
-__global__ void k_round_moves(const int64_t *dM, const int32_t *node, const int32_t *from, const int32_t *to,
-                              const int32_t *size, EvArgs ev, const int64_t *giso, const unsigned long long *gacc,
-                              int64_t *gseq) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= *dM) return;
+__device__ __forceinline__ void round_move(int64_t i, const int32_t *node, const int32_t *from, const int32_t *to,
+                                           const int32_t *size, EvArgs ev, const int64_t *giso,
+                                           const unsigned long long *gacc, int64_t *gseq) {
     gseq[i] = giso[i] + (int64_t)gacc[i];
     const int32_t s = size[node[i]], f = from[i], t = to[i];
     const int32_t a = ev.in_from[i], b = ev.in_to[i];
@@ -1592,6 +1607,14 @@ __global__ void k_round_moves(const int64_t *dM, const int32_t *node, const int3
     put(0, t, s);
     if (a) put(1, f, a);
     if (b) put(1, t, b);
+}
+__global__ void k_round_moves(const int64_t *dM, const int32_t *node, const int32_t *from, const int32_t *to,
+                              const int32_t *size, EvArgs ev, const int64_t *giso, const unsigned long long *gacc,
+                              int64_t *gseq, bool spec) {
+    const int64_t M = *dM;
+    if (spec && M > kSpecCap) return;  // speculative launch, M too large
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < M; i += (int64_t)gridDim.x * blockDim.x)
+        round_move(i, node, from, to, size, ev, giso, gacc, gseq);
 }
 
 
@@ -1867,7 +1890,8 @@ __global__ void k_mark_psize(int32_t N, const int32_t *target, const uint8_t *fs
 
 // the round's movers' h-edges (for the sequence gains and inbound events)
 __global__ void k_mover_edges(const int64_t *dM, const int32_t *node, const int64_t *inc_off, const int32_t *inc_dat,
-                              int32_t *emflag, int32_t *mlist, int32_t *mcount) {
+                              int32_t *emflag, int32_t *mlist, int32_t *mcount, bool spec) {
+    if (spec && *dM > kSpecCap) return;  // speculative launch, M too large
     grid_incidences(*dM, [&](int64_t i) { return node[i]; }, inc_off, inc_dat,
                     [&](int64_t, int32_t e) { push_once(&emflag[e], 1, e, mlist, mcount); });
 }
@@ -2302,91 +2326,137 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
             }
             scan_excl<uint8_t>(c, flags, mpos, N);
         }
-        // ---- sync 1: M and the connectivity of the round's assignment -----
+        // ---- the round's tail (sort, moves, A15, A17 select) is launched
+        // before M is on the host: speculatively for up to kSpecCap movers,
+        // with M read on device (the kernels are no-ops beyond that, and the
+        // host then relaunches it for the real M).  One host sync per round
+        // reads M, the connectivity and the selection together.  Unpacked
+        // sequence keys need the ordered scan, hence M first.
+        const bool spec = packed;
         int64_t M = 0;
         unsigned long long conn_h = 0;
-        c.d2h(&M, dM, 1);
-        c.d2h(&conn_h, conn_d, 1);
-        c.sync();
-        conns.push_back((double)(int64_t)conn_h);
-        need_final = false;
-        if (M == 0) break;
-        if (packed) {
-            if (M <= kSmallSort)
-                small_sort_packed(c, mk, mv, M);
-            else
-                radix_sort_pairs(c, mk, mv, mkt, mvt, M, nullptr, gmax_bits + 32);
-        } else {
-            if (N > 0) {
-                k_mover_keys<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(N, flags, mpos, gain, W.wsum, mk, mv);
+        if (!spec) {
+            c.d2h(&M, dM, 1);
+            c.d2h(&conn_h, conn_d, 1);
+            c.sync();
+            conns.push_back((double)(int64_t)conn_h);
+            need_final = false;
+            if (M == 0) break;
+        }
+        int ibits = 1;
+        EvArgs ev{};
+        int64_t *dlt = nullptr, *act_ex = nullptr, *cum = nullptr;
+        auto launch_tail = [&](bool sp, int64_t Mh) {
+            // capacity of this launch (the per-move buffers hold N entries)
+            const int64_t Mc = sp ? std::min<int64_t>(kSpecCap, N) : Mh;
+            if (packed) {
+                if (sp)
+                    small_sort_packed(c, mk, mv, 0, dM);
+                else if (Mh <= kSmallSort)
+                    small_sort_packed(c, mk, mv, Mh);
+                else
+                    radix_sort_pairs(c, mk, mv, mkt, mvt, Mh, nullptr, gmax_bits + 32);
+            } else {
+                if (N > 0) {
+                    k_mover_keys<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(N, flags, mpos, gain, W.wsum, mk, mv);
+                    DHGP_LAUNCHED(c);
+                }
+                if (Mh <= kSmallSort)
+                    small_sort_pairs(c, mk, mv, Mh);  // vals (nodes) are distinct and ascend: stable
+                else
+                    radix_sort_pairs(c, mk, mv, mkt, mvt, Mh, nullptr, gmax_bits);
+                fill_i32(c, pos, -1, N);
+            }
+            k_build_moves_dn<<<(unsigned)std::max<int64_t>(1, cdiv(Mc, 256)), 256, 0, c.stream>>>(
+                dM, mv, assign, target, gain, node, from, to, giso, pos, sp);
+            DHGP_LAUNCHED(c);
+            // h-edges holding a mover: the only ones with sequence-gain terms or
+            // inbound events (incremental mode; the full mode scans every h-edge)
+            const int32_t *elist = nullptr, *elist_n = nullptr;
+            if (st.inc) {
+                k_mover_edges<<<g_me, 256, 0, c.stream>>>(dM, node, L.inc_off, L.inc_dat, st.emflag, st.mlist,
+                                                          st.ctr + CT_MLIST, sp);
+                DHGP_LAUNCHED(c);
+                elist = st.mlist;
+                elist_n = st.ctr + CT_MLIST;
+            }
+            // --- A15 sequence gains + A17 events (replicated: O(sum |e|), no exchange)
+            ibits = std::max(1, bitlen((uint64_t)Mc));
+            ev = EvArgs{ibits, pbits, ek, evv, ecount};
+            ev.in_from = ev_from;
+            ev.in_to = ev_to;
+            {
+                KScope ks(c, "seq_gains", 0.0);
+                unsigned long long *gacc = (unsigned long long *)gseq_acc;
+                zero_many(c,
+                          {{gacc, 8 * Mc}, {sg_ctr, 8}, {ctr, 16}, {ev_from, 4 * Mc}, {ev_to, 4 * Mc}, {ecount, 8}});
+                if (L.E > 0) {
+                    static int g_re = resident_grid(c, k_round_edges, 256, 0);
+                    const unsigned gre = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(L.E, 8), g_re));
+                    k_round_edges<<<gre, 256, 0, c.stream>>>(L.E, elist, elist_n, L.pin_off, L.pin_dat, L.dst_off,
+                                                             L.dst_dat, W.wi, r, pos, from, to, gacc, ev, sg_big,
+                                                             sg_ctr, big, ctr, tiers().edge_movers,
+                                                             sp ? dM : nullptr);
+                    DHGP_LAUNCHED(c);
+                    k_seq_gains_edge_block<<<c.num_sms, 256, 0, c.stream>>>(L.pin_off, L.pin_dat, W.wi, r, pos, from,
+                                                                             to, gacc, sg_big, sg_ctr, sg_ctr + 1);
+                    DHGP_LAUNCHED(c);
+                    k_inbound_events_block<<<c.num_sms, 256, 0, c.stream>>>(L.dst_off, L.dst_dat, r, pos, from, to,
+                                                                             ev, big, ctr, ctr + 2);
+                    DHGP_LAUNCHED(c);
+                }
+                k_round_moves<<<(unsigned)std::max<int64_t>(1, cdiv(Mc, 256)), 256, 0, c.stream>>>(
+                    dM, node, from, to, L.size, ev, giso, gacc, gseq, sp);
                 DHGP_LAUNCHED(c);
             }
-            if (M <= kSmallSort)
-                small_sort_pairs(c, mk, mv, M);  // vals (nodes) are distinct and ascend: stable
-            else
-                radix_sort_pairs(c, mk, mv, mkt, mvt, M, nullptr, gmax_bits);
-            fill_i32(c, pos, -1, N);
-        }
-        k_build_moves_dn<<<(unsigned)cdiv(M, 256), 256, 0, c.stream>>>(dM, mv, assign, target, gain, node, from, to,
-                                                                       giso, pos);
-        DHGP_LAUNCHED(c);
-        // h-edges holding a mover: the only ones with sequence-gain terms or
-        // inbound events (incremental mode; the full mode scans every h-edge)
-        const int32_t *elist = nullptr, *elist_n = nullptr;
-        if (st.inc) {
-            k_mover_edges<<<g_me, 256, 0, c.stream>>>(dM, node, L.inc_off, L.inc_dat, st.emflag, st.mlist,
-                                                      st.ctr + CT_MLIST);
-            DHGP_LAUNCHED(c);
-            elist = st.mlist;
-            elist_n = st.ctr + CT_MLIST;
-        }
-        // --- A15 sequence gains + A17 events (replicated: O(sum |e|), no exchange)
-        const int ibits = std::max(1, bitlen((uint64_t)M));
-        EvArgs ev{ibits, pbits, ek, evv, ecount};
-        ev.in_from = ev_from;
-        ev.in_to = ev_to;
-        {
-            KScope ks(c, "seq_gains", 0.0);
-            unsigned long long *gacc = (unsigned long long *)gseq_acc;
-            zero_many(c, {{gacc, 8 * M}, {sg_ctr, 8}, {ctr, 16}, {ev_from, 4 * M}, {ev_to, 4 * M}, {ecount, 8}});
-            if (L.E > 0) {
-                static int g_re = resident_grid(c, k_round_edges, 256, 0);
-                const unsigned gre = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(L.E, 8), g_re));
-                k_round_edges<<<gre, 256, 0, c.stream>>>(L.E, elist, elist_n, L.pin_off, L.pin_dat, L.dst_off,
-                                                         L.dst_dat, W.wi, r, pos, from, to, gacc, ev, sg_big, sg_ctr,
-                                                         big, ctr, tiers().edge_movers);
-                DHGP_LAUNCHED(c);
-                k_seq_gains_edge_block<<<c.num_sms, 256, 0, c.stream>>>(L.pin_off, L.pin_dat, W.wi, r, pos, from, to,
-                                                                         gacc, sg_big, sg_ctr, sg_ctr + 1);
-                DHGP_LAUNCHED(c);
-                k_inbound_events_block<<<c.num_sms, 256, 0, c.stream>>>(L.dst_off, L.dst_dat, r, pos, from, to, ev,
-                                                                         big, ctr, ctr + 2);
-                DHGP_LAUNCHED(c);
-            }
-            k_round_moves<<<(unsigned)cdiv(M, 256), 256, 0, c.stream>>>(dM, node, from, to, L.size, ev, giso, gacc,
-                                                                       gseq);
-            DHGP_LAUNCHED(c);
-        }
-        // --- A17 select: one CTA for small rounds, T read on device ----------
-        int64_t kbest = 0, total_gain = 0;
-        int64_t *dlt = c.alloc<int64_t>(M + 1);
-        int64_t *act_ex = c.alloc<int64_t>(M + 2);
-        int64_t *cum = c.alloc<int64_t>(M + 1);
-        {
+            // --- A17 select: one CTA for small rounds, T and M read on device
+            dlt = c.alloc<int64_t>(Mc + 1);
+            act_ex = c.alloc<int64_t>(Mc + 2);
+            cum = c.alloc<int64_t>(Mc + 1);
             KScope ks(c, "select", 0.0, N);
             const bool packed_ev = 1 + ibits + pbits <= 32;
-            k_select_small<<<1, SEL_THREADS, sel_smem(), c.stream>>>(ecount, M, ek, evv, gseq, psizes, pinbound,
+            k_select_small<<<1, SEL_THREADS, sel_smem(), c.stream>>>(ecount, dM, ek, evv, gseq, psizes, pinbound,
                                                                     omega, delta, ibits, pbits, act_ex, sres,
                                                                     packed_ev);
             DHGP_LAUNCHED(c);
-            // ---- sync 2: the selected prefix (or "too large"), error flags ---
+        };
+        auto free_tail = [&]() {
+            c.free(dlt);
+            c.free(act_ex);
+            c.free(cum);
+            dlt = act_ex = cum = nullptr;
+        };
+        launch_tail(spec, M);
+        int64_t kbest = 0, total_gain = 0;
+        {
+            // ---- the round's sync: the selected prefix (or "too large"), error flags
             long long hr[3];
             int32_t hc[4];
             int32_t hs[2];
             c.d2h(hr, sres, 3);
             c.d2h(hc, ctr, 4);
             c.d2h(hs, sg_ctr, 2);
+            if (spec) {
+                c.d2h(&M, dM, 1);
+                c.d2h(&conn_h, conn_d, 1);
+            }
             c.sync();
+            if (spec) {
+                conns.push_back((double)(int64_t)conn_h);
+                need_final = false;
+                if (M == 0) {
+                    free_tail();
+                    break;
+                }
+                if (M > kSpecCap) {  // the speculative launch did nothing: relaunch for the real M
+                    free_tail();
+                    launch_tail(false, M);
+                    c.d2h(hr, sres, 3);
+                    c.d2h(hc, ctr, 4);
+                    c.d2h(hs, sg_ctr, 2);
+                    c.sync();
+                }
+            }
             if (hc[2] || hs[1]) throw Error{DHGP_ERR_UNSUPPORTED, "too many movers on one h-edge"};
             kbest = hr[0];
             total_gain = hr[1];
