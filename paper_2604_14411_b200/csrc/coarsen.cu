@@ -21,6 +21,7 @@ namespace {
 // ---------------------------------------------------------------------------
 // `work` (profiling only) accumulates the algorithmic bytes read: 28 B per
 // incident h-edge (list entry, two offsets, weight) + 4 B per pin
+constexpr int kPinsInFlight = 8;
 template <class F>
 __device__ __forceinline__ void warp_for_pins(const int32_t *inc_dat, int64_t ilo, int64_t ihi, int64_t first,
                                               int64_t stride, const int64_t *pin_off, const int32_t *pin_dat,
@@ -41,12 +42,12 @@ __device__ __forceinline__ void warp_for_pins(const int32_t *inc_dat, int64_t il
         const int total = __shfl_sync(FULL_MASK, incl, 31);
         const int excl = incl - len;
         wb += 28ull * (unsigned long long)min((int64_t)bsz, ihi - base) + 4ull * (unsigned long long)total;
-        // four pins per lane in flight before any is used (the loads are the
+        // eight pins per lane in flight before any is used (the loads are the
         // latency; the hash inserts are cheap)
-        for (int s0 = 0; s0 < total; s0 += 128) {
-            int32_t oe[4], m[4];
+        for (int s0 = 0; s0 < total; s0 += 32 * kPinsInFlight) {
+            int32_t oe[kPinsInFlight], m[kPinsInFlight];
 #pragma unroll
-            for (int u = 0; u < 4; u++) {
+            for (int u = 0; u < kPinsInFlight; u++) {
                 const int s = s0 + u * 32 + lane;
                 int owner = 0;
 #pragma unroll
@@ -60,7 +61,7 @@ __device__ __forceinline__ void warp_for_pins(const int32_t *inc_dat, int64_t il
                 m[u] = s < total ? pin_dat[oplo + (s - oex)] : -1;
             }
 #pragma unroll
-            for (int u = 0; u < 4; u++)
+            for (int u = 0; u < kPinsInFlight; u++)
                 if (s0 + u * 32 + lane < total) f(oe[u], m[u]);
         }
     }
@@ -103,7 +104,12 @@ struct ScoreArgs {
     unsigned long long *work = nullptr;  // profiling: algorithmic bytes
     // diagnostics (DHGP_TRACE): candidate iterations and nodes, warp / block tier
     unsigned long long *probe = nullptr;
+    // list mode with few listed nodes (<= this; 0 = off): the block tier
+    // takes every node above kHeavySmallInc incident h-edges (idle SMs
+    // otherwise; a node's latency is the level's critical path)
+    int32_t heavy_small_list = 0;
 };
+constexpr int64_t kHeavySmallInc = 48;
 
 // next node of a persistent scoring loop: [lo, hi) or the listed nodes in it
 // (-1 = done, -2 = skip)
@@ -164,21 +170,29 @@ __device__ __forceinline__ void filter_emit(const ScoreArgs &a, int32_t node, in
         }
 #pragma unroll
         for (int u = 0; u < U; u++) {
-            if (k[u] < 0) continue;
             const int s = s0 + u * stride;
-            if (szn + sz[u] > a.omega) {
-                keys[s] = -2;
-                continue;
+            const bool valid = k[u] >= 0;
+            const bool fail = valid && szn + sz[u] > a.omega;
+            if (fail) keys[s] = -2;
+            // emit_tuple with the gathers above; one atomic per warp
+            bool emit = false;
+            long long h = 0;
+            if (valid && !fail && a.mb && mbv[u] < 0) {
+                h = (long long)vals[s];
+                emit = !(tp[u] >= 0 && !(h > ts[u] || (h == ts[u] && rn >= tp[u])));
             }
-            // emit_tuple with the gathers above
-            if (!a.mb || mbv[u] >= 0) continue;
-            const long long h = (long long)vals[s];
-            if (tp[u] >= 0 && !(h > ts[u] || (h == ts[u] && rn >= tp[u]))) continue;
-            const int i = atomicAdd(a.tup_count, 1);
-            if (i < a.tup_cap) {
-                a.tup_v[i] = k[u];
-                a.tup_b[i] = node;
-                a.tup_h[i] = h;
+            const uint32_t bal = __ballot_sync(FULL_MASK, emit);
+            if (bal) {
+                const int lane = lane_id(), leader = __ffs(bal) - 1;
+                int base = 0;
+                if (lane == leader) base = atomicAdd(a.tup_count, __popc(bal));
+                base = __shfl_sync(FULL_MASK, base, leader);
+                const int i = base + __popc(bal & ((1u << lane) - 1u));
+                if (emit && i < a.tup_cap) {
+                    a.tup_v[i] = k[u];
+                    a.tup_b[i] = node;
+                    a.tup_h[i] = h;
+                }
             }
         }
     }
@@ -209,7 +223,7 @@ __device__ __forceinline__ bool warp_union_ok(const ScoreArgs &a, int32_t n, int
 }
 
 template <class Acc>
-__global__ void __launch_bounds__(SS_WARPS * 32) k_score_warp(ScoreArgs a) {
+__global__ void __launch_bounds__(SS_WARPS * 32, 3) k_score_warp(ScoreArgs a) {
     extern __shared__ unsigned long long smem_u64[];
     Acc *svals = (Acc *)smem_u64;
     int32_t *skeys = (int32_t *)(svals + SS_WARPS * SS_CAP);
@@ -226,7 +240,10 @@ __global__ void __launch_bounds__(SS_WARPS * 32) k_score_warp(ScoreArgs a) {
         if (node == -1) break;
         if (node < 0) continue;
         const int64_t ilo = a.inc_off[node], ihi = a.inc_off[node + 1];
-        if (ihi - ilo > a.t.ss_heavy_inc) {  // hub: a whole block per node
+        const int64_t hthr = (a.heavy_small_list && *a.list_count <= a.heavy_small_list)
+                                 ? min((int64_t)a.t.ss_heavy_inc, kHeavySmallInc)
+                                 : (int64_t)a.t.ss_heavy_inc;
+        if (ihi - ilo > hthr) {  // hub: a whole block per node
             if (lane == 0) a.heavy_list[atomicAdd(a.heavy_count, 1)] = node;
             continue;
         }
@@ -814,6 +831,7 @@ void score_select_inc(Ctx &c, const DLevel &L, const DWeights &W, int64_t omega,
     a.tup_h = th;
     a.tup_count = lc + 2;
     a.tup_cap = cap;
+    a.heavy_small_list = 2 * c.num_sms;
     unsigned long long *probe = nullptr;
     if (trace_enabled()) {
         probe = c.alloc<unsigned long long>(4);

@@ -1218,6 +1218,7 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select_small(const unsigned lon
     __shared__ long long s_bv[32], s_bk[32];
     const int64_t T = (int64_t)*ecount;
     const int64_t M = *dM;
+    if (M == 0) return;  // a speculative launch for a round without movers (the host stops there)
     if (T > SEL_T || M > SEL_M - 2) {
         if (threadIdx.x == 0) res[2] = 1;
         return;
