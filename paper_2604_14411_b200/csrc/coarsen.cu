@@ -357,6 +357,7 @@ __global__ void __launch_bounds__(SH_THREADS) k_score_heavy(ScoreArgs a) {
     __shared__ long long r_v[SH_THREADS / 32];
     __shared__ int32_t r_k[SH_THREADS / 32], r_s[SH_THREADS / 32];
     __shared__ long long r_c[SH_THREADS / 32];
+    static_assert(SH_THREADS == 1024, "the winner reduction reads one entry per lane");
     const int w = warp_id(), lane = lane_id(), nw = SH_THREADS / 32;
     const int nheavy = *a.heavy_count;
     for (int t = blockIdx.x; t < nheavy; t += gridDim.x) {
@@ -371,6 +372,7 @@ __global__ void __launch_bounds__(SH_THREADS) k_score_heavy(ScoreArgs a) {
         }
         __syncthreads();
         const int64_t ilo = a.inc_off[node], ihi = a.inc_off[node + 1];
+        int pend = 0;  // this thread's new keys not yet added to snk
         // h-edges per warp batch: a node's h-edges spread over all warps
         const int bsz = (int)max((int64_t)1, min((int64_t)32, (ihi - ilo + nw - 1) / nw));
         warp_for_pins(a.inc_dat, ilo, ihi, (int64_t)w * bsz, (int64_t)nw * bsz, a.pin_off, a.pin_dat,
@@ -384,7 +386,13 @@ __global__ void __launch_bounds__(SH_THREADS) k_score_heavy(ScoreArgs a) {
                               if (k == -1) {
                                   int prev = atomicCAS(&keys[slot], -1, m);
                                   if (prev == -1) {
-                                      if (atomicAdd(&snk, 1) >= a.t.sh_limit) sover = 1;
+                                      // new keys counted in pairs (half the
+                                      // shared atomics; the limit only picks
+                                      // the tier, never the result)
+                                      if (++pend == 2) {
+                                          pend = 0;
+                                          if (atomicAdd(&snk, 2) + 2 > a.t.sh_limit) sover = 1;
+                                      }
                                       k = m;
                                   } else {
                                       k = prev;
@@ -441,15 +449,21 @@ __global__ void __launch_bounds__(SH_THREADS) k_score_heavy(ScoreArgs a) {
                 r_s[w] = bs;
             }
             __syncthreads();
-            bv = r_v[0];
-            bk = r_k[0];
-            bs = r_s[0];
-            for (int j = 1; j < nw; j++)
-                if (r_v[j] > bv || (r_v[j] == bv && r_k[j] > bk)) {
-                    bv = r_v[j];
-                    bk = r_k[j];
-                    bs = r_s[j];
+            // every warp reduces the 32 per-warp winners by shuffles
+            bv = r_v[lane];
+            bk = r_k[lane];
+            bs = r_s[lane];
+#pragma unroll
+            for (int d = 16; d > 0; d >>= 1) {
+                long long ov = __shfl_xor_sync(FULL_MASK, bv, d);
+                int32_t ok = __shfl_xor_sync(FULL_MASK, bk, d);
+                int32_t os = __shfl_xor_sync(FULL_MASK, bs, d);
+                if (ov > bv || (ov == bv && ok > bk)) {
+                    bv = ov;
+                    bk = ok;
+                    bs = os;
                 }
+            }
             __syncthreads();
             if (bk < 0) break;
             const int64_t nlo = a.in_off[node], nn = a.in_off[node + 1] - nlo;
@@ -783,10 +797,11 @@ void score_select(Ctx &c, const DLevel &L, const DWeights &W, int64_t omega, int
     }
     score_tiers(c, a, W, s, L.N);
     if (work) {  // measured algorithmic bytes (lists actually read) + outputs
+        ks.stop();
         unsigned long long h = 0;
         c.d2h(&h, work, 1);
         c.sync();
-        ks.bytes = (double)h + 12.0 * (double)(sh.hi - sh.lo);
+        ks.set_bytes((double)h + 12.0 * (double)(sh.hi - sh.lo));
         c.free(work);
     }
     if (sh.on) {  // complete (pair, score) from the other ranks' node ranges
@@ -864,12 +879,13 @@ void score_select_inc(Ctx &c, const DLevel &L, const DWeights &W, int64_t omega,
     score_tiers(c, b, W, s, N);
     if (work) {  // measured algorithmic bytes: lists read by both passes, the per-node
                  // carry (pair, score, gamma, members: 24 B) and the tuples (16 B each)
+        ks.stop();
         unsigned long long h = 0;
         int32_t nt = 0;
         c.d2h(&h, work, 1);
         c.d2h(&nt, lc + 2, 1);
         c.sync();
-        ks.bytes = (double)h + 36.0 * N + 16.0 * std::min<int64_t>(nt, cap);
+        ks.set_bytes((double)h + 36.0 * N + 16.0 * std::min<int64_t>(nt, cap));
         c.free(work);
     }
     if (trace_enabled()) {

@@ -168,6 +168,20 @@ struct KScope {
         }
     }
     ~KScope() { close(); }
+    // records the end now (before a profiling readback that syncs); the
+    // measured bytes can be set afterwards with set_bytes
+    int stopped = -1;
+    void stop() {
+        if (idx >= 0) c.kend(idx, bytes);
+        stopped = idx;
+        idx = -1;
+    }
+    void set_bytes(double b) {
+        if (stopped >= 0)
+            c.pending_bytes[stopped] = b;
+        else
+            bytes = b;
+    }
     // ends the scope early (the destructor then does nothing)
     void close() {
         if (idx >= 0) c.kend(idx, bytes);

@@ -2289,10 +2289,11 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
                 }
             }
             if (work) {  // measured algorithmic bytes: lists read (+ per node assign/size/outputs, full mode)
+                ks.stop();
                 unsigned long long h = 0;
                 c.d2h(&h, work, 1);
                 c.sync();
-                ks.bytes = (double)h + 24.0 * (full ? (double)N : 0.0);
+                ks.set_bytes((double)h + 24.0 * (full ? (double)N : 0.0));
                 c.free(work);
             }
             if (trace_enabled()) {
