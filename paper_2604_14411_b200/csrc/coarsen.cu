@@ -22,7 +22,7 @@ namespace {
 // `work` (profiling only) accumulates the algorithmic bytes read: 28 B per
 // incident h-edge (list entry, two offsets, weight) + 4 B per pin
 constexpr int kPinsInFlight = 8;
-template <class F>
+template <int kPinsInFlight = kPinsInFlight, class F>
 __device__ __forceinline__ void warp_for_pins(const int32_t *inc_dat, int64_t ilo, int64_t ihi, int64_t first,
                                               int64_t stride, const int64_t *pin_off, const int32_t *pin_dat,
                                               F &&f, unsigned long long *work = nullptr, int bsz = 32) {
@@ -375,7 +375,7 @@ __global__ void __launch_bounds__(SH_THREADS) k_score_heavy(ScoreArgs a) {
         int pend = 0;  // this thread's new keys not yet added to snk
         // h-edges per warp batch: a node's h-edges spread over all warps
         const int bsz = (int)max((int64_t)1, min((int64_t)32, (ihi - ilo + nw - 1) / nw));
-        warp_for_pins(a.inc_dat, ilo, ihi, (int64_t)w * bsz, (int64_t)nw * bsz, a.pin_off, a.pin_dat,
+        warp_for_pins<4>(a.inc_dat, ilo, ihi, (int64_t)w * bsz, (int64_t)nw * bsz, a.pin_off, a.pin_dat,
                       [&](int32_t e, int32_t m) {
                           if (m == node || sover) return;
                           const Acc we = (Acc)a.wi[e];
@@ -412,7 +412,7 @@ __global__ void __launch_bounds__(SH_THREADS) k_score_heavy(ScoreArgs a) {
             __syncthreads();
             continue;
         }
-        filter_emit<8>(a, node, keys, vals, threadIdx.x, SH_THREADS, SH_CAP);
+        filter_emit<4>(a, node, keys, vals, threadIdx.x, SH_THREADS, SH_CAP);
         __syncthreads();
         int32_t best_m = -1;
         long long best_v = 0;
@@ -528,7 +528,7 @@ __global__ void __launch_bounds__(SB_THREADS) k_score_block(ScoreArgs a, long lo
         const int64_t ilo = a.inc_off[node], ihi = a.inc_off[node + 1];
         // h-edges per warp batch: a node's h-edges spread over all warps
         const int bsz = (int)max((int64_t)1, min((int64_t)32, (ihi - ilo + nw - 1) / nw));
-        warp_for_pins(a.inc_dat, ilo, ihi, (int64_t)w * bsz, (int64_t)nw * bsz, a.pin_off, a.pin_dat,
+        warp_for_pins<4>(a.inc_dat, ilo, ihi, (int64_t)w * bsz, (int64_t)nw * bsz, a.pin_off, a.pin_dat,
                       [&](int32_t e, int32_t m) {
                           if (m == node) return;
                           long long old = atomicCAS((unsigned long long *)&dense[m], ~0ull, 0ull);

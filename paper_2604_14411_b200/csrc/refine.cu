@@ -328,9 +328,11 @@ __device__ __forceinline__ void write_proposal(const ProposeArgs &a, int32_t nod
 template <class F>
 __device__ __forceinline__ int64_t warp_for_runs(const int32_t *inc_dat, int64_t ilo, int64_t ihi, int64_t first,
                                                  int64_t stride, int bsz, const int64_t *pin_off, const int32_t *len,
-                                                 const int64_t *wi, unsigned long long *work, F &&f) {
+                                                 const int64_t *wi, unsigned long long *work, const int32_t *rpart,
+                                                 const int32_t *rcnt, F &&f) {
     // `work` (profiling only): algorithmic bytes read — 24 B per incident
     // h-edge (list entry, run base, run count, weight) + 8 B per run
+    constexpr int U = 4;  // run slots per lane in flight
     const int lane = lane_id();
     int64_t total = 0;
     unsigned long long wb = 0;
@@ -350,19 +352,29 @@ __device__ __forceinline__ int64_t warp_for_runs(const int32_t *inc_dat, int64_t
         const int tot = __shfl_sync(FULL_MASK, incl, 31);
         const int excl = incl - l;
         wb += 24ull * (unsigned long long)min((int64_t)bsz, ihi - base) + 8ull * (unsigned long long)tot;
-        for (int s0 = 0; s0 < tot; s0 += 32) {
-            const int sl = s0 + lane;
-            int owner = 0;
+        for (int s0 = 0; s0 < tot; s0 += 32 * U) {
+            int32_t oe[U], rp[U], rc[U];
+            int64_t owe[U];
 #pragma unroll
-            for (int step = 16; step > 0; step >>= 1) {
-                const int ex = __shfl_sync(FULL_MASK, excl, owner + step);
-                if (ex <= sl) owner += step;
+            for (int u = 0; u < U; u++) {
+                const int sl = s0 + u * 32 + lane;
+                int owner = 0;
+#pragma unroll
+                for (int step = 16; step > 0; step >>= 1) {
+                    const int ex = __shfl_sync(FULL_MASK, excl, owner + step);
+                    if (ex <= sl) owner += step;
+                }
+                oe[u] = __shfl_sync(FULL_MASK, e, owner);
+                const int64_t oplo = __shfl_sync(FULL_MASK, plo, owner);
+                owe[u] = __shfl_sync(FULL_MASK, we, owner);
+                const int oex = __shfl_sync(FULL_MASK, excl, owner);
+                const int64_t k = oplo + (sl - oex);
+                rp[u] = sl < tot ? rpart[k] : -1;
+                rc[u] = sl < tot ? rcnt[k] : 0;
             }
-            const int32_t oe = __shfl_sync(FULL_MASK, e, owner);
-            const int64_t oplo = __shfl_sync(FULL_MASK, plo, owner);
-            const int64_t owe = __shfl_sync(FULL_MASK, we, owner);
-            const int oex = __shfl_sync(FULL_MASK, excl, owner);
-            if (sl < tot) f(oe, owe, oplo + (sl - oex));
+#pragma unroll
+            for (int u = 0; u < U; u++)
+                if (s0 + u * 32 + lane < tot) f(oe[u], owe[u], rp[u], rc[u]);
         }
     }
     if (work && lane == 0 && wb) atomicAdd(work, wb);
@@ -379,7 +391,7 @@ __device__ __forceinline__ uint32_t pslot(int32_t p) { return ((uint32_t)p * 265
 
 
 template <class Acc>
-__global__ void __launch_bounds__(PR_WARPS * 32) k_propose_warp(ProposeArgs a) {
+__global__ void __launch_bounds__(PR_WARPS * 32, 4) k_propose_warp(ProposeArgs a) {
     extern __shared__ unsigned long long smem_u64[];
     Acc *svals = (Acc *)smem_u64;
     int32_t *skeys = (int32_t *)(svals + PR_WARPS * PR_CAP);
@@ -428,9 +440,8 @@ __global__ void __launch_bounds__(PR_WARPS * 32) k_propose_warp(ProposeArgs a) {
         __syncwarp();
         const int32_t ps = a.assign[node];
         int64_t total = 0, saving = 0;
-        total = warp_for_runs(a.inc_dat, ilo, ihi, 0, 32, 32, a.r.off, a.r.len, a.wi, a.work, [&](int32_t, int64_t we, int64_t k) {
-            const int32_t p = a.r.part[k];
-            if (p == ps && a.r.cnt[k] == 1) saving += we;
+        total = warp_for_runs(a.inc_dat, ilo, ihi, 0, 32, 32, a.r.off, a.r.len, a.wi, a.work, a.r.part, a.r.cnt, [&](int32_t, int64_t we, int32_t p, int32_t pc) {
+            if (p == ps && pc == 1) saving += we;
             if (sover[w]) return;
             const uint32_t h = pslot(p);
             for (int probe = 0; probe < PR_CAP; probe++) {
@@ -515,7 +526,7 @@ __device__ __forceinline__ void block_best_gain(long long bg, int32_t bp, long l
 }
 
 template <class Acc>
-__global__ void __launch_bounds__(PM_THREADS) k_propose_mid(ProposeArgs a) {
+__global__ void __launch_bounds__(PM_THREADS, 4) k_propose_mid(ProposeArgs a) {
     extern __shared__ unsigned long long smem_u64[];
     Acc *vals = (Acc *)smem_u64;
     int32_t *keys = (int32_t *)(vals + PM_CAP);
@@ -559,9 +570,9 @@ __global__ void __launch_bounds__(PM_THREADS) k_propose_mid(ProposeArgs a) {
         // h-edges per warp batch: a node's h-edges spread over all warps
         const int rb = (int)max((int64_t)1, min((int64_t)32, (ihi - ilo + nw - 1) / nw));
         total = warp_for_runs(a.inc_dat, ilo, ihi, (int64_t)w * rb, (int64_t)nw * rb, rb, a.r.off, a.r.len, a.wi, a.work,
-                              [&](int32_t, int64_t we, int64_t k) {
-                                  const int32_t p = a.r.part[k];
-                                  if (p == ps && a.r.cnt[k] == 1) saving += we;
+                              a.r.part, a.r.cnt,
+                              [&](int32_t, int64_t we, int32_t p, int32_t pc) {
+                                  if (p == ps && pc == 1) saving += we;
                                   if (sover) return;
                                   const uint32_t h = ((uint32_t)p * 2654435761u) >> (32 - lg);
                                   for (int probe = 0; probe < cap; probe++) {
@@ -657,9 +668,9 @@ __global__ void __launch_bounds__(THREADS) k_propose_heavy(ProposeArgs a) {
         // h-edges per warp batch: a node's h-edges spread over all warps
         const int rb = (int)max((int64_t)1, min((int64_t)32, (ihi - ilo + nw - 1) / nw));
         total = warp_for_runs(a.inc_dat, ilo, ihi, (int64_t)w * rb, (int64_t)nw * rb, rb, a.r.off, a.r.len, a.wi, a.work,
-                              [&](int32_t, int64_t we, int64_t k) {
-                                  const int32_t p = a.r.part[k];
-                                  if (p == ps && a.r.cnt[k] == 1) saving += we;
+                              a.r.part, a.r.cnt,
+                              [&](int32_t, int64_t we, int32_t p, int32_t pc) {
+                                  if (p == ps && pc == 1) saving += we;
                                   atomicAdd(&pres[p], (Acc)we);
                                   const uint32_t bit = 1u << (p & 31);
                                   if (!(atomicOr(&touched[p >> 5], bit) & bit)) tlist[atomicAdd(&s_nt, 1)] = p;
@@ -773,9 +784,9 @@ __global__ void __launch_bounds__(256) k_propose_hub(ProposeArgs a, long long *h
         // h-edges per warp batch: a node's h-edges spread over all warps
         const int rb = (int)max((int64_t)1, min((int64_t)32, (ihi - ilo + nw - 1) / nw));
         total = warp_for_runs(a.inc_dat, ilo, ihi, (int64_t)w * rb, (int64_t)nw * rb, rb, a.r.off, a.r.len, a.wi, a.work,
-                              [&](int32_t, int64_t we, int64_t k) {
-                                  const int32_t p = a.r.part[k];
-                                  if (p == ps && a.r.cnt[k] == 1) saving += we;
+                              a.r.part, a.r.cnt,
+                              [&](int32_t, int64_t we, int32_t p, int32_t pc) {
+                                  if (p == ps && pc == 1) saving += we;
                                   atomicAdd(&pres[p], (Acc)we);
                               });
         total = warp_sum(total);
@@ -852,9 +863,9 @@ __global__ void __launch_bounds__(PB_THREADS) k_propose_block(ProposeArgs a, lon
         // h-edges per warp batch: a node's h-edges spread over all warps
         const int rb = (int)max((int64_t)1, min((int64_t)32, (ihi - ilo + nw - 1) / nw));
         total = warp_for_runs(a.inc_dat, ilo, ihi, (int64_t)w * rb, (int64_t)nw * rb, rb, a.r.off, a.r.len, a.wi, a.work,
-                              [&](int32_t, int64_t we, int64_t k) {
-                                  const int32_t p = a.r.part[k];
-                                  if (p == ps && a.r.cnt[k] == 1) saving += we;
+                              a.r.part, a.r.cnt,
+                              [&](int32_t, int64_t we, int32_t p, int32_t pc) {
+                                  if (p == ps && pc == 1) saving += we;
                                   const long long old = atomicCAS((unsigned long long *)&dense[p], ~0ull, 0ull);
                                   if (old == -1ll) touched[atomicAdd(&s_nt, 1)] = p;
                                   atomicAdd((unsigned long long *)&dense[p], (unsigned long long)we);
@@ -1938,7 +1949,7 @@ __global__ void k_project_state(int32_t N, const int32_t *gamma, const int32_t *
                                 const int32_t *fpart_c, const int32_t *ndirty_c, int32_t *assign_f,
                                 int32_t *target_f, int64_t *gain_f, uint8_t *fsens_f, int32_t *fpart_f,
                                 int32_t *ndirty_f, int32_t *nlist, int32_t *ncount,
-                                int32_t *splist, int32_t *spcount) {
+                                int32_t *splist, int32_t *spcount, int32_t *spfirst) {
     const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (n >= N) return;
     const int32_t g = gamma[n];
@@ -1952,13 +1963,46 @@ __global__ void k_project_state(int32_t N, const int32_t *gamma, const int32_t *
     const bool d = split || ndirty_c[g];
     ndirty_f[n] = d;
     if (d) nlist[atomicAdd(ncount, 1)] = (int32_t)n;
-    if (split) splist[atomicAdd(spcount, 1)] = (int32_t)n;
+    if (split) {  // the second half of a cluster to arrive emits the pair
+        const int32_t o = atomicExch(&spfirst[g], (int32_t)n);
+        if (o >= 0) {
+            const int i = atomicAdd(spcount, 1);
+            splist[2 * i] = min(o, (int32_t)n);
+            splist[2 * i + 1] = max(o, (int32_t)n);
+        }
+    }
 }
 
-__global__ void k_mark_split_edges(const int32_t *splist, const int32_t *spcount, const int64_t *inc_off,
-                                   const int32_t *inc_dat, int32_t *edirty, int32_t *elist, int32_t *ecount) {
-    grid_incidences(*spcount, [&](int64_t i) { return splist[i]; }, inc_off, inc_dat,
-                    [&](int64_t, int32_t e) { push_once(&edirty[e], 1, e, elist, ecount); });
+// Run counts after a split: cluster c of part P splits into halves a, b.  An
+// h-edge holding one half held c, so its counts stand; one holding both gains
+// a pin of P (pins[e, P] + 1) and, when both halves are destinations, a
+// destination pin (pins_in[e, P] + 1).  Parts, lambda and the distinct-inbound
+// counts are unchanged.  A CTA per split: inc(a) n inc(b) and in(a) n in(b)
+// by binary search of the shorter list in the longer.
+__global__ void k_split_counts(const int32_t *splist, const int32_t *spcount, const int64_t *inc_off,
+                               const int32_t *inc_dat, const int64_t *in_off, const int32_t *in_dat,
+                               const int32_t *assign, Runs r) {
+    const int n = *spcount;
+    for (int t = blockIdx.x; t < n; t += gridDim.x) {
+        const int32_t a = splist[2 * t], b = splist[2 * t + 1], P = assign[a];
+#pragma unroll
+        for (int fam = 0; fam < 2; fam++) {
+            const int64_t *off = fam ? in_off : inc_off;
+            const int32_t *dat = fam ? in_dat : inc_dat;
+            const int64_t alo = off[a], na = off[a + 1] - alo, blo = off[b], nb = off[b + 1] - blo;
+            const bool as = na <= nb;
+            const int32_t *S = dat + (as ? alo : blo), *L = dat + (as ? blo : alo);
+            const int64_t ns = as ? na : nb, nl = as ? nb : na;
+            int32_t *cnt = fam ? r.cin : r.cnt;
+            for (int64_t i = threadIdx.x; i < ns; i += blockDim.x) {
+                const int32_t e = S[i];
+                if (bsearch_dev(L, 0, nl, e) < 0) continue;
+                const int64_t lo = r.off[e];
+                const int32_t k = run_find(r, lo, r.len[e], P);
+                atomicAdd(&cnt[lo + k], 1);
+            }
+        }
+    }
 }
 
 enum { CT_NLIST = 0, CT_ELIST = 1, CT_MLIST = 2, CT_SPLIST = 3, CT_WIDE = 4 };
@@ -1992,6 +2036,7 @@ void refine_state_init(Ctx &c, RefineState &st, const DLevel &level0, int32_t K,
     st.ndirty2 = c.alloc<int32_t>(n0);
     st.nlist = c.alloc<int32_t>(n0);
     st.splist = c.alloc<int32_t>(n0);
+    st.spfirst = c.alloc<int32_t>(n0);
     st.ccount = c.alloc<int32_t>(n0);
     st.edirty = c.alloc<int32_t>(e0);
     st.elist = c.alloc<int32_t>(e0);
@@ -2022,7 +2067,7 @@ void refine_state_release(Ctx &c, RefineState &st) {
     for (void *p : {(void *)st.rpart, (void *)st.rcnt, (void *)st.rcin, (void *)st.rlen, (void *)st.psizes,
                     (void *)st.pinbound, (void *)st.pflags, (void *)st.conn, (void *)st.target, (void *)st.target2,
                     (void *)st.gain, (void *)st.gain2, (void *)st.fsens, (void *)st.fsens2, (void *)st.fpart, (void *)st.fpart2, (void *)st.ndirty,
-                    (void *)st.ndirty2, (void *)st.nlist, (void *)st.splist, (void *)st.ccount, (void *)st.edirty,
+                    (void *)st.ndirty2, (void *)st.nlist, (void *)st.splist, (void *)st.spfirst, (void *)st.ccount, (void *)st.edirty,
                     (void *)st.elist, (void *)st.emflag, (void *)st.mlist, (void *)st.wide, (void *)st.ctr, (void *)st.hacc,
                     (void *)st.htot, (void *)st.hdone, (void *)st.hlist, (void *)st.hpref})
         c.free(p);
@@ -2039,14 +2084,20 @@ void refine_project(Ctx &c, RefineState &st, const DLevel &fine, int32_t coarse_
             DHGP_LAUNCHED(c);
             c.zero(st.ctr + CT_NLIST, 1);
             c.zero(st.ctr + CT_SPLIST, 1);
+            c.fill_bytes(st.spfirst, 0xff, std::max<int32_t>(1, coarse_n));
             k_project_state<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(
                 N, fine.gamma, st.ccount, assign, st.target, st.gain, st.fsens, st.fpart, st.ndirty, assign2,
                 st.target2, st.gain2, st.fsens2, st.fpart2, st.ndirty2, st.nlist, st.ctr + CT_NLIST, st.splist,
-                st.ctr + CT_SPLIST);
+                st.ctr + CT_SPLIST, st.spfirst);
             DHGP_LAUNCHED(c);
-            static int g = resident_grid(c, k_mark_split_edges, 256, 0);
-            k_mark_split_edges<<<g, 256, 0, c.stream>>>(st.splist, st.ctr + CT_SPLIST, fine.inc_off, fine.inc_dat,
-                                                        st.edirty, st.elist, st.ctr + CT_ELIST);
+            Runs r;
+            r.off = st.roff;
+            r.part = st.rpart;
+            r.cnt = st.rcnt;
+            r.cin = st.rcin;
+            r.len = st.rlen;
+            k_split_counts<<<2 * c.num_sms, 256, 0, c.stream>>>(st.splist, st.ctr + CT_SPLIST, fine.inc_off,
+                                                                fine.inc_dat, fine.in_off, fine.in_dat, assign2, r);
             DHGP_LAUNCHED(c);
             std::swap(st.target, st.target2);
             std::swap(st.gain, st.gain2);

@@ -46,7 +46,9 @@ struct RefineState {
     uint8_t *fsens = nullptr, *fsens2 = nullptr;           // filtered positive parts: count (3 = more)
     int32_t *fpart = nullptr, *fpart2 = nullptr;           // [2 ncap] the first two of them
     int32_t *ndirty = nullptr, *ndirty2 = nullptr;         // [N0] dirty-node flags
-    int32_t *nlist = nullptr, *splist = nullptr, *ccount = nullptr;  // [N0]
+    int32_t *nlist = nullptr, *ccount = nullptr;  // [N0]
+    int32_t *splist = nullptr;   // [N0] split clusters' halves as (min, max) pairs
+    int32_t *spfirst = nullptr;  // [N0] per coarse node: the first half seen (pairing)
     int32_t *edirty = nullptr, *elist = nullptr;           // [E] dirty h-edges (bit 0 split, bit 1 moved)
     int32_t *emflag = nullptr, *mlist = nullptr;           // [E] h-edges of the round's movers
     int32_t *wide = nullptr;                               // [E] dirty h-edges over 128 pins (block update)
