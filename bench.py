@@ -328,6 +328,7 @@ def run_ours(args, ws, rank, local):
         "roofline": roofline,
         "cpu_baseline": cpu,
         "phase_ms": phases,
+        "step_s": [round(t, 4) for t in times],
         "exchange": xstats,
         "kernels": sorted(kstats, key=lambda k: -k["ms"])[:12],
     }
