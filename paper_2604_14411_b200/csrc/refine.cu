@@ -476,11 +476,23 @@ __global__ void __launch_bounds__(PR_WARPS * 32, 4) k_propose_warp(ProposeArgs a
         int32_t bp = -1;
         if (lane == 0) s_nf[w] = 0;
         __syncwarp();
-        for (int s = lane; s < PR_CAP; s += 32) {
-            const int32_t p = keys[s];
-            if (p < 0 || p == ps) continue;
-            consider_part(p, saving - (total - (long long)vals[s]), a.psizes[p] + sz <= a.omega, bg, bp, &s_nf[w],
-                          s_f[w]);
+        // the parts' sizes are gathered 4 slots at a time (one round trip each)
+        for (int s0 = lane; s0 < PR_CAP; s0 += 4 * 32) {
+            int32_t pp[4];
+            long long vv[4], pz[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const int s = s0 + u * 32;
+                pp[u] = s < PR_CAP ? keys[s] : -1;
+                if (pp[u] == ps) pp[u] = -1;
+                vv[u] = pp[u] >= 0 ? (long long)vals[s] : 0;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; u++) pz[u] = pp[u] >= 0 ? a.psizes[pp[u]] : 0;
+#pragma unroll
+            for (int u = 0; u < 4; u++)
+                if (pp[u] >= 0)
+                    consider_part(pp[u], saving - (total - vv[u]), pz[u] + sz <= a.omega, bg, bp, &s_nf[w], s_f[w]);
         }
         warp_best_gain(bg, bp);
         __syncwarp();
@@ -618,10 +630,22 @@ __global__ void __launch_bounds__(PM_THREADS, 4) k_propose_mid(ProposeArgs a) {
         int32_t bp = -1;
         if (threadIdx.x == 0) s_nf = 0;
         __syncthreads();
-        for (int s = threadIdx.x; s < cap; s += PM_THREADS) {
-            const int32_t p = keys[s];
-            if (p < 0 || p == ps) continue;
-            consider_part(p, saving - (total - (long long)vals[s]), a.psizes[p] + sz <= a.omega, bg, bp, &s_nf, s_f);
+        for (int s0 = threadIdx.x; s0 < cap; s0 += 4 * PM_THREADS) {  // sizes gathered 4 slots at a time
+            int32_t pp[4];
+            long long vv[4], pz[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const int s = s0 + u * PM_THREADS;
+                pp[u] = s < cap ? keys[s] : -1;
+                if (pp[u] == ps) pp[u] = -1;
+                vv[u] = pp[u] >= 0 ? (long long)vals[s] : 0;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; u++) pz[u] = pp[u] >= 0 ? a.psizes[pp[u]] : 0;
+#pragma unroll
+            for (int u = 0; u < 4; u++)
+                if (pp[u] >= 0)
+                    consider_part(pp[u], saving - (total - vv[u]), pz[u] + sz <= a.omega, bg, bp, &s_nf, s_f);
         }
         long long g;
         int32_t p;
@@ -695,13 +719,28 @@ __global__ void __launch_bounds__(THREADS) k_propose_heavy(ProposeArgs a) {
         int32_t bp = -1;
         if (threadIdx.x == 0) s_nf = 0;
         __syncthreads();
-        for (int i = threadIdx.x; i < nt; i += THREADS) {
-            const int32_t p = tlist[i];
-            const long long pv = (long long)pres[p];
-            pres[p] = 0;
-            touched[p >> 5] = 0;
-            if (p == ps) continue;
-            consider_part(p, saving - (total - pv), a.psizes[p] + sz <= a.omega, bg, bp, &s_nf, s_f);
+        for (int i0 = threadIdx.x; i0 < nt; i0 += 4 * THREADS) {  // sizes gathered 4 parts at a time
+            int32_t pp[4];
+            long long vv[4], pz[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const int i = i0 + u * THREADS;
+                pp[u] = -1;
+                vv[u] = 0;
+                if (i < nt) {
+                    const int32_t p = tlist[i];
+                    vv[u] = (long long)pres[p];
+                    pres[p] = 0;
+                    touched[p >> 5] = 0;
+                    pp[u] = p == ps ? -1 : p;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; u++) pz[u] = pp[u] >= 0 ? a.psizes[pp[u]] : 0;
+#pragma unroll
+            for (int u = 0; u < 4; u++)
+                if (pp[u] >= 0)
+                    consider_part(pp[u], saving - (total - vv[u]), pz[u] + sz <= a.omega, bg, bp, &s_nf, s_f);
         }
         long long g;
         int32_t p;
