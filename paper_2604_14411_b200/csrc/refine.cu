@@ -16,8 +16,10 @@ namespace {
 
 struct Runs {
     const int64_t *off = nullptr;  // [E+1] run base per h-edge (>= |pins(e)| slots each)
-    int32_t *part = nullptr;  // [U] distinct parts per h-edge (ascending)
-    int32_t *cnt = nullptr;   // [U] pins of the h-edge in that part
+    // [2U] per run slot k: pc[2k] = the part (ascending within an h-edge),
+    // pc[2k+1] = the h-edge's pins in that part — interleaved so that one
+    // sector serves both (the proposal tiers read them together)
+    int32_t *pc = nullptr;
     int32_t *cin = nullptr;   // [U] destination pins of the h-edge in that part
     int32_t *len = nullptr;   // [E] lambda(e)
 };
@@ -28,8 +30,16 @@ struct Runs {
 constexpr int64_t kSpecCap = kSmallSort;
 
 __device__ __forceinline__ int32_t run_find(const Runs &r, int64_t lo, int32_t len, int32_t p) {
-    int64_t k = lower_bound_dev<int32_t>(r.part, lo, lo + len, p);
-    return (k < lo + len && r.part[k] == p) ? (int32_t)(k - lo) : -1;
+    int64_t a = lo, b = lo + len;  // lower bound of p among the parts pc[2a], ...
+    while (a < b) {
+        const int64_t mid = (a + b) >> 1;
+        if (r.pc[2 * mid] < p)
+            a = mid + 1;
+        else
+            b = mid;
+    }
+    const int64_t k = a;
+    return (k < lo + len && r.pc[2 * (k)] == p) ? (int32_t)(k - lo) : -1;
 }
 
 // per h-edge: run lists from the per-edge sorted parts, connectivity
@@ -48,8 +58,8 @@ __global__ void k_edge_runs(int32_t E, const int64_t *pin_off, const int32_t *so
             int32_t p = sorted_parts[j];
             int64_t j2 = j + 1;
             while (j2 < hi && sorted_parts[j2] == p) j2++;
-            r.part[lo + lam] = p;
-            r.cnt[lo + lam] = (int32_t)(j2 - j);
+            r.pc[2 * (lo + lam)] = p;
+            r.pc[2 * (lo + lam) + 1] = (int32_t)(j2 - j);
             r.cin[lo + lam] = 0;
             lam++;
             j = j2;
@@ -61,7 +71,7 @@ __global__ void k_edge_runs(int32_t E, const int64_t *pin_off, const int32_t *so
         }
         if (pinbound)
             for (int32_t k = 0; k < lam; k++)
-                if (r.cin[lo + k] > 0) atomicAdd((unsigned long long *)&pinbound[r.part[lo + k]], 1ull);
+                if (r.cin[lo + k] > 0) atomicAdd((unsigned long long *)&pinbound[r.pc[2 * (lo + k)]], 1ull);
         if (lam > 0) contrib = wi[e] * (int64_t)(lam - 1);
     }
     int64_t t = block_sum<int64_t>(contrib, sh);
@@ -90,28 +100,28 @@ __global__ void k_edge_runs_warp(int32_t E, const int64_t *pin_off, const int32_
             const uint32_t bal = __ballot_sync(FULL_MASK, head);
             if (head) {
                 const int32_t j = lam + __popc(bal & lt);
-                r.part[lo + j] = p;
-                r.cnt[lo + j] = (int32_t)i;  // run start for now
+                r.pc[2 * (lo + j)] = p;
+                r.pc[2 * (lo + j) + 1] = (int32_t)i;  // run start for now
                 r.cin[lo + j] = 0;
             }
             lam += __popc(bal);
         }
         __syncwarp();
         for (int32_t j = lane; j < lam; j += 32) {
-            const int32_t st = r.cnt[lo + j];
-            const int32_t nx = j + 1 < lam ? r.cnt[lo + j + 1] : (int32_t)len;
+            const int32_t st = r.pc[2 * (lo + j) + 1];
+            const int32_t nx = j + 1 < lam ? r.pc[2 * (lo + j + 1) + 1] : (int32_t)len;
             __syncwarp(__activemask());
-            r.cnt[lo + j] = nx - st;
+            r.pc[2 * (lo + j) + 1] = nx - st;
         }
         __syncwarp();
         // second pass turns starts into lengths; the loop above may race when
         // lam > 32, so recompute those from the sorted parts directly
         if (lam > 32) {
             for (int32_t j = lane; j < lam; j += 32) {
-                const int32_t p = r.part[lo + j];
+                const int32_t p = r.pc[2 * (lo + j)];
                 int64_t a0 = lower_bound_dev<int32_t>(sorted_parts, plo, plo + len, p);
                 int64_t a1 = lower_bound_dev<int32_t>(sorted_parts, plo, plo + len, p + 1);
-                r.cnt[lo + j] = (int32_t)(a1 - a0);
+                r.pc[2 * (lo + j) + 1] = (int32_t)(a1 - a0);
             }
             __syncwarp();
         }
@@ -123,7 +133,7 @@ __global__ void k_edge_runs_warp(int32_t E, const int64_t *pin_off, const int32_
         __syncwarp();
         if (pinbound)
             for (int32_t j = lane; j < lam; j += 32)
-                if (r.cin[lo + j] > 0) atomicAdd((unsigned long long *)&pinbound[r.part[lo + j]], 1ull);
+                if (r.cin[lo + j] > 0) atomicAdd((unsigned long long *)&pinbound[r.pc[2 * (lo + j)]], 1ull);
         if (lane == 0 && lam > 0) contrib += wi[e] * (int64_t)(lam - 1);
     }
     if (lane == 0 && contrib) atomicAdd(conn, (unsigned long long)contrib);
@@ -171,8 +181,8 @@ __device__ __forceinline__ int32_t warp_edge_runs(int64_t e, int64_t plo, int64_
                     if (bal[k2]) next = k2 * 32 + __ffs(bal[k2]) - 1;
             }
             const int32_t j = before + __popc(bal[k] & lt);
-            r.part[lo + j] = (int32_t)v[k];
-            r.cnt[lo + j] = next - i;
+            r.pc[2 * (lo + j)] = (int32_t)v[k];
+            r.pc[2 * (lo + j) + 1] = next - i;
             r.cin[lo + j] = 0;
         }
         before += __popc(bal[k]);
@@ -186,7 +196,7 @@ __device__ __forceinline__ int32_t warp_edge_runs(int64_t e, int64_t plo, int64_
     __syncwarp();
     if (pinbound)
         for (int32_t j = lane; j < lam; j += 32)
-            if (r.cin[lo + j] > 0) atomicAdd((unsigned long long *)&pinbound[r.part[lo + j]], 1ull);
+            if (r.cin[lo + j] > 0) atomicAdd((unsigned long long *)&pinbound[r.pc[2 * (lo + j)]], 1ull);
     return lam;
 }
 
@@ -328,8 +338,8 @@ __device__ __forceinline__ void write_proposal(const ProposeArgs &a, int32_t nod
 template <class F>
 __device__ __forceinline__ int64_t warp_for_runs(const int32_t *inc_dat, int64_t ilo, int64_t ihi, int64_t first,
                                                  int64_t stride, int bsz, const int64_t *pin_off, const int32_t *len,
-                                                 const int64_t *wi, unsigned long long *work, const int32_t *rpart,
-                                                 const int32_t *rcnt, F &&f) {
+                                                 const int64_t *wi, unsigned long long *work, const int32_t *rpc,
+                                                 F &&f) {
     // `work` (profiling only): algorithmic bytes read — 24 B per incident
     // h-edge (list entry, run base, run count, weight) + 8 B per run
     constexpr int U = 4;  // run slots per lane in flight
@@ -369,8 +379,9 @@ __device__ __forceinline__ int64_t warp_for_runs(const int32_t *inc_dat, int64_t
                 owe[u] = __shfl_sync(FULL_MASK, we, owner);
                 const int oex = __shfl_sync(FULL_MASK, excl, owner);
                 const int64_t k = oplo + (sl - oex);
-                rp[u] = sl < tot ? rpart[k] : -1;
-                rc[u] = sl < tot ? rcnt[k] : 0;
+                const int2 v = sl < tot ? reinterpret_cast<const int2 *>(rpc)[k] : make_int2(-1, 0);
+                rp[u] = v.x;
+                rc[u] = v.y;
             }
 #pragma unroll
             for (int u = 0; u < U; u++)
@@ -440,7 +451,7 @@ __global__ void __launch_bounds__(PR_WARPS * 32, 4) k_propose_warp(ProposeArgs a
         __syncwarp();
         const int32_t ps = a.assign[node];
         int64_t total = 0, saving = 0;
-        total = warp_for_runs(a.inc_dat, ilo, ihi, 0, 32, 32, a.r.off, a.r.len, a.wi, a.work, a.r.part, a.r.cnt, [&](int32_t, int64_t we, int32_t p, int32_t pc) {
+        total = warp_for_runs(a.inc_dat, ilo, ihi, 0, 32, 32, a.r.off, a.r.len, a.wi, a.work, a.r.pc, [&](int32_t, int64_t we, int32_t p, int32_t pc) {
             if (p == ps && pc == 1) saving += we;
             if (sover[w]) return;
             const uint32_t h = pslot(p);
@@ -582,7 +593,7 @@ __global__ void __launch_bounds__(PM_THREADS, 4) k_propose_mid(ProposeArgs a) {
         // h-edges per warp batch: a node's h-edges spread over all warps
         const int rb = (int)max((int64_t)1, min((int64_t)32, (ihi - ilo + nw - 1) / nw));
         total = warp_for_runs(a.inc_dat, ilo, ihi, (int64_t)w * rb, (int64_t)nw * rb, rb, a.r.off, a.r.len, a.wi, a.work,
-                              a.r.part, a.r.cnt,
+                              a.r.pc,
                               [&](int32_t, int64_t we, int32_t p, int32_t pc) {
                                   if (p == ps && pc == 1) saving += we;
                                   if (sover) return;
@@ -692,7 +703,7 @@ __global__ void __launch_bounds__(THREADS) k_propose_heavy(ProposeArgs a) {
         // h-edges per warp batch: a node's h-edges spread over all warps
         const int rb = (int)max((int64_t)1, min((int64_t)32, (ihi - ilo + nw - 1) / nw));
         total = warp_for_runs(a.inc_dat, ilo, ihi, (int64_t)w * rb, (int64_t)nw * rb, rb, a.r.off, a.r.len, a.wi, a.work,
-                              a.r.part, a.r.cnt,
+                              a.r.pc,
                               [&](int32_t, int64_t we, int32_t p, int32_t pc) {
                                   if (p == ps && pc == 1) saving += we;
                                   atomicAdd(&pres[p], (Acc)we);
@@ -823,7 +834,7 @@ __global__ void __launch_bounds__(256) k_propose_hub(ProposeArgs a, long long *h
         // h-edges per warp batch: a node's h-edges spread over all warps
         const int rb = (int)max((int64_t)1, min((int64_t)32, (ihi - ilo + nw - 1) / nw));
         total = warp_for_runs(a.inc_dat, ilo, ihi, (int64_t)w * rb, (int64_t)nw * rb, rb, a.r.off, a.r.len, a.wi, a.work,
-                              a.r.part, a.r.cnt,
+                              a.r.pc,
                               [&](int32_t, int64_t we, int32_t p, int32_t pc) {
                                   if (p == ps && pc == 1) saving += we;
                                   atomicAdd(&pres[p], (Acc)we);
@@ -902,7 +913,7 @@ __global__ void __launch_bounds__(PB_THREADS) k_propose_block(ProposeArgs a, lon
         // h-edges per warp batch: a node's h-edges spread over all warps
         const int rb = (int)max((int64_t)1, min((int64_t)32, (ihi - ilo + nw - 1) / nw));
         total = warp_for_runs(a.inc_dat, ilo, ihi, (int64_t)w * rb, (int64_t)nw * rb, rb, a.r.off, a.r.len, a.wi, a.work,
-                              a.r.part, a.r.cnt,
+                              a.r.pc,
                               [&](int32_t, int64_t we, int32_t p, int32_t pc) {
                                   if (p == ps && pc == 1) saving += we;
                                   const long long old = atomicCAS((unsigned long long *)&dense[p], ~0ull, 0ull);
@@ -1509,9 +1520,9 @@ __global__ void k_seq_gains_edge_block(const int64_t *pin_off, const int32_t *pi
                 ent_ps += st[b] == ps;
             }
             int32_t k = run_find(r, ro, lam, ps);
-            const int32_t base_ps = k >= 0 ? r.cnt[ro + k] : 0;
+            const int32_t base_ps = k >= 0 ? r.pc[2 * (ro + k) + 1] : 0;
             k = run_find(r, ro, lam, pd);
-            const int32_t base_pd = k >= 0 ? r.cnt[ro + k] : 0;
+            const int32_t base_pd = k >= 0 ? r.pc[2 * (ro + k) + 1] : 0;
             const int64_t net = seq_net(we, base_ps, base_pd, leav_pd, ent_pd, leav_ps, ent_ps);
             if (net) atomicAdd(&gacc[smv[a]], (unsigned long long)net);
         }
@@ -1584,9 +1595,9 @@ __global__ void __launch_bounds__(256) k_round_edges(int32_t E, const int32_t *e
             }
             if (lane < nm) {
                 int32_t k = run_find(r, ro, lam, ps);
-                const int32_t base_ps = k >= 0 ? r.cnt[ro + k] : 0;
+                const int32_t base_ps = k >= 0 ? r.pc[2 * (ro + k) + 1] : 0;
                 k = run_find(r, ro, lam, pd);
-                const int32_t base_pd = k >= 0 ? r.cnt[ro + k] : 0;
+                const int32_t base_pd = k >= 0 ? r.pc[2 * (ro + k) + 1] : 0;
                 const int64_t net = seq_net(wi[e], base_ps, base_pd, leav_pd, ent_pd, leav_ps, ent_ps);
                 if (net) atomicAdd(&gacc[i], (unsigned long long)net);
             }
@@ -1727,13 +1738,13 @@ __global__ void k_runs_update(const int32_t *elist, const int32_t *ecount, int32
         int32_t *op = s_oldp[warp_id()], *oc = s_oldc[warp_id()];
         if (moved)
             for (int32_t j = lane; j < old; j += 32) {
-                op[j] = r.part[lo + j];
-                oc[j] = r.cnt[lo + j];
+                op[j] = r.pc[2 * (lo + j)];
+                oc[j] = r.pc[2 * (lo + j) + 1];
                 if (r.cin[lo + j] > 0) {
                     if (local)
-                        atomicSub(&sdelta[r.part[lo + j]], 1);
+                        atomicSub(&sdelta[r.pc[2 * (lo + j)]], 1);
                     else
-                        atomicAdd((unsigned long long *)&pinbound[r.part[lo + j]], ~0ull);
+                        atomicAdd((unsigned long long *)&pinbound[r.pc[2 * (lo + j)]], ~0ull);
                 }
             }
         __syncwarp();
@@ -1749,9 +1760,9 @@ __global__ void k_runs_update(const int32_t *elist, const int32_t *ecount, int32
             for (int32_t j = lane; j < lam; j += 32)
                 if (r.cin[lo + j] > 0) {
                     if (local)
-                        atomicAdd(&sdelta[r.part[lo + j]], 1);
+                        atomicAdd(&sdelta[r.pc[2 * (lo + j)]], 1);
                     else
-                        atomicAdd((unsigned long long *)&pinbound[r.part[lo + j]], 1ull);
+                        atomicAdd((unsigned long long *)&pinbound[r.pc[2 * (lo + j)]], 1ull);
                 }
             bool same = lam == old;
             uint32_t flips[4] = {0u, 0u, 0u, 0u};
@@ -1761,8 +1772,8 @@ __global__ void k_runs_update(const int32_t *elist, const int32_t *ecount, int32
                     const int32_t j = q * 32 + lane;
                     bool f = false;
                     if (j < lam) {
-                        same &= r.part[lo + j] == op[j];
-                        f = (r.cnt[lo + j] == 1) != (oc[j] == 1);
+                        same &= r.pc[2 * (lo + j)] == op[j];
+                        f = (r.pc[2 * (lo + j) + 1] == 1) != (oc[j] == 1);
                     }
                     flips[q] = __ballot_sync(FULL_MASK, f);
                 }
@@ -1839,8 +1850,8 @@ __global__ void __launch_bounds__(1024) k_runs_update_wide(const int32_t *wide, 
         const int len = (int)(pin_off[e + 1] - plo);
         const int32_t old = r.len[e];
         for (int j = t; j < old; j += blockDim.x) {
-            op[j] = r.part[lo + j];
-            oc[j] = r.cnt[lo + j];
+            op[j] = r.pc[2 * (lo + j)];
+            oc[j] = r.pc[2 * (lo + j) + 1];
             if (moved && r.cin[lo + j] > 0) atomicAdd((unsigned long long *)&pinbound[op[j]], ~0ull);
         }
         const int np = next_pow2(len);
@@ -1861,7 +1872,7 @@ __global__ void __launch_bounds__(1024) k_runs_update_wide(const int32_t *wide, 
             }
             if (head) {
                 const int k = before + __popc(bal & ((1u << lane) - 1u));
-                r.part[lo + k] = (int32_t)sv[i];
+                r.pc[2 * (lo + k)] = (int32_t)sv[i];
                 r.cin[lo + k] = 0;
             }
             base += tot;
@@ -1870,7 +1881,7 @@ __global__ void __launch_bounds__(1024) k_runs_update_wide(const int32_t *wide, 
         const int lam = base;
         // run lengths from the sorted parts (binary searches; no in-place hazard)
         for (int k = t; k < lam; k += blockDim.x) {
-            const uint32_t p = (uint32_t)r.part[lo + k];
+            const uint32_t p = (uint32_t)r.pc[2 * (lo + k)];
             int a0 = 0, a1 = len;  // first index with sv >= p
             while (a0 < a1) {
                 const int m = (a0 + a1) >> 1;
@@ -1881,7 +1892,7 @@ __global__ void __launch_bounds__(1024) k_runs_update_wide(const int32_t *wide, 
                 const int m = (b0 + b1) >> 1;
                 if (sv[m] <= p) b0 = m + 1; else b1 = m;
             }
-            r.cnt[lo + k] = b0 - a0;
+            r.pc[2 * (lo + k) + 1] = b0 - a0;
         }
         __syncthreads();
         for (int64_t qd = dst_off[e] + t; qd < dst_off[e + 1]; qd += blockDim.x) {
@@ -1891,13 +1902,13 @@ __global__ void __launch_bounds__(1024) k_runs_update_wide(const int32_t *wide, 
         __syncthreads();
         if (moved) {
             for (int k = t; k < lam; k += blockDim.x)
-                if (r.cin[lo + k] > 0) atomicAdd((unsigned long long *)&pinbound[r.part[lo + k]], 1ull);
+                if (r.cin[lo + k] > 0) atomicAdd((unsigned long long *)&pinbound[r.pc[2 * (lo + k)]], 1ull);
             if (t == 0) s_same = lam == old;
             __syncthreads();
             if (s_same)
                 for (int k = t; k < lam; k += blockDim.x) {
-                    if (r.part[lo + k] != op[k]) s_same = 0;
-                    flip[k] = (r.cnt[lo + k] == 1) != (oc[k] == 1);
+                    if (r.pc[2 * (lo + k)] != op[k]) s_same = 0;
+                    flip[k] = (r.pc[2 * (lo + k) + 1] == 1) != (oc[k] == 1);
                 }
             __syncthreads();
             const bool same = s_same;
@@ -2032,13 +2043,12 @@ __global__ void k_split_counts(const int32_t *splist, const int32_t *spcount, co
             const bool as = na <= nb;
             const int32_t *S = dat + (as ? alo : blo), *L = dat + (as ? blo : alo);
             const int64_t ns = as ? na : nb, nl = as ? nb : na;
-            int32_t *cnt = fam ? r.cin : r.cnt;
             for (int64_t i = threadIdx.x; i < ns; i += blockDim.x) {
                 const int32_t e = S[i];
                 if (bsearch_dev(L, 0, nl, e) < 0) continue;
                 const int64_t lo = r.off[e];
                 const int32_t k = run_find(r, lo, r.len[e], P);
-                atomicAdd(&cnt[lo + k], 1);
+                atomicAdd(fam ? &r.cin[lo + k] : &r.pc[2 * (lo + k) + 1], 1);
             }
         }
     }
@@ -2054,8 +2064,7 @@ void refine_state_init(Ctx &c, RefineState &st, const DLevel &level0, int32_t K,
     st.E = level0.E;
     st.ncap = std::max<int64_t>(1, shard_capacity(c.comm, level0.N));
     st.roff = level0.pin_off;
-    st.rpart = c.alloc<int32_t>(level0.U);
-    st.rcnt = c.alloc<int32_t>(level0.U);
+    st.rpc = c.alloc<int32_t>(2 * level0.U);
     st.rcin = c.alloc<int32_t>(level0.U);
     st.rlen = c.alloc<int32_t>(level0.E);
     st.psizes = c.alloc<int64_t>(K);
@@ -2103,7 +2112,7 @@ void refine_state_init(Ctx &c, RefineState &st, const DLevel &level0, int32_t K,
 }
 
 void refine_state_release(Ctx &c, RefineState &st) {
-    for (void *p : {(void *)st.rpart, (void *)st.rcnt, (void *)st.rcin, (void *)st.rlen, (void *)st.psizes,
+    for (void *p : {(void *)st.rpc, (void *)st.rcin, (void *)st.rlen, (void *)st.psizes,
                     (void *)st.pinbound, (void *)st.pflags, (void *)st.conn, (void *)st.target, (void *)st.target2,
                     (void *)st.gain, (void *)st.gain2, (void *)st.fsens, (void *)st.fsens2, (void *)st.fpart, (void *)st.fpart2, (void *)st.ndirty,
                     (void *)st.ndirty2, (void *)st.nlist, (void *)st.splist, (void *)st.spfirst, (void *)st.ccount, (void *)st.edirty,
@@ -2131,8 +2140,7 @@ void refine_project(Ctx &c, RefineState &st, const DLevel &fine, int32_t coarse_
             DHGP_LAUNCHED(c);
             Runs r;
             r.off = st.roff;
-            r.part = st.rpart;
-            r.cnt = st.rcnt;
+            r.pc = st.rpc;
             r.cin = st.rcin;
             r.len = st.rlen;
             k_split_counts<<<2 * c.num_sms, 256, 0, c.stream>>>(st.splist, st.ctr + CT_SPLIST, fine.inc_off,
@@ -2176,8 +2184,7 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
     // ---- state (run lists at the level-0 pin offsets, part counters) -------
     Runs r;
     r.off = st.roff;
-    r.part = st.rpart;
-    r.cnt = st.rcnt;
+    r.pc = st.rpc;
     r.cin = st.rcin;
     r.len = st.rlen;
     int64_t *psizes = st.psizes, *pinbound = st.pinbound;
@@ -2665,8 +2672,7 @@ void evaluate_assign(Ctx &c, const DLevel &L, const DWeights &W, const int32_t *
                      int64_t *d_sizes, int64_t *d_inbound, double *h_conn) {
     Runs r;
     r.off = L.pin_off;
-    r.part = c.alloc<int32_t>(L.U);
-    r.cnt = c.alloc<int32_t>(L.U);
+    r.pc = c.alloc<int32_t>(2 * L.U);
     r.cin = c.alloc<int32_t>(L.U);
     r.len = c.alloc<int32_t>(L.E);
     int32_t *tmp = c.alloc<int32_t>(L.U);
@@ -2693,8 +2699,7 @@ void evaluate_assign(Ctx &c, const DLevel &L, const DWeights &W, const int32_t *
         *h_conn = (double)(int64_t)h;
     }
     c.free(conn);
-    c.free(r.part);
-    c.free(r.cnt);
+    c.free(r.pc);
     c.free(r.cin);
     c.free(r.len);
     c.free(tmp);

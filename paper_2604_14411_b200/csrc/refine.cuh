@@ -37,7 +37,7 @@ struct RefineState {
     int32_t K = 0, E = 0;
     int64_t ncap = 0;
     const int64_t *roff = nullptr;                         // [E+1] run base (level-0 pin offsets)
-    int32_t *rpart = nullptr, *rcnt = nullptr, *rcin = nullptr, *rlen = nullptr;
+    int32_t *rpc = nullptr, *rcin = nullptr, *rlen = nullptr;  // runs: (part, count) pairs [2U], count_in [U], lambda [E]
     int64_t *psizes = nullptr, *pinbound = nullptr;        // [K]
     uint8_t *pflags = nullptr;                             // [K] bit 1: part shrank
     unsigned long long *conn = nullptr;                    // connectivity of the current runs
