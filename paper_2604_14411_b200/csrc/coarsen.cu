@@ -28,16 +28,27 @@ __device__ __forceinline__ void warp_for_pins(const int32_t *inc_dat, int64_t il
                                               F &&f, unsigned long long *work = nullptr, int bsz = 32) {
     const int lane = lane_id();
     unsigned long long wb = 0;
+    // software pipelining: the next batch's offsets and the entries of the
+    // one after are loaded before this batch's pins
+    auto entry = [&](int64_t b) { return (lane < bsz && b + lane < ihi) ? inc_dat[b + lane] : -1; };
+    int32_t ne = entry(ilo + first);
+    int64_t nplo = 0, nphi = 0;
+    if (ne >= 0) {
+        nplo = pin_off[ne];
+        nphi = pin_off[ne + 1];
+    }
+    int32_t ne2 = entry(ilo + first + stride);
     for (int64_t base = ilo + first; base < ihi; base += stride) {
-        const int64_t ii = base + lane;
-        int32_t e = -1;
-        int64_t plo = 0;
-        int len = 0;
-        if (lane < bsz && ii < ihi) {
-            e = inc_dat[ii];
-            plo = pin_off[e];
-            len = (int)(pin_off[e + 1] - plo);
+        const int32_t e = ne;
+        const int64_t plo = nplo;
+        const int len = (int)(nphi - nplo);
+        ne = ne2;
+        nplo = nphi = 0;
+        if (ne >= 0) {
+            nplo = pin_off[ne];
+            nphi = pin_off[ne + 1];
         }
+        ne2 = entry(base + 2 * stride);
         const int incl = warp_incl_scan(len);
         const int total = __shfl_sync(FULL_MASK, incl, 31);
         const int excl = incl - len;

@@ -346,18 +346,35 @@ __device__ __forceinline__ int64_t warp_for_runs(const int32_t *inc_dat, int64_t
     const int lane = lane_id();
     int64_t total = 0;
     unsigned long long wb = 0;
+    // the next batch's h-edge entries are loaded before this batch's run
+    // slots (software pipelining of the incident-list -> offsets chain)
+    auto entry = [&](int64_t b) { return (lane < bsz && b + lane < ihi) ? inc_dat[b + lane] : -1; };
+    int32_t ne = entry(ilo + first);
+    int64_t nplo = 0, nwe = 0;
+    int nl = 0;
+    if (ne >= 0) {
+        nplo = pin_off[ne];
+        nl = len[ne];
+        nwe = wi[ne];
+    }
+    int32_t ne2 = entry(ilo + first + stride);
     for (int64_t base = ilo + first; base < ihi; base += stride) {
-        const int64_t ii = base + lane;
-        int32_t e = -1;
-        int64_t plo = 0, we = 0;
-        int l = 0;
-        if (lane < bsz && ii < ihi) {
-            e = inc_dat[ii];
-            plo = pin_off[e];
-            l = len[e];
-            we = wi[e];
-            total += we;
+        const int32_t e = ne;
+        const int64_t plo = nplo, we = nwe;
+        const int l = nl;
+        if (e >= 0) total += we;
+        // stage the next batch: its offsets / lengths / weights, and the
+        // entries of the one after
+        ne = ne2;
+        nplo = 0;
+        nwe = 0;
+        nl = 0;
+        if (ne >= 0) {
+            nplo = pin_off[ne];
+            nl = len[ne];
+            nwe = wi[ne];
         }
+        ne2 = entry(base + 2 * stride);
         const int incl = warp_incl_scan(l);
         const int tot = __shfl_sync(FULL_MASK, incl, 31);
         const int excl = incl - l;
@@ -575,6 +592,14 @@ __global__ void __launch_bounds__(PM_THREADS, 4) k_propose_mid(ProposeArgs a) {
         nr = warp_sum(nr);
         if (lane == 0) atomicAdd((unsigned long long *)&s_runs, (unsigned long long)nr);
         __syncthreads();
+        // a node with many more runs than the table's limit nearly always
+        // overflows it: straight to the dense tier (the tier never changes
+        // the result, only the cost)
+        if (s_runs > 2ll * a.t.pm_limit && a.K > a.t.pm_limit) {
+            if (threadIdx.x == 0) a.dense_list[atomicAdd(a.dense_count, 1)] = node;
+            __syncthreads();
+            continue;
+        }
         int lg = 6;
         while ((1ll << lg) < 2 * min((long long)a.K, s_runs) && lg < 13) lg++;
         const int cap = 1 << lg;
