@@ -592,10 +592,10 @@ __global__ void __launch_bounds__(PM_THREADS, 4) k_propose_mid(ProposeArgs a) {
         nr = warp_sum(nr);
         if (lane == 0) atomicAdd((unsigned long long *)&s_runs, (unsigned long long)nr);
         __syncthreads();
-        // a node with many more runs than the table's limit nearly always
-        // overflows it: straight to the dense tier (the tier never changes
-        // the result, only the cost)
-        if (s_runs > 2ll * a.t.pm_limit && a.K > a.t.pm_limit) {
+        // a node with more runs than the table's part limit: straight to the
+        // dense shared-memory tier, which indexes parts directly (the tier
+        // never changes the result, only the cost)
+        if (s_runs > (long long)a.t.pm_limit && a.K > a.t.pm_limit) {
             if (threadIdx.x == 0) a.dense_list[atomicAdd(a.dense_count, 1)] = node;
             __syncthreads();
             continue;
