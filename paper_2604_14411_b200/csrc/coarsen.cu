@@ -6,6 +6,8 @@
 // test_coarsen.py:183-192), so each warp accumulates hist(n, .) for one node
 // in a shared-memory hash table keyed by neighbour id, then scans it in
 // (hist desc, id desc) order with the deferred size/inbound checks.
+#include <cooperative_groups.h>
+
 #include "coarsen.cuh"
 #include "comm.cuh"
 #include "prims.cuh"
@@ -358,8 +360,15 @@ constexpr int SH_CAP = 16384;
 template <class Acc>
 constexpr int sh_smem() { return SH_CAP * (4 + (int)sizeof(Acc)); }
 
-template <class Acc>
-__global__ void __launch_bounds__(SH_THREADS) k_score_heavy(ScoreArgs a) {
+// CL = 2: a thread-block cluster (CTA pair on two SMs) per node.  Each CTA
+// hashes half of the node's h-edges into its own table; the second then
+// merges its table — distinct neighbours, far fewer than pins — into the
+// first's over distributed shared memory, and the first selects.
+// Pairs when the list fits them (a node each: the level's hubs, C2's merged
+// clusters), else single CTAs over the whole list (many hubs: every SM on its
+// own node); `pairs` = the pair launch's cluster count, the other launch exits.
+template <class Acc, int CL>
+__global__ void __launch_bounds__(SH_THREADS) k_score_heavy(ScoreArgs a, int pairs) {
     extern __shared__ unsigned long long smem_u64[];
     Acc *vals = (Acc *)smem_u64;
     int32_t *keys = (int32_t *)(vals + SH_CAP);
@@ -369,9 +378,13 @@ __global__ void __launch_bounds__(SH_THREADS) k_score_heavy(ScoreArgs a) {
     __shared__ int32_t r_k[SH_THREADS / 32], r_s[SH_THREADS / 32];
     __shared__ long long r_c[SH_THREADS / 32];
     static_assert(SH_THREADS == 1024, "the winner reduction reads one entry per lane");
+    static_assert(CL == 1 || CL == 2, "one CTA or a CTA pair per node");
     const int w = warp_id(), lane = lane_id(), nw = SH_THREADS / 32;
     const int nheavy = *a.heavy_count;
-    for (int t = blockIdx.x; t < nheavy; t += gridDim.x) {
+    if ((CL == 2) != (nheavy <= pairs)) return;
+    int rank = 0;
+    if constexpr (CL == 2) rank = (int)cooperative_groups::this_cluster().block_rank();
+    for (int t = (int)blockIdx.x / CL; t < nheavy; t += gridDim.x / CL) {
         const int32_t node = a.heavy_list[t];
         for (int s = threadIdx.x; s < SH_CAP; s += SH_THREADS) {
             keys[s] = -1;
@@ -385,8 +398,10 @@ __global__ void __launch_bounds__(SH_THREADS) k_score_heavy(ScoreArgs a) {
         const int64_t ilo = a.inc_off[node], ihi = a.inc_off[node + 1];
         int pend = 0;  // this thread's new keys not yet added to snk
         // h-edges per warp batch: a node's h-edges spread over all warps
-        const int bsz = (int)max((int64_t)1, min((int64_t)32, (ihi - ilo + nw - 1) / nw));
-        warp_for_pins<4>(a.inc_dat, ilo, ihi, (int64_t)w * bsz, (int64_t)nw * bsz, a.pin_off, a.pin_dat,
+        // (of both CTAs of a pair)
+        const int bsz = (int)max((int64_t)1, min((int64_t)32, (ihi - ilo + CL * nw - 1) / (CL * nw)));
+        warp_for_pins<4>(a.inc_dat, ilo, ihi, (int64_t)(rank * nw + w) * bsz, (int64_t)CL * nw * bsz, a.pin_off,
+                         a.pin_dat,
                       [&](int32_t e, int32_t m) {
                           if (m == node || sover) return;
                           const Acc we = (Acc)a.wi[e];
@@ -418,6 +433,47 @@ __global__ void __launch_bounds__(SH_THREADS) k_score_heavy(ScoreArgs a) {
                       },
                       a.work, bsz);
         __syncthreads();
+        if constexpr (CL == 2) {
+            cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
+            cl.sync();  // both partial tables complete
+            if (rank == 1) {
+                int32_t *keys0 = cl.map_shared_rank(keys, 0);
+                Acc *vals0 = cl.map_shared_rank(vals, 0);
+                int32_t *snk0 = cl.map_shared_rank(&snk, 0);
+                volatile int32_t *sover0 = cl.map_shared_rank(const_cast<int32_t *>(&sover), 0);
+                if (sover) {
+                    if (threadIdx.x == 0) *sover0 = 1;
+                } else {
+                    for (int s = threadIdx.x; s < SH_CAP; s += SH_THREADS) {
+                        const int32_t m = keys[s];
+                        if (m < 0 || *sover0) continue;
+                        const Acc v = vals[s];
+                        const uint32_t h = ((uint32_t)m * 2654435761u) >> (32 - 14);
+                        bool done = false;
+                        for (int probe = 0; probe < SH_CAP && !done; probe++) {
+                            const int slot = (h + probe) & (SH_CAP - 1);
+                            int k = ((volatile int32_t *)keys0)[slot];
+                            if (k == -1) {
+                                const int prev = atomicCAS(&keys0[slot], -1, m);
+                                if (prev == -1) {
+                                    if (atomicAdd(snk0, 1) + 1 > a.t.sh_limit) *sover0 = 1;
+                                    k = m;
+                                } else {
+                                    k = prev;
+                                }
+                            }
+                            if (k == m) {
+                                atomicAdd(&vals0[slot], v);
+                                done = true;
+                            }
+                        }
+                        if (!done) *sover0 = 1;
+                    }
+                }
+            }
+            cl.sync();  // the merge is complete
+            if (rank == 1) continue;
+        }
         if (sover) {
             if (threadIdx.x == 0) a.big_list[atomicAdd(a.big_count, 1)] = node;
             __syncthreads();
@@ -749,6 +805,37 @@ void score_scratch_release(Ctx &c, ScoreScratch &s) {
     s = ScoreScratch();
 }
 
+// the block tier as CTA pairs (thread-block clusters of 2), as many pairs as
+// can be co-resident
+template <class Acc>
+static void launch_heavy_pairs(Ctx &c, const ScoreArgs &a) {
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.blockDim = dim3(SH_THREADS);
+    cfg.dynamicSmemBytes = sh_smem<Acc>();
+    cfg.stream = c.stream;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    static int pairs = 0;
+    if (!pairs) {
+        cfg.gridDim = dim3(2 * (c.num_sms / 2));
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, (void *)k_score_heavy<Acc, 2>, &cfg) != cudaSuccess || n < 1)
+            n = c.num_sms / 2;
+        pairs = std::min(n, c.num_sms / 2);
+    }
+    cfg.gridDim = dim3(2 * pairs);
+    DHGP_CUDA(cudaLaunchKernelEx(&cfg, k_score_heavy<Acc, 2>, a, pairs));
+    DHGP_LAUNCHED(c);
+    // more nodes than pairs: single CTAs (exactly one of the two launches works)
+    k_score_heavy<Acc, 1><<<c.num_sms, SH_THREADS, sh_smem<Acc>(), c.stream>>>(a, pairs);
+    DHGP_LAUNCHED(c);
+}
+
 static void score_attrs(Ctx &c) {
     static bool attr = false;
     if (attr) return;
@@ -756,9 +843,13 @@ static void score_attrs(Ctx &c) {
                                    ss_smem<unsigned>()));
     DHGP_CUDA(cudaFuncSetAttribute(k_score_warp<unsigned long long>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    ss_smem<unsigned long long>()));
-    DHGP_CUDA(cudaFuncSetAttribute(k_score_heavy<unsigned>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    DHGP_CUDA(cudaFuncSetAttribute(k_score_heavy<unsigned, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    sh_smem<unsigned>()));
-    DHGP_CUDA(cudaFuncSetAttribute(k_score_heavy<unsigned long long>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    DHGP_CUDA(cudaFuncSetAttribute(k_score_heavy<unsigned long long, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   sh_smem<unsigned long long>()));
+    DHGP_CUDA(cudaFuncSetAttribute(k_score_heavy<unsigned, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   sh_smem<unsigned>()));
+    DHGP_CUDA(cudaFuncSetAttribute(k_score_heavy<unsigned long long, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    sh_smem<unsigned long long>()));
     attr = true;
 }
@@ -779,10 +870,9 @@ static void score_tiers(Ctx &c, ScoreArgs a, const DWeights &W, ScoreScratch &s,
     DHGP_LAUNCHED(c);
     // heavy tier: reads the escalation count on device, exits when zero
     if (W.wsum < (1ll << 32))
-        k_score_heavy<unsigned><<<c.num_sms, SH_THREADS, sh_smem<unsigned>(), c.stream>>>(a);
+        launch_heavy_pairs<unsigned>(c, a);
     else
-        k_score_heavy<unsigned long long><<<c.num_sms, SH_THREADS, sh_smem<unsigned long long>(), c.stream>>>(a);
-    DHGP_LAUNCHED(c);
+        launch_heavy_pairs<unsigned long long>(c, a);
     // dense tier: reads the escalation count on device, exits when zero;
     // dense rows have stride s.cap and are restored to -1 after each node
     a.N = (int32_t)s.cap;
