@@ -260,6 +260,47 @@ def test_timings_and_determinism():
     assert set(s2.phase_ms) == {"coarsen", "refine", "total"} and all(v >= 0 for v in s2.phase_ms.values())
 
 
+def test_driver_invariants_on_gpu_results():
+    """The reference driver tests' properties, checked on the GPU result itself
+    (pkg/tests/test_driver.py:60-121): valid and compacted, traces non-increasing
+    within a level, strictly shrinking levels, final connectivity = trace end,
+    observer counts, RunStats.to_dict shape."""
+    d = dp()
+    rs = np.random.RandomState(113)
+    for trial in range(12):
+        n = int(rs.randint(12, 300))
+        omega = int(rs.choice([4, 8, 16]))
+        g, c = make_instance(n, int(1.5 * n), 5, seed=1100 + trial, omega=omega, delta_slack=omega)
+        seen = {"level": 0, "round": 0}
+
+        def obs(kind, payload):
+            seen[kind] += 1
+            if kind == "level":
+                assert payload["coarse"].num_nodes < payload["fine"].num_nodes
+                assert payload["cmap"].num_coarse == payload["coarse"].num_nodes
+            else:
+                assert payload["selection"].k >= 0
+
+        part, st = d.partition(g, d.Config(c), observer=obs)
+        assert d.check_validity(g, part, c) == []
+        assert np.unique(part.assign).tolist() == list(range(part.num_parts)) and st.num_partitions == part.num_parts
+        for tr in st.connectivity_trace:
+            assert all(b <= a for a, b in zip(tr, tr[1:]))
+        sizes = [lv["nodes"] for lv in st.levels]
+        assert all(b < a for a, b in zip(sizes, sizes[1:]))
+        assert st.connectivity_trace[-1][-1] == d.connectivity(g, part)
+        # a round is observed iff it proposed moves (refine.py:289-306): every
+        # applied round was observed, and at most max_rounds per level
+        applied = sum(len(tr) - 1 for tr in st.connectivity_trace)
+        assert seen["level"] == len(st.levels) - 1 and applied <= seen["round"] <= 8 * len(st.levels)
+        assert set(st.to_dict()) == {"levels", "connectivity_trace", "phase_ms", "num_partitions"}
+    # the reference test's own instance (test_driver.py:97-111)
+    g, c = make_instance(100, 150, 5, seed=47, omega=8)
+    seen = {"level": 0, "round": 0}
+    part, st = d.partition(g, d.Config(c), observer=lambda kind, _p: seen.__setitem__(kind, seen[kind] + 1))
+    assert seen["level"] == len(st.levels) - 1 and seen["round"] >= len(st.levels)
+
+
 def test_gpu_smoke_entry():
     import __graft_entry__
 
