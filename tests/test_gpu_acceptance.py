@@ -75,3 +75,43 @@ def test_brute_force_sanity():
         assert conn >= _optimum(g, c)
         beat_or_tie += conn <= d.connectivity(g, d.one_pass(g, c))
     assert beat_or_tie >= 24
+
+
+def test_batch_size_invariance():
+    """Criterion 6 (test_acceptance.py:222-246) at the partition level: the
+    histogram batch changes no output (fill_histograms is batch-invariant)."""
+    import paper_2604_14411_b200 as d
+
+    rs = np.random.RandomState(661)
+    for i in range(20):
+        n = int(rs.randint(30, 301))
+        omega = int(rs.choice([4, 8, 16]))
+        g, c = make_instance(n, int(1.5 * n), 5, seed=30_000 + i, omega=omega, delta_slack=omega)
+        ref, rst = d.partition(g, d.Config(c, batch_size=1))
+        for b in (7, 32):
+            got, st = d.partition(g, d.Config(c, batch_size=b))
+            assert ref.assign.tobytes() == got.assign.tobytes() and rst.to_dict() == st.to_dict()
+
+
+def test_pin_scaling():
+    """Criterion 10 (test_acceptance.py:334-360): median partition time grows at
+    most 2.5x per doubling of the pins."""
+    import statistics
+    import time
+
+    import paper_2604_14411_b200 as d
+    from paper_2604_14411_b200 import workloads as W
+
+    medians = []
+    for nodes, edges in ((2000, 2500), (4000, 5000), (8000, 10000)):
+        n, w, so, sd, do, dd = W.random_dhg(nodes, edges, 6, seed=2)
+        g = d.Hypergraph._from_csr(n, w, d.CsrSets(so, sd), d.CsrSets(do, dd))
+        c = d.Constraints(16, max(int(g.node_in.lengths().max()), 24))
+        d.partition(g, d.Config(c))
+        times = []
+        for _ in range(5):
+            t0 = time.perf_counter()
+            d.partition(g, d.Config(c))
+            times.append(time.perf_counter() - t0)
+        medians.append(statistics.median(times))
+    assert medians[1] / medians[0] <= 2.5 and medians[2] / medians[1] <= 2.5, medians
