@@ -38,6 +38,7 @@ __device__ __forceinline__ bool bit_set(uint32_t *b, int32_t e) {
 __global__ void k_one_pass(int32_t N, const int32_t *size, const int64_t *in_off, const int32_t *in_dat,
                            int64_t omega, int64_t delta, uint32_t *bits, int32_t *list, int32_t *assign,
                            int32_t *num_parts) {
+    pdl_entry();
     const int lane = lane_id();
     const uint32_t lt = (1u << lane) - 1u;
     int32_t cur = -1;
@@ -98,6 +99,7 @@ __global__ void __launch_bounds__(OG_T) k_overlap_greedy(int32_t N, const int32_
                                                          const int32_t *inc_dat, const int64_t *pin_off,
                                                          const int32_t *pin_dat, int64_t omega, int64_t delta,
                                                          OgState s, int32_t *assign, int32_t *num_parts) {
+    pdl_entry();
     __shared__ int64_t s_in_cnt;
     __shared__ int32_t s_ninc, s_nin, s_nfront;
     __shared__ long long r_key[OG_T / 32];
@@ -259,7 +261,7 @@ int dhgp_baseline(const dhgp_graph *g, int64_t max_size, int64_t max_inbound, in
             uint32_t *bits = c.alloc<uint32_t>(words);
             int32_t *list = c.alloc<int32_t>(E);
             c.zero(bits, words);
-            k_one_pass<<<1, 32, 0, c.stream>>>(N, L.size, L.in_off, L.in_dat, max_size, max_inbound, bits, list,
+            pdl_launch(k_one_pass, 1, 32, 0, c.stream, N, L.size, L.in_off, L.in_dat, max_size, max_inbound, bits, list,
                                                assign, np);
             DHGP_LAUNCHED(c);
             c.free(bits);
@@ -278,7 +280,7 @@ int dhgp_baseline(const dhgp_graph *g, int64_t max_size, int64_t max_inbound, in
             c.zero(s.ov, N);
             c.zero(s.excl, N);
             fill_i32(c, assign, -1, N);
-            k_overlap_greedy<<<1, OG_T, 0, c.stream>>>(N, L.size, L.in_off, L.in_dat, L.inc_off, L.inc_dat, L.pin_off,
+            pdl_launch(k_overlap_greedy, 1, OG_T, 0, c.stream, N, L.size, L.in_off, L.in_dat, L.inc_off, L.inc_dat, L.pin_off,
                                                      L.pin_dat, max_size, max_inbound, s, assign, np);
             DHGP_LAUNCHED(c);
             for (void *p : {(void *)s.inc_bits, (void *)s.in_bits, (void *)s.inc_list, (void *)s.in_list,

@@ -237,6 +237,7 @@ __device__ __forceinline__ bool warp_union_ok(const ScoreArgs &a, int32_t n, int
 
 template <class Acc>
 __global__ void __launch_bounds__(SS_WARPS * 32, 3) k_score_warp(ScoreArgs a) {
+    pdl_entry();
     extern __shared__ unsigned long long smem_u64[];
     Acc *svals = (Acc *)smem_u64;
     int32_t *skeys = (int32_t *)(svals + SS_WARPS * SS_CAP);
@@ -369,6 +370,7 @@ constexpr int sh_smem() { return SH_CAP * (4 + (int)sizeof(Acc)); }
 // own node); `pairs` = the pair launch's cluster count, the other launch exits.
 template <class Acc, int CL>
 __global__ void __launch_bounds__(SH_THREADS) k_score_heavy(ScoreArgs a, int pairs) {
+    pdl_entry();
     extern __shared__ unsigned long long smem_u64[];
     Acc *vals = (Acc *)smem_u64;
     int32_t *keys = (int32_t *)(vals + SH_CAP);
@@ -577,6 +579,7 @@ __global__ void __launch_bounds__(SH_THREADS) k_score_heavy(ScoreArgs a, int pai
 constexpr int SB_THREADS = 512;
 __global__ void __launch_bounds__(SB_THREADS) k_score_block(ScoreArgs a, long long *dense_all, int32_t *touched_all,
                                                              long long *cval_all, int32_t n_real) {
+    pdl_entry();
     (void)n_real;
     __shared__ int32_t s_nt;
     __shared__ long long s_bv[SB_THREADS / 32];
@@ -703,6 +706,7 @@ __global__ void __launch_bounds__(SB_THREADS) k_score_block(ScoreArgs a, long lo
 __global__ void k_inc_base(int32_t N, const int32_t *ma, const int32_t *mb, const int32_t *gamma_prev,
                            const int32_t *prev_pair, const double *prev_score, uint8_t *kind, int64_t *thr_s,
                            int32_t *thr_p, unsigned long long *best, int32_t *list, int32_t *list_count) {
+    pdl_entry();
     const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= N) return;
     best[c] = 0ull;
@@ -729,6 +733,7 @@ __device__ __forceinline__ unsigned long long tuple_key(long long h, int32_t b) 
     return ((unsigned long long)(h + 1) << 32) | (unsigned long long)(uint32_t)b;
 }
 __global__ void k_inc_tuples_quick(ScoreArgs a, unsigned long long *best, int32_t *hard, int32_t *hard_count) {
+    pdl_entry();
     const int64_t nt = min((int64_t)*a.tup_count, a.tup_cap);
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nt; i += (int64_t)gridDim.x * blockDim.x) {
         const int32_t v = a.tup_v[i], b = a.tup_b[i];
@@ -739,6 +744,7 @@ __global__ void k_inc_tuples_quick(ScoreArgs a, unsigned long long *best, int32_
     }
 }
 __global__ void k_inc_tuples(ScoreArgs a, unsigned long long *best, const int32_t *hard, const int32_t *hard_count) {
+    pdl_entry();
     const int64_t nt = *hard_count;
     const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
     for (int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id(); t < nt; t += nw) {
@@ -750,6 +756,7 @@ __global__ void k_inc_tuples(ScoreArgs a, unsigned long long *best, const int32_
 __global__ void k_inc_finalize(int32_t N, const uint8_t *kind, const int64_t *thr_s, const int32_t *thr_p,
                                const unsigned long long *best, const int32_t *gamma_prev, const int32_t *tup_count,
                                int64_t tup_cap, int32_t *pair, double *score, int32_t *list, int32_t *list_count) {
+    pdl_entry();
     const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= N) return;
     const int k = kind[c];
@@ -774,6 +781,7 @@ __global__ void k_inc_finalize(int32_t N, const uint8_t *kind, const int64_t *th
 }
 
 __global__ void k_fill_ll(long long *p, long long v, int64_t n) {
+    pdl_entry();
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) p[i] = v;
 }
@@ -790,7 +798,7 @@ void score_scratch_init(Ctx &c, ScoreScratch &s, int64_t n_cap) {
     s.big = c.alloc<int32_t>(s.cap);
     s.heavy = c.alloc<int32_t>(s.cap);
     s.ctr = c.alloc<int32_t>(3);
-    k_fill_ll<<<(unsigned)cdiv((int64_t)s.blocks * s.cap, 256), 256, 0, c.stream>>>(s.dense, -1ll,
+    pdl_launch(k_fill_ll, (unsigned)cdiv((int64_t)s.blocks * s.cap, 256), 256, 0, c.stream, s.dense, -1ll,
                                                                                    (int64_t)s.blocks * s.cap);
     DHGP_LAUNCHED(c);
 }
@@ -832,7 +840,7 @@ static void launch_heavy_pairs(Ctx &c, const ScoreArgs &a) {
     DHGP_CUDA(cudaLaunchKernelEx(&cfg, k_score_heavy<Acc, 2>, a, pairs));
     DHGP_LAUNCHED(c);
     // more nodes than pairs: single CTAs (exactly one of the two launches works)
-    k_score_heavy<Acc, 1><<<c.num_sms, SH_THREADS, sh_smem<Acc>(), c.stream>>>(a, pairs);
+    pdl_launch(k_score_heavy<Acc, 1>, c.num_sms, SH_THREADS, sh_smem<Acc>(), c.stream, a, pairs);
     DHGP_LAUNCHED(c);
 }
 
@@ -861,11 +869,11 @@ static void score_tiers(Ctx &c, ScoreArgs a, const DWeights &W, ScoreScratch &s,
     if (W.wsum < (1ll << 32)) {
         static int g32 = resident_grid(c, k_score_warp<unsigned>, SS_WARPS * 32, ss_smem<unsigned>());
         int blocks = (int)std::min<int64_t>(cdiv(nmine, SS_WARPS), g32);
-        k_score_warp<unsigned><<<blocks, SS_WARPS * 32, ss_smem<unsigned>(), c.stream>>>(a);
+        pdl_launch(k_score_warp<unsigned>, blocks, SS_WARPS * 32, ss_smem<unsigned>(), c.stream, a);
     } else {
         static int g64 = resident_grid(c, k_score_warp<unsigned long long>, SS_WARPS * 32, ss_smem<unsigned long long>());
         int blocks = (int)std::min<int64_t>(cdiv(nmine, SS_WARPS), g64);
-        k_score_warp<unsigned long long><<<blocks, SS_WARPS * 32, ss_smem<unsigned long long>(), c.stream>>>(a);
+        pdl_launch(k_score_warp<unsigned long long>, blocks, SS_WARPS * 32, ss_smem<unsigned long long>(), c.stream, a);
     }
     DHGP_LAUNCHED(c);
     // heavy tier: reads the escalation count on device, exits when zero
@@ -876,7 +884,7 @@ static void score_tiers(Ctx &c, ScoreArgs a, const DWeights &W, ScoreScratch &s,
     // dense tier: reads the escalation count on device, exits when zero;
     // dense rows have stride s.cap and are restored to -1 after each node
     a.N = (int32_t)s.cap;
-    k_score_block<<<s.blocks, SB_THREADS, 0, c.stream>>>(a, s.dense, s.touched, s.cval, n_real);
+    pdl_launch(k_score_block, s.blocks, SB_THREADS, 0, c.stream, a, s.dense, s.touched, s.cval, n_real);
     DHGP_LAUNCHED(c);
 }
 
@@ -930,7 +938,7 @@ void score_select_inc(Ctx &c, const DLevel &L, const DWeights &W, int64_t omega,
     int32_t *tv = c.alloc<int32_t>(cap), *tb = c.alloc<int32_t>(cap), *hard = c.alloc<int32_t>(cap);
     int64_t *th = c.alloc<int64_t>(cap);
     c.zero(lc, 4);
-    k_inc_base<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(N, cy.ma, cy.mb, cy.gamma_prev, cy.prev_pair,
+    pdl_launch(k_inc_base, (unsigned)cdiv(N, 256), 256, 0, c.stream, N, cy.ma, cy.mb, cy.gamma_prev, cy.prev_pair,
                                                             cy.prev_score, kind, thr_s, thr_p, best, list, lc);
     DHGP_LAUNCHED(c);
     // pass 1: the merged clusters, emitting their beating neighbour tuples
@@ -962,12 +970,12 @@ void score_select_inc(Ctx &c, const DLevel &L, const DWeights &W, int64_t omega,
     }
     score_tiers(c, a, W, s, N);
     static int gq = resident_grid(c, k_inc_tuples_quick, 256, 0);
-    k_inc_tuples_quick<<<gq, 256, 0, c.stream>>>(a, best, hard, lc + 3);
+    pdl_launch(k_inc_tuples_quick, gq, 256, 0, c.stream, a, best, hard, lc + 3);
     DHGP_LAUNCHED(c);
     static int gt = resident_grid(c, k_inc_tuples, 256, 0);
-    k_inc_tuples<<<gt, 256, 0, c.stream>>>(a, best, hard, lc + 3);
+    pdl_launch(k_inc_tuples, gt, 256, 0, c.stream, a, best, hard, lc + 3);
     DHGP_LAUNCHED(c);
-    k_inc_finalize<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(N, kind, thr_s, thr_p, best, cy.gamma_prev, lc + 2,
+    pdl_launch(k_inc_finalize, (unsigned)cdiv(N, 256), 256, 0, c.stream, N, kind, thr_s, thr_p, best, cy.gamma_prev, lc + 2,
                                                                 cap, pair, score, list2, lc + 1);
     DHGP_LAUNCHED(c);
     // pass 2: singletons whose carried pair merged and no cluster outranks it
@@ -1023,6 +1031,7 @@ __device__ __forceinline__ bool claimant(const int32_t *pair, int32_t v) {
 
 __global__ void k_match_claim1(int32_t N, const int32_t *pair, const double *score, unsigned long long *best,
                                int64_t *status) {
+    pdl_entry();
     int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= N) return;
     int32_t p = pair[v];
@@ -1038,6 +1047,7 @@ __global__ void k_match_claim1(int32_t N, const int32_t *pair, const double *sco
 
 __global__ void k_match_claim2(int32_t N, const int32_t *pair, const double *score, const unsigned long long *best,
                                int32_t *claim) {
+    pdl_entry();
     int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= N) return;
     if (!claimant(pair, (int32_t)v)) return;
@@ -1053,6 +1063,7 @@ constexpr int kWalkLimit = 64;
 
 __global__ void k_match_final(int32_t N, const int32_t *pair, const int32_t *claim, const int32_t *runlen,
                               int32_t *match, uint8_t *isrep, int64_t *status) {
+    pdl_entry();
     __shared__ int64_t sh[33];
     int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int64_t moved = 0;
@@ -1087,6 +1098,7 @@ __global__ void k_match_final(int32_t N, const int32_t *pair, const int32_t *cla
 }
 
 __global__ void k_pj_init(int32_t N, const int32_t *pair, const int32_t *claim, int32_t *r, int32_t *nxt) {
+    pdl_entry();
     int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= N) return;
     bool wv = won(pair, claim, (int32_t)v);
@@ -1094,6 +1106,7 @@ __global__ void k_pj_init(int32_t N, const int32_t *pair, const int32_t *claim, 
     nxt[v] = wv ? pair[v] : -1;
 }
 __global__ void k_pj_step(int32_t N, const int32_t *r0, const int32_t *n0, int32_t *r1, int32_t *n1) {
+    pdl_entry();
     int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= N) return;
     int32_t nx = n0[v];
@@ -1103,6 +1116,7 @@ __global__ void k_pj_step(int32_t N, const int32_t *r0, const int32_t *n0, int32
 
 // exact sequential cycle check, the reference's DFS (_kernels.pyx:124-155)
 __global__ void k_cycle_check(int32_t N, const int32_t *pair, int8_t *state, int32_t *path, int32_t *out_len) {
+    pdl_entry();
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     *out_len = 0;
     for (int32_t s = 0; s < N; s++) {
@@ -1135,11 +1149,11 @@ void launch_matching(Ctx &c, int32_t N, const int32_t *pair, const double *score
     c.zero(best, N);
     fill_i32(c, claim, -1, N);
     const unsigned g = (unsigned)cdiv(N, 256);
-    k_match_claim1<<<g, 256, 0, c.stream>>>(N, pair, score, best, d_status);
+    pdl_launch(k_match_claim1, g, 256, 0, c.stream, N, pair, score, best, d_status);
     DHGP_LAUNCHED(c);
-    k_match_claim2<<<g, 256, 0, c.stream>>>(N, pair, score, best, claim);
+    pdl_launch(k_match_claim2, g, 256, 0, c.stream, N, pair, score, best, claim);
     DHGP_LAUNCHED(c);
-    k_match_final<<<g, 256, 0, c.stream>>>(N, pair, claim, nullptr, match, isrep, d_status);
+    pdl_launch(k_match_final, g, 256, 0, c.stream, N, pair, claim, nullptr, match, isrep, d_status);
     DHGP_LAUNCHED(c);
     c.free(best);
 }
@@ -1153,7 +1167,7 @@ bool matching_fallbacks(Ctx &c, int32_t N, const int32_t *pair, const double *sc
         int32_t *path = c.alloc<int32_t>(N);
         int32_t *clen = c.alloc<int32_t>(1);
         c.zero(state, N);
-        k_cycle_check<<<1, 1, 0, c.stream>>>(N, pair, state, path, clen);
+        pdl_launch(k_cycle_check, 1, 1, 0, c.stream, N, pair, state, path, clen);
         DHGP_LAUNCHED(c);
         int32_t hl = 0;
         c.d2h(&hl, clen, 1);
@@ -1169,15 +1183,15 @@ bool matching_fallbacks(Ctx &c, int32_t N, const int32_t *pair, const double *sc
         int32_t *r1 = c.alloc<int32_t>(N), *n1 = c.alloc<int32_t>(N);
         int64_t *status = c.alloc<int64_t>(kStatusWords);
         c.zero(status, kStatusWords);
-        k_pj_init<<<g, 256, 0, c.stream>>>(N, pair, claim, r0, n0);
+        pdl_launch(k_pj_init, g, 256, 0, c.stream, N, pair, claim, r0, n0);
         DHGP_LAUNCHED(c);
         for (int it = 0; it <= bitlen((uint64_t)N); it++) {
-            k_pj_step<<<g, 256, 0, c.stream>>>(N, r0, n0, r1, n1);
+            pdl_launch(k_pj_step, g, 256, 0, c.stream, N, r0, n0, r1, n1);
             DHGP_LAUNCHED(c);
             std::swap(r0, r1);
             std::swap(n0, n1);
         }
-        k_match_final<<<g, 256, 0, c.stream>>>(N, pair, claim, r0, match, isrep, status);
+        pdl_launch(k_match_final, g, 256, 0, c.stream, N, pair, claim, r0, match, isrep, status);
         DHGP_LAUNCHED(c);
         c.d2h(&st.moved, status, 1);
         c.sync();
@@ -1213,6 +1227,7 @@ int64_t resolve_matching(Ctx &c, int32_t N, const int32_t *pair, const double *s
 namespace {
 __global__ void k_gamma(int32_t N, const int32_t *match, const int64_t *rank, const int32_t *size, int32_t *gamma,
                         int32_t *ma, int32_t *mb, int32_t *csize, int32_t *mlist, int32_t *mcount) {
+    pdl_entry();
     int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= N) return;
     int32_t m = match[v];
@@ -1230,6 +1245,7 @@ __global__ void k_gamma(int32_t N, const int32_t *match, const int64_t *rank, co
 // gathers the coarse totals into the status words
 __global__ void k_contract_status(int32_t N, int32_t E, const int64_t *rank, const int64_t *so, const int64_t *dof,
                                   const int64_t *po, const int64_t *io, const int64_t *co, int64_t *status) {
+    pdl_entry();
     if (threadIdx.x || blockIdx.x) return;
     const int64_t nc = rank[N];
     status[3] = nc;
@@ -1278,6 +1294,7 @@ __device__ __forceinline__ int64_t blk_excl_flags(bool f, int64_t *sh_w, int64_t
 // thread per coarse node: a singleton's count is its member's length; zero
 // past nc (the offsets scan runs over the fine count)
 __global__ void k_node_count(int64_t nc_cap, const int64_t *d_nc, const int32_t *ma, const int32_t *mb, NodeFams fs) {
+    pdl_entry();
     const NodeFam &f = fs.f[blockIdx.y];
     const int64_t nc = *d_nc;
     for (int64_t cn = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; cn < nc_cap;
@@ -1308,6 +1325,7 @@ template <bool WRITE>
 __global__ void __launch_bounds__(UN_THREADS) k_node_union(const int32_t *ma, const int32_t *mb, const int32_t *mlist,
                                                            const int32_t *mcount, NodeFams fs, uint8_t *emark,
                                                            int words) {
+    pdl_entry();
     extern __shared__ uint32_t s_bm[];
     __shared__ int32_t s_val[kUnionStage], s_pre[kUnionStage + 1];
     __shared__ int64_t sh[32];
@@ -1457,6 +1475,7 @@ __global__ void __launch_bounds__(UN_THREADS) k_node_union(const int32_t *ma, co
 // is found by a search over the chunk's prefix).  Merged clusters are skipped.
 __global__ void __launch_bounds__(256) k_node_write(int64_t nc, int split, const int32_t *ma, const int32_t *mb,
                                                     NodeFams fs) {
+    pdl_entry();
     const NodeFam &f = fs.f[blockIdx.y];
     __shared__ int64_t s_src[kNodeChunk], s_dst[kNodeChunk], s_end[kNodeChunk];
     const int64_t nch = (nc + kNodeChunk - 1) / kNodeChunk;
@@ -1588,6 +1607,7 @@ __device__ __forceinline__ int warp_gamma_short(uint32_t g, int len, int32_t *ou
 }
 __global__ void __launch_bounds__(256) k_contract_edges(int32_t E, const int32_t *gamma, EdgeFam f0, EdgeFam f1,
                                                         EdgeFam f2, bool write, const uint8_t *emark) {
+    pdl_entry();
     const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
     const int lane = lane_id();
     for (int64_t e = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id(); e < E; e += nw) {
@@ -1714,6 +1734,7 @@ __device__ __forceinline__ void flat_family(const EdgeFam &f, int64_t e0, int nb
 __global__ void __launch_bounds__(256) k_contract_flat(int32_t E, const int32_t *gamma, EdgeFam f0, EdgeFam f1,
                                                        EdgeFam f2, bool write, uint8_t *slow,
                                                        const uint8_t *emark) {
+    pdl_entry();
     __shared__ int32_t s_run[8][32];
     __shared__ uint8_t s_bad[8][32];
     const int w = warp_id();
@@ -1760,7 +1781,7 @@ void contract_count(Ctx &c, DLevel &fine, const int32_t *match, const uint8_t *i
     s.mcount = c.alloc<int32_t>(1);
     s.emark = c.alloc<uint8_t>(E);
     zero_many(c, {{s.mcount, 4}, {s.emark, E}});
-    k_gamma<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(N, match, s.rank, fine.size, fine.gamma, s.ma, s.mb,
+    pdl_launch(k_gamma, (unsigned)cdiv(N, 256), 256, 0, c.stream, N, match, s.rank, fine.size, fine.gamma, s.ma, s.mb,
                                                          coarse.size, s.mlist, s.mcount);
     DHGP_LAUNCHED(c);
     // per-node families first: the merged clusters flag the h-edges whose
@@ -1773,10 +1794,10 @@ void contract_count(Ctx &c, DLevel &fine, const int32_t *match, const uint8_t *i
         const NodeFams fs{{NodeFam{fine.in_off, fine.in_dat, ncnt, nullptr, nullptr},
                            NodeFam{fine.inc_off, fine.inc_dat, ncnt + N, nullptr, nullptr}}};
         const unsigned ga = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(N, 256), (int64_t)c.num_sms * 8));
-        k_node_count<<<dim3(ga, 2), 256, 0, c.stream>>>(N, d_nc, s.ma, s.mb, fs);
+        pdl_launch(k_node_count, dim3(ga, 2), 256, 0, c.stream, N, d_nc, s.ma, s.mb, fs);
         DHGP_LAUNCHED(c);
         const int words = union_words(c, E);
-        k_node_union<false><<<dim3(c.num_sms, 2), UN_THREADS, 4 * words, c.stream>>>(s.ma, s.mb, s.mlist, s.mcount, fs,
+        pdl_launch(k_node_union<false>, dim3(c.num_sms, 2), UN_THREADS, 4 * words, c.stream, s.ma, s.mb, s.mlist, s.mcount, fs,
                                                                                      s.emark, words);
         DHGP_LAUNCHED(c);
     }
@@ -1800,11 +1821,11 @@ void contract_count(Ctx &c, DLevel &fine, const int32_t *match, const uint8_t *i
             if (s.flat) {
                 static int g = resident_grid(c, k_contract_flat, 256, 0);
                 const unsigned gr = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(E, 256), g));
-                k_contract_flat<<<gr, 256, 0, c.stream>>>(E, fine.gamma, f0, f1, f2, false, s.slow, s.emark);
+                pdl_launch(k_contract_flat, gr, 256, 0, c.stream, E, fine.gamma, f0, f1, f2, false, s.slow, s.emark);
             } else {
                 static int g = resident_grid(c, k_contract_edges, 256, 0);
                 const unsigned gr = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(E, 8), g));
-                k_contract_edges<<<gr, 256, 0, c.stream>>>(E, fine.gamma, f0, f1, f2, false, s.emark);
+                pdl_launch(k_contract_edges, gr, 256, 0, c.stream, E, fine.gamma, f0, f1, f2, false, s.emark);
             }
             DHGP_LAUNCHED(c);
         }
@@ -1834,7 +1855,7 @@ void contract_count(Ctx &c, DLevel &fine, const int32_t *match, const uint8_t *i
     c.free(cnt);
     }
     kcs.close();
-    k_contract_status<<<1, 32, 0, c.stream>>>(N, E, s.rank, coarse.src_off, coarse.dst_off, coarse.pin_off,
+    pdl_launch(k_contract_status, 1, 32, 0, c.stream, N, E, s.rank, coarse.src_off, coarse.dst_off, coarse.pin_off,
                                               coarse.in_off, coarse.inc_off, d_status);
     DHGP_LAUNCHED(c);
 }
@@ -1870,11 +1891,11 @@ void contract_write(Ctx &c, DLevel &fine, DLevel &coarse, ContractScratch &s, co
                 if (s.flat) {
                     static int g = resident_grid(c, k_contract_flat, 256, 0);
                     const unsigned gr = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(E, 256), g));
-                    k_contract_flat<<<gr, 256, 0, c.stream>>>(E, fine.gamma, f0, f1, f2, true, s.slow, nullptr);
+                    pdl_launch(k_contract_flat, gr, 256, 0, c.stream, E, fine.gamma, f0, f1, f2, true, s.slow, nullptr);
                 } else {
                     static int g = resident_grid(c, k_contract_edges, 256, 0);
                     const unsigned gr = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(E, 8), g));
-                    k_contract_edges<<<gr, 256, 0, c.stream>>>(E, fine.gamma, f0, f1, f2, true, nullptr);
+                    pdl_launch(k_contract_edges, gr, 256, 0, c.stream, E, fine.gamma, f0, f1, f2, true, nullptr);
                 }
                 DHGP_LAUNCHED(c);
             }
@@ -1894,10 +1915,10 @@ void contract_write(Ctx &c, DLevel &fine, DLevel &coarse, ContractScratch &s, co
             const int split = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(per_chunk, 4096), 64));
             const int64_t items = cdiv(st.nc, kNodeChunk) * split;
             const unsigned g = (unsigned)std::min<int64_t>(items, (int64_t)c.num_sms * 16);
-            k_node_write<<<dim3(g, 2), 256, 0, c.stream>>>(st.nc, split, s.ma, s.mb, fs);
+            pdl_launch(k_node_write, dim3(g, 2), 256, 0, c.stream, st.nc, split, s.ma, s.mb, fs);
             DHGP_LAUNCHED(c);
             const int words = union_words(c, E);
-            k_node_union<true><<<dim3(c.num_sms, 2), UN_THREADS, 4 * words, c.stream>>>(s.ma, s.mb, s.mlist, s.mcount,
+            pdl_launch(k_node_union<true>, dim3(c.num_sms, 2), UN_THREADS, 4 * words, c.stream, s.ma, s.mb, s.mlist, s.mcount,
                                                                                         fs, nullptr, words);
             DHGP_LAUNCHED(c);
         }
@@ -1911,6 +1932,7 @@ void contract_write(Ctx &c, DLevel &fine, DLevel &coarse, ContractScratch &s, co
 
 namespace {
 __global__ void k_members(int32_t N, const int32_t *gamma, int32_t *lo, int32_t *hi) {
+    pdl_entry();
     int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= N) return;
     atomicMin(&lo[gamma[v]], (int32_t)v);
@@ -1918,6 +1940,7 @@ __global__ void k_members(int32_t N, const int32_t *gamma, int32_t *lo, int32_t 
 }
 __global__ void k_match_of(int32_t N, const int32_t *gamma, const int32_t *lo, const int32_t *hi, int32_t *match,
                            uint8_t *isrep) {
+    pdl_entry();
     int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= N) return;
     const int32_t a = lo[gamma[v]], b = hi[gamma[v]];
@@ -1931,9 +1954,9 @@ void match_from_gamma(Ctx &c, int32_t N, int32_t nc, const int32_t *gamma, int32
     int32_t *lo = c.alloc<int32_t>(nc), *hi = c.alloc<int32_t>(nc);
     fill_i32(c, lo, 0x7fffffff, nc);
     fill_i32(c, hi, -1, nc);
-    k_members<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(N, gamma, lo, hi);
+    pdl_launch(k_members, (unsigned)cdiv(N, 256), 256, 0, c.stream, N, gamma, lo, hi);
     DHGP_LAUNCHED(c);
-    k_match_of<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(N, gamma, lo, hi, match, isrep);
+    pdl_launch(k_match_of, (unsigned)cdiv(N, 256), 256, 0, c.stream, N, gamma, lo, hi, match, isrep);
     DHGP_LAUNCHED(c);
     c.free(lo);
     c.free(hi);

@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/dhgp.h"
@@ -42,6 +43,34 @@ const char *last_error();
                                                    " (" + __FILE__ + ":" + std::to_string(__LINE__) + ")"}; \
         (ctx).launches++;                                                                            \
     } while (0)
+
+// ---------------------------------------------------------------------------
+// Programmatic dependent launch.  Every kernel is launched with programmatic
+// stream serialization, so the next kernel's CTAs are scheduled while this one
+// drains (hiding the ~2-3 us launch gap of the short dependent kernels that
+// make up a level / round).  Each kernel's first statement is pdl_entry():
+// griddepcontrol.wait blocks until the previous grid has completed and its
+// writes are visible, so stream order is unchanged for every memory access.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void pdl_entry() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+template <typename... P, typename... A>
+inline void pdl_launch(void (*kernel)(P...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream, A &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    DHGP_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<A>(args)...));
+}
 
 // ---------------------------------------------------------------------------
 // execution context: one stream per call, stream-ordered pool allocations

@@ -221,10 +221,12 @@ void seams_setup(Ctx &c, int device) { setup(c, device); }
 
 namespace {
 __global__ void k_used(int32_t N, const int32_t *assign, uint8_t *used) {
+    pdl_entry();
     int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (v < N) used[assign[v]] = 1;
 }
 __global__ void k_remap(int32_t N, const int64_t *rank, int32_t *assign) {
+    pdl_entry();
     int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (v < N) assign[v] = (int32_t)rank[assign[v]];
 }
@@ -561,10 +563,10 @@ static void run_partition(Ctx &c, const DInput &in, const dhgp_config &cfg, Part
             uint8_t *used = c.alloc<uint8_t>(K);
             int64_t *rank = c.alloc<int64_t>((int64_t)K + 1);
             c.zero(used, K);
-            k_used<<<(unsigned)cdiv(N0, 256), 256, 0, c.stream>>>(N0, assign, used);
+            pdl_launch(k_used, (unsigned)cdiv(N0, 256), 256, 0, c.stream, N0, assign, used);
             DHGP_LAUNCHED(c);
             scan_excl<uint8_t>(c, used, rank, K);
-            k_remap<<<(unsigned)cdiv(N0, 256), 256, 0, c.stream>>>(N0, rank, assign);
+            pdl_launch(k_remap, (unsigned)cdiv(N0, 256), 256, 0, c.stream, N0, rank, assign);
             DHGP_LAUNCHED(c);
             int64_t fp = 0;
             c.d2h(&fp, rank + K, 1);

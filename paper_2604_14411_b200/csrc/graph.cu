@@ -10,6 +10,7 @@ namespace {
 // weights: finite, >= 0; exact-integer mode needs integral values with a
 // total < 2^53 so every partial sum in any order is exact.
 __global__ void k_check_weights(const double *w, int64_t E, int64_t *wi, unsigned long long *sum, int32_t *flags) {
+    pdl_entry();
     __shared__ int64_t sh[33];
     int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int64_t v = 0;
@@ -25,17 +26,20 @@ __global__ void k_check_weights(const double *w, int64_t E, int64_t *wi, unsigne
 }
 
 __global__ void k_rebase(int64_t *off, int64_t n, int64_t base) {
+    pdl_entry();
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) off[i] -= base;
 }
 
 __global__ void k_max_edge(int64_t E, const int64_t *so, const int64_t *dof, int32_t *mx) {
+    pdl_entry();
     int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e < E) atomicMax(mx, (int32_t)(so[e + 1] - so[e] + dof[e + 1] - dof[e]));
 }
 
 __global__ void k_comb(int64_t E, const int64_t *so, const int32_t *sd, const int64_t *dof, const int32_t *dd,
                        int64_t *co, int32_t *cd) {
+    pdl_entry();
     int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e > E) return;
     co[e] = so[e] + dof[e];
@@ -47,6 +51,7 @@ __global__ void k_comb(int64_t E, const int64_t *so, const int32_t *sd, const in
 
 __global__ void k_feasible(int32_t N, const int32_t *size, const int64_t *in_off, int64_t omega, int64_t delta,
                            int32_t *bad) {
+    pdl_entry();
     int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (n >= N) return;
     if ((int64_t)size[n] > omega) atomicMin(&bad[0], (int32_t)n);
@@ -72,11 +77,11 @@ void upload_input(Ctx &c, const dhgp_graph &g, DInput &in) {
     c.h2d(in.dst_dat, g.dst_dat + db, in.Pd);
     c.h2d(in.w, g.edge_weight, E);
     if (sb) {
-        k_rebase<<<(unsigned)cdiv(E + 1, 256), 256, 0, c.stream>>>(in.src_off, E + 1, sb);
+        pdl_launch(k_rebase, (unsigned)cdiv(E + 1, 256), 256, 0, c.stream, in.src_off, E + 1, sb);
         DHGP_LAUNCHED(c);
     }
     if (db) {
-        k_rebase<<<(unsigned)cdiv(E + 1, 256), 256, 0, c.stream>>>(in.dst_off, E + 1, db);
+        pdl_launch(k_rebase, (unsigned)cdiv(E + 1, 256), 256, 0, c.stream, in.dst_off, E + 1, db);
         DHGP_LAUNCHED(c);
     }
     in.size = c.alloc<int32_t>(in.N);
@@ -88,7 +93,7 @@ void upload_input(Ctx &c, const dhgp_graph &g, DInput &in) {
     int32_t *mx = c.alloc<int32_t>(1);
     c.zero(mx, 1);
     if (E > 0) {
-        k_max_edge<<<(unsigned)cdiv(E, 256), 256, 0, c.stream>>>(E, in.src_off, in.dst_off, mx);
+        pdl_launch(k_max_edge, (unsigned)cdiv(E, 256), 256, 0, c.stream, E, in.src_off, in.dst_off, mx);
         DHGP_LAUNCHED(c);
     }
     c.d2h(&in.max_edge_pins, mx, 1);
@@ -105,7 +110,7 @@ void prepare_weights(Ctx &c, const DInput &in, DWeights &W) {
     c.zero(sum, 1);
     c.zero(flags, 1);
     if (W.E > 0) {
-        k_check_weights<<<(unsigned)cdiv(W.E, 256), 256, 0, c.stream>>>(W.w, W.E, W.wi, sum, flags);
+        pdl_launch(k_check_weights, (unsigned)cdiv(W.E, 256), 256, 0, c.stream, W.w, W.E, W.wi, sum, flags);
         DHGP_LAUNCHED(c);
     }
     unsigned long long hs = 0;
@@ -143,7 +148,7 @@ void derive_incidence(Ctx &c, DLevel &L) {
     int64_t *co = c.alloc<int64_t>(E + 1);
     int32_t *cd = c.alloc<int32_t>(cap);
     int32_t *tmp = c.alloc<int32_t>(cap);
-    k_comb<<<(unsigned)cdiv(E + 1, 256), 256, 0, c.stream>>>(E, L.src_off, L.src_dat, L.dst_off, L.dst_dat, co, cd);
+    pdl_launch(k_comb, (unsigned)cdiv(E + 1, 256), 256, 0, c.stream, E, L.src_off, L.src_dat, L.dst_off, L.dst_dat, co, cd);
     DHGP_LAUNCHED(c);
     seg_sort(c, E, co, cd, nullptr, tmp);
     int64_t *cnt = c.alloc<int64_t>(E);
@@ -176,7 +181,7 @@ void feasibility(Ctx &c, const DLevel &L, int64_t omega, int64_t delta, int32_t 
     int32_t *bad = c.alloc<int32_t>(2);
     fill_i32(c, bad, 0x7fffffff, 2);
     if (L.N > 0) {
-        k_feasible<<<(unsigned)cdiv(L.N, 256), 256, 0, c.stream>>>(L.N, L.size, L.in_off, omega, delta, bad);
+        pdl_launch(k_feasible, (unsigned)cdiv(L.N, 256), 256, 0, c.stream, L.N, L.size, L.in_off, omega, delta, bad);
         DHGP_LAUNCHED(c);
     }
     int32_t h[2];

@@ -23,6 +23,7 @@ constexpr int NL_BYTES = 32;  // bytes per thread
 constexpr int NL_TILE = NL_THREADS * NL_BYTES;
 
 __global__ void k_nl_count(const char *text, int64_t len, int64_t *counts) {
+    pdl_entry();
     __shared__ int64_t sh[33];
     const int64_t base = (int64_t)blockIdx.x * NL_TILE + (int64_t)threadIdx.x * NL_BYTES;
     int64_t c = 0;
@@ -36,6 +37,7 @@ __global__ void k_nl_count(const char *text, int64_t len, int64_t *counts) {
 
 // line_start[0] = 0; line_start[k + 1] = (position of the k-th newline) + 1
 __global__ void k_nl_write(const char *text, int64_t len, const int64_t *block_off, int64_t *line_start) {
+    pdl_entry();
     __shared__ int64_t sh[33];
     const int64_t base = (int64_t)blockIdx.x * NL_TILE + (int64_t)threadIdx.x * NL_BYTES;
     int64_t c = 0;
@@ -87,6 +89,7 @@ constexpr uint8_t LN_OK = 0, LN_SLOW = 1, LN_ERR = 2;
 // Warp per line: token count, the first three tokens, slow / error status.
 __global__ void k_line_pass1(const char *text, const int64_t *line_start, int64_t E, double *w, int64_t *ks,
                              int64_t *kd, uint8_t *status, int64_t *slow_idx, unsigned long long *nslow) {
+    pdl_entry();
     const int lane = lane_id();
     const uint32_t lt = (1u << lane) - 1u;
     const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -149,6 +152,7 @@ __global__ void k_line_pass1(const char *text, const int64_t *line_start, int64_
 __global__ void k_line_pass2(const char *text, const int64_t *line_start, int64_t E, int64_t num_nodes,
                              const uint8_t *status, const int64_t *ks, const int64_t *src_off, const int64_t *dst_off,
                              int32_t *src_dat, int32_t *dst_dat, uint8_t *bad) {
+    pdl_entry();
     const int lane = lane_id();
     const uint32_t lt = (1u << lane) - 1u;
     const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -189,6 +193,7 @@ __global__ void k_line_pass2(const char *text, const int64_t *line_start, int64_
 __global__ void k_slow_counts(int64_t nslow, const int64_t *slow_idx, const int64_t *sks, const int64_t *skd,
                               const double *sw, const uint8_t *serr, int64_t *ks, int64_t *kd, double *w,
                               uint8_t *bad) {
+    pdl_entry();
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= nslow) return;
     const int64_t e = slow_idx[i];
@@ -200,6 +205,7 @@ __global__ void k_slow_counts(int64_t nslow, const int64_t *slow_idx, const int6
 __global__ void k_slow_ids(int64_t nslow, const int64_t *slow_idx, const int64_t *ids_off, const int32_t *ids,
                            const int64_t *ks, const int64_t *src_off, const int64_t *dst_off, int32_t *src_dat,
                            int32_t *dst_dat) {
+    pdl_entry();
     const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
     for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id(); i < nslow; i += nw) {
         const int64_t e = slow_idx[i];
@@ -215,11 +221,13 @@ __global__ void k_slow_ids(int64_t nslow, const int64_t *slow_idx, const int64_t
 }
 
 __global__ void k_err_flags(int64_t E, const uint8_t *status, uint8_t *bad) {
+    pdl_entry();
     int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e < E && status[e] == LN_ERR) bad[e] = 1;
 }
 // a repeated id within one side: adjacent equal values of the sorted side
 __global__ void k_dup_flags(int64_t E, const int64_t *off, const int32_t *sorted, uint8_t *bad) {
+    pdl_entry();
     int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= E || off[e + 1] - off[e] > kMaxSegSort) return;
     for (int64_t p = off[e] + 1; p < off[e + 1]; p++)
@@ -229,6 +237,7 @@ __global__ void k_dup_flags(int64_t E, const int64_t *off, const int32_t *sorted
         }
 }
 __global__ void k_dup_big(int64_t E, const int64_t *off, const int32_t *dat, uint8_t *bad) {
+    pdl_entry();
     __shared__ int s_found;
     for (int64_t e = blockIdx.x; e < E; e += gridDim.x) {
         const int64_t lo = off[e], n = off[e + 1] - lo;
@@ -247,6 +256,7 @@ __global__ void k_dup_big(int64_t E, const int64_t *off, const int32_t *dat, uin
     }
 }
 __global__ void k_first_bad(int64_t E, const uint8_t *bad, unsigned long long *first) {
+    pdl_entry();
     int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e < E && bad[e]) atomicMin(first, (unsigned long long)e);
 }
@@ -311,7 +321,7 @@ int dhgp_parse_dhg_begin(const char *text, int64_t len, int64_t num_edges, int64
     c.h2d(ps->text, text, len);
     const int64_t nb = std::max<int64_t>(1, cdiv(len, NL_TILE));
     int64_t *counts = c.alloc<int64_t>(nb), *boff = c.alloc<int64_t>(nb + 1);
-    k_nl_count<<<(unsigned)nb, NL_THREADS, 0, c.stream>>>(ps->text, len, counts);
+    pdl_launch(k_nl_count, (unsigned)nb, NL_THREADS, 0, c.stream, ps->text, len, counts);
     DHGP_LAUNCHED(c);
     scan_excl<int64_t>(c, counts, boff, nb);
     int64_t nl = 0;
@@ -328,7 +338,7 @@ int dhgp_parse_dhg_begin(const char *text, int64_t len, int64_t num_edges, int64
     const int64_t E = num_edges;
     ps->E = E;
     ps->line_start = c.alloc<int64_t>(E + 1);
-    k_nl_write<<<(unsigned)nb, NL_THREADS, 0, c.stream>>>(ps->text, len, boff, ps->line_start);
+    pdl_launch(k_nl_write, (unsigned)nb, NL_THREADS, 0, c.stream, ps->text, len, boff, ps->line_start);
     DHGP_LAUNCHED(c);
     // sentinel: the last line ends at len (as if followed by '\n')
     const int64_t endp = len + 1;
@@ -345,7 +355,7 @@ int dhgp_parse_dhg_begin(const char *text, int64_t len, int64_t num_edges, int64
     c.zero(ps->w, E);
     if (E > 0) {
         const int blocks = (int)std::min<int64_t>(cdiv(E, 8), (int64_t)c.num_sms * 16);
-        k_line_pass1<<<blocks, 256, 0, c.stream>>>(ps->text, ps->line_start, E, ps->w, ps->ks, ps->kd, ps->status,
+        pdl_launch(k_line_pass1, blocks, 256, 0, c.stream, ps->text, ps->line_start, E, ps->w, ps->ks, ps->kd, ps->status,
                                                    ps->slow_idx, ps->nslow);
         DHGP_LAUNCHED(c);
     }
@@ -401,7 +411,7 @@ int dhgp_parse_dhg_finish(dhgp_parse *ps, const int64_t *slow_ks, const int64_t 
         c.h2d(dkd, slow_kd, ns);
         c.h2d(dw, slow_w, ns);
         c.h2d(de, slow_err, ns);
-        k_slow_counts<<<(unsigned)cdiv(ns, 256), 256, 0, c.stream>>>(ns, ps->slow_idx, dks, dkd, dw, de, ps->ks,
+        pdl_launch(k_slow_counts, (unsigned)cdiv(ns, 256), 256, 0, c.stream, ns, ps->slow_idx, dks, dkd, dw, de, ps->ks,
                                                                       ps->kd, ps->w, ps->bad);
         DHGP_LAUNCHED(c);
         c.free(dks);
@@ -423,10 +433,10 @@ int dhgp_parse_dhg_finish(dhgp_parse *ps, const int64_t *slow_ks, const int64_t 
     ps->dst_dat = c.alloc<int32_t>(tot[1]);
     if (E > 0) {
         const int blocks = (int)std::min<int64_t>(cdiv(E, 8), (int64_t)c.num_sms * 16);
-        k_line_pass2<<<blocks, 256, 0, c.stream>>>(ps->text, ps->line_start, E, ps->N, ps->status, ps->ks,
+        pdl_launch(k_line_pass2, blocks, 256, 0, c.stream, ps->text, ps->line_start, E, ps->N, ps->status, ps->ks,
                                                    ps->src_off, ps->dst_off, ps->src_dat, ps->dst_dat, ps->bad);
         DHGP_LAUNCHED(c);
-        k_err_flags<<<(unsigned)cdiv(E, 256), 256, 0, c.stream>>>(E, ps->status, ps->bad);
+        pdl_launch(k_err_flags, (unsigned)cdiv(E, 256), 256, 0, c.stream, E, ps->status, ps->bad);
         DHGP_LAUNCHED(c);
     }
     if (ns > 0) {
@@ -436,7 +446,7 @@ int dhgp_parse_dhg_finish(dhgp_parse *ps, const int64_t *slow_ks, const int64_t 
         c.h2d(doff, slow_ids_off, ns + 1);
         c.h2d(dids, slow_ids, nids);
         const int blocks = (int)std::min<int64_t>(cdiv(ns, 8), (int64_t)c.num_sms * 16);
-        k_slow_ids<<<blocks, 256, 0, c.stream>>>(ns, ps->slow_idx, doff, dids, ps->ks, ps->src_off, ps->dst_off,
+        pdl_launch(k_slow_ids, blocks, 256, 0, c.stream, ns, ps->slow_idx, doff, dids, ps->ks, ps->src_off, ps->dst_off,
                                                  ps->src_dat, ps->dst_dat);
         DHGP_LAUNCHED(c);
         c.free(doff);
@@ -448,14 +458,14 @@ int dhgp_parse_dhg_finish(dhgp_parse *ps, const int64_t *slow_ks, const int64_t 
         // longer ones (rare): a block compares all pairs
         int32_t *tmp = c.alloc<int32_t>(std::max(tot[0], tot[1]));
         seg_sort(c, E, ps->src_off, ps->src_dat, nullptr, tmp);
-        k_dup_flags<<<(unsigned)cdiv(E, 256), 256, 0, c.stream>>>(E, ps->src_off, tmp, ps->bad);
+        pdl_launch(k_dup_flags, (unsigned)cdiv(E, 256), 256, 0, c.stream, E, ps->src_off, tmp, ps->bad);
         DHGP_LAUNCHED(c);
-        k_dup_big<<<c.num_sms, 1024, 0, c.stream>>>(E, ps->src_off, ps->src_dat, ps->bad);
+        pdl_launch(k_dup_big, c.num_sms, 1024, 0, c.stream, E, ps->src_off, ps->src_dat, ps->bad);
         DHGP_LAUNCHED(c);
         seg_sort(c, E, ps->dst_off, ps->dst_dat, nullptr, tmp);
-        k_dup_flags<<<(unsigned)cdiv(E, 256), 256, 0, c.stream>>>(E, ps->dst_off, tmp, ps->bad);
+        pdl_launch(k_dup_flags, (unsigned)cdiv(E, 256), 256, 0, c.stream, E, ps->dst_off, tmp, ps->bad);
         DHGP_LAUNCHED(c);
-        k_dup_big<<<c.num_sms, 1024, 0, c.stream>>>(E, ps->dst_off, ps->dst_dat, ps->bad);
+        pdl_launch(k_dup_big, c.num_sms, 1024, 0, c.stream, E, ps->dst_off, ps->dst_dat, ps->bad);
         DHGP_LAUNCHED(c);
         c.free(tmp);
     }
@@ -463,7 +473,7 @@ int dhgp_parse_dhg_finish(dhgp_parse *ps, const int64_t *slow_ks, const int64_t 
     const unsigned long long none = ~0ull;
     c.h2d(first, &none, 1);
     if (E > 0) {
-        k_first_bad<<<(unsigned)cdiv(E, 256), 256, 0, c.stream>>>(E, ps->bad, first);
+        pdl_launch(k_first_bad, (unsigned)cdiv(E, 256), 256, 0, c.stream, E, ps->bad, first);
         DHGP_LAUNCHED(c);
     }
     unsigned long long fb = 0;

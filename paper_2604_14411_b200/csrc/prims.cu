@@ -68,6 +68,7 @@ struct ScanSet {
 
 template <class T>
 __global__ void __launch_bounds__(SC_BT) k_scan_final(ScanSet<T> set, int64_t n, const int64_t *partial) {
+    pdl_entry();
     const T *in = set.in[blockIdx.y];
     int64_t *out = set.out[blockIdx.y];
     __shared__ int64_t sh[SC_BT / 32];
@@ -87,6 +88,7 @@ constexpr uint32_t kAggBit = 1u, kIncBit = 2u;
 template <class T>
 __global__ void __launch_bounds__(SC_BT) k_scan_onepass(ScanSet<T> set, int64_t n, uint32_t *flag0, int64_t *agg0,
                                                         int64_t *inc0, int64_t stride, uint32_t epoch) {
+    pdl_entry();
     const T *in = set.in[blockIdx.y];
     int64_t *out = set.out[blockIdx.y];
     uint32_t *flag = flag0 + blockIdx.y * stride;
@@ -164,7 +166,7 @@ static void scan_set(Ctx &c, const ScanSet<T> &set, int k, int64_t n) {
     }
     const int64_t ntiles = cdiv(n, SC_TILE);
     if (ntiles == 1) {
-        k_scan_final<T><<<dim3(1, k), SC_BT, 0, c.stream>>>(set, n, nullptr);
+        pdl_launch(k_scan_final<T>, dim3(1, k), SC_BT, 0, c.stream, set, n, nullptr);
         DHGP_LAUNCHED(c);
         return;
     }
@@ -190,7 +192,7 @@ static void scan_set(Ctx &c, const ScanSet<T> &set, int k, int64_t n) {
         DHGP_CUDA(cudaMemsetAsync(ss.flag, 0, sizeof(uint32_t) * ss.cap, c.stream));
         ss.epoch = 1;
     }
-    k_scan_onepass<T><<<dim3((unsigned)ntiles, k), SC_BT, 0, c.stream>>>(s2, n, ss.flag, ss.agg, ss.inc, ntiles,
+    pdl_launch(k_scan_onepass<T>, dim3((unsigned)ntiles, k), SC_BT, 0, c.stream, s2, n, ss.flag, ss.agg, ss.inc, ntiles,
                                                                          ss.epoch);
     DHGP_LAUNCHED(c);
 }
@@ -242,6 +244,7 @@ __device__ __forceinline__ int64_t block_incl_max(int64_t v, int64_t *sh, int64_
     return r;
 }
 __global__ void k_max_reduce(const int64_t *in, int64_t n, int64_t *partial) {
+    pdl_entry();
     __shared__ int64_t sh[33];
     int64_t base = (int64_t)blockIdx.x * SC_TILE, m = LLONG_MIN;
     for (int i = 0; i < SC_IPT; i++) {
@@ -253,6 +256,7 @@ __global__ void k_max_reduce(const int64_t *in, int64_t n, int64_t *partial) {
     if (threadIdx.x == 0) partial[blockIdx.x] = t;
 }
 __global__ void k_max_partials(int64_t *partial, int64_t ntiles) {
+    pdl_entry();
     // exclusive running max over tiles: the carry into each tile
     __shared__ int64_t sh[33];
     __shared__ int64_t incl_s[1024];
@@ -272,6 +276,7 @@ __global__ void k_max_partials(int64_t *partial, int64_t ntiles) {
     }
 }
 __global__ void k_max_final(const int64_t *in, int64_t n, const int64_t *partial, int64_t *out) {
+    pdl_entry();
     __shared__ int64_t sh[33];
     __shared__ int64_t buf[SC_TILE];
     int64_t base = (int64_t)blockIdx.x * SC_TILE;
@@ -310,16 +315,16 @@ void scan_incl_max(Ctx &c, const int64_t *in, int64_t *out, int64_t n) {
     if (n <= 0) return;
     int64_t ntiles = cdiv(n, SC_TILE);
     if (ntiles == 1) {
-        k_max_final<<<1, SC_BT, 0, c.stream>>>(in, n, nullptr, out);
+        pdl_launch(k_max_final, 1, SC_BT, 0, c.stream, in, n, nullptr, out);
         DHGP_LAUNCHED(c);
         return;
     }
     int64_t *partial = c.alloc<int64_t>(ntiles + 1);
-    k_max_reduce<<<(unsigned)ntiles, SC_BT, 0, c.stream>>>(in, n, partial);
+    pdl_launch(k_max_reduce, (unsigned)ntiles, SC_BT, 0, c.stream, in, n, partial);
     DHGP_LAUNCHED(c);
-    k_max_partials<<<1, 1024, 0, c.stream>>>(partial, ntiles);
+    pdl_launch(k_max_partials, 1, 1024, 0, c.stream, partial, ntiles);
     DHGP_LAUNCHED(c);
-    k_max_final<<<(unsigned)ntiles, SC_BT, 0, c.stream>>>(in, n, partial, out);
+    pdl_launch(k_max_final, (unsigned)ntiles, SC_BT, 0, c.stream, in, n, partial, out);
     DHGP_LAUNCHED(c);
     c.free(partial);
 }
@@ -338,6 +343,7 @@ constexpr int RS_TILE = RS_BT * RS_STEPS;
 
 __global__ void k_rs_up(const uint64_t *kin, int64_t ncap, const int64_t *dn, int shift, int64_t *counts,
                         int64_t ntiles) {
+    pdl_entry();
     __shared__ uint32_t cnt[256];
     const int64_t n = dn ? *dn : ncap;
     cnt[threadIdx.x] = 0;
@@ -356,6 +362,7 @@ __global__ void k_rs_up(const uint64_t *kin, int64_t ncap, const int64_t *dn, in
 
 __global__ void k_rs_down(const uint64_t *kin, const uint32_t *vin, uint64_t *kout, uint32_t *vout, int64_t ncap,
                           const int64_t *dn, int shift, const int64_t *offs, int64_t ntiles) {
+    pdl_entry();
     __shared__ uint32_t wcnt[RS_BT / 32][256];
     const int64_t n = dn ? *dn : ncap;
     const int64_t base = (int64_t)blockIdx.x * RS_TILE;
@@ -408,6 +415,7 @@ __global__ void k_rs_down(const uint64_t *kin, const uint32_t *vin, uint64_t *ko
 
 namespace {
 __global__ void __launch_bounds__(1024) k_small_sort(uint64_t *keys, uint32_t *vals, int n) {
+    pdl_entry();
     __shared__ uint64_t sk[kSmallSort];
     __shared__ uint32_t sv[kSmallSort];
     int np = 1;
@@ -443,6 +451,7 @@ __global__ void __launch_bounds__(1024) k_small_sort(uint64_t *keys, uint32_t *v
 // unique u64 keys whose low 32 bits are the value (the packed mover keys)
 __global__ void __launch_bounds__(1024) k_small_sort_packed(uint64_t *keys, uint32_t *vals, int n,
                                                             const int64_t *dn) {
+    pdl_entry();
     if (dn) {  // count on device: a no-op when it does not fit
         const int64_t m = *dn;
         if (m <= 1 || m > kSmallSort) return;
@@ -463,7 +472,7 @@ __global__ void __launch_bounds__(1024) k_small_sort_packed(uint64_t *keys, uint
 void small_sort_pairs(Ctx &c, uint64_t *keys, uint32_t *vals, int64_t n) {
     if (n <= 1) return;
     KScope ks(c, "radix_sort");
-    k_small_sort<<<1, 1024, 0, c.stream>>>(keys, vals, (int)n);
+    pdl_launch(k_small_sort, 1, 1024, 0, c.stream, keys, vals, (int)n);
     DHGP_LAUNCHED(c);
 }
 void small_sort_packed(Ctx &c, uint64_t *keys, uint32_t *vals, int64_t n, const int64_t *dn) {
@@ -475,7 +484,7 @@ void small_sort_packed(Ctx &c, uint64_t *keys, uint32_t *vals, int64_t n, const 
                                        (int)(2 * kSmallSort * sizeof(uint64_t))));
         attr = true;
     }
-    k_small_sort_packed<<<1, 1024, 2 * kSmallSort * sizeof(uint64_t), c.stream>>>(keys, vals, (int)n, dn);
+    pdl_launch(k_small_sort_packed, 1, 1024, 2 * kSmallSort * sizeof(uint64_t), c.stream, keys, vals, (int)n, dn);
     DHGP_LAUNCHED(c);
 }
 
@@ -491,10 +500,10 @@ void radix_sort_pairs(Ctx &c, uint64_t *keys, uint32_t *vals, uint64_t *ktmp, ui
     const int passes = (bits + 7) / 8;
     for (int p = 0; p < passes; p++) {
         const int shift = 8 * p;
-        k_rs_up<<<(unsigned)ntiles, RS_BT, 0, c.stream>>>(ka, n_cap, d_n, shift, counts, ntiles);
+        pdl_launch(k_rs_up, (unsigned)ntiles, RS_BT, 0, c.stream, ka, n_cap, d_n, shift, counts, ntiles);
         DHGP_LAUNCHED(c);
         scan_excl<int64_t>(c, counts, offs, 256 * ntiles);
-        k_rs_down<<<(unsigned)ntiles, RS_BT, 0, c.stream>>>(ka, va, kb, vb, n_cap, d_n, shift, offs, ntiles);
+        pdl_launch(k_rs_down, (unsigned)ntiles, RS_BT, 0, c.stream, ka, va, kb, vb, n_cap, d_n, shift, offs, ntiles);
         DHGP_LAUNCHED(c);
         std::swap(ka, kb);
         std::swap(va, vb);
@@ -517,6 +526,7 @@ constexpr int kWarpTier = 128;
 
 __global__ void k_seg_sort_thread(int64_t nseg, const int64_t *off, const int32_t *dat, const int32_t *map,
                                   int32_t *tmp, int32_t *warp_list, int32_t *block_list, int32_t *counts) {
+    pdl_entry();
     int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= nseg) return;
     int64_t lo = off[s], len = off[s + 1] - lo;
@@ -583,6 +593,7 @@ __device__ __forceinline__ void warp_sort_segment(int64_t lo, int len, const int
 
 __global__ void k_seg_sort_warp(const int64_t *off, const int32_t *dat, const int32_t *map, int32_t *tmp,
                                 const int32_t *list, const int32_t *counts) {
+    pdl_entry();
     const int nw = gridDim.x * (blockDim.x >> 5);
     const int n = counts[0];
     for (int t = blockIdx.x * (blockDim.x >> 5) + warp_id(); t < n; t += nw) {
@@ -600,6 +611,7 @@ __global__ void k_seg_sort_warp(const int64_t *off, const int32_t *dat, const in
 
 __global__ void k_seg_sort_block(const int64_t *off, const int32_t *dat, const int32_t *map, int32_t *tmp,
                                  const int32_t *list, const int32_t *counts, int32_t *err) {
+    pdl_entry();
     extern __shared__ uint32_t sbuf[];
     const int n = counts[1];
     for (int t = blockIdx.x; t < n; t += gridDim.x) {
@@ -634,13 +646,13 @@ void seg_sort(Ctx &c, int64_t nseg, const int64_t *off, const int32_t *dat, cons
     int32_t *bl = c.alloc<int32_t>(nseg);
     int32_t *cnt = c.alloc<int32_t>(3);
     c.zero(cnt, 3);
-    k_seg_sort_thread<<<(unsigned)cdiv(nseg, 256), 256, 0, c.stream>>>(nseg, off, dat, map, tmp, wl, bl, cnt);
+    pdl_launch(k_seg_sort_thread, (unsigned)cdiv(nseg, 256), 256, 0, c.stream, nseg, off, dat, map, tmp, wl, bl, cnt);
     DHGP_LAUNCHED(c);
-    k_seg_sort_warp<<<(unsigned)(c.num_sms * 8), 256, 0, c.stream>>>(off, dat, map, tmp, wl, cnt);
+    pdl_launch(k_seg_sort_warp, (unsigned)(c.num_sms * 8), 256, 0, c.stream, off, dat, map, tmp, wl, cnt);
     DHGP_LAUNCHED(c);
     // segment lengths are bounded by kMaxSegSort at upload (max h-edge degree
     // only shrinks under contraction), so the block tier never overflows
-    k_seg_sort_block<<<(unsigned)(c.num_sms), 1024, kMaxSegSort * sizeof(uint32_t), c.stream>>>(off, dat, map, tmp,
+    pdl_launch(k_seg_sort_block, (unsigned)(c.num_sms), 1024, kMaxSegSort * sizeof(uint32_t), c.stream, off, dat, map, tmp,
                                                                                                  bl, cnt, cnt + 2);
     DHGP_LAUNCHED(c);
     c.free(wl);
@@ -650,6 +662,7 @@ void seg_sort(Ctx &c, int64_t nseg, const int64_t *off, const int32_t *dat, cons
 
 namespace {
 __global__ void k_seg_unique_count(int64_t nseg, const int64_t *off, const int32_t *tmp, int64_t *cnt) {
+    pdl_entry();
     int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= nseg) return;
     int64_t lo = off[s], hi = off[s + 1];
@@ -664,6 +677,7 @@ __global__ void k_seg_unique_count(int64_t nseg, const int64_t *off, const int32
 }
 __global__ void k_seg_unique_write(int64_t nseg, const int64_t *off, const int32_t *tmp, const int64_t *out_off,
                                    int32_t *out) {
+    pdl_entry();
     int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= nseg) return;
     int64_t lo = off[s], hi = off[s + 1];
@@ -679,13 +693,13 @@ __global__ void k_seg_unique_write(int64_t nseg, const int64_t *off, const int32
 
 void seg_unique_count(Ctx &c, int64_t nseg, const int64_t *off, const int32_t *tmp, int64_t *cnt) {
     if (nseg <= 0) return;
-    k_seg_unique_count<<<(unsigned)cdiv(nseg, 256), 256, 0, c.stream>>>(nseg, off, tmp, cnt);
+    pdl_launch(k_seg_unique_count, (unsigned)cdiv(nseg, 256), 256, 0, c.stream, nseg, off, tmp, cnt);
     DHGP_LAUNCHED(c);
 }
 void seg_unique_write(Ctx &c, int64_t nseg, const int64_t *off, const int32_t *tmp, const int64_t *out_off,
                       int32_t *out) {
     if (nseg <= 0) return;
-    k_seg_unique_write<<<(unsigned)cdiv(nseg, 256), 256, 0, c.stream>>>(nseg, off, tmp, out_off, out);
+    pdl_launch(k_seg_unique_write, (unsigned)cdiv(nseg, 256), 256, 0, c.stream, nseg, off, tmp, out_off, out);
     DHGP_LAUNCHED(c);
 }
 
@@ -712,6 +726,7 @@ __device__ __forceinline__ void merge_count_body(int64_t nc_cap, const int64_t *
                                                  int64_t *cnt, int32_t *big_list, int32_t *big_count);
 __global__ void k_merge_count2(int64_t nc_cap, const int64_t *d_nc, const int32_t *ma, const int32_t *mb,
                                MergeFams fs) {
+    pdl_entry();
     const MergeFam &f = fs.f[blockIdx.y];
     merge_count_body(nc_cap, d_nc, ma, mb, f.off, f.dat, f.cnt, f.big_list, f.big_count);
 }
@@ -755,6 +770,7 @@ __device__ __forceinline__ void merge_write_body(int64_t nc, const int32_t *ma, 
                                                  const int32_t *dat, const int64_t *out_off, int32_t *out,
                                                  bool skip_big);
 __global__ void k_merge_write2(int64_t nc, const int32_t *ma, const int32_t *mb, MergeFams fs, bool skip_big) {
+    pdl_entry();
     const MergeFam &f = fs.f[blockIdx.y];
     merge_write_body(nc, ma, mb, f.off, f.dat, f.out_off, f.out, skip_big);
 }
@@ -841,6 +857,7 @@ __device__ __forceinline__ void merge_count_big_body(const int32_t *list, const 
                                                      const int32_t *mb, const int64_t *off, const int32_t *dat,
                                                      int64_t *cnt);
 __global__ void k_merge_count_big2(const int32_t *ma, const int32_t *mb, MergeFams fs) {
+    pdl_entry();
     const MergeFam &f = fs.f[blockIdx.y];
     merge_count_big_body(f.big_list, f.big_count, ma, mb, f.off, f.dat, f.cnt);
 }
@@ -866,6 +883,7 @@ __device__ __forceinline__ void merge_write_big_body(const int32_t *list, const 
                                                      const int32_t *mb, const int64_t *off, const int32_t *dat,
                                                      const int64_t *out_off, int32_t *out);
 __global__ void k_merge_write_big2(const int32_t *ma, const int32_t *mb, MergeFams fs) {
+    pdl_entry();
     const MergeFam &f = fs.f[blockIdx.y];
     merge_write_big_body(f.big_list, f.big_count, ma, mb, f.off, f.dat, f.out_off, f.out);
 }
@@ -929,9 +947,9 @@ void merge_union_count2(Ctx &c, int64_t nc, const int32_t *ma, const int32_t *mb
     MergeFams fs{{MergeFam{off0, dat0, cnt0, nullptr, nullptr, big0, bigc0},
                   MergeFam{off1, dat1, cnt1, nullptr, nullptr, big1, bigc1}}};
     const int64_t blocks = std::min<int64_t>(cdiv(nc, 8), (int64_t)c.num_sms * 16);
-    k_merge_count2<<<dim3((unsigned)blocks, 2), 256, 0, c.stream>>>(nc, d_nc, ma, mb, fs);
+    pdl_launch(k_merge_count2, dim3((unsigned)blocks, 2), 256, 0, c.stream, nc, d_nc, ma, mb, fs);
     DHGP_LAUNCHED(c);
-    k_merge_count_big2<<<dim3(c.num_sms, 2), 1024, 0, c.stream>>>(ma, mb, fs);
+    pdl_launch(k_merge_count_big2, dim3(c.num_sms, 2), 1024, 0, c.stream, ma, mb, fs);
     DHGP_LAUNCHED(c);
 }
 void merge_union_write2(Ctx &c, int64_t nc, const int32_t *ma, const int32_t *mb, const int64_t *off0,
@@ -942,9 +960,9 @@ void merge_union_write2(Ctx &c, int64_t nc, const int32_t *ma, const int32_t *mb
     MergeFams fs{{MergeFam{off0, dat0, nullptr, out_off0, out0, big0, bigc0},
                   MergeFam{off1, dat1, nullptr, out_off1, out1, big1, bigc1}}};
     const int64_t blocks = std::min<int64_t>(cdiv(nc, 8), (int64_t)c.num_sms * 16);
-    k_merge_write2<<<dim3((unsigned)blocks, 2), 256, 0, c.stream>>>(nc, ma, mb, fs, true);
+    pdl_launch(k_merge_write2, dim3((unsigned)blocks, 2), 256, 0, c.stream, nc, ma, mb, fs, true);
     DHGP_LAUNCHED(c);
-    k_merge_write_big2<<<dim3(c.num_sms, 2), 1024, 0, c.stream>>>(ma, mb, fs);
+    pdl_launch(k_merge_write_big2, dim3(c.num_sms, 2), 1024, 0, c.stream, ma, mb, fs);
     DHGP_LAUNCHED(c);
 }
 
@@ -957,6 +975,7 @@ struct ZeroSet {
     int64_t bytes[8];
 };
 __global__ void k_zero_many(ZeroSet z) {
+    pdl_entry();
     char *p = (char *)z.p[blockIdx.y];
     const int64_t nb = z.bytes[blockIdx.y];
     const int64_t nw = nb >> 2;
@@ -979,7 +998,7 @@ void zero_many(Ctx &c, std::initializer_list<std::pair<void *, int64_t>> bufs) {
     }
     if (n == 0) return;
     const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(mx / 4, 256), 64));
-    k_zero_many<<<dim3(gx, n), 256, 0, c.stream>>>(z);
+    pdl_launch(k_zero_many, dim3(gx, n), 256, 0, c.stream, z);
     DHGP_LAUNCHED(c);
 }
 
@@ -988,20 +1007,24 @@ void zero_many(Ctx &c, std::initializer_list<std::pair<void *, int64_t>> bufs) {
 // ===========================================================================
 namespace {
 __global__ void k_iota(int32_t *p, int64_t n) {
+    pdl_entry();
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) p[i] = (int32_t)i;
 }
 __global__ void k_fill32(int32_t *p, int32_t v, int64_t n) {
+    pdl_entry();
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) p[i] = v;
 }
 __global__ void k_fill64(int64_t *p, int64_t v, int64_t n) {
+    pdl_entry();
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) p[i] = v;
 }
 // per pin: key = node id, val = edge id (pins enumerated in edge order)
 __global__ void k_expand_pairs(int64_t nseg, const int64_t *off, const int32_t *dat, uint64_t *keys,
                                uint32_t *vals, int32_t *node_count) {
+    pdl_entry();
     int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= nseg) return;
     int64_t lo = off[e] - off[0], hi = off[e + 1] - off[0];
@@ -1013,6 +1036,7 @@ __global__ void k_expand_pairs(int64_t nseg, const int64_t *off, const int32_t *
     }
 }
 __global__ void k_u32_to_i32(const uint32_t *a, int32_t *b, int64_t n) {
+    pdl_entry();
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) b[i] = (int32_t)a[i];
 }
@@ -1020,17 +1044,17 @@ __global__ void k_u32_to_i32(const uint32_t *a, int32_t *b, int64_t n) {
 
 void iota_i32(Ctx &c, int32_t *p, int64_t n) {
     if (n <= 0) return;
-    k_iota<<<(unsigned)cdiv(n, 256), 256, 0, c.stream>>>(p, n);
+    pdl_launch(k_iota, (unsigned)cdiv(n, 256), 256, 0, c.stream, p, n);
     DHGP_LAUNCHED(c);
 }
 void fill_i32(Ctx &c, int32_t *p, int32_t v, int64_t n) {
     if (n <= 0) return;
-    k_fill32<<<(unsigned)cdiv(n, 256), 256, 0, c.stream>>>(p, v, n);
+    pdl_launch(k_fill32, (unsigned)cdiv(n, 256), 256, 0, c.stream, p, v, n);
     DHGP_LAUNCHED(c);
 }
 void fill_i64(Ctx &c, int64_t *p, int64_t v, int64_t n) {
     if (n <= 0) return;
-    k_fill64<<<(unsigned)cdiv(n, 256), 256, 0, c.stream>>>(p, v, n);
+    pdl_launch(k_fill64, (unsigned)cdiv(n, 256), 256, 0, c.stream, p, v, n);
     DHGP_LAUNCHED(c);
 }
 
@@ -1046,10 +1070,10 @@ void transpose_csr(Ctx &c, int64_t nseg, int32_t N, const int64_t *off, const in
     }
     uint64_t *k = c.alloc<uint64_t>(nnz), *kt = c.alloc<uint64_t>(nnz);
     uint32_t *v = c.alloc<uint32_t>(nnz), *vt = c.alloc<uint32_t>(nnz);
-    k_expand_pairs<<<(unsigned)cdiv(nseg, 256), 256, 0, c.stream>>>(nseg, off, dat, k, v, cnt);
+    pdl_launch(k_expand_pairs, (unsigned)cdiv(nseg, 256), 256, 0, c.stream, nseg, off, dat, k, v, cnt);
     DHGP_LAUNCHED(c);
     radix_sort_pairs(c, k, v, kt, vt, nnz, nullptr, bitlen((uint64_t)(N > 0 ? N - 1 : 0)));
-    k_u32_to_i32<<<(unsigned)cdiv(nnz, 256), 256, 0, c.stream>>>(v, out_dat, nnz);
+    pdl_launch(k_u32_to_i32, (unsigned)cdiv(nnz, 256), 256, 0, c.stream, v, out_dat, nnz);
     DHGP_LAUNCHED(c);
     scan_excl<int32_t>(c, cnt, out_off, N);
     c.free(cnt);

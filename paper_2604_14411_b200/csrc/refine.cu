@@ -48,6 +48,7 @@ __device__ __forceinline__ int32_t run_find(const Runs &r, int64_t lo, int32_t l
 __global__ void k_edge_runs(int32_t E, const int64_t *pin_off, const int32_t *sorted_parts, const int64_t *dst_off,
                             const int32_t *dst_dat, const int32_t *assign, const int64_t *wi, Runs r,
                             unsigned long long *conn, int64_t *pinbound) {
+    pdl_entry();
     __shared__ int64_t sh[33];
     int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int64_t contrib = 0;
@@ -82,6 +83,7 @@ __global__ void k_edge_runs(int32_t E, const int64_t *pin_off, const int32_t *so
 __global__ void k_edge_runs_warp(int32_t E, const int64_t *pin_off, const int32_t *sorted_parts,
                                  const int64_t *dst_off, const int32_t *dst_dat, const int32_t *assign,
                                  const int64_t *wi, Runs r, unsigned long long *conn, int64_t *pinbound) {
+    pdl_entry();
     const int lane = lane_id();
     const uint32_t lt = (1u << lane) - 1u;
     const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -203,6 +205,7 @@ __device__ __forceinline__ int32_t warp_edge_runs(int64_t e, int64_t plo, int64_
 __global__ void k_edge_runs_fused(int32_t E, const int64_t *pin_off, const int32_t *pin_dat, const int64_t *dst_off,
                                   const int32_t *dst_dat, const int32_t *assign, const int64_t *wi, Runs r,
                                   unsigned long long *conn, int64_t *pinbound) {
+    pdl_entry();
     const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
     int64_t contrib = 0;
     for (int64_t e = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id(); e < E; e += nw) {
@@ -224,6 +227,7 @@ __global__ void k_edge_runs_fused(int32_t E, const int64_t *pin_off, const int32
 }
 
 __global__ void k_part_sizes(int32_t N, const int32_t *assign, const int32_t *size, int64_t *psizes) {
+    pdl_entry();
     int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (n < N) atomicAdd((unsigned long long *)&psizes[assign[n]], (unsigned long long)(int64_t)size[n]);
 }
@@ -420,6 +424,7 @@ __device__ __forceinline__ uint32_t pslot(int32_t p) { return ((uint32_t)p * 265
 
 template <class Acc>
 __global__ void __launch_bounds__(PR_WARPS * 32, 4) k_propose_warp(ProposeArgs a) {
+    pdl_entry();
     extern __shared__ unsigned long long smem_u64[];
     Acc *svals = (Acc *)smem_u64;
     int32_t *skeys = (int32_t *)(svals + PR_WARPS * PR_CAP);
@@ -567,6 +572,7 @@ __device__ __forceinline__ void block_best_gain(long long bg, int32_t bp, long l
 
 template <class Acc>
 __global__ void __launch_bounds__(PM_THREADS, 4) k_propose_mid(ProposeArgs a) {
+    pdl_entry();
     extern __shared__ unsigned long long smem_u64[];
     Acc *vals = (Acc *)smem_u64;
     int32_t *keys = (int32_t *)(vals + PM_CAP);
@@ -703,6 +709,7 @@ template <class Acc>
 constexpr size_t ph_smem(int K) { return (size_t)K * (sizeof(Acc) + 4) + 4 * (size_t)((K + 31) / 32) + 16; }
 template <class Acc, int THREADS = PH_THREADS>
 __global__ void __launch_bounds__(THREADS) k_propose_heavy(ProposeArgs a) {
+    pdl_entry();
     extern __shared__ unsigned long long smem_u64[];
     Acc *pres = (Acc *)smem_u64;
     int32_t *tlist = (int32_t *)(pres + a.K);
@@ -791,6 +798,7 @@ __global__ void __launch_bounds__(THREADS) k_propose_heavy(ProposeArgs a) {
 // work items are (hub, chunk) pairs)
 __global__ void __launch_bounds__(1024) k_hub_prefix(const int32_t *hub_list, const int32_t *hub_count, int hub_max,
                                                      const int64_t *inc_off, int32_t *pref) {
+    pdl_entry();
     __shared__ int32_t s_wt[32];
     const int nh = min(*hub_count, hub_max);
     const int lane = lane_id(), w = warp_id();
@@ -824,6 +832,7 @@ __global__ void __launch_bounds__(1024) k_hub_prefix(const int32_t *hub_list, co
 template <class Acc>
 __global__ void __launch_bounds__(256) k_propose_hub(ProposeArgs a, long long *hacc, long long *htot,
                                                      int32_t *hdone) {
+    pdl_entry();
     extern __shared__ unsigned long long smem_u64[];
     Acc *pres = (Acc *)smem_u64;
     __shared__ long long r_a[8], r_b[8];
@@ -919,6 +928,7 @@ __global__ void __launch_bounds__(256) k_propose_hub(ProposeArgs a, long long *h
 constexpr int PB_THREADS = 512;
 __global__ void __launch_bounds__(PB_THREADS) k_propose_block(ProposeArgs a, long long *dense_all,
                                                                int32_t *touched_all) {
+    pdl_entry();
     __shared__ int32_t s_nt;
     __shared__ long long s_red[PB_THREADS / 32][2];
     __shared__ int32_t s_p[PB_THREADS / 32];
@@ -993,11 +1003,13 @@ __global__ void __launch_bounds__(PB_THREADS) k_propose_block(ProposeArgs a, lon
 }
 
 __global__ void k_fill_ll(long long *p, long long v, int64_t n) {
+    pdl_entry();
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) p[i] = v;
 }
 
 __global__ void k_mover_flags(int32_t N, const int32_t *target, uint8_t *flags) {
+    pdl_entry();
     int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (n < N) flags[n] = target[n] >= 0;
 }
@@ -1006,6 +1018,7 @@ __global__ void k_mover_flags(int32_t N, const int32_t *target, uint8_t *flags) 
 // refine.py:108-110)
 __global__ void k_mover_keys(int32_t N, const uint8_t *flags, const int64_t *pos, const int64_t *gain, int64_t gmax,
                              uint64_t *keys, uint32_t *vals) {
+    pdl_entry();
     int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (n < N && flags[n]) {
         keys[pos[n]] = (uint64_t)(gmax - gain[n]);
@@ -1044,6 +1057,7 @@ constexpr int kEvParts = 2 * kEvBlockMax;  // hash slots (>= distinct parts: 2 p
 __global__ void __launch_bounds__(256) k_inbound_events_block(const int64_t *dst_off, const int32_t *dst_dat, Runs r,
                                        const int32_t *pos, const int32_t *from, const int32_t *to, EvArgs ev,
                                        const int32_t *big_list, const int32_t *big_count, int32_t *err) {
+    pdl_entry();
     __shared__ uint32_t smv[kEvBlockMax];
     __shared__ int32_t skey[kEvParts];
     __shared__ int32_t sparts[kEvParts];
@@ -1132,6 +1146,7 @@ __global__ void __launch_bounds__(256) k_inbound_events_block(const int64_t *dst
 // the limit.
 __global__ void k_ev_prep(int64_t T, const uint64_t *key, const uint32_t *val, int ibits, int64_t *gs, int64_t *ss,
                           int64_t *dv) {
+    pdl_entry();
     int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= T) return;
     const uint64_t kk = key[k];
@@ -1142,6 +1157,7 @@ __global__ void k_ev_prep(int64_t T, const uint64_t *key, const uint32_t *val, i
 __global__ void k_ev_toggle(int64_t T, const uint64_t *key, const int64_t *ex, const int64_t *gstart,
                             const int64_t *sstart, int ibits, int pbits, const int64_t *psizes,
                             const int64_t *pinbound, int64_t omega, int64_t delta, int64_t *dlt) {
+    pdl_entry();
     int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= T) return;
     const uint64_t kk = key[k];
@@ -1160,6 +1176,7 @@ __global__ void k_ev_toggle(int64_t T, const uint64_t *key, const int64_t *ex, c
 // smallest argmax of cum over prefixes with active == 0 (refine.py:244-247)
 __global__ void k_best_prefix_partial(int64_t n, const int64_t *active_ex, const int64_t *cum, long long *bv,
                                       long long *bk) {
+    pdl_entry();
     __shared__ long long sv[32], sk[32];
     long long v = LLONG_MIN, k = LLONG_MAX;
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
@@ -1196,6 +1213,7 @@ __global__ void k_best_prefix_partial(int64_t n, const int64_t *active_ex, const
     }
 }
 __global__ void k_best_prefix_final(int nb, const long long *bv, const long long *bk, long long *out) {
+    pdl_entry();
     if (threadIdx.x != 0) return;
     long long v = LLONG_MIN, k = LLONG_MAX;
     for (int b = 0; b < nb; b++)
@@ -1299,6 +1317,7 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select_small(const unsigned lon
                                                               const int64_t *pinbound, int64_t omega, int64_t delta,
                                                               int ibits, int pbits, int64_t *act_ex_out,
                                                               long long *res, bool packed) {
+    pdl_entry();
     extern __shared__ unsigned long long smem_u64[];
     __shared__ int64_t sh[33];
     __shared__ long long s_bv[32], s_bk[32];
@@ -1420,6 +1439,7 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select_small(const unsigned lon
 }
 
 __global__ void k_apply(int64_t k, const int32_t *node, const int32_t *to, int32_t *assign) {
+    pdl_entry();
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < k) assign[node[i]] = to[i];
 }
@@ -1438,7 +1458,7 @@ static void build_runs(Ctx &c, const DLevel &L, const DWeights &W, const int32_t
         if (L.E > 0) {
             static int g = resident_grid(c, k_edge_runs_fused, 256, 0);
             int blocks = (int)std::min<int64_t>(cdiv(L.E, 8), g);
-            k_edge_runs_fused<<<blocks, 256, 0, c.stream>>>(L.E, L.pin_off, L.pin_dat, L.dst_off, L.dst_dat, assign,
+            pdl_launch(k_edge_runs_fused, blocks, 256, 0, c.stream, L.E, L.pin_off, L.pin_dat, L.dst_off, L.dst_dat, assign,
                                                            W.wi, r, conn, pinbound);
             DHGP_LAUNCHED(c);
         }
@@ -1448,10 +1468,10 @@ static void build_runs(Ctx &c, const DLevel &L, const DWeights &W, const int32_t
     if (L.E > 0) {
         if (L.U >= 12 * (int64_t)L.E) {
             int blocks = (int)std::min<int64_t>(cdiv(L.E, 8), (int64_t)c.num_sms * 16);
-            k_edge_runs_warp<<<blocks, 256, 0, c.stream>>>(L.E, L.pin_off, tmp_parts, L.dst_off, L.dst_dat, assign,
+            pdl_launch(k_edge_runs_warp, blocks, 256, 0, c.stream, L.E, L.pin_off, tmp_parts, L.dst_off, L.dst_dat, assign,
                                                           W.wi, r, conn, pinbound);
         } else {
-            k_edge_runs<<<(unsigned)cdiv(L.E, 256), 256, 0, c.stream>>>(L.E, L.pin_off, tmp_parts, L.dst_off,
+            pdl_launch(k_edge_runs, (unsigned)cdiv(L.E, 256), 256, 0, c.stream, L.E, L.pin_off, tmp_parts, L.dst_off,
                                                                        L.dst_dat, assign, W.wi, r, conn, pinbound);
         }
         DHGP_LAUNCHED(c);
@@ -1463,6 +1483,7 @@ namespace {
 __global__ void k_build_moves_dn(const int64_t *dM, const uint32_t *sorted_nodes, const int32_t *assign,
                                  const int32_t *target, const int64_t *gain, int32_t *node, int32_t *from, int32_t *to,
                                  int64_t *giso, int32_t *pos, bool spec) {
+    pdl_entry();
     const int64_t M = *dM;
     if (spec && M > kSpecCap) return;  // speculative launch, M too large
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < M; i += (int64_t)gridDim.x * blockDim.x) {
@@ -1501,6 +1522,7 @@ __global__ void k_seq_gains_edge_block(const int64_t *pin_off, const int32_t *pi
                                        const int32_t *pos, const int32_t *from, const int32_t *to,
                                        unsigned long long *gacc, const int32_t *big_list, const int32_t *big_count,
                                        int32_t *err) {
+    pdl_entry();
     __shared__ uint32_t smv[kSgBlockMax];
     __shared__ int32_t sf[kSgBlockMax], st[kSgBlockMax];
     __shared__ int32_t snm;
@@ -1589,6 +1611,7 @@ __global__ void __launch_bounds__(256) k_round_edges(int32_t E, const int32_t *e
                                                      unsigned long long *gacc, EvArgs ev, int32_t *sg_big,
                                                      int32_t *sg_count, int32_t *ev_big, int32_t *ev_count,
                                                      int cap, const int64_t *spec_m) {
+    pdl_entry();
     if (spec_m && *spec_m > kSpecCap) return;  // speculative launch, M too large
     __shared__ int32_t s_mv[8][32];
     const int lane = lane_id();
@@ -1661,6 +1684,7 @@ __global__ void __launch_bounds__(256) k_round_edges(int32_t E, const int32_t *e
 // gains order by node (refine.py:108-110) in any sort; pos[] reset on the way
 __global__ void k_mover_compact(int32_t N, const int32_t *target, const int64_t *gain, int64_t gmax, uint64_t *keys,
                                 uint32_t *vals, int32_t *pos, unsigned long long *count) {
+    pdl_entry();
     const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const bool mv = n < N && target[n] >= 0;
     if (n < N) pos[n] = -1;
@@ -1698,6 +1722,7 @@ __device__ __forceinline__ void round_move(int64_t i, const int32_t *node, const
 __global__ void k_round_moves(const int64_t *dM, const int32_t *node, const int32_t *from, const int32_t *to,
                               const int32_t *size, EvArgs ev, const int64_t *giso, const unsigned long long *gacc,
                               int64_t *gseq, bool spec) {
+    pdl_entry();
     const int64_t M = *dM;
     if (spec && M > kSpecCap) return;  // speculative launch, M too large
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < M; i += (int64_t)gridDim.x * blockDim.x)
@@ -1739,6 +1764,7 @@ __global__ void k_runs_update(const int32_t *elist, const int32_t *ecount, int32
                               const int32_t *assign, const int64_t *wi, Runs r, unsigned long long *conn,
                               int64_t *pinbound, int32_t K, int32_t *ndirty, int32_t *nlist, int32_t *ncount,
                               int32_t *wide, int32_t *wide_count) {
+    pdl_entry();
     __shared__ int32_t sdelta[RU_SMEM_K];
     __shared__ int32_t s_oldp[8][128], s_oldc[8][128];
     const bool local = K <= RU_SMEM_K;
@@ -1859,6 +1885,7 @@ __global__ void __launch_bounds__(1024) k_runs_update_wide(const int32_t *wide, 
                                                            const int64_t *wi, Runs r, unsigned long long *conn,
                                                            int64_t *pinbound, int32_t *ndirty, int32_t *nlist,
                                                            int32_t *ncount) {
+    pdl_entry();
     extern __shared__ unsigned long long smem_u64[];
     uint32_t *sv = (uint32_t *)smem_u64;              // [kMaxSegSort] sorted parts
     int32_t *op = (int32_t *)(sv + kMaxSegSort);      // [kMaxSegSort] old parts
@@ -1963,6 +1990,7 @@ __global__ void __launch_bounds__(1024) k_runs_update_wide(const int32_t *wide, 
 __global__ void k_mark_psize(int32_t N, const int32_t *target, const uint8_t *fsens, const int32_t *fpart,
                              const uint8_t *pflags, const int64_t *psizes, const int32_t *size, int64_t omega,
                              int32_t *ndirty, int32_t *nlist, int32_t *ncount) {
+    pdl_entry();
     const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (n >= N) return;
     const int32_t t = target[n];
@@ -1978,6 +2006,7 @@ __global__ void k_mark_psize(int32_t N, const int32_t *target, const uint8_t *fs
 // the round's movers' h-edges (for the sequence gains and inbound events)
 __global__ void k_mover_edges(const int64_t *dM, const int32_t *node, const int64_t *inc_off, const int32_t *inc_dat,
                               int32_t *emflag, int32_t *mlist, int32_t *mcount, bool spec) {
+    pdl_entry();
     if (spec && *dM > kSpecCap) return;  // speculative launch, M too large
     grid_incidences(*dM, [&](int64_t i) { return node[i]; }, inc_off, inc_dat,
                     [&](int64_t, int32_t e) { push_once(&emflag[e], 1, e, mlist, mcount); });
@@ -1991,6 +2020,7 @@ __global__ void k_apply_inc(int64_t k, const int32_t *node, const int32_t *from,
                             int64_t *psizes, uint8_t *pflags, int32_t *edirty, int32_t *elist, int32_t *ecount,
                             int32_t *emflag, const int32_t *mlist, const int32_t *mcount, int32_t *ndirty,
                             int32_t *nlist, int32_t *ncount) {
+    pdl_entry();
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = tid; i < k; i += nt) {
         const int32_t n = node[i];
@@ -2008,11 +2038,13 @@ __global__ void k_apply_inc(int64_t k, const int32_t *node, const int32_t *from,
 }
 
 __global__ void k_project(int32_t N, const int32_t *gamma, const int32_t *coarse, int32_t *fine) {
+    pdl_entry();
     int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (v < N) fine[v] = coarse[gamma[v]];
 }
 
 __global__ void k_gamma_count(int32_t N, const int32_t *gamma, int32_t *ccount) {
+    pdl_entry();
     const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (n < N) atomicAdd(&ccount[gamma[n]], 1);
 }
@@ -2025,6 +2057,7 @@ __global__ void k_project_state(int32_t N, const int32_t *gamma, const int32_t *
                                 int32_t *target_f, int64_t *gain_f, uint8_t *fsens_f, int32_t *fpart_f,
                                 int32_t *ndirty_f, int32_t *nlist, int32_t *ncount,
                                 int32_t *splist, int32_t *spcount, int32_t *spfirst) {
+    pdl_entry();
     const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (n >= N) return;
     const int32_t g = gamma[n];
@@ -2057,6 +2090,7 @@ __global__ void k_project_state(int32_t N, const int32_t *gamma, const int32_t *
 __global__ void k_split_counts(const int32_t *splist, const int32_t *spcount, const int64_t *inc_off,
                                const int32_t *inc_dat, const int64_t *in_off, const int32_t *in_dat,
                                const int32_t *assign, Runs r) {
+    pdl_entry();
     const int n = *spcount;
     for (int t = blockIdx.x; t < n; t += gridDim.x) {
         const int32_t a = splist[2 * t], b = splist[2 * t + 1], P = assign[a];
@@ -2153,12 +2187,12 @@ void refine_project(Ctx &c, RefineState &st, const DLevel &fine, int32_t coarse_
     if (N > 0) {
         if (st.inc) {
             c.zero(st.ccount, std::max<int32_t>(1, coarse_n));
-            k_gamma_count<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(N, fine.gamma, st.ccount);
+            pdl_launch(k_gamma_count, (unsigned)cdiv(N, 256), 256, 0, c.stream, N, fine.gamma, st.ccount);
             DHGP_LAUNCHED(c);
             c.zero(st.ctr + CT_NLIST, 1);
             c.zero(st.ctr + CT_SPLIST, 1);
             c.fill_bytes(st.spfirst, 0xff, std::max<int32_t>(1, coarse_n));
-            k_project_state<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(
+            pdl_launch(k_project_state, (unsigned)cdiv(N, 256), 256, 0, c.stream, 
                 N, fine.gamma, st.ccount, assign, st.target, st.gain, st.fsens, st.fpart, st.ndirty, assign2,
                 st.target2, st.gain2, st.fsens2, st.fpart2, st.ndirty2, st.nlist, st.ctr + CT_NLIST, st.splist,
                 st.ctr + CT_SPLIST, st.spfirst);
@@ -2168,7 +2202,7 @@ void refine_project(Ctx &c, RefineState &st, const DLevel &fine, int32_t coarse_
             r.pc = st.rpc;
             r.cin = st.rcin;
             r.len = st.rlen;
-            k_split_counts<<<2 * c.num_sms, 256, 0, c.stream>>>(st.splist, st.ctr + CT_SPLIST, fine.inc_off,
+            pdl_launch(k_split_counts, 2 * c.num_sms, 256, 0, c.stream, st.splist, st.ctr + CT_SPLIST, fine.inc_off,
                                                                 fine.inc_dat, fine.in_off, fine.in_dat, assign2, r);
             DHGP_LAUNCHED(c);
             std::swap(st.target, st.target2);
@@ -2177,7 +2211,7 @@ void refine_project(Ctx &c, RefineState &st, const DLevel &fine, int32_t coarse_
             std::swap(st.fpart, st.fpart2);
             std::swap(st.ndirty, st.ndirty2);
         } else {
-            k_project<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(N, fine.gamma, assign, assign2);
+            pdl_launch(k_project, (unsigned)cdiv(N, 256), 256, 0, c.stream, N, fine.gamma, assign, assign2);
             DHGP_LAUNCHED(c);
         }
     }
@@ -2245,7 +2279,7 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
     long long *pdense = c.alloc<long long>((int64_t)pb_blocks * K);
     int32_t *ptouched = c.alloc<int32_t>((int64_t)pb_blocks * K);
     if (K > 0) {
-        k_fill_ll<<<(unsigned)cdiv((int64_t)pb_blocks * K, 256), 256, 0, c.stream>>>(pdense, -1ll,
+        pdl_launch(k_fill_ll, (unsigned)cdiv((int64_t)pb_blocks * K, 256), 256, 0, c.stream, pdense, -1ll,
                                                                                    (int64_t)pb_blocks * K);
         DHGP_LAUNCHED(c);
     }
@@ -2259,7 +2293,7 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
     static int g_ap = resident_grid(c, k_apply_inc, 256, 0);
     const bool wide_edges = max_edge_pins > 128;
     auto runs_update = [&](bool reset) {
-        k_runs_update<<<g_ru, 256, 0, c.stream>>>(st.elist, st.ctr + CT_ELIST, st.edirty, L.pin_off, L.pin_dat,
+        pdl_launch(k_runs_update, g_ru, 256, 0, c.stream, st.elist, st.ctr + CT_ELIST, st.edirty, L.pin_off, L.pin_dat,
                                                  L.dst_off, L.dst_dat, assign, W.wi, r, conn_d, pinbound, K, st.ndirty,
                                                  st.nlist, st.ctr + CT_NLIST, st.wide, st.ctr + CT_WIDE);
         DHGP_LAUNCHED(c);
@@ -2270,7 +2304,7 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
                                                (int)(13 * kMaxSegSort)));
                 wattr = true;
             }
-            k_runs_update_wide<<<c.num_sms, 1024, 13 * kMaxSegSort, c.stream>>>(
+            pdl_launch(k_runs_update_wide, c.num_sms, 1024, 13 * kMaxSegSort, c.stream, 
                 st.wide, st.ctr + CT_WIDE, st.edirty, L.pin_off, L.pin_dat, L.dst_off, L.dst_dat, assign, W.wi, r,
                 conn_d, pinbound, st.ndirty, st.nlist, st.ctr + CT_NLIST);
             DHGP_LAUNCHED(c);
@@ -2286,7 +2320,7 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
             build_runs(c, L, W, assign, r, tmp_parts, pinbound, K, conn_d, max_edge_pins);
             c.zero(psizes, K);
             if (N > 0) {
-                k_part_sizes<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(N, assign, L.size, psizes);
+                pdl_launch(k_part_sizes, (unsigned)cdiv(N, 256), 256, 0, c.stream, N, assign, L.size, psizes);
                 DHGP_LAUNCHED(c);
             }
         } else {
@@ -2295,7 +2329,7 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
             runs_update(false);
             const bool mp = st.moved && N > 0;
             if (mp) {
-                k_mark_psize<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(N, target, st.fsens, st.fpart, st.pflags,
+                pdl_launch(k_mark_psize, (unsigned)cdiv(N, 256), 256, 0, c.stream, N, target, st.fsens, st.fpart, st.pflags,
                                                                            psizes, L.size, omega, st.ndirty,
                                                                            st.nlist, st.ctr + CT_NLIST);
                 DHGP_LAUNCHED(c);
@@ -2347,28 +2381,26 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
                 if (narrow) {
                     static int g32 = resident_grid(c, k_propose_warp<unsigned>, PR_WARPS * 32, pr_smem<unsigned>());
                     int blocks = (int)std::min<int64_t>(cdiv(nmine, PR_WARPS), g32);
-                    k_propose_warp<unsigned><<<blocks, PR_WARPS * 32, pr_smem<unsigned>(), c.stream>>>(a);
+                    pdl_launch(k_propose_warp<unsigned>, blocks, PR_WARPS * 32, pr_smem<unsigned>(), c.stream, a);
                 } else {
                     static int g64 = resident_grid(c, k_propose_warp<unsigned long long>, PR_WARPS * 32,
                                                    pr_smem<unsigned long long>());
                     int blocks = (int)std::min<int64_t>(cdiv(nmine, PR_WARPS), g64);
-                    k_propose_warp<unsigned long long>
-                        <<<blocks, PR_WARPS * 32, pr_smem<unsigned long long>(), c.stream>>>(a);
+                    pdl_launch(k_propose_warp<unsigned long long>, blocks, PR_WARPS * 32, pr_smem<unsigned long long>(), c.stream, a);
                 }
                 DHGP_LAUNCHED(c);
                 // the dirty-node list is consumed; the mover count starts at zero
                 zero_many(c, {{full ? nullptr : (void *)(st.ctr + CT_NLIST), 4}, {dM, 8}});
                 KScope kh(c, "propose_heavy");
                 if (small_k) {
-                    k_hub_prefix<<<1, 1024, 0, c.stream>>>(st.hlist, ctr + 3, st.hub_max, L.inc_off, st.hpref);
+                    pdl_launch(k_hub_prefix, 1, 1024, 0, c.stream, st.hlist, ctr + 3, st.hub_max, L.inc_off, st.hpref);
                     DHGP_LAUNCHED(c);
                     if (narrow) {
                         static int h32 = resident_grid(c, k_propose_hub<unsigned>, 256, 4 * kSmallK);
-                        k_propose_hub<unsigned><<<h32, 256, 4 * K, c.stream>>>(a, st.hacc, st.htot, st.hdone);
+                        pdl_launch(k_propose_hub<unsigned>, h32, 256, 4 * K, c.stream, a, st.hacc, st.htot, st.hdone);
                     } else {
                         static int h64 = resident_grid(c, k_propose_hub<unsigned long long>, 256, 8 * kSmallK);
-                        k_propose_hub<unsigned long long>
-                            <<<h64, 256, 8 * K, c.stream>>>(a, st.hacc, st.htot, st.hdone);
+                        pdl_launch(k_propose_hub<unsigned long long>, h64, 256, 8 * K, c.stream, a, st.hacc, st.htot, st.hdone);
                     }
                     DHGP_LAUNCHED(c);
                     // few parts: the escalated nodes go straight to dense shared
@@ -2379,33 +2411,30 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
                     if (narrow) {
                         static int s32 = resident_grid(c, k_propose_heavy<unsigned, 256>, 256,
                                                        ph_smem<unsigned>(kSmallK));
-                        k_propose_heavy<unsigned, 256><<<s32, 256, ph_smem<unsigned>(K), c.stream>>>(b);
+                        pdl_launch(k_propose_heavy<unsigned, 256>, s32, 256, ph_smem<unsigned>(K), c.stream, b);
                     } else {
                         static int s64 = resident_grid(c, k_propose_heavy<unsigned long long, 256>, 256,
                                                        ph_smem<unsigned long long>(kSmallK));
-                        k_propose_heavy<unsigned long long, 256>
-                            <<<s64, 256, ph_smem<unsigned long long>(K), c.stream>>>(b);
+                        pdl_launch(k_propose_heavy<unsigned long long, 256>, s64, 256, ph_smem<unsigned long long>(K), c.stream, b);
                     }
                     DHGP_LAUNCHED(c);
                 } else {
                     // medium tier: reads the escalation count on device, exits when zero
                     if (narrow) {
                         static int m32 = resident_grid(c, k_propose_mid<unsigned>, PM_THREADS, pm_smem<unsigned>());
-                        k_propose_mid<unsigned><<<m32, PM_THREADS, pm_smem<unsigned>(), c.stream>>>(a);
+                        pdl_launch(k_propose_mid<unsigned>, m32, PM_THREADS, pm_smem<unsigned>(), c.stream, a);
                     } else {
                         static int m64 = resident_grid(c, k_propose_mid<unsigned long long>, PM_THREADS,
                                                        pm_smem<unsigned long long>());
-                        k_propose_mid<unsigned long long>
-                            <<<m64, PM_THREADS, pm_smem<unsigned long long>(), c.stream>>>(a);
+                        pdl_launch(k_propose_mid<unsigned long long>, m64, PM_THREADS, pm_smem<unsigned long long>(), c.stream, a);
                     }
                     DHGP_LAUNCHED(c);
                     if (narrow && K <= ph_maxk<unsigned>()) {
-                        k_propose_heavy<unsigned><<<c.num_sms, PH_THREADS, ph_smem<unsigned>(K), c.stream>>>(a);
+                        pdl_launch(k_propose_heavy<unsigned>, c.num_sms, PH_THREADS, ph_smem<unsigned>(K), c.stream, a);
                     } else if (!narrow && K <= ph_maxk<unsigned long long>()) {
-                        k_propose_heavy<unsigned long long>
-                            <<<c.num_sms, PH_THREADS, ph_smem<unsigned long long>(K), c.stream>>>(a);
+                        pdl_launch(k_propose_heavy<unsigned long long>, c.num_sms, PH_THREADS, ph_smem<unsigned long long>(K), c.stream, a);
                     } else {
-                        k_propose_block<<<pb_blocks, PB_THREADS, 0, c.stream>>>(a, pdense, ptouched);
+                        pdl_launch(k_propose_block, pb_blocks, PB_THREADS, 0, c.stream, a, pdense, ptouched);
                     }
                     DHGP_LAUNCHED(c);
                 }
@@ -2439,13 +2468,13 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
         if (packed) {
             if (N == 0) c.zero(dM, 1);
             if (N > 0) {
-                k_mover_compact<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(N, target, gain, W.wsum, mk, mv, pos,
+                pdl_launch(k_mover_compact, (unsigned)cdiv(N, 256), 256, 0, c.stream, N, target, gain, W.wsum, mk, mv, pos,
                                                                              (unsigned long long *)dM);
                 DHGP_LAUNCHED(c);
             }
         } else {
             if (N > 0) {
-                k_mover_flags<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(N, target, flags);
+                pdl_launch(k_mover_flags, (unsigned)cdiv(N, 256), 256, 0, c.stream, N, target, flags);
                 DHGP_LAUNCHED(c);
             }
             scan_excl<uint8_t>(c, flags, mpos, N);
@@ -2482,7 +2511,7 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
                     radix_sort_pairs(c, mk, mv, mkt, mvt, Mh, nullptr, gmax_bits + 32);
             } else {
                 if (N > 0) {
-                    k_mover_keys<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(N, flags, mpos, gain, W.wsum, mk, mv);
+                    pdl_launch(k_mover_keys, (unsigned)cdiv(N, 256), 256, 0, c.stream, N, flags, mpos, gain, W.wsum, mk, mv);
                     DHGP_LAUNCHED(c);
                 }
                 if (Mh <= kSmallSort)
@@ -2491,14 +2520,14 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
                     radix_sort_pairs(c, mk, mv, mkt, mvt, Mh, nullptr, gmax_bits);
                 fill_i32(c, pos, -1, N);
             }
-            k_build_moves_dn<<<(unsigned)std::max<int64_t>(1, cdiv(Mc, 256)), 256, 0, c.stream>>>(
+            pdl_launch(k_build_moves_dn, (unsigned)std::max<int64_t>(1, cdiv(Mc, 256)), 256, 0, c.stream, 
                 dM, mv, assign, target, gain, node, from, to, giso, pos, sp);
             DHGP_LAUNCHED(c);
             // h-edges holding a mover: the only ones with sequence-gain terms or
             // inbound events (incremental mode; the full mode scans every h-edge)
             const int32_t *elist = nullptr, *elist_n = nullptr;
             if (st.inc) {
-                k_mover_edges<<<g_me, 256, 0, c.stream>>>(dM, node, L.inc_off, L.inc_dat, st.emflag, st.mlist,
+                pdl_launch(k_mover_edges, g_me, 256, 0, c.stream, dM, node, L.inc_off, L.inc_dat, st.emflag, st.mlist,
                                                           st.ctr + CT_MLIST, sp);
                 DHGP_LAUNCHED(c);
                 elist = st.mlist;
@@ -2517,19 +2546,19 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
                 if (L.E > 0) {
                     static int g_re = resident_grid(c, k_round_edges, 256, 0);
                     const unsigned gre = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(L.E, 8), g_re));
-                    k_round_edges<<<gre, 256, 0, c.stream>>>(L.E, elist, elist_n, L.pin_off, L.pin_dat, L.dst_off,
+                    pdl_launch(k_round_edges, gre, 256, 0, c.stream, L.E, elist, elist_n, L.pin_off, L.pin_dat, L.dst_off,
                                                              L.dst_dat, W.wi, r, pos, from, to, gacc, ev, sg_big,
                                                              sg_ctr, big, ctr, tiers().edge_movers,
                                                              sp ? dM : nullptr);
                     DHGP_LAUNCHED(c);
-                    k_seq_gains_edge_block<<<c.num_sms, 256, 0, c.stream>>>(L.pin_off, L.pin_dat, W.wi, r, pos, from,
+                    pdl_launch(k_seq_gains_edge_block, c.num_sms, 256, 0, c.stream, L.pin_off, L.pin_dat, W.wi, r, pos, from,
                                                                              to, gacc, sg_big, sg_ctr, sg_ctr + 1);
                     DHGP_LAUNCHED(c);
-                    k_inbound_events_block<<<c.num_sms, 256, 0, c.stream>>>(L.dst_off, L.dst_dat, r, pos, from, to,
+                    pdl_launch(k_inbound_events_block, c.num_sms, 256, 0, c.stream, L.dst_off, L.dst_dat, r, pos, from, to,
                                                                              ev, big, ctr, ctr + 2);
                     DHGP_LAUNCHED(c);
                 }
-                k_round_moves<<<(unsigned)std::max<int64_t>(1, cdiv(Mc, 256)), 256, 0, c.stream>>>(
+                pdl_launch(k_round_moves, (unsigned)std::max<int64_t>(1, cdiv(Mc, 256)), 256, 0, c.stream, 
                     dM, node, from, to, L.size, ev, giso, gacc, gseq, sp);
                 DHGP_LAUNCHED(c);
             }
@@ -2539,7 +2568,7 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
             cum = c.alloc<int64_t>(Mc + 1);
             KScope ks(c, "select", 0.0, N);
             const bool packed_ev = 1 + ibits + pbits <= 32;
-            k_select_small<<<1, SEL_THREADS, sel_smem(), c.stream>>>(ecount, dM, ek, evv, gseq, psizes, pinbound,
+            pdl_launch(k_select_small, 1, SEL_THREADS, sel_smem(), c.stream, ecount, dM, ek, evv, gseq, psizes, pinbound,
                                                                     omega, delta, ibits, pbits, act_ex, sres,
                                                                     packed_ev);
             DHGP_LAUNCHED(c);
@@ -2597,12 +2626,12 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
                 int64_t *ex = c.alloc<int64_t>(T + 1), *gst = c.alloc<int64_t>(T), *sst = c.alloc<int64_t>(T);
                 c.zero(dlt, M + 1);
                 if (T > 0) {
-                    k_ev_prep<<<(unsigned)cdiv(T, 256), 256, 0, c.stream>>>((int64_t)T, ek, evv, ibits, gs, ss, dv);
+                    pdl_launch(k_ev_prep, (unsigned)cdiv(T, 256), 256, 0, c.stream, (int64_t)T, ek, evv, ibits, gs, ss, dv);
                     DHGP_LAUNCHED(c);
                     scan_excl<int64_t>(c, dv, ex, T);
                     scan_incl_max(c, gs, gst, T);
                     scan_incl_max(c, ss, sst, T);
-                    k_ev_toggle<<<(unsigned)cdiv(T, 256), 256, 0, c.stream>>>((int64_t)T, ek, ex, gst, sst, ibits,
+                    pdl_launch(k_ev_toggle, (unsigned)cdiv(T, 256), 256, 0, c.stream, (int64_t)T, ek, ex, gst, sst, ibits,
                                                                               pbits, psizes, pinbound, omega, delta,
                                                                               dlt);
                     DHGP_LAUNCHED(c);
@@ -2611,9 +2640,9 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
                 scan_excl<int64_t>(c, gseq, cum, M);        // cum[j] = sum of the first j gains
                 const int nb = (int)std::min<int64_t>(cdiv(M + 1, 256), 256);
                 long long *bv = c.alloc<long long>(nb), *bk = c.alloc<long long>(nb), *res = c.alloc<long long>(2);
-                k_best_prefix_partial<<<nb, 256, 0, c.stream>>>(M + 1, act_ex, cum, bv, bk);
+                pdl_launch(k_best_prefix_partial, nb, 256, 0, c.stream, M + 1, act_ex, cum, bv, bk);
                 DHGP_LAUNCHED(c);
-                k_best_prefix_final<<<1, 32, 0, c.stream>>>(nb, bv, bk, res);
+                pdl_launch(k_best_prefix_final, 1, 32, 0, c.stream, nb, bv, bk, res);
                 DHGP_LAUNCHED(c);
                 long long h2[2];
                 c.d2h(h2, res, 2);
@@ -2653,7 +2682,7 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
         }
         if (st.inc) {
             // apply + record the dirt; clears the mover-edge flags either way
-            k_apply_inc<<<g_ap, 256, 0, c.stream>>>(kbest, node, from, to, L.size, L.inc_off, L.inc_dat, assign,
+            pdl_launch(k_apply_inc, g_ap, 256, 0, c.stream, kbest, node, from, to, L.size, L.inc_off, L.inc_dat, assign,
                                                     psizes, st.pflags, st.edirty, st.elist, st.ctr + CT_ELIST,
                                                     st.emflag, st.mlist, st.ctr + CT_MLIST, st.ndirty, st.nlist,
                                                     st.ctr + CT_NLIST);
@@ -2661,7 +2690,7 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
             c.zero(st.ctr + CT_MLIST, 1);
             if (kbest > 0) st.moved = true;
         } else if (kbest > 0) {
-            k_apply<<<(unsigned)cdiv(kbest, 256), 256, 0, c.stream>>>(kbest, node, to, assign);
+            pdl_launch(k_apply, (unsigned)cdiv(kbest, 256), 256, 0, c.stream, kbest, node, to, assign);
             DHGP_LAUNCHED(c);
         }
         c.free(dlt);
@@ -2706,14 +2735,14 @@ void evaluate_assign(Ctx &c, const DLevel &L, const DWeights &W, const int32_t *
     c.zero(conn, 1);
     if (d_inbound) c.zero(d_inbound, K);
     if (L.E > 0) {
-        k_edge_runs<<<(unsigned)cdiv(L.E, 256), 256, 0, c.stream>>>(L.E, L.pin_off, tmp, L.dst_off, L.dst_dat, assign,
+        pdl_launch(k_edge_runs, (unsigned)cdiv(L.E, 256), 256, 0, c.stream, L.E, L.pin_off, tmp, L.dst_off, L.dst_dat, assign,
                                                                    W.wi, r, conn, d_inbound);
         DHGP_LAUNCHED(c);
     }
     if (d_sizes) {
         c.zero(d_sizes, K);
         if (L.N > 0) {
-            k_part_sizes<<<(unsigned)cdiv(L.N, 256), 256, 0, c.stream>>>(L.N, assign, L.size, d_sizes);
+            pdl_launch(k_part_sizes, (unsigned)cdiv(L.N, 256), 256, 0, c.stream, L.N, assign, L.size, d_sizes);
             DHGP_LAUNCHED(c);
         }
     }

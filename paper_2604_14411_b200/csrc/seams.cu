@@ -46,6 +46,7 @@ struct DevBuf {
 __global__ void k_fill_hist(int32_t N, const int64_t *inc_off, const int32_t *inc_dat, const int64_t *pin_off,
                             const int32_t *pin_dat, const double *w, const int64_t *nbr_off, const int32_t *nbr_dat,
                             double *hist) {
+    pdl_entry();
     const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
     const int lane = lane_id();
     for (int64_t n = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id(); n < N; n += nw) {
@@ -68,6 +69,7 @@ __global__ void k_select_first_valid(int32_t N, const int64_t *order, const int6
                                      const double *hist, const int32_t *size, const int64_t *in_off,
                                      const int32_t *in_dat, int64_t omega, int64_t delta, int32_t *pair,
                                      double *score) {
+    pdl_entry();
     int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (n >= N) return;
     pair[n] = -1;
@@ -89,6 +91,7 @@ __global__ void k_select_first_valid(int32_t N, const int64_t *order, const int6
 // ---- connectivity_value (_kernels.pyx:184-213) -----------------------------
 __global__ void k_edge_lambda(int32_t E, const int64_t *pin_off, const int32_t *sorted_parts, const double *w,
                               double *contrib) {
+    pdl_entry();
     int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= E) return;
     int64_t lam = 0;
@@ -98,6 +101,7 @@ __global__ void k_edge_lambda(int32_t E, const int64_t *pin_off, const int32_t *
 // the reference sums in ascending edge order; one thread keeps that order so
 // the result is bit-exact for non-integral weights as well
 __global__ void k_ordered_sum(int64_t n, const double *x, double *out) {
+    pdl_entry();
     if (threadIdx.x || blockIdx.x) return;
     double t = 0.0;
     for (int64_t i = 0; i < n; i++) t += x[i];
@@ -107,6 +111,7 @@ __global__ void k_ordered_sum(int64_t n, const double *x, double *out) {
 // ---- compute_pins (_kernels.pyx:216-231): thread per h-edge row -----------
 __global__ void k_dense_pins(int32_t E, const int64_t *off, const int32_t *dat, const int32_t *assign, int32_t K,
                              int32_t *pins) {
+    pdl_entry();
     int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= E) return;
     for (int64_t p = off[e]; p < off[e + 1]; p++) pins[e * (int64_t)K + assign[dat[p]]]++;
@@ -115,6 +120,7 @@ __global__ void k_dense_pins(int32_t E, const int64_t *off, const int32_t *dat, 
 // ---- propose_moves (_kernels.pyx:234-311): thread per node ----------------
 __global__ void k_node_work(int32_t N, const int64_t *inc_off, const int32_t *inc_dat, const int64_t *pin_off,
                             int64_t *work) {
+    pdl_entry();
     int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (n >= N) return;
     int64_t acc = 0;
@@ -126,6 +132,7 @@ __global__ void k_propose_dense(int32_t N, const int64_t *inc_off, const int32_t
                                 const int32_t *assign, const int64_t *psizes, const int32_t *size, int64_t omega,
                                 const int64_t *scratch_off, int32_t *cand, double *pres, int32_t *eparts,
                                 int32_t *target, double *gain) {
+    pdl_entry();
     int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (n >= N) return;
     target[n] = -1;
@@ -186,6 +193,7 @@ __global__ void k_seq_dense(int32_t M, const int64_t *inc_off, const int32_t *in
                             const int32_t *pin_dat, const double *w, const int32_t *pins, int32_t K,
                             const int32_t *node, const int32_t *from, const int32_t *to, const double *giso,
                             const int64_t *pos, double *out) {
+    pdl_entry();
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= M) return;
     const int32_t n = node[i], ps = from[i], pd = to[i];
@@ -219,6 +227,7 @@ __global__ void k_seq_dense(int32_t M, const int64_t *inc_off, const int32_t *in
 }
 
 __global__ void k_union_size(const int32_t *a, int64_t na, const int32_t *b, int64_t nb, unsigned long long *out) {
+    pdl_entry();
     int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k < nb && bsearch_dev(a, 0, na, b[k]) < 0) atomicAdd(out, 1ull);
 }
@@ -226,6 +235,7 @@ __global__ void k_union_size(const int32_t *a, int64_t na, const int32_t *b, int
 // ---- neighbours (coarsen.py:78-85): (node, pin) keys, radix-sorted ---------
 __global__ void k_nbr_count(int32_t N, const int64_t *inc_off, const int32_t *inc_dat, const int64_t *pin_off,
                             int64_t *cnt) {
+    pdl_entry();
     int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (n >= N) return;
     int64_t acc = 0;
@@ -234,6 +244,7 @@ __global__ void k_nbr_count(int32_t N, const int64_t *inc_off, const int32_t *in
 }
 __global__ void k_nbr_expand(int32_t N, const int64_t *inc_off, const int32_t *inc_dat, const int64_t *pin_off,
                              const int32_t *pin_dat, const int64_t *xoff, uint64_t *keys, uint32_t *vals) {
+    pdl_entry();
     int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (n >= N) return;
     int64_t o = xoff[n];
@@ -247,6 +258,7 @@ __global__ void k_nbr_expand(int32_t N, const int64_t *inc_off, const int32_t *i
     }
 }
 __global__ void k_nbr_keep(int64_t X, const uint64_t *keys, uint8_t *keep, int64_t *node_cnt) {
+    pdl_entry();
     int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= X) return;
     const uint64_t key = keys[k];
@@ -256,6 +268,7 @@ __global__ void k_nbr_keep(int64_t X, const uint64_t *keys, uint8_t *keep, int64
     if (kp) atomicAdd((unsigned long long *)&node_cnt[n], 1ull);
 }
 __global__ void k_nbr_write(int64_t X, const uint64_t *keys, const uint8_t *keep, const int64_t *kpos, int32_t *out) {
+    pdl_entry();
     int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k < X && keep[k]) out[kpos[k]] = (int32_t)(uint32_t)keys[k];
 }
@@ -293,6 +306,7 @@ __global__ void k_seam_select(int32_t M, int32_t K, const int64_t *in_off, const
                               const int32_t *node_size, const int32_t *node, const int32_t *from, const int32_t *to,
                               const double *gain_seq, int32_t *pins_in, int64_t *psize, int64_t *pinb, int64_t omega,
                               int64_t delta, int64_t *active, int64_t *k_out, double *total) {
+    pdl_entry();
     if (threadIdx.x || blockIdx.x) return;
     int64_t act = 0;
     active[0] = 0;
@@ -384,7 +398,7 @@ int dhgp_neighbors(const dhgp_graph *g, int32_t device, int64_t *nb_off, int32_t
     int64_t *cnt = c.alloc<int64_t>(N), *xoff = c.alloc<int64_t>((int64_t)N + 1);
     int64_t X = 0;
     if (N > 0) {
-        k_nbr_count<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(N, L.inc_off, L.inc_dat, L.pin_off, cnt);
+        pdl_launch(k_nbr_count, (unsigned)cdiv(N, 256), 256, 0, c.stream, N, L.inc_off, L.inc_dat, L.pin_off, cnt);
         DHGP_LAUNCHED(c);
     }
     scan_excl<int64_t>(c, cnt, xoff, N);
@@ -393,7 +407,7 @@ int dhgp_neighbors(const dhgp_graph *g, int32_t device, int64_t *nb_off, int32_t
     uint64_t *k = c.alloc<uint64_t>(X), *kt = c.alloc<uint64_t>(X);
     uint32_t *v = c.alloc<uint32_t>(X), *vt = c.alloc<uint32_t>(X);
     if (N > 0) {
-        k_nbr_expand<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(N, L.inc_off, L.inc_dat, L.pin_off, L.pin_dat,
+        pdl_launch(k_nbr_expand, (unsigned)cdiv(N, 256), 256, 0, c.stream, N, L.inc_off, L.inc_dat, L.pin_off, L.pin_dat,
                                                                   xoff, k, v);
         DHGP_LAUNCHED(c);
     }
@@ -402,7 +416,7 @@ int dhgp_neighbors(const dhgp_graph *g, int32_t device, int64_t *nb_off, int32_t
     int64_t *kpos = c.alloc<int64_t>(X + 1);
     c.zero(cnt, N);
     if (X > 0) {
-        k_nbr_keep<<<(unsigned)cdiv(X, 256), 256, 0, c.stream>>>(X, k, keep, cnt);
+        pdl_launch(k_nbr_keep, (unsigned)cdiv(X, 256), 256, 0, c.stream, X, k, keep, cnt);
         DHGP_LAUNCHED(c);
     }
     scan_excl<uint8_t>(c, keep, kpos, X);
@@ -411,7 +425,7 @@ int dhgp_neighbors(const dhgp_graph *g, int32_t device, int64_t *nb_off, int32_t
     c.sync();
     int32_t *out = c.alloc<int32_t>(nnz);
     if (X > 0) {
-        k_nbr_write<<<(unsigned)cdiv(X, 256), 256, 0, c.stream>>>(X, k, keep, kpos, out);
+        pdl_launch(k_nbr_write, (unsigned)cdiv(X, 256), 256, 0, c.stream, X, k, keep, kpos, out);
         DHGP_LAUNCHED(c);
     }
     scan_excl<int64_t>(c, cnt, xoff, N);
@@ -485,10 +499,10 @@ int dhgp_evaluate(const dhgp_graph *g, const int32_t *assign, int32_t num_parts,
         double *contrib = c.alloc<double>(L.E), *res = c.alloc<double>(1);
         seg_sort(c, L.E, L.pin_off, L.pin_dat, da.p, tmp);
         if (L.E > 0) {
-            k_edge_lambda<<<(unsigned)cdiv(L.E, 256), 256, 0, c.stream>>>(L.E, L.pin_off, tmp, in.w, contrib);
+            pdl_launch(k_edge_lambda, (unsigned)cdiv(L.E, 256), 256, 0, c.stream, L.E, L.pin_off, tmp, in.w, contrib);
             DHGP_LAUNCHED(c);
         }
-        k_ordered_sum<<<1, 32, 0, c.stream>>>(L.E, contrib, res);
+        pdl_launch(k_ordered_sum, 1, 32, 0, c.stream, L.E, contrib, res);
         DHGP_LAUNCHED(c);
         c.d2h(connectivity_out, res, 1);
         c.sync();
@@ -509,7 +523,7 @@ int dhgp_union_size_sorted(const int32_t *a, int64_t na, const int32_t *b, int64
     DevBuf<unsigned long long> r(c, 1);
     c.zero(r.p, 1);
     if (nb > 0) {
-        k_union_size<<<(unsigned)cdiv(nb, 256), 256, 0, c.stream>>>(da.p, na, db.p, nb, r.p);
+        pdl_launch(k_union_size, (unsigned)cdiv(nb, 256), 256, 0, c.stream, da.p, na, db.p, nb, r.p);
         DHGP_LAUNCHED(c);
     }
     unsigned long long h = 0;
@@ -529,7 +543,7 @@ int dhgp_fill_histograms(int32_t N, const int64_t *inc_off, const int32_t *inc_d
     DevBuf<double> dw(c, w, E), dh(c, nbr_off[N]);
     c.zero(dh.p, nbr_off[N]);
     if (N > 0) {
-        k_fill_hist<<<(unsigned)std::min<int64_t>(cdiv(N, 8), 4096), 256, 0, c.stream>>>(N, io.p, id.p, po.p, pd.p,
+        pdl_launch(k_fill_hist, (unsigned)std::min<int64_t>(cdiv(N, 8), 4096), 256, 0, c.stream, N, io.p, id.p, po.p, pd.p,
                                                                                       dw.p, no.p, nd.p, dh.p);
         DHGP_LAUNCHED(c);
     }
@@ -546,7 +560,7 @@ int dhgp_select_first_valid(int32_t N, const int64_t *order, const int64_t *nbr_
     DevBuf<int32_t> nd(c, nbr_dat, NB), sz(c, node_size, N), id(c, in_dat, in_off[N]), dp(c, N);
     DevBuf<double> dh(c, hist, NB), ds(c, N);
     if (N > 0) {
-        k_select_first_valid<<<(unsigned)cdiv(N, 128), 128, 0, c.stream>>>(N, dord.p, no.p, nd.p, dh.p, sz.p, io.p,
+        pdl_launch(k_select_first_valid, (unsigned)cdiv(N, 128), 128, 0, c.stream, N, dord.p, no.p, nd.p, dh.p, sz.p, io.p,
                                                                           id.p, max_size, max_inbound, dp.p, ds.p);
         DHGP_LAUNCHED(c);
     }
@@ -573,10 +587,10 @@ int dhgp_connectivity_value(int32_t E, const int64_t *pin_off, const int32_t *pi
     DevBuf<double> dw(c, w, E), contrib(c, E), res(c, 1);
     seg_sort(c, E, po.p, pd.p, da.p, tmp.p);
     if (E > 0) {
-        k_edge_lambda<<<(unsigned)cdiv(E, 256), 256, 0, c.stream>>>(E, po.p, tmp.p, dw.p, contrib.p);
+        pdl_launch(k_edge_lambda, (unsigned)cdiv(E, 256), 256, 0, c.stream, E, po.p, tmp.p, dw.p, contrib.p);
         DHGP_LAUNCHED(c);
     }
-    k_ordered_sum<<<1, 32, 0, c.stream>>>(E, contrib.p, res.p);
+    pdl_launch(k_ordered_sum, 1, 32, 0, c.stream, E, contrib.p, res.p);
     DHGP_LAUNCHED(c);
     res.get(out);
     SEAM_END
@@ -592,9 +606,9 @@ int dhgp_compute_pins(int32_t E, const int64_t *pin_off, const int32_t *pin_dat,
     c.zero(dpins.p, (int64_t)E * K);
     c.zero(dpin.p, (int64_t)E * K);
     if (E > 0) {
-        k_dense_pins<<<(unsigned)cdiv(E, 256), 256, 0, c.stream>>>(E, po.p, pd.p, da.p, K, dpins.p);
+        pdl_launch(k_dense_pins, (unsigned)cdiv(E, 256), 256, 0, c.stream, E, po.p, pd.p, da.p, K, dpins.p);
         DHGP_LAUNCHED(c);
-        k_dense_pins<<<(unsigned)cdiv(E, 256), 256, 0, c.stream>>>(E, dof.p, dd.p, da.p, K, dpin.p);
+        pdl_launch(k_dense_pins, (unsigned)cdiv(E, 256), 256, 0, c.stream, E, dof.p, dd.p, da.p, K, dpin.p);
         DHGP_LAUNCHED(c);
     }
     dpins.get(pins);
@@ -613,7 +627,7 @@ int dhgp_propose_moves(int32_t N, const int64_t *inc_off, const int32_t *inc_dat
     DevBuf<double> dw(c, w, E), dg(c, N);
     DevBuf<int64_t> work(c, N), woff(c, (int64_t)N + 1);
     if (N > 0) {
-        k_node_work<<<(unsigned)cdiv(N, 256), 256, 0, c.stream>>>(N, io.p, id.p, po.p, work.p);
+        pdl_launch(k_node_work, (unsigned)cdiv(N, 256), 256, 0, c.stream, N, io.p, id.p, po.p, work.p);
         DHGP_LAUNCHED(c);
     }
     scan_excl<int64_t>(c, work.p, woff.p, N);
@@ -623,7 +637,7 @@ int dhgp_propose_moves(int32_t N, const int64_t *inc_off, const int32_t *inc_dat
     DevBuf<int32_t> cand(c, X), ep(c, X);
     DevBuf<double> pres(c, X);
     if (N > 0) {
-        k_propose_dense<<<(unsigned)cdiv(N, 128), 128, 0, c.stream>>>(N, io.p, id.p, po.p, pd.p, dw.p, dpins.p, K, da.p,
+        pdl_launch(k_propose_dense, (unsigned)cdiv(N, 128), 128, 0, c.stream, N, io.p, id.p, po.p, pd.p, dw.p, dpins.p, K, da.p,
                                                                      ps.p, sz.p, max_size, woff.p, cand.p, pres.p,
                                                                      ep.p, dt.p, dg.p);
         DHGP_LAUNCHED(c);
@@ -643,7 +657,7 @@ int dhgp_sequence_gains(int32_t N, const int64_t *inc_off, const int32_t *inc_da
     DevBuf<int32_t> dn(c, node, M), df(c, from_part, M), dt(c, to_part, M);
     DevBuf<double> dw(c, w, E), dgi(c, gain_iso, M), dgs(c, M);
     if (M > 0) {
-        k_seq_dense<<<(unsigned)cdiv(M, 128), 128, 0, c.stream>>>(M, io.p, id.p, po.p, pd.p, dw.p, dpins.p, K, dn.p,
+        pdl_launch(k_seq_dense, (unsigned)cdiv(M, 128), 128, 0, c.stream, M, io.p, id.p, po.p, pd.p, dw.p, dpins.p, K, dn.p,
                                                                  df.p, dt.p, dgi.p, dpos.p, dgs.p);
         DHGP_LAUNCHED(c);
     }
@@ -664,7 +678,7 @@ int dhgp_build_events_and_select(int32_t N, const int64_t *in_off, const int32_t
     DevBuf<double> dg(c, gain_seq, M);
     DevBuf<int64_t> act(c, (int64_t)M + 1), res(c, 1);
     DevBuf<double> tot(c, 1);
-    k_seam_select<<<1, 1, 0, c.stream>>>(M, K, io.p, id.p, ns.p, dn.p, df.p, dt.p, dg.p, cnt.p, ps.p, pi.p, max_size,
+    pdl_launch(k_seam_select, 1, 1, 0, c.stream, M, K, io.p, id.p, ns.p, dn.p, df.p, dt.p, dg.p, cnt.p, ps.p, pi.p, max_size,
                                          max_inbound, act.p, res.p, tot.p);
     DHGP_LAUNCHED(c);
     act.get(active);
