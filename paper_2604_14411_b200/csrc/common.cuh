@@ -71,6 +71,10 @@ inline void pdl_launch(void (*kernel)(P...), dim3 grid, dim3 block, size_t smem,
     cfg.numAttrs = 1;
     DHGP_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<A>(args)...));
 }
+// byte fill / device copy as PDL kernels (prims.cu), so a cudaMemsetAsync /
+// cudaMemcpyAsync node does not break the launch overlap of the kernel chain
+void dev_fill(void *p, int byte, size_t bytes, cudaStream_t s);
+void dev_copy(void *dst, const void *src, size_t bytes, cudaStream_t s);
 
 // ---------------------------------------------------------------------------
 // execution context: one stream per call, stream-ordered pool allocations
@@ -130,11 +134,17 @@ struct Ctx {
     }
     template <class T>
     void zero(T *p, int64_t n) {
-        if (n > 0) DHGP_CUDA(cudaMemsetAsync(p, 0, (size_t)n * sizeof(T), stream));
+        if (n > 0) {
+            dev_fill(p, 0, (size_t)n * sizeof(T), stream);
+            launches++;
+        }
     }
     template <class T>
     void fill_bytes(T *p, int v, int64_t n) {
-        if (n > 0) DHGP_CUDA(cudaMemsetAsync(p, v, (size_t)n * sizeof(T), stream));
+        if (n > 0) {
+            dev_fill(p, v, (size_t)n * sizeof(T), stream);
+            launches++;
+        }
     }
     template <class T>
     void h2d(T *d, const T *h, int64_t n) {
@@ -155,7 +165,10 @@ struct Ctx {
     }
     template <class T>
     void d2d(T *dst, const T *src, int64_t n) {
-        if (n > 0) DHGP_CUDA(cudaMemcpyAsync(dst, src, (size_t)n * sizeof(T), cudaMemcpyDeviceToDevice, stream));
+        if (n > 0) {
+            dev_copy(dst, src, (size_t)n * sizeof(T), stream);
+            launches++;
+        }
     }
     // diagnostics: host time blocked in sync() and the number of syncs
     double sync_wait_ms = 0.0;

@@ -983,7 +983,37 @@ __global__ void k_zero_many(ZeroSet z) {
         ((uint32_t *)p)[i] = 0u;
     if (blockIdx.x == 0 && threadIdx.x < (nb & 3)) p[nw * 4 + threadIdx.x] = 0;
 }
+// 16-byte stores when both ends allow, bytes otherwise (sizes here are whole
+// elements of arena blocks, so the vector path is the common one)
+__global__ void k_fill(uint8_t *p, uint32_t word, size_t bytes) {
+    pdl_entry();
+    const size_t stride = (size_t)gridDim.x * blockDim.x, t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if ((((uintptr_t)p | bytes) & 15) == 0) {
+        const uint4 v = make_uint4(word, word, word, word);
+        for (size_t i = t; i < (bytes >> 4); i += stride) ((uint4 *)p)[i] = v;
+    } else {
+        for (size_t i = t; i < bytes; i += stride) p[i] = (uint8_t)word;
+    }
+}
+__global__ void k_copy(uint8_t *d, const uint8_t *s, size_t bytes) {
+    pdl_entry();
+    const size_t stride = (size_t)gridDim.x * blockDim.x, t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if ((((uintptr_t)d | (uintptr_t)s | bytes) & 15) == 0) {
+        for (size_t i = t; i < (bytes >> 4); i += stride) ((uint4 *)d)[i] = ((const uint4 *)s)[i];
+    } else {
+        for (size_t i = t; i < bytes; i += stride) d[i] = s[i];
+    }
+}
+unsigned fill_grid(size_t bytes) { return (unsigned)std::max<size_t>(1, std::min<size_t>((bytes / 16 + 255) / 256, 148 * 8)); }
 }  // namespace
+
+void dev_fill(void *p, int byte, size_t bytes, cudaStream_t s) {
+    const uint32_t w = (uint32_t)(byte & 0xff) * 0x01010101u;
+    pdl_launch(k_fill, fill_grid(bytes), 256, 0, s, (uint8_t *)p, w, bytes);
+}
+void dev_copy(void *dst, const void *src, size_t bytes, cudaStream_t s) {
+    pdl_launch(k_copy, fill_grid(bytes), 256, 0, s, (uint8_t *)dst, (const uint8_t *)src, bytes);
+}
 
 void zero_many(Ctx &c, std::initializer_list<std::pair<void *, int64_t>> bufs) {
     ZeroSet z;
