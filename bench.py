@@ -43,9 +43,15 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", default="C2")
-    ap.add_argument("--cpu-sample", default="2x1000", help="layers x width of the scaled CPU sample")
+    ap.add_argument("--config", default="C3", help="C1..C5 (SURVEY.md §8(d)); C3 is the north-star config")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--cpu-budget", type=float, default=30.0,
+                    help="our arm's cpu_baseline: wall budget (s) of the reference on the same workload")
+    ap.add_argument("--ref-total", type=float, default=1500.0,
+                    help="reference arm: total wall budget (s) over the K timed steps")
+    ap.add_argument("--ref-budget", type=float, default=None, help="reference arm: per-step budget (s)")
+    ap.add_argument("--ref-warmup-budget", type=float, default=2.0,
+                    help="reference arm: budget (s) of each untimed warm-up attempt")
     ap.add_argument("--min-units", type=int, default=None,
                     help="N>1: phases over fewer nodes/moves run replicated (library default 65536)")
     return ap.parse_args()
@@ -131,32 +137,19 @@ def host_graph(arrs):
 
 
 # ---------------------------------------------------------------------------
-# CPU baseline: reference on a bounded sample, scaled by pins processed
+# CPU baseline of our arm: the reference arm, one bounded attempt, in a child
+# process (keeps the reference out of this process)
 # ---------------------------------------------------------------------------
-def cpu_sample(spec: str, omega: int, delta: int, target_pin_work: int):
-    from oracle import ref_loader
-    from paper_2604_14411_b200 import workloads as W
-
-    ref = ref_loader.load()
-    layers, width = (int(x) for x in spec.split("x"))
-    n, w, so, sd, do, dd = W.layered_snn(layers, width)
-    g = ref.Hypergraph._from_csr(n, w, ref.CsrSets(so, sd), ref.CsrSets(do, dd))
-    t = time.perf_counter()
-    _, s = ref.partition(g, ref.Config(ref.Constraints(omega, delta), max_levels=1 << 20))
-    dt = time.perf_counter() - t
-    work = sum(lv["pins"] for lv in s.levels)
-    return {
-        "value": dt * target_pin_work / work,
-        "unit": "s",
-        "cores": 1,
-        "kind": "reference",
-        "sample": (f"reference partition() (compiled Cython backend, single-threaded) of the C2 recipe scaled to "
-                   f"{layers} layers x {width} neurons (same fan-out/window/Omega/Delta): {dt:.2f} s for "
-                   f"{len(s.levels)} levels / {work} level-pins; scaled linearly by level-pins to C2's "
-                   f"{target_pin_work} level-pins (an extrapolation; measured in this container the reference "
-                   f"needs 190 s for C2's first level alone)"),
-        "sample_seconds": dt,
-    }
+def cpu_baseline(args) -> dict:
+    cmd = [sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--config", args.config,
+           "--steps", "1", "--warmup", "0", "--ref-budget", str(args.cpu_budget)]
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=args.cpu_budget + 900)
+    line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    cb = dict(line["cpu_baseline"])
+    cb.update({"dnf": line["dnf"], "lower_bound": line["lower_bound"], "budget_s": line["budget_s"],
+               "levels_completed": line["levels_completed"], "extrapolated": line.get("extrapolated")})
+    return cb
 
 
 # ---------------------------------------------------------------------------
@@ -293,12 +286,10 @@ def run_ours(args, ws, rank, local):
     del keep
     if rank != 0:
         return
-    total_pin_work = int(sum(ref_out[4]))
     cpu = None
-    if not args.no_cpu:
+    if not args.no_cpu and ws == 1:
         try:
-            cpu = cpu_sample(args.cpu_sample, omega, delta, total_pin_work)
-            cpu.pop("sample_seconds", None)
+            cpu = cpu_baseline(args)
         except Exception as ex:  # reported, never fatal
             cpu = {"value": None, "unit": "s", "cores": 1, "kind": "reference", "sample": f"unavailable: {ex}"}
     n, w, so, sd, do, dd = arrs
@@ -338,51 +329,233 @@ def run_ours(args, ws, rank, local):
 # ---------------------------------------------------------------------------
 # reference arm: the reference's own CPU implementation (oracle/_ref)
 # ---------------------------------------------------------------------------
+def load_workloads_module():
+    """workloads.py by file path: the reference arm must not import this
+    repo's package (whose __init__ pulls in the libdhgp bindings)."""
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location("_bench_workloads",
+                                                  ROOT / "paper_2604_14411_b200" / "workloads.py")
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+def host_cpu() -> str:
+    try:
+        for ln in Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown cpu"
+
+
+def mem_available_bytes() -> int:
+    try:
+        for ln in Path("/proc/meminfo").read_text().splitlines():
+            if ln.startswith("MemAvailable:"):
+                return int(ln.split()[1]) * 1024
+    except OSError:
+        pass
+    return 32 << 30
+
+
+class RefRunner:
+    """Times the reference's ``partition(g, cfg)`` (driver.py:76-163; the
+    unmodified dhgpart package from oracle/_ref with its compiled Cython
+    backend) on an in-memory Hypergraph under a wall budget.
+
+    Each attempt runs in a forked child (the parent keeps the constructed
+    Hypergraph, so no attempt pays for input construction).  The child
+    reports its start, every coarsening level and refinement level it
+    completes (through the reference's observer), and its finish, over a
+    pipe; the parent SIGKILLs it at the budget.  A child address-space cap
+    (75% of MemAvailable) turns a memory blow-up into a reported failure
+    instead of an out-of-memory host.  The reference is single-threaded
+    (Cython nogil without prange), so one core per attempt."""
+
+    def __init__(self, dp, arrs, omega, delta, max_rounds=8):
+        n, w, so, sd, do, dd = arrs
+        t = time.perf_counter()
+        self.dp = dp
+        self.g = dp.Hypergraph._from_csr(n, w, dp.CsrSets(so, sd), dp.CsrSets(do, dd))
+        self.build_s = time.perf_counter() - t
+        self.cfg = dp.Config(dp.Constraints(omega, delta), max_rounds=max_rounds, max_levels=1 << 20)
+        self.mem_cap = int(0.75 * mem_available_bytes())
+
+    def _child(self, wfd):
+        import resource
+
+        def send(msg):
+            os.write(wfd, (msg + "\n").encode())
+
+        try:
+            resource.setrlimit(resource.RLIMIT_AS, (self.mem_cap, self.mem_cap))
+            seen = {"level": 0, "round": 0, "rlevels": set()}
+
+            def obs(kind, p):
+                if kind == "level":
+                    seen["level"] += 1
+                    send(f"L {time.monotonic():.6f} {p['index']} {p['coarse'].num_nodes}")
+                else:
+                    seen["round"] += 1
+                    send(f"R {time.monotonic():.6f} {p['level']} {p['round']}")
+
+            send(f"S {time.monotonic():.6f}")
+            part, st = self.dp.partition(self.g, self.cfg, observer=obs)
+            send(f"D {time.monotonic():.6f} {len(st.levels)} {part.num_parts} {st.connectivity_trace[-1][-1]!r}")
+        except MemoryError:
+            send(f"M {time.monotonic():.6f}")
+        except BaseException as ex:  # noqa: BLE001 - reported to the parent
+            send(f"E {time.monotonic():.6f} {type(ex).__name__}: {ex}".replace("\n", " ")[:300])
+        finally:
+            os._exit(0)
+
+    def attempt(self, budget_s: float) -> dict:
+        import select
+        import signal
+
+        rfd, wfd = os.pipe()
+        pid = os.fork()
+        if pid == 0:
+            os.close(rfd)
+            self._child(wfd)
+        os.close(wfd)
+        buf, start, end, status = b"", None, None, "running"
+        levels = rounds = 0
+        last_level, result, detail = None, None, ""
+        t_fork = time.monotonic()
+        while True:
+            deadline = (start if start is not None else t_fork) + budget_s
+            timeout = deadline - time.monotonic()
+            if timeout <= 0:
+                break
+            r, _, _ = select.select([rfd], [], [], min(timeout, 1.0))
+            if not r:
+                continue
+            chunk = os.read(rfd, 1 << 16)
+            if not chunk:
+                break
+            buf += chunk
+            while b"\n" in buf:
+                line, buf = buf.split(b"\n", 1)
+                f = line.decode().split(" ", 2)
+                tag, ts = f[0], float(f[1])
+                if tag == "S":
+                    start = ts
+                elif tag == "L":
+                    levels += 1
+                    last_level = f[2]
+                elif tag == "R":
+                    rounds += 1
+                elif tag in ("D", "M", "E"):
+                    end, status = ts, {"D": "done", "M": "memory", "E": "error"}[tag]
+                    result = f[2] if len(f) > 2 else None
+            if status != "running":
+                break
+        if status == "running":
+            os.kill(pid, signal.SIGKILL)
+            status = "budget"
+        os.waitpid(pid, 0)
+        os.close(rfd)
+        if start is None:
+            start = t_fork
+        elapsed = (end if end is not None else time.monotonic()) - start
+        if status == "done":
+            detail = result
+        elif status in ("memory", "error"):
+            detail = result or ""
+        return {"status": status, "seconds": min(elapsed, budget_s) if status == "budget" else elapsed,
+                "levels_completed": levels, "rounds_completed": rounds, "last_level": last_level, "detail": detail}
+
+
 def run_reference(args, ws, rank, local):
+    """The reference arm (task ④): rank 0 only; the other ranks exit 0.
+
+    Every timed step is one attempt at the WHOLE workload (the same config
+    as our arm) under a per-step wall budget sized so the K timed steps fit
+    the driver's limit.  When the reference does not finish inside the
+    budget (C3: it needs days), the step's value is the budget
+    itself, flagged ``dnf`` — a measured lower bound on the reference's
+    time, so the driver's ratio is a lower bound on the speed-up.  A
+    labelled extrapolation from measured per-level reference times sits in
+    a separate field and is never the value."""
     if rank != 0:
         return
-    arrs, omega, delta, desc = build_workload(args.config)
+    from oracle import ref_loader
+
+    W = load_workloads_module()
+    dp = ref_loader.load()
+    arrs, omega, delta, desc = W.make_config(args.config)
     n, w, so, sd, do, dd = arrs
-    # level-pins of the full workload: from the level schedule of one GPU run
-    # when a GPU is present (bit-identical to the reference's by parity), else
-    # the level-0 pins as a floor.
-    total = None
-    try:
-        import ctypes as C
-
-        from paper_2604_14411_b200 import _lib
-        import paper_2604_14411_b200 as dp
-
-        _lib.load()
-        g = host_graph(arrs)
-        _, st = dp.partition(g, dp.Config(dp.Constraints(omega, delta), max_levels=1 << 20))
-        total = sum(lv["pins"] for lv in st.levels)
-    except Exception:
-        total = int(len(sd) + len(dd))
-    vals = []
-    samp = None
-    for i in range(args.warmup + args.steps):
-        s = cpu_sample(args.cpu_sample, omega, delta, total)
-        if i >= args.warmup:
-            vals.append(s["value"])
-            samp = s
-    v = float(np.mean(vals))
+    budget = args.ref_budget if args.ref_budget else max(10.0, min(600.0, args.ref_total / max(1, args.steps)))
+    runner = RefRunner(dp, arrs, omega, delta)
+    for _ in range(args.warmup):  # untimed: exercises the fork/observer path on the built graph
+        runner.attempt(min(budget, args.ref_warmup_budget))
+    steps = [runner.attempt(budget) for _ in range(args.steps)]
+    v = float(np.mean([s["seconds"] for s in steps]))
+    dnf = any(s["status"] != "done" for s in steps)
+    best = max(steps, key=lambda s: (s["levels_completed"], s["rounds_completed"]))
+    sample = (f"reference dhgpart.partition(g, cfg) (oracle/_ref: the unmodified package, compiled Cython "
+              f"backend, single-threaded) on the full {args.config} workload, {args.steps} attempts under a "
+              f"{budget:.0f} s wall budget each; " +
+              ("finished every attempt" if not dnf else
+               f"did NOT finish (reached {best['levels_completed']} coarsening levels, "
+               f"{best['rounds_completed']} refinement rounds; " +
+               ("stopped at the budget: value is the budget, a measured lower bound" if best["status"] == "budget"
+                else f"stopped by {best['status']} ({best['detail'] or 'address-space cap '} "
+                     f"{runner.mem_cap / 2**30:.0f} GiB) after the value's seconds: a lower bound") + ")"))
     line = {
         "impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "s", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(v * 1e3, 1), "higher_is_better": False,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "weak" if ws > 1 else "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{args.config}: {desc}", "nodes": int(n), "h_edges": int(len(w)),
                    "pins": int(len(sd) + len(dd)), "max_size": omega, "max_inbound": delta},
-        "cpu_baseline": {"value": round(v, 3), "unit": "s", "cores": 1, "kind": "reference",
-                         "sample": samp["sample"]},
+        "dnf": dnf, "lower_bound": dnf, "budget_s": round(budget, 1),
+        "levels_completed": best["levels_completed"], "rounds_completed": best["rounds_completed"],
+        "attempts": [{k: (round(v2, 3) if isinstance(v2, float) else v2) for k, v2 in s.items()} for s in steps],
+        "graph_build_s": round(runner.build_s, 2),
+        "cpu_baseline": {"value": round(v, 3), "unit": "s", "cores": 1, "kind": "reference", "sample": sample,
+                         "host": f"{host_cpu()}; {os.cpu_count()} logical cpus; 1 used (single-threaded)"},
         "e2e": {"value": round(v, 3), "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "extrapolated": reference_extrapolation(args.config),
     }
     print(json.dumps(line), flush=True)
+
+
+def reference_extrapolation(config: str):
+    """A LABELLED estimate of the reference's full time, from the committed
+    per-level measurements of the reference itself (profiles/
+    reference_levels_<config>.json).  Never used as a value."""
+    p = ROOT / "profiles" / f"reference_levels_{config}.json"
+    if not p.exists():
+        return None
+    d = json.loads(p.read_text())
+    return {k: d[k] for k in ("value", "unit", "basis") if k in d}
+
+
+def spawn_ranks(args) -> int:
+    """``bench.py --gpus N`` (N > 1) without a torchrun environment: launch
+    the N ranks ourselves, one process per GPU, exactly as the driver's
+    torchrun line would, and pass rank 0's JSON line through."""
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(ROOT / "bench.py")] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
     args = parse_args()
     ws, rank, local = dist_env()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
+    if ws > 1 and ws != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={ws}")
     if args.impl == "reference":
         run_reference(args, ws, rank, local)
     else:

@@ -19,6 +19,7 @@ from __future__ import annotations
 import argparse
 import ctypes as C
 import json
+import os
 import sys
 import time
 from collections import defaultdict
@@ -91,51 +92,89 @@ def gpu_run_sampled(g, omega, delta, coarsen_levels, refine_levels, max_rounds=8
     return stats, graphs, level_ev, rounds
 
 
-def check_config(name, coarsen_levels, refine_levels, log=print):
-    import paper_2604_14411_b200 as dp
+_JOBS: list = []  # (kind, level, args) set before the pool forks; workers get an index
+
+
+def _replay(i):
     from oracle import oracle as orc
+
+    kind, lv, args, kw = _JOBS[i]
+    t = time.time()
+    out = orc.coarsen_level(*args, **kw) if kind == "c" else orc.refine_level(*args, **kw)
+    return i, out, time.time() - t
+
+
+def auto_levels(nlev: int):
+    """Early levels (where the full / block / dense scoring tiers run on the
+    most nodes) plus levels spread to the tail."""
+    co = {0, 1, 2, 8, 32} | {int(round(x)) for x in np.linspace(64, nlev - 2, 6)}
+    re = {0, 1, nlev // 2, nlev - 2, nlev - 1}
+    return sorted(x for x in co if 0 <= x < nlev - 1), sorted(x for x in re if 0 <= x < nlev)
+
+
+def check_config(name, coarsen_levels, refine_levels, log=print, procs=None):
+    import multiprocessing as mp
+
+    import paper_2604_14411_b200 as dp
     from paper_2604_14411_b200 import workloads as W
 
     arrs, omega, delta, desc = W.make_config(name)
     n, w, so, sd, do, dd = arrs
     g = dp.Hypergraph._from_csr(n, w, dp.CsrSets(so, sd), dp.CsrSets(do, dd))
+    if coarsen_levels is None or refine_levels is None:  # auto: needs the level count first
+        _, st0 = dp.partition(g, dp.Config(dp.Constraints(omega, delta), max_levels=1 << 20))
+        ac, ar = auto_levels(len(st0.levels))
+        coarsen_levels = ac if coarsen_levels is None else coarsen_levels
+        refine_levels = ar if refine_levels is None else refine_levels
     t0 = time.time()
     stats, graphs, level_ev, rounds = gpu_run_sampled(g, omega, delta, coarsen_levels, refine_levels)
     nlev = len(stats.levels)
     out = {"config": name, "desc": desc, "levels": nlev, "gpu_run_s": round(time.time() - t0, 2),
            "coarsen": [], "refine": []}
+    _JOBS.clear()
     for lv in sorted(coarsen_levels):
-        if lv >= nlev - 1:
-            continue
-        gl = graphs[lv]
-        t = time.time()
-        ref = orc.coarsen_level(gl[0], w, gl[1], gl[2], gl[3], gl[4], gl[5], max_size=omega, max_inbound=delta)
-        mine = level_ev[lv]
-        ok = ref is not None and all(np.array_equal(ref[k], mine[k]) for k in ("pair", "score", "match", "gamma"))
-        c = mine["coarse"]
-        ok = ok and ref["num_coarse"] == c[0] and all(
-            np.array_equal(ref[k], v) for k, v in zip(("src_off", "src_dat", "dst_off", "dst_dat", "node_size"), c[1:]))
-        rec = {"level": lv, "nodes": int(gl[0]), "pins": int(len(gl[2]) + len(gl[4])), "coarse_nodes": int(c[0]),
-               "bit_exact": bool(ok), "oracle_s": round(time.time() - t, 2)}
-        out["coarsen"].append(rec)
-        log(json.dumps(rec))
+        if lv < nlev - 1:
+            gl = graphs[lv]
+            _JOBS.append(("c", lv, (gl[0], w, gl[1], gl[2], gl[3], gl[4], gl[5]),
+                          dict(max_size=omega, max_inbound=delta)))
     for lv in sorted(refine_levels):
-        if lv >= nlev or not rounds.get(lv):
-            continue
+        if lv < nlev and rounds.get(lv):
+            gl = graphs[lv]
+            _JOBS.append(("r", lv, (gl[0], w, gl[1], gl[2], gl[3], gl[4], gl[5], rounds[lv][0]["assign"],
+                                    rounds[lv][0]["num_parts"]), dict(max_size=omega, max_inbound=delta, level=lv)))
+    procs = procs or max(1, min(len(_JOBS), (os.cpu_count() or 2) - 1))
+    results = {}
+    # largest levels first so the pool's tail is short
+    order = sorted(range(len(_JOBS)), key=lambda i: -len(_JOBS[i][2][2]) - len(_JOBS[i][2][4]))
+    with mp.get_context("fork").Pool(procs) as pool:
+        for i, res, secs in pool.imap_unordered(_replay, order):
+            results[i] = (res, secs)
+    for i, (kind, lv, args, _) in enumerate(_JOBS):
+        ref, secs = results[i]
         gl = graphs[lv]
-        rs = rounds[lv]
-        t = time.time()
-        a, conns, evs = orc.refine_level(gl[0], w, gl[1], gl[2], gl[3], gl[4], gl[5], rs[0]["assign"],
-                                         rs[0]["num_parts"], max_size=omega, max_inbound=delta, level=lv)
-        ok = len(evs) == len(rs)
-        for e, r in zip(evs, rs):
-            ok = ok and e["k"] == r["k"] and e["total_gain"] == r["total_gain"] and all(
-                np.array_equal(e[k], r[k]) for k in ("assign", "node", "from_part", "to_part", "gain_iso",
-                                                     "gain_seq", "active"))
-        ok = ok and conns == stats.connectivity_trace[nlev - 1 - lv]
-        rec = {"level": lv, "nodes": int(gl[0]), "rounds": len(rs), "moves": int(sum(len(r["node"]) for r in rs)),
-               "bit_exact": bool(ok), "oracle_s": round(time.time() - t, 2)}
-        out["refine"].append(rec)
+        if kind == "c":
+            mine = level_ev[lv]
+            ok = ref is not None and all(np.array_equal(ref[k], mine[k]) for k in ("pair", "score", "match", "gamma"))
+            c = mine["coarse"]
+            ok = ok and ref["num_coarse"] == c[0] and all(
+                np.array_equal(ref[k], v)
+                for k, v in zip(("src_off", "src_dat", "dst_off", "dst_dat", "node_size"), c[1:]))
+            rec = {"level": lv, "nodes": int(gl[0]), "pins": int(len(gl[2]) + len(gl[4])),
+                   "coarse_nodes": int(c[0]), "pairs": int(np.sum(mine["match"] != np.arange(gl[0])) // 2),
+                   "bit_exact": bool(ok), "oracle_s": round(secs, 2)}
+            out["coarsen"].append(rec)
+        else:
+            a, conns, evs = ref
+            rs = rounds[lv]
+            ok = len(evs) == len(rs)
+            for e, r in zip(evs, rs):
+                ok = ok and e["k"] == r["k"] and e["total_gain"] == r["total_gain"] and all(
+                    np.array_equal(e[k], r[k]) for k in ("assign", "node", "from_part", "to_part", "gain_iso",
+                                                         "gain_seq", "active"))
+            ok = ok and conns == stats.connectivity_trace[nlev - 1 - lv]
+            rec = {"level": lv, "nodes": int(gl[0]), "rounds": len(rs),
+                   "moves": int(sum(len(r["node"]) for r in rs)), "bit_exact": bool(ok), "oracle_s": round(secs, 2)}
+            out["refine"].append(rec)
         log(json.dumps(rec))
     return out
 
@@ -143,12 +182,15 @@ def check_config(name, coarsen_levels, refine_levels, log=print):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("config")
-    ap.add_argument("--coarsen", default="")
-    ap.add_argument("--refine", default="")
+    ap.add_argument("--coarsen", default="auto", help="comma list of levels, or 'auto'")
+    ap.add_argument("--refine", default="auto", help="comma list of levels, or 'auto'")
+    ap.add_argument("--head", default=None, help="commit the product code was built from (recorded)")
+    ap.add_argument("--procs", type=int, default=None, help="oracle replays in parallel (fork)")
     ap.add_argument("--json", default=None)
     a = ap.parse_args()
-    lv = lambda s: [int(x) for x in s.split(",") if x != ""]  # noqa: E731
-    out = check_config(a.config, lv(a.coarsen), lv(a.refine))
+    lv = lambda s: None if s == "auto" else [int(x) for x in s.split(",") if x != ""]  # noqa: E731
+    out = check_config(a.config, lv(a.coarsen), lv(a.refine), procs=a.procs)
+    out["head"] = a.head
     print(json.dumps({k: v for k, v in out.items() if k not in ("coarsen", "refine")}))
     if a.json:
         Path(a.json).write_text(json.dumps(out, indent=1))
