@@ -21,7 +21,7 @@
 namespace dhgp {
 
 void seams_setup(Ctx &c, int device);
-extern std::mutex g_mu;
+std::recursive_mutex &device_mutex(int device);
 
 namespace {
 
@@ -216,7 +216,7 @@ extern "C" {
 
 int dhgp_baseline(const dhgp_graph *g, int64_t max_size, int64_t max_inbound, int32_t method, int32_t device,
                   int32_t *assign_out, int32_t *num_parts_out) {
-    std::lock_guard<std::mutex> lk(g_mu);
+    std::lock_guard<std::recursive_mutex> lk(device_mutex(device));
     try {
         Ctx c;
         seams_setup(c, device);

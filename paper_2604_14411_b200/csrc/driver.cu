@@ -97,9 +97,13 @@ void Ctx::flush_profile() {
 }
 
 // ---------------------------------------------------------------------------
-// device setup: one cached stream per device (memory: the arena above)
+// one in-flight call per device: calls on different devices run concurrently;
+// the mutex is recursive so that an observer (run on the calling thread while
+// the partition is paused at a synchronised point) may call back into the
+// library, as the reference allows (its observer gets live objects).
 // ---------------------------------------------------------------------------
-std::mutex g_mu;
+static std::recursive_mutex g_dev_mu[65];
+std::recursive_mutex &device_mutex(int device) { return g_dev_mu[(device >= 0 && device < 64) ? device : 64]; }
 
 // ---------------------------------------------------------------------------
 // device arena (common.cuh)
@@ -295,6 +299,17 @@ static void run_partition(Ctx &c, const DInput &in, const dhgp_config &cfg, Part
     // check_feasibility order (hgraph.py:382-401)
     if (omega < 1) throw Error{DHGP_ERR_INFEASIBLE, "max_size must be >= 1, got " + std::to_string(omega)};
     if (delta < 0) throw Error{DHGP_ERR_INFEASIBLE, "max_inbound must be >= 0, got " + std::to_string(delta)};
+    const int32_t N0 = in.N;
+    {
+        int32_t bs, bi, sz = 0, deg = 0;
+        feasibility_input(c, in, omega, delta, &bs, &bi, &sz, &deg);
+        if (bs >= 0)
+            throw Error{DHGP_ERR_INFEASIBLE, "node " + std::to_string(bs) + " has size " + std::to_string(sz) +
+                                                 " > max_size " + std::to_string(omega)};
+        if (bi >= 0)
+            throw Error{DHGP_ERR_INFEASIBLE, "node " + std::to_string(bi) + " has " + std::to_string(deg) +
+                                                 " inbound edges > max_inbound " + std::to_string(delta)};
+    }
     if (in.max_edge_pins > kMaxSegSort)
         throw Error{DHGP_ERR_UNSUPPORTED, "h-edge with " + std::to_string(in.max_edge_pins) +
                                               " pin slots exceeds the supported maximum " +
@@ -310,29 +325,6 @@ static void run_partition(Ctx &c, const DInput &in, const dhgp_config &cfg, Part
     std::vector<DLevel> levels(1);
     build_level0(c, in, levels[0]);
 
-    const int32_t N0 = in.N;
-    if (N0 > 0) {
-        int32_t bs, bi;
-        feasibility(c, levels[0], omega, delta, &bs, &bi);
-        if (bs >= 0) {
-            int32_t sz;
-            c.d2h(&sz, levels[0].size + bs, 1);
-            c.sync();
-            levels[0].release(c);
-            W.release(c);
-            throw Error{DHGP_ERR_INFEASIBLE, "node " + std::to_string(bs) + " has size " + std::to_string(sz) +
-                                                 " > max_size " + std::to_string(omega)};
-        }
-        if (bi >= 0) {
-            int64_t o[2];
-            c.d2h(o, levels[0].in_off + bi, 2);
-            c.sync();
-            levels[0].release(c);
-            W.release(c);
-            throw Error{DHGP_ERR_INFEASIBLE, "node " + std::to_string(bi) + " has " + std::to_string(o[1] - o[0]) +
-                                                 " inbound edges > max_inbound " + std::to_string(delta)};
-        }
-    }
     const double t0 = now_ms();
     c.sync_wait_ms = 0.0;
     c.syncs = 0;
@@ -663,8 +655,8 @@ struct dhgp_session {
     std::vector<KernelStat> kstats;
 };
 
-#define DHGP_GUARD_BEGIN \
-    std::lock_guard<std::mutex> _lk(g_mu); \
+#define DHGP_GUARD_BEGIN(dev) \
+    std::lock_guard<std::recursive_mutex> _lk(device_mutex(dev)); \
     try {
 #define DHGP_GUARD_END                      \
     }                                       \
@@ -708,7 +700,7 @@ int dhgp_device_count(int32_t *count) {
 
 static int partition_impl(const dhgp_graph *g, const dhgp_config *cfg, dhgp_comm *cm, int32_t *assign_out,
                           int32_t *num_parts_out, dhgp_stats *stats_out, dhgp_observer_fn obs, void *user) {
-    DHGP_GUARD_BEGIN
+    DHGP_GUARD_BEGIN(cfg ? cfg->device : 0)
     check_graph(g);
     Ctx c;
     setup(c, cfg->device);
@@ -757,7 +749,7 @@ void dhgp_stats_free(dhgp_stats *s) {
 }
 
 int dhgp_session_create(const dhgp_graph *g, int32_t device, dhgp_session **out) {
-    DHGP_GUARD_BEGIN
+    DHGP_GUARD_BEGIN(device)
     check_graph(g);
     Ctx c;
     setup(c, device);
@@ -771,7 +763,7 @@ int dhgp_session_create(const dhgp_graph *g, int32_t device, dhgp_session **out)
 
 int dhgp_session_partition(dhgp_session *s, const dhgp_config *cfg, int32_t *assign_out, int32_t *num_parts_out,
                            dhgp_stats *stats_out) {
-    DHGP_GUARD_BEGIN
+    DHGP_GUARD_BEGIN(s->device)
     Ctx c;
     setup(c, s->device);
     c.comm = comm_of(s->comm);
@@ -803,7 +795,7 @@ int dhgp_session_partition(dhgp_session *s, const dhgp_config *cfg, int32_t *ass
 
 void dhgp_session_destroy(dhgp_session *s) {
     if (!s) return;
-    std::lock_guard<std::mutex> lk(g_mu);
+    std::lock_guard<std::recursive_mutex> lk(device_mutex(s->device));
     try {
         Ctx c;
         setup(c, s->device);

@@ -57,6 +57,19 @@ __global__ void k_feasible(int32_t N, const int32_t *size, const int64_t *in_off
     if ((int64_t)size[n] > omega) atomicMin(&bad[0], (int32_t)n);
     if (in_off[n + 1] - in_off[n] > delta) atomicMin(&bad[1], (int32_t)n);
 }
+__global__ void k_indegree(int64_t Pd, const int32_t *dst_dat, int32_t *deg) {
+    pdl_entry();
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < Pd; i += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(&deg[dst_dat[i]], 1);
+}
+__global__ void k_feasible_deg(int32_t N, const int32_t *size, const int32_t *deg, int64_t omega, int64_t delta,
+                               int32_t *bad) {
+    pdl_entry();
+    int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (n >= N) return;
+    if ((int64_t)size[n] > omega) atomicMin(&bad[0], (int32_t)n);
+    if ((int64_t)deg[n] > delta) atomicMin(&bad[1], (int32_t)n);
+}
 }  // namespace
 
 void upload_input(Ctx &c, const dhgp_graph &g, DInput &in) {
@@ -190,6 +203,32 @@ void feasibility(Ctx &c, const DLevel &L, int64_t omega, int64_t delta, int32_t 
     c.free(bad);
     *bad_size = h[0] == 0x7fffffff ? -1 : h[0];
     *bad_in = h[1] == 0x7fffffff ? -1 : h[1];
+}
+
+void feasibility_input(Ctx &c, const DInput &in, int64_t omega, int64_t delta, int32_t *bad_size, int32_t *bad_in,
+                       int32_t *size_val, int32_t *indeg_val) {
+    *bad_size = *bad_in = -1;
+    if (in.N <= 0) return;
+    int32_t *deg = c.alloc<int32_t>((int64_t)in.N + 2);
+    int32_t *bad = deg + in.N;
+    c.zero(deg, in.N);
+    fill_i32(c, bad, 0x7fffffff, 2);
+    if (in.Pd > 0) {
+        pdl_launch(k_indegree, (unsigned)std::min<int64_t>(cdiv(in.Pd, 256), (int64_t)c.num_sms * 16), 256, 0,
+                   c.stream, in.Pd, in.dst_dat, deg);
+        DHGP_LAUNCHED(c);
+    }
+    pdl_launch(k_feasible_deg, (unsigned)cdiv(in.N, 256), 256, 0, c.stream, in.N, in.size, deg, omega, delta, bad);
+    DHGP_LAUNCHED(c);
+    int32_t h[2];
+    c.d2h(h, bad, 2);
+    c.sync();
+    *bad_size = h[0] == 0x7fffffff ? -1 : h[0];
+    *bad_in = h[1] == 0x7fffffff ? -1 : h[1];
+    if (*bad_size >= 0) c.d2h(size_val, in.size + *bad_size, 1);
+    if (*bad_in >= 0) c.d2h(indeg_val, deg + *bad_in, 1);
+    c.sync();
+    c.free(deg);
 }
 
 }  // namespace dhgp

@@ -73,5 +73,12 @@ void derive_out(Ctx &c, const DLevel &L, int64_t *out_off, int32_t *out_dat);
 // check_feasibility (hgraph.py:376-401): returns first offending node or -1
 // for each of (size > omega, |in| > delta).
 void feasibility(Ctx &c, const DLevel &L, int64_t omega, int64_t delta, int32_t *bad_size, int32_t *bad_in);
+// The same check straight from the resident input (in-degree = occurrences in
+// the destination lists), so that it runs before anything that could reject
+// the input as unsupported — the reference checks feasibility first
+// (driver.py:89 -> hgraph.py:376-401).  *size_val / *indeg_val receive the
+// offending values.
+void feasibility_input(Ctx &c, const DInput &in, int64_t omega, int64_t delta, int32_t *bad_size, int32_t *bad_in,
+                       int32_t *size_val, int32_t *indeg_val);
 
 }  // namespace dhgp

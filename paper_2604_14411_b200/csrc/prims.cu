@@ -983,23 +983,34 @@ __global__ void k_zero_many(ZeroSet z) {
         ((uint32_t *)p)[i] = 0u;
     if (blockIdx.x == 0 && threadIdx.x < (nb & 3)) p[nw * 4 + threadIdx.x] = 0;
 }
-// 16-byte stores when both ends allow, bytes otherwise (sizes here are whole
-// elements of arena blocks, so the vector path is the common one)
+// 16-byte stores over the aligned body, single bytes only for the head up to
+// the first 16-byte boundary and the tail after the last one
 __global__ void k_fill(uint8_t *p, uint32_t word, size_t bytes) {
     pdl_entry();
     const size_t stride = (size_t)gridDim.x * blockDim.x, t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if ((((uintptr_t)p | bytes) & 15) == 0) {
-        const uint4 v = make_uint4(word, word, word, word);
-        for (size_t i = t; i < (bytes >> 4); i += stride) ((uint4 *)p)[i] = v;
-    } else {
-        for (size_t i = t; i < bytes; i += stride) p[i] = (uint8_t)word;
-    }
+    const size_t head = std::min<size_t>(bytes, (16 - ((uintptr_t)p & 15)) & 15);
+    const size_t body = (bytes - head) >> 4;
+    const uint4 v = make_uint4(word, word, word, word);
+    uint4 *q = (uint4 *)(p + head);
+    for (size_t i = t; i < body; i += stride) q[i] = v;
+    const size_t tail0 = head + (body << 4);
+    if (t < head) p[t] = (uint8_t)word;
+    if (t < bytes - tail0) p[tail0 + t] = (uint8_t)word;
 }
+// 16-byte loads and stores when source and destination share their offset
+// within 16 bytes (the arena's blocks always do), bytes otherwise
 __global__ void k_copy(uint8_t *d, const uint8_t *s, size_t bytes) {
     pdl_entry();
     const size_t stride = (size_t)gridDim.x * blockDim.x, t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if ((((uintptr_t)d | (uintptr_t)s | bytes) & 15) == 0) {
-        for (size_t i = t; i < (bytes >> 4); i += stride) ((uint4 *)d)[i] = ((const uint4 *)s)[i];
+    if ((((uintptr_t)d ^ (uintptr_t)s) & 15) == 0) {
+        const size_t head = std::min<size_t>(bytes, (16 - ((uintptr_t)d & 15)) & 15);
+        const size_t body = (bytes - head) >> 4;
+        const uint4 *sq = (const uint4 *)(s + head);
+        uint4 *dq = (uint4 *)(d + head);
+        for (size_t i = t; i < body; i += stride) dq[i] = sq[i];
+        const size_t tail0 = head + (body << 4);
+        if (t < head) d[t] = s[t];
+        if (t < bytes - tail0) d[tail0 + t] = s[tail0 + t];
     } else {
         for (size_t i = t; i < bytes; i += stride) d[i] = s[i];
     }

@@ -14,7 +14,7 @@
 
 namespace dhgp {
 void seams_setup(Ctx &c, int device);
-extern std::mutex g_mu;
+std::recursive_mutex &device_mutex(int device);
 }
 
 using namespace dhgp;
@@ -98,14 +98,79 @@ __global__ void k_edge_lambda(int32_t E, const int64_t *pin_off, const int32_t *
     for (int64_t p = pin_off[e]; p < pin_off[e + 1]; p++) lam += (p == pin_off[e]) || sorted_parts[p] != sorted_parts[p - 1];
     contrib[e] = lam > 0 ? w[e] * (double)(lam - 1) : 0.0;
 }
-// the reference sums in ascending edge order; one thread keeps that order so
-// the result is bit-exact for non-integral weights as well
-__global__ void k_ordered_sum(int64_t n, const double *x, double *out) {
+// Sum of x[0..n) equal to the reference's sequential f64 sum in ascending
+// order (connectivity_value, _kernels.pyx:199-213).  Every x is a multiple
+// of 2^-S for S = the most fractional bits of any element; when
+// sum|x| * 2^S < 2^53, every partial sum of any order is an exactly
+// representable multiple of 2^-S, so an int64 reduction of x * 2^S in any
+// order is bit-identical to the sequential f64 sum.  Pass 1 finds S and
+// sum|x|; pass 2 reduces in parallel when that holds, else one thread walks
+// the elements in order.
+__device__ __forceinline__ int frac_bits(double x) {
+    if (x == 0.0 || !isfinite(x)) return 0;
+    int e;
+    const double m = frexp(fabs(x), &e);  // x = m * 2^e, m in [0.5, 1)
+    const unsigned long long mant = (unsigned long long)ldexp(m, 53);
+    const int tz = __ffsll((long long)mant) - 1;  // trailing zero bits of the 53-bit mantissa
+    const int fb = 53 - tz - e;                     // bits after the binary point
+    return fb > 0 ? fb : 0;
+}
+__global__ void k_sum_probe(int64_t n, const double *x, int *maxbits, double *abssum) {
     pdl_entry();
-    if (threadIdx.x || blockIdx.x) return;
-    double t = 0.0;
-    for (int64_t i = 0; i < n; i++) t += x[i];
-    *out = t;
+    int mb = 0;
+    double a = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        mb = max(mb, frac_bits(x[i]));
+        a += fabs(x[i]);
+    }
+    for (int o = 16; o; o >>= 1) {
+        mb = max(mb, __shfl_xor_sync(0xffffffffu, mb, o));
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(maxbits, mb);
+        atomicAdd(abssum, a);
+    }
+}
+__global__ void k_sum_exact(int64_t n, const double *x, const int *maxbits, const double *abssum,
+                            unsigned long long *acc, double *out) {
+    pdl_entry();
+    const int S = *maxbits;
+    // margin: the probe's own f64 sum of |x| may round by a relative 2^-40
+    const bool parallel = S <= 60 && ldexp(*abssum, S) < 0x1p52;
+    if (!parallel) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            double t = 0.0;
+            for (int64_t i = 0; i < n; i++) t += x[i];
+            *out = t;
+        }
+        return;
+    }
+    long long v = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        v += (long long)ldexp(x[i], S);
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(acc, (unsigned long long)v);
+}
+__global__ void k_sum_finish(const int *maxbits, const double *abssum, const unsigned long long *acc, double *out) {
+    pdl_entry();
+    const int S = *maxbits;
+    if (S <= 60 && ldexp(*abssum, S) < 0x1p52) *out = ldexp((double)(long long)*acc, -S);
+}
+// scratch: 32 bytes
+void exact_sum(Ctx &c, int64_t n, const double *x, double *out, void *scratch) {
+    int *mb = (int *)scratch;
+    double *as = (double *)((char *)scratch + 8);
+    unsigned long long *acc = (unsigned long long *)((char *)scratch + 16);
+    c.zero((char *)scratch, 24);
+    c.zero(out, 1);
+    const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), (int64_t)c.num_sms * 8));
+    pdl_launch(k_sum_probe, g, 256, 0, c.stream, n, x, mb, as);
+    DHGP_LAUNCHED(c);
+    pdl_launch(k_sum_exact, g, 256, 0, c.stream, n, x, mb, as, acc, out);
+    DHGP_LAUNCHED(c);
+    pdl_launch(k_sum_finish, 1, 32, 0, c.stream, mb, as, acc, out);
+    DHGP_LAUNCHED(c);
 }
 
 // ---- compute_pins (_kernels.pyx:216-231): thread per h-edge row -----------
@@ -276,7 +341,7 @@ __global__ void k_nbr_write(int64_t X, const uint64_t *keys, const uint8_t *keep
 }  // namespace
 
 #define SEAM_BEGIN                           \
-    std::lock_guard<std::mutex> _lk(g_mu);   \
+    std::lock_guard<std::recursive_mutex> _lk(device_mutex(device));   \
     try {                                    \
         Ctx c;                               \
         seams_setup(c, device);
@@ -496,14 +561,13 @@ int dhgp_evaluate(const dhgp_graph *g, const int32_t *assign, int32_t num_parts,
     // connectivity with the reference's ascending-edge f64 summation
     if (connectivity_out) {
         int32_t *tmp = c.alloc<int32_t>(L.U);
-        double *contrib = c.alloc<double>(L.E), *res = c.alloc<double>(1);
+        double *contrib = c.alloc<double>(L.E), *res = c.alloc<double>(5);
         seg_sort(c, L.E, L.pin_off, L.pin_dat, da.p, tmp);
         if (L.E > 0) {
             pdl_launch(k_edge_lambda, (unsigned)cdiv(L.E, 256), 256, 0, c.stream, L.E, L.pin_off, tmp, in.w, contrib);
             DHGP_LAUNCHED(c);
         }
-        pdl_launch(k_ordered_sum, 1, 32, 0, c.stream, L.E, contrib, res);
-        DHGP_LAUNCHED(c);
+        exact_sum(c, L.E, contrib, res, res + 1);
         c.d2h(connectivity_out, res, 1);
         c.sync();
         c.free(tmp);
@@ -584,15 +648,14 @@ int dhgp_connectivity_value(int32_t E, const int64_t *pin_off, const int32_t *pi
     SEAM_BEGIN
     DevBuf<int64_t> po(c, pin_off, (int64_t)E + 1);
     DevBuf<int32_t> pd(c, pin_dat, pin_off[E]), da(c, assign, N), tmp(c, pin_off[E]);
-    DevBuf<double> dw(c, w, E), contrib(c, E), res(c, 1);
+    DevBuf<double> dw(c, w, E), contrib(c, E), res(c, 5);
     seg_sort(c, E, po.p, pd.p, da.p, tmp.p);
     if (E > 0) {
         pdl_launch(k_edge_lambda, (unsigned)cdiv(E, 256), 256, 0, c.stream, E, po.p, tmp.p, dw.p, contrib.p);
         DHGP_LAUNCHED(c);
     }
-    pdl_launch(k_ordered_sum, 1, 32, 0, c.stream, E, contrib.p, res.p);
-    DHGP_LAUNCHED(c);
-    res.get(out);
+    exact_sum(c, E, contrib.p, res.p, res.p + 1);
+    c.d2h(out, res.p, 1);
     SEAM_END
 }
 
