@@ -319,8 +319,8 @@ static void run_partition(Ctx &c, const DInput &in, const dhgp_config &cfg, Part
     if (!W.integral) {
         W.release(c);
         throw Error{DHGP_ERR_UNSUPPORTED,
-                    "non-integral h-edge weights (or a weight total >= 2^53) are outside the exact-integer "
-                    "device path"};
+                    "h-edge weights that are not multiples of one power of two 2^-S (S <= 62) with "
+                    "sum(w) * 2^S < 2^53 are outside the exact-integer device path"};
     }
     std::vector<DLevel> levels(1);
     build_level0(c, in, levels[0]);
@@ -432,6 +432,7 @@ static void run_partition(Ctx &c, const DInput &in, const dhgp_config &cfg, Part
                 c.d2h(hdd.data(), cl.dst_dat, cl.Pd);
                 c.d2h(hsz.data(), cl.size, cl.N);
                 c.sync();
+                for (auto &x : hs) x *= W.unit;  // scaled-integer hist -> the reference's f64 value
                 dhgp_event ev;
                 memset(&ev, 0, sizeof ev);
                 ev.kind = DHGP_EVENT_LEVEL;

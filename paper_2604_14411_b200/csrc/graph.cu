@@ -9,16 +9,43 @@ namespace dhgp {
 namespace {
 // weights: finite, >= 0; exact-integer mode needs integral values with a
 // total < 2^53 so every partial sum in any order is exact.
-__global__ void k_check_weights(const double *w, int64_t E, int64_t *wi, unsigned long long *sum, int32_t *flags) {
+// Weights w = m * 2^e are all multiples of 2^-S, S = the most fractional
+// bits of any weight (0 for integral weights).  With the scaled integers
+// w * 2^S summing below 2^53, every partial sum the reference forms in its
+// fixed order is an exactly representable multiple of 2^-S, so
+// integer accumulation in any order followed by one multiplication by 2^-S
+// is bit-identical to it.
+__device__ __forceinline__ int weight_frac_bits(double x) {
+    if (x == 0.0) return 0;
+    int e;
+    const double m = frexp(x, &e);
+    const unsigned long long mant = (unsigned long long)ldexp(m, 53);
+    const int fb = 53 - (__ffsll((long long)mant) - 1) - e;
+    return fb > 0 ? fb : 0;
+}
+__global__ void k_check_weights(const double *w, int64_t E, int32_t *flags, int32_t *maxbits) {
     pdl_entry();
-    __shared__ int64_t sh[33];
     int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    int64_t v = 0;
+    int mb = 0;
     if (e < E) {
         double x = w[e];
-        if (!(x >= 0.0) || !isfinite(x)) atomicOr(&flags[0], 1);          // invalid weight
-        if (x != floor(x) || x >= 9007199254740992.0) atomicOr(&flags[0], 2);  // non-integral
-        v = (x >= 0.0 && x < 9007199254740992.0) ? (int64_t)x : 0;
+        if (!(x >= 0.0) || !isfinite(x)) atomicOr(&flags[0], 1);  // invalid weight
+        else mb = weight_frac_bits(x);
+    }
+    for (int o = 16; o; o >>= 1) mb = max(mb, __shfl_xor_sync(0xffffffffu, mb, o));
+    if ((threadIdx.x & 31) == 0 && mb) atomicMax(maxbits, mb);
+}
+__global__ void k_scale_weights(const double *w, int64_t E, const int32_t *maxbits, int64_t *wi,
+                                unsigned long long *sum, int32_t *flags) {
+    pdl_entry();
+    __shared__ int64_t sh[33];
+    const int S = *maxbits;
+    int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int64_t v = 0;
+    if (e < E && S <= 62) {
+        const double x = ldexp(w[e], S);
+        if (x >= 9007199254740992.0) atomicOr(&flags[0], 2);  // a scaled weight alone reaches 2^53
+        else v = (int64_t)x;
         wi[e] = v;
     }
     int64_t t = block_sum<int64_t>(v, sh);
@@ -119,22 +146,26 @@ void prepare_weights(Ctx &c, const DInput &in, DWeights &W) {
     W.w = in.w;
     W.wi = c.alloc<int64_t>(W.E);
     unsigned long long *sum = c.alloc<unsigned long long>(1);
-    int32_t *flags = c.alloc<int32_t>(1);
+    int32_t *flags = c.alloc<int32_t>(2);
     c.zero(sum, 1);
-    c.zero(flags, 1);
+    c.zero(flags, 2);
     if (W.E > 0) {
-        pdl_launch(k_check_weights, (unsigned)cdiv(W.E, 256), 256, 0, c.stream, W.w, W.E, W.wi, sum, flags);
+        pdl_launch(k_check_weights, (unsigned)cdiv(W.E, 256), 256, 0, c.stream, W.w, W.E, flags, flags + 1);
+        DHGP_LAUNCHED(c);
+        pdl_launch(k_scale_weights, (unsigned)cdiv(W.E, 256), 256, 0, c.stream, W.w, W.E, flags + 1, W.wi, sum, flags);
         DHGP_LAUNCHED(c);
     }
     unsigned long long hs = 0;
-    int32_t hf = 0;
+    int32_t hf[2] = {0, 0};
     c.d2h(&hs, sum, 1);
-    c.d2h(&hf, flags, 1);
+    c.d2h(hf, flags, 2);
     c.sync();
     c.free(sum);
     c.free(flags);
-    if (hf & 1) throw Error{DHGP_ERR_ARG, "edge weights must be finite and >= 0"};
-    W.integral = !(hf & 2) && hs < (1ull << 53);
+    if (hf[0] & 1) throw Error{DHGP_ERR_ARG, "edge weights must be finite and >= 0"};
+    W.scale_bits = hf[1];
+    W.unit = ldexp(1.0, -hf[1]);
+    W.integral = !(hf[0] & 2) && hf[1] <= 62 && hs < (1ull << 53);
     W.wsum = (int64_t)hs;
 }
 

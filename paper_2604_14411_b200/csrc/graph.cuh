@@ -36,9 +36,11 @@ struct DLevel {
 struct DWeights {
     int32_t E = 0;
     const double *w = nullptr;  // [E] as given (borrowed from the input)
-    int64_t *wi = nullptr;      // [E] integral copy (exact-integer mode)
-    int64_t wsum = 0;
-    bool integral = true;
+    int64_t *wi = nullptr;      // [E] w * 2^scale_bits as integers (exact-integer mode)
+    int64_t wsum = 0;           // sum of wi
+    int scale_bits = 0;         // S: every weight is a multiple of 2^-S (0 when integral)
+    double unit = 1.0;          // 2^-S: a sum of wi times unit is the reference's f64 value
+    bool integral = true;       // wi exact and wsum < 2^53: the exact-integer device path applies
     void release(Ctx &c) {
         c.free(wi);
         *this = DWeights();
@@ -61,7 +63,8 @@ struct DInput {
 };
 // host -> HBM copy of the primary fields (offsets rebased to 0)
 void upload_input(Ctx &c, const dhgp_graph &g, DInput &in);
-// Validates the weights (finite, >= 0) and derives the exact-integer copy.
+// Validates the weights (finite, >= 0) and derives the exact-integer copy:
+// dyadic weights (multiples of 2^-S, e.g. 0.5 steps) are scaled by 2^S.
 void prepare_weights(Ctx &c, const DInput &in, DWeights &W);
 // Level 0 over a resident input (Hypergraph._from_csr, hgraph.py:212-238).
 void build_level0(Ctx &c, const DInput &in, DLevel &L);

@@ -2492,7 +2492,7 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
             c.d2h(&M, dM, 1);
             c.d2h(&conn_h, conn_d, 1);
             c.sync();
-            conns.push_back((double)(int64_t)conn_h);
+            conns.push_back((double)(int64_t)conn_h * W.unit);
             need_final = false;
             if (M == 0) break;
         }
@@ -2595,7 +2595,7 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
             }
             c.sync();
             if (spec) {
-                conns.push_back((double)(int64_t)conn_h);
+                conns.push_back((double)(int64_t)conn_h * W.unit);
                 need_final = false;
                 if (M == 0) {
                     free_tail();
@@ -2661,7 +2661,7 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
             rec.round = rnd;
             rec.num_parts = K;
             rec.k = (int32_t)kbest;
-            rec.total_gain = (double)total_gain;
+            rec.total_gain = (double)total_gain * W.unit;
             rec.assign.resize(N);
             rec.node.resize(M);
             rec.from.resize(M);
@@ -2675,8 +2675,12 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
             c.d2h(gs.data(), gseq, M);
             c.d2h(ae.data(), act_ex, M + 2);
             c.sync();
-            rec.gain_iso.assign(gi.begin(), gi.end());
-            rec.gain_seq.assign(gs.begin(), gs.end());
+            rec.gain_iso.resize(M);
+            rec.gain_seq.resize(M);
+            for (int64_t i = 0; i < M; i++) {
+                rec.gain_iso[i] = (double)gi[i] * W.unit;
+                rec.gain_seq[i] = (double)gs[i] * W.unit;
+            }
             rec.active.assign(ae.begin() + 1, ae.begin() + 2 + M);
             (*obs)(rec);
         }
@@ -2706,7 +2710,7 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
             unsigned long long h = 0;
             c.d2h(&h, conn_d, 1);
             c.sync();
-            conns.push_back((double)(int64_t)h);
+            conns.push_back((double)(int64_t)h * W.unit);
         } else {
             double v;
             evaluate_assign(c, L, W, assign, K, nullptr, nullptr, &v);
@@ -2750,7 +2754,7 @@ void evaluate_assign(Ctx &c, const DLevel &L, const DWeights &W, const int32_t *
         unsigned long long h = 0;
         c.d2h(&h, conn, 1);
         c.sync();
-        *h_conn = (double)(int64_t)h;
+        *h_conn = (double)(int64_t)h * W.unit;
     }
     c.free(conn);
     c.free(r.pc);

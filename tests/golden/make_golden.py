@@ -143,8 +143,40 @@ def kernels_fixture(dp):
     np.savez_compressed(OUT / "kernels.npz", **out)
 
 
+def fractional(dp):
+    """weights.npz: instances with fractional weights — dyadic (0.5 / 0.25
+    steps: exact-integer after scaling) and decimal (0.1 steps: every f64 sum
+    rounds, so only the reference's own summation order reproduces it) —
+    with the reference's partition() outputs and every observer payload."""
+    out = {}
+    rs = np.random.RandomState(4242)
+    kinds = []
+    for t in range(12):
+        n = int(rs.randint(30, 400))
+        omega = int(rs.choice([4, 8, 16]))
+        n_, w, so, sd, do, dd = W.random_dhg(n, int(1.5 * n), int(rs.choice([3, 4, 6])), seed=7000 + t)
+        kind = ("half", "quarter", "decimal")[t % 3]
+        if kind == "half":
+            w = rs.randint(1, 20, size=len(w)) / 2.0
+        elif kind == "quarter":
+            w = rs.randint(1, 40, size=len(w)) / 4.0
+        else:
+            w = rs.randint(1, 90, size=len(w)) * 0.1
+        arr = (n_, w, so, sd, do, dd)
+        indeg = int(np.bincount(dd, minlength=n).max()) if len(dd) else 0
+        delta = max(indeg, 1) + int(rs.randint(0, 2 * omega))
+        pack_run(dp, arr, omega, delta, f"c{t}_", out)
+        kinds.append(kind)
+    out["kinds"] = np.asarray(kinds)
+    out["cases"] = np.arange(len(kinds))
+    np.savez_compressed(OUT / "weights.npz", **out)
+
+
 def main():
     dp = ref_loader.load()
+    if "--only" in sys.argv:
+        {"fractional": fractional}[sys.argv[sys.argv.index("--only") + 1]](dp)
+        return
     partition_small(dp)
     kernels_fixture(dp)
     out = {}

@@ -54,6 +54,13 @@ def assert_same_as_oracle(g, omega, delta, max_levels=1 << 20, **kw):
 def test_partition_small_golden_with_observer_payloads():
     z = load_npz("partition_small.npz")
     for t in z["cases"]:
+        check_golden_case(z, t)
+
+
+def check_golden_case(z, t):
+    """partition() of fixture case t against the reference's outputs and
+    every per-level / per-round observer payload it recorded."""
+    if True:
         p = f"c{t}_"
         g = graph([z[f"{p}in_{k}"] for k in ("n", "w", "so", "sd", "do", "dd")])
         part, st, ev = run_gpu(g, int(z[p + "omega"]), int(z[p + "delta"]), record=True, max_levels=1 << 20)
@@ -244,11 +251,52 @@ def test_max_levels_guard_message():
         d.partition(g, d.Config(c, max_levels=1))
 
 
-def test_non_integral_weights_are_rejected_loudly():
+def test_dyadic_fractional_weights_bit_exact():
+    """0.5- and 0.25-step weights (tests/golden/weights.npz, produced by the
+    reference): exact after scaling by 2^S, so every payload is bit-exact."""
+    z = load_npz("weights.npz")
+    for t in z["cases"]:
+        if str(z["kinds"][t]) in ("half", "quarter"):
+            check_golden_case(z, t)
+
+
+def test_non_dyadic_weights_are_rejected_loudly():
     d = dp()
-    g = d.Hypergraph.from_edges(3, [0.5, 1.0], [[0], [1]], [[1], [2]])
-    with pytest.raises(d.DhgError, match="non-integral"):
+    g = d.Hypergraph.from_edges(3, [0.1, 1.0], [[0], [1]], [[1], [2]])
+    with pytest.raises(d.DhgError, match="power of two"):
         d.partition(g, d.Config(d.Constraints(2, 2)))
+
+
+def test_feasibility_precedes_unsupported_input():
+    """The reference checks feasibility first (driver.py:89): an infeasible
+    graph with unsupported weights raises InfeasibleError, not DhgError."""
+    d = dp()
+    g = d.Hypergraph.from_edges(3, [0.1, 1.0], [[0], [1]], [[1, 2], [2]])
+    with pytest.raises(d.InfeasibleError, match="inbound"):
+        d.partition(g, d.Config(d.Constraints(2, 1)))
+
+
+def test_observer_may_call_the_library():
+    """An observer that evaluates the live payload objects (connectivity,
+    sizes, validity) from inside the callback; the reference allows it."""
+    d = dp()
+    g, c = make_instance(300, 450, 5, seed=17, omega=8)
+    seen = []
+
+    def obs(kind, p):
+        if kind == "level":
+            co = p["coarse"]
+            seen.append(("level", len(co.node_in.data), d.connectivity(co, d.Partitioning(
+                np.arange(co.num_nodes, dtype=np.int32), co.num_nodes))))
+        else:
+            gr = p["graph"]
+            part = d.Partitioning(p["assign"], p["num_parts"])
+            seen.append(("round", d.connectivity(gr, part), len(d.check_validity(gr, part, c)) >= 0))
+
+    part, st = d.partition(g, d.Config(c, max_levels=1 << 20), observer=obs)
+    ref, _ = d.partition(g, d.Config(c, max_levels=1 << 20))
+    assert np.array_equal(part.assign, ref.assign)
+    assert any(k == "level" for k, *_ in seen) and any(k == "round" for k, *_ in seen)
 
 
 def test_timings_and_determinism():
@@ -417,3 +465,22 @@ def test_full_and_incremental_paths_agree(monkeypatch):
         res.append(run_gpu(g, om, de, max_levels=1 << 20)[:2])
     (p1, s1), (p2, s2) = res
     assert np.array_equal(p1.assign, p2.assign) and s1.to_dict() == s2.to_dict()
+
+
+def test_connectivity_exact_for_any_weights():
+    """connectivity() (dhgp_evaluate) and the connectivity_value seam equal the
+    reference's ascending-edge f64 sum (_kernels.pyx:199-213, via the pinned
+    oracle) for integral, dyadic and decimal weights alike: a parallel int64
+    sum when it is provably exact, else the ordered walk."""
+    d = dp()
+    from paper_2604_14411_b200 import kernels as K
+
+    rs = np.random.RandomState(99)
+    for t, scale in enumerate((1.0, 0.5, 0.125, 0.1, 1e-3, 3.0e15)):
+        g, c = make_instance(500, 800, 6, seed=200 + t, omega=8)
+        w = rs.randint(1, 50, size=g.num_edges) * scale
+        g = d.Hypergraph._from_csr(g.num_nodes, w, g.edge_src, g.edge_dst)
+        a = rs.randint(0, 37, size=g.num_nodes).astype(np.int32)
+        want = orc.connectivity_value(g.edge_pins.offsets, g.edge_pins.data, w, a)
+        assert d.connectivity(g, d.Partitioning(a, 37)) == want, scale
+        assert K.connectivity_value(g.edge_pins.offsets, g.edge_pins.data, w, a) == want, scale
