@@ -511,6 +511,36 @@ __device__ __forceinline__ void block_bitonic_sort32(uint32_t *s, int n_pow2) {
     __syncthreads();
 }
 
+// In-place ascending sort of s[0..n) for any n, by the block, in any memory
+// (segments too long for shared memory sort in global memory).  The network
+// is the bitonic sorter written with ascending comparators only (each merge
+// first compares i with its mirror in the block, then half-cleans), so a
+// virtual +inf padding up to the next power of two never moves and every
+// comparator touching an index >= n is skipped.
+template <class T>
+__device__ __forceinline__ void block_sort_asc_any(T *s, int64_t n) {
+    int64_t np = 1;
+    while (np < n) np <<= 1;
+    for (int64_t size = 2; size <= np; size <<= 1) {
+        for (int64_t j = size >> 1; j > 0; j >>= 1) {
+            __syncthreads();
+            for (int64_t t = threadIdx.x; t < (np >> 1); t += blockDim.x) {
+                const int64_t blk = t / j, off = t % j;
+                const int64_t lo = 2 * j * blk + off;
+                // first step of a merge: mirror partner; later steps: +j
+                const int64_t hi = (j == (size >> 1)) ? (lo - off) + (2 * j - 1 - off) : lo + j;
+                if (hi >= n) continue;
+                const T a = s[lo], b = s[hi];
+                if (b < a) {
+                    s[lo] = b;
+                    s[hi] = a;
+                }
+            }
+        }
+    }
+    __syncthreads();
+}
+
 __host__ __device__ __forceinline__ int next_pow2(int x) {
     int p = 1;
     while (p < x) p <<= 1;

@@ -310,10 +310,6 @@ static void run_partition(Ctx &c, const DInput &in, const dhgp_config &cfg, Part
             throw Error{DHGP_ERR_INFEASIBLE, "node " + std::to_string(bi) + " has " + std::to_string(deg) +
                                                  " inbound edges > max_inbound " + std::to_string(delta)};
     }
-    if (in.max_edge_pins > kMaxSegSort)
-        throw Error{DHGP_ERR_UNSUPPORTED, "h-edge with " + std::to_string(in.max_edge_pins) +
-                                              " pin slots exceeds the supported maximum " +
-                                              std::to_string(kMaxSegSort)};
     DWeights W;
     prepare_weights(c, in, W);
     if (!W.integral) {

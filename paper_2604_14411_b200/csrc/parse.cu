@@ -229,31 +229,12 @@ __global__ void k_err_flags(int64_t E, const uint8_t *status, uint8_t *bad) {
 __global__ void k_dup_flags(int64_t E, const int64_t *off, const int32_t *sorted, uint8_t *bad) {
     pdl_entry();
     int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= E || off[e + 1] - off[e] > kMaxSegSort) return;
+    if (e >= E) return;
     for (int64_t p = off[e] + 1; p < off[e + 1]; p++)
         if (sorted[p] == sorted[p - 1]) {
             bad[e] = 1;
             return;
         }
-}
-__global__ void k_dup_big(int64_t E, const int64_t *off, const int32_t *dat, uint8_t *bad) {
-    pdl_entry();
-    __shared__ int s_found;
-    for (int64_t e = blockIdx.x; e < E; e += gridDim.x) {
-        const int64_t lo = off[e], n = off[e + 1] - lo;
-        if (n <= kMaxSegSort) continue;
-        if (threadIdx.x == 0) s_found = 0;
-        __syncthreads();
-        for (int64_t i = threadIdx.x; i < n && !s_found; i += blockDim.x)
-            for (int64_t j = i + 1; j < n; j++)
-                if (dat[lo + i] == dat[lo + j]) {
-                    s_found = 1;
-                    break;
-                }
-        __syncthreads();
-        if (threadIdx.x == 0 && s_found) bad[e] = 1;
-        __syncthreads();
-    }
 }
 __global__ void k_first_bad(int64_t E, const uint8_t *bad, unsigned long long *first) {
     pdl_entry();
@@ -454,18 +435,13 @@ int dhgp_parse_dhg_finish(dhgp_parse *ps, const int64_t *slow_ks, const int64_t 
     }
     // repeated pins within one side (hgraph.py:462-463)
     if (E > 0) {
-        // sides of up to kMaxSegSort ids: per-segment sort + adjacent check;
-        // longer ones (rare): a block compares all pairs
+        // per-side sort (any length) + adjacent check
         int32_t *tmp = c.alloc<int32_t>(std::max(tot[0], tot[1]));
         seg_sort(c, E, ps->src_off, ps->src_dat, nullptr, tmp);
         pdl_launch(k_dup_flags, (unsigned)cdiv(E, 256), 256, 0, c.stream, E, ps->src_off, tmp, ps->bad);
         DHGP_LAUNCHED(c);
-        pdl_launch(k_dup_big, c.num_sms, 1024, 0, c.stream, E, ps->src_off, ps->src_dat, ps->bad);
-        DHGP_LAUNCHED(c);
         seg_sort(c, E, ps->dst_off, ps->dst_dat, nullptr, tmp);
         pdl_launch(k_dup_flags, (unsigned)cdiv(E, 256), 256, 0, c.stream, E, ps->dst_off, tmp, ps->bad);
-        DHGP_LAUNCHED(c);
-        pdl_launch(k_dup_big, c.num_sms, 1024, 0, c.stream, E, ps->dst_off, ps->dst_dat, ps->bad);
         DHGP_LAUNCHED(c);
         c.free(tmp);
     }

@@ -618,8 +618,14 @@ __global__ void k_seg_sort_block(const int64_t *off, const int32_t *dat, const i
         int64_t s = list[t];
         int64_t lo = off[s];
         int len = (int)(off[s + 1] - lo);
-        if (len > kMaxSegSort) {
-            if (threadIdx.x == 0) atomicMax(err, len);
+        if (len > kMaxSegSort) {  // in place in global memory (tmp is the segment's own output)
+            (void)err;
+            __syncthreads();
+            for (int64_t i = threadIdx.x; i < len; i += blockDim.x) {
+                const int32_t x = dat[lo + i];
+                tmp[lo + i] = map ? map[x] : x;
+            }
+            block_sort_asc_any<uint32_t>((uint32_t *)(tmp + lo), len);
             continue;
         }
         int np = next_pow2(len);
@@ -650,8 +656,7 @@ void seg_sort(Ctx &c, int64_t nseg, const int64_t *off, const int32_t *dat, cons
     DHGP_LAUNCHED(c);
     pdl_launch(k_seg_sort_warp, (unsigned)(c.num_sms * 8), 256, 0, c.stream, off, dat, map, tmp, wl, cnt);
     DHGP_LAUNCHED(c);
-    // segment lengths are bounded by kMaxSegSort at upload (max h-edge degree
-    // only shrinks under contraction), so the block tier never overflows
+    // segments above kMaxSegSort (shared memory) sort in place in global memory
     pdl_launch(k_seg_sort_block, (unsigned)(c.num_sms), 1024, kMaxSegSort * sizeof(uint32_t), c.stream, off, dat, map, tmp,
                                                                                                  bl, cnt, cnt + 2);
     DHGP_LAUNCHED(c);

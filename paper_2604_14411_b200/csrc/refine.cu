@@ -1056,7 +1056,8 @@ constexpr int kEvBlockMax = 2048;
 constexpr int kEvParts = 2 * kEvBlockMax;  // hash slots (>= distinct parts: 2 per mover)
 __global__ void __launch_bounds__(256) k_inbound_events_block(const int64_t *dst_off, const int32_t *dst_dat, Runs r,
                                        const int32_t *pos, const int32_t *from, const int32_t *to, EvArgs ev,
-                                       const int32_t *big_list, const int32_t *big_count, int32_t *err) {
+                                       const int32_t *big_list, const int32_t *big_count, int32_t *huge,
+                                       int32_t *huge_count) {
     pdl_entry();
     __shared__ uint32_t smv[kEvBlockMax];
     __shared__ int32_t skey[kEvParts];
@@ -1081,8 +1082,8 @@ __global__ void __launch_bounds__(256) k_inbound_events_block(const int64_t *dst
         }
         __syncthreads();
         const int nm = snm;
-        if (nm > kEvBlockMax) {
-            if (threadIdx.x == 0) atomicMax(err, nm);
+        if (nm > kEvBlockMax) {  // global-memory path (k_edge_movers_huge)
+            if (threadIdx.x == 0) huge[atomicAdd(huge_count, 1)] = e;
             __syncthreads();
             continue;
         }
@@ -1521,7 +1522,7 @@ constexpr int kSgBlockMax = 2048;
 __global__ void k_seq_gains_edge_block(const int64_t *pin_off, const int32_t *pin_dat, const int64_t *wi, Runs r,
                                        const int32_t *pos, const int32_t *from, const int32_t *to,
                                        unsigned long long *gacc, const int32_t *big_list, const int32_t *big_count,
-                                       int32_t *err) {
+                                       int32_t *huge, int32_t *huge_count) {
     pdl_entry();
     __shared__ uint32_t smv[kSgBlockMax];
     __shared__ int32_t sf[kSgBlockMax], st[kSgBlockMax];
@@ -1541,8 +1542,8 @@ __global__ void k_seq_gains_edge_block(const int64_t *pin_off, const int32_t *pi
         }
         __syncthreads();
         const int nm = snm;
-        if (nm > kSgBlockMax) {
-            if (threadIdx.x == 0) atomicMax(err, nm);
+        if (nm > kSgBlockMax) {  // global-memory path (k_edge_movers_huge)
+            if (threadIdx.x == 0) huge[atomicAdd(huge_count, 1)] = e;
             __syncthreads();
             continue;
         }
@@ -1572,6 +1573,77 @@ __global__ void k_seq_gains_edge_block(const int64_t *pin_off, const int32_t *pi
             const int32_t base_pd = k >= 0 ? r.pc[2 * (ro + k) + 1] : 0;
             const int64_t net = seq_net(we, base_ps, base_pd, leav_pd, ent_pd, leav_ps, ent_ps);
             if (net) atomicAdd(&gacc[smv[a]], (unsigned long long)net);
+        }
+        __syncthreads();
+    }
+}
+
+// H-edges with more movers than the block kernels hold in shared memory: a
+// CTA per h-edge with global scratch.  The movers' sequence positions are
+// sorted; the (from, position) and (to, position) keys are sorted too, so
+// "#earlier movers leaving / entering part x" for mover a is the distance
+// between two lower bounds — O(m log m) per h-edge.  mode 0: sequence-gain
+// terms over the pins (base = pin counts, rules (a)-(d)); mode 1: inbound
+// crossings over the destination pins (base = destination-pin counts), the
+// same running count as the per-part sweep of k_inbound_events_block.
+__device__ __forceinline__ int64_t lb_u64(const unsigned long long *a, int64_t n, unsigned long long key) {
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+        const int64_t m = (lo + hi) >> 1;
+        if (a[m] < key) lo = m + 1; else hi = m;
+    }
+    return lo;
+}
+__device__ __forceinline__ int32_t earlier(const unsigned long long *keys, int64_t nm, int32_t part, int64_t a) {
+    const unsigned long long k0 = (unsigned long long)(uint32_t)part << 32;
+    return (int32_t)(lb_u64(keys, nm, k0 | (unsigned long long)a) - lb_u64(keys, nm, k0));
+}
+__global__ void __launch_bounds__(1024) k_edge_movers_huge(int mode, const int64_t *off, const int32_t *dat,
+                                                           const int64_t *wi, Runs r, const int32_t *pos,
+                                                           const int32_t *from, const int32_t *to,
+                                                           unsigned long long *gacc, EvArgs ev, const int32_t *huge,
+                                                           const int32_t *huge_count, uint8_t *gscr, int64_t gcap) {
+    pdl_entry();
+    __shared__ int32_t snm;
+    const int nh = *huge_count;
+    uint32_t *smv = (uint32_t *)(gscr + (int64_t)blockIdx.x * ((20 * gcap + 15) & ~(int64_t)7));
+    unsigned long long *kf = (unsigned long long *)(smv + gcap + (gcap & 1));
+    unsigned long long *kt = kf + gcap;
+    for (int t = blockIdx.x; t < nh; t += gridDim.x) {
+        const int32_t e = huge[t];
+        if (threadIdx.x == 0) snm = 0;
+        __syncthreads();
+        for (int64_t q = off[e] + threadIdx.x; q < off[e + 1]; q += blockDim.x) {
+            const int32_t j = pos[dat[q]];
+            if (j >= 0) smv[atomicAdd(&snm, 1)] = (uint32_t)j;
+        }
+        __syncthreads();
+        const int64_t nm = snm;
+        block_sort_asc_any<uint32_t>(smv, nm);
+        for (int64_t a = threadIdx.x; a < nm; a += blockDim.x) {
+            const int32_t i = (int32_t)smv[a];
+            kf[a] = ((unsigned long long)(uint32_t)from[i] << 32) | (unsigned long long)a;
+            kt[a] = ((unsigned long long)(uint32_t)to[i] << 32) | (unsigned long long)a;
+        }
+        block_sort_asc_any<unsigned long long>(kf, nm);
+        block_sort_asc_any<unsigned long long>(kt, nm);
+        const int64_t ro = r.off[e];
+        const int32_t lam = r.len[e];
+        for (int64_t a = threadIdx.x; a < nm; a += blockDim.x) {
+            const int32_t i = (int32_t)smv[a], ps = from[i], pd = to[i];
+            const int32_t leav_ps = earlier(kf, nm, ps, a), ent_ps = earlier(kt, nm, ps, a);
+            const int32_t leav_pd = earlier(kf, nm, pd, a), ent_pd = earlier(kt, nm, pd, a);
+            const int32_t ks = run_find(r, ro, lam, ps), kd = run_find(r, ro, lam, pd);
+            if (mode == 0) {
+                const int32_t base_ps = ks >= 0 ? r.pc[2 * (ro + ks) + 1] : 0;
+                const int32_t base_pd = kd >= 0 ? r.pc[2 * (ro + kd) + 1] : 0;
+                const int64_t net = seq_net(wi[e], base_ps, base_pd, leav_pd, ent_pd, leav_ps, ent_ps);
+                if (net) atomicAdd(&gacc[i], (unsigned long long)net);
+            } else if (ps != pd) {
+                const int32_t in_ps = ks >= 0 ? r.cin[ro + ks] : 0, in_pd = kd >= 0 ? r.cin[ro + kd] : 0;
+                if (in_ps - leav_ps + ent_ps - 1 == 0) inbound_leave(ev, i);
+                if (in_pd - leav_pd + ent_pd + 1 == 1) inbound_enter(ev, i);
+            }
         }
         __syncthreads();
     }
@@ -1884,13 +1956,9 @@ __global__ void __launch_bounds__(1024) k_runs_update_wide(const int32_t *wide, 
                                                            const int32_t *dst_dat, const int32_t *assign,
                                                            const int64_t *wi, Runs r, unsigned long long *conn,
                                                            int64_t *pinbound, int32_t *ndirty, int32_t *nlist,
-                                                           int32_t *ncount) {
+                                                           int32_t *ncount, uint8_t *gscr, int64_t gcap) {
     pdl_entry();
     extern __shared__ unsigned long long smem_u64[];
-    uint32_t *sv = (uint32_t *)smem_u64;              // [kMaxSegSort] sorted parts
-    int32_t *op = (int32_t *)(sv + kMaxSegSort);      // [kMaxSegSort] old parts
-    int32_t *oc = op + kMaxSegSort;                   // [kMaxSegSort] old counts
-    uint8_t *flip = (uint8_t *)(oc + kMaxSegSort);    // [kMaxSegSort] per new run
     __shared__ int32_t s_wsum[32];
     __shared__ int s_same;
     const int t = threadIdx.x, lane = lane_id(), w = warp_id(), nwarp = blockDim.x >> 5;
@@ -1901,14 +1969,28 @@ __global__ void __launch_bounds__(1024) k_runs_update_wide(const int32_t *wide, 
         const int64_t plo = pin_off[e], lo = r.off[e];
         const int len = (int)(pin_off[e + 1] - plo);
         const int32_t old = r.len[e];
+        // working arrays: shared memory up to kMaxSegSort slots, else this
+        // CTA's slice of the global scratch (h-edges of up to gcap pins)
+        const bool huge = len > kMaxSegSort || old > kMaxSegSort;
+        const int64_t cap = huge ? gcap : kMaxSegSort;
+        uint8_t *wbuf = huge ? gscr + (int64_t)blockIdx.x * ((13 * gcap + 15) & ~(int64_t)15) : (uint8_t *)smem_u64;
+        uint32_t *sv = (uint32_t *)wbuf;           // [cap] sorted parts
+        int32_t *op = (int32_t *)(sv + cap);       // [cap] old parts
+        int32_t *oc = op + cap;                    // [cap] old counts
+        uint8_t *flip = (uint8_t *)(oc + cap);     // [cap] per new run
         for (int j = t; j < old; j += blockDim.x) {
             op[j] = r.pc[2 * (lo + j)];
             oc[j] = r.pc[2 * (lo + j) + 1];
             if (moved && r.cin[lo + j] > 0) atomicAdd((unsigned long long *)&pinbound[op[j]], ~0ull);
         }
-        const int np = next_pow2(len);
-        for (int j = t; j < np; j += blockDim.x) sv[j] = j < len ? (uint32_t)assign[pin_dat[plo + j]] : 0xffffffffu;
-        block_bitonic_sort32(sv, np);
+        if (huge) {
+            for (int j = t; j < len; j += blockDim.x) sv[j] = (uint32_t)assign[pin_dat[plo + j]];
+            block_sort_asc_any<uint32_t>(sv, len);
+        } else {
+            const int np = next_pow2(len);
+            for (int j = t; j < np; j += blockDim.x) sv[j] = j < len ? (uint32_t)assign[pin_dat[plo + j]] : 0xffffffffu;
+            block_bitonic_sort32(sv, np);
+        }
         // heads -> run slots by a block exclusive scan (one pass per 1024 slots)
         int base = 0;
         for (int c0 = 0; c0 < len; c0 += blockDim.x) {
@@ -2263,7 +2345,20 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
     int32_t *node = c.alloc<int32_t>(N), *from = c.alloc<int32_t>(N), *to = c.alloc<int32_t>(N);
     int64_t *giso = c.alloc<int64_t>(N), *gseq = c.alloc<int64_t>(N), *gseq_acc = c.alloc<int64_t>(N);
     int32_t *ev_from = c.alloc<int32_t>(N), *ev_to = c.alloc<int32_t>(N);
-    int32_t *sg_big = c.alloc<int32_t>(L.E), *sg_ctr = c.alloc<int32_t>(2);
+    int32_t *sg_big = c.alloc<int32_t>(L.E), *sg_ctr = c.alloc<int32_t>(4);  // [2], [3]: huge-list counts
+    // h-edges with more movers than shared memory holds (only possible when
+    // an h-edge has more than 2048 pins): huge lists + 20 B/pin scratch per CTA
+    const bool huge_movers = max_edge_pins > std::min(kSgBlockMax, kEvBlockMax);
+    int32_t *hv_sg = nullptr, *hv_ev = nullptr;
+    uint8_t *mv_scr = nullptr;
+    int mv_grid = 1;
+    if (huge_movers) {
+        hv_sg = c.alloc<int32_t>(L.E);
+        hv_ev = c.alloc<int32_t>(L.E);
+        mv_grid = (int)std::max<int64_t>(1, std::min<int64_t>(c.num_sms, (int64_t)(4ll << 30) /
+                                                                           (20ll * max_edge_pins + 8)));
+        mv_scr = c.alloc<uint8_t>((int64_t)mv_grid * ((20 * (int64_t)max_edge_pins + 15) & ~(int64_t)7));
+    }
     const int64_t ecap = 4 * (int64_t)N + 4;  // 2 size + 2 aggregated inbound events per move
     uint64_t *ek = c.alloc<uint64_t>(ecap), *ekt = c.alloc<uint64_t>(ecap);
     uint32_t *evv = c.alloc<uint32_t>(ecap), *evt = c.alloc<uint32_t>(ecap);
@@ -2292,6 +2387,14 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
     static int g_me = resident_grid(c, k_mover_edges, 256, 0);
     static int g_ap = resident_grid(c, k_apply_inc, 256, 0);
     const bool wide_edges = max_edge_pins > 128;
+    // h-edges beyond shared memory: 13 B per pin slot of global scratch per CTA
+    uint8_t *huge_scr = nullptr;
+    int huge_grid = c.num_sms;
+    if (max_edge_pins > kMaxSegSort) {
+        huge_grid = (int)std::max<int64_t>(1, std::min<int64_t>(c.num_sms, (int64_t)(4ll << 30) /
+                                                                             (13ll * max_edge_pins)));
+        huge_scr = c.alloc<uint8_t>((int64_t)huge_grid * ((13 * (int64_t)max_edge_pins + 15) & ~(int64_t)15));
+    }
     auto runs_update = [&](bool reset) {
         pdl_launch(k_runs_update, g_ru, 256, 0, c.stream, st.elist, st.ctr + CT_ELIST, st.edirty, L.pin_off, L.pin_dat,
                                                  L.dst_off, L.dst_dat, assign, W.wi, r, conn_d, pinbound, K, st.ndirty,
@@ -2304,9 +2407,9 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
                                                (int)(13 * kMaxSegSort)));
                 wattr = true;
             }
-            pdl_launch(k_runs_update_wide, c.num_sms, 1024, 13 * kMaxSegSort, c.stream, 
+            pdl_launch(k_runs_update_wide, huge_grid, 1024, 13 * kMaxSegSort, c.stream,
                 st.wide, st.ctr + CT_WIDE, st.edirty, L.pin_off, L.pin_dat, L.dst_off, L.dst_dat, assign, W.wi, r,
-                conn_d, pinbound, st.ndirty, st.nlist, st.ctr + CT_NLIST);
+                conn_d, pinbound, st.ndirty, st.nlist, st.ctr + CT_NLIST, huge_scr, (int64_t)max_edge_pins);
             DHGP_LAUNCHED(c);
         }
         if (reset) zero_many(c, {{st.ctr + CT_ELIST, 4}, {st.ctr + CT_WIDE, 4}});
@@ -2542,7 +2645,7 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
                 KScope ks(c, "seq_gains", 0.0);
                 unsigned long long *gacc = (unsigned long long *)gseq_acc;
                 zero_many(c,
-                          {{gacc, 8 * Mc}, {sg_ctr, 8}, {ctr, 16}, {ev_from, 4 * Mc}, {ev_to, 4 * Mc}, {ecount, 8}});
+                          {{gacc, 8 * Mc}, {sg_ctr, 16}, {ctr, 16}, {ev_from, 4 * Mc}, {ev_to, 4 * Mc}, {ecount, 8}});
                 if (L.E > 0) {
                     static int g_re = resident_grid(c, k_round_edges, 256, 0);
                     const unsigned gre = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(L.E, 8), g_re));
@@ -2552,11 +2655,19 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
                                                              sp ? dM : nullptr);
                     DHGP_LAUNCHED(c);
                     pdl_launch(k_seq_gains_edge_block, c.num_sms, 256, 0, c.stream, L.pin_off, L.pin_dat, W.wi, r, pos, from,
-                                                                             to, gacc, sg_big, sg_ctr, sg_ctr + 1);
+                                                                             to, gacc, sg_big, sg_ctr, hv_sg, sg_ctr + 2);
                     DHGP_LAUNCHED(c);
                     pdl_launch(k_inbound_events_block, c.num_sms, 256, 0, c.stream, L.dst_off, L.dst_dat, r, pos, from, to,
-                                                                             ev, big, ctr, ctr + 2);
+                                                                             ev, big, ctr, hv_ev, sg_ctr + 3);
                     DHGP_LAUNCHED(c);
+                    if (huge_movers) {  // exit at once when the huge lists are empty
+                        pdl_launch(k_edge_movers_huge, mv_grid, 1024, 0, c.stream, 0, L.pin_off, L.pin_dat, W.wi, r,
+                                   pos, from, to, gacc, ev, hv_sg, sg_ctr + 2, mv_scr, (int64_t)max_edge_pins);
+                        DHGP_LAUNCHED(c);
+                        pdl_launch(k_edge_movers_huge, mv_grid, 1024, 0, c.stream, 1, L.dst_off, L.dst_dat, W.wi, r,
+                                   pos, from, to, gacc, ev, hv_ev, sg_ctr + 3, mv_scr, (int64_t)max_edge_pins);
+                        DHGP_LAUNCHED(c);
+                    }
                 }
                 pdl_launch(k_round_moves, (unsigned)std::max<int64_t>(1, cdiv(Mc, 256)), 256, 0, c.stream, 
                     dM, node, from, to, L.size, ev, giso, gacc, gseq, sp);
@@ -2610,7 +2721,6 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
                     c.sync();
                 }
             }
-            if (hc[2] || hs[1]) throw Error{DHGP_ERR_UNSUPPORTED, "too many movers on one h-edge"};
             kbest = hr[0];
             total_gain = hr[1];
             if (hr[2]) {  // a large round: the multi-kernel path
@@ -2722,7 +2832,8 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
                     (void *)to, (void *)giso, (void *)gseq, (void *)gseq_acc, (void *)ev_from, (void *)ev_to,
                     (void *)sg_big, (void *)sg_ctr,
                     (void *)ek, (void *)ekt, (void *)evv, (void *)evt, (void *)ecount, (void *)sres, (void *)pdense,
-                    (void *)ptouched})
+                    (void *)ptouched, (void *)huge_scr, (void *)hv_sg,
+                    (void *)hv_ev, (void *)mv_scr})
         c.free(p);
 }
 
