@@ -162,6 +162,21 @@ def check_config(name, coarsen_levels, refine_levels, log=print, procs=None):
             rec = {"level": lv, "nodes": int(gl[0]), "pins": int(len(gl[2]) + len(gl[4])),
                    "coarse_nodes": int(c[0]), "pairs": int(np.sum(mine["match"] != np.arange(gl[0])) // 2),
                    "bit_exact": bool(ok), "oracle_s": round(secs, 2)}
+            if not ok and ref is not None:  # diagnostics: which payload differs, and where first
+                diff = {}
+                for k in ("pair", "score", "match", "gamma"):
+                    a_, b_ = np.asarray(ref[k]), np.asarray(mine[k])
+                    if a_.shape != b_.shape:
+                        diff[k] = f"shape {a_.shape} vs {b_.shape}"
+                    elif not np.array_equal(a_, b_):
+                        bad = np.flatnonzero(a_ != b_)
+                        i0 = int(bad[0])
+                        diff[k] = {"count": int(len(bad)), "first": i0, "oracle": a_[i0].item(),
+                                   "gpu": b_[i0].item()}
+                        if k == "pair":
+                            diff[k]["score_oracle"] = float(ref["score"][i0])
+                            diff[k]["score_gpu"] = float(mine["score"][i0])
+                rec["diff"] = diff
             out["coarsen"].append(rec)
         else:
             a, conns, evs = ref
