@@ -1811,7 +1811,8 @@ void contract_count(Ctx &c, DLevel &fine, const int32_t *match, const uint8_t *i
     // short lists on average (the tail of C3): slots flattened over the warp;
     // longer ones: a warp per h-edge
     // (when there are enough h-edges to give every resident warp a batch)
-    s.flat = fine.Ps + fine.Pd + fine.U <= 3 * 12 * (int64_t)E && (int64_t)E >= 32 * 48 * (int64_t)c.num_sms;
+    const int64_t flat_min = tiers().flat_edges >= 0 ? tiers().flat_edges : 32 * 48 * (int64_t)c.num_sms;
+    s.flat = fine.Ps + fine.Pd + fine.U <= 3 * 12 * (int64_t)E && (int64_t)E >= flat_min;
     if (s.fused) {
         int32_t *cnt = c.alloc<int32_t>(3 * (int64_t)E);
         s.slow = c.alloc<uint8_t>(3 * (int64_t)E);

@@ -255,6 +255,9 @@ struct Tiers {
     int small_k = 4096;       // propose: K up to which escalated nodes use dense shared arrays
     int pr_hub_inc = 128;     // propose: incident h-edges above which a node is split over many CTAs
     int edge_movers = 32;     // events / sequence gains: movers per h-edge for the thread tier (<= 32)
+    int seg_smem = 8192;      // per-segment sorts / wide run updates: longest list kept in shared memory
+    int mv_block = 2048;      // events / sequence gains: movers per h-edge for the shared-memory block tier
+    int flat_edges = -1;      // contraction: fewest h-edges for the flattened kernel (-1: 48 warps per SM)
 };
 const Tiers &tiers();
 

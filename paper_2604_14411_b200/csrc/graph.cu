@@ -181,6 +181,19 @@ void build_level0(Ctx &c, const DInput &in, DLevel &L) {
     L.size = in.size;
     L.borrowed = true;
     L.maxp = in.max_edge_pins;
+    // Sides in ascending order.  The reference keeps level-0 sides as given
+    // but every coarse side is sorted unique (coarsen.py:163-166) and no
+    // result depends on the level-0 order; sorted sides
+    // let contraction keep an h-edge's gamma image as is whenever no absorbed
+    // member sits in it (gamma is increasing on the cluster minima).
+    {
+        int32_t *tmp = c.alloc<int32_t>(std::max<int64_t>(std::max(in.Ps, in.Pd), 1));
+        seg_sort(c, in.E, in.src_off, in.src_dat, nullptr, tmp);
+        c.d2d(in.src_dat, tmp, in.Ps);
+        seg_sort(c, in.E, in.dst_off, in.dst_dat, nullptr, tmp);
+        c.d2d(in.dst_dat, tmp, in.Pd);
+        c.free(tmp);
+    }
     derive_incidence(c, L);
 }
 

@@ -610,7 +610,7 @@ __global__ void k_seg_sort_warp(const int64_t *off, const int32_t *dat, const in
 }
 
 __global__ void k_seg_sort_block(const int64_t *off, const int32_t *dat, const int32_t *map, int32_t *tmp,
-                                 const int32_t *list, const int32_t *counts, int32_t *err) {
+                                 const int32_t *list, const int32_t *counts, int smem_max) {
     pdl_entry();
     extern __shared__ uint32_t sbuf[];
     const int n = counts[1];
@@ -618,8 +618,7 @@ __global__ void k_seg_sort_block(const int64_t *off, const int32_t *dat, const i
         int64_t s = list[t];
         int64_t lo = off[s];
         int len = (int)(off[s + 1] - lo);
-        if (len > kMaxSegSort) {  // in place in global memory (tmp is the segment's own output)
-            (void)err;
+        if (len > smem_max) {  // in place in global memory (tmp is the segment's own output)
             __syncthreads();
             for (int64_t i = threadIdx.x; i < len; i += blockDim.x) {
                 const int32_t x = dat[lo + i];
@@ -658,7 +657,8 @@ void seg_sort(Ctx &c, int64_t nseg, const int64_t *off, const int32_t *dat, cons
     DHGP_LAUNCHED(c);
     // segments above kMaxSegSort (shared memory) sort in place in global memory
     pdl_launch(k_seg_sort_block, (unsigned)(c.num_sms), 1024, kMaxSegSort * sizeof(uint32_t), c.stream, off, dat, map, tmp,
-                                                                                                 bl, cnt, cnt + 2);
+                                                                                                 bl, cnt,
+               std::min<int>((int)kMaxSegSort, tiers().seg_smem));
     DHGP_LAUNCHED(c);
     c.free(wl);
     c.free(bl);

@@ -1057,7 +1057,7 @@ constexpr int kEvParts = 2 * kEvBlockMax;  // hash slots (>= distinct parts: 2 p
 __global__ void __launch_bounds__(256) k_inbound_events_block(const int64_t *dst_off, const int32_t *dst_dat, Runs r,
                                        const int32_t *pos, const int32_t *from, const int32_t *to, EvArgs ev,
                                        const int32_t *big_list, const int32_t *big_count, int32_t *huge,
-                                       int32_t *huge_count) {
+                                       int32_t *huge_count, int mv_max) {
     pdl_entry();
     __shared__ uint32_t smv[kEvBlockMax];
     __shared__ int32_t skey[kEvParts];
@@ -1082,7 +1082,7 @@ __global__ void __launch_bounds__(256) k_inbound_events_block(const int64_t *dst
         }
         __syncthreads();
         const int nm = snm;
-        if (nm > kEvBlockMax) {  // global-memory path (k_edge_movers_huge)
+        if (nm > mv_max) {  // global-memory path (k_edge_movers_huge)
             if (threadIdx.x == 0) huge[atomicAdd(huge_count, 1)] = e;
             __syncthreads();
             continue;
@@ -1522,7 +1522,7 @@ constexpr int kSgBlockMax = 2048;
 __global__ void k_seq_gains_edge_block(const int64_t *pin_off, const int32_t *pin_dat, const int64_t *wi, Runs r,
                                        const int32_t *pos, const int32_t *from, const int32_t *to,
                                        unsigned long long *gacc, const int32_t *big_list, const int32_t *big_count,
-                                       int32_t *huge, int32_t *huge_count) {
+                                       int32_t *huge, int32_t *huge_count, int mv_max) {
     pdl_entry();
     __shared__ uint32_t smv[kSgBlockMax];
     __shared__ int32_t sf[kSgBlockMax], st[kSgBlockMax];
@@ -1542,7 +1542,7 @@ __global__ void k_seq_gains_edge_block(const int64_t *pin_off, const int32_t *pi
         }
         __syncthreads();
         const int nm = snm;
-        if (nm > kSgBlockMax) {  // global-memory path (k_edge_movers_huge)
+        if (nm > mv_max) {  // global-memory path (k_edge_movers_huge)
             if (threadIdx.x == 0) huge[atomicAdd(huge_count, 1)] = e;
             __syncthreads();
             continue;
@@ -1956,7 +1956,8 @@ __global__ void __launch_bounds__(1024) k_runs_update_wide(const int32_t *wide, 
                                                            const int32_t *dst_dat, const int32_t *assign,
                                                            const int64_t *wi, Runs r, unsigned long long *conn,
                                                            int64_t *pinbound, int32_t *ndirty, int32_t *nlist,
-                                                           int32_t *ncount, uint8_t *gscr, int64_t gcap) {
+                                                           int32_t *ncount, uint8_t *gscr, int64_t gcap,
+                                                           int smem_max) {
     pdl_entry();
     extern __shared__ unsigned long long smem_u64[];
     __shared__ int32_t s_wsum[32];
@@ -1971,7 +1972,7 @@ __global__ void __launch_bounds__(1024) k_runs_update_wide(const int32_t *wide, 
         const int32_t old = r.len[e];
         // working arrays: shared memory up to kMaxSegSort slots, else this
         // CTA's slice of the global scratch (h-edges of up to gcap pins)
-        const bool huge = len > kMaxSegSort || old > kMaxSegSort;
+        const bool huge = len > smem_max || old > smem_max;
         const int64_t cap = huge ? gcap : kMaxSegSort;
         uint8_t *wbuf = huge ? gscr + (int64_t)blockIdx.x * ((13 * gcap + 15) & ~(int64_t)15) : (uint8_t *)smem_u64;
         uint32_t *sv = (uint32_t *)wbuf;           // [cap] sorted parts
@@ -2348,7 +2349,8 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
     int32_t *sg_big = c.alloc<int32_t>(L.E), *sg_ctr = c.alloc<int32_t>(4);  // [2], [3]: huge-list counts
     // h-edges with more movers than shared memory holds (only possible when
     // an h-edge has more than 2048 pins): huge lists + 20 B/pin scratch per CTA
-    const bool huge_movers = max_edge_pins > std::min(kSgBlockMax, kEvBlockMax);
+    const int mv_max = std::min(std::min(kSgBlockMax, kEvBlockMax), tiers().mv_block);
+    const bool huge_movers = max_edge_pins > mv_max;
     int32_t *hv_sg = nullptr, *hv_ev = nullptr;
     uint8_t *mv_scr = nullptr;
     int mv_grid = 1;
@@ -2390,7 +2392,8 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
     // h-edges beyond shared memory: 13 B per pin slot of global scratch per CTA
     uint8_t *huge_scr = nullptr;
     int huge_grid = c.num_sms;
-    if (max_edge_pins > kMaxSegSort) {
+    const int seg_smem = std::min<int>((int)kMaxSegSort, tiers().seg_smem);
+    if (max_edge_pins > seg_smem) {
         huge_grid = (int)std::max<int64_t>(1, std::min<int64_t>(c.num_sms, (int64_t)(4ll << 30) /
                                                                              (13ll * max_edge_pins)));
         huge_scr = c.alloc<uint8_t>((int64_t)huge_grid * ((13 * (int64_t)max_edge_pins + 15) & ~(int64_t)15));
@@ -2409,7 +2412,8 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
             }
             pdl_launch(k_runs_update_wide, huge_grid, 1024, 13 * kMaxSegSort, c.stream,
                 st.wide, st.ctr + CT_WIDE, st.edirty, L.pin_off, L.pin_dat, L.dst_off, L.dst_dat, assign, W.wi, r,
-                conn_d, pinbound, st.ndirty, st.nlist, st.ctr + CT_NLIST, huge_scr, (int64_t)max_edge_pins);
+                conn_d, pinbound, st.ndirty, st.nlist, st.ctr + CT_NLIST, huge_scr, (int64_t)max_edge_pins,
+                seg_smem);
             DHGP_LAUNCHED(c);
         }
         if (reset) zero_many(c, {{st.ctr + CT_ELIST, 4}, {st.ctr + CT_WIDE, 4}});
@@ -2655,10 +2659,11 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
                                                              sp ? dM : nullptr);
                     DHGP_LAUNCHED(c);
                     pdl_launch(k_seq_gains_edge_block, c.num_sms, 256, 0, c.stream, L.pin_off, L.pin_dat, W.wi, r, pos, from,
-                                                                             to, gacc, sg_big, sg_ctr, hv_sg, sg_ctr + 2);
+                                                                             to, gacc, sg_big, sg_ctr, hv_sg, sg_ctr + 2,
+                                                                             mv_max);
                     DHGP_LAUNCHED(c);
                     pdl_launch(k_inbound_events_block, c.num_sms, 256, 0, c.stream, L.dst_off, L.dst_dat, r, pos, from, to,
-                                                                             ev, big, ctr, hv_ev, sg_ctr + 3);
+                                                                             ev, big, ctr, hv_ev, sg_ctr + 3, mv_max);
                     DHGP_LAUNCHED(c);
                     if (huge_movers) {  // exit at once when the huge lists are empty
                         pdl_launch(k_edge_movers_huge, mv_grid, 1024, 0, c.stream, 0, L.pin_off, L.pin_dat, W.wi, r,

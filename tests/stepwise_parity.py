@@ -176,6 +176,26 @@ def check_config(name, coarsen_levels, refine_levels, log=print, procs=None):
                         if k == "pair":
                             diff[k]["score_oracle"] = float(ref["score"][i0])
                             diff[k]["score_gpu"] = float(mine["score"][i0])
+                if ref["num_coarse"] != c[0]:
+                    diff["num_coarse"] = [int(ref["num_coarse"]), int(c[0])]
+                for k, v in zip(("src_off", "src_dat", "dst_off", "dst_dat", "node_size"), c[1:]):
+                    a_, b_ = np.asarray(ref[k]), np.asarray(v)
+                    if a_.shape != b_.shape:
+                        diff[k] = f"shape {a_.shape} vs {b_.shape}"
+                    elif not np.array_equal(a_, b_):
+                        bad = np.flatnonzero(a_ != b_)
+                        i0 = int(bad[0])
+                        diff[k] = {"count": int(len(bad)), "first": i0, "oracle": a_[max(0, i0 - 3):i0 + 4].tolist(),
+                                   "gpu": b_[max(0, i0 - 3):i0 + 4].tolist()}
+                        if k.endswith("_dat"):  # the owning h-edge and its lists
+                            off_o = np.asarray(ref[k[:3] + "_off"])
+                            e = int(np.searchsorted(off_o, i0, side="right") - 1)
+                            off_g = np.asarray(c[1] if k == "src_dat" else c[3])
+                            diff[k]["edge"] = e
+                            diff[k]["edge_oracle"] = a_[off_o[e]:off_o[e + 1]].tolist()
+                            diff[k]["edge_gpu"] = b_[off_g[e]:off_g[e + 1]].tolist()
+                            fo, fd = (gl[1], gl[2]) if k == "src_dat" else (gl[3], gl[4])
+                            diff[k]["edge_fine"] = np.asarray(fd[fo[e]:fo[e + 1]]).tolist()
                 rec["diff"] = diff
             out["coarsen"].append(rec)
         else:

@@ -396,10 +396,22 @@ indeg = int(np.bincount(arr[5], minlength=1500).max())
 n, w, so, sd, do, dd = arr
 cases.append((dp.Hypergraph._from_csr(n, w, dp.CsrSets(so, sd), dp.CsrSets(do, dd)), 128, max(indeg, 256)))
 for g, om, de in cases:
-    part, st = dp.partition(g, dp.Config(dp.Constraints(om, de), max_levels=1 << 20))
-    a, k, ost, _ = orc.partition(*arrays_of(g), g.node_size, max_size=om, max_inbound=de, max_levels=1 << 20)
+    lev = []
+    obs = lambda kind, p: lev.append(p) if kind == "level" else None
+    part, st = dp.partition(g, dp.Config(dp.Constraints(om, de), max_levels=1 << 20), observer=obs)
+    a, k, ost, oev = orc.partition(*arrays_of(g), g.node_size, max_size=om, max_inbound=de, max_levels=1 << 20,
+                                   record=True)
     assert np.array_equal(part.assign, a), "assign differs"
     assert st.levels == ost["levels"] and st.connectivity_trace == ost["connectivity_trace"]
+    olev = [e for e in oev if e["kind"] == "level"]
+    assert len(olev) == len(lev)
+    for e, o in zip(lev, olev):  # every level payload, the coarse graph's side order included
+        f, cm, co = e["forest"], e["cmap"], e["coarse"]
+        for got, key in ((f.pair, "pair"), (f.score, "score"), (f.match, "match"), (cm.gamma, "gamma"),
+                         (co.edge_src.offsets, "src_off"), (co.edge_src.data, "src_dat"),
+                         (co.edge_dst.offsets, "dst_off"), (co.edge_dst.data, "dst_dat"),
+                         (co.node_size, "node_size")):
+            assert np.array_equal(got, o[key]), ("level payload differs", e["index"], key)
 print("forced tiers ok", len(cases))
 """
 
