@@ -496,3 +496,16 @@ def test_connectivity_exact_for_any_weights():
         want = orc.connectivity_value(g.edge_pins.offsets, g.edge_pins.data, w, a)
         assert d.connectivity(g, d.Partitioning(a, 37)) == want, scale
         assert K.connectivity_value(g.edge_pins.offsets, g.edge_pins.data, w, a) == want, scale
+
+
+def test_hedge_beyond_shared_memory_golden():
+    """One h-edge of 8,300 pins (more than the 8,192 slots a per-segment sort
+    or a wide run update keeps in shared memory): the global-memory paths,
+    bit-exact against the reference's own partition (tests/golden/bigedge.npz)."""
+    z = load_npz("bigedge.npz")
+    g = graph([z[f"in_{k}"] for k in ("n", "w", "so", "sd", "do", "dd")])
+    assert int(np.diff(g.edge_pins.offsets).max()) > 8192
+    part, st, _ = run_gpu(g, int(z["omega"]), int(z["delta"]), max_levels=1 << 20)
+    ref = json.loads(bytes(z["stats"]).decode())
+    assert np.array_equal(part.assign, z["assign"]) and part.num_parts == int(z["num_parts"])
+    assert st.levels == ref["levels"] and st.connectivity_trace == ref["trace"]
