@@ -9,6 +9,7 @@
 #include "coarsen.cuh"
 #include "comm.cuh"
 #include "prims.cuh"
+#include "ordered.cuh"
 #include "refine.cuh"
 
 namespace dhgp {
@@ -289,8 +290,230 @@ static void rebuild_levels(Ctx &c, std::vector<DLevel> &levels, size_t hi) {
     c.free(status);
 }
 
+// the "level" observer payload (driver.py:106-116) from device arrays; the
+// scores are scaled-integer histograms times `unit` (the reference's f64)
+static void emit_level_event(Ctx &c, dhgp_observer_fn obs, void *user, int32_t level, const DLevel &f,
+                             const DLevel &cl, int32_t n, const int32_t *pair, const double *score,
+                             const int32_t *match, double unit) {
+    std::vector<int32_t> hp(n), hm(n), hg(n), hsd(cl.Ps), hdd(cl.Pd), hsz(cl.N);
+    std::vector<double> hs(n);
+    std::vector<int64_t> hso((int64_t)cl.E + 1), hdo((int64_t)cl.E + 1);
+    c.d2h(hp.data(), pair, n);
+    c.d2h(hs.data(), score, n);
+    c.d2h(hm.data(), match, n);
+    c.d2h(hg.data(), f.gamma, n);
+    c.d2h(hso.data(), cl.src_off, (int64_t)cl.E + 1);
+    c.d2h(hsd.data(), cl.src_dat, cl.Ps);
+    c.d2h(hdo.data(), cl.dst_off, (int64_t)cl.E + 1);
+    c.d2h(hdd.data(), cl.dst_dat, cl.Pd);
+    c.d2h(hsz.data(), cl.size, cl.N);
+    c.sync();
+    if (unit != 1.0)
+        for (auto &x : hs) x *= unit;
+    dhgp_event ev;
+    memset(&ev, 0, sizeof ev);
+    ev.kind = DHGP_EVENT_LEVEL;
+    ev.level = level;
+    ev.num_nodes = n;
+    ev.num_edges = cl.E;
+    ev.num_coarse = cl.N;
+    ev.pair = hp.data();
+    ev.score = hs.data();
+    ev.match = hm.data();
+    ev.gamma = hg.data();
+    ev.c_src_off = hso.data();
+    ev.c_src_dat = hsd.data();
+    ev.c_dst_off = hdo.data();
+    ev.c_dst_dat = hdd.data();
+    ev.c_node_size = hsz.data();
+    obs(&ev, user);
+}
+
+static RoundObserver round_observer(dhgp_observer_fn obs, void *user, int32_t E) {
+    if (!obs) return RoundObserver();
+    return [obs, user, E](const RoundRecord &r) {
+        dhgp_event ev;
+        memset(&ev, 0, sizeof ev);
+        ev.kind = DHGP_EVENT_ROUND;
+        ev.level = r.level;
+        ev.round = r.round;
+        ev.num_nodes = (int32_t)r.assign.size();
+        ev.num_edges = E;
+        ev.num_parts = r.num_parts;
+        ev.assign = r.assign.data();
+        ev.num_moves = (int32_t)r.node.size();
+        ev.mv_node = r.node.data();
+        ev.mv_from = r.from.data();
+        ev.mv_to = r.to.data();
+        ev.mv_gain_iso = r.gain_iso.data();
+        ev.mv_gain_seq = r.gain_seq.data();
+        ev.k = r.k;
+        ev.total_gain = r.total_gain;
+        ev.active = r.active.data();
+        obs(&ev, user);
+    };
+}
+
+// compaction (driver.py:137-143) + check_validity (144-146) of the level-0
+// assignment; fills res.assign / res.num_parts
+static void finish_partition(Ctx &c, const DLevel &L0, const DWeights &W, int32_t *assign, int32_t K, int64_t omega,
+                             int64_t delta, PartitionResult &res) {
+    const int32_t N0 = L0.N;
+    int32_t final_parts = 0;
+    if (N0 > 0) {
+        uint8_t *used = c.alloc<uint8_t>(K);
+        int64_t *rank = c.alloc<int64_t>((int64_t)K + 1);
+        c.zero(used, K);
+        pdl_launch(k_used, (unsigned)cdiv(N0, 256), 256, 0, c.stream, N0, assign, used);
+        DHGP_LAUNCHED(c);
+        scan_excl<uint8_t>(c, used, rank, K);
+        pdl_launch(k_remap, (unsigned)cdiv(N0, 256), 256, 0, c.stream, N0, rank, assign);
+        DHGP_LAUNCHED(c);
+        int64_t fp = 0;
+        c.d2h(&fp, rank + K, 1);
+        c.sync();
+        final_parts = (int32_t)fp;
+        c.free(used);
+        c.free(rank);
+        int64_t *sz = c.alloc<int64_t>(final_parts), *ib = c.alloc<int64_t>(final_parts);
+        evaluate_assign(c, L0, W, assign, final_parts, sz, ib, nullptr);
+        std::vector<int64_t> hsz(final_parts), hib(final_parts);
+        c.d2h(hsz.data(), sz, final_parts);
+        c.d2h(hib.data(), ib, final_parts);
+        res.assign.resize(N0);
+        c.d2h(res.assign.data(), assign, N0);
+        c.sync();
+        c.free(sz);
+        c.free(ib);
+        for (int32_t p = 0; p < final_parts; p++) {
+            if (hsz[p] > omega || hib[p] > delta) {
+                std::string kind = hsz[p] > omega ? "size" : "inbound";
+                int64_t actual = hsz[p] > omega ? hsz[p] : hib[p];
+                int64_t limit = hsz[p] > omega ? omega : delta;
+                throw Error{DHGP_ERR_INVALID_RESULT,
+                            "internal error: produced an invalid partitioning: [Violation(part=" + std::to_string(p) +
+                                ", kind='" + kind + "', actual=" + std::to_string(actual) +
+                                ", limit=" + std::to_string(limit) + ")]"};
+            }
+        }
+    }
+    res.num_parts = final_parts;
+}
+
 static double now_ms() {
     return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+// partition for weights outside the exact-integer contract: the same level
+// loop with the reference-order f64 scoring and refinement of ordered.cuh
+// (weight-independent phases — incidence, matching, contraction — are the
+// production kernels).  Every level is kept (no checkpoint / rebuild).
+static void run_partition_ordered(Ctx &c, const DInput &in, const dhgp_config &cfg, DWeights &W,
+                                  PartitionResult &res, dhgp_observer_fn obs, void *user) {
+    const int64_t omega = cfg.max_size, delta = cfg.max_inbound;
+    const int32_t N0 = in.N;
+    std::vector<DLevel> levels(1);
+    int64_t *status = nullptr;
+    int32_t *assign = nullptr, *assign2 = nullptr;
+    try {
+        build_level0(c, in, levels[0]);
+        const double t0 = now_ms();
+        const int64_t target = (N0 + omega - 1) / omega;
+        status = c.alloc<int64_t>(kStatusWords);
+        while (levels.back().N > target) {
+            if ((int64_t)levels.size() - 1 >= cfg.max_levels)
+                throw Error{DHGP_ERR_MAX_LEVELS, "coarsening exceeded max_levels=" + std::to_string(cfg.max_levels) +
+                                                     " (" + std::to_string(levels.back().N) + " nodes, target " +
+                                                     std::to_string(target) + ")"};
+            const int32_t n = levels.back().N;
+            int32_t *pair = c.alloc<int32_t>(n), *match = c.alloc<int32_t>(n), *claim = c.alloc<int32_t>(n);
+            double *score = c.alloc<double>(n);
+            uint8_t *isrep = c.alloc<uint8_t>(n);
+            c.zero(status, kStatusWords);
+            ord_score(c, levels.back(), W.w, omega, delta, pair, score);
+            launch_matching(c, n, pair, score, match, isrep, claim, status);
+            DLevel coarse;
+            ContractScratch cs;
+            contract_count(c, levels.back(), match, isrep, coarse, cs, status);
+            LevelStatus st;
+            c.d2h((int64_t *)&st, status, kStatusWords);
+            c.sync();
+            if ((st.bad_cert || st.long_run) && matching_fallbacks(c, n, pair, score, match, isrep, claim, st)) {
+                contract_release(c, cs);
+                coarse.release(c);
+                c.free(levels.back().gamma);
+                levels.back().gamma = nullptr;
+                c.zero(status, kStatusWords);
+                contract_count(c, levels.back(), match, isrep, coarse, cs, status);
+                const int64_t moved = st.moved;
+                c.d2h((int64_t *)&st, status, kStatusWords);
+                c.sync();
+                st.moved = moved;
+            }
+            const bool stop = st.moved == 0;
+            if (stop) {
+                contract_release(c, cs);
+                coarse.release(c);
+                c.free(levels.back().gamma);
+                levels.back().gamma = nullptr;
+            } else {
+                contract_write(c, levels.back(), coarse, cs, st);
+                levels.push_back(coarse);
+                if (obs)
+                    emit_level_event(c, obs, user, (int32_t)levels.size() - 2, levels[levels.size() - 2],
+                                     levels.back(), n, pair, score, match, 1.0);
+            }
+            contract_release_members(c, cs);
+            for (void *q : {(void *)pair, (void *)match, (void *)claim, (void *)score, (void *)isrep}) c.free(q);
+            if (stop) break;
+        }
+        c.free(status);
+        status = nullptr;
+        const double t1 = now_ms();
+        // ---- initial partitioning + uncoarsening (driver.py:121-134) -----------
+        const int32_t K = levels.back().N;
+        assign = c.alloc<int32_t>(std::max(N0, 1));
+        assign2 = c.alloc<int32_t>(std::max(N0, 1));
+        iota_i32(c, assign, K);
+        res.trace.assign(levels.size(), {});
+        for (auto &L : levels) {
+            DLevel m;
+            m.N = L.N;
+            m.E = L.E;
+            m.Ps = L.Ps;
+            m.Pd = L.Pd;
+            res.levels_meta.push_back(m);
+        }
+        RoundObserver robs = round_observer(obs, user, in.E);
+        const int64_t nl = (int64_t)levels.size();
+        for (int64_t li = nl - 1; li >= 0; li--) {
+            if (li < nl - 1) {
+                ord_project(c, levels[li].N, levels[li].gamma, assign, assign2);
+                std::swap(assign, assign2);
+                levels[li + 1].release(c);
+            }
+            ord_refine_level(c, levels[li], W.w, assign, K, omega, delta, cfg.max_rounds, (int32_t)li,
+                             res.trace[nl - 1 - li], obs ? &robs : nullptr);
+        }
+        const double t2 = now_ms();
+        finish_partition(c, levels[0], W, assign, K, omega, delta, res);
+        const double t3 = now_ms();
+        res.phase_ms[0] = t1 - t0;
+        res.phase_ms[1] = t2 - t1;
+        res.phase_ms[2] = t3 - t0;
+    } catch (...) {
+        c.free(status);
+        c.free(assign);
+        c.free(assign2);
+        for (auto &L : levels) L.release(c);
+        W.release(c);
+        throw;
+    }
+    c.free(assign);
+    c.free(assign2);
+    for (auto &L : levels) L.release(c);
+    W.release(c);
+    c.sync();
 }
 
 // partition (driver.py:76-163) over a resident input
@@ -315,11 +538,9 @@ static void run_partition(Ctx &c, const DInput &in, const dhgp_config &cfg, Part
     }
     DWeights W;
     prepare_weights(c, in, W);
-    if (!W.integral) {
-        W.release(c);
-        throw Error{DHGP_ERR_UNSUPPORTED,
-                    "h-edge weights that are not multiples of one power of two 2^-S (S <= 62) with "
-                    "sum(w) * 2^S < 2^53 are outside the exact-integer device path"};
+    if (!W.integral) {  // the reference-order f64 path (ordered.cuh)
+        run_partition_ordered(c, in, cfg, W, res, obs, user);
+        return;
     }
     std::vector<DLevel> levels(1);
     build_level0(c, in, levels[0]);
@@ -415,41 +636,9 @@ static void run_partition(Ctx &c, const DInput &in, const dhgp_config &cfg, Part
                 contract_write(c, levels.back(), coarse, cs, st);
                 levels.push_back(coarse);
             }
-            if (!stop && obs) {
-                DLevel &f = levels[levels.size() - 2];
-                DLevel &cl = levels.back();
-                std::vector<int32_t> hp(n), hm(n), hg(n), hsd(cl.Ps), hdd(cl.Pd), hsz(cl.N);
-                std::vector<double> hs(n);
-                std::vector<int64_t> hso((int64_t)cl.E + 1), hdo((int64_t)cl.E + 1);
-                c.d2h(hp.data(), pair, n);
-                c.d2h(hs.data(), score, n);
-                c.d2h(hm.data(), match, n);
-                c.d2h(hg.data(), f.gamma, n);
-                c.d2h(hso.data(), cl.src_off, (int64_t)cl.E + 1);
-                c.d2h(hsd.data(), cl.src_dat, cl.Ps);
-                c.d2h(hdo.data(), cl.dst_off, (int64_t)cl.E + 1);
-                c.d2h(hdd.data(), cl.dst_dat, cl.Pd);
-                c.d2h(hsz.data(), cl.size, cl.N);
-                c.sync();
-                for (auto &x : hs) x *= W.unit;  // scaled-integer hist -> the reference's f64 value
-                dhgp_event ev;
-                memset(&ev, 0, sizeof ev);
-                ev.kind = DHGP_EVENT_LEVEL;
-                ev.level = (int32_t)levels.size() - 2;
-                ev.num_nodes = n;
-                ev.num_edges = cl.E;
-                ev.num_coarse = cl.N;
-                ev.pair = hp.data();
-                ev.score = hs.data();
-                ev.match = hm.data();
-                ev.gamma = hg.data();
-                ev.c_src_off = hso.data();
-                ev.c_src_dat = hsd.data();
-                ev.c_dst_off = hdo.data();
-                ev.c_dst_dat = hdd.data();
-                ev.c_node_size = hsz.data();
-                obs(&ev, user);
-            }
+            if (!stop && obs)
+                emit_level_event(c, obs, user, (int32_t)levels.size() - 2, levels[levels.size() - 2], levels.back(),
+                                 n, pair, score, match, W.unit);
             free_carry();
             if (!stop && inc_score) {  // this level's choices and clusters feed the next scoring
                 prev_pair = pair;
@@ -503,30 +692,7 @@ static void run_partition(Ctx &c, const DInput &in, const dhgp_config &cfg, Part
         m.Pd = L.Pd;
         res.levels_meta.push_back(m);
     }
-    RoundObserver robs;
-    if (obs) {
-        robs = [&](const RoundRecord &r) {
-            dhgp_event ev;
-            memset(&ev, 0, sizeof ev);
-            ev.kind = DHGP_EVENT_ROUND;
-            ev.level = r.level;
-            ev.round = r.round;
-            ev.num_nodes = (int32_t)r.assign.size();
-            ev.num_edges = in.E;
-            ev.num_parts = r.num_parts;
-            ev.assign = r.assign.data();
-            ev.num_moves = (int32_t)r.node.size();
-            ev.mv_node = r.node.data();
-            ev.mv_from = r.from.data();
-            ev.mv_to = r.to.data();
-            ev.mv_gain_iso = r.gain_iso.data();
-            ev.mv_gain_seq = r.gain_seq.data();
-            ev.k = r.k;
-            ev.total_gain = r.total_gain;
-            ev.active = r.active.data();
-            obs(&ev, user);
-        };
-    }
+    RoundObserver robs = round_observer(obs, user, in.E);
     // incremental refinement (refine.cuh) unless DHGP_FULL_REFINE=1 (tests:
     // both modes)
     RefineState rst;
@@ -550,45 +716,7 @@ static void run_partition(Ctx &c, const DInput &in, const dhgp_config &cfg, Part
         refine_state_release(c, rst);
         const double t2 = now_ms();
         // ---- compaction (driver.py:137-143) + check_validity (144-146) ------
-        int32_t final_parts = 0;
-        if (N0 > 0) {
-            uint8_t *used = c.alloc<uint8_t>(K);
-            int64_t *rank = c.alloc<int64_t>((int64_t)K + 1);
-            c.zero(used, K);
-            pdl_launch(k_used, (unsigned)cdiv(N0, 256), 256, 0, c.stream, N0, assign, used);
-            DHGP_LAUNCHED(c);
-            scan_excl<uint8_t>(c, used, rank, K);
-            pdl_launch(k_remap, (unsigned)cdiv(N0, 256), 256, 0, c.stream, N0, rank, assign);
-            DHGP_LAUNCHED(c);
-            int64_t fp = 0;
-            c.d2h(&fp, rank + K, 1);
-            c.sync();
-            final_parts = (int32_t)fp;
-            c.free(used);
-            c.free(rank);
-            int64_t *sz = c.alloc<int64_t>(final_parts), *ib = c.alloc<int64_t>(final_parts);
-            evaluate_assign(c, levels[0], W, assign, final_parts, sz, ib, nullptr);
-            std::vector<int64_t> hsz(final_parts), hib(final_parts);
-            c.d2h(hsz.data(), sz, final_parts);
-            c.d2h(hib.data(), ib, final_parts);
-            res.assign.resize(N0);
-            c.d2h(res.assign.data(), assign, N0);
-            c.sync();
-            c.free(sz);
-            c.free(ib);
-            for (int32_t p = 0; p < final_parts; p++) {
-                if (hsz[p] > omega || hib[p] > delta) {
-                    std::string kind = hsz[p] > omega ? "size" : "inbound";
-                    int64_t actual = hsz[p] > omega ? hsz[p] : hib[p];
-                    int64_t limit = hsz[p] > omega ? omega : delta;
-                    throw Error{DHGP_ERR_INVALID_RESULT,
-                                "internal error: produced an invalid partitioning: [Violation(part=" +
-                                    std::to_string(p) + ", kind='" + kind + "', actual=" + std::to_string(actual) +
-                                    ", limit=" + std::to_string(limit) + ")]"};
-                }
-            }
-        }
-        res.num_parts = final_parts;
+        finish_partition(c, levels[0], W, assign, K, omega, delta, res);
         const double t3 = now_ms();
         res.phase_ms[0] = t1 - t0;
         res.phase_ms[1] = t2 - t1;

@@ -751,3 +751,374 @@ int dhgp_build_events_and_select(int32_t N, const int64_t *in_off, const int32_t
 }
 
 }  // extern "C"
+
+// ===========================================================================
+// The reference-order f64 path (ordered.cuh): device launchers over the seam
+// kernels above plus the candidate walk.
+// ===========================================================================
+#include "ordered.cuh"
+
+namespace dhgp {
+namespace ordk {
+// warp per node: repeated argmax over the node's neighbour slots in (hist
+// desc, id desc) order — the order np.lexsort((-ids, -hist, seg)) gives
+// (coarsen.py:118-120) — first one passing the size and inbound-union checks
+// (_kernels.pyx:75-103); slots failing a check are marked taken
+__global__ void k_ord_select(int32_t N, const int64_t *nb_off, const int32_t *nb_dat, const double *hist,
+                             const int32_t *size, const int64_t *in_off, const int32_t *in_dat, int64_t omega,
+                             int64_t delta, uint8_t *taken, int32_t *pair, double *score) {
+    pdl_entry();
+    const int lane = lane_id();
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t n = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id(); n < N; n += nw) {
+        const int64_t lo = nb_off[n], hi = nb_off[n + 1];
+        const int64_t szn = size[n];
+        for (int64_t j = lo + lane; j < hi; j += 32) taken[j] = szn + size[nb_dat[j]] > omega;
+        __syncwarp();
+        int32_t best_m = -1;
+        double best_h = 0.0;
+        while (true) {
+            double bh = 0.0;
+            int32_t bm = -1;
+            int64_t bj = -1;
+            for (int64_t j = lo + lane; j < hi; j += 32) {
+                if (taken[j]) continue;
+                const double h = hist[j];
+                const int32_t m = nb_dat[j];
+                if (bj < 0 || h > bh || (h == bh && m > bm)) {
+                    bh = h;
+                    bm = m;
+                    bj = j;
+                }
+            }
+            for (int d = 16; d > 0; d >>= 1) {
+                const double oh = __shfl_xor_sync(FULL_MASK, bh, d);
+                const int32_t om = __shfl_xor_sync(FULL_MASK, bm, d);
+                const int64_t oj = __shfl_xor_sync(FULL_MASK, bj, d);
+                if (oj >= 0 && (bj < 0 || oh > bh || (oh == bh && om > bm))) {
+                    bh = oh;
+                    bm = om;
+                    bj = oj;
+                }
+            }
+            if (bj < 0) break;
+            // |in(n) u in(m)| <= delta
+            const int64_t nlo = in_off[n], nn = in_off[n + 1] - nlo, mlo = in_off[bm], nm = in_off[bm + 1] - mlo;
+            int64_t extra = 0;
+            for (int64_t k = lane; k < nm; k += 32) extra += bsearch_dev(in_dat, nlo, nlo + nn, in_dat[mlo + k]) < 0;
+            for (int d = 16; d > 0; d >>= 1) extra += __shfl_xor_sync(FULL_MASK, extra, d);
+            if (nn + extra <= delta) {
+                best_m = bm;
+                best_h = bh;
+                break;
+            }
+            if (lane == 0) taken[bj] = 1;
+            __syncwarp();
+        }
+        if (lane == 0) {
+            pair[n] = best_m;
+            score[n] = best_m >= 0 ? best_h : 0.0;
+        }
+        __syncwarp();
+    }
+}
+__global__ void k_ord_pinbound(int64_t EK, int32_t K, const int32_t *pins_in, int64_t *pinb) {
+    pdl_entry();
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < EK; i += (int64_t)gridDim.x * blockDim.x)
+        if (pins_in[i] > 0) atomicAdd((unsigned long long *)&pinb[i % K], 1ull);
+}
+__global__ void k_ord_psizes(int32_t N, const int32_t *assign, const int32_t *size, int64_t *psizes) {
+    pdl_entry();
+    const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (n < N) atomicAdd((unsigned long long *)&psizes[assign[n]], (unsigned long long)(int64_t)size[n]);
+}
+__global__ void k_ord_flags(int32_t N, const int32_t *target, uint8_t *flags) {
+    pdl_entry();
+    const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (n < N) flags[n] = target[n] >= 0;
+}
+// movers in ascending node order, keyed by descending gain (gains are > 0,
+// so the complemented bit pattern orders them): a stable sort by the key
+// gives (gain desc, node asc) (refine.py:108-110)
+__global__ void k_ord_mover_keys(int32_t N, const uint8_t *flags, const int64_t *mpos, const double *gain,
+                                 uint64_t *keys, uint32_t *vals) {
+    pdl_entry();
+    const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (n >= N || !flags[n]) return;
+    keys[mpos[n]] = ~(uint64_t)__double_as_longlong(gain[n]);
+    vals[mpos[n]] = (uint32_t)n;
+}
+__global__ void k_ord_moves(int64_t M, const uint32_t *vals, const int32_t *assign, const int32_t *target,
+                            const double *gain, int32_t *node, int32_t *from, int32_t *to, double *giso,
+                            int64_t *pos) {
+    pdl_entry();
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= M) return;
+    const int32_t n = (int32_t)vals[i];
+    node[i] = n;
+    from[i] = assign[n];
+    to[i] = target[n];
+    giso[i] = gain[n];
+    pos[n] = i;
+}
+__global__ void k_ord_apply(int64_t k, const int32_t *node, const int32_t *to, int32_t *assign) {
+    pdl_entry();
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < k) assign[node[i]] = to[i];
+}
+__global__ void k_ord_project(int32_t N, const int32_t *gamma, const int32_t *coarse, int32_t *fine) {
+    pdl_entry();
+    const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v < N) fine[v] = coarse[gamma[v]];
+}
+}  // namespace ordk
+using namespace ordk;
+
+void ord_neighbors(Ctx &c, const DLevel &L, int64_t **nb_off, int32_t **nb_dat, int64_t *nnz_out) {
+    const int32_t N = L.N;
+    int64_t *cnt = c.alloc<int64_t>(N), *xoff = c.alloc<int64_t>((int64_t)N + 1);
+    int64_t X = 0;
+    if (N > 0) {
+        pdl_launch(k_nbr_count, (unsigned)cdiv(N, 256), 256, 0, c.stream, N, L.inc_off, L.inc_dat, L.pin_off, cnt);
+        DHGP_LAUNCHED(c);
+    }
+    scan_excl<int64_t>(c, cnt, xoff, N);
+    c.d2h(&X, xoff + N, 1);
+    c.sync();
+    uint64_t *k = c.alloc<uint64_t>(X), *kt = c.alloc<uint64_t>(X);
+    uint32_t *v = c.alloc<uint32_t>(X), *vt = c.alloc<uint32_t>(X);
+    if (N > 0) {
+        pdl_launch(k_nbr_expand, (unsigned)cdiv(N, 256), 256, 0, c.stream, N, L.inc_off, L.inc_dat, L.pin_off,
+                   L.pin_dat, xoff, k, v);
+        DHGP_LAUNCHED(c);
+    }
+    radix_sort_pairs(c, k, v, kt, vt, X, nullptr, 32 + bitlen((uint64_t)(N > 0 ? N - 1 : 0)));
+    uint8_t *keep = c.alloc<uint8_t>(X);
+    int64_t *kpos = c.alloc<int64_t>(X + 1);
+    c.zero(cnt, N);
+    if (X > 0) {
+        pdl_launch(k_nbr_keep, (unsigned)cdiv(X, 256), 256, 0, c.stream, X, k, keep, cnt);
+        DHGP_LAUNCHED(c);
+    }
+    scan_excl<uint8_t>(c, keep, kpos, X);
+    int64_t nnz = 0;
+    c.d2h(&nnz, kpos + X, 1);
+    c.sync();
+    int32_t *out = c.alloc<int32_t>(std::max<int64_t>(nnz, 1));
+    if (X > 0) {
+        pdl_launch(k_nbr_write, (unsigned)cdiv(X, 256), 256, 0, c.stream, X, k, keep, kpos, out);
+        DHGP_LAUNCHED(c);
+    }
+    scan_excl<int64_t>(c, cnt, xoff, N);
+    for (void *p : {(void *)cnt, (void *)k, (void *)kt, (void *)v, (void *)vt, (void *)keep, (void *)kpos}) c.free(p);
+    *nb_off = xoff;
+    *nb_dat = out;
+    *nnz_out = nnz;
+}
+
+void ord_fill_hist(Ctx &c, const DLevel &L, const double *w, const int64_t *nb_off, const int32_t *nb_dat,
+                   double *hist) {
+    int64_t nnz = 0;
+    c.d2h(&nnz, nb_off + L.N, 1);
+    c.sync();
+    c.zero(hist, nnz);
+    if (L.N > 0) {
+        pdl_launch(k_fill_hist, (unsigned)std::min<int64_t>(cdiv(L.N, 8), (int64_t)c.num_sms * 16), 256, 0, c.stream,
+                   L.N, L.inc_off, L.inc_dat, L.pin_off, L.pin_dat, w, nb_off, nb_dat, hist);
+        DHGP_LAUNCHED(c);
+    }
+}
+
+void ord_select(Ctx &c, const DLevel &L, const int64_t *nb_off, const int32_t *nb_dat, const double *hist,
+                int64_t nnz, int64_t omega, int64_t delta, int32_t *pair, double *score) {
+    if (L.N == 0) return;
+    uint8_t *taken = c.alloc<uint8_t>(std::max<int64_t>(nnz, 1));
+    pdl_launch(k_ord_select, (unsigned)std::min<int64_t>(cdiv(L.N, 8), (int64_t)c.num_sms * 16), 256, 0, c.stream,
+               L.N, nb_off, nb_dat, hist, L.size, L.in_off, L.in_dat, omega, delta, taken, pair, score);
+    DHGP_LAUNCHED(c);
+    c.free(taken);
+}
+
+void ord_dense_pins(Ctx &c, const DLevel &L, const int32_t *assign, int32_t K, int32_t *pins, int32_t *pins_in) {
+    c.zero(pins, (int64_t)L.E * K);
+    c.zero(pins_in, (int64_t)L.E * K);
+    if (L.E > 0) {
+        pdl_launch(k_dense_pins, (unsigned)cdiv(L.E, 256), 256, 0, c.stream, L.E, L.pin_off, L.pin_dat, assign, K, pins);
+        DHGP_LAUNCHED(c);
+        pdl_launch(k_dense_pins, (unsigned)cdiv(L.E, 256), 256, 0, c.stream, L.E, L.dst_off, L.dst_dat, assign, K,
+                   pins_in);
+        DHGP_LAUNCHED(c);
+    }
+}
+
+void ord_propose(Ctx &c, const DLevel &L, const double *w, const int32_t *pins, int32_t K, const int32_t *assign,
+                 const int64_t *psizes, int64_t omega, int32_t *target, double *gain) {
+    const int32_t N = L.N;
+    if (N == 0) return;
+    int64_t *work = c.alloc<int64_t>(N), *woff = c.alloc<int64_t>((int64_t)N + 1);
+    pdl_launch(k_node_work, (unsigned)cdiv(N, 256), 256, 0, c.stream, N, L.inc_off, L.inc_dat, L.pin_off, work);
+    DHGP_LAUNCHED(c);
+    scan_excl<int64_t>(c, work, woff, N);
+    int64_t X = 0;
+    c.d2h(&X, woff + N, 1);
+    c.sync();
+    int32_t *cand = c.alloc<int32_t>(std::max<int64_t>(X, 1)), *ep = c.alloc<int32_t>(std::max<int64_t>(X, 1));
+    double *pres = c.alloc<double>(std::max<int64_t>(X, 1));
+    pdl_launch(k_propose_dense, (unsigned)cdiv(N, 128), 128, 0, c.stream, N, L.inc_off, L.inc_dat, L.pin_off,
+               L.pin_dat, w, pins, K, assign, psizes, L.size, omega, woff, cand, pres, ep, target, gain);
+    DHGP_LAUNCHED(c);
+    for (void *p : {(void *)work, (void *)woff, (void *)cand, (void *)ep, (void *)pres}) c.free(p);
+}
+
+void ord_seq_gains(Ctx &c, const DLevel &L, const double *w, const int32_t *pins, int32_t K, int32_t M,
+                   const int32_t *node, const int32_t *from, const int32_t *to, const double *giso,
+                   const int64_t *pos, double *gseq) {
+    if (M <= 0) return;
+    pdl_launch(k_seq_dense, (unsigned)cdiv(M, 128), 128, 0, c.stream, M, L.inc_off, L.inc_dat, L.pin_off, L.pin_dat,
+               w, pins, K, node, from, to, giso, pos, gseq);
+    DHGP_LAUNCHED(c);
+}
+
+void ord_pinbound(Ctx &c, int32_t E, int32_t K, const int32_t *pins_in, int64_t *pinb) {
+    c.zero(pinb, K);
+    const int64_t EK = (int64_t)E * K;
+    if (EK > 0) {
+        pdl_launch(k_ord_pinbound, (unsigned)std::min<int64_t>(cdiv(EK, 256), (int64_t)c.num_sms * 32), 256, 0,
+                   c.stream, EK, K, pins_in, pinb);
+        DHGP_LAUNCHED(c);
+    }
+}
+
+void ord_select_prefix(Ctx &c, const DLevel &L, int32_t K, int32_t M, const int32_t *node, const int32_t *from,
+                       const int32_t *to, const double *gseq, int32_t *pins_in, int64_t *psizes, int64_t *pinb,
+                       int64_t omega, int64_t delta, int64_t *active, int64_t *k_out, double *total) {
+    pdl_launch(k_seam_select, 1, 1, 0, c.stream, M, K, L.in_off, L.in_dat, L.size, node, from, to, gseq, pins_in,
+               psizes, pinb, omega, delta, active, k_out, total);
+    DHGP_LAUNCHED(c);
+}
+
+double ord_connectivity(Ctx &c, const DLevel &L, const double *w, const int32_t *assign) {
+    int32_t *tmp = c.alloc<int32_t>(std::max<int64_t>(L.U, 1));
+    double *contrib = c.alloc<double>(std::max<int64_t>(L.E, 1)), *res = c.alloc<double>(5);
+    seg_sort(c, L.E, L.pin_off, L.pin_dat, assign, tmp);
+    if (L.E > 0) {
+        pdl_launch(k_edge_lambda, (unsigned)cdiv(L.E, 256), 256, 0, c.stream, L.E, L.pin_off, tmp, w, contrib);
+        DHGP_LAUNCHED(c);
+    }
+    exact_sum(c, L.E, contrib, res, res + 1);
+    double h = 0.0;
+    c.d2h(&h, res, 1);
+    c.sync();
+    c.free(tmp);
+    c.free(contrib);
+    c.free(res);
+    return h;
+}
+
+void ord_score(Ctx &c, const DLevel &L, const double *w, int64_t omega, int64_t delta, int32_t *pair,
+               double *score) {
+    int64_t *nbo = nullptr, nnz = 0;
+    int32_t *nbd = nullptr;
+    ord_neighbors(c, L, &nbo, &nbd, &nnz);
+    double *hist = c.alloc<double>(std::max<int64_t>(nnz, 1));
+    ord_fill_hist(c, L, w, nbo, nbd, hist);
+    ord_select(c, L, nbo, nbd, hist, nnz, omega, delta, pair, score);
+    c.free(hist);
+    c.free(nbo);
+    c.free(nbd);
+}
+
+void ord_project(Ctx &c, int32_t N, const int32_t *gamma, const int32_t *coarse, int32_t *fine) {
+    if (N > 0) {
+        pdl_launch(k_ord_project, (unsigned)cdiv(N, 256), 256, 0, c.stream, N, gamma, coarse, fine);
+        DHGP_LAUNCHED(c);
+    }
+}
+
+void ord_refine_level(Ctx &c, const DLevel &L, const double *w, int32_t *assign, int32_t K, int64_t omega,
+                      int64_t delta, int32_t max_rounds, int32_t level, std::vector<double> &conns,
+                      const RoundObserver *obs) {
+    const int32_t N = L.N, E = L.E;
+    const int64_t EK = (int64_t)E * K;
+    int32_t *pins = c.alloc<int32_t>(std::max<int64_t>(EK, 1)), *pins_in = c.alloc<int32_t>(std::max<int64_t>(EK, 1));
+    int64_t *psizes = c.alloc<int64_t>(std::max(K, 1)), *pinb = c.alloc<int64_t>(std::max(K, 1));
+    int32_t *target = c.alloc<int32_t>(std::max(N, 1)), *node = c.alloc<int32_t>(std::max(N, 1));
+    int32_t *from = c.alloc<int32_t>(std::max(N, 1)), *to = c.alloc<int32_t>(std::max(N, 1));
+    double *gain = c.alloc<double>(std::max(N, 1)), *giso = c.alloc<double>(std::max(N, 1));
+    double *gseq = c.alloc<double>(std::max(N, 1)), *tot = c.alloc<double>(1);
+    uint8_t *flags = c.alloc<uint8_t>(std::max(N, 1));
+    int64_t *mpos = c.alloc<int64_t>((int64_t)N + 1), *pos = c.alloc<int64_t>(std::max(N, 1));
+    int64_t *active = c.alloc<int64_t>((int64_t)N + 1), *kd = c.alloc<int64_t>(1);
+    uint64_t *mk = c.alloc<uint64_t>(std::max(N, 1)), *mkt = c.alloc<uint64_t>(std::max(N, 1));
+    uint32_t *mv = c.alloc<uint32_t>(std::max(N, 1)), *mvt = c.alloc<uint32_t>(std::max(N, 1));
+    conns.push_back(ord_connectivity(c, L, w, assign));
+    for (int32_t rnd = 0; rnd < max_rounds; rnd++) {
+        ord_dense_pins(c, L, assign, K, pins, pins_in);
+        c.zero(psizes, K);
+        if (N > 0) {
+            pdl_launch(k_ord_psizes, (unsigned)cdiv(N, 256), 256, 0, c.stream, N, assign, L.size, psizes);
+            DHGP_LAUNCHED(c);
+        }
+        ord_propose(c, L, w, pins, K, assign, psizes, omega, target, gain);
+        int64_t M = 0;
+        if (N > 0) {
+            pdl_launch(k_ord_flags, (unsigned)cdiv(N, 256), 256, 0, c.stream, N, target, flags);
+            DHGP_LAUNCHED(c);
+            scan_excl<uint8_t>(c, flags, mpos, N);
+            c.d2h(&M, mpos + N, 1);
+            c.sync();
+        }
+        if (M == 0) break;
+        pdl_launch(k_ord_mover_keys, (unsigned)cdiv(N, 256), 256, 0, c.stream, N, flags, mpos, gain, mk, mv);
+        DHGP_LAUNCHED(c);
+        radix_sort_pairs(c, mk, mv, mkt, mvt, M, nullptr, 64);
+        fill_i64(c, pos, -1, N);
+        pdl_launch(k_ord_moves, (unsigned)cdiv(M, 256), 256, 0, c.stream, M, mv, assign, target, gain, node, from, to,
+                   giso, pos);
+        DHGP_LAUNCHED(c);
+        ord_seq_gains(c, L, w, pins, K, (int32_t)M, node, from, to, giso, pos, gseq);
+        ord_pinbound(c, E, K, pins_in, pinb);
+        ord_select_prefix(c, L, K, (int32_t)M, node, from, to, gseq, pins_in, psizes, pinb, omega, delta, active, kd,
+                          tot);
+        int64_t k = 0;
+        double total = 0.0;
+        c.d2h(&k, kd, 1);
+        c.d2h(&total, tot, 1);
+        c.sync();
+        if (obs && *obs) {
+            RoundRecord rec;
+            rec.level = level;
+            rec.round = rnd;
+            rec.num_parts = K;
+            rec.k = (int32_t)k;
+            rec.total_gain = total;
+            rec.assign.resize(N);
+            rec.node.resize(M);
+            rec.from.resize(M);
+            rec.to.resize(M);
+            rec.gain_iso.resize(M);
+            rec.gain_seq.resize(M);
+            rec.active.resize(M + 1);
+            c.d2h(rec.assign.data(), assign, N);
+            c.d2h(rec.node.data(), node, M);
+            c.d2h(rec.from.data(), from, M);
+            c.d2h(rec.to.data(), to, M);
+            c.d2h(rec.gain_iso.data(), giso, M);
+            c.d2h(rec.gain_seq.data(), gseq, M);
+            c.d2h(rec.active.data(), active, M + 1);
+            c.sync();
+            (*obs)(rec);
+        }
+        if (k == 0) break;
+        pdl_launch(k_ord_apply, (unsigned)cdiv(k, 256), 256, 0, c.stream, k, node, to, assign);
+        DHGP_LAUNCHED(c);
+        conns.push_back(ord_connectivity(c, L, w, assign));
+    }
+    for (void *p : {(void *)pins, (void *)pins_in, (void *)psizes, (void *)pinb, (void *)target, (void *)node,
+                    (void *)from, (void *)to, (void *)gain, (void *)giso, (void *)gseq, (void *)tot, (void *)flags,
+                    (void *)mpos, (void *)pos, (void *)active, (void *)kd, (void *)mk, (void *)mkt, (void *)mv,
+                    (void *)mvt})
+        c.free(p);
+}
+
+}  // namespace dhgp
