@@ -97,7 +97,7 @@ struct ScoreArgs {
     int32_t *next;        // work counter
     int32_t *big_list;    // nodes escalated to the global dense tier
     int32_t *big_count;
-    int32_t *heavy_list;  // nodes for the block tier (many incident h-edges)
+    int32_t *heavy_list;  // nodes for the 1024-thread tier (hubs, or too many neighbours for a mid table)
     int32_t *heavy_count;
     Tiers t;
     int32_t lo, hi;  // this rank's node range (comm.cuh); [0, N) on one GPU
@@ -121,6 +121,8 @@ struct ScoreArgs {
     // takes every node above kHeavySmallInc incident h-edges (idle SMs
     // otherwise; a node's latency is the level's critical path)
     int32_t heavy_small_list = 0;
+    int32_t *mid_list = nullptr;   // nodes for the 256-thread tier
+    int32_t *mid_count = nullptr;
 };
 constexpr int64_t kHeavySmallInc = 48;
 
@@ -254,11 +256,17 @@ __global__ void __launch_bounds__(SS_WARPS * 32, 3) k_score_warp(ScoreArgs a) {
         if (node == -1) break;
         if (node < 0) continue;
         const int64_t ilo = a.inc_off[node], ihi = a.inc_off[node + 1];
-        const int64_t hthr = (a.heavy_small_list && *a.list_count <= a.heavy_small_list)
-                                 ? min((int64_t)a.t.ss_heavy_inc, kHeavySmallInc)
-                                 : (int64_t)a.t.ss_heavy_inc;
-        if (ihi - ilo > hthr) {  // hub: a whole block per node
-            if (lane == 0) a.heavy_list[atomicAdd(a.heavy_count, 1)] = node;
+        // list mode (merged clusters, rescored nodes): every node above
+        // kHeavySmallInc incident h-edges gets a CTA (a node's latency is the
+        // level's critical path); full scoring: above ss_heavy_inc
+        const int64_t hthr = a.list ? min((int64_t)a.t.ss_heavy_inc, kHeavySmallInc) : (int64_t)a.t.ss_heavy_inc;
+        if (ihi - ilo > hthr) {
+            if (lane == 0) {
+                if (ihi - ilo > a.t.sm_heavy_inc)
+                    a.heavy_list[atomicAdd(a.heavy_count, 1)] = node;
+                else
+                    a.mid_list[atomicAdd(a.mid_count, 1)] = node;
+            }
             continue;
         }
         for (int s = lane; s < SS_CAP; s += 32) {
@@ -295,7 +303,7 @@ __global__ void __launch_bounds__(SS_WARPS * 32, 3) k_score_warp(ScoreArgs a) {
         }, a.work);
         __syncwarp();
         if (sover[w]) {
-            if (lane == 0) a.heavy_list[atomicAdd(a.heavy_count, 1)] = node;
+            if (lane == 0) a.mid_list[atomicAdd(a.mid_count, 1)] = node;
             __syncwarp();
             continue;
         }
@@ -350,6 +358,164 @@ __global__ void __launch_bounds__(SS_WARPS * 32, 3) k_score_warp(ScoreArgs a) {
             }
         }
         __syncwarp();
+    }
+}
+
+// Mid tier: a 256-thread CTA per node with a 4096-slot shared hash table —
+// the merged clusters and rescored nodes of the incremental levels (a few
+// hundred to a few thousand per level, each a few thousand pins), several
+// CTAs per SM so that all of a level's nodes run at once.  The 8 warps
+// flatten the pins of their share of the incident h-edges; nodes with more
+// distinct neighbours than sm_limit go on to the 1024-thread tier.
+constexpr int SM_THREADS = 256;
+constexpr int SM_CAP = 4096;
+template <class Acc>
+constexpr int sm_smem() { return SM_CAP * (4 + (int)sizeof(Acc)); }
+
+template <class Acc>
+__global__ void __launch_bounds__(SM_THREADS) k_score_mid(ScoreArgs a) {
+    pdl_entry();
+    extern __shared__ unsigned long long smem_u64[];
+    Acc *vals = (Acc *)smem_u64;
+    int32_t *keys = (int32_t *)(vals + SM_CAP);
+    __shared__ int32_t snk, s_next;
+    __shared__ volatile int32_t sover;
+    __shared__ long long r_v[SM_THREADS / 32], r_c[SM_THREADS / 32];
+    __shared__ int32_t r_k[SM_THREADS / 32], r_s[SM_THREADS / 32];
+    constexpr int NW = SM_THREADS / 32;
+    const int w = warp_id(), lane = lane_id();
+    const int nmid = *a.mid_count;
+    if (nmid <= (int)gridDim.x / 4) {
+        // few nodes (SMs would idle): the 1024-thread tier (CTA pairs) takes them
+        for (int t = blockIdx.x * SM_THREADS + threadIdx.x; t < nmid; t += gridDim.x * SM_THREADS)
+            a.heavy_list[atomicAdd(a.heavy_count, 1)] = a.mid_list[t];
+        return;
+    }
+    while (true) {
+        if (threadIdx.x == 0) s_next = atomicAdd(a.next + 3, 1);
+        __syncthreads();
+        const int t = s_next;
+        if (t >= nmid) break;
+        const int32_t node = a.mid_list[t];
+        for (int s = threadIdx.x; s < SM_CAP; s += SM_THREADS) {
+            keys[s] = -1;
+            vals[s] = 0;
+        }
+        if (threadIdx.x == 0) {
+            snk = 0;
+            sover = 0;
+        }
+        __syncthreads();
+        const int64_t ilo = a.inc_off[node], ihi = a.inc_off[node + 1];
+        const int bsz = (int)max((int64_t)1, min((int64_t)32, (ihi - ilo + NW - 1) / NW));
+        warp_for_pins<4>(a.inc_dat, ilo, ihi, (int64_t)w * bsz, (int64_t)NW * bsz, a.pin_off, a.pin_dat,
+                         [&](int32_t e, int32_t m) {
+                             if (m == node || sover) return;
+                             const Acc we = (Acc)a.wi[e];
+                             uint32_t h = ((uint32_t)m * 2654435761u) >> (32 - 12);
+                             for (int probe = 0; probe < SM_CAP; probe++) {
+                                 const int slot = (h + probe) & (SM_CAP - 1);
+                                 int k = keys[slot];
+                                 if (k == -1) {
+                                     const int prev = atomicCAS(&keys[slot], -1, m);
+                                     if (prev == -1) {
+                                         if (atomicAdd(&snk, 1) + 1 > a.t.sm_limit) sover = 1;
+                                         k = m;
+                                     } else {
+                                         k = prev;
+                                     }
+                                 }
+                                 if (k == m) {
+                                     atomicAdd(&vals[slot], we);
+                                     return;
+                                 }
+                             }
+                             sover = 1;
+                         },
+                         a.work, bsz);
+        __syncthreads();
+        if (sover) {
+            if (threadIdx.x == 0) a.heavy_list[atomicAdd(a.heavy_count, 1)] = node;
+            __syncthreads();
+            continue;
+        }
+        filter_emit<8>(a, node, keys, vals, threadIdx.x, SM_THREADS, SM_CAP);
+        __syncthreads();
+        int32_t best_m = -1;
+        long long best_v = 0;
+        while (true) {
+            long long bv = -1;
+            int32_t bk = -1, bs = -1;
+            for (int s = threadIdx.x; s < SM_CAP; s += SM_THREADS) {
+                const int k = keys[s];
+                if (k >= 0) {
+                    const long long v = (long long)vals[s];
+                    if (v > bv || (v == bv && k > bk)) {
+                        bv = v;
+                        bk = k;
+                        bs = s;
+                    }
+                }
+            }
+#pragma unroll
+            for (int d = 16; d > 0; d >>= 1) {
+                const long long ov = __shfl_xor_sync(FULL_MASK, bv, d);
+                const int32_t ok = __shfl_xor_sync(FULL_MASK, bk, d), os = __shfl_xor_sync(FULL_MASK, bs, d);
+                if (ov > bv || (ov == bv && ok > bk)) {
+                    bv = ov;
+                    bk = ok;
+                    bs = os;
+                }
+            }
+            if (lane == 0) {
+                r_v[w] = bv;
+                r_k[w] = bk;
+                r_s[w] = bs;
+            }
+            __syncthreads();
+            bv = r_v[0];
+            bk = r_k[0];
+            bs = r_s[0];
+#pragma unroll
+            for (int j = 1; j < NW; j++)
+                if (r_v[j] > bv || (r_v[j] == bv && r_k[j] > bk)) {
+                    bv = r_v[j];
+                    bk = r_k[j];
+                    bs = r_s[j];
+                }
+            __syncthreads();
+            if (bk < 0) break;
+            const int64_t nlo = a.in_off[node], nn = a.in_off[node + 1] - nlo;
+            const int64_t mlo = a.in_off[bk], nm = a.in_off[bk + 1] - mlo;
+            bool ok = true;
+            if (nn + nm > a.delta) {
+                const bool ns = nn <= nm;
+                const int32_t *sp = a.in_dat + (ns ? nlo : mlo), *lp = a.in_dat + (ns ? mlo : nlo);
+                const int64_t cs = ns ? nn : nm, cl = ns ? nm : nn;
+                long long common = 0;
+                for (int64_t i = threadIdx.x; i < cs; i += SM_THREADS) common += bsearch_dev(lp, 0, cl, sp[i]) >= 0;
+                common = warp_sum(common);
+                if (lane == 0) r_c[w] = common;
+                __syncthreads();
+                long long tot = 0;
+#pragma unroll
+                for (int j = 0; j < NW; j++) tot += r_c[j];
+                __syncthreads();
+                ok = nn + nm - tot <= a.delta;
+            }
+            if (ok) {
+                best_m = bk;
+                best_v = bv;
+                break;
+            }
+            if (threadIdx.x == 0) keys[bs] = -2;
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            a.pair[node] = best_m;
+            a.score[node] = best_m >= 0 ? (double)best_v : 0.0;
+        }
+        __syncthreads();
     }
 }
 
@@ -797,7 +963,8 @@ void score_scratch_init(Ctx &c, ScoreScratch &s, int64_t n_cap) {
     s.touched = c.alloc<int32_t>((int64_t)s.blocks * s.cap);
     s.big = c.alloc<int32_t>(s.cap);
     s.heavy = c.alloc<int32_t>(s.cap);
-    s.ctr = c.alloc<int32_t>(3);
+    s.mid = c.alloc<int32_t>(s.cap);
+    s.ctr = c.alloc<int32_t>(6);
     pdl_launch(k_fill_ll, (unsigned)cdiv((int64_t)s.blocks * s.cap, 256), 256, 0, c.stream, s.dense, -1ll,
                                                                                    (int64_t)s.blocks * s.cap);
     DHGP_LAUNCHED(c);
@@ -809,6 +976,7 @@ void score_scratch_release(Ctx &c, ScoreScratch &s) {
     c.free(s.touched);
     c.free(s.big);
     c.free(s.heavy);
+    c.free(s.mid);
     c.free(s.ctr);
     s = ScoreScratch();
 }
@@ -851,6 +1019,10 @@ static void score_attrs(Ctx &c) {
                                    ss_smem<unsigned>()));
     DHGP_CUDA(cudaFuncSetAttribute(k_score_warp<unsigned long long>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    ss_smem<unsigned long long>()));
+    DHGP_CUDA(cudaFuncSetAttribute(k_score_mid<unsigned>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   sm_smem<unsigned>()));
+    DHGP_CUDA(cudaFuncSetAttribute(k_score_mid<unsigned long long>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   sm_smem<unsigned long long>()));
     DHGP_CUDA(cudaFuncSetAttribute(k_score_heavy<unsigned, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    sh_smem<unsigned>()));
     DHGP_CUDA(cudaFuncSetAttribute(k_score_heavy<unsigned long long, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -864,8 +1036,11 @@ static void score_attrs(Ctx &c) {
 
 // the three scoring tiers over all of [a.lo, a.hi) or over a.list
 static void score_tiers(Ctx &c, ScoreArgs a, const DWeights &W, ScoreScratch &s, int32_t n_real) {
-    c.zero(s.ctr, 3);
+    c.zero(s.ctr, 6);
+    a.mid_list = s.mid;
+    a.mid_count = s.ctr + 4;
     const int64_t nmine = a.list ? ((int64_t)1 << 40) : std::max<int64_t>(1, (int64_t)a.hi - a.lo);
+    KScope kw(c, "sc_warp");
     if (W.wsum < (1ll << 32)) {
         static int g32 = resident_grid(c, k_score_warp<unsigned>, SS_WARPS * 32, ss_smem<unsigned>());
         int blocks = (int)std::min<int64_t>(cdiv(nmine, SS_WARPS), g32);
@@ -876,11 +1051,26 @@ static void score_tiers(Ctx &c, ScoreArgs a, const DWeights &W, ScoreScratch &s,
         pdl_launch(k_score_warp<unsigned long long>, blocks, SS_WARPS * 32, ss_smem<unsigned long long>(), c.stream, a);
     }
     DHGP_LAUNCHED(c);
+    kw.close();
+    // mid tier: persistent CTAs over the escalated list (exits when empty)
+    KScope km(c, "sc_mid");
+    if (W.wsum < (1ll << 32)) {
+        static int m32 = resident_grid(c, k_score_mid<unsigned>, SM_THREADS, sm_smem<unsigned>());
+        pdl_launch(k_score_mid<unsigned>, m32, SM_THREADS, sm_smem<unsigned>(), c.stream, a);
+    } else {
+        static int m64 = resident_grid(c, k_score_mid<unsigned long long>, SM_THREADS, sm_smem<unsigned long long>());
+        pdl_launch(k_score_mid<unsigned long long>, m64, SM_THREADS, sm_smem<unsigned long long>(), c.stream, a);
+    }
+    DHGP_LAUNCHED(c);
+    km.close();
     // heavy tier: reads the escalation count on device, exits when zero
+    KScope kh(c, "sc_heavy");
     if (W.wsum < (1ll << 32))
         launch_heavy_pairs<unsigned>(c, a);
     else
         launch_heavy_pairs<unsigned long long>(c, a);
+    kh.close();
+    KScope kd(c, "sc_dense");
     // dense tier: reads the escalation count on device, exits when zero;
     // dense rows have stride s.cap and are restored to -1 after each node
     a.N = (int32_t)s.cap;
@@ -969,12 +1159,14 @@ void score_select_inc(Ctx &c, const DLevel &L, const DWeights &W, int64_t omega,
         a.work = work;
     }
     score_tiers(c, a, W, s, N);
+    KScope kt(c, "sc_tuples");
     static int gq = resident_grid(c, k_inc_tuples_quick, 256, 0);
     pdl_launch(k_inc_tuples_quick, gq, 256, 0, c.stream, a, best, hard, lc + 3);
     DHGP_LAUNCHED(c);
     static int gt = resident_grid(c, k_inc_tuples, 256, 0);
     pdl_launch(k_inc_tuples, gt, 256, 0, c.stream, a, best, hard, lc + 3);
     DHGP_LAUNCHED(c);
+    kt.close();
     pdl_launch(k_inc_finalize, (unsigned)cdiv(N, 256), 256, 0, c.stream, N, kind, thr_s, thr_p, best, cy.gamma_prev, lc + 2,
                                                                 cap, pair, score, list2, lc + 1);
     DHGP_LAUNCHED(c);
@@ -1320,6 +1512,75 @@ __global__ void k_node_count(int64_t nc_cap, const int64_t *d_nc, const int32_t 
 // The count pass also flags, in emark, the h-edges of the absorbed member:
 // only their src / dst / pin lists can map to an unsorted or duplicated
 // gamma image (gamma is strictly increasing on the minimum members).
+// Small unions (the common case: merged clusters of a few members), a warp
+// each: the shorter list S and the running count of its elements absent from
+// the longer list L sit in this warp's shared memory; x = L[i] lands at
+// i + (S-only elements below x), y = S[j] not in L at lb_L(y) + (S-only
+// elements before j).  The count pass is |A| + |B| - |A n B| by searches of
+// S in L.  Larger unions are left to k_node_union (one CTA each).
+constexpr int kWarpUnionS = 512;   // shorter list length for the warp path
+constexpr int kWarpUnionL = 512;   // longer list length for the warp path (longer: a CTA)
+constexpr int UW_WARPS = 4;
+__device__ __forceinline__ bool warp_union_path(int64_t na, int64_t nb) {
+    return min(na, nb) <= kWarpUnionS && max(na, nb) <= kWarpUnionL;
+}
+template <bool WRITE>
+__global__ void __launch_bounds__(UW_WARPS * 32) k_node_union_warp(const int32_t *ma, const int32_t *mb,
+                                                                  const int32_t *mlist, const int32_t *mcount,
+                                                                  NodeFams fs, uint8_t *emark) {
+    pdl_entry();
+    __shared__ int32_t s_val[UW_WARPS][kWarpUnionS], s_pre[UW_WARPS][kWarpUnionS + 1];
+    const NodeFam &f = fs.f[blockIdx.y];
+    const int lane = lane_id(), w = warp_id();
+    int32_t *sv = s_val[w], *sp = s_pre[w];
+    const int n = *mcount;
+    for (int t = blockIdx.x * UW_WARPS + w; t < n; t += gridDim.x * UW_WARPS) {
+        const int32_t cn = mlist[t], a = ma[cn], b = mb[cn];
+        const int64_t alo = f.off[a], na = f.off[a + 1] - alo, blo = f.off[b], nb = f.off[b + 1] - blo;
+        if (!warp_union_path(na, nb)) continue;
+        if (!WRITE && emark && blockIdx.y == 1)
+            for (int64_t i = lane; i < nb; i += 32) emark[f.dat[blo + i]] = 1;
+        const bool a_short = na <= nb;
+        const int32_t *S = f.dat + (a_short ? alo : blo), *L = f.dat + (a_short ? blo : alo);
+        const int ns = (int)(a_short ? na : nb), nl = (int)(a_short ? nb : na);
+        if (!WRITE) {
+            int common = 0;
+            for (int j = lane; j < ns; j += 32) common += bsearch_dev(L, 0, nl, S[j]) >= 0;
+            common = warp_sum(common);
+            if (lane == 0) f.cnt[cn] = na + nb - common;
+            continue;
+        }
+        int32_t *o = f.out + f.out_off[cn];
+        int run = 0;
+        for (int j0 = 0; j0 < ns; j0 += 32) {
+            const int j = j0 + lane;
+            int32_t y = 0;
+            int64_t lb = 0;
+            bool only = false;
+            if (j < ns) {
+                y = S[j];
+                lb = lower_bound_dev<int32_t>(L, 0, nl, y);
+                only = !(lb < nl && L[lb] == y);
+                sv[j] = y;
+            }
+            const uint32_t bal = __ballot_sync(FULL_MASK, only);
+            const int ex = run + __popc(bal & ((1u << lane) - 1u));
+            if (j < ns) {
+                sp[j] = ex;
+                if (only) o[lb + ex] = y;
+            }
+            run += __popc(bal);
+        }
+        if (lane == 0) sp[ns] = run;
+        __syncwarp();
+        for (int i = lane; i < nl; i += 32) {
+            const int32_t x = L[i];
+            o[i + sp[lower_bound_dev<int32_t>(sv, 0, ns, x)]] = x;
+        }
+        __syncwarp();
+    }
+}
+
 constexpr int UN_THREADS = 1024;
 template <bool WRITE>
 __global__ void __launch_bounds__(UN_THREADS) k_node_union(const int32_t *ma, const int32_t *mb, const int32_t *mlist,
@@ -1334,6 +1595,7 @@ __global__ void __launch_bounds__(UN_THREADS) k_node_union(const int32_t *ma, co
     for (int t = blockIdx.x; t < n; t += gridDim.x) {
         const int32_t cn = mlist[t], a = ma[cn], b = mb[cn];
         const int64_t alo = f.off[a], na = f.off[a + 1] - alo, blo = f.off[b], nb = f.off[b + 1] - blo;
+        if (warp_union_path(na, nb)) continue;  // k_node_union_warp
         if (!WRITE && emark && blockIdx.y == 1)
             for (int64_t i = threadIdx.x; i < nb; i += blockDim.x) emark[f.dat[blo + i]] = 1;
         const bool a_short = na <= nb;
@@ -1797,6 +2059,9 @@ void contract_count(Ctx &c, DLevel &fine, const int32_t *match, const uint8_t *i
         pdl_launch(k_node_count, dim3(ga, 2), 256, 0, c.stream, N, d_nc, s.ma, s.mb, fs);
         DHGP_LAUNCHED(c);
         const int words = union_words(c, E);
+        pdl_launch(k_node_union_warp<false>, dim3(4 * c.num_sms, 2), UW_WARPS * 32, 0, c.stream, s.ma, s.mb, s.mlist,
+                   s.mcount, fs, s.emark);
+        DHGP_LAUNCHED(c);
         pdl_launch(k_node_union<false>, dim3(c.num_sms, 2), UN_THREADS, 4 * words, c.stream, s.ma, s.mb, s.mlist, s.mcount, fs,
                                                                                      s.emark, words);
         DHGP_LAUNCHED(c);
@@ -1919,6 +2184,9 @@ void contract_write(Ctx &c, DLevel &fine, DLevel &coarse, ContractScratch &s, co
             pdl_launch(k_node_write, dim3(g, 2), 256, 0, c.stream, st.nc, split, s.ma, s.mb, fs);
             DHGP_LAUNCHED(c);
             const int words = union_words(c, E);
+            pdl_launch(k_node_union_warp<true>, dim3(4 * c.num_sms, 2), UW_WARPS * 32, 0, c.stream, s.ma, s.mb, s.mlist,
+                       s.mcount, fs, nullptr);
+            DHGP_LAUNCHED(c);
             pdl_launch(k_node_union<true>, dim3(c.num_sms, 2), UN_THREADS, 4 * words, c.stream, s.ma, s.mb, s.mlist, s.mcount,
                                                                                         fs, nullptr, words);
             DHGP_LAUNCHED(c);

@@ -15,7 +15,7 @@ struct ScoreScratch {
     int64_t cap = 0;
     int blocks = 0;
     long long *dense = nullptr, *cval = nullptr;
-    int32_t *touched = nullptr, *big = nullptr, *heavy = nullptr, *ctr = nullptr;
+    int32_t *touched = nullptr, *big = nullptr, *heavy = nullptr, *mid = nullptr, *ctr = nullptr;
 };
 void score_scratch_init(Ctx &c, ScoreScratch &s, int64_t n_cap);
 void score_scratch_release(Ctx &c, ScoreScratch &s);

@@ -41,6 +41,8 @@ const Tiers &tiers() {
             x.ss_limit = 3;
             x.ss_heavy_inc = 2;
             x.sh_limit = 6;
+            x.sm_limit = 4;
+            x.sm_heavy_inc = 3;
             x.pr_limit = 2;
             x.pr_heavy_inc = 1;
             x.pr_hub_inc = 6;
