@@ -1867,12 +1867,41 @@ __device__ __forceinline__ int warp_gamma_short(uint32_t g, int len, int32_t *ou
     if (out && head) out[__popc(bal & lt)] = (int32_t)v[0];
     return __popc(bal);
 }
+// count pass, thread per h-edge: an h-edge without an absorbed member keeps
+// every slot of its three lists (gamma is strictly increasing on the cluster
+// minima and the lists are sorted), the others are listed for the warp kernel
+__global__ void k_edge_count_bulk(int32_t E, EdgeFam f0, EdgeFam f1, EdgeFam f2, const uint8_t *emark,
+                                  int32_t *elist, int32_t *ecount) {
+    pdl_entry();
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool marked = e < E && emark[e];
+    if (e < E && !marked) {
+        f0.cnt[e] = (int32_t)(f0.off[e + 1] - f0.off[e]);
+        f1.cnt[e] = (int32_t)(f1.off[e + 1] - f1.off[e]);
+        f2.cnt[e] = (int32_t)(f2.off[e + 1] - f2.off[e]);
+    }
+    const uint32_t bal = __ballot_sync(FULL_MASK, marked);
+    if (!bal) return;
+    const int lane = lane_id(), leader = __ffs(bal) - 1;
+    int base = 0;
+    if (lane == leader) base = atomicAdd(ecount, __popc(bal));
+    base = __shfl_sync(FULL_MASK, base, leader);
+    if (marked) elist[base + __popc(bal & ((1u << lane) - 1u))] = (int32_t)e;
+}
+// Warp per h-edge: the sorted unique gamma image of its three lists.  Count
+// pass: over the listed (marked) h-edges only.  Write pass: every h-edge; an
+// unmarked one is a plain element-wise map (its image is already strictly
+// ascending), a marked one is sorted when needed and de-duplicated.
 __global__ void __launch_bounds__(256) k_contract_edges(int32_t E, const int32_t *gamma, EdgeFam f0, EdgeFam f1,
-                                                        EdgeFam f2, bool write, const uint8_t *emark) {
+                                                        EdgeFam f2, bool write, const uint8_t *emark,
+                                                        const int32_t *elist = nullptr,
+                                                        const int32_t *ecount = nullptr) {
     pdl_entry();
     const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
     const int lane = lane_id();
-    for (int64_t e = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id(); e < E; e += nw) {
+    const int64_t ne = elist ? (int64_t)*ecount : (int64_t)E;
+    for (int64_t idx = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id(); idx < ne; idx += nw) {
+        const int64_t e = elist ? elist[idx] : idx;
         const int64_t l0 = f0.off[e], l1 = f1.off[e], l2 = f2.off[e];
         const int n0 = (int)(f0.off[e + 1] - l0), n1 = (int)(f1.off[e + 1] - l1), n2 = (int)(f2.off[e + 1] - l2);
         if (!write && emark && !emark[e]) {  // no absorbed member: the image keeps every slot
@@ -1880,6 +1909,18 @@ __global__ void __launch_bounds__(256) k_contract_edges(int32_t E, const int32_t
                 f0.cnt[e] = n0;
                 f1.cnt[e] = n1;
                 f2.cnt[e] = n2;
+            }
+            continue;
+        }
+        if (write && emark && !emark[e]) {  // plain map, the three lists' loads issued together
+            int32_t *o0 = f0.out + f0.out_off[e], *o1 = f1.out + f1.out_off[e], *o2 = f2.out + f2.out_off[e];
+            const int nmax = max(n0, max(n1, n2));
+            for (int i = lane; i < nmax; i += 32) {
+                const int32_t x0 = i < n0 ? f0.dat[l0 + i] : 0, x1 = i < n1 ? f1.dat[l1 + i] : 0,
+                              x2 = i < n2 ? f2.dat[l2 + i] : 0;
+                if (i < n0) o0[i] = gamma[x0];
+                if (i < n1) o1[i] = gamma[x1];
+                if (i < n2) o2[i] = gamma[x2];
             }
             continue;
         }
@@ -1909,103 +1950,133 @@ __global__ void __launch_bounds__(256) k_contract_edges(int32_t E, const int32_t
     }
 }
 
-// Flattened contraction of one list family over a batch of 32 h-edges: the
-// warp spreads the batch's list slots over its lanes (as warp_for_pins), so
-// short lists do not leave lanes idle and 32 slots' gamma gathers are in
-// flight together.  A slot is a head when it differs from its predecessor in
-// the same list; a list whose gamma image is not strictly ascending (a
-// displaced cluster member) is "slow" and redone per list by
-// warp_gamma_any.  Count pass: per-list head counts and slow flags; write
-// pass: heads at out_off + (heads before it), with ranks inside a chunk from
-// __match_any_sync over the owning list.
-__device__ __forceinline__ void flat_family(const EdgeFam &f, int64_t e0, int nb, const int32_t *gamma, bool write,
-                                            uint8_t *slow, int32_t *run, uint8_t *bad, const uint8_t *emark) {
-    const int lane = lane_id();
-    const uint32_t lt = (1u << lane) - 1u;
-    int64_t lo = 0;
-    int len = 0;
-    uint8_t sl = 0;
-    bool keep = false;  // count pass, no absorbed member: the image keeps every slot
-    if (lane < nb) {
-        lo = f.off[e0 + lane];
-        len = (int)(f.off[e0 + lane + 1] - lo);
-        if (write) sl = slow[e0 + lane];
-        if (!write && emark && !emark[e0 + lane]) {
-            keep = true;
-            slow[e0 + lane] = 0;
-            f.cnt[e0 + lane] = len;
-            len = 0;
-        }
-    }
-    const int incl = warp_incl_scan(len);
-    const int total = __shfl_sync(FULL_MASK, incl, 31);
-    const int excl = incl - len;
-    run[lane] = 0;
-    bad[lane] = 0;
-    __syncwarp();
-    uint32_t pv = 0;
-    for (int s0 = 0; s0 < total; s0 += 32) {
-        const int s = s0 + lane;
-        int own = 0;
-#pragma unroll
-        for (int step = 16; step > 0; step >>= 1) {
-            const int ex = __shfl_sync(FULL_MASK, excl, own + step);
-            if (ex <= s) own += step;
-        }
-        const bool valid = s < total;
-        const int64_t olo = __shfl_sync(FULL_MASK, lo, own);
-        const int oex = __shfl_sync(FULL_MASK, excl, own);
-        const uint8_t osl = (uint8_t)__shfl_sync(FULL_MASK, (int)sl, own);
-        const uint32_t g = valid ? (uint32_t)gamma[f.dat[olo + (s - oex)]] : 0xffffffffu;
-        const uint32_t up = __shfl_up_sync(FULL_MASK, g, 1);
-        const uint32_t prev = lane == 0 ? pv : up;
-        const bool first = s == oex;
-        if (valid && !first && !(prev < g)) bad[own] = 1;
-        const bool head = valid && (first || g != prev);
-        const uint32_t hm = __ballot_sync(FULL_MASK, head);
-        const uint32_t peers = __match_any_sync(FULL_MASK, valid ? own : 64 + lane);
-        const int rank = __popc(peers & hm & lt);
-        if (write && head && !osl) f.out[f.out_off[e0 + own] + run[own] + rank] = (int32_t)g;
-        __syncwarp();
-        if (valid && lane == 31 - __clz(peers)) run[own] += __popc(peers & hm);
-        pv = __shfl_sync(FULL_MASK, g, 31);
-        __syncwarp();
-    }
-    bool sw = false;  // this lane's list needs the per-list path
-    if (lane < nb) {
-        if (write) {
-            sw = sl;
-        } else if (!keep) {
-            sw = bad[lane];
-            slow[e0 + lane] = (uint8_t)sw;
-            if (!sw) f.cnt[e0 + lane] = run[lane];
-        }
-    }
-    uint32_t m = __ballot_sync(FULL_MASK, sw);
-    while (m) {
-        const int j = __ffs(m) - 1;
-        m &= m - 1;
-        const int64_t e = e0 + j;
-        const int64_t lj = __shfl_sync(FULL_MASK, lo, j);
-        const int nj = __shfl_sync(FULL_MASK, len, j);
-        const int n = warp_gamma_any(f.dat, lj, nj, gamma, write ? f.out + f.out_off[e] : nullptr);
-        if (!write && lane == 0) f.cnt[e] = n;
-    }
-    __syncwarp();
-}
-__global__ void __launch_bounds__(256) k_contract_flat(int32_t E, const int32_t *gamma, EdgeFam f0, EdgeFam f1,
-                                                       EdgeFam f2, bool write, uint8_t *slow,
-                                                       const uint8_t *emark) {
+}  // namespace
+
+namespace {
+__global__ void k_marked_list(int32_t E, const uint8_t *emark, const int64_t *epos, int32_t *elist, int32_t *ecount) {
     pdl_entry();
-    __shared__ int32_t s_run[8][32];
-    __shared__ uint8_t s_bad[8][32];
-    const int w = warp_id();
-    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
-    for (int64_t e0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + w) * 32; e0 < E; e0 += nw * 32) {
-        const int nb = (int)min((int64_t)32, (int64_t)E - e0);
-        flat_family(f0, e0, nb, gamma, write, slow, s_run[w], s_bad[w], emark);
-        flat_family(f1, e0, nb, gamma, write, slow + E, s_run[w], s_bad[w], emark);
-        flat_family(f2, e0, nb, gamma, write, slow + 2 * (int64_t)E, s_run[w], s_bad[w], emark);
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < E && emark[e]) elist[epos[e]] = (int32_t)e;
+    if (e == 0) *ecount = (int32_t)epos[E];
+}
+// Write pass of the unmarked lists: between two marked h-edges every list is
+// the element-wise gamma image at a constant shift (fine offset - coarse
+// offset), so each family's data array is mapped linearly — 16-byte loads,
+// chunks of MG_CHUNK slots per CTA — skipping the marked h-edges' slots (the
+// warp kernel writes those).  A CTA finds the marked h-edges inside its
+// chunk with one search of the ascending marked list and keeps up to
+// MG_LOCAL of them (start, end, shift after) in shared memory.
+constexpr int MG_CHUNK = 8192, MG_LOCAL = 256;
+__global__ void __launch_bounds__(256) k_map_gaps(int32_t E, const int32_t *gamma, EdgeFam f0, EdgeFam f1, EdgeFam f2,
+                                                  const int32_t *elist, const int32_t *ecount) {
+    pdl_entry();
+    __shared__ int64_t s_b[MG_LOCAL], s_e[MG_LOCAL], s_sh[MG_LOCAL];
+    __shared__ int64_t s_base, s_w1;
+    __shared__ int s_k0;
+    const EdgeFam f = blockIdx.y == 0 ? f0 : (blockIdx.y == 1 ? f1 : f2);
+    const int64_t P = f.off[E];
+    const int nm = *ecount;
+    for (int64_t c0 = (int64_t)blockIdx.x * MG_CHUNK; c0 < P; c0 += (int64_t)gridDim.x * MG_CHUNK) {
+        const int64_t c1 = min(P, c0 + MG_CHUNK);
+        if (threadIdx.x < 32) {  // first marked h-edge ending after c0: a 32-ary search by warp 0
+            const int lane = threadIdx.x;
+            int lo = 0, hi = nm;  // answer in [lo, hi]
+            while (hi - lo > 0) {
+                const int64_t span = hi - lo;
+                const int probe = lo + (int)((span * (lane + 1)) / 33);  // 32 pivots inside [lo, hi)
+                const bool le = probe < hi && f.off[elist[probe] + 1] <= c0;
+                const uint32_t bal = __ballot_sync(FULL_MASK, le);
+                // pivots are ascending; the last one that is <= c0 bounds lo, the first one > c0 bounds hi
+                const int nle = __popc(bal);
+                const int plo = nle > 0 ? __shfl_sync(FULL_MASK, probe, nle - 1) + 1 : lo;
+                const int phi = nle < 32 ? __shfl_sync(FULL_MASK, probe, nle) : hi;
+                if (plo == lo && phi == hi) {  // span too small for distinct pivots: finish linearly
+                    int k = lo;
+                    while (k < hi && f.off[elist[k] + 1] <= c0) k++;
+                    lo = hi = k;
+                } else {
+                    lo = plo;
+                    hi = phi;
+                }
+            }
+            if (lane == 0) s_k0 = lo;
+        }
+        __syncthreads();
+        int64_t w0 = c0;
+        while (w0 < c1) {
+            const int k0 = s_k0;
+            if (threadIdx.x == 0) {
+                const int32_t prev = k0 > 0 ? elist[k0 - 1] : -1;
+                s_base = prev >= 0 ? f.off[prev + 1] - f.out_off[prev + 1] : 0;
+            }
+            // the marked h-edges starting before c1, up to MG_LOCAL of them
+            for (int j = threadIdx.x; j < MG_LOCAL; j += blockDim.x) {
+                const int k = k0 + j;
+                if (k < nm) {
+                    const int32_t e = elist[k];
+                    const int64_t b = f.off[e];
+                    if (b < c1) {
+                        s_b[j] = b;
+                        s_e[j] = f.off[e + 1];
+                        s_sh[j] = f.off[e + 1] - f.out_off[e + 1];
+                    } else {
+                        s_b[j] = INT64_MAX;
+                    }
+                } else {
+                    s_b[j] = INT64_MAX;
+                }
+            }
+            static_assert(MG_LOCAL == 256, "one local entry per thread");
+            const int n = __syncthreads_count(s_b[threadIdx.x] != INT64_MAX);  // loaded entries are a prefix
+            if (threadIdx.x == 0) {
+                // a full window ends at the last loaded marked h-edge's end
+                s_w1 = (n == MG_LOCAL) ? min(c1, s_e[n - 1]) : c1;
+                s_k0 = k0 + n;
+            }
+            __syncthreads();
+            const int64_t w1 = s_w1, base = s_base;
+            // 16 consecutive slots per thread and pass (four 16-byte loads in
+            // flight before the gathers); the local entry is found once per
+            // group and advanced within it
+            constexpr int G = 16;
+            for (int64_t g0 = (w0 & ~(int64_t)3) + G * (int64_t)threadIdx.x; g0 < w1; g0 += G * (int64_t)blockDim.x) {
+                int32_t x[G];
+#pragma unroll
+                for (int q = 0; q < G / 4; q++) {
+                    const int64_t i0 = g0 + 4 * q;
+                    if (i0 >= w0 && i0 + 4 <= w1) {
+                        const int4 v = *(const int4 *)(f.dat + i0);
+                        x[4 * q] = v.x; x[4 * q + 1] = v.y; x[4 * q + 2] = v.z; x[4 * q + 3] = v.w;
+                    } else {
+#pragma unroll
+                        for (int u = 0; u < 4; u++) x[4 * q + u] = (i0 + u >= w0 && i0 + u < w1) ? f.dat[i0 + u] : 0;
+                    }
+                }
+                int lo = 0, hi = n;  // last local marked h-edge starting at or before g0
+                while (lo < hi) {
+                    const int m = (lo + hi) >> 1;
+                    if (s_b[m] <= g0) lo = m + 1; else hi = m;
+                }
+                int jr = lo - 1;
+                int32_t y[G];
+#pragma unroll
+                for (int u = 0; u < G; u++) {
+                    const int64_t i = g0 + u;
+                    y[u] = (i >= w0 && i < w1) ? gamma[x[u]] : 0;
+                }
+#pragma unroll
+                for (int u = 0; u < G; u++) {
+                    const int64_t i = g0 + u;
+                    if (i < w0 || i >= w1) continue;
+                    while (jr + 1 < n && s_b[jr + 1] <= i) jr++;
+                    if (jr >= 0 && i < s_e[jr]) continue;  // a marked list's slot
+                    f.out[i - (jr >= 0 ? s_sh[jr] : base)] = y[u];
+                }
+            }
+            __syncthreads();
+            w0 = w1;
+        }
+        __syncthreads();
     }
 }
 }  // namespace
@@ -2072,27 +2143,33 @@ void contract_count(Ctx &c, DLevel &fine, const int32_t *match, const uint8_t *i
     // per-h-edge families: sorted unique gamma image (coarsen.py:163-166)
     KScope kcs(c, "cc_edges");
     coarse.maxp = fine.maxp;
+    // lists of <= 128 slots: counts in bulk + a warp per marked h-edge, then
+    // the linear gap map (contract_write); longer lists: segmented sorts
     s.fused = fine.maxp <= 128;
-    // short lists on average (the tail of C3): slots flattened over the warp;
-    // longer ones: a warp per h-edge
-    // (when there are enough h-edges to give every resident warp a batch)
-    const int64_t flat_min = tiers().flat_edges >= 0 ? tiers().flat_edges : 32 * 48 * (int64_t)c.num_sms;
-    s.flat = fine.Ps + fine.Pd + fine.U <= 3 * 12 * (int64_t)E && (int64_t)E >= flat_min;
     if (s.fused) {
         int32_t *cnt = c.alloc<int32_t>(3 * (int64_t)E);
-        s.slow = c.alloc<uint8_t>(3 * (int64_t)E);
         if (E > 0) {
             const EdgeFam f0{fine.src_off, fine.src_dat, cnt}, f1{fine.dst_off, fine.dst_dat, cnt + E},
                 f2{fine.pin_off, fine.pin_dat, cnt + 2 * (int64_t)E};
-            if (s.flat) {
-                static int g = resident_grid(c, k_contract_flat, 256, 0);
-                const unsigned gr = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(E, 256), g));
-                pdl_launch(k_contract_flat, gr, 256, 0, c.stream, E, fine.gamma, f0, f1, f2, false, s.slow, s.emark);
-            } else {
-                static int g = resident_grid(c, k_contract_edges, 256, 0);
-                const unsigned gr = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(E, 8), g));
-                pdl_launch(k_contract_edges, gr, 256, 0, c.stream, E, fine.gamma, f0, f1, f2, false, s.emark);
-            }
+            // unmarked h-edges in bulk (thread per h-edge), the marked ones
+            // (ascending, kept for the write pass) a warp each
+            int32_t *elist_any = c.alloc<int32_t>(E), *ecnt_any = c.alloc<int32_t>(1);
+            c.zero(ecnt_any, 1);
+            pdl_launch(k_edge_count_bulk, (unsigned)cdiv(E, 256), 256, 0, c.stream, E, f0, f1, f2, s.emark,
+                       elist_any, ecnt_any);
+            DHGP_LAUNCHED(c);
+            c.free(elist_any);
+            c.free(ecnt_any);
+            s.epos = c.alloc<int64_t>((int64_t)E + 1);
+            s.elist = c.alloc<int32_t>(E);
+            s.ecount = c.alloc<int32_t>(1);
+            scan_excl<uint8_t>(c, s.emark, s.epos, E);
+            pdl_launch(k_marked_list, (unsigned)cdiv(E, 256), 256, 0, c.stream, E, s.emark, s.epos, s.elist, s.ecount);
+            DHGP_LAUNCHED(c);
+            static int g = resident_grid(c, k_contract_edges, 256, 0);
+            const unsigned gr = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(E, 8), g));
+            pdl_launch(k_contract_edges, gr, 256, 0, c.stream, E, fine.gamma, f0, f1, f2, false, s.emark,
+                       (const int32_t *)s.elist, (const int32_t *)s.ecount);
             DHGP_LAUNCHED(c);
         }
         coarse.src_off = c.alloc<int64_t>((int64_t)E + 1);
@@ -2154,16 +2231,27 @@ void contract_write(Ctx &c, DLevel &fine, DLevel &coarse, ContractScratch &s, co
                 const EdgeFam f0{fine.src_off, fine.src_dat, nullptr, coarse.src_off, coarse.src_dat},
                     f1{fine.dst_off, fine.dst_dat, nullptr, coarse.dst_off, coarse.dst_dat},
                     f2{fine.pin_off, fine.pin_dat, nullptr, coarse.pin_off, coarse.pin_dat};
-                if (s.flat) {
-                    static int g = resident_grid(c, k_contract_flat, 256, 0);
-                    const unsigned gr = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(E, 256), g));
-                    pdl_launch(k_contract_flat, gr, 256, 0, c.stream, E, fine.gamma, f0, f1, f2, true, s.slow, nullptr);
+                static int g = resident_grid(c, k_contract_edges, 256, 0);
+                const unsigned gr = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(E, 8), g));
+                if ((int64_t)E < 32 * 48 * (int64_t)c.num_sms) {
+                    // few h-edges (a few per resident warp): a warp per h-edge, the
+                    // unmarked ones as plain maps
+                    pdl_launch(k_contract_edges, gr, 256, 0, c.stream, E, fine.gamma, f0, f1, f2, true,
+                               (const uint8_t *)s.emark, (const int32_t *)nullptr, (const int32_t *)nullptr);
+                    DHGP_LAUNCHED(c);
                 } else {
-                    static int g = resident_grid(c, k_contract_edges, 256, 0);
-                    const unsigned gr = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(E, 8), g));
-                    pdl_launch(k_contract_edges, gr, 256, 0, c.stream, E, fine.gamma, f0, f1, f2, true, nullptr);
+                    // marked lists: sorted / de-duplicated images, a warp each
+                    pdl_launch(k_contract_edges, gr, 256, 0, c.stream, E, fine.gamma, f0, f1, f2, true,
+                               (const uint8_t *)nullptr, (const int32_t *)s.elist, (const int32_t *)s.ecount);
+                    DHGP_LAUNCHED(c);
+                    // everything else: linear element-wise map at the per-gap shift
+                    const int64_t pmax = std::max(std::max(fine.Ps, fine.Pd), fine.U);
+                    const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(pmax, MG_CHUNK),
+                                                                                        (int64_t)c.num_sms * 8));
+                    pdl_launch(k_map_gaps, dim3(gx, 3), 256, 0, c.stream, E, fine.gamma, f0, f1, f2,
+                               (const int32_t *)s.elist, (const int32_t *)s.ecount);
+                    DHGP_LAUNCHED(c);
                 }
-                DHGP_LAUNCHED(c);
             }
         } else {
             seg_unique_write(c, E, fine.src_off, s.tmp_src, coarse.src_off, coarse.src_dat);
@@ -2264,7 +2352,9 @@ void contract_release(Ctx &c, ContractScratch &s) {
     c.free(s.mlist);
     c.free(s.mcount);
     c.free(s.emark);
-    c.free(s.slow);
+    c.free(s.elist);
+    c.free(s.ecount);
+    c.free(s.epos);
     s = ContractScratch();
 }
 

@@ -74,9 +74,10 @@ struct ContractScratch {
     int64_t *rank = nullptr;
     int32_t *mlist = nullptr, *mcount = nullptr;  // merged coarse nodes (any order) and their count
     uint8_t *emark = nullptr;  // [E] h-edges holding an absorbed (non-minimum) member
-    bool fused = false;  // h-edge lists rebuilt by the flattened warp kernel (no sorted temporaries)
-    uint8_t *slow = nullptr;  // [3E] lists that need the per-list sort (count pass -> write pass)
-    bool flat = false;        // flattened kernel (short lists) vs warp per h-edge
+    bool fused = false;  // h-edge lists of <= 128 slots: warp kernels + the linear gap map (no sorted temporaries)
+    int32_t *elist = nullptr;  // marked h-edges (emark), ascending ...
+    int32_t *ecount = nullptr; // ... and their count
+    int64_t *epos = nullptr;   // [E+1] exclusive scan of emark
 };
 void contract_count(Ctx &c, DLevel &fine, const int32_t *match, const uint8_t *isrep, DLevel &coarse,
                     ContractScratch &s, int64_t *d_status);

@@ -259,7 +259,6 @@ struct Tiers {
     int edge_movers = 32;     // events / sequence gains: movers per h-edge for the thread tier (<= 32)
     int seg_smem = 8192;      // per-segment sorts / wide run updates: longest list kept in shared memory
     int mv_block = 2048;      // events / sequence gains: movers per h-edge for the shared-memory block tier
-    int flat_edges = -1;      // contraction: fewest h-edges for the flattened kernel (-1: 48 warps per SM)
 };
 const Tiers &tiers();
 
