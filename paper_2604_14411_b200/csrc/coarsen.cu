@@ -1881,7 +1881,7 @@ __global__ void k_edge_count_bulk(int32_t E, EdgeFam f0, EdgeFam f1, EdgeFam f2,
         f2.cnt[e] = (int32_t)(f2.off[e + 1] - f2.off[e]);
     }
     const uint32_t bal = __ballot_sync(FULL_MASK, marked);
-    if (!bal) return;
+    if (!bal || !elist) return;
     const int lane = lane_id(), leader = __ffs(bal) - 1;
     int base = 0;
     if (lane == leader) base = atomicAdd(ecount, __popc(bal));
@@ -2153,19 +2153,22 @@ void contract_count(Ctx &c, DLevel &fine, const int32_t *match, const uint8_t *i
                 f2{fine.pin_off, fine.pin_dat, cnt + 2 * (int64_t)E};
             // unmarked h-edges in bulk (thread per h-edge), the marked ones
             // (ascending, kept for the write pass) a warp each
-            int32_t *elist_any = c.alloc<int32_t>(E), *ecnt_any = c.alloc<int32_t>(1);
-            c.zero(ecnt_any, 1);
-            pdl_launch(k_edge_count_bulk, (unsigned)cdiv(E, 256), 256, 0, c.stream, E, f0, f1, f2, s.emark,
-                       elist_any, ecnt_any);
-            DHGP_LAUNCHED(c);
-            c.free(elist_any);
-            c.free(ecnt_any);
-            s.epos = c.alloc<int64_t>((int64_t)E + 1);
+            // (the write pass's gap map needs the list ascending: a scan of the
+            // marks when there are many h-edges; else the bulk kernel's list)
             s.elist = c.alloc<int32_t>(E);
             s.ecount = c.alloc<int32_t>(1);
-            scan_excl<uint8_t>(c, s.emark, s.epos, E);
-            pdl_launch(k_marked_list, (unsigned)cdiv(E, 256), 256, 0, c.stream, E, s.emark, s.epos, s.elist, s.ecount);
+            const bool sorted_list = (int64_t)E >= 32 * 48 * (int64_t)c.num_sms;
+            c.zero(s.ecount, 1);
+            pdl_launch(k_edge_count_bulk, (unsigned)cdiv(E, 256), 256, 0, c.stream, E, f0, f1, f2, s.emark,
+                       sorted_list ? (int32_t *)nullptr : s.elist, s.ecount);
             DHGP_LAUNCHED(c);
+            if (sorted_list) {
+                s.epos = c.alloc<int64_t>((int64_t)E + 1);
+                scan_excl<uint8_t>(c, s.emark, s.epos, E);
+                pdl_launch(k_marked_list, (unsigned)cdiv(E, 256), 256, 0, c.stream, E, s.emark, s.epos, s.elist,
+                           s.ecount);
+                DHGP_LAUNCHED(c);
+            }
             static int g = resident_grid(c, k_contract_edges, 256, 0);
             const unsigned gr = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(E, 8), g));
             pdl_launch(k_contract_edges, gr, 256, 0, c.stream, E, fine.gamma, f0, f1, f2, false, s.emark,
