@@ -259,6 +259,7 @@ struct Tiers {
     int edge_movers = 32;     // events / sequence gains: movers per h-edge for the thread tier (<= 32)
     int seg_smem = 8192;      // per-segment sorts / wide run updates: longest list kept in shared memory
     int mv_block = 2048;      // events / sequence gains: movers per h-edge for the shared-memory block tier
+    int speculate = 1;        // refinement: launch a round's tail before its mover count is on the host
 };
 const Tiers &tiers();
 

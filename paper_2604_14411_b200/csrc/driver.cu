@@ -50,6 +50,7 @@ const Tiers &tiers() {
             x.edge_movers = 2;
             x.seg_smem = 48;
             x.mv_block = 6;
+            x.speculate = 0;
         }
         const char *h = getenv("DHGP_HUB_INC");  // tuning: propose hub-tier threshold
         if (h) x.pr_hub_inc = atoi(h);

@@ -1675,6 +1675,55 @@ __device__ __forceinline__ int warp_collect_movers(const int32_t *dat, int64_t l
     __syncwarp();
     return nm;
 }
+// the terms of one h-edge from its movers, lane a holding the a-th mover in
+// sequence order (i = its move index; nm <= 32 movers)
+__device__ __forceinline__ void edge_seq_terms(int32_t e, int nm, int32_t i, const int64_t *wi, const Runs &r,
+                                               const int32_t *from, const int32_t *to, unsigned long long *gacc) {
+    const int lane = lane_id();
+    const int64_t ro = r.off[e];
+    const int32_t lam = r.len[e];
+    const int32_t ps = lane < nm ? from[i] : -1, pd = lane < nm ? to[i] : -1;
+    int32_t leav_pd = 0, ent_pd = 0, leav_ps = 0, ent_ps = 0;
+    for (int b = 0; b < nm; b++) {
+        const int32_t fb = __shfl_sync(FULL_MASK, ps, b), tb = __shfl_sync(FULL_MASK, pd, b);
+        if (b < lane) {
+            leav_pd += fb == pd;
+            ent_pd += tb == pd;
+            leav_ps += fb == ps;
+            ent_ps += tb == ps;
+        }
+    }
+    if (lane < nm) {
+        int32_t k = run_find(r, ro, lam, ps);
+        const int32_t base_ps = k >= 0 ? r.pc[2 * (ro + k) + 1] : 0;
+        k = run_find(r, ro, lam, pd);
+        const int32_t base_pd = k >= 0 ? r.pc[2 * (ro + k) + 1] : 0;
+        const int64_t net = seq_net(wi[e], base_ps, base_pd, leav_pd, ent_pd, leav_ps, ent_ps);
+        if (net) atomicAdd(&gacc[i], (unsigned long long)net);
+    }
+}
+__device__ __forceinline__ void edge_event_terms(int32_t e, int nm, int32_t i, const Runs &r, const int32_t *from,
+                                                 const int32_t *to, EvArgs ev) {
+    const int lane = lane_id();
+    const int64_t ro = r.off[e];
+    const int32_t lam = r.len[e];
+    const int32_t pf = lane < nm ? from[i] : -1, pt = lane < nm ? to[i] : -1;
+    int32_t df = 0, dt = 0;  // net arrivals minus departures of pf / pt before mover a
+    for (int b = 0; b < nm; b++) {
+        const int32_t fb = __shfl_sync(FULL_MASK, pf, b), tb = __shfl_sync(FULL_MASK, pt, b);
+        if (b < lane) {
+            df += (tb == pf) - (fb == pf);
+            dt += (tb == pt) - (fb == pt);
+        }
+    }
+    if (lane < nm) {
+        int32_t k = run_find(r, ro, lam, pf);
+        if ((k >= 0 ? r.cin[ro + k] : 0) + df - 1 == 0) inbound_leave(ev, i);
+        k = run_find(r, ro, lam, pt);
+        if ((k >= 0 ? r.cin[ro + k] : 0) + dt == 0) inbound_enter(ev, i);
+    }
+}
+
 __global__ void __launch_bounds__(256) k_round_edges(int32_t E, const int32_t *elist, const int32_t *ecount,
                                                      const int64_t *pin_off, const int32_t *pin_dat,
                                                      const int64_t *dst_off, const int32_t *dst_dat,
@@ -1692,8 +1741,6 @@ __global__ void __launch_bounds__(256) k_round_edges(int32_t E, const int32_t *e
     const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
     for (int64_t idx = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id(); idx < ne; idx += nw) {
         const int32_t e = elist ? elist[idx] : (int32_t)idx;
-        const int64_t ro = r.off[e];
-        const int32_t lam = r.len[e];
         // ---- sequence gains over all pins --------------------------------
         int nm = warp_collect_movers(pin_dat, pin_off[e], pin_off[e + 1], pos, smv);
         if (nm > cap) {
@@ -1701,26 +1748,7 @@ __global__ void __launch_bounds__(256) k_round_edges(int32_t E, const int32_t *e
         } else if (nm > 0) {
             uint32_t v[1] = {lane < nm ? (uint32_t)smv[lane] : 0xffffffffu};
             warp_bitonic_sort<1>(v);
-            const int32_t i = (int32_t)v[0];
-            const int32_t ps = lane < nm ? from[i] : -1, pd = lane < nm ? to[i] : -1;
-            int32_t leav_pd = 0, ent_pd = 0, leav_ps = 0, ent_ps = 0;
-            for (int b = 0; b < nm; b++) {
-                const int32_t fb = __shfl_sync(FULL_MASK, ps, b), tb = __shfl_sync(FULL_MASK, pd, b);
-                if (b < lane) {
-                    leav_pd += fb == pd;
-                    ent_pd += tb == pd;
-                    leav_ps += fb == ps;
-                    ent_ps += tb == ps;
-                }
-            }
-            if (lane < nm) {
-                int32_t k = run_find(r, ro, lam, ps);
-                const int32_t base_ps = k >= 0 ? r.pc[2 * (ro + k) + 1] : 0;
-                k = run_find(r, ro, lam, pd);
-                const int32_t base_pd = k >= 0 ? r.pc[2 * (ro + k) + 1] : 0;
-                const int64_t net = seq_net(wi[e], base_ps, base_pd, leav_pd, ent_pd, leav_ps, ent_ps);
-                if (net) atomicAdd(&gacc[i], (unsigned long long)net);
-            }
+            edge_seq_terms(e, nm, (int32_t)v[0], wi, r, from, to, gacc);
         }
         __syncwarp();
         // ---- inbound-track crossings over the destination pins -----------
@@ -1730,22 +1758,7 @@ __global__ void __launch_bounds__(256) k_round_edges(int32_t E, const int32_t *e
         } else if (nm > 0) {
             uint32_t v[1] = {lane < nm ? (uint32_t)smv[lane] : 0xffffffffu};
             warp_bitonic_sort<1>(v);
-            const int32_t i = (int32_t)v[0];
-            const int32_t pf = lane < nm ? from[i] : -1, pt = lane < nm ? to[i] : -1;
-            int32_t df = 0, dt = 0;  // net arrivals minus departures of pf / pt before mover a
-            for (int b = 0; b < nm; b++) {
-                const int32_t fb = __shfl_sync(FULL_MASK, pf, b), tb = __shfl_sync(FULL_MASK, pt, b);
-                if (b < lane) {
-                    df += (tb == pf) - (fb == pf);
-                    dt += (tb == pt) - (fb == pt);
-                }
-            }
-            if (lane < nm) {
-                int32_t k = run_find(r, ro, lam, pf);
-                if ((k >= 0 ? r.cin[ro + k] : 0) + df - 1 == 0) inbound_leave(ev, i);
-                k = run_find(r, ro, lam, pt);
-                if ((k >= 0 ? r.cin[ro + k] : 0) + dt == 0) inbound_enter(ev, i);
-            }
+            edge_event_terms(e, nm, (int32_t)v[0], r, from, to, ev);
         }
         __syncwarp();
     }
@@ -2592,7 +2605,7 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
         // host then relaunches it for the real M).  One host sync per round
         // reads M, the connectivity and the selection together.  Unpacked
         // sequence keys need the ordered scan, hence M first.
-        const bool spec = packed;
+        const bool spec = packed && tiers().speculate;
         int64_t M = 0;
         unsigned long long conn_h = 0;
         if (!spec) {
