@@ -512,3 +512,22 @@ def test_hedge_beyond_shared_memory_golden():
     ref = json.loads(bytes(z["stats"]).decode())
     assert np.array_equal(part.assign, z["assign"]) and part.num_parts == int(z["num_parts"])
     assert st.levels == ref["levels"] and st.connectivity_trace == ref["trace"]
+
+
+def test_c2_whole_run_matches_reference():
+    """C2 (100k-node layered SNN, the reference's 9,755 s single-core run,
+    tests/golden/make_c2_golden.py): the GPU partition's assignment, part
+    count, every level's sizes and the whole connectivity trace equal the
+    reference's (driver.py:76-163 end to end)."""
+    from paper_2604_14411_b200 import workloads as W
+
+    z = load_npz("c2.npz")
+    meta = json.loads(bytes(z["meta"]).decode())
+    arrs, omega, delta, _ = W.make_config("C2")
+    g = graph(arrs)
+    part, st, _ = run_gpu(g, omega, delta, max_levels=1 << 20)
+    ref = json.loads(bytes(z["stats"]).decode())
+    assert (omega, delta) == (meta["omega"], meta["delta"])
+    assert np.array_equal(part.assign, z["assign"]) and part.num_parts == int(z["num_parts"])
+    assert st.levels == ref["levels"]
+    assert st.connectivity_trace == ref["trace"]
