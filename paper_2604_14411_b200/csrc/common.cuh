@@ -104,8 +104,22 @@ struct Ctx {
     cudaStream_t stream = nullptr;
     int64_t launches = 0;
     int num_sms = 148;
-    // optional per-kernel event timing (bench/profiling only)
+    // optional per-kernel event timing (bench/profiling only); only the
+    // outermost scope of a nest is recorded, so the classes are disjoint
     bool profiling = false;
+    int prof_depth = 0;
+    // device counters of algorithmic bytes for data-dependent classes
+    // (profiling only; slots below), added to their class at flush_profile
+    unsigned long long *prof_work = nullptr;
+    enum { PW_SEQ_GAINS = 0, PW_RUNS_UPDATE = 1, PW_SELECT = 2, PW_SLOTS = 4 };
+    unsigned long long *work_slot(int k) {
+        if (!profiling) return nullptr;
+        if (!prof_work) {
+            prof_work = alloc<unsigned long long>(PW_SLOTS);
+            DHGP_CUDA(cudaMemsetAsync(prof_work, 0, PW_SLOTS * sizeof(unsigned long long), stream));
+        }
+        return prof_work + k;
+    }
     std::vector<KernelStat> kstats;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending_ev;
     std::vector<int> pending_idx;
@@ -201,8 +215,13 @@ struct KScope {
     const char *name;
     long long tag;
     cudaEvent_t t0 = nullptr, t1 = nullptr;
+    bool nested = false;  // counted in the profiling depth
     KScope(Ctx &ctx, const char *nm, double b = 0, long long tg = -1) : c(ctx), idx(-1), bytes(b), name(nm), tag(tg) {
-        if (c.profiling) idx = c.kbegin(name);
+        if (c.profiling) {
+            if (c.prof_depth == 0) idx = c.kbegin(name);
+            c.prof_depth++;
+            nested = true;
+        }
         if (trace_enabled()) {
             cudaEventCreate(&t0);
             cudaEventCreate(&t1);
@@ -228,6 +247,10 @@ struct KScope {
     void close() {
         if (idx >= 0) c.kend(idx, bytes);
         idx = -1;
+        if (nested) {
+            c.prof_depth--;
+            nested = false;
+        }
         if (t0) {
             cudaEventRecord(t1, c.stream);
             cudaEventSynchronize(t1);

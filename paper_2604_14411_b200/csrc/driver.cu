@@ -85,6 +85,21 @@ void Ctx::kend(int p, double bytes) {
     pending_bytes[p] = bytes;
 }
 void Ctx::flush_profile() {
+    if (prof_work) {  // device-counted bytes of the data-dependent classes
+        unsigned long long h[PW_SLOTS];
+        DHGP_CUDA(cudaMemcpyAsync(h, prof_work, sizeof h, cudaMemcpyDeviceToHost, stream));
+        DHGP_CUDA(cudaStreamSynchronize(stream));
+        const char *names[PW_SLOTS] = {"seq_gains", "runs_update", "select", nullptr};
+        for (int k = 0; k < PW_SLOTS; k++)
+            if (names[k] && h[k])
+                for (size_t i = 0; i < pending_idx.size(); i++)
+                    if (kstats[pending_idx[i]].name == std::string(names[k])) {
+                        pending_bytes[i] += (double)h[k];  // the class total, carried by its first launch
+                        break;
+                    }
+        free(prof_work);
+        prof_work = nullptr;
+    }
     if (pending_ev.empty()) return;
     DHGP_CUDA(cudaStreamSynchronize(stream));
     for (size_t i = 0; i < pending_ev.size(); i++) {

@@ -198,7 +198,10 @@ void build_level0(Ctx &c, const DInput &in, DLevel &L) {
 }
 
 void derive_incidence(Ctx &c, DLevel &L) {
-    KScope ks(c, "incidence");
+    // algorithmic bytes: the sides read twice (combine, transpose: 8 B per
+    // pin slot each), the pin lists written and read back (8 B per pin), the
+    // two transposes' outputs (4 B per entry) and the offsets
+    KScope ks(c, "incidence", (double)(16.0 * (L.Ps + L.Pd) + 12.0 * L.U + 4.0 * L.Pd + 32.0 * L.E + 16.0 * L.N));
     const int64_t E = L.E;
     // edge_pins = sorted unique (src ∪ dst) per h-edge  (hgraph.py:219-221)
     const int64_t cap = L.Ps + L.Pd;

@@ -491,7 +491,8 @@ void small_sort_packed(Ctx &c, uint64_t *keys, uint32_t *vals, int64_t n, const 
 void radix_sort_pairs(Ctx &c, uint64_t *keys, uint32_t *vals, uint64_t *ktmp, uint32_t *vtmp, int64_t n_cap,
                       const int64_t *d_n, int bits) {
     if (n_cap <= 1 || bits <= 0) return;
-    KScope ks(c, "radix_sort");
+    // algorithmic bytes: every pass reads and writes the (key, value) pairs
+    KScope ks(c, "radix_sort", 24.0 * (double)n_cap * (double)((bits + 7) / 8));
     const int64_t ntiles = cdiv(n_cap, RS_TILE);
     int64_t *counts = c.alloc<int64_t>(256 * ntiles);
     int64_t *offs = c.alloc<int64_t>(256 * ntiles + 1);
@@ -646,7 +647,7 @@ __global__ void k_seg_sort_block(const int64_t *off, const int32_t *dat, const i
 
 void seg_sort(Ctx &c, int64_t nseg, const int64_t *off, const int32_t *dat, const int32_t *map, int32_t *tmp) {
     if (nseg <= 0) return;
-    KScope ks(c, "seg_sort");
+    KScope ks(c, "seg_sort");  // (bytes: only as part of an enclosing class)
     int32_t *wl = c.alloc<int32_t>(nseg);
     int32_t *bl = c.alloc<int32_t>(nseg);
     int32_t *cnt = c.alloc<int32_t>(3);

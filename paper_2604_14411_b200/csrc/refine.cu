@@ -1317,7 +1317,7 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select_small(const unsigned lon
                                                               const int64_t *gseq, const int64_t *psizes,
                                                               const int64_t *pinbound, int64_t omega, int64_t delta,
                                                               int ibits, int pbits, int64_t *act_ex_out,
-                                                              long long *res, bool packed) {
+                                                              long long *res, bool packed, unsigned long long *work) {
     pdl_entry();
     extern __shared__ unsigned long long smem_u64[];
     __shared__ int64_t sh[33];
@@ -1325,6 +1325,8 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select_small(const unsigned lon
     const int64_t T = (int64_t)*ecount;
     const int64_t M = *dM;
     if (M == 0) return;  // a speculative launch for a round without movers (the host stops there)
+    // algorithmic bytes (profiling): events (12 B), gains in and prefix flags out (16 B per move)
+    if (work && threadIdx.x == 0 && T <= SEL_T && M <= SEL_M - 2) atomicAdd(work, 12ull * T + 16ull * M);
     if (T > SEL_T || M > SEL_M - 2) {
         if (threadIdx.x == 0) res[2] = 1;
         return;
@@ -1731,7 +1733,7 @@ __global__ void __launch_bounds__(256) k_round_edges(int32_t E, const int32_t *e
                                                      const int32_t *from, const int32_t *to,
                                                      unsigned long long *gacc, EvArgs ev, int32_t *sg_big,
                                                      int32_t *sg_count, int32_t *ev_big, int32_t *ev_count,
-                                                     int cap, const int64_t *spec_m) {
+                                                     int cap, const int64_t *spec_m, unsigned long long *work) {
     pdl_entry();
     if (spec_m && *spec_m > kSpecCap) return;  // speculative launch, M too large
     __shared__ int32_t s_mv[8][32];
@@ -1741,6 +1743,10 @@ __global__ void __launch_bounds__(256) k_round_edges(int32_t E, const int32_t *e
     const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
     for (int64_t idx = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id(); idx < ne; idx += nw) {
         const int32_t e = elist ? elist[idx] : (int32_t)idx;
+        // algorithmic bytes (profiling): pins and destination pins with their
+        // positions (8 B each), offsets / runs / weight (48 B)
+        if (work && lane == 0)
+            atomicAdd(work, 8ull * (uint64_t)(pin_off[e + 1] - pin_off[e] + dst_off[e + 1] - dst_off[e]) + 48ull);
         // ---- sequence gains over all pins --------------------------------
         int nm = warp_collect_movers(pin_dat, pin_off[e], pin_off[e + 1], pos, smv);
         if (nm > cap) {
@@ -1848,7 +1854,7 @@ __global__ void k_runs_update(const int32_t *elist, const int32_t *ecount, int32
                               const int32_t *pin_dat, const int64_t *dst_off, const int32_t *dst_dat,
                               const int32_t *assign, const int64_t *wi, Runs r, unsigned long long *conn,
                               int64_t *pinbound, int32_t K, int32_t *ndirty, int32_t *nlist, int32_t *ncount,
-                              int32_t *wide, int32_t *wide_count) {
+                              int32_t *wide, int32_t *wide_count, unsigned long long *work) {
     pdl_entry();
     __shared__ int32_t sdelta[RU_SMEM_K];
     __shared__ int32_t s_oldp[8][128], s_oldc[8][128];
@@ -1871,6 +1877,9 @@ __global__ void k_runs_update(const int32_t *elist, const int32_t *ecount, int32
             continue;
         }
         const int32_t old = r.len[e];
+        // algorithmic bytes (profiling): the pin list and its parts (8 B per
+        // pin), old and new runs (12 B each), offsets / flags / weight (32 B)
+        if (work && lane == 0) atomicAdd(work, 8ull * len + 24ull * old + 32ull);
         int32_t *op = s_oldp[warp_id()], *oc = s_oldc[warp_id()];
         if (moved)
             for (int32_t j = lane; j < old; j += 32) {
@@ -2414,7 +2423,8 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
     auto runs_update = [&](bool reset) {
         pdl_launch(k_runs_update, g_ru, 256, 0, c.stream, st.elist, st.ctr + CT_ELIST, st.edirty, L.pin_off, L.pin_dat,
                                                  L.dst_off, L.dst_dat, assign, W.wi, r, conn_d, pinbound, K, st.ndirty,
-                                                 st.nlist, st.ctr + CT_NLIST, st.wide, st.ctr + CT_WIDE);
+                                                 st.nlist, st.ctr + CT_NLIST, st.wide, st.ctr + CT_WIDE,
+                                                 c.work_slot(Ctx::PW_RUNS_UPDATE));
         DHGP_LAUNCHED(c);
         if (wide_edges) {
             static bool wattr = false;
@@ -2669,7 +2679,7 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
                     pdl_launch(k_round_edges, gre, 256, 0, c.stream, L.E, elist, elist_n, L.pin_off, L.pin_dat, L.dst_off,
                                                              L.dst_dat, W.wi, r, pos, from, to, gacc, ev, sg_big,
                                                              sg_ctr, big, ctr, tiers().edge_movers,
-                                                             sp ? dM : nullptr);
+                                                             sp ? dM : nullptr, c.work_slot(Ctx::PW_SEQ_GAINS));
                     DHGP_LAUNCHED(c);
                     pdl_launch(k_seq_gains_edge_block, c.num_sms, 256, 0, c.stream, L.pin_off, L.pin_dat, W.wi, r, pos, from,
                                                                              to, gacc, sg_big, sg_ctr, hv_sg, sg_ctr + 2,
@@ -2699,7 +2709,7 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
             const bool packed_ev = 1 + ibits + pbits <= 32;
             pdl_launch(k_select_small, 1, SEL_THREADS, sel_smem(), c.stream, ecount, dM, ek, evv, gseq, psizes, pinbound,
                                                                     omega, delta, ibits, pbits, act_ex, sres,
-                                                                    packed_ev);
+                                                                    packed_ev, c.work_slot(Ctx::PW_SELECT));
             DHGP_LAUNCHED(c);
         };
         auto free_tail = [&]() {
