@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(SS_WARPS * 32, 3) k_score_warp(ScoreArgs a) {
     Acc *svals = (Acc *)smem_u64;
     int32_t *skeys = (int32_t *)(svals + SS_WARPS * SS_CAP);
     __shared__ int32_t snk[SS_WARPS];
-    __shared__ volatile int32_t sover[SS_WARPS];
+    __shared__ int32_t sover[SS_WARPS];
     const int w = warp_id(), lane = lane_id();
     int32_t *keys = skeys + w * SS_CAP;
     Acc *vals = svals + w * SS_CAP;
@@ -279,7 +279,7 @@ __global__ void __launch_bounds__(SS_WARPS * 32, 3) k_score_warp(ScoreArgs a) {
         }
         __syncwarp();
         warp_for_pins(a.inc_dat, ilo, ihi, 0, 32, a.pin_off, a.pin_dat, [&](int32_t e, int32_t m) {
-            if (m == node || sover[w]) return;
+            if (m == node || flag_get(&sover[w])) return;
             const Acc we = (Acc)a.wi[e];
             uint32_t h = hslot(m);
             for (int probe = 0; probe < SS_CAP; probe++) {
@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(SS_WARPS * 32, 3) k_score_warp(ScoreArgs a) {
                 if (k == -1) {
                     int prev = atomicCAS(&keys[slot], -1, m);
                     if (prev == -1) {
-                        if (atomicAdd(&snk[w], 1) >= a.t.ss_limit) sover[w] = 1;
+                        if (atomicAdd(&snk[w], 1) >= a.t.ss_limit) flag_set(&sover[w]);
                         k = m;
                     } else {
                         k = prev;
@@ -299,7 +299,7 @@ __global__ void __launch_bounds__(SS_WARPS * 32, 3) k_score_warp(ScoreArgs a) {
                     return;
                 }
             }
-            sover[w] = 1;
+            flag_set(&sover[w]);
         }, a.work);
         __syncwarp();
         if (sover[w]) {
@@ -379,7 +379,7 @@ __global__ void __launch_bounds__(SM_THREADS) k_score_mid(ScoreArgs a) {
     Acc *vals = (Acc *)smem_u64;
     int32_t *keys = (int32_t *)(vals + SM_CAP);
     __shared__ int32_t snk, s_next;
-    __shared__ volatile int32_t sover;
+    __shared__ int32_t sover;
     __shared__ long long r_v[SM_THREADS / 32], r_c[SM_THREADS / 32];
     __shared__ int32_t r_k[SM_THREADS / 32], r_s[SM_THREADS / 32];
     constexpr int NW = SM_THREADS / 32;
@@ -410,7 +410,7 @@ __global__ void __launch_bounds__(SM_THREADS) k_score_mid(ScoreArgs a) {
         const int bsz = (int)max((int64_t)1, min((int64_t)32, (ihi - ilo + NW - 1) / NW));
         warp_for_pins<4>(a.inc_dat, ilo, ihi, (int64_t)w * bsz, (int64_t)NW * bsz, a.pin_off, a.pin_dat,
                          [&](int32_t e, int32_t m) {
-                             if (m == node || sover) return;
+                             if (m == node || flag_get(&sover)) return;
                              const Acc we = (Acc)a.wi[e];
                              uint32_t h = ((uint32_t)m * 2654435761u) >> (32 - 12);
                              for (int probe = 0; probe < SM_CAP; probe++) {
@@ -419,7 +419,7 @@ __global__ void __launch_bounds__(SM_THREADS) k_score_mid(ScoreArgs a) {
                                  if (k == -1) {
                                      const int prev = atomicCAS(&keys[slot], -1, m);
                                      if (prev == -1) {
-                                         if (atomicAdd(&snk, 1) + 1 > a.t.sm_limit) sover = 1;
+                                         if (atomicAdd(&snk, 1) + 1 > a.t.sm_limit) flag_set(&sover);
                                          k = m;
                                      } else {
                                          k = prev;
@@ -430,7 +430,7 @@ __global__ void __launch_bounds__(SM_THREADS) k_score_mid(ScoreArgs a) {
                                      return;
                                  }
                              }
-                             sover = 1;
+                             flag_set(&sover);
                          },
                          a.work, bsz);
         __syncthreads();
@@ -541,7 +541,7 @@ __global__ void __launch_bounds__(SH_THREADS) k_score_heavy(ScoreArgs a, int pai
     Acc *vals = (Acc *)smem_u64;
     int32_t *keys = (int32_t *)(vals + SH_CAP);
     __shared__ int32_t snk;
-    __shared__ volatile int32_t sover;
+    __shared__ int32_t sover;
     __shared__ long long r_v[SH_THREADS / 32];
     __shared__ int32_t r_k[SH_THREADS / 32], r_s[SH_THREADS / 32];
     __shared__ long long r_c[SH_THREADS / 32];
@@ -571,7 +571,7 @@ __global__ void __launch_bounds__(SH_THREADS) k_score_heavy(ScoreArgs a, int pai
         warp_for_pins<4>(a.inc_dat, ilo, ihi, (int64_t)(rank * nw + w) * bsz, (int64_t)CL * nw * bsz, a.pin_off,
                          a.pin_dat,
                       [&](int32_t e, int32_t m) {
-                          if (m == node || sover) return;
+                          if (m == node || flag_get(&sover)) return;
                           const Acc we = (Acc)a.wi[e];
                           uint32_t h = ((uint32_t)m * 2654435761u) >> (32 - 14);
                           for (int probe = 0; probe < SH_CAP; probe++) {
@@ -585,7 +585,7 @@ __global__ void __launch_bounds__(SH_THREADS) k_score_heavy(ScoreArgs a, int pai
                                       // the tier, never the result)
                                       if (++pend == 2) {
                                           pend = 0;
-                                          if (atomicAdd(&snk, 2) + 2 > a.t.sh_limit) sover = 1;
+                                          if (atomicAdd(&snk, 2) + 2 > a.t.sh_limit) flag_set(&sover);
                                       }
                                       k = m;
                                   } else {
@@ -597,7 +597,7 @@ __global__ void __launch_bounds__(SH_THREADS) k_score_heavy(ScoreArgs a, int pai
                                   return;
                               }
                           }
-                          sover = 1;
+                          flag_set(&sover);
                       },
                       a.work, bsz);
         __syncthreads();
@@ -608,13 +608,13 @@ __global__ void __launch_bounds__(SH_THREADS) k_score_heavy(ScoreArgs a, int pai
                 int32_t *keys0 = cl.map_shared_rank(keys, 0);
                 Acc *vals0 = cl.map_shared_rank(vals, 0);
                 int32_t *snk0 = cl.map_shared_rank(&snk, 0);
-                volatile int32_t *sover0 = cl.map_shared_rank(const_cast<int32_t *>(&sover), 0);
+                int32_t *sover0 = cl.map_shared_rank(&sover, 0);
                 if (sover) {
-                    if (threadIdx.x == 0) *sover0 = 1;
+                    if (threadIdx.x == 0) atomicExch(sover0, 1);
                 } else {
                     for (int s = threadIdx.x; s < SH_CAP; s += SH_THREADS) {
                         const int32_t m = keys[s];
-                        if (m < 0 || *sover0) continue;
+                        if (m < 0 || atomicAdd(sover0, 0)) continue;
                         const Acc v = vals[s];
                         const uint32_t h = ((uint32_t)m * 2654435761u) >> (32 - 14);
                         bool done = false;
@@ -624,7 +624,7 @@ __global__ void __launch_bounds__(SH_THREADS) k_score_heavy(ScoreArgs a, int pai
                             if (k == -1) {
                                 const int prev = atomicCAS(&keys0[slot], -1, m);
                                 if (prev == -1) {
-                                    if (atomicAdd(snk0, 1) + 1 > a.t.sh_limit) *sover0 = 1;
+                                    if (atomicAdd(snk0, 1) + 1 > a.t.sh_limit) atomicExch(sover0, 1);
                                     k = m;
                                 } else {
                                     k = prev;
@@ -635,7 +635,7 @@ __global__ void __launch_bounds__(SH_THREADS) k_score_heavy(ScoreArgs a, int pai
                                 done = true;
                             }
                         }
-                        if (!done) *sover0 = 1;
+                        if (!done) atomicExch(sover0, 1);
                     }
                 }
             }
@@ -879,6 +879,7 @@ __global__ void k_inc_base(int32_t N, const int32_t *ma, const int32_t *mb, cons
     if (mb[c] >= 0) {
         kind[c] = 0;
         thr_p[c] = -1;
+        thr_s[c] = 0;  // (gathered alongside thr_p by filter_emit, never used when thr_p < 0)
         list[atomicAdd(list_count, 1)] = (int32_t)c;
         return;
     }
@@ -886,6 +887,7 @@ __global__ void k_inc_base(int32_t N, const int32_t *ma, const int32_t *mb, cons
     if (p < 0) {
         kind[c] = 2;
         thr_p[c] = -1;
+        thr_s[c] = 0;
         return;
     }
     thr_s[c] = (int64_t)prev_score[f];

@@ -429,7 +429,7 @@ __global__ void __launch_bounds__(PR_WARPS * 32, 4) k_propose_warp(ProposeArgs a
     Acc *svals = (Acc *)smem_u64;
     int32_t *skeys = (int32_t *)(svals + PR_WARPS * PR_CAP);
     __shared__ int32_t snk[PR_WARPS];
-    __shared__ volatile int32_t sover[PR_WARPS];
+    __shared__ int32_t sover[PR_WARPS];
     __shared__ int s_nf[PR_WARPS];
     __shared__ int32_t s_f[PR_WARPS][2];
     const int w = warp_id(), lane = lane_id();
@@ -475,7 +475,7 @@ __global__ void __launch_bounds__(PR_WARPS * 32, 4) k_propose_warp(ProposeArgs a
         int64_t total = 0, saving = 0;
         total = warp_for_runs(a.inc_dat, ilo, ihi, 0, 32, 32, a.r.off, a.r.len, a.wi, a.work, a.r.pc, [&](int32_t, int64_t we, int32_t p, int32_t pc) {
             if (p == ps && pc == 1) saving += we;
-            if (sover[w]) return;
+            if (flag_get(&sover[w])) return;
             const uint32_t h = pslot(p);
             for (int probe = 0; probe < PR_CAP; probe++) {
                 const int slot = (h + probe) & (PR_CAP - 1);
@@ -483,7 +483,7 @@ __global__ void __launch_bounds__(PR_WARPS * 32, 4) k_propose_warp(ProposeArgs a
                 if (kk == -1) {
                     const int prev = atomicCAS(&keys[slot], -1, p);
                     if (prev == -1) {
-                        if (atomicAdd(&snk[w], 1) >= a.t.pr_limit) sover[w] = 1;
+                        if (atomicAdd(&snk[w], 1) >= a.t.pr_limit) flag_set(&sover[w]);
                         kk = p;
                     } else {
                         kk = prev;
@@ -494,7 +494,7 @@ __global__ void __launch_bounds__(PR_WARPS * 32, 4) k_propose_warp(ProposeArgs a
                     return;
                 }
             }
-            sover[w] = 1;
+            flag_set(&sover[w]);
         });
         total = warp_sum(total);
         saving = warp_sum(saving);
@@ -577,7 +577,7 @@ __global__ void __launch_bounds__(PM_THREADS, 4) k_propose_mid(ProposeArgs a) {
     Acc *vals = (Acc *)smem_u64;
     int32_t *keys = (int32_t *)(vals + PM_CAP);
     __shared__ int32_t snk;
-    __shared__ volatile int32_t sover;
+    __shared__ int32_t sover;
     __shared__ long long r_a[PM_THREADS / 32], r_b[PM_THREADS / 32];
     __shared__ int32_t r_p[PM_THREADS / 32];
     __shared__ int s_nf;
@@ -627,7 +627,7 @@ __global__ void __launch_bounds__(PM_THREADS, 4) k_propose_mid(ProposeArgs a) {
                               a.r.pc,
                               [&](int32_t, int64_t we, int32_t p, int32_t pc) {
                                   if (p == ps && pc == 1) saving += we;
-                                  if (sover) return;
+                                  if (flag_get(&sover)) return;
                                   const uint32_t h = ((uint32_t)p * 2654435761u) >> (32 - lg);
                                   for (int probe = 0; probe < cap; probe++) {
                                       const int slot = (h + probe) & (cap - 1);
@@ -635,7 +635,7 @@ __global__ void __launch_bounds__(PM_THREADS, 4) k_propose_mid(ProposeArgs a) {
                                       if (kk == -1) {
                                           const int prev = atomicCAS(&keys[slot], -1, p);
                                           if (prev == -1) {
-                                              if (atomicAdd(&snk, 1) >= limit) sover = 1;
+                                              if (atomicAdd(&snk, 1) >= limit) flag_set(&sover);
                                               kk = p;
                                           } else {
                                               kk = prev;
@@ -646,7 +646,7 @@ __global__ void __launch_bounds__(PM_THREADS, 4) k_propose_mid(ProposeArgs a) {
                                           return;
                                       }
                                   }
-                                  sover = 1;
+                                  flag_set(&sover);
                               });
         total = warp_sum(total);
         saving = warp_sum(saving);
