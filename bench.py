@@ -270,8 +270,19 @@ def run_ours(args, ws, rank, local):
     dom = max(with_bytes, key=lambda k: k["ms"]) if with_bytes else None
     traffic = None
     tp = ROOT / "profiles" / "ncu_traffic.json"
-    if dom and tp.exists():
-        traffic = json.loads(tp.read_text()).get(dom["name"])
+    ncu_tr = json.loads(tp.read_text()) if tp.exists() else {}
+    if dom:
+        traffic = ncu_tr.get(dom["name"])
+    # every class: algorithmic GB/s and its fraction of the measured peak; the
+    # ncu DRAM bytes per launch (profiles/ncu_traffic.json, a launch window of
+    # this workload) and the DRAM rate they imply at this run's class time
+    for k in kstats:
+        sec = k["ms"] / 1e3
+        k["achieved_gbs"] = round(k["bytes"] / sec / 1e9, 1) if sec > 0 and k["bytes"] > 0 else None
+        k["frac"] = round(k["achieved_gbs"] / peak, 4) if k["achieved_gbs"] else None
+        tr = ncu_tr.get(k["name"])
+        k["ncu_dram_bytes_per_launch"] = tr
+        k["ncu_dram_gbs"] = round(tr * k["launches"] / sec / 1e9, 1) if tr and sec > 0 else None
     roofline = None
     if dom:
         ach = dom["bytes"] / (dom["ms"] / 1e3) / 1e9
