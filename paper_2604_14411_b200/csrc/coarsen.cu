@@ -83,7 +83,7 @@ __device__ __forceinline__ void warp_for_pins(const int32_t *inc_dat, int64_t il
 
 struct ScoreArgs {
     int32_t N;
-    const int64_t *inc_off;
+    const int64_t *inc_off;  // per-node list begin ...
     const int32_t *inc_dat;
     const int64_t *pin_off;
     const int32_t *pin_dat;
@@ -91,6 +91,8 @@ struct ScoreArgs {
     const int32_t *size;
     const int64_t *in_off;
     const int32_t *in_dat;
+    const int64_t *inc_end = nullptr;  // ... and end (DLevel::inc_e / in_e)
+    const int64_t *in_end = nullptr;
     int64_t omega, delta;
     int32_t *pair;
     double *score;
@@ -224,8 +226,8 @@ __device__ __forceinline__ uint32_t hslot(int32_t m) { return ((uint32_t)m * 265
 
 // |in(n) ∪ in(m)| <= delta, warp-cooperative (_kernels.pyx:94-98)
 __device__ __forceinline__ bool warp_union_ok(const ScoreArgs &a, int32_t n, int32_t m) {
-    const int64_t nlo = a.in_off[n], nn = a.in_off[n + 1] - nlo;
-    const int64_t mlo = a.in_off[m], nm = a.in_off[m + 1] - mlo;
+    const int64_t nlo = a.in_off[n], nn = a.in_end[n] - nlo;
+    const int64_t mlo = a.in_off[m], nm = a.in_end[m] - mlo;
     if (nn + nm <= a.delta) return true;
     const bool ns = nn <= nm;
     const int32_t *sp = a.in_dat + (ns ? nlo : mlo);
@@ -255,7 +257,7 @@ __global__ void __launch_bounds__(SS_WARPS * 32, 3) k_score_warp(ScoreArgs a) {
         const int32_t node = score_node(a, idx);
         if (node == -1) break;
         if (node < 0) continue;
-        const int64_t ilo = a.inc_off[node], ihi = a.inc_off[node + 1];
+        const int64_t ilo = a.inc_off[node], ihi = a.inc_end[node];
         // list mode (merged clusters, rescored nodes): every node above
         // kHeavySmallInc incident h-edges gets a CTA (a node's latency is the
         // level's critical path); full scoring: above ss_heavy_inc
@@ -406,7 +408,7 @@ __global__ void __launch_bounds__(SM_THREADS) k_score_mid(ScoreArgs a) {
             sover = 0;
         }
         __syncthreads();
-        const int64_t ilo = a.inc_off[node], ihi = a.inc_off[node + 1];
+        const int64_t ilo = a.inc_off[node], ihi = a.inc_end[node];
         const int bsz = (int)max((int64_t)1, min((int64_t)32, (ihi - ilo + NW - 1) / NW));
         warp_for_pins<4>(a.inc_dat, ilo, ihi, (int64_t)w * bsz, (int64_t)NW * bsz, a.pin_off, a.pin_dat,
                          [&](int32_t e, int32_t m) {
@@ -485,8 +487,8 @@ __global__ void __launch_bounds__(SM_THREADS) k_score_mid(ScoreArgs a) {
                 }
             __syncthreads();
             if (bk < 0) break;
-            const int64_t nlo = a.in_off[node], nn = a.in_off[node + 1] - nlo;
-            const int64_t mlo = a.in_off[bk], nm = a.in_off[bk + 1] - mlo;
+            const int64_t nlo = a.in_off[node], nn = a.in_end[node] - nlo;
+            const int64_t mlo = a.in_off[bk], nm = a.in_end[bk] - mlo;
             bool ok = true;
             if (nn + nm > a.delta) {
                 const bool ns = nn <= nm;
@@ -563,7 +565,7 @@ __global__ void __launch_bounds__(SH_THREADS) k_score_heavy(ScoreArgs a, int pai
             sover = 0;
         }
         __syncthreads();
-        const int64_t ilo = a.inc_off[node], ihi = a.inc_off[node + 1];
+        const int64_t ilo = a.inc_off[node], ihi = a.inc_end[node];
         int pend = 0;  // this thread's new keys not yet added to snk
         // h-edges per warp batch: a node's h-edges spread over all warps
         // (of both CTAs of a pair)
@@ -701,8 +703,8 @@ __global__ void __launch_bounds__(SH_THREADS) k_score_heavy(ScoreArgs a, int pai
             }
             __syncthreads();
             if (bk < 0) break;
-            const int64_t nlo = a.in_off[node], nn = a.in_off[node + 1] - nlo;
-            const int64_t mlo = a.in_off[bk], nm = a.in_off[bk + 1] - mlo;
+            const int64_t nlo = a.in_off[node], nn = a.in_end[node] - nlo;
+            const int64_t mlo = a.in_off[bk], nm = a.in_end[bk] - mlo;
             bool ok = true;
             if (nn + nm > a.delta) {
                 const bool ns = nn <= nm;
@@ -761,7 +763,7 @@ __global__ void __launch_bounds__(SB_THREADS) k_score_block(ScoreArgs a, long lo
         const int32_t node = a.big_list[t];
         if (threadIdx.x == 0) s_nt = 0;
         __syncthreads();
-        const int64_t ilo = a.inc_off[node], ihi = a.inc_off[node + 1];
+        const int64_t ilo = a.inc_off[node], ihi = a.inc_end[node];
         // h-edges per warp batch: a node's h-edges spread over all warps
         const int bsz = (int)max((int64_t)1, min((int64_t)32, (ihi - ilo + nw - 1) / nw));
         warp_for_pins<4>(a.inc_dat, ilo, ihi, (int64_t)w * bsz, (int64_t)nw * bsz, a.pin_off, a.pin_dat,
@@ -829,8 +831,8 @@ __global__ void __launch_bounds__(SB_THREADS) k_score_block(ScoreArgs a, long lo
             __syncthreads();
             if (bk < 0) break;
             // union check by the whole block
-            const int64_t nlo = a.in_off[node], nn = a.in_off[node + 1] - nlo;
-            const int64_t mlo = a.in_off[bk], nm = a.in_off[bk + 1] - mlo;
+            const int64_t nlo = a.in_off[node], nn = a.in_end[node] - nlo;
+            const int64_t mlo = a.in_off[bk], nm = a.in_end[bk] - mlo;
             bool ok;
             if (nn + nm <= a.delta) {
                 ok = true;
@@ -905,7 +907,7 @@ __global__ void k_inc_tuples_quick(ScoreArgs a, unsigned long long *best, int32_
     const int64_t nt = min((int64_t)*a.tup_count, a.tup_cap);
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nt; i += (int64_t)gridDim.x * blockDim.x) {
         const int32_t v = a.tup_v[i], b = a.tup_b[i];
-        if ((a.in_off[v + 1] - a.in_off[v]) + (a.in_off[b + 1] - a.in_off[b]) <= a.delta)
+        if ((a.in_end[v] - a.in_off[v]) + (a.in_end[b] - a.in_off[b]) <= a.delta)
             atomicMax(&best[v], tuple_key(a.tup_h[i], b));
         else
             hard[atomicAdd(hard_count, 1)] = (int32_t)i;
@@ -1085,8 +1087,8 @@ void score_select(Ctx &c, const DLevel &L, const DWeights &W, int64_t omega, int
     if (L.N == 0) return;
     KScope ks(c, "score_select", 0.0, L.N);
     score_attrs(c);
-    ScoreArgs a{L.N, L.inc_off, L.inc_dat, L.pin_off, L.pin_dat, W.wi, L.size, L.in_off, L.in_dat, omega, delta,
-                pair, score, s.ctr, s.big, s.ctr + 1, s.heavy, s.ctr + 2, tiers(), 0, L.N};
+    ScoreArgs a{L.N, L.inc_off, L.inc_dat, L.pin_off, L.pin_dat, W.wi, L.size, L.in_off, L.in_dat, L.inc_e(), L.in_e(),
+                omega, delta, pair, score, s.ctr, s.big, s.ctr + 1, s.heavy, s.ctr + 2, tiers(), 0, L.N};
     const Shard sh = shard_of(c.comm, L.N);
     a.lo = (int32_t)sh.lo;
     a.hi = (int32_t)sh.hi;
@@ -1134,8 +1136,8 @@ void score_select_inc(Ctx &c, const DLevel &L, const DWeights &W, int64_t omega,
                                                             cy.prev_score, kind, thr_s, thr_p, best, list, lc);
     DHGP_LAUNCHED(c);
     // pass 1: the merged clusters, emitting their beating neighbour tuples
-    ScoreArgs a{N, L.inc_off, L.inc_dat, L.pin_off, L.pin_dat, W.wi, L.size, L.in_off, L.in_dat, omega, delta,
-                pair, score, s.ctr, s.big, s.ctr + 1, s.heavy, s.ctr + 2, tiers(), 0, N};
+    ScoreArgs a{N, L.inc_off, L.inc_dat, L.pin_off, L.pin_dat, W.wi, L.size, L.in_off, L.in_dat, L.inc_e(), L.in_e(),
+                omega, delta, pair, score, s.ctr, s.big, s.ctr + 1, s.heavy, s.ctr + 2, tiers(), 0, N};
     a.list = list;
     a.list_count = lc;
     a.mb = cy.mb;
@@ -1173,8 +1175,8 @@ void score_select_inc(Ctx &c, const DLevel &L, const DWeights &W, int64_t omega,
                                                                 cap, pair, score, list2, lc + 1);
     DHGP_LAUNCHED(c);
     // pass 2: singletons whose carried pair merged and no cluster outranks it
-    ScoreArgs b{N, L.inc_off, L.inc_dat, L.pin_off, L.pin_dat, W.wi, L.size, L.in_off, L.in_dat, omega, delta,
-                pair, score, s.ctr, s.big, s.ctr + 1, s.heavy, s.ctr + 2, tiers(), 0, N};
+    ScoreArgs b{N, L.inc_off, L.inc_dat, L.pin_off, L.pin_dat, W.wi, L.size, L.in_off, L.in_dat, L.inc_e(), L.in_e(),
+                omega, delta, pair, score, s.ctr, s.big, s.ctr + 1, s.heavy, s.ctr + 2, tiers(), 0, N};
     b.list = list2;
     b.list_count = lc + 1;
     b.work = work;
@@ -1438,7 +1440,8 @@ __global__ void k_gamma(int32_t N, const int32_t *match, const int64_t *rank, co
 }
 // gathers the coarse totals into the status words
 __global__ void k_contract_status(int32_t N, int32_t E, const int64_t *rank, const int64_t *so, const int64_t *dof,
-                                  const int64_t *po, const int64_t *io, const int64_t *co, int64_t *status) {
+                                  const int64_t *po, const int64_t *io, const int64_t *co, int64_t *status,
+                                  const unsigned long long *pool_ctr, int64_t fine_sin, int64_t fine_uinc) {
     pdl_entry();
     if (threadIdx.x || blockIdx.x) return;
     const int64_t nc = rank[N];
@@ -1446,8 +1449,15 @@ __global__ void k_contract_status(int32_t N, int32_t E, const int64_t *rank, con
     status[4] = so[E];
     status[5] = dof[E];
     status[6] = po[E];
-    status[7] = io[nc];
-    status[8] = co[nc];
+    if (pool_ctr) {  // pooled: totals = fine totals - what the unions removed; the pool's tops
+        status[7] = fine_sin - (int64_t)pool_ctr[2];
+        status[8] = fine_uinc - (int64_t)pool_ctr[3];
+        status[9] = (int64_t)pool_ctr[0];
+        status[10] = (int64_t)pool_ctr[1];
+    } else {
+        status[7] = io[nc];
+        status[8] = co[nc];
+    }
 }
 
 // Per-node families (in, inc) of the coarse level: the sorted union of the
@@ -1460,9 +1470,14 @@ __global__ void k_contract_status(int32_t N, int32_t E, const int64_t *rank, con
 struct NodeFam {
     const int64_t *off;
     const int32_t *dat;
-    int64_t *cnt;            // count pass
-    const int64_t *out_off;  // write pass
+    int64_t *cnt;            // count pass (CSR mode)
+    const int64_t *out_off;  // write pass: where the coarse list starts
     int32_t *out;
+    const int64_t *end = nullptr;   // fine list ends (DLevel::in_e / inc_e)
+    int64_t *obeg = nullptr;        // pooled mode, count pass: coarse begin / end ...
+    int64_t *oend = nullptr;
+    unsigned long long *top = nullptr;     // ... the pool's next free slot
+    unsigned long long *shrink = nullptr;  // ... and the total removed by the unions (|a|+|b|-|a u b|)
 };
 struct NodeFams {
     NodeFam f[2];
@@ -1487,18 +1502,37 @@ __device__ __forceinline__ int64_t blk_excl_flags(bool f, int64_t *sh_w, int64_t
 
 // thread per coarse node: a singleton's count is its member's length; zero
 // past nc (the offsets scan runs over the fine count)
+// (pooled mode: a singleton keeps its member's list where it is)
 __global__ void k_node_count(int64_t nc_cap, const int64_t *d_nc, const int32_t *ma, const int32_t *mb, NodeFams fs) {
     pdl_entry();
     const NodeFam &f = fs.f[blockIdx.y];
     const int64_t nc = *d_nc;
     for (int64_t cn = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; cn < nc_cap;
          cn += (int64_t)gridDim.x * blockDim.x) {
-        if (cn >= nc) {
+        if (f.obeg) {
+            if (cn < nc && mb[cn] < 0) {
+                const int32_t a = ma[cn];
+                f.obeg[cn] = f.off[a];
+                f.oend[cn] = f.end[a];
+            }
+        } else if (cn >= nc) {
             f.cnt[cn] = 0;
         } else if (mb[cn] < 0) {
             const int32_t a = ma[cn];
-            f.cnt[cn] = f.off[a + 1] - f.off[a];
+            f.cnt[cn] = f.end[a] - f.off[a];
         }
+    }
+}
+// count pass of a merged cluster: the union's length u (CSR: its count;
+// pooled: slots reserved at the pool's top)
+__device__ __forceinline__ void union_counted(const NodeFam &f, int32_t cn, int64_t na, int64_t nb, int64_t u) {
+    if (f.obeg) {
+        const int64_t b = (int64_t)atomicAdd(f.top, (unsigned long long)u);
+        f.obeg[cn] = b;
+        f.oend[cn] = b + u;
+        if (na + nb - u) atomicAdd(f.shrink, (unsigned long long)(na + nb - u));
+    } else {
+        f.cnt[cn] = u;
     }
 }
 
@@ -1538,7 +1572,7 @@ __global__ void __launch_bounds__(UW_WARPS * 32) k_node_union_warp(const int32_t
     const int n = *mcount;
     for (int t = blockIdx.x * UW_WARPS + w; t < n; t += gridDim.x * UW_WARPS) {
         const int32_t cn = mlist[t], a = ma[cn], b = mb[cn];
-        const int64_t alo = f.off[a], na = f.off[a + 1] - alo, blo = f.off[b], nb = f.off[b + 1] - blo;
+        const int64_t alo = f.off[a], na = f.end[a] - alo, blo = f.off[b], nb = f.end[b] - blo;
         if (!warp_union_path(na, nb)) continue;
         if (!WRITE && emark && blockIdx.y == 1)
             for (int64_t i = lane; i < nb; i += 32) emark[f.dat[blo + i]] = 1;
@@ -1549,7 +1583,7 @@ __global__ void __launch_bounds__(UW_WARPS * 32) k_node_union_warp(const int32_t
             int common = 0;
             for (int j = lane; j < ns; j += 32) common += bsearch_dev(L, 0, nl, S[j]) >= 0;
             common = warp_sum(common);
-            if (lane == 0) f.cnt[cn] = na + nb - common;
+            if (lane == 0) union_counted(f, cn, na, nb, na + nb - common);
             continue;
         }
         int32_t *o = f.out + f.out_off[cn];
@@ -1596,7 +1630,7 @@ __global__ void __launch_bounds__(UN_THREADS) k_node_union(const int32_t *ma, co
     const int n = *mcount;
     for (int t = blockIdx.x; t < n; t += gridDim.x) {
         const int32_t cn = mlist[t], a = ma[cn], b = mb[cn];
-        const int64_t alo = f.off[a], na = f.off[a + 1] - alo, blo = f.off[b], nb = f.off[b + 1] - blo;
+        const int64_t alo = f.off[a], na = f.end[a] - alo, blo = f.off[b], nb = f.end[b] - blo;
         if (warp_union_path(na, nb)) continue;  // k_node_union_warp
         if (!WRITE && emark && blockIdx.y == 1)
             for (int64_t i = threadIdx.x; i < nb; i += blockDim.x) emark[f.dat[blo + i]] = 1;
@@ -1643,7 +1677,7 @@ __global__ void __launch_bounds__(UN_THREADS) k_node_union(const int32_t *ma, co
                     }
                 }
             } else if (threadIdx.x == 0) {
-                f.cnt[cn] = tot;
+                union_counted(f, cn, na, nb, tot);
             }
             __syncthreads();
             continue;
@@ -1652,7 +1686,7 @@ __global__ void __launch_bounds__(UN_THREADS) k_node_union(const int32_t *ma, co
             int64_t common = 0;
             for (int64_t i = threadIdx.x; i < ns; i += blockDim.x) common += bsearch_dev(L, 0, nl, S[i]) >= 0;
             const int64_t tot = block_sum<int64_t>(common, sh);
-            if (threadIdx.x == 0) f.cnt[cn] = na + nb - tot;
+            if (threadIdx.x == 0) union_counted(f, cn, na, nb, na + nb - tot);
             __syncthreads();
             continue;
         }
@@ -1754,7 +1788,7 @@ __global__ void __launch_bounds__(256) k_node_write(int64_t nc, int split, const
         if (cn < c1) clean = mb[cn] < 0 && ma[cn] == a0 + (int32_t)(cn - c0);
         if (__syncthreads_and(clean)) {
             const int32_t a1 = ma[c1 - 1];
-            const int64_t lo = f.off[a0], len = f.off[a1 + 1] - lo;
+            const int64_t lo = f.off[a0], len = f.end[a1] - lo;
             const int32_t *src = f.dat + lo;
             int32_t *dst = f.out + f.out_off[c0];
             int64_t i = sl * blockDim.x + threadIdx.x;
@@ -1777,7 +1811,7 @@ __global__ void __launch_bounds__(256) k_node_write(int64_t nc, int split, const
                     const int32_t a = ma[q];
                     s_src[threadIdx.x + 32 * h] = f.off[a];
                     s_dst[threadIdx.x + 32 * h] = f.out_off[q];
-                    len[h] = f.off[a + 1] - f.off[a];
+                    len[h] = f.end[a] - f.off[a];
                 }
             }
             const int64_t i0 = warp_incl_scan(len[0]);
@@ -2098,7 +2132,7 @@ static int union_words(Ctx &c, int32_t E) {
 }
 
 void contract_count(Ctx &c, DLevel &fine, const int32_t *match, const uint8_t *isrep, DLevel &coarse,
-                    ContractScratch &s, int64_t *d_status) {
+                    ContractScratch &s, int64_t *d_status, NodePool *pool) {
     // algorithmic bytes: each fine h-edge list entry and its gamma image read
     // once (8 B), per-h-edge offsets read and counts / coarse offsets written
     // (60 B), per-node rank / gamma / members (24 B)
@@ -2122,12 +2156,35 @@ void contract_count(Ctx &c, DLevel &fine, const int32_t *match, const uint8_t *i
     // per-node families first: the merged clusters flag the h-edges whose
     // lists need the sort / de-duplication
     KScope kcn(c, "cc_nodes");
-    int64_t *ncnt = c.alloc<int64_t>(2 * (int64_t)N);
+    int64_t *ncnt = pool ? nullptr : c.alloc<int64_t>(2 * (int64_t)N);
     coarse.in_off = c.alloc<int64_t>((int64_t)N + 1);
     coarse.inc_off = c.alloc<int64_t>((int64_t)N + 1);
+    unsigned long long *pool_ctr = nullptr;  // pooled: [0..1] pool tops (in, inc), [2..3] union shrink
+    if (pool) {
+        coarse.in_end = c.alloc<int64_t>(N);
+        coarse.inc_end = c.alloc<int64_t>(N);
+        coarse.pooled = true;
+        coarse.in_dat = pool->dat[0];
+        coarse.inc_dat = pool->dat[1];
+        s.pool_ctr = pool_ctr = c.alloc<unsigned long long>(4);
+        c.d2d((int64_t *)pool_ctr, pool->top, 2);
+        c.zero(pool_ctr + 2, 2);
+    }
     {
-        const NodeFams fs{{NodeFam{fine.in_off, fine.in_dat, ncnt, nullptr, nullptr},
-                           NodeFam{fine.inc_off, fine.inc_dat, ncnt + N, nullptr, nullptr}}};
+        NodeFams fs{{NodeFam{fine.in_off, fine.in_dat, ncnt, nullptr, nullptr},
+                     NodeFam{fine.inc_off, fine.inc_dat, ncnt ? ncnt + N : nullptr, nullptr, nullptr}}};
+        fs.f[0].end = fine.in_e();
+        fs.f[1].end = fine.inc_e();
+        if (pool) {
+            fs.f[0].obeg = coarse.in_off;
+            fs.f[0].oend = coarse.in_end;
+            fs.f[1].obeg = coarse.inc_off;
+            fs.f[1].oend = coarse.inc_end;
+            fs.f[0].top = pool_ctr;
+            fs.f[1].top = pool_ctr + 1;
+            fs.f[0].shrink = pool_ctr + 2;
+            fs.f[1].shrink = pool_ctr + 3;
+        }
         const unsigned ga = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(N, 256), (int64_t)c.num_sms * 8));
         pdl_launch(k_node_count, dim3(ga, 2), 256, 0, c.stream, N, d_nc, s.ma, s.mb, fs);
         DHGP_LAUNCHED(c);
@@ -2139,8 +2196,10 @@ void contract_count(Ctx &c, DLevel &fine, const int32_t *match, const uint8_t *i
                                                                                      s.emark, words);
         DHGP_LAUNCHED(c);
     }
-    scan_excl3<int64_t>(c, ncnt, coarse.in_off, ncnt + N, coarse.inc_off, nullptr, nullptr, N);
-    c.free(ncnt);
+    if (!pool) {
+        scan_excl3<int64_t>(c, ncnt, coarse.in_off, ncnt + N, coarse.inc_off, nullptr, nullptr, N);
+        c.free(ncnt);
+    }
     kcn.close();
     // per-h-edge families: sorted unique gamma image (coarsen.py:163-166)
     KScope kcs(c, "cc_edges");
@@ -2204,11 +2263,12 @@ void contract_count(Ctx &c, DLevel &fine, const int32_t *match, const uint8_t *i
     }
     kcs.close();
     pdl_launch(k_contract_status, 1, 32, 0, c.stream, N, E, s.rank, coarse.src_off, coarse.dst_off, coarse.pin_off,
-                                              coarse.in_off, coarse.inc_off, d_status);
+               coarse.in_off, coarse.inc_off, d_status, (const unsigned long long *)pool_ctr, fine.Sin, fine.U);
     DHGP_LAUNCHED(c);
 }
 
-void contract_write(Ctx &c, DLevel &fine, DLevel &coarse, ContractScratch &s, const LevelStatus &st) {
+void contract_write(Ctx &c, DLevel &fine, DLevel &coarse, ContractScratch &s, const LevelStatus &st,
+                    NodePool *pool) {
     // algorithmic bytes: fine h-edge lists + gamma read (8 B per entry), coarse
     // lists written (4 B), fine node lists read and coarse ones written (4 B
     // each), offsets (16 B per h-edge, 16 B per coarse node)
@@ -2226,8 +2286,14 @@ void contract_write(Ctx &c, DLevel &fine, DLevel &coarse, ContractScratch &s, co
         coarse.src_dat = c.alloc<int32_t>(st.ps);
         coarse.dst_dat = c.alloc<int32_t>(st.pd);
         coarse.pin_dat = c.alloc<int32_t>(st.u);
-        coarse.in_dat = c.alloc<int32_t>(st.sin);
-        coarse.inc_dat = c.alloc<int32_t>(st.uinc);
+        if (!pool) {
+            coarse.in_dat = c.alloc<int32_t>(st.sin);
+            coarse.inc_dat = c.alloc<int32_t>(st.uinc);
+        } else {  // the pool may have grown since the count pass
+            coarse.in_dat = pool->dat[0];
+            coarse.inc_dat = pool->dat[1];
+            c.h2d(pool->top, st.pool_top, 2);
+        }
     }
     {
         KScope k2(c, "cw_unique");
@@ -2267,15 +2333,19 @@ void contract_write(Ctx &c, DLevel &fine, DLevel &coarse, ContractScratch &s, co
     {
         KScope k2(c, "cw_merge");
         if (st.nc > 0) {
-            const NodeFams fs{{NodeFam{fine.in_off, fine.in_dat, nullptr, coarse.in_off, coarse.in_dat},
-                               NodeFam{fine.inc_off, fine.inc_dat, nullptr, coarse.inc_off, coarse.inc_dat}}};
-            // slices per chunk: about 4K list entries per CTA
-            const int64_t per_chunk = cdiv(std::max(fine.Sin, fine.U) * kNodeChunk, std::max<int64_t>(1, fine.N));
-            const int split = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(per_chunk, 4096), 64));
-            const int64_t items = cdiv(st.nc, kNodeChunk) * split;
-            const unsigned g = (unsigned)std::min<int64_t>(items, (int64_t)c.num_sms * 16);
-            pdl_launch(k_node_write, dim3(g, 2), 256, 0, c.stream, st.nc, split, s.ma, s.mb, fs);
-            DHGP_LAUNCHED(c);
+            NodeFams fs{{NodeFam{fine.in_off, fine.in_dat, nullptr, coarse.in_off, coarse.in_dat},
+                         NodeFam{fine.inc_off, fine.inc_dat, nullptr, coarse.inc_off, coarse.inc_dat}}};
+            fs.f[0].end = fine.in_e();
+            fs.f[1].end = fine.inc_e();
+            if (!pool) {  // CSR: the singletons' lists are copied (pooled: they stay where they are)
+                // slices per chunk: about 4K list entries per CTA
+                const int64_t per_chunk = cdiv(std::max(fine.Sin, fine.U) * kNodeChunk, std::max<int64_t>(1, fine.N));
+                const int split = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(per_chunk, 4096), 64));
+                const int64_t items = cdiv(st.nc, kNodeChunk) * split;
+                const unsigned g = (unsigned)std::min<int64_t>(items, (int64_t)c.num_sms * 16);
+                pdl_launch(k_node_write, dim3(g, 2), 256, 0, c.stream, st.nc, split, s.ma, s.mb, fs);
+                DHGP_LAUNCHED(c);
+            }
             const int words = union_words(c, E);
             pdl_launch(k_node_union_warp<true>, dim3(4 * c.num_sms, 2), UW_WARPS * 32, 0, c.stream, s.ma, s.mb, s.mlist,
                        s.mcount, fs, nullptr);
@@ -2360,7 +2430,40 @@ void contract_release(Ctx &c, ContractScratch &s) {
     c.free(s.elist);
     c.free(s.ecount);
     c.free(s.epos);
+    c.free(s.pool_ctr);
     s = ContractScratch();
+}
+
+void node_pool_init(Ctx &c, NodePool &pool, DLevel &L0, double factor) {
+    const int64_t n[2] = {L0.Sin, L0.U};
+    int32_t *src[2] = {L0.in_dat, L0.inc_dat};
+    pool.top = c.alloc<int64_t>(2);
+    for (int f = 0; f < 2; f++) {
+        pool.cap[f] = (int64_t)(factor * (double)n[f]) + (1 << 20);
+        pool.dat[f] = c.alloc<int32_t>(pool.cap[f]);
+        c.d2d(pool.dat[f], src[f], n[f]);
+        c.free(src[f]);
+    }
+    c.h2d(pool.top, n, 2);
+    L0.in_dat = pool.dat[0];
+    L0.inc_dat = pool.dat[1];
+    L0.pooled = true;
+}
+
+void node_pool_fit(Ctx &c, NodePool &pool, const int64_t top[2], std::vector<DLevel> &levels, DLevel *extra) {
+    for (int f = 0; f < 2; f++) {
+        if (top[f] <= pool.cap[f]) continue;
+        const int64_t cap = std::max<int64_t>(2 * pool.cap[f], top[f] + (top[f] >> 1));
+        int32_t *d = c.alloc<int32_t>(cap);
+        c.d2d(d, pool.dat[f], pool.cap[f]);
+        int32_t *old = pool.dat[f];
+        for (auto &L : levels)
+            if (L.pooled) (f ? L.inc_dat : L.in_dat) = d;
+        if (extra && extra->pooled) (f ? extra->inc_dat : extra->in_dat) = d;
+        c.free(old);
+        pool.dat[f] = d;
+        pool.cap[f] = cap;
+    }
 }
 
 }  // namespace dhgp

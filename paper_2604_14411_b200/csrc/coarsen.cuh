@@ -1,5 +1,7 @@
 // coarsen.cuh — one coarsening level on device.
 #pragma once
+#include <vector>
+
 #include "graph.cuh"
 
 namespace dhgp {
@@ -48,8 +50,9 @@ struct LevelStatus {
     int64_t bad_cert;  // (score, id) monotonicity certificate failed somewhere
     int64_t long_run;  // a run of won claims longer than the walk limit
     int64_t nc, ps, pd, u, sin, uinc;  // coarse sizes
+    int64_t pool_top[2];               // node pool: slots in use after this level's unions (pooled mode)
 };
-constexpr int kStatusWords = 9;
+constexpr int kStatusWords = 11;
 
 // A7: pseudo-forest -> involution (_kernels.pyx:106-181), no host sync:
 // status->moved / bad_cert / long_run are written on device.
@@ -78,10 +81,21 @@ struct ContractScratch {
     int32_t *elist = nullptr;  // marked h-edges (emark), ascending ...
     int32_t *ecount = nullptr; // ... and their count
     int64_t *epos = nullptr;   // [E+1] exclusive scan of emark
+    unsigned long long *pool_ctr = nullptr;  // pooled mode: pool tops + union shrink (count pass)
 };
+// With a node pool, the coarse level's per-node lists are pooled: an
+// unmerged node keeps its list, a merged cluster's union is appended to the
+// pool (reserved in the count pass; the host grows the pool with
+// node_pool_fit when the status words show it overflowed); otherwise
+// (pool == nullptr) the coarse level gets its own CSR node lists.
 void contract_count(Ctx &c, DLevel &fine, const int32_t *match, const uint8_t *isrep, DLevel &coarse,
-                    ContractScratch &s, int64_t *d_status);
-void contract_write(Ctx &c, DLevel &fine, DLevel &coarse, ContractScratch &s, const LevelStatus &st);
+                    ContractScratch &s, int64_t *d_status, NodePool *pool = nullptr);
+void contract_write(Ctx &c, DLevel &fine, DLevel &coarse, ContractScratch &s, const LevelStatus &st,
+                    NodePool *pool = nullptr);
+// node pool: create from level 0 (its lists move into the pool) and grow so
+// that the reserved slots fit (levels' data pointers follow)
+void node_pool_init(Ctx &c, NodePool &pool, DLevel &level0, double factor);
+void node_pool_fit(Ctx &c, NodePool &pool, const int64_t top[2], std::vector<DLevel> &levels, DLevel *extra);
 void contract_release(Ctx &c, ContractScratch &s);
 // contract_write leaves s.ma / s.mb (cluster members, for ScoreCarry); the
 // caller frees them with this

@@ -270,12 +270,14 @@ constexpr size_t kCheckpoint = 16;
 
 // device bytes of one level's lists (what level_to_stub would release)
 static size_t level_bytes(const DLevel &L) {
+    if (L.pooled)  // the node lists live in the pool: only their (begin, end) arrays are the level's
+        return 8 * (3 * (size_t)L.E + 4 * (size_t)L.N + 5) + 4 * ((size_t)L.Ps + L.Pd + L.U + L.N);
     return 8 * (3 * (size_t)L.E + 2 * (size_t)L.N + 5) + 4 * ((size_t)L.Ps + L.Pd + L.U + L.Sin + L.U + L.N);
 }
 
 // Rebuilds stub levels (lo, hi] by re-running the contraction from the
 // nearest full level below, using the stored gammas (bit-identical).
-static void rebuild_levels(Ctx &c, std::vector<DLevel> &levels, size_t hi) {
+static void rebuild_levels(Ctx &c, std::vector<DLevel> &levels, size_t hi, NodePool *pool) {
     size_t lo = hi;
     while (levels[lo].stub) lo--;
     int64_t *status = c.alloc<int64_t>(kStatusWords);
@@ -291,11 +293,12 @@ static void rebuild_levels(Ctx &c, std::vector<DLevel> &levels, size_t hi) {
         DLevel coarse;
         ContractScratch cs;
         c.zero(status, kStatusWords);
-        contract_count(c, f, match, isrep, coarse, cs, status);
+        contract_count(c, f, match, isrep, coarse, cs, status, pool);
         LevelStatus st;
         c.d2h((int64_t *)&st, status, kStatusWords);
         c.sync();
-        contract_write(c, f, coarse, cs, st);
+        if (pool) node_pool_fit(c, *pool, st.pool_top, levels, &coarse);
+        contract_write(c, f, coarse, cs, st, pool);
         contract_release_members(c, cs);
         coarse.gamma = next.gamma;  // the stored map to the level above
         next.gamma = nullptr;
@@ -561,6 +564,9 @@ static void run_partition(Ctx &c, const DInput &in, const dhgp_config &cfg, Part
     }
     std::vector<DLevel> levels(1);
     build_level0(c, in, levels[0]);
+    // per-node lists of every level in one pool (room for three times level 0's)
+    NodePool pool;
+    node_pool_init(c, pool, levels[0], 3.0);
 
     const double t0 = now_ms();
     c.sync_wait_ms = 0.0;
@@ -625,7 +631,7 @@ static void run_partition(Ctx &c, const DInput &in, const dhgp_config &cfg, Part
             launch_matching(c, n, pair, score, match, isrep, claim, status);
             DLevel coarse;
             ContractScratch cs;
-            contract_count(c, levels.back(), match, isrep, coarse, cs, status);
+            contract_count(c, levels.back(), match, isrep, coarse, cs, status, &pool);
             LevelStatus st;
             c.d2h((int64_t *)&st, status, kStatusWords);
             c.sync();
@@ -636,7 +642,7 @@ static void run_partition(Ctx &c, const DInput &in, const dhgp_config &cfg, Part
                     c.free(levels.back().gamma);
                     levels.back().gamma = nullptr;
                     c.zero(status, kStatusWords);
-                    contract_count(c, levels.back(), match, isrep, coarse, cs, status);
+                    contract_count(c, levels.back(), match, isrep, coarse, cs, status, &pool);
                     int64_t moved = st.moved;
                     c.d2h((int64_t *)&st, status, kStatusWords);
                     c.sync();
@@ -650,7 +656,8 @@ static void run_partition(Ctx &c, const DInput &in, const dhgp_config &cfg, Part
                 c.free(levels.back().gamma);
                 levels.back().gamma = nullptr;
             } else {
-                contract_write(c, levels.back(), coarse, cs, st);
+                node_pool_fit(c, pool, st.pool_top, levels, &coarse);
+                contract_write(c, levels.back(), coarse, cs, st, &pool);
                 levels.push_back(coarse);
             }
             if (!stop && obs)
@@ -687,6 +694,7 @@ static void run_partition(Ctx &c, const DInput &in, const dhgp_config &cfg, Part
     } catch (...) {
         free_carry();
         for (auto &L : levels) L.release(c);
+        pool.release(c);
         W.release(c);
         score_scratch_release(c, sscr);
         c.free(status);
@@ -723,7 +731,7 @@ static void run_partition(Ctx &c, const DInput &in, const dhgp_config &cfg, Part
         refine_level(c, levels[L - 1], W, rst, assign, K, omega, delta, cfg.max_rounds, (int32_t)(L - 1),
                      res.trace[0], obs ? &robs : nullptr, in.max_edge_pins);
         for (int64_t li = L - 2; li >= 0; li--) {
-            if (levels[li].stub) rebuild_levels(c, levels, (size_t)li);
+            if (levels[li].stub) rebuild_levels(c, levels, (size_t)li, &pool);
             DLevel &f = levels[li];
             refine_project(c, rst, f, levels[li + 1].N, assign, assign2);
             levels[li + 1].release(c);
@@ -744,12 +752,14 @@ static void run_partition(Ctx &c, const DInput &in, const dhgp_config &cfg, Part
     } catch (...) {
         refine_state_release(c, rst);
         for (auto &L : levels) L.release(c);
+        pool.release(c);
         W.release(c);
         c.free(assign);
         c.free(assign2);
         throw;
     }
     for (auto &L : levels) L.release(c);
+    pool.release(c);
     W.release(c);
     c.free(assign);
     c.free(assign2);

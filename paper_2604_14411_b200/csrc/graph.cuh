@@ -18,6 +18,13 @@ struct DLevel {
     int64_t *src_off = nullptr, *dst_off = nullptr, *pin_off = nullptr, *in_off = nullptr, *inc_off = nullptr;
     int32_t *src_dat = nullptr, *dst_dat = nullptr, *pin_dat = nullptr, *in_dat = nullptr, *inc_dat = nullptr;
     int32_t *size = nullptr;
+    // Per-node lists may live in a shared pool (node_pool): node n's list is
+    // [in_off[n], in_end[n]) of in_dat.  in_end == nullptr means plain CSR
+    // (end = in_off + 1); in_e() / inc_e() give the end array either way.
+    int64_t *in_end = nullptr, *inc_end = nullptr;
+    bool pooled = false;       // in_dat / inc_dat belong to the partition's node pool
+    const int64_t *in_e() const { return in_end ? in_end : in_off + 1; }
+    const int64_t *inc_e() const { return inc_end ? inc_end : inc_off + 1; }
     int32_t *gamma = nullptr;  // fine -> coarse map once this level has been contracted
     int32_t maxp = 0;          // bound on any h-edge's pin slots (src + dst) at this level
     bool borrowed = false;     // src/dst/size belong to a resident input (level 0)
@@ -27,9 +34,31 @@ struct DLevel {
             c.free(src_off); c.free(dst_off); c.free(src_dat); c.free(dst_dat); c.free(size);
         }
         c.free(pin_off); c.free(in_off); c.free(inc_off);
-        c.free(pin_dat); c.free(in_dat); c.free(inc_dat);
+        c.free(in_end); c.free(inc_end);
+        c.free(pin_dat);
+        if (!pooled) {
+            c.free(in_dat);
+            c.free(inc_dat);
+        }
         c.free(gamma);
         *this = DLevel();
+    }
+};
+
+// Shared storage of the per-node lists (in, inc) of every level: level 0's
+// lists, then each contraction's merged-cluster unions appended; an unmerged
+// node keeps pointing at its list where it is, so a contraction writes only
+// the unions and a kept level costs only its (begin, end) arrays.  Offsets
+// are relative to dat[f]; growing the pool moves the data and keeps them.
+struct NodePool {
+    int32_t *dat[2] = {nullptr, nullptr};  // [0] in lists, [1] inc lists
+    int64_t cap[2] = {0, 0};
+    int64_t *top = nullptr;                // device [2]: next free slot of each family
+    void release(Ctx &c) {
+        c.free(dat[0]);
+        c.free(dat[1]);
+        c.free(top);
+        *this = NodePool();
     }
 };
 

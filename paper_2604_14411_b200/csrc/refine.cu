@@ -277,6 +277,7 @@ struct ProposeArgs {
     int32_t hub_max = 0;
     const int32_t *hub_pref = nullptr;  // [hub_max + 1] chunk prefix (k_hub_prefix)
     unsigned long long *work = nullptr;  // profiling: algorithmic bytes
+    const int64_t *inc_end = nullptr;  // per-node list ends (DLevel::inc_e)
 };
 // hubs per propose pass: as many as 256 MB of accumulator rows allow (more go
 // to the block tiers); the chunk prefix over them is one small kernel
@@ -443,7 +444,7 @@ __global__ void __launch_bounds__(PR_WARPS * 32, 4) k_propose_warp(ProposeArgs a
         if (node == -1) break;
         if (a.ndirty && lane == 0 && a.list) a.ndirty[a.list[idx]] = 0;
         if (node < 0) continue;
-        const int64_t ilo = a.inc_off[node], ihi = a.inc_off[node + 1];
+        const int64_t ilo = a.inc_off[node], ihi = a.inc_end[node];
         if (ihi == ilo || a.K < 2) {
             if (lane == 0) write_proposal(a, node, 0, -1, 0, nullptr);
             continue;
@@ -587,7 +588,7 @@ __global__ void __launch_bounds__(PM_THREADS, 4) k_propose_mid(ProposeArgs a) {
     const int nmid = *a.big_count;
     for (int t = blockIdx.x; t < nmid; t += gridDim.x) {
         const int32_t node = a.big_list[t];
-        const int64_t ilo = a.inc_off[node], ihi = a.inc_off[node + 1];
+        const int64_t ilo = a.inc_off[node], ihi = a.inc_end[node];
         // table sized to the node: its distinct parts are at most min(K, sum of
         // its h-edges' run counts); zeroing and scanning 8192 slots per node
         // dominated when K is large and nodes touch few parts
@@ -729,7 +730,7 @@ __global__ void __launch_bounds__(THREADS) k_propose_heavy(ProposeArgs a) {
         const int32_t node = a.dense_list[t];
         if (threadIdx.x == 0) s_nt = 0;
         __syncthreads();
-        const int64_t ilo = a.inc_off[node], ihi = a.inc_off[node + 1];
+        const int64_t ilo = a.inc_off[node], ihi = a.inc_end[node];
         const int32_t ps = a.assign[node];
         long long total = 0, saving = 0;
         // h-edges per warp batch: a node's h-edges spread over all warps
@@ -797,7 +798,8 @@ __global__ void __launch_bounds__(THREADS) k_propose_heavy(ProposeArgs a) {
 // chunk counts of the listed hubs, scanned by one CTA (the hub kernel's
 // work items are (hub, chunk) pairs)
 __global__ void __launch_bounds__(1024) k_hub_prefix(const int32_t *hub_list, const int32_t *hub_count, int hub_max,
-                                                     const int64_t *inc_off, int32_t *pref) {
+                                                     const int64_t *inc_off, const int64_t *inc_end,
+                                                     int32_t *pref) {
     pdl_entry();
     __shared__ int32_t s_wt[32];
     const int nh = min(*hub_count, hub_max);
@@ -809,7 +811,7 @@ __global__ void __launch_bounds__(1024) k_hub_prefix(const int32_t *hub_list, co
         int32_t cnt = 0;
         if (i < nh) {
             const int32_t n = hub_list[i];
-            cnt = (int32_t)cdiv_dev(inc_off[n + 1] - inc_off[n], (int64_t)HUB_CHUNK);
+            cnt = (int32_t)cdiv_dev(inc_end[n] - inc_off[n], (int64_t)HUB_CHUNK);
         }
         const int32_t incl = warp_incl_scan(cnt);
         if (lane == 31) s_wt[w] = incl;
@@ -860,7 +862,7 @@ __global__ void __launch_bounds__(256) k_propose_hub(ProposeArgs a, long long *h
         const int64_t nch = s_pref[h + 1] - s_pref[h];
         const int32_t node = a.hub_list[h];
         const int64_t ilo = a.inc_off[node] + chunk * HUB_CHUNK;
-        const int64_t ihi = min(a.inc_off[node + 1], ilo + (int64_t)HUB_CHUNK);
+        const int64_t ihi = min(a.inc_end[node], ilo + (int64_t)HUB_CHUNK);
         for (int p = threadIdx.x; p < K; p += blockDim.x) pres[p] = 0;
         __syncthreads();
         const int32_t ps = a.assign[node];
@@ -942,7 +944,7 @@ __global__ void __launch_bounds__(PB_THREADS) k_propose_block(ProposeArgs a, lon
         const int32_t node = a.dense_list[t];
         if (threadIdx.x == 0) s_nt = 0;
         __syncthreads();
-        const int64_t ilo = a.inc_off[node], ihi = a.inc_off[node + 1];
+        const int64_t ilo = a.inc_off[node], ihi = a.inc_end[node];
         const int32_t ps = a.assign[node];
         long long total = 0, saving = 0;
         // h-edges per warp batch: a node's h-edges spread over all warps
@@ -1955,14 +1957,14 @@ __global__ void k_runs_update(const int32_t *elist, const int32_t *ecount, int32
 // hub's thousands of h-edges do not serialise on one warp
 template <class NodeOf, class F>
 __device__ __forceinline__ void grid_incidences(int64_t nitems, NodeOf node_of, const int64_t *inc_off,
-                                                const int32_t *inc_dat, F f) {
+                                                const int64_t *inc_end, const int32_t *inc_dat, F f) {
     if (nitems <= 0) return;
     const int64_t G = gridDim.x;
     const int64_t slices = G > nitems ? G / nitems : 1;  // CTAs per item
     for (int64_t t = blockIdx.x; t < nitems * slices; t += G) {
         const int64_t i = t / slices, sl = t - i * slices;
         const int32_t n = node_of(i);
-        const int64_t hi = inc_off[n + 1];
+        const int64_t hi = inc_end[n];
         for (int64_t j = inc_off[n] + sl * blockDim.x + threadIdx.x; j < hi; j += slices * blockDim.x)
             f(i, inc_dat[j]);
     }
@@ -2109,11 +2111,11 @@ __global__ void k_mark_psize(int32_t N, const int32_t *target, const uint8_t *fs
 }
 
 // the round's movers' h-edges (for the sequence gains and inbound events)
-__global__ void k_mover_edges(const int64_t *dM, const int32_t *node, const int64_t *inc_off, const int32_t *inc_dat,
-                              int32_t *emflag, int32_t *mlist, int32_t *mcount, bool spec) {
+__global__ void k_mover_edges(const int64_t *dM, const int32_t *node, const int64_t *inc_off, const int64_t *inc_end,
+                              const int32_t *inc_dat, int32_t *emflag, int32_t *mlist, int32_t *mcount, bool spec) {
     pdl_entry();
     if (spec && *dM > kSpecCap) return;  // speculative launch, M too large
-    grid_incidences(*dM, [&](int64_t i) { return node[i]; }, inc_off, inc_dat,
+    grid_incidences(*dM, [&](int64_t i) { return node[i]; }, inc_off, inc_end, inc_dat,
                     [&](int64_t, int32_t e) { push_once(&emflag[e], 1, e, mlist, mcount); });
 }
 
@@ -2121,7 +2123,8 @@ __global__ void k_mover_edges(const int64_t *dM, const int32_t *node, const int6
 // part sizes, grown parts, the movers' h-edges; also clears the round's
 // mover-edge flags
 __global__ void k_apply_inc(int64_t k, const int32_t *node, const int32_t *from, const int32_t *to,
-                            const int32_t *size, const int64_t *inc_off, const int32_t *inc_dat, int32_t *assign,
+                            const int32_t *size, const int64_t *inc_off, const int64_t *inc_end,
+                            const int32_t *inc_dat, int32_t *assign,
                             int64_t *psizes, uint8_t *pflags, int32_t *edirty, int32_t *elist, int32_t *ecount,
                             int32_t *emflag, const int32_t *mlist, const int32_t *mcount, int32_t *ndirty,
                             int32_t *nlist, int32_t *ncount) {
@@ -2136,7 +2139,7 @@ __global__ void k_apply_inc(int64_t k, const int32_t *node, const int32_t *from,
         atomicAdd((unsigned long long *)&psizes[to[i]], (unsigned long long)s);
         pflags[from[i]] = 2;
     }
-    grid_incidences(k, [&](int64_t i) { return node[i]; }, inc_off, inc_dat,
+    grid_incidences(k, [&](int64_t i) { return node[i]; }, inc_off, inc_end, inc_dat,
                     [&](int64_t, int32_t e) { push_once(&edirty[e], 2, e, elist, ecount); });
     const int64_t nm = *mcount;
     for (int64_t i = tid; i < nm; i += nt) emflag[mlist[i]] = 0;
@@ -2193,17 +2196,17 @@ __global__ void k_project_state(int32_t N, const int32_t *gamma, const int32_t *
 // counts are unchanged.  A CTA per split: inc(a) n inc(b) and in(a) n in(b)
 // by binary search of the shorter list in the longer.
 __global__ void k_split_counts(const int32_t *splist, const int32_t *spcount, const int64_t *inc_off,
-                               const int32_t *inc_dat, const int64_t *in_off, const int32_t *in_dat,
-                               const int32_t *assign, Runs r) {
+                               const int64_t *inc_end, const int32_t *inc_dat, const int64_t *in_off,
+                               const int64_t *in_end, const int32_t *in_dat, const int32_t *assign, Runs r) {
     pdl_entry();
     const int n = *spcount;
     for (int t = blockIdx.x; t < n; t += gridDim.x) {
         const int32_t a = splist[2 * t], b = splist[2 * t + 1], P = assign[a];
 #pragma unroll
         for (int fam = 0; fam < 2; fam++) {
-            const int64_t *off = fam ? in_off : inc_off;
+            const int64_t *off = fam ? in_off : inc_off, *end = fam ? in_end : inc_end;
             const int32_t *dat = fam ? in_dat : inc_dat;
-            const int64_t alo = off[a], na = off[a + 1] - alo, blo = off[b], nb = off[b + 1] - blo;
+            const int64_t alo = off[a], na = end[a] - alo, blo = off[b], nb = end[b] - blo;
             const bool as = na <= nb;
             const int32_t *S = dat + (as ? alo : blo), *L = dat + (as ? blo : alo);
             const int64_t ns = as ? na : nb, nl = as ? nb : na;
@@ -2308,7 +2311,7 @@ void refine_project(Ctx &c, RefineState &st, const DLevel &fine, int32_t coarse_
             r.cin = st.rcin;
             r.len = st.rlen;
             pdl_launch(k_split_counts, 2 * c.num_sms, 256, 0, c.stream, st.splist, st.ctr + CT_SPLIST, fine.inc_off,
-                                                                fine.inc_dat, fine.in_off, fine.in_dat, assign2, r);
+                       fine.inc_e(), fine.inc_dat, fine.in_off, fine.in_e(), fine.in_dat, assign2, r);
             DHGP_LAUNCHED(c);
             std::swap(st.target, st.target2);
             std::swap(st.gain, st.gain2);
@@ -2480,6 +2483,7 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
             if (full) c.zero(ctr, 4);
             ProposeArgs a{N, K, L.inc_off, L.inc_dat, W.wi, r, assign, psizes, L.size, omega,
                           target, gain, ctr, big, ctr + 1, big2, ctr + 2, tiers(), 0, N};
+            a.inc_end = L.inc_e();
             a.fsens = st.fsens;
             a.fpart = st.fpart;
             a.work = work;
@@ -2523,7 +2527,8 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
                 zero_many(c, {{full ? nullptr : (void *)(st.ctr + CT_NLIST), 4}, {dM, 8}});
                 KScope kh(c, "propose_heavy");
                 if (small_k) {
-                    pdl_launch(k_hub_prefix, 1, 1024, 0, c.stream, st.hlist, ctr + 3, st.hub_max, L.inc_off, st.hpref);
+                    pdl_launch(k_hub_prefix, 1, 1024, 0, c.stream, st.hlist, ctr + 3, st.hub_max, L.inc_off, L.inc_e(),
+                               st.hpref);
                     DHGP_LAUNCHED(c);
                     if (narrow) {
                         static int h32 = resident_grid(c, k_propose_hub<unsigned>, 256, 4 * kSmallK);
@@ -2657,7 +2662,7 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
             // inbound events (incremental mode; the full mode scans every h-edge)
             const int32_t *elist = nullptr, *elist_n = nullptr;
             if (st.inc) {
-                pdl_launch(k_mover_edges, g_me, 256, 0, c.stream, dM, node, L.inc_off, L.inc_dat, st.emflag, st.mlist,
+                pdl_launch(k_mover_edges, g_me, 256, 0, c.stream, dM, node, L.inc_off, L.inc_e(), L.inc_dat, st.emflag, st.mlist,
                                                           st.ctr + CT_MLIST, sp);
                 DHGP_LAUNCHED(c);
                 elist = st.mlist;
@@ -2824,7 +2829,7 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
         }
         if (st.inc) {
             // apply + record the dirt; clears the mover-edge flags either way
-            pdl_launch(k_apply_inc, g_ap, 256, 0, c.stream, kbest, node, from, to, L.size, L.inc_off, L.inc_dat, assign,
+            pdl_launch(k_apply_inc, g_ap, 256, 0, c.stream, kbest, node, from, to, L.size, L.inc_off, L.inc_e(), L.inc_dat, assign,
                                                     psizes, st.pflags, st.edirty, st.elist, st.ctr + CT_ELIST,
                                                     st.emflag, st.mlist, st.ctr + CT_MLIST, st.ndirty, st.nlist,
                                                     st.ctr + CT_NLIST);
