@@ -599,7 +599,7 @@ static void run_partition(Ctx &c, const DInput &in, const dhgp_config &cfg, Part
     {
         size_t freeb = 0, total = 0;
         DHGP_CUDA(cudaMemGetInfo(&freeb, &total));
-        keep_budget = (size_t)(0.65 * (double)(freeb + arena_reserved(c.device)));
+        keep_budget = (size_t)(0.80 * (double)(freeb + arena_reserved(c.device)));
         const char *e = getenv("DHGP_KEEP_LEVELS_BYTES");  // tests: force the checkpoint/rebuild path
         if (e) keep_budget = (size_t)strtoull(e, nullptr, 10);
     }
