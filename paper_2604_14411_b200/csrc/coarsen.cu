@@ -384,6 +384,7 @@ __global__ void __launch_bounds__(SM_THREADS) k_score_mid(ScoreArgs a) {
     __shared__ int32_t sover;
     __shared__ long long r_v[SM_THREADS / 32], r_c[SM_THREADS / 32];
     __shared__ int32_t r_k[SM_THREADS / 32], r_s[SM_THREADS / 32];
+    __shared__ long long s_pins;
     constexpr int NW = SM_THREADS / 32;
     const int w = warp_id(), lane = lane_id();
     const int nmid = *a.mid_count;
@@ -399,7 +400,28 @@ __global__ void __launch_bounds__(SM_THREADS) k_score_mid(ScoreArgs a) {
         const int t = s_next;
         if (t >= nmid) break;
         const int32_t node = a.mid_list[t];
-        for (int s = threadIdx.x; s < SM_CAP; s += SM_THREADS) {
+        const int64_t ilo = a.inc_off[node], ihi = a.inc_end[node];
+        {  // table sized to the node (>= twice its pin slots), as in k_score_heavy
+            long long pe = 0;
+            for (int64_t i = ilo + threadIdx.x; i < ihi; i += SM_THREADS) {
+                const int32_t e = a.inc_dat[i];
+                pe += a.pin_off[e + 1] - a.pin_off[e];
+            }
+            pe = warp_sum(pe);
+            if (lane == 0) r_c[w] = pe;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                long long tot = 0;
+                for (int j = 0; j < NW; j++) tot += r_c[j];
+                s_pins = tot;
+            }
+            __syncthreads();
+        }
+        int lg = 12;
+        while (lg > 8 && (1ll << (lg - 1)) >= 2 * s_pins) lg--;
+        const int cap = 1 << lg;
+        const int limit = min(a.t.sm_limit, cap - (cap >> 2));
+        for (int s = threadIdx.x; s < cap; s += SM_THREADS) {
             keys[s] = -1;
             vals[s] = 0;
         }
@@ -408,20 +430,19 @@ __global__ void __launch_bounds__(SM_THREADS) k_score_mid(ScoreArgs a) {
             sover = 0;
         }
         __syncthreads();
-        const int64_t ilo = a.inc_off[node], ihi = a.inc_end[node];
         const int bsz = (int)max((int64_t)1, min((int64_t)32, (ihi - ilo + NW - 1) / NW));
         warp_for_pins<4>(a.inc_dat, ilo, ihi, (int64_t)w * bsz, (int64_t)NW * bsz, a.pin_off, a.pin_dat,
                          [&](int32_t e, int32_t m) {
                              if (m == node || flag_get(&sover)) return;
                              const Acc we = (Acc)a.wi[e];
-                             uint32_t h = ((uint32_t)m * 2654435761u) >> (32 - 12);
-                             for (int probe = 0; probe < SM_CAP; probe++) {
-                                 const int slot = (h + probe) & (SM_CAP - 1);
+                             uint32_t h = ((uint32_t)m * 2654435761u) >> (32 - lg);
+                             for (int probe = 0; probe < cap; probe++) {
+                                 const int slot = (h + probe) & (cap - 1);
                                  int k = keys[slot];
                                  if (k == -1) {
                                      const int prev = atomicCAS(&keys[slot], -1, m);
                                      if (prev == -1) {
-                                         if (atomicAdd(&snk, 1) + 1 > a.t.sm_limit) flag_set(&sover);
+                                         if (atomicAdd(&snk, 1) + 1 > limit) flag_set(&sover);
                                          k = m;
                                      } else {
                                          k = prev;
@@ -441,14 +462,14 @@ __global__ void __launch_bounds__(SM_THREADS) k_score_mid(ScoreArgs a) {
             __syncthreads();
             continue;
         }
-        filter_emit<8>(a, node, keys, vals, threadIdx.x, SM_THREADS, SM_CAP);
+        filter_emit<8>(a, node, keys, vals, threadIdx.x, SM_THREADS, cap);
         __syncthreads();
         int32_t best_m = -1;
         long long best_v = 0;
         while (true) {
             long long bv = -1;
             int32_t bk = -1, bs = -1;
-            for (int s = threadIdx.x; s < SM_CAP; s += SM_THREADS) {
+            for (int s = threadIdx.x; s < cap; s += SM_THREADS) {
                 const int k = keys[s];
                 if (k >= 0) {
                     const long long v = (long long)vals[s];
@@ -547,6 +568,7 @@ __global__ void __launch_bounds__(SH_THREADS) k_score_heavy(ScoreArgs a, int pai
     __shared__ long long r_v[SH_THREADS / 32];
     __shared__ int32_t r_k[SH_THREADS / 32], r_s[SH_THREADS / 32];
     __shared__ long long r_c[SH_THREADS / 32];
+    __shared__ long long s_pins;
     static_assert(SH_THREADS == 1024, "the winner reduction reads one entry per lane");
     static_assert(CL == 1 || CL == 2, "one CTA or a CTA pair per node");
     const int w = warp_id(), lane = lane_id(), nw = SH_THREADS / 32;
@@ -556,7 +578,31 @@ __global__ void __launch_bounds__(SH_THREADS) k_score_heavy(ScoreArgs a, int pai
     if constexpr (CL == 2) rank = (int)cooperative_groups::this_cluster().block_rank();
     for (int t = (int)blockIdx.x / CL; t < nheavy; t += gridDim.x / CL) {
         const int32_t node = a.heavy_list[t];
-        for (int s = threadIdx.x; s < SH_CAP; s += SH_THREADS) {
+        const int64_t ilo = a.inc_off[node], ihi = a.inc_end[node];
+        // table sized to the node: at least twice its pin slots (its distinct
+        // neighbours are fewer), so the clear / filter / argmax scans cost
+        // what the node needs rather than the full 16K slots
+        {
+            long long pe = 0;
+            for (int64_t i = ilo + threadIdx.x; i < ihi; i += SH_THREADS) {
+                const int32_t e = a.inc_dat[i];
+                pe += a.pin_off[e + 1] - a.pin_off[e];
+            }
+            pe = warp_sum(pe);
+            if (lane == 0) r_c[w] = pe;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                long long tot = 0;
+                for (int j = 0; j < nw; j++) tot += r_c[j];
+                s_pins = tot;
+            }
+            __syncthreads();
+        }
+        int lg = 14;
+        while (lg > 10 && (1ll << (lg - 1)) >= 2 * s_pins) lg--;
+        const int cap = 1 << lg;
+        const int limit = min(a.t.sh_limit, cap - (cap >> 2));
+        for (int s = threadIdx.x; s < cap; s += SH_THREADS) {
             keys[s] = -1;
             vals[s] = 0;
         }
@@ -565,7 +611,6 @@ __global__ void __launch_bounds__(SH_THREADS) k_score_heavy(ScoreArgs a, int pai
             sover = 0;
         }
         __syncthreads();
-        const int64_t ilo = a.inc_off[node], ihi = a.inc_end[node];
         int pend = 0;  // this thread's new keys not yet added to snk
         // h-edges per warp batch: a node's h-edges spread over all warps
         // (of both CTAs of a pair)
@@ -575,9 +620,9 @@ __global__ void __launch_bounds__(SH_THREADS) k_score_heavy(ScoreArgs a, int pai
                       [&](int32_t e, int32_t m) {
                           if (m == node || flag_get(&sover)) return;
                           const Acc we = (Acc)a.wi[e];
-                          uint32_t h = ((uint32_t)m * 2654435761u) >> (32 - 14);
-                          for (int probe = 0; probe < SH_CAP; probe++) {
-                              const int slot = (h + probe) & (SH_CAP - 1);
+                          uint32_t h = ((uint32_t)m * 2654435761u) >> (32 - lg);
+                          for (int probe = 0; probe < cap; probe++) {
+                              const int slot = (h + probe) & (cap - 1);
                               int k = keys[slot];
                               if (k == -1) {
                                   int prev = atomicCAS(&keys[slot], -1, m);
@@ -587,7 +632,7 @@ __global__ void __launch_bounds__(SH_THREADS) k_score_heavy(ScoreArgs a, int pai
                                       // the tier, never the result)
                                       if (++pend == 2) {
                                           pend = 0;
-                                          if (atomicAdd(&snk, 2) + 2 > a.t.sh_limit) flag_set(&sover);
+                                          if (atomicAdd(&snk, 2) + 2 > limit) flag_set(&sover);
                                       }
                                       k = m;
                                   } else {
@@ -614,19 +659,19 @@ __global__ void __launch_bounds__(SH_THREADS) k_score_heavy(ScoreArgs a, int pai
                 if (sover) {
                     if (threadIdx.x == 0) atomicExch(sover0, 1);
                 } else {
-                    for (int s = threadIdx.x; s < SH_CAP; s += SH_THREADS) {
+                    for (int s = threadIdx.x; s < cap; s += SH_THREADS) {
                         const int32_t m = keys[s];
                         if (m < 0 || atomicAdd(sover0, 0)) continue;
                         const Acc v = vals[s];
-                        const uint32_t h = ((uint32_t)m * 2654435761u) >> (32 - 14);
+                        const uint32_t h = ((uint32_t)m * 2654435761u) >> (32 - lg);
                         bool done = false;
-                        for (int probe = 0; probe < SH_CAP && !done; probe++) {
-                            const int slot = (h + probe) & (SH_CAP - 1);
+                        for (int probe = 0; probe < cap && !done; probe++) {
+                            const int slot = (h + probe) & (cap - 1);
                             int k = ((volatile int32_t *)keys0)[slot];
                             if (k == -1) {
                                 const int prev = atomicCAS(&keys0[slot], -1, m);
                                 if (prev == -1) {
-                                    if (atomicAdd(snk0, 1) + 1 > a.t.sh_limit) atomicExch(sover0, 1);
+                                    if (atomicAdd(snk0, 1) + 1 > limit) atomicExch(sover0, 1);
                                     k = m;
                                 } else {
                                     k = prev;
@@ -649,7 +694,7 @@ __global__ void __launch_bounds__(SH_THREADS) k_score_heavy(ScoreArgs a, int pai
             __syncthreads();
             continue;
         }
-        filter_emit<4>(a, node, keys, vals, threadIdx.x, SH_THREADS, SH_CAP);
+        filter_emit<4>(a, node, keys, vals, threadIdx.x, SH_THREADS, cap);
         __syncthreads();
         int32_t best_m = -1;
         long long best_v = 0;
@@ -658,7 +703,7 @@ __global__ void __launch_bounds__(SH_THREADS) k_score_heavy(ScoreArgs a, int pai
             iters++;
             long long bv = -1;
             int32_t bk = -1, bs = -1;
-            for (int s = threadIdx.x; s < SH_CAP; s += SH_THREADS) {
+            for (int s = threadIdx.x; s < cap; s += SH_THREADS) {
                 int k = keys[s];
                 if (k >= 0) {
                     long long v = (long long)vals[s];
@@ -1637,7 +1682,7 @@ __global__ void __launch_bounds__(UN_THREADS) k_node_union(const int32_t *ma, co
         const bool a_short = na <= nb;
         const int32_t *S = f.dat + (a_short ? alo : blo), *L = f.dat + (a_short ? blo : alo);
         const int64_t ns = a_short ? na : nb, nl = a_short ? nb : na;
-        if (words > 0 && 8 * (na + nb) >= words) {
+        if (words > 0 && na + nb >= 2 * (int64_t)words) {  // the bitmap's clear + scan pays off
             for (int w = threadIdx.x; w < words; w += blockDim.x) s_bm[w] = 0u;
             __syncthreads();
             for (int64_t i = threadIdx.x; i < na; i += blockDim.x) {
