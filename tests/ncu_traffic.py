@@ -22,7 +22,7 @@ CLASSES = {
                                    "k_propose_mid", "k_propose_block"}),
     "contract": ("k_gamma", {"k_gamma", "k_node_count", "k_node_union_warp@count", "k_node_union@count",
                              "k_edge_count_bulk", "k_marked_list", "k_contract_edges@count", "k_contract_status"}),
-    "contract_write": ("k_node_write", {"k_contract_edges@write", "k_map_gaps", "k_node_write",
+    "contract_write": ("k_node_union_warp@write", {"k_contract_edges@write", "k_map_gaps", "k_node_write",
                                         "k_node_union_warp@write", "k_node_union@write"}),
     "seq_gains": ("k_round_moves", {"k_round_edges", "k_seq_gains_edge_block", "k_inbound_events_block",
                                     "k_edge_movers_huge", "k_round_moves"}),
@@ -47,7 +47,7 @@ def per_unit(paths):
             m = per[i]
             b = m.get("dram__bytes_read.sum", 0.0) + m.get("dram__bytes_write.sum", 0.0)
             for cls, (unit, members) in CLASSES.items():
-                if n == unit:
+                if key == unit:
                     units[cls] += 1
                 if key in members:
                     dram[cls] += b
