@@ -281,10 +281,11 @@ __global__ void __launch_bounds__(SS_WARPS * 32, 3) k_score_warp(ScoreArgs a) {
         }
         __syncwarp();
         warp_for_pins(a.inc_dat, ilo, ihi, 0, 32, a.pin_off, a.pin_dat, [&](int32_t e, int32_t m) {
-            if (m == node || flag_get(&sover[w])) return;
+            if (m == node) return;
             const Acc we = (Acc)a.wi[e];
             uint32_t h = hslot(m);
             for (int probe = 0; probe < SS_CAP; probe++) {
+                if (probe % kFlagPoll == kFlagPoll - 1 && flag_get(&sover[w])) return;
                 const int slot = (h + probe) & (SS_CAP - 1);
                 int k = keys[slot];
                 if (k == -1) {
@@ -433,10 +434,11 @@ __global__ void __launch_bounds__(SM_THREADS) k_score_mid(ScoreArgs a) {
         const int bsz = (int)max((int64_t)1, min((int64_t)32, (ihi - ilo + NW - 1) / NW));
         warp_for_pins<4>(a.inc_dat, ilo, ihi, (int64_t)w * bsz, (int64_t)NW * bsz, a.pin_off, a.pin_dat,
                          [&](int32_t e, int32_t m) {
-                             if (m == node || flag_get(&sover)) return;
+                             if (m == node) return;
                              const Acc we = (Acc)a.wi[e];
                              uint32_t h = ((uint32_t)m * 2654435761u) >> (32 - lg);
                              for (int probe = 0; probe < cap; probe++) {
+                                 if (probe % kFlagPoll == kFlagPoll - 1 && flag_get(&sover)) return;
                                  const int slot = (h + probe) & (cap - 1);
                                  int k = keys[slot];
                                  if (k == -1) {
@@ -618,10 +620,11 @@ __global__ void __launch_bounds__(SH_THREADS) k_score_heavy(ScoreArgs a, int pai
         warp_for_pins<4>(a.inc_dat, ilo, ihi, (int64_t)(rank * nw + w) * bsz, (int64_t)CL * nw * bsz, a.pin_off,
                          a.pin_dat,
                       [&](int32_t e, int32_t m) {
-                          if (m == node || flag_get(&sover)) return;
+                          if (m == node) return;
                           const Acc we = (Acc)a.wi[e];
                           uint32_t h = ((uint32_t)m * 2654435761u) >> (32 - lg);
                           for (int probe = 0; probe < cap; probe++) {
+                              if (probe % kFlagPoll == kFlagPoll - 1 && flag_get(&sover)) return;
                               const int slot = (h + probe) & (cap - 1);
                               int k = keys[slot];
                               if (k == -1) {

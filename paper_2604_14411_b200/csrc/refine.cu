@@ -476,9 +476,9 @@ __global__ void __launch_bounds__(PR_WARPS * 32, 4) k_propose_warp(ProposeArgs a
         int64_t total = 0, saving = 0;
         total = warp_for_runs(a.inc_dat, ilo, ihi, 0, 32, 32, a.r.off, a.r.len, a.wi, a.work, a.r.pc, [&](int32_t, int64_t we, int32_t p, int32_t pc) {
             if (p == ps && pc == 1) saving += we;
-            if (flag_get(&sover[w])) return;
             const uint32_t h = pslot(p);
             for (int probe = 0; probe < PR_CAP; probe++) {
+                if (probe % kFlagPoll == kFlagPoll - 1 && flag_get(&sover[w])) return;
                 const int slot = (h + probe) & (PR_CAP - 1);
                 int kk = keys[slot];
                 if (kk == -1) {
@@ -628,9 +628,9 @@ __global__ void __launch_bounds__(PM_THREADS, 4) k_propose_mid(ProposeArgs a) {
                               a.r.pc,
                               [&](int32_t, int64_t we, int32_t p, int32_t pc) {
                                   if (p == ps && pc == 1) saving += we;
-                                  if (flag_get(&sover)) return;
                                   const uint32_t h = ((uint32_t)p * 2654435761u) >> (32 - lg);
                                   for (int probe = 0; probe < cap; probe++) {
+                                      if (probe % kFlagPoll == kFlagPoll - 1 && flag_get(&sover)) return;
                                       const int slot = (h + probe) & (cap - 1);
                                       int kk = keys[slot];
                                       if (kk == -1) {
