@@ -1162,7 +1162,8 @@ void score_select(Ctx &c, const DLevel &L, const DWeights &W, int64_t omega, int
 }
 
 bool score_inc_supported(const Ctx &c, const DWeights &W) {
-    return !shard_of(c.comm, 1).on && W.wsum < (1ll << 31) - 2;
+    (void)c;
+    return W.wsum < (1ll << 31) - 2;
 }
 
 void score_select_inc(Ctx &c, const DLevel &L, const DWeights &W, int64_t omega, int64_t delta, int32_t *pair,
@@ -1198,6 +1199,12 @@ void score_select_inc(Ctx &c, const DLevel &L, const DWeights &W, int64_t omega,
     a.tup_count = lc + 2;
     a.tup_cap = cap;
     a.heavy_small_list = 2 * c.num_sms;
+    // node-range sharding (comm.cuh): each rank rescores the merged clusters
+    // and rescore-listed nodes of its range; the per-node best tuple keys are
+    // max-reduced across ranks and (pair, score) allgathered at the end
+    const Shard sh = shard_of(c.comm, N);
+    a.lo = (int32_t)sh.lo;
+    a.hi = (int32_t)sh.hi;
     unsigned long long *probe = nullptr;
     if (trace_enabled()) {
         probe = c.alloc<unsigned long long>(4);
@@ -1219,6 +1226,10 @@ void score_select_inc(Ctx &c, const DLevel &L, const DWeights &W, int64_t omega,
     pdl_launch(k_inc_tuples, gt, 256, 0, c.stream, a, best, hard, lc + 3);
     DHGP_LAUNCHED(c);
     kt.close();
+    if (sh.on) {  // tuples of every rank's clusters; a tuple overflow anywhere rescores everywhere
+        allreduce_max_u64(c, c.comm, best, N);
+        allreduce_sum_i32(c, c.comm, lc + 2, 1);
+    }
     pdl_launch(k_inc_finalize, (unsigned)cdiv(N, 256), 256, 0, c.stream, N, kind, thr_s, thr_p, best, cy.gamma_prev, lc + 2,
                                                                 cap, pair, score, list2, lc + 1);
     DHGP_LAUNCHED(c);
@@ -1229,7 +1240,13 @@ void score_select_inc(Ctx &c, const DLevel &L, const DWeights &W, int64_t omega,
     b.list_count = lc + 1;
     b.work = work;
     b.probe = probe;
+    b.lo = (int32_t)sh.lo;
+    b.hi = (int32_t)sh.hi;
     score_tiers(c, b, W, s, N);
+    if (sh.on) {  // every node's (pair, score) from the rank owning it
+        allgather(c, c.comm, pair, sizeof(int32_t), sh.chunk);
+        allgather(c, c.comm, score, sizeof(double), sh.chunk);
+    }
     if (work) {  // measured algorithmic bytes: lists read by both passes, the per-node
                  // carry (pair, score, gamma, members: 24 B) and the tuples (16 B each)
         ks.stop();

@@ -106,6 +106,38 @@ void allgather(Ctx &c, Comm *cm, void *buf, size_t elem, int64_t chunk) {
     DHGP_CUDA(cudaMemcpyAsync(buf, h, total, cudaMemcpyHostToDevice, c.stream));
 }
 
+namespace {
+template <class T, bool MAX>
+__global__ void k_reduce_ranks(int64_t n, int world, const T *parts, T *out) {
+    pdl_entry();
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        T v = parts[i];
+        for (int r = 1; r < world; r++) {
+            const T x = parts[(int64_t)r * n + i];
+            v = MAX ? (x > v ? x : v) : (T)(v + x);
+        }
+        out[i] = v;
+    }
+}
+template <class T, bool MAX>
+void allreduce(Ctx &c, Comm *cm, T *buf, int64_t n) {
+    if (!comm_active(cm) || n <= 0) return;
+    T *parts = c.alloc<T>((int64_t)cm->world * n);
+    c.d2d(parts + (int64_t)cm->rank * n, buf, n);
+    allgather(c, cm, parts, sizeof(T), n);
+    pdl_launch(k_reduce_ranks<T, MAX>, (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), 4096)), 256, 0,
+               c.stream, n, cm->world, (const T *)parts, buf);
+    DHGP_LAUNCHED(c);
+    c.free(parts);
+}
+}  // namespace
+
+void allreduce_max_u64(Ctx &c, Comm *cm, unsigned long long *buf, int64_t n) {
+    allreduce<unsigned long long, true>(c, cm, buf, n);
+}
+void allreduce_sum_i64(Ctx &c, Comm *cm, long long *buf, int64_t n) { allreduce<long long, false>(c, cm, buf, n); }
+void allreduce_sum_i32(Ctx &c, Comm *cm, int32_t *buf, int64_t n) { allreduce<int32_t, false>(c, cm, buf, n); }
+
 }  // namespace dhgp
 
 // ===========================================================================

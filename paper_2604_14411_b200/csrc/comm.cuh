@@ -42,4 +42,15 @@ int64_t shard_capacity(const Comm *cm, int64_t n);
 // NCCL; the host mode synchronises and calls the user's allgather.
 void allgather(Ctx &c, Comm *cm, void *buf, size_t elem, int64_t chunk);
 
+// Element-wise reduction across ranks of buf[0..n) (every rank ends with the
+// result), as an allgather of every rank's whole array followed by an on-device
+// reduction in rank order (exact: integer max / sum).  Used for the phases whose
+// per-rank outputs overlap: the incremental scoring's per-node best tuple key
+// (max) and the in-sequence gain / inbound-crossing terms of each move (sum).
+void allreduce_max_u64(Ctx &c, Comm *cm, unsigned long long *buf, int64_t n);
+void allreduce_sum_i64(Ctx &c, Comm *cm, long long *buf, int64_t n);
+void allreduce_sum_i32(Ctx &c, Comm *cm, int32_t *buf, int64_t n);
+// is the communicator live (world > 1, or exercised at world 1)?
+inline bool comm_active(const Comm *cm) { return cm && (cm->world > 1 || cm->exercise); }
+
 }  // namespace dhgp

@@ -1735,7 +1735,8 @@ __global__ void __launch_bounds__(256) k_round_edges(int32_t E, const int32_t *e
                                                      const int32_t *from, const int32_t *to,
                                                      unsigned long long *gacc, EvArgs ev, int32_t *sg_big,
                                                      int32_t *sg_count, int32_t *ev_big, int32_t *ev_count,
-                                                     int cap, const int64_t *spec_m, unsigned long long *work) {
+                                                     int cap, const int64_t *spec_m, unsigned long long *work,
+                                                     int64_t elo, int64_t ehi) {
     pdl_entry();
     if (spec_m && *spec_m > kSpecCap) return;  // speculative launch, M too large
     __shared__ int32_t s_mv[8][32];
@@ -1745,6 +1746,7 @@ __global__ void __launch_bounds__(256) k_round_edges(int32_t E, const int32_t *e
     const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
     for (int64_t idx = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id(); idx < ne; idx += nw) {
         const int32_t e = elist ? elist[idx] : (int32_t)idx;
+        if (e < elo || e >= ehi) continue;  // another rank's h-edge (node-range sharding by h-edge id)
         // algorithmic bytes (profiling): pins and destination pins with their
         // positions (8 B each), offsets / runs / weight (48 B)
         if (work && lane == 0)
@@ -2678,13 +2680,17 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
                 unsigned long long *gacc = (unsigned long long *)gseq_acc;
                 zero_many(c,
                           {{gacc, 8 * Mc}, {sg_ctr, 16}, {ctr, 16}, {ev_from, 4 * Mc}, {ev_to, 4 * Mc}, {ecount, 8}});
+                // sharding: each rank takes the mover h-edges of its h-edge id
+                // range; a move's terms are then summed across ranks
+                const Shard esh = shard_of(c.comm, L.E);
                 if (L.E > 0) {
                     static int g_re = resident_grid(c, k_round_edges, 256, 0);
                     const unsigned gre = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(L.E, 8), g_re));
                     pdl_launch(k_round_edges, gre, 256, 0, c.stream, L.E, elist, elist_n, L.pin_off, L.pin_dat, L.dst_off,
                                                              L.dst_dat, W.wi, r, pos, from, to, gacc, ev, sg_big,
                                                              sg_ctr, big, ctr, tiers().edge_movers,
-                                                             sp ? dM : nullptr, c.work_slot(Ctx::PW_SEQ_GAINS));
+                                                             sp ? dM : nullptr, c.work_slot(Ctx::PW_SEQ_GAINS),
+                                                             esh.lo, esh.hi);
                     DHGP_LAUNCHED(c);
                     pdl_launch(k_seq_gains_edge_block, c.num_sms, 256, 0, c.stream, L.pin_off, L.pin_dat, W.wi, r, pos, from,
                                                                              to, gacc, sg_big, sg_ctr, hv_sg, sg_ctr + 2,
@@ -2701,6 +2707,11 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
                                    pos, from, to, gacc, ev, hv_ev, sg_ctr + 3, mv_scr, (int64_t)max_edge_pins);
                         DHGP_LAUNCHED(c);
                     }
+                }
+                if (esh.on) {
+                    allreduce_sum_i64(c, c.comm, (long long *)gacc, Mc);
+                    allreduce_sum_i32(c, c.comm, ev_from, Mc);
+                    allreduce_sum_i32(c, c.comm, ev_to, Mc);
                 }
                 pdl_launch(k_round_moves, (unsigned)std::max<int64_t>(1, cdiv(Mc, 256)), 256, 0, c.stream, 
                     dM, node, from, to, L.size, ev, giso, gacc, gseq, sp);

@@ -135,7 +135,17 @@ def _instances():
     return out
 
 
-def _sharded_worker(rank, world, port, q):
+def _large_instances():
+    """Above the default min_units (65,536 nodes / h-edges): the sharded
+    phases run with the library's default threshold."""
+    import paper_2604_14411_b200 as dp
+    from paper_2604_14411_b200 import workloads as W
+
+    n, w, so, sd, do, dd = W.layered_snn(70, 1000, seed=5)
+    return [(dp.Hypergraph._from_csr(n, w, dp.CsrSets(so, sd), dp.CsrSets(do, dd)), 1024, 4096)]
+
+
+def _sharded_worker(rank, world, port, q, default_min_units=False):
     try:
         import sys
         from pathlib import Path
@@ -146,9 +156,10 @@ def _sharded_worker(rank, world, port, q):
         from paper_2604_14411_b200 import distributed as dd
 
         cm = dd.Communicator.host()
-        cm.set_min_units(0)  # shard every level and every round
+        if not default_min_units:
+            cm.set_min_units(0)  # shard every level and every round
         out = []
-        for g, om, de in _instances():
+        for g, om, de in (_large_instances() if default_min_units else _instances()):
             part, st = dd.partition(g, dp.Config(dp.Constraints(om, de), max_levels=1 << 20), cm)
             out.append((part.assign.tobytes(), part.num_parts, st.levels, st.connectivity_trace))
         q.put((rank, out, cm.stats()["allgathers"]))
@@ -160,8 +171,13 @@ def _sharded_worker(rank, world, port, q):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world", [2, 3])
-def test_sharded_partition_is_bit_identical(world):
+@pytest.mark.parametrize("world,default_min_units", [(2, False), (3, False), (2, True)])
+def test_sharded_partition_is_bit_identical(world, default_min_units):
+    """Node-range sharding (full and incremental scoring, proposals, the
+    in-sequence gain / inbound terms by h-edge range) over world 2/3 ranks on
+    one GPU with the host (gloo) allgather: every rank's result equals the
+    single-GPU one.  min_units 0 shards every level and round; the default
+    threshold (65,536) shards the 70k-node instance's large phases."""
     import sys
     from pathlib import Path
 
@@ -169,13 +185,13 @@ def test_sharded_partition_is_bit_identical(world):
     import paper_2604_14411_b200 as dp
 
     ref = []
-    for g, om, de in _instances():
+    for g, om, de in (_large_instances() if default_min_units else _instances()):
         part, st = dp.partition(g, dp.Config(dp.Constraints(om, de), max_levels=1 << 20))
         ref.append((part.assign.tobytes(), part.num_parts, st.levels, st.connectivity_trace))
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    ps = [ctx.Process(target=_sharded_worker, args=(r, world, port, q)) for r in range(world)]
+    ps = [ctx.Process(target=_sharded_worker, args=(r, world, port, q, default_min_units)) for r in range(world)]
     for p in ps:
         p.start()
     res = sorted((q.get(timeout=600) for _ in range(world)), key=lambda x: x[0])
