@@ -1,6 +1,8 @@
 // prims.cu — scans, radix sort, per-segment sorts, sorted-set merges.
 #include <climits>
 
+#include <cmath>
+
 #include "prims.cuh"
 
 namespace dhgp {
@@ -486,6 +488,105 @@ void small_sort_packed(Ctx &c, uint64_t *keys, uint32_t *vals, int64_t n, const 
     }
     pdl_launch(k_small_sort_packed, 1, 1024, 2 * kSmallSort * sizeof(uint64_t), c.stream, keys, vals, (int)n, dn);
     DHGP_LAUNCHED(c);
+}
+
+// ===========================================================================
+// merge sort of (key, val) pairs by (key, val) for mid-size arrays: chunks of
+// MS_CHUNK sorted in shared memory (one CTA each, bitonic), then merge passes
+// that double the run width (merge path: each thread finds its co-rank once
+// and emits MS_PER consecutive outputs).  A handful of launches instead of
+// three per 8-bit radix pass.
+// ===========================================================================
+namespace {
+constexpr int MS_CHUNK = 2048, MS_THREADS = 1024, MS_PER = 8;
+__device__ __forceinline__ bool pair_less(uint64_t ka, uint32_t va, uint64_t kb, uint32_t vb) {
+    return ka < kb || (ka == kb && va < vb);
+}
+__global__ void __launch_bounds__(MS_THREADS) k_chunk_sort(uint64_t *keys, uint32_t *vals, int64_t n) {
+    pdl_entry();
+    __shared__ uint64_t sk[MS_CHUNK];
+    __shared__ uint32_t sv[MS_CHUNK];
+    const int64_t base = (int64_t)blockIdx.x * MS_CHUNK;
+    const int m = (int)min((int64_t)MS_CHUNK, n - base);
+    for (int i = threadIdx.x; i < MS_CHUNK; i += MS_THREADS) {
+        sk[i] = i < m ? keys[base + i] : ~0ull;
+        sv[i] = i < m ? vals[base + i] : 0xffffffffu;
+    }
+    for (int size = 2; size <= MS_CHUNK; size <<= 1) {
+        for (int j = size >> 1; j > 0; j >>= 1) {
+            __syncthreads();
+            for (int t = threadIdx.x; t < MS_CHUNK / 2; t += MS_THREADS) {
+                const int lo = 2 * j * (t / j) + (t % j), hi = lo + j;
+                const bool asc = (lo & size) == 0;
+                const uint64_t a = sk[lo], b = sk[hi];
+                const uint32_t va = sv[lo], vb = sv[hi];
+                if (pair_less(b, vb, a, va) == asc) {
+                    sk[lo] = b;
+                    sk[hi] = a;
+                    sv[lo] = vb;
+                    sv[hi] = va;
+                }
+            }
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < m; i += MS_THREADS) {
+        keys[base + i] = sk[i];
+        vals[base + i] = sv[i];
+    }
+}
+// merge of the sorted runs [r0, r0 + w) and [r0 + w, r0 + 2w) (clipped to n)
+__global__ void k_merge_pass(const uint64_t *ki, const uint32_t *vi, uint64_t *ko, uint32_t *vo, int64_t n,
+                             int64_t w) {
+    pdl_entry();
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t o = t * MS_PER;
+    if (o >= n) return;
+    const int64_t r0 = (o / (2 * w)) * (2 * w);
+    const int64_t a0 = r0, a1 = min(n, r0 + w), b0 = a1, b1 = min(n, r0 + 2 * w);
+    const int64_t na = a1 - a0, nb = b1 - b0, k = o - r0;  // output rank within the merged run
+    // co-rank: i elements from A, k - i from B, with A[i-1] <= B[k-i] and B[k-i-1] < A[i]
+    int64_t lo = max((int64_t)0, k - nb), hi = min(k, na);
+    while (lo < hi) {
+        const int64_t i = (lo + hi) >> 1;  // take i from A: is A[i] <= B[k-i-1]? then more from A
+        if (!pair_less(ki[b0 + k - i - 1], vi[b0 + k - i - 1], ki[a0 + i], vi[a0 + i])) lo = i + 1;
+        else hi = i;
+    }
+    int64_t i = lo, j = k - lo;
+    const int64_t end = min(n, o + MS_PER);
+    for (int64_t q = o; q < end; q++) {
+        const bool takeA = j >= nb || (i < na && !pair_less(ki[b0 + j], vi[b0 + j], ki[a0 + i], vi[a0 + i]));
+        if (takeA) {
+            ko[q] = ki[a0 + i];
+            vo[q] = vi[a0 + i];
+            i++;
+        } else {
+            ko[q] = ki[b0 + j];
+            vo[q] = vi[b0 + j];
+            j++;
+        }
+    }
+}
+}  // namespace
+
+void merge_sort_pairs(Ctx &c, uint64_t *keys, uint32_t *vals, uint64_t *ktmp, uint32_t *vtmp, int64_t n) {
+    if (n <= 1) return;
+    KScope ks(c, "radix_sort", 24.0 * (double)n * (1.0 + std::max(0.0, std::ceil(std::log2((double)n / MS_CHUNK)))));
+    pdl_launch(k_chunk_sort, (unsigned)cdiv(n, MS_CHUNK), MS_THREADS, 0, c.stream, keys, vals, n);
+    DHGP_LAUNCHED(c);
+    uint64_t *ka = keys, *kb = ktmp;
+    uint32_t *va = vals, *vb = vtmp;
+    for (int64_t w = MS_CHUNK; w < n; w *= 2) {
+        pdl_launch(k_merge_pass, (unsigned)cdiv(cdiv(n, MS_PER), 256), 256, 0, c.stream, (const uint64_t *)ka,
+                   (const uint32_t *)va, kb, vb, n, w);
+        DHGP_LAUNCHED(c);
+        std::swap(ka, kb);
+        std::swap(va, vb);
+    }
+    if (ka != keys) {
+        c.d2d(keys, ka, n);
+        c.d2d(vals, va, n);
+    }
 }
 
 void radix_sort_pairs(Ctx &c, uint64_t *keys, uint32_t *vals, uint64_t *ktmp, uint32_t *vtmp, int64_t n_cap,

@@ -25,6 +25,12 @@ void scan_incl_max(Ctx &c, const int64_t *in, int64_t *out, int64_t n);
 void radix_sort_pairs(Ctx &c, uint64_t *keys, uint32_t *vals, uint64_t *ktmp, uint32_t *vtmp, int64_t n_cap,
                       const int64_t *d_n, int bits);
 
+// Sort of (key, val) pairs by (key, val) (for distinct vals ascending in the
+// input this is the stable key order): CTA chunk sorts + merge-path passes,
+// for the mid-size sorts of the refinement rounds (n up to ~1M).
+void merge_sort_pairs(Ctx &c, uint64_t *keys, uint32_t *vals, uint64_t *ktmp, uint32_t *vtmp, int64_t n);
+constexpr int64_t kMergeSortMax = 1 << 20;
+
 // Single-CTA sort of (key, val) pairs by (key, val) for n <= kSmallSort
 // (one launch; not stable in general, stable when vals ascend in input order
 // and are distinct).

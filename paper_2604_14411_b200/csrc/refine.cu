@@ -2645,7 +2645,8 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
                 else if (Mh <= kSmallSort)
                     small_sort_packed(c, mk, mv, Mh);
                 else
-                    radix_sort_pairs(c, mk, mv, mkt, mvt, Mh, nullptr, gmax_bits + 32);
+                    (Mh <= kMergeSortMax) ? merge_sort_pairs(c, mk, mv, mkt, mvt, Mh)
+                                          : radix_sort_pairs(c, mk, mv, mkt, mvt, Mh, nullptr, gmax_bits + 32);
             } else {
                 if (N > 0) {
                     pdl_launch(k_mover_keys, (unsigned)cdiv(N, 256), 256, 0, c.stream, N, flags, mpos, gain, W.wsum, mk, mv);
@@ -2654,7 +2655,8 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
                 if (Mh <= kSmallSort)
                     small_sort_pairs(c, mk, mv, Mh);  // vals (nodes) are distinct and ascend: stable
                 else
-                    radix_sort_pairs(c, mk, mv, mkt, mvt, Mh, nullptr, gmax_bits);
+                    (Mh <= kMergeSortMax) ? merge_sort_pairs(c, mk, mv, mkt, mvt, Mh)
+                                          : radix_sort_pairs(c, mk, mv, mkt, mvt, Mh, nullptr, gmax_bits);
                 fill_i32(c, pos, -1, N);
             }
             pdl_launch(k_build_moves_dn, (unsigned)std::max<int64_t>(1, cdiv(Mc, 256)), 256, 0, c.stream, 
@@ -2775,7 +2777,9 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
                 if ((int64_t)T <= kSmallSort)
                     small_sort_pairs(c, ek, evv, (int64_t)T);  // equal keys only need grouping
                 else
-                    radix_sort_pairs(c, ek, evv, ekt, evt, (int64_t)T, nullptr, 1 + ibits + pbits);
+                    ((int64_t)T <= kMergeSortMax)
+                        ? merge_sort_pairs(c, ek, evv, ekt, evt, (int64_t)T)
+                        : radix_sort_pairs(c, ek, evv, ekt, evt, (int64_t)T, nullptr, 1 + ibits + pbits);
                 int64_t *gs = c.alloc<int64_t>(T), *ss = c.alloc<int64_t>(T), *dv = c.alloc<int64_t>(T);
                 int64_t *ex = c.alloc<int64_t>(T + 1), *gst = c.alloc<int64_t>(T), *sst = c.alloc<int64_t>(T);
                 c.zero(dlt, M + 1);
