@@ -279,7 +279,7 @@ struct Tiers {
     int pm_limit = 3072;      // propose: distinct parts per medium-tier table
     int small_k = 4096;       // propose: K up to which escalated nodes use dense shared arrays
     int pr_hub_inc = 128;     // propose: incident h-edges above which a node is split over many CTAs
-    int edge_movers = 32;     // events / sequence gains: movers per h-edge for the thread tier (<= 32)
+    int edge_movers = 64;     // events / sequence gains: movers per h-edge for the warp tier (<= 64; 2 per lane above 32)
     int seg_smem = 8192;      // per-segment sorts / wide run updates: longest list kept in shared memory
     int mv_block = 2048;      // events / sequence gains: movers per h-edge for the shared-memory block tier
     int speculate = 1;        // refinement: launch a round's tail before its mover count is on the host

@@ -47,7 +47,7 @@ const Tiers &tiers() {
             x.pr_heavy_inc = 1;
             x.pr_hub_inc = 6;
             x.pm_limit = 3;
-            x.edge_movers = 2;
+            x.edge_movers = e[0] == '1' ? 2 : 40;  // =2: the 33-64 two-per-lane tier up to 40, block above
             x.seg_smem = 48;
             x.mv_block = 6;
             x.speculate = 0;

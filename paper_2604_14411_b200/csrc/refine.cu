@@ -1672,7 +1672,7 @@ __device__ __forceinline__ int warp_collect_movers(const int32_t *dat, int64_t l
         const uint32_t bal = __ballot_sync(FULL_MASK, j >= 0);
         if (j >= 0) {
             const int slot = nm + __popc(bal & lt);
-            if (slot < 32) smv[slot] = j;
+            if (slot < 64) smv[slot] = j;
         }
         nm += __popc(bal);
     }
@@ -1728,6 +1728,77 @@ __device__ __forceinline__ void edge_event_terms(int32_t e, int nm, int32_t i, c
     }
 }
 
+// the same for 33..64 movers: lane a holds movers a and 32 + a
+__device__ __forceinline__ void edge_seq_terms2(int32_t e, int nm, const int32_t (&i)[2], const int64_t *wi,
+                                                const Runs &r, const int32_t *from, const int32_t *to,
+                                                unsigned long long *gacc) {
+    const int lane = lane_id();
+    const int64_t ro = r.off[e];
+    const int32_t lam = r.len[e];
+    int32_t ps[2], pd[2], leav_pd[2] = {0, 0}, ent_pd[2] = {0, 0}, leav_ps[2] = {0, 0}, ent_ps[2] = {0, 0};
+#pragma unroll
+    for (int k = 0; k < 2; k++) {
+        const bool v = 32 * k + lane < nm;
+        ps[k] = v ? from[i[k]] : -1;
+        pd[k] = v ? to[i[k]] : -1;
+    }
+    for (int b = 0; b < nm; b++) {
+        const int kb = b >> 5, lb = b & 31;
+        const int32_t fb = __shfl_sync(FULL_MASK, kb ? ps[1] : ps[0], lb);
+        const int32_t tb = __shfl_sync(FULL_MASK, kb ? pd[1] : pd[0], lb);
+#pragma unroll
+        for (int k = 0; k < 2; k++)
+            if (b < 32 * k + lane) {
+                leav_pd[k] += fb == pd[k];
+                ent_pd[k] += tb == pd[k];
+                leav_ps[k] += fb == ps[k];
+                ent_ps[k] += tb == ps[k];
+            }
+    }
+#pragma unroll
+    for (int k = 0; k < 2; k++)
+        if (32 * k + lane < nm) {
+            int32_t q = run_find(r, ro, lam, ps[k]);
+            const int32_t base_ps = q >= 0 ? r.pc[2 * (ro + q) + 1] : 0;
+            q = run_find(r, ro, lam, pd[k]);
+            const int32_t base_pd = q >= 0 ? r.pc[2 * (ro + q) + 1] : 0;
+            const int64_t net = seq_net(wi[e], base_ps, base_pd, leav_pd[k], ent_pd[k], leav_ps[k], ent_ps[k]);
+            if (net) atomicAdd(&gacc[i[k]], (unsigned long long)net);
+        }
+}
+__device__ __forceinline__ void edge_event_terms2(int32_t e, int nm, const int32_t (&i)[2], const Runs &r,
+                                                  const int32_t *from, const int32_t *to, EvArgs ev) {
+    const int lane = lane_id();
+    const int64_t ro = r.off[e];
+    const int32_t lam = r.len[e];
+    int32_t pf[2], pt[2], df[2] = {0, 0}, dt[2] = {0, 0};
+#pragma unroll
+    for (int k = 0; k < 2; k++) {
+        const bool v = 32 * k + lane < nm;
+        pf[k] = v ? from[i[k]] : -1;
+        pt[k] = v ? to[i[k]] : -1;
+    }
+    for (int b = 0; b < nm; b++) {
+        const int kb = b >> 5, lb = b & 31;
+        const int32_t fb = __shfl_sync(FULL_MASK, kb ? pf[1] : pf[0], lb);
+        const int32_t tb = __shfl_sync(FULL_MASK, kb ? pt[1] : pt[0], lb);
+#pragma unroll
+        for (int k = 0; k < 2; k++)
+            if (b < 32 * k + lane) {
+                df[k] += (tb == pf[k]) - (fb == pf[k]);
+                dt[k] += (tb == pt[k]) - (fb == pt[k]);
+            }
+    }
+#pragma unroll
+    for (int k = 0; k < 2; k++)
+        if (32 * k + lane < nm) {
+            int32_t q = run_find(r, ro, lam, pf[k]);
+            if ((q >= 0 ? r.cin[ro + q] : 0) + df[k] - 1 == 0) inbound_leave(ev, i[k]);
+            q = run_find(r, ro, lam, pt[k]);
+            if ((q >= 0 ? r.cin[ro + q] : 0) + dt[k] == 0) inbound_enter(ev, i[k]);
+        }
+}
+
 __global__ void __launch_bounds__(256) k_round_edges(int32_t E, const int32_t *elist, const int32_t *ecount,
                                                      const int64_t *pin_off, const int32_t *pin_dat,
                                                      const int64_t *dst_off, const int32_t *dst_dat,
@@ -1739,7 +1810,7 @@ __global__ void __launch_bounds__(256) k_round_edges(int32_t E, const int32_t *e
                                                      int64_t elo, int64_t ehi) {
     pdl_entry();
     if (spec_m && *spec_m > kSpecCap) return;  // speculative launch, M too large
-    __shared__ int32_t s_mv[8][32];
+    __shared__ int32_t s_mv[8][64];
     const int lane = lane_id();
     int32_t *smv = s_mv[warp_id()];
     const int64_t ne = elist ? (int64_t)*ecount : (int64_t)E;
@@ -1755,6 +1826,11 @@ __global__ void __launch_bounds__(256) k_round_edges(int32_t E, const int32_t *e
         int nm = warp_collect_movers(pin_dat, pin_off[e], pin_off[e + 1], pos, smv);
         if (nm > cap) {
             if (lane == 0) sg_big[atomicAdd(sg_count, 1)] = e;
+        } else if (nm > 32) {
+            uint32_t v[2] = {(uint32_t)smv[lane], 32 + lane < nm ? (uint32_t)smv[32 + lane] : 0xffffffffu};
+            warp_bitonic_sort<2>(v);
+            const int32_t i2[2] = {(int32_t)v[0], (int32_t)v[1]};
+            edge_seq_terms2(e, nm, i2, wi, r, from, to, gacc);
         } else if (nm > 0) {
             uint32_t v[1] = {lane < nm ? (uint32_t)smv[lane] : 0xffffffffu};
             warp_bitonic_sort<1>(v);
@@ -1765,6 +1841,11 @@ __global__ void __launch_bounds__(256) k_round_edges(int32_t E, const int32_t *e
         nm = warp_collect_movers(dst_dat, dst_off[e], dst_off[e + 1], pos, smv);
         if (nm > cap) {
             if (lane == 0) ev_big[atomicAdd(ev_count, 1)] = e;
+        } else if (nm > 32) {
+            uint32_t v[2] = {(uint32_t)smv[lane], 32 + lane < nm ? (uint32_t)smv[32 + lane] : 0xffffffffu};
+            warp_bitonic_sort<2>(v);
+            const int32_t i2[2] = {(int32_t)v[0], (int32_t)v[1]};
+            edge_event_terms2(e, nm, i2, r, from, to, ev);
         } else if (nm > 0) {
             uint32_t v[1] = {lane < nm ? (uint32_t)smv[lane] : 0xffffffffu};
             warp_bitonic_sort<1>(v);
