@@ -119,14 +119,13 @@ struct ScoreArgs {
     unsigned long long *work = nullptr;  // profiling: algorithmic bytes
     // diagnostics (DHGP_TRACE): candidate iterations and nodes, warp / block tier
     unsigned long long *probe = nullptr;
-    // list mode with few listed nodes (<= this; 0 = off): the block tier
-    // takes every node above kHeavySmallInc incident h-edges (idle SMs
-    // otherwise; a node's latency is the level's critical path)
+    // list mode with few listed nodes (<= this; 0 = off): the CTA pair tier
+    // is preferred (idle SMs otherwise; a node's latency is the level's
+    // critical path)
     int32_t heavy_small_list = 0;
     int32_t *mid_list = nullptr;   // nodes for the 256-thread tier
     int32_t *mid_count = nullptr;
 };
-constexpr int64_t kHeavySmallInc = 48;
 
 // next node of a persistent scoring loop: [lo, hi) or the listed nodes in it
 // (-1 = done, -2 = skip)
@@ -259,9 +258,9 @@ __global__ void __launch_bounds__(SS_WARPS * 32, 3) k_score_warp(ScoreArgs a) {
         if (node < 0) continue;
         const int64_t ilo = a.inc_off[node], ihi = a.inc_end[node];
         // list mode (merged clusters, rescored nodes): every node above
-        // kHeavySmallInc incident h-edges gets a CTA (a node's latency is the
+        // ss_list_inc incident h-edges gets a CTA (a node's latency is the
         // level's critical path); full scoring: above ss_heavy_inc
-        const int64_t hthr = a.list ? min((int64_t)a.t.ss_heavy_inc, kHeavySmallInc) : (int64_t)a.t.ss_heavy_inc;
+        const int64_t hthr = a.list ? min(a.t.ss_heavy_inc, a.t.ss_list_inc) : (int64_t)a.t.ss_heavy_inc;
         if (ihi - ilo > hthr) {
             if (lane == 0) {
                 if (ihi - ilo > a.t.sm_heavy_inc)

@@ -54,6 +54,9 @@ const Tiers &tiers() {
         }
         const char *h = getenv("DHGP_HUB_INC");  // tuning: propose hub-tier threshold
         if (h) x.pr_hub_inc = atoi(h);
+        if (const char *v = getenv("DHGP_SM_HEAVY_INC")) x.sm_heavy_inc = atoi(v);  // tuning: mid -> 1024-thread tier
+        if (const char *v = getenv("DHGP_SS_HEAVY_INC")) x.ss_heavy_inc = atoi(v);  // tuning: warp -> CTA (full scoring)
+        if (const char *v = getenv("DHGP_SS_LIST_INC")) x.ss_list_inc = atoi(v);    // tuning: warp -> CTA (list mode)
         return x;
     }();
     return t;
