@@ -2067,7 +2067,7 @@ __global__ void k_marked_list(int32_t E, const uint8_t *emark, const int64_t *ep
 // chunk with one search of the ascending marked list and keeps up to
 // MG_LOCAL of them (start, end, shift after) in shared memory.
 constexpr int MG_CHUNK = 8192, MG_LOCAL = 256;
-__global__ void __launch_bounds__(256) k_map_gaps(int32_t E, const int32_t *gamma, EdgeFam f0, EdgeFam f1, EdgeFam f2,
+__global__ void __launch_bounds__(256, 6) k_map_gaps(int32_t E, const int32_t *gamma, EdgeFam f0, EdgeFam f1, EdgeFam f2,
                                                   const int32_t *elist, const int32_t *ecount) {
     pdl_entry();
     __shared__ int64_t s_b[MG_LOCAL], s_e[MG_LOCAL], s_sh[MG_LOCAL];
@@ -2138,7 +2138,7 @@ __global__ void __launch_bounds__(256) k_map_gaps(int32_t E, const int32_t *gamm
             // 16 consecutive slots per thread and pass (four 16-byte loads in
             // flight before the gathers); the local entry is found once per
             // group and advanced within it
-            constexpr int G = 16;
+            constexpr int G = 8;
             for (int64_t g0 = (w0 & ~(int64_t)3) + G * (int64_t)threadIdx.x; g0 < w1; g0 += G * (int64_t)blockDim.x) {
                 int32_t x[G];
 #pragma unroll
