@@ -375,7 +375,7 @@ template <class Acc>
 constexpr int sm_smem() { return SM_CAP * (4 + (int)sizeof(Acc)); }
 
 template <class Acc>
-__global__ void __launch_bounds__(SM_THREADS) k_score_mid(ScoreArgs a) {
+__global__ void __launch_bounds__(SM_THREADS, 5) k_score_mid(ScoreArgs a) {
     pdl_entry();
     extern __shared__ unsigned long long smem_u64[];
     Acc *vals = (Acc *)smem_u64;

@@ -1799,7 +1799,7 @@ __device__ __forceinline__ void edge_event_terms2(int32_t e, int nm, const int32
         }
 }
 
-__global__ void __launch_bounds__(256) k_round_edges(int32_t E, const int32_t *elist, const int32_t *ecount,
+__global__ void __launch_bounds__(256, 6) k_round_edges(int32_t E, const int32_t *elist, const int32_t *ecount,
                                                      const int64_t *pin_off, const int32_t *pin_dat,
                                                      const int64_t *dst_off, const int32_t *dst_dat,
                                                      const int64_t *wi, Runs r, const int32_t *pos,
