@@ -832,7 +832,7 @@ __global__ void __launch_bounds__(1024) k_hub_prefix(const int32_t *hub_list, co
 // present[] for its chunk in shared memory and adds it to the hub's global
 // row; the CTA finishing a hub's last chunk selects the target.
 template <class Acc>
-__global__ void __launch_bounds__(256) k_propose_hub(ProposeArgs a, long long *hacc, long long *htot,
+__global__ void __launch_bounds__(256, 6) k_propose_hub(ProposeArgs a, long long *hacc, long long *htot,
                                                      int32_t *hdone) {
     pdl_entry();
     extern __shared__ unsigned long long smem_u64[];
