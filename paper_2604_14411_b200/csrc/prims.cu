@@ -498,7 +498,7 @@ void small_sort_packed(Ctx &c, uint64_t *keys, uint32_t *vals, int64_t n, const 
 // three per 8-bit radix pass.
 // ===========================================================================
 namespace {
-constexpr int MS_CHUNK = 2048, MS_THREADS = 1024, MS_PER = 8;
+constexpr int MS_CHUNK = 512, MS_THREADS = 256, MS_PER = 8;
 __device__ __forceinline__ bool pair_less(uint64_t ka, uint32_t va, uint64_t kb, uint32_t vb) {
     return ka < kb || (ka == kb && va < vb);
 }
