@@ -14,6 +14,8 @@ from pathlib import Path
 import numpy as np
 
 LIB_PATH = Path(__file__).resolve().parent / "libdhgp.so"
+if os.environ.get("DHGP_LIB_VARIANT"):  # diagnostics: an in-tree A/B build, libdhgp_<variant>.so
+    LIB_PATH = LIB_PATH.with_name(f"libdhgp_{os.environ['DHGP_LIB_VARIANT']}.so")
 
 # status codes (include/dhgp.h)
 OK = 0

@@ -284,6 +284,7 @@ struct Tiers {
     int seg_smem = 8192;      // per-segment sorts / wide run updates: longest list kept in shared memory
     int mv_block = 2048;      // events / sequence gains: movers per h-edge for the shared-memory block tier
     int speculate = 1;        // refinement: launch a round's tail before its mover count is on the host
+    long long fe_min = 32768; // sequence gains / events: mover h-edges from which the flat kernel takes a round
 };
 const Tiers &tiers();
 

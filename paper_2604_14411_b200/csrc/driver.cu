@@ -51,12 +51,14 @@ const Tiers &tiers() {
             x.seg_smem = 48;
             x.mv_block = 6;
             x.speculate = 0;
+            x.fe_min = 0;  // every round through the flat kernel (and its deferrals)
         }
         const char *h = getenv("DHGP_HUB_INC");  // tuning: propose hub-tier threshold
         if (h) x.pr_hub_inc = atoi(h);
         if (const char *v = getenv("DHGP_SM_HEAVY_INC")) x.sm_heavy_inc = atoi(v);  // tuning: mid -> 1024-thread tier
         if (const char *v = getenv("DHGP_SS_HEAVY_INC")) x.ss_heavy_inc = atoi(v);  // tuning: warp -> CTA (full scoring)
         if (const char *v = getenv("DHGP_SS_LIST_INC")) x.ss_list_inc = atoi(v);    // tuning: warp -> CTA (list mode)
+        if (const char *v = getenv("DHGP_FE_MIN")) x.fe_min = atoll(v);  // tuning: flat round-edges threshold
         return x;
     }();
     return t;

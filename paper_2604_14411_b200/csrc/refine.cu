@@ -1799,6 +1799,48 @@ __device__ __forceinline__ void edge_event_terms2(int32_t e, int nm, const int32
         }
 }
 
+// one h-edge's round terms, the warp together (movers gathered from its pin
+// lists by position, sorted by sequence index; more than `cap` movers go to
+// the block kernels' lists)
+__device__ __forceinline__ void round_edge_warp(int32_t e, const int64_t *pin_off, const int32_t *pin_dat,
+                                                const int64_t *dst_off, const int32_t *dst_dat, const int64_t *wi,
+                                                const Runs &r, const int32_t *pos, const int32_t *from,
+                                                const int32_t *to, unsigned long long *gacc, const EvArgs &ev,
+                                                int32_t *sg_big, int32_t *sg_count, int32_t *ev_big,
+                                                int32_t *ev_count, int cap, int32_t *smv) {
+    const int lane = lane_id();
+    // ---- sequence gains over all pins --------------------------------
+    int nm = warp_collect_movers(pin_dat, pin_off[e], pin_off[e + 1], pos, smv);
+    if (nm > cap) {
+        if (lane == 0) sg_big[atomicAdd(sg_count, 1)] = e;
+    } else if (nm > 32) {
+        uint32_t v[2] = {(uint32_t)smv[lane], 32 + lane < nm ? (uint32_t)smv[32 + lane] : 0xffffffffu};
+        warp_bitonic_sort<2>(v);
+        const int32_t i2[2] = {(int32_t)v[0], (int32_t)v[1]};
+        edge_seq_terms2(e, nm, i2, wi, r, from, to, gacc);
+    } else if (nm > 0) {
+        uint32_t v[1] = {lane < nm ? (uint32_t)smv[lane] : 0xffffffffu};
+        warp_bitonic_sort<1>(v);
+        edge_seq_terms(e, nm, (int32_t)v[0], wi, r, from, to, gacc);
+    }
+    __syncwarp();
+    // ---- inbound-track crossings over the destination pins -----------
+    nm = warp_collect_movers(dst_dat, dst_off[e], dst_off[e + 1], pos, smv);
+    if (nm > cap) {
+        if (lane == 0) ev_big[atomicAdd(ev_count, 1)] = e;
+    } else if (nm > 32) {
+        uint32_t v[2] = {(uint32_t)smv[lane], 32 + lane < nm ? (uint32_t)smv[32 + lane] : 0xffffffffu};
+        warp_bitonic_sort<2>(v);
+        const int32_t i2[2] = {(int32_t)v[0], (int32_t)v[1]};
+        edge_event_terms2(e, nm, i2, r, from, to, ev);
+    } else if (nm > 0) {
+        uint32_t v[1] = {lane < nm ? (uint32_t)smv[lane] : 0xffffffffu};
+        warp_bitonic_sort<1>(v);
+        edge_event_terms(e, nm, (int32_t)v[0], r, from, to, ev);
+    }
+    __syncwarp();
+}
+
 __global__ void __launch_bounds__(256, 6) k_round_edges(int32_t E, const int32_t *elist, const int32_t *ecount,
                                                      const int64_t *pin_off, const int32_t *pin_dat,
                                                      const int64_t *dst_off, const int32_t *dst_dat,
@@ -1807,12 +1849,20 @@ __global__ void __launch_bounds__(256, 6) k_round_edges(int32_t E, const int32_t
                                                      unsigned long long *gacc, EvArgs ev, int32_t *sg_big,
                                                      int32_t *sg_count, int32_t *ev_big, int32_t *ev_count,
                                                      int cap, const int64_t *spec_m, unsigned long long *work,
-                                                     int64_t elo, int64_t ehi) {
+                                                     int64_t elo, int64_t ehi, const int32_t *alt_list,
+                                                     const int32_t *alt_count, int64_t fe_min) {
     pdl_entry();
     if (spec_m && *spec_m > kSpecCap) return;  // speculative launch, M too large
     __shared__ int32_t s_mv[8][64];
     const int lane = lane_id();
     int32_t *smv = s_mv[warp_id()];
+    // after k_round_edges_flat: when it took the round (at least fe_min
+    // h-edges), only the h-edges it listed remain; else all of them
+    if (alt_list && (elist ? (int64_t)*ecount : (int64_t)E) >= fe_min) {
+        elist = alt_list;
+        ecount = alt_count;
+        work = nullptr;  // counted by the flat kernel
+    }
     const int64_t ne = elist ? (int64_t)*ecount : (int64_t)E;
     const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
     for (int64_t idx = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id(); idx < ne; idx += nw) {
@@ -1822,34 +1872,293 @@ __global__ void __launch_bounds__(256, 6) k_round_edges(int32_t E, const int32_t
         // positions (8 B each), offsets / runs / weight (48 B)
         if (work && lane == 0)
             atomicAdd(work, 8ull * (uint64_t)(pin_off[e + 1] - pin_off[e] + dst_off[e + 1] - dst_off[e]) + 48ull);
-        // ---- sequence gains over all pins --------------------------------
-        int nm = warp_collect_movers(pin_dat, pin_off[e], pin_off[e + 1], pos, smv);
-        if (nm > cap) {
-            if (lane == 0) sg_big[atomicAdd(sg_count, 1)] = e;
-        } else if (nm > 32) {
-            uint32_t v[2] = {(uint32_t)smv[lane], 32 + lane < nm ? (uint32_t)smv[32 + lane] : 0xffffffffu};
-            warp_bitonic_sort<2>(v);
-            const int32_t i2[2] = {(int32_t)v[0], (int32_t)v[1]};
-            edge_seq_terms2(e, nm, i2, wi, r, from, to, gacc);
-        } else if (nm > 0) {
-            uint32_t v[1] = {lane < nm ? (uint32_t)smv[lane] : 0xffffffffu};
-            warp_bitonic_sort<1>(v);
-            edge_seq_terms(e, nm, (int32_t)v[0], wi, r, from, to, gacc);
+        round_edge_warp(e, pin_off, pin_dat, dst_off, dst_dat, wi, r, pos, from, to, gacc, ev, sg_big, sg_count, ev_big,
+                        ev_count, cap, smv);
+    }
+}
+
+// The same terms for many small h-edges at once.  Per-edge warps wait on a
+// chain of dependent loads (list entry -> offsets -> pins -> positions ->
+// moves -> runs) for a handful of pins each; here a warp takes 32 h-edges and
+// flattens the pins of those with at most FE_SMALL pins over its lanes (up to
+// FE_CAP pins per pass, eight in flight per lane), so one chain serves 32
+// h-edges.  The movers found are appended in slot order, i.e. grouped by
+// h-edge; a mover's counts over the earlier movers of its h-edge are taken by
+// comparing sequence indices within the group (no sort), and a group's first
+// mover has no terms (seq_net of zero counts is 0), so run lists are searched
+// only where a term can be non-zero.  Larger h-edges are listed for the
+// per-edge kernel (k_round_edges over that list).
+constexpr int FE_WARPS = 8;
+constexpr int FE_CAP = 256;
+constexpr int FE_SMALL = 32;
+struct FlatWarp {
+    int32_t j[FE_CAP], f[FE_CAP], t[FE_CAP];
+    uint8_t own[FE_CAP];
+    int32_t cnt[32], seg[32], e[32], lam[32], dfr[32];
+    int64_t ro[32];
+    long long net[32];
+};
+constexpr int FE_GROUP = 8;  // more movers on one h-edge: the per-edge warp kernel
+
+// mode 0: the pins (sequence-gain terms); mode 1: the destination pins
+// (inbound crossings).  Lanes with take=false contribute nothing.
+template <int MODE>
+__device__ __forceinline__ void flat_pass(FlatWarp &fw, bool take, int64_t lo, int len, const int32_t *dat,
+                                          const int64_t *wi, const Runs &r, const int32_t *pos, const int32_t *from,
+                                          const int32_t *to, unsigned long long *gacc, const EvArgs &ev,
+                                          int32_t *big, int32_t *big_count, int cap, int32_t *lg_list,
+                                          int32_t *lg_count) {
+    const int lane = lane_id();
+    const uint32_t lt = (1u << lane) - 1u;
+    if (!take) len = 0;
+    const int incl = warp_incl_scan(len);
+    const int total = __shfl_sync(FULL_MASK, incl, 31);
+    const int excl = incl - len;
+    int nent = 0;
+    constexpr int U = 8;
+    for (int s0 = 0; s0 < total; s0 += 32 * U) {
+        int32_t jj[U], ow[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int s = s0 + u * 32 + lane;
+            int owner = 0;
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+                const int ex = __shfl_sync(FULL_MASK, excl, owner + step);
+                if (ex <= s) owner += step;
+            }
+            const int64_t olo = __shfl_sync(FULL_MASK, lo, owner);
+            const int oex = __shfl_sync(FULL_MASK, excl, owner);
+            ow[u] = owner;
+            jj[u] = s < total ? dat[olo + (s - oex)] : -1;
         }
-        __syncwarp();
-        // ---- inbound-track crossings over the destination pins -----------
-        nm = warp_collect_movers(dst_dat, dst_off[e], dst_off[e + 1], pos, smv);
-        if (nm > cap) {
-            if (lane == 0) ev_big[atomicAdd(ev_count, 1)] = e;
-        } else if (nm > 32) {
-            uint32_t v[2] = {(uint32_t)smv[lane], 32 + lane < nm ? (uint32_t)smv[32 + lane] : 0xffffffffu};
-            warp_bitonic_sort<2>(v);
-            const int32_t i2[2] = {(int32_t)v[0], (int32_t)v[1]};
-            edge_event_terms2(e, nm, i2, r, from, to, ev);
-        } else if (nm > 0) {
-            uint32_t v[1] = {lane < nm ? (uint32_t)smv[lane] : 0xffffffffu};
-            warp_bitonic_sort<1>(v);
-            edge_event_terms(e, nm, (int32_t)v[0], r, from, to, ev);
+#pragma unroll
+        for (int u = 0; u < U; u++) jj[u] = jj[u] >= 0 ? pos[jj[u]] : -1;
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const bool mv = jj[u] >= 0;
+            const uint32_t bal = __ballot_sync(FULL_MASK, mv);
+            if (mv) {
+                const int k = nent + __popc(bal & lt);
+                fw.j[k] = jj[u];
+                fw.own[k] = (uint8_t)ow[u];
+            }
+            nent += __popc(bal);
+        }
+    }
+    if (MODE == 0) fw.dfr[lane] = 0;
+    if (nent == 0) return;  // uniform
+    __syncwarp();
+    {
+        // the entries ascend by owner: each lane finds its group by search
+        // (no same-address shared atomics)
+        int a = 0, b = nent;
+        while (a < b) {
+            const int mid = (a + b) >> 1;
+            if (fw.own[mid] < lane) a = mid + 1; else b = mid;
+        }
+        int z = a;
+        b = nent;
+        while (z < b) {
+            const int mid = (z + b) >> 1;
+            if (fw.own[mid] <= lane) z = mid + 1; else b = mid;
+        }
+        const int c = z - a;
+        fw.cnt[lane] = c;
+        fw.seg[lane] = a;
+        // many movers on one h-edge (the O(c^2) counts would serialise on
+        // one lane): the h-edge goes whole to the per-edge warp kernel,
+        // decided on its pins (a superset of its destination pins)
+        bool dfr = false;
+        if (MODE == 0) {
+            dfr = c > FE_GROUP;
+            fw.dfr[lane] = dfr;
+            const uint32_t bal = __ballot_sync(FULL_MASK, dfr);
+            if (bal) {
+                int b = 0;
+                if (lane == 0) b = atomicAdd(lg_count, __popc(bal));
+                b = __shfl_sync(FULL_MASK, b, 0);
+                if (dfr) lg_list[b + __popc(bal & lt)] = fw.e[lane];
+            }
+        } else {
+            dfr = fw.dfr[lane];
+        }
+        // a group beyond the warp tiers' capacity goes to the block kernels
+        if (!dfr && c > cap) big[atomicAdd(big_count, 1)] = fw.e[lane];
+    }
+    for (int k = lane; k < nent; k += 32) {
+        const int32_t jk = fw.j[k];
+        fw.f[k] = from[jk];
+        fw.t[k] = to[jk];
+    }
+    __syncwarp();
+    // TU entries per lane at a time: their run-list searches advance in
+    // lockstep, so a lane waits for one chain of loads per TU entries
+    constexpr int TU = 2;
+    for (int k0 = 0; k0 < nent; k0 += 32 * TU) {
+        // per entry: sequence index, parts (from, to), its h-edge's warp slot
+        // (-1 = no term) and the four counts over the earlier movers, packed
+        // a byte each (at most FE_GROUP movers per group)
+        int32_t jk[TU], pp[2 * TU], ow[TU];
+        uint32_t dd[TU];
+#pragma unroll
+        for (int u = 0; u < TU; u++) {
+            const int k = k0 + u * 32 + lane;
+            ow[u] = -1;
+            jk[u] = pp[2 * u] = pp[2 * u + 1] = 0;
+            dd[u] = 0;
+            if (k >= nent) continue;
+            const int o = fw.own[k];
+            const int c = fw.cnt[o];
+            if (c > cap || fw.dfr[o]) continue;
+            if (MODE == 0 && c == 1) continue;  // a lone mover: no sequence term
+            const int b0 = fw.seg[o];
+            jk[u] = fw.j[k];
+            const int32_t pf = fw.f[k], pt = fw.t[k];
+            uint32_t d = 0;
+            for (int b = b0; b < b0 + c; b++) {
+                if (fw.j[b] >= jk[u]) continue;
+                const int32_t fb = fw.f[b], tb = fw.t[b];
+                d += (fb == pt ? 1u : 0u)          // leav_pd (mode 0) / departures from pt (mode 1)
+                     + (tb == pt ? 1u << 8 : 0u)   // ent_pd / arrivals at pt
+                     + (fb == pf ? 1u << 16 : 0u)  // leav_ps / departures from pf
+                     + (tb == pf ? 1u << 24 : 0u); // ent_ps / arrivals at pf
+            }
+            if (MODE == 0 && !d) continue;  // the first of its group: no term
+            ow[u] = o;
+            dd[u] = d;
+            pp[2 * u] = pf;
+            pp[2 * u + 1] = pt;
+        }
+        // lower bounds of pf / pt among the h-edge's run parts, in lockstep
+        int32_t lo[2 * TU], hi[2 * TU];
+#pragma unroll
+        for (int q = 0; q < 2 * TU; q++) {
+            lo[q] = 0;
+            hi[q] = ow[q >> 1] >= 0 ? fw.lam[ow[q >> 1]] : 0;
+        }
+        while (true) {
+            bool any = false;
+            int32_t v[2 * TU];
+#pragma unroll
+            for (int q = 0; q < 2 * TU; q++)
+                if (lo[q] < hi[q]) {
+                    any = true;
+                    v[q] = r.pc[2 * (fw.ro[ow[q >> 1]] + ((lo[q] + hi[q]) >> 1))];
+                }
+            if (!any) break;
+#pragma unroll
+            for (int q = 0; q < 2 * TU; q++)
+                if (lo[q] < hi[q]) {
+                    const int32_t mid = (lo[q] + hi[q]) >> 1;
+                    if (v[q] < pp[q])
+                        lo[q] = mid + 1;
+                    else
+                        hi[q] = mid;
+                }
+        }
+        // the run's pin count (mode 0) / destination-pin count (mode 1); 0 if absent
+        int32_t cv[2 * TU];
+#pragma unroll
+        for (int q = 0; q < 2 * TU; q++) {
+            cv[q] = 0;
+            const int o = ow[q >> 1];
+            if (o >= 0 && lo[q] < fw.lam[o]) {
+                const int64_t slot = fw.ro[o] + lo[q];
+                const int2 pc = *(const int2 *)(r.pc + 2 * slot);
+                if (pc.x == pp[q]) cv[q] = MODE == 0 ? pc.y : r.cin[slot];
+            }
+        }
+        // the lanes' entries often belong to the same move (few movers, many
+        // h-edges): one atomic per distinct move and warp instruction
+#pragma unroll
+        for (int u = 0; u < TU; u++) {
+            const int32_t a0 = dd[u] & 255, a1 = (dd[u] >> 8) & 255, a2 = (dd[u] >> 16) & 255, a3 = dd[u] >> 24;
+            const bool on = ow[u] >= 0;
+            const uint32_t grp = __match_any_sync(FULL_MASK, on ? jk[u] : -1 - lane);
+            const bool lead = on && lane == __ffs(grp) - 1;
+            if (MODE == 0) {
+                const int64_t net = on ? seq_net(wi[fw.e[ow[u]]], cv[2 * u], cv[2 * u + 1], a0, a1, a2, a3) : 0;
+                fw.net[lane] = net;
+                __syncwarp();
+                if (lead) {
+                    long long tot = 0;
+                    for (uint32_t g = grp; g; g &= g - 1) tot += fw.net[__ffs(g) - 1];
+                    if (tot) atomicAdd(&gacc[jk[u]], (unsigned long long)tot);
+                }
+                __syncwarp();
+            } else {
+                const uint32_t lv = __ballot_sync(FULL_MASK, on && cv[2 * u] + (a3 - a2) - 1 == 0) & grp;
+                const uint32_t en = __ballot_sync(FULL_MASK, on && cv[2 * u + 1] + (a1 - a0) == 0) & grp;
+                if (lead && lv) atomicSub(&ev.in_from[jk[u]], __popc(lv));
+                if (lead && en) atomicAdd(&ev.in_to[jk[u]], __popc(en));
+            }
+        }
+    }
+    __syncwarp();
+}
+
+__global__ void __launch_bounds__(FE_WARPS * 32, 4) k_round_edges_flat(
+    int32_t E, const int32_t *elist, const int32_t *ecount, const int64_t *pin_off, const int32_t *pin_dat,
+    const int64_t *dst_off, const int32_t *dst_dat, const int64_t *wi, Runs r, const int32_t *pos,
+    const int32_t *from, const int32_t *to, unsigned long long *gacc, EvArgs ev, int32_t *sg_big,
+    int32_t *sg_count, int32_t *ev_big, int32_t *ev_count, int cap, const int64_t *spec_m,
+    unsigned long long *work, int64_t elo, int64_t ehi, int32_t *lg_list, int32_t *lg_count, int64_t fe_min) {
+    pdl_entry();
+    if (spec_m && *spec_m > kSpecCap) return;  // speculative launch, M too large
+    // few h-edges: a chunk's load chain would be the round's critical path,
+    // the per-edge kernel (a warp each) takes them all
+    if ((elist ? (int64_t)*ecount : (int64_t)E) < fe_min) return;
+    __shared__ FlatWarp fe_w[FE_WARPS];
+    FlatWarp &fw = fe_w[warp_id()];
+    const int lane = lane_id();
+    const int64_t ne = elist ? (int64_t)*ecount : (int64_t)E;
+    const int64_t nw = (int64_t)gridDim.x * FE_WARPS;
+    for (int64_t base = ((int64_t)blockIdx.x * FE_WARPS + warp_id()) * 32; base < ne; base += nw * 32) {
+        const int64_t idx = base + lane;
+        int32_t e = -1;
+        if (idx < ne) {
+            e = elist ? elist[idx] : (int32_t)idx;
+            if (e < elo || e >= ehi) e = -1;  // another rank's h-edge
+        }
+        int64_t plo = 0, phi = 0, dlo = 0, dhi = 0, ro = 0;
+        int32_t lam = 0;
+        if (e >= 0) {
+            plo = pin_off[e];
+            phi = pin_off[e + 1];
+            dlo = dst_off[e];
+            dhi = dst_off[e + 1];
+            ro = r.off[e];
+            lam = r.len[e];
+        }
+        if (work) {  // algorithmic bytes (profiling), as k_round_edges
+            unsigned long long b = e >= 0 ? 8ull * (uint64_t)(phi - plo + dhi - dlo) + 48ull : 0ull;
+            b = warp_sum(b);
+            if (lane == 0 && b) atomicAdd(work, b);
+        }
+        const bool small = e >= 0 && phi - plo <= FE_SMALL;
+        fw.e[lane] = e;
+        fw.ro[lane] = ro;
+        fw.lam[lane] = lam;
+        uint32_t rem = __ballot_sync(FULL_MASK, small);
+        while (rem) {  // passes over the small h-edges, at most FE_CAP pins each
+            const bool mine = (rem >> lane) & 1u;
+            const int in = warp_incl_scan(mine ? (int)(phi - plo) : 0);
+            const bool take = mine && in <= FE_CAP;
+            rem &= ~__ballot_sync(FULL_MASK, take);
+            flat_pass<0>(fw, take, plo, (int)(phi - plo), pin_dat, wi, r, pos, from, to, gacc, ev, sg_big, sg_count,
+                         cap, lg_list, lg_count);
+            flat_pass<1>(fw, take, dlo, (int)(dhi - dlo), dst_dat, wi, r, pos, from, to, gacc, ev, ev_big, ev_count,
+                         cap, lg_list, lg_count);
+        }
+        // larger h-edges: listed for the per-edge warp kernel (a warp each)
+        const bool lg = e >= 0 && !small;
+        const uint32_t bal = __ballot_sync(FULL_MASK, lg);
+        if (bal) {
+            int b = 0;
+            if (lane == 0) b = atomicAdd(lg_count, __popc(bal));
+            b = __shfl_sync(FULL_MASK, b, 0);
+            if (lg) lg_list[b + __popc(bal & ((1u << lane) - 1u))] = e;
         }
         __syncwarp();
     }
@@ -2454,7 +2763,8 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
     int32_t *node = c.alloc<int32_t>(N), *from = c.alloc<int32_t>(N), *to = c.alloc<int32_t>(N);
     int64_t *giso = c.alloc<int64_t>(N), *gseq = c.alloc<int64_t>(N), *gseq_acc = c.alloc<int64_t>(N);
     int32_t *ev_from = c.alloc<int32_t>(N), *ev_to = c.alloc<int32_t>(N);
-    int32_t *sg_big = c.alloc<int32_t>(L.E), *sg_ctr = c.alloc<int32_t>(4);  // [2], [3]: huge-list counts
+    // sg_ctr [2], [3]: huge-list counts; [4]: the flat kernel's large h-edges (lg_list)
+    int32_t *sg_big = c.alloc<int32_t>(L.E), *sg_ctr = c.alloc<int32_t>(8), *lg_list = c.alloc<int32_t>(L.E);
     // h-edges with more movers than shared memory holds (only possible when
     // an h-edge has more than 2048 pins): huge lists + 20 B/pin scratch per CTA
     const int mv_max = std::min(std::min(kSgBlockMax, kEvBlockMax), tiers().mv_block);
@@ -2762,18 +3072,31 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
                 KScope ks(c, "seq_gains", 0.0);
                 unsigned long long *gacc = (unsigned long long *)gseq_acc;
                 zero_many(c,
-                          {{gacc, 8 * Mc}, {sg_ctr, 16}, {ctr, 16}, {ev_from, 4 * Mc}, {ev_to, 4 * Mc}, {ecount, 8}});
+                          {{gacc, 8 * Mc}, {sg_ctr, 32}, {ctr, 16}, {ev_from, 4 * Mc}, {ev_to, 4 * Mc}, {ecount, 8}});
                 // sharding: each rank takes the mover h-edges of its h-edge id
                 // range; a move's terms are then summed across ranks
                 const Shard esh = shard_of(c.comm, L.E);
                 if (L.E > 0) {
-                    static int g_re = resident_grid(c, k_round_edges, 256, 0);
-                    const unsigned gre = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(L.E, 8), g_re));
-                    pdl_launch(k_round_edges, gre, 256, 0, c.stream, L.E, elist, elist_n, L.pin_off, L.pin_dat, L.dst_off,
-                                                             L.dst_dat, W.wi, r, pos, from, to, gacc, ev, sg_big,
-                                                             sg_ctr, big, ctr, tiers().edge_movers,
-                                                             sp ? dM : nullptr, c.work_slot(Ctx::PW_SEQ_GAINS),
-                                                             esh.lo, esh.hi);
+                    {
+                        // the flat kernel takes rounds of many mover h-edges
+                        // (small ones in warp chunks; the rest listed), the
+                        // per-edge kernel the listed ones, or all of a small round
+                        const int64_t fe_min = tiers().fe_min;
+                        static int g_fe = resident_grid(c, k_round_edges_flat, FE_WARPS * 32, 0);
+                        const unsigned gre =
+                            (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(L.E, 32 * FE_WARPS), g_fe));
+                        pdl_launch(k_round_edges_flat, gre, FE_WARPS * 32, 0, c.stream, L.E, elist, elist_n,
+                                   L.pin_off, L.pin_dat, L.dst_off, L.dst_dat, W.wi, r, pos, from, to, gacc, ev,
+                                   sg_big, sg_ctr, big, ctr, tiers().edge_movers, sp ? dM : nullptr,
+                                   c.work_slot(Ctx::PW_SEQ_GAINS), esh.lo, esh.hi, lg_list, sg_ctr + 4, fe_min);
+                        DHGP_LAUNCHED(c);
+                        static int g_re = resident_grid(c, k_round_edges, 256, 0);
+                        const unsigned gpe = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(L.E, 8), g_re));
+                        pdl_launch(k_round_edges, gpe, 256, 0, c.stream, L.E, elist, elist_n, L.pin_off, L.pin_dat,
+                                   L.dst_off, L.dst_dat, W.wi, r, pos, from, to, gacc, ev, sg_big, sg_ctr, big, ctr,
+                                   tiers().edge_movers, sp ? dM : nullptr, c.work_slot(Ctx::PW_SEQ_GAINS), esh.lo,
+                                   esh.hi, lg_list, sg_ctr + 4, fe_min);
+                    }
                     DHGP_LAUNCHED(c);
                     pdl_launch(k_seq_gains_edge_block, c.num_sms, 256, 0, c.stream, L.pin_off, L.pin_dat, W.wi, r, pos, from,
                                                                              to, gacc, sg_big, sg_ctr, hv_sg, sg_ctr + 2,
@@ -2850,6 +3173,13 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
             }
             kbest = hr[0];
             total_gain = hr[1];
+            if (trace_enabled()) {  // diagnostics: movers and the h-edges holding one
+                int32_t hm[CT_MLIST + 1];
+                c.d2h(hm, st.ctr, CT_MLIST + 1);
+                c.sync();
+                fprintf(stderr, "round level %d N %d E %d M %lld elist %d\n", level, N, L.E, (long long)M,
+                        st.inc ? hm[CT_MLIST] : L.E);
+            }
             if (hr[2]) {  // a large round: the multi-kernel path
                 unsigned long long T = 0;
                 c.d2h(&T, ecount, 1);
@@ -2959,7 +3289,7 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
     for (void *p : {(void *)tmp_parts, (void *)flags, (void *)mpos, (void *)pos, (void *)ctr, (void *)big,
                     (void *)big2, (void *)mk, (void *)mkt, (void *)mv, (void *)mvt, (void *)node, (void *)from,
                     (void *)to, (void *)giso, (void *)gseq, (void *)gseq_acc, (void *)ev_from, (void *)ev_to,
-                    (void *)sg_big, (void *)sg_ctr,
+                    (void *)sg_big, (void *)sg_ctr, (void *)lg_list,
                     (void *)ek, (void *)ekt, (void *)evv, (void *)evt, (void *)ecount, (void *)sres, (void *)pdense,
                     (void *)ptouched, (void *)huge_scr, (void *)hv_sg,
                     (void *)hv_ev, (void *)mv_scr})

@@ -1,4 +1,4 @@
-"""Diagnostics: per-scope timing histogram of one C2 partition (DHGP_TRACE=1)."""
+"""Diagnostics: per-scope timing histogram of one warm partition (default C2; DHGP_TRACE=1)."""
 import os, subprocess, sys, collections
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if os.environ.get("DHGP_TRACE") != "1":
@@ -8,7 +8,8 @@ if os.environ.get("DHGP_TRACE") != "1":
         with open(os.environ["DHGP_TRACE_RAW"], "w") as f:
             f.write(r.stdout + r.stderr)
     agg = collections.defaultdict(lambda: [0, 0.0, []])
-    for ln in r.stderr.splitlines():
+    err = r.stderr.split("=== WARM ===")[-1]  # the second (warm) partition only
+    for ln in err.splitlines():
         if ln.startswith("trace "):
             _, nm, ms, tag = ln.split()
             a = agg[nm]; a[0] += 1; a[1] += float(ms); a[2].append((float(ms), int(tag)))
@@ -30,6 +31,8 @@ arrs, om, de, _ = W.make_config(sys.argv[1] if len(sys.argv) > 1 else "C2")
 n, w, so, sd, do, dd = arrs
 g = dp.Hypergraph._from_csr(n, w, dp.CsrSets(so, sd), dp.CsrSets(do, dd))
 import time
+dp.partition(g, dp.Config(dp.Constraints(om, de), max_levels=1 << 20))  # warm-up (allocator, module load)
+print("=== WARM ===", file=sys.stderr, flush=True)
 t = time.perf_counter()
 p, s = dp.partition(g, dp.Config(dp.Constraints(om, de), max_levels=1 << 20))
 print("total", time.perf_counter() - t, len(s.levels), p.num_parts)
