@@ -1890,7 +1890,7 @@ __global__ void __launch_bounds__(256, 6) k_round_edges(int32_t E, const int32_t
 // per-edge kernel (k_round_edges over that list).
 constexpr int FE_WARPS = 8;
 constexpr int FE_CAP = 256;
-constexpr int FE_SMALL = 32;
+constexpr int FE_SMALL = 64;
 struct FlatWarp {
     int32_t j[FE_CAP], f[FE_CAP], t[FE_CAP];
     uint8_t own[FE_CAP];
@@ -1898,7 +1898,7 @@ struct FlatWarp {
     int64_t ro[32];
     long long net[32];
 };
-constexpr int FE_GROUP = 8;  // more movers on one h-edge: the per-edge warp kernel
+constexpr int FE_GROUP = 16; // more movers on one h-edge: the per-edge warp kernel
 
 // mode 0: the pins (sequence-gain terms); mode 1: the destination pins
 // (inbound crossings).  Lanes with take=false contribute nothing.
