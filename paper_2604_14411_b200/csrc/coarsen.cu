@@ -125,6 +125,9 @@ struct ScoreArgs {
     int32_t heavy_small_list = 0;
     int32_t *mid_list = nullptr;   // nodes for the 256-thread tier
     int32_t *mid_count = nullptr;
+    // incremental scoring: per node {size, mb, thr_p, thr_s} in one 16-byte
+    // record, so a neighbour's checks in filter_emit cost one gather, not four
+    const int4 *pk = nullptr;
 };
 
 // next node of a persistent scoring loop: [lo, hi) or the listed nodes in it
@@ -179,10 +182,18 @@ __device__ __forceinline__ void filter_emit(const ScoreArgs &a, int32_t node, in
 #pragma unroll
         for (int u = 0; u < U; u++) {
             const bool v = k[u] >= 0;
-            sz[u] = v ? a.size[k[u]] : 0;
-            mbv[u] = (v && a.mb) ? a.mb[k[u]] : 0;
-            tp[u] = (v && a.mb) ? a.thr_p[k[u]] : -1;
-            ts[u] = (v && a.mb) ? (long long)a.thr_s[k[u]] : 0;
+            if (a.pk) {
+                const int4 q = v ? a.pk[k[u]] : make_int4(0, 0, -1, 0);
+                sz[u] = q.x;
+                mbv[u] = q.y;
+                tp[u] = q.z;
+                ts[u] = q.w;
+            } else {
+                sz[u] = v ? a.size[k[u]] : 0;
+                mbv[u] = (v && a.mb) ? a.mb[k[u]] : 0;
+                tp[u] = (v && a.mb) ? a.thr_p[k[u]] : -1;
+                ts[u] = (v && a.mb) ? (long long)a.thr_s[k[u]] : 0;
+            }
         }
 #pragma unroll
         for (int u = 0; u < U; u++) {
@@ -920,15 +931,18 @@ __global__ void __launch_bounds__(SB_THREADS) k_score_block(ScoreArgs a, long lo
 // 2 no carried pair, 3 carried pair merged (rescored unless a tuple wins)
 __global__ void k_inc_base(int32_t N, const int32_t *ma, const int32_t *mb, const int32_t *gamma_prev,
                            const int32_t *prev_pair, const double *prev_score, uint8_t *kind, int64_t *thr_s,
-                           int32_t *thr_p, unsigned long long *best, int32_t *list, int32_t *list_count) {
+                           int32_t *thr_p, unsigned long long *best, int32_t *list, int32_t *list_count,
+                           const int32_t *size, int4 *pk) {
     pdl_entry();
     const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= N) return;
     best[c] = 0ull;
-    if (mb[c] >= 0) {
+    const int32_t m = mb[c], sz = size[c];
+    if (m >= 0) {
         kind[c] = 0;
         thr_p[c] = -1;
         thr_s[c] = 0;  // (gathered alongside thr_p by filter_emit, never used when thr_p < 0)
+        pk[c] = make_int4(sz, m, -1, 0);
         list[atomicAdd(list_count, 1)] = (int32_t)c;
         return;
     }
@@ -937,10 +951,13 @@ __global__ void k_inc_base(int32_t N, const int32_t *ma, const int32_t *mb, cons
         kind[c] = 2;
         thr_p[c] = -1;
         thr_s[c] = 0;
+        pk[c] = make_int4(sz, m, -1, 0);
         return;
     }
+    // carried scores are hist values < 2^31 (incremental mode: total weight < 2^31)
     thr_s[c] = (int64_t)prev_score[f];
     thr_p[c] = p;
+    pk[c] = make_int4(sz, m, p, (int32_t)(int64_t)prev_score[f]);
     kind[c] = mb[gamma_prev[p]] >= 0 ? 3 : 1;
 }
 // tuples that pass the inbound-union bound compete by (hist, cluster id):
@@ -1179,9 +1196,10 @@ void score_select_inc(Ctx &c, const DLevel &L, const DWeights &W, int64_t omega,
     const int64_t cap = 8 * (int64_t)N + (1 << 20);
     int32_t *tv = c.alloc<int32_t>(cap), *tb = c.alloc<int32_t>(cap), *hard = c.alloc<int32_t>(cap);
     int64_t *th = c.alloc<int64_t>(cap);
+    int4 *pk = c.alloc<int4>(N);
     c.zero(lc, 4);
     pdl_launch(k_inc_base, (unsigned)cdiv(N, 256), 256, 0, c.stream, N, cy.ma, cy.mb, cy.gamma_prev, cy.prev_pair,
-                                                            cy.prev_score, kind, thr_s, thr_p, best, list, lc);
+                                                            cy.prev_score, kind, thr_s, thr_p, best, list, lc, L.size, pk);
     DHGP_LAUNCHED(c);
     // pass 1: the merged clusters, emitting their beating neighbour tuples
     ScoreArgs a{N, L.inc_off, L.inc_dat, L.pin_off, L.pin_dat, W.wi, L.size, L.in_off, L.in_dat, L.inc_e(), L.in_e(),
@@ -1197,6 +1215,7 @@ void score_select_inc(Ctx &c, const DLevel &L, const DWeights &W, int64_t omega,
     a.tup_h = th;
     a.tup_count = lc + 2;
     a.tup_cap = cap;
+    a.pk = pk;
     a.heavy_small_list = 2 * c.num_sms;
     // node-range sharding (comm.cuh): each rank rescores the merged clusters
     // and rescore-listed nodes of its range; the per-node best tuple keys are
@@ -1268,7 +1287,7 @@ void score_select_inc(Ctx &c, const DLevel &L, const DWeights &W, int64_t omega,
         c.free(probe);
     }
     for (void *q : {(void *)kind, (void *)thr_s, (void *)thr_p, (void *)best, (void *)list, (void *)list2, (void *)lc,
-                    (void *)tv, (void *)tb, (void *)th, (void *)hard})
+                    (void *)tv, (void *)tb, (void *)th, (void *)hard, (void *)pk})
         c.free(q);
 }
 
