@@ -2204,6 +2204,22 @@ __device__ __forceinline__ void round_move(int64_t i, const int32_t *node, const
     if (a) put(1, f, a);
     if (b) put(1, t, b);
 }
+// the round's results for the host in one record (one copy per round sync
+// instead of five): selection (k, gain, large), movers, connectivity, the
+// tiers' overflow counters
+__global__ void k_round_summary(const long long *sres, const int32_t *ctr, const int32_t *sg, const int64_t *dM,
+                                const unsigned long long *conn, long long *out) {
+    pdl_entry();
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    out[0] = sres[0];
+    out[1] = sres[1];
+    out[2] = sres[2];
+    out[3] = dM ? (long long)*dM : 0;
+    out[4] = conn ? (long long)*conn : 0;
+    for (int i = 0; i < 4; i++) out[5 + i] = ctr[i];
+    out[9] = sg[0];
+    out[10] = sg[1];
+}
 __global__ void k_round_moves(const int64_t *dM, const int32_t *node, const int32_t *from, const int32_t *to,
                               const int32_t *size, EvArgs ev, const int64_t *giso, const unsigned long long *gacc,
                               int64_t *gseq, bool spec) {
@@ -2684,6 +2700,8 @@ void refine_state_release(Ctx &c, RefineState &st) {
 void refine_project(Ctx &c, RefineState &st, const DLevel &fine, int32_t coarse_n, int32_t *&assign,
                     int32_t *&assign2) {
     const int32_t N = fine.N;
+    // algorithmic bytes: gamma, the assignment and the carried proposal state per node
+    KScope ks(c, "project", 40.0 * (double)N);
     if (N > 0) {
         if (st.inc) {
             c.zero(st.ccount, std::max<int32_t>(1, coarse_n));
@@ -2784,6 +2802,7 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
     uint32_t *evv = c.alloc<uint32_t>(ecap), *evt = c.alloc<uint32_t>(ecap);
     unsigned long long *ecount = c.alloc<unsigned long long>(1);
     long long *sres = c.alloc<long long>(4);
+    long long *rsum = c.alloc<long long>(11);
     // dense global tier (K too large for shared memory): per-block rows of K
     // counters + touched lists, as many blocks as ~1 GiB allows (4 per SM max)
     const bool need_dense = K > ph_maxk<unsigned>() && K > std::min(4096, tiers().small_k);
@@ -2993,6 +3012,8 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
         // packed (key, node) when the key fits 32 bits: an unordered atomic
         // compaction then sorts correctly; else the ordered flags + scan
         const bool packed = gmax_bits <= 32;
+        // algorithmic bytes: target, gain and position per node
+        KScope km(c, "movers", 16.0 * (double)N);
         if (packed) {
             if (N == 0) c.zero(dM, 1);
             if (N > 0) {
@@ -3007,6 +3028,7 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
             }
             scan_excl<uint8_t>(c, flags, mpos, N);
         }
+        km.close();
         // ---- the round's tail (sort, moves, A15, A17 select) is launched
         // before M is on the host: speculatively for up to kSpecCap movers,
         // with M read on device (the kernels are no-ops beyond that, and the
@@ -3147,14 +3169,24 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
             long long hr[3];
             int32_t hc[4];
             int32_t hs[2];
-            c.d2h(hr, sres, 3);
-            c.d2h(hc, ctr, 4);
-            c.d2h(hs, sg_ctr, 2);
-            if (spec) {
-                c.d2h(&M, dM, 1);
-                c.d2h(&conn_h, conn_d, 1);
-            }
-            c.sync();
+            long long sum[11];
+            auto read_round = [&](bool with_m) {
+                pdl_launch(k_round_summary, 1, 32, 0, c.stream, (const long long *)sres, (const int32_t *)ctr,
+                           (const int32_t *)sg_ctr, with_m ? (const int64_t *)dM : nullptr,
+                           with_m ? (const unsigned long long *)conn_d : nullptr, rsum);
+                DHGP_LAUNCHED(c);
+                c.d2h(sum, rsum, 11);
+                c.sync();
+                for (int i = 0; i < 3; i++) hr[i] = sum[i];
+                if (with_m) {
+                    M = sum[3];
+                    conn_h = (unsigned long long)sum[4];
+                }
+                for (int i = 0; i < 4; i++) hc[i] = (int32_t)sum[5 + i];
+                hs[0] = (int32_t)sum[9];
+                hs[1] = (int32_t)sum[10];
+            };
+            read_round(spec);
             if (spec) {
                 conns.push_back((double)(int64_t)conn_h * W.unit);
                 need_final = false;
@@ -3165,10 +3197,7 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
                 if (M > kSpecCap) {  // the speculative launch did nothing: relaunch for the real M
                     free_tail();
                     launch_tail(false, M);
-                    c.d2h(hr, sres, 3);
-                    c.d2h(hc, ctr, 4);
-                    c.d2h(hs, sg_ctr, 2);
-                    c.sync();
+                    read_round(false);
                 }
             }
             kbest = hr[0];
@@ -3253,6 +3282,8 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
             rec.active.assign(ae.begin() + 1, ae.begin() + 2 + M);
             (*obs)(rec);
         }
+        // algorithmic bytes (lower bound): the applied moves (node, from, to, size) and their assignment
+        KScope kap(c, "apply", 24.0 * (double)kbest);
         if (st.inc) {
             // apply + record the dirt; clears the mover-edge flags either way
             pdl_launch(k_apply_inc, g_ap, 256, 0, c.stream, kbest, node, from, to, L.size, L.inc_off, L.inc_e(), L.inc_dat, assign,
@@ -3266,6 +3297,7 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
             pdl_launch(k_apply, (unsigned)cdiv(kbest, 256), 256, 0, c.stream, kbest, node, to, assign);
             DHGP_LAUNCHED(c);
         }
+        kap.close();
         c.free(dlt);
         c.free(act_ex);
         c.free(cum);
@@ -3290,7 +3322,7 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
                     (void *)big2, (void *)mk, (void *)mkt, (void *)mv, (void *)mvt, (void *)node, (void *)from,
                     (void *)to, (void *)giso, (void *)gseq, (void *)gseq_acc, (void *)ev_from, (void *)ev_to,
                     (void *)sg_big, (void *)sg_ctr, (void *)lg_list,
-                    (void *)ek, (void *)ekt, (void *)evv, (void *)evt, (void *)ecount, (void *)sres, (void *)pdense,
+                    (void *)ek, (void *)ekt, (void *)evv, (void *)evt, (void *)ecount, (void *)sres, (void *)rsum, (void *)pdense,
                     (void *)ptouched, (void *)huge_scr, (void *)hv_sg,
                     (void *)hv_ev, (void *)mv_scr})
         c.free(p);
