@@ -1077,9 +1077,10 @@ void merge_union_write2(Ctx &c, int64_t nc, const int32_t *ma, const int32_t *mb
 // several small zero-fills in one launch (blockIdx.y = buffer)
 // ===========================================================================
 namespace {
+constexpr int kZeroMax = 16;
 struct ZeroSet {
-    void *p[8];
-    int64_t bytes[8];
+    void *p[kZeroMax];
+    int64_t bytes[kZeroMax];
 };
 __global__ void k_zero_many(ZeroSet z) {
     pdl_entry();
@@ -1133,17 +1134,20 @@ void dev_copy(void *dst, const void *src, size_t bytes, cudaStream_t s) {
     pdl_launch(k_copy, fill_grid(bytes), 256, 0, s, (uint8_t *)dst, (const uint8_t *)src, bytes);
 }
 
-void zero_many(Ctx &c, std::initializer_list<std::pair<void *, int64_t>> bufs) {
+void zero_many(Ctx &c, std::initializer_list<std::pair<void *, int64_t>> bufs,
+               std::initializer_list<std::pair<void *, int64_t>> more) {
     ZeroSet z;
     int n = 0;
     int64_t mx = 0;
-    for (const auto &b : bufs) {
-        if (b.second <= 0 || !b.first) continue;
-        z.p[n] = b.first;
-        z.bytes[n] = b.second;
-        mx = std::max(mx, b.second);
-        n++;
-    }
+    for (const auto *set : {&bufs, &more})
+        for (const auto &b : *set) {
+            if (b.second <= 0 || !b.first) continue;
+            if (n == kZeroMax) throw Error{DHGP_ERR_CUDA, "zero_many: too many buffers"};
+            z.p[n] = b.first;
+            z.bytes[n] = b.second;
+            mx = std::max(mx, b.second);
+            n++;
+        }
     if (n == 0) return;
     const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(mx / 4, 256), 64));
     pdl_launch(k_zero_many, dim3(gx, n), 256, 0, c.stream, z);

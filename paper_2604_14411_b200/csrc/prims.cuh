@@ -36,7 +36,8 @@ constexpr int64_t kMergeSortMax = 1 << 20;
 // and are distinct).
 constexpr int64_t kSmallSort = 4096;
 // up to eight zero-fills (pointer, bytes; 4-byte aligned) in one launch
-void zero_many(Ctx &c, std::initializer_list<std::pair<void *, int64_t>> bufs);
+using ZeroSpan = std::pair<void *, int64_t>;  // (pointer, bytes)
+void zero_many(Ctx &c, std::initializer_list<ZeroSpan> bufs, std::initializer_list<ZeroSpan> more = {});
 // the same for unique keys carrying their value in the low 32 bits
 // dn != null: the count is read on device (n ignored); no-op above kSmallSort
 void small_sort_packed(Ctx &c, uint64_t *keys, uint32_t *vals, int64_t n, const int64_t *dn = nullptr);

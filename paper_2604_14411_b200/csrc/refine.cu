@@ -1010,9 +1010,10 @@ __global__ void k_fill_ll(long long *p, long long v, int64_t n) {
     if (i < n) p[i] = v;
 }
 
-__global__ void k_mover_flags(int32_t N, const int32_t *target, uint8_t *flags) {
+__global__ void k_mover_flags(int32_t N, const int32_t *target, uint8_t *flags, int32_t *reset) {
     pdl_entry();
     int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (reset && n == 0) *reset = 0;
     if (n < N) flags[n] = target[n] >= 0;
 }
 
@@ -2168,9 +2169,10 @@ __global__ void __launch_bounds__(FE_WARPS * 32, 4) k_round_edges_flat(
 // sequence key (gain desc) with the node id in the low 32 bits, so equal
 // gains order by node (refine.py:108-110) in any sort; pos[] reset on the way
 __global__ void k_mover_compact(int32_t N, const int32_t *target, const int64_t *gain, int64_t gmax, uint64_t *keys,
-                                uint32_t *vals, int32_t *pos, unsigned long long *count) {
+                                uint32_t *vals, int32_t *pos, unsigned long long *count, int32_t *reset) {
     pdl_entry();
     const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (reset && n == 0) *reset = 0;
     const bool mv = n < N && target[n] >= 0;
     if (n < N) pos[n] = -1;
     const uint32_t bal = __ballot_sync(FULL_MASK, mv);
@@ -2781,6 +2783,7 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
     int32_t *node = c.alloc<int32_t>(N), *from = c.alloc<int32_t>(N), *to = c.alloc<int32_t>(N);
     int64_t *giso = c.alloc<int64_t>(N), *gseq = c.alloc<int64_t>(N), *gseq_acc = c.alloc<int64_t>(N);
     int32_t *ev_from = c.alloc<int32_t>(N), *ev_to = c.alloc<int32_t>(N);
+    int32_t *ectr = c.alloc<int32_t>(4);  // the event stage's overflow-list counters (ctr is the proposals')
     // sg_ctr [2], [3]: huge-list counts; [4]: the flat kernel's large h-edges (lg_list)
     int32_t *sg_big = c.alloc<int32_t>(L.E), *sg_ctr = c.alloc<int32_t>(8), *lg_list = c.alloc<int32_t>(L.E);
     // h-edges with more movers than shared memory holds (only possible when
@@ -2860,10 +2863,18 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
     bool need_final = false;
     for (int32_t rnd = 0; rnd < max_rounds; rnd++) {
         const bool full = !st.inc || st.fresh;
+        // the round's counters and, for a speculative tail, its per-move
+        // accumulators start at zero: one fill at the round's start (the mover
+        // count, the mover-edge list, the h-edge terms, the event lists)
+        const bool spec_round = gmax_bits <= 32 && tiers().speculate;
+        const int64_t mc0 = spec_round ? std::min<int64_t>(kSpecCap, N) : 0;
+        const std::initializer_list<ZeroSpan> round_zero = {
+            {dM, 8}, {st.ctr + CT_MLIST, 4}, {sg_ctr, 32}, {ectr, 16}, {ecount, 8}, {gseq_acc, 8 * mc0},
+            {ev_from, 4 * mc0}, {ev_to, 4 * mc0}};
         if (full) {
             // --- A11/A12/A16 + A13 over everything ----------------------------
             build_runs(c, L, W, assign, r, tmp_parts, pinbound, K, conn_d, max_edge_pins);
-            c.zero(psizes, K);
+            zero_many(c, round_zero, {{psizes, 8 * (int64_t)K}, {ctr, 16}});
             if (N > 0) {
                 pdl_launch(k_part_sizes, (unsigned)cdiv(N, 256), 256, 0, c.stream, N, assign, L.size, psizes);
                 DHGP_LAUNCHED(c);
@@ -2881,7 +2892,8 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
             }
             // the dirty-edge list is consumed, the shrink flags too; the
             // propose counters start at zero
-            zero_many(c, {{st.ctr + CT_ELIST, 4}, {st.pflags, mp ? (int64_t)K : 0}, {ctr, 16}, {st.ctr + CT_WIDE, 4}});
+            zero_many(c, round_zero,
+                      {{st.ctr + CT_ELIST, 4}, {st.pflags, mp ? (int64_t)K : 0}, {ctr, 16}, {st.ctr + CT_WIDE, 4}});
         }
         st.moved = false;
         // --- A14 propose (warp tier + block tier, no host sync) -------------
@@ -2892,7 +2904,6 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
                 work = c.alloc<unsigned long long>(1);
                 c.zero(work, 1);
             }
-            if (full) c.zero(ctr, 4);
             ProposeArgs a{N, K, L.inc_off, L.inc_dat, W.wi, r, assign, psizes, L.size, omega,
                           target, gain, ctr, big, ctr + 1, big2, ctr + 2, tiers(), 0, N};
             a.inc_end = L.inc_e();
@@ -2935,8 +2946,6 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
                     pdl_launch(k_propose_warp<unsigned long long>, blocks, PR_WARPS * 32, pr_smem<unsigned long long>(), c.stream, a);
                 }
                 DHGP_LAUNCHED(c);
-                // the dirty-node list is consumed; the mover count starts at zero
-                zero_many(c, {{full ? nullptr : (void *)(st.ctr + CT_NLIST), 4}, {dM, 8}});
                 KScope kh(c, "propose_heavy");
                 if (small_k) {
                     pdl_launch(k_hub_prefix, 1, 1024, 0, c.stream, st.hlist, ctr + 3, st.hub_max, L.inc_off, L.inc_e(),
@@ -3015,15 +3024,18 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
         // algorithmic bytes: target, gain and position per node
         KScope km(c, "movers", 16.0 * (double)N);
         if (packed) {
-            if (N == 0) c.zero(dM, 1);
             if (N > 0) {
+                // (the dirty-node list was consumed by the proposals: its count
+                // is reset here, incremental rounds only)
                 pdl_launch(k_mover_compact, (unsigned)cdiv(N, 256), 256, 0, c.stream, N, target, gain, W.wsum, mk, mv, pos,
-                                                                             (unsigned long long *)dM);
+                                                                             (unsigned long long *)dM,
+                                                                             full ? nullptr : st.ctr + CT_NLIST);
                 DHGP_LAUNCHED(c);
             }
         } else {
             if (N > 0) {
-                pdl_launch(k_mover_flags, (unsigned)cdiv(N, 256), 256, 0, c.stream, N, target, flags);
+                pdl_launch(k_mover_flags, (unsigned)cdiv(N, 256), 256, 0, c.stream, N, target, flags,
+                           full ? nullptr : st.ctr + CT_NLIST);
                 DHGP_LAUNCHED(c);
             }
             scan_excl<uint8_t>(c, flags, mpos, N);
@@ -3093,8 +3105,9 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
             {
                 KScope ks(c, "seq_gains", 0.0);
                 unsigned long long *gacc = (unsigned long long *)gseq_acc;
-                zero_many(c,
-                          {{gacc, 8 * Mc}, {sg_ctr, 32}, {ctr, 16}, {ev_from, 4 * Mc}, {ev_to, 4 * Mc}, {ecount, 8}});
+                // (a speculative tail's accumulators were zeroed at the round's start)
+                if (!sp) zero_many(c, {{gacc, 8 * Mc}, {sg_ctr, 32}, {ectr, 16}, {ev_from, 4 * Mc}, {ev_to, 4 * Mc},
+                                       {ecount, 8}});
                 // sharding: each rank takes the mover h-edges of its h-edge id
                 // range; a move's terms are then summed across ranks
                 const Shard esh = shard_of(c.comm, L.E);
@@ -3109,13 +3122,13 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
                             (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(L.E, 32 * FE_WARPS), g_fe));
                         pdl_launch(k_round_edges_flat, gre, FE_WARPS * 32, 0, c.stream, L.E, elist, elist_n,
                                    L.pin_off, L.pin_dat, L.dst_off, L.dst_dat, W.wi, r, pos, from, to, gacc, ev,
-                                   sg_big, sg_ctr, big, ctr, tiers().edge_movers, sp ? dM : nullptr,
+                                   sg_big, sg_ctr, big, ectr, tiers().edge_movers, sp ? dM : nullptr,
                                    c.work_slot(Ctx::PW_SEQ_GAINS), esh.lo, esh.hi, lg_list, sg_ctr + 4, fe_min);
                         DHGP_LAUNCHED(c);
                         static int g_re = resident_grid(c, k_round_edges, 256, 0);
                         const unsigned gpe = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(L.E, 8), g_re));
                         pdl_launch(k_round_edges, gpe, 256, 0, c.stream, L.E, elist, elist_n, L.pin_off, L.pin_dat,
-                                   L.dst_off, L.dst_dat, W.wi, r, pos, from, to, gacc, ev, sg_big, sg_ctr, big, ctr,
+                                   L.dst_off, L.dst_dat, W.wi, r, pos, from, to, gacc, ev, sg_big, sg_ctr, big, ectr,
                                    tiers().edge_movers, sp ? dM : nullptr, c.work_slot(Ctx::PW_SEQ_GAINS), esh.lo,
                                    esh.hi, lg_list, sg_ctr + 4, fe_min);
                     }
@@ -3125,7 +3138,7 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
                                                                              mv_max);
                     DHGP_LAUNCHED(c);
                     pdl_launch(k_inbound_events_block, c.num_sms, 256, 0, c.stream, L.dst_off, L.dst_dat, r, pos, from, to,
-                                                                             ev, big, ctr, hv_ev, sg_ctr + 3, mv_max);
+                                                                             ev, big, ectr, hv_ev, sg_ctr + 3, mv_max);
                     DHGP_LAUNCHED(c);
                     if (huge_movers) {  // exit at once when the huge lists are empty
                         pdl_launch(k_edge_movers_huge, mv_grid, 1024, 0, c.stream, 0, L.pin_off, L.pin_dat, W.wi, r,
@@ -3291,7 +3304,6 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
                                                     st.emflag, st.mlist, st.ctr + CT_MLIST, st.ndirty, st.nlist,
                                                     st.ctr + CT_NLIST);
             DHGP_LAUNCHED(c);
-            c.zero(st.ctr + CT_MLIST, 1);
             if (kbest > 0) st.moved = true;
         } else if (kbest > 0) {
             pdl_launch(k_apply, (unsigned)cdiv(kbest, 256), 256, 0, c.stream, kbest, node, to, assign);
@@ -3322,7 +3334,7 @@ void refine_level(Ctx &c, const DLevel &L, const DWeights &W, RefineState &st, i
                     (void *)big2, (void *)mk, (void *)mkt, (void *)mv, (void *)mvt, (void *)node, (void *)from,
                     (void *)to, (void *)giso, (void *)gseq, (void *)gseq_acc, (void *)ev_from, (void *)ev_to,
                     (void *)sg_big, (void *)sg_ctr, (void *)lg_list,
-                    (void *)ek, (void *)ekt, (void *)evv, (void *)evt, (void *)ecount, (void *)sres, (void *)rsum, (void *)pdense,
+                    (void *)ek, (void *)ekt, (void *)evv, (void *)evt, (void *)ecount, (void *)ectr, (void *)sres, (void *)rsum, (void *)pdense,
                     (void *)ptouched, (void *)huge_scr, (void *)hv_sg,
                     (void *)hv_ev, (void *)mv_scr})
         c.free(p);
