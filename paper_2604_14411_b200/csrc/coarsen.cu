@@ -2350,6 +2350,31 @@ void contract_count(Ctx &c, DLevel &fine, const int32_t *match, const uint8_t *i
     DHGP_LAUNCHED(c);
 }
 
+// the merged clusters' node lists (and, CSR mode, the singletons' copies)
+static void node_merge_launch(Ctx &c, DLevel &fine, DLevel &coarse, ContractScratch &s, const LevelStatus &st,
+                              NodePool *pool, cudaStream_t stream) {
+    NodeFams fs{{NodeFam{fine.in_off, fine.in_dat, nullptr, coarse.in_off, coarse.in_dat},
+                 NodeFam{fine.inc_off, fine.inc_dat, nullptr, coarse.inc_off, coarse.inc_dat}}};
+    fs.f[0].end = fine.in_e();
+    fs.f[1].end = fine.inc_e();
+    if (!pool) {  // CSR: the singletons' lists are copied (pooled: they stay where they are)
+        // slices per chunk: about 4K list entries per CTA
+        const int64_t per_chunk = cdiv(std::max(fine.Sin, fine.U) * kNodeChunk, std::max<int64_t>(1, fine.N));
+        const int split = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(per_chunk, 4096), 64));
+        const int64_t items = cdiv(st.nc, kNodeChunk) * split;
+        const unsigned g = (unsigned)std::min<int64_t>(items, (int64_t)c.num_sms * 16);
+        pdl_launch(k_node_write, dim3(g, 2), 256, 0, stream, st.nc, split, s.ma, s.mb, fs);
+        DHGP_LAUNCHED(c);
+    }
+    const int words = union_words(c, fine.E);
+    pdl_launch(k_node_union_warp<true>, dim3(4 * c.num_sms, 2), UW_WARPS * 32, 0, stream, s.ma, s.mb, s.mlist,
+               s.mcount, fs, nullptr);
+    DHGP_LAUNCHED(c);
+    pdl_launch(k_node_union<true>, dim3(c.num_sms, 2), UN_THREADS, 4 * words, stream, s.ma, s.mb, s.mlist, s.mcount,
+               fs, nullptr, words);
+    DHGP_LAUNCHED(c);
+}
+
 void contract_write(Ctx &c, DLevel &fine, DLevel &coarse, ContractScratch &s, const LevelStatus &st,
                     NodePool *pool) {
     // algorithmic bytes: fine h-edge lists + gamma read (8 B per entry), coarse
@@ -2377,6 +2402,17 @@ void contract_write(Ctx &c, DLevel &fine, DLevel &coarse, ContractScratch &s, co
             coarse.inc_dat = pool->dat[1];
             c.h2d(pool->top, st.pool_top, 2);
         }
+    }
+    // the node lists of the merged clusters (cw_merge) and the h-edge lists
+    // (cw_unique) are independent: the merge runs on the side stream, forked
+    // here and joined below, so its latency-bound union kernels overlap the
+    // h-edge rewrite
+    const bool fork = c.side && st.nc > 0;
+    if (fork) {
+        DHGP_CUDA(cudaEventRecord(c.ev_fork, c.stream));
+        DHGP_CUDA(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
+        node_merge_launch(c, fine, coarse, s, st, pool, c.side);
+        DHGP_CUDA(cudaEventRecord(c.ev_join, c.side));
     }
     {
         KScope k2(c, "cw_unique");
@@ -2413,30 +2449,11 @@ void contract_write(Ctx &c, DLevel &fine, DLevel &coarse, ContractScratch &s, co
             seg_unique_write(c, E, fine.pin_off, s.tmp_pin, coarse.pin_off, coarse.pin_dat);
         }
     }
-    {
+    if (fork) {
+        DHGP_CUDA(cudaStreamWaitEvent(c.stream, c.ev_join, 0));
+    } else if (st.nc > 0) {
         KScope k2(c, "cw_merge");
-        if (st.nc > 0) {
-            NodeFams fs{{NodeFam{fine.in_off, fine.in_dat, nullptr, coarse.in_off, coarse.in_dat},
-                         NodeFam{fine.inc_off, fine.inc_dat, nullptr, coarse.inc_off, coarse.inc_dat}}};
-            fs.f[0].end = fine.in_e();
-            fs.f[1].end = fine.inc_e();
-            if (!pool) {  // CSR: the singletons' lists are copied (pooled: they stay where they are)
-                // slices per chunk: about 4K list entries per CTA
-                const int64_t per_chunk = cdiv(std::max(fine.Sin, fine.U) * kNodeChunk, std::max<int64_t>(1, fine.N));
-                const int split = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(per_chunk, 4096), 64));
-                const int64_t items = cdiv(st.nc, kNodeChunk) * split;
-                const unsigned g = (unsigned)std::min<int64_t>(items, (int64_t)c.num_sms * 16);
-                pdl_launch(k_node_write, dim3(g, 2), 256, 0, c.stream, st.nc, split, s.ma, s.mb, fs);
-                DHGP_LAUNCHED(c);
-            }
-            const int words = union_words(c, E);
-            pdl_launch(k_node_union_warp<true>, dim3(4 * c.num_sms, 2), UW_WARPS * 32, 0, c.stream, s.ma, s.mb, s.mlist,
-                       s.mcount, fs, nullptr);
-            DHGP_LAUNCHED(c);
-            pdl_launch(k_node_union<true>, dim3(c.num_sms, 2), UN_THREADS, 4 * words, c.stream, s.ma, s.mb, s.mlist, s.mcount,
-                                                                                        fs, nullptr, words);
-            DHGP_LAUNCHED(c);
-        }
+        node_merge_launch(c, fine, coarse, s, st, pool, c.stream);
     }
     int32_t *ma = s.ma, *mb = s.mb;
     s.ma = s.mb = nullptr;

@@ -102,6 +102,10 @@ struct Ctx {
     Comm *comm = nullptr;  // node-range sharding across ranks (comm.cuh); null = single GPU
     int device = 0;
     cudaStream_t stream = nullptr;
+    // a second stream for independent work forked from `stream` and joined
+    // back (fork / join events); see contract_write
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int64_t launches = 0;
     int num_sms = 148;
     // optional per-kernel event timing (bench/profiling only); only the

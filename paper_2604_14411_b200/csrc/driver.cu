@@ -229,7 +229,8 @@ static size_t arena_reserved(int device) {
     return g_arena[device].reserved;
 }
 void arena_free(int device, void *p) { g_arena[device].release(p); }
-static cudaStream_t g_streams[64];
+static cudaStream_t g_streams[64], g_side[64];
+static cudaEvent_t g_fork[64], g_join[64];
 static int g_sms[64];
 static char *g_pinned[64];
 
@@ -239,10 +240,16 @@ static void setup(Ctx &c, int device) {
     DHGP_CUDA(cudaSetDevice(device));
     if (!g_streams[device]) {
         DHGP_CUDA(cudaStreamCreateWithFlags(&g_streams[device], cudaStreamNonBlocking));
+        DHGP_CUDA(cudaStreamCreateWithFlags(&g_side[device], cudaStreamNonBlocking));
+        DHGP_CUDA(cudaEventCreateWithFlags(&g_fork[device], cudaEventDisableTiming));
+        DHGP_CUDA(cudaEventCreateWithFlags(&g_join[device], cudaEventDisableTiming));
         DHGP_CUDA(cudaDeviceGetAttribute(&g_sms[device], cudaDevAttrMultiProcessorCount, device));
         DHGP_CUDA(cudaHostAlloc((void **)&g_pinned[device], Ctx::kPinnedBytes, cudaHostAllocDefault));
     }
     c.stream = g_streams[device];
+    c.side = g_side[device];
+    c.ev_fork = g_fork[device];
+    c.ev_join = g_join[device];
     c.num_sms = g_sms[device];
     c.pinned = g_pinned[device];
 }
