@@ -24,8 +24,11 @@ CLASSES = {
                              "k_edge_count_bulk", "k_marked_list", "k_contract_edges@count", "k_contract_status"}),
     "contract_write": ("k_node_union_warp@write", {"k_contract_edges@write", "k_map_gaps", "k_node_write",
                                         "k_node_union_warp@write", "k_node_union@write"}),
-    "seq_gains": ("k_round_moves", {"k_round_edges", "k_seq_gains_edge_block", "k_inbound_events_block",
-                                    "k_edge_movers_huge", "k_round_moves"}),
+    "seq_gains": ("k_round_moves", {"k_round_edges", "k_round_edges_flat", "k_seq_gains_edge_block",
+                                    "k_inbound_events_block", "k_edge_movers_huge", "k_round_moves"}),
+    "project": ("k_project_state", {"k_gamma_count", "k_project_state", "k_split_counts", "k_project"}),
+    "movers": ("k_mover_compact", {"k_mover_compact", "k_mover_flags"}),
+    "apply": ("k_apply_inc", {"k_apply_inc", "k_apply"}),
     "select": ("k_select_small", {"k_select_small"}),
     "runs_update": ("k_runs_update", {"k_runs_update", "k_runs_update_wide"}),
 }
