@@ -277,7 +277,7 @@ struct Tiers {
     int ss_heavy_inc = 192;   // score: incident h-edges above which a CTA takes the node (full scoring)
     int sm_limit = 2816;      // score: distinct neighbours per 256-thread CTA table (4096 slots)
     int sm_heavy_inc = 512;   // score: incident h-edges above which the 1024-thread tier takes the node
-    int ss_list_inc = 48;     // score, list mode (incremental levels): incident h-edges above which a CTA takes the node
+    int ss_list_inc = 80;     // score, list mode (incremental levels): incident h-edges above which a CTA takes the node
     int sh_limit = 12288;     // score: distinct neighbours per block table
     int pr_limit = 400;       // propose: distinct parts per warp table
     int pr_heavy_inc = 64;    // propose: incident h-edges above which a block takes the node
