@@ -1054,16 +1054,18 @@ void score_scratch_release(Ctx &c, ScoreScratch &s) {
 template <class Acc>
 static void launch_heavy_pairs(Ctx &c, const ScoreArgs &a) {
     cudaLaunchConfig_t cfg = {};
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = 2;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // as pdl_launch (the kernel waits first)
+    at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.blockDim = dim3(SH_THREADS);
     cfg.dynamicSmemBytes = sh_smem<Acc>();
     cfg.stream = c.stream;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 1;  // the occupancy query takes the cluster shape only
     static int pairs = 0;
     if (!pairs) {
         cfg.gridDim = dim3(2 * (c.num_sms / 2));
@@ -1073,6 +1075,7 @@ static void launch_heavy_pairs(Ctx &c, const ScoreArgs &a) {
         pairs = std::min(n, c.num_sms / 2);
     }
     cfg.gridDim = dim3(2 * pairs);
+    cfg.numAttrs = 2;
     DHGP_CUDA(cudaLaunchKernelEx(&cfg, k_score_heavy<Acc, 2>, a, pairs));
     DHGP_LAUNCHED(c);
     // more nodes than pairs: single CTAs (exactly one of the two launches works)
